@@ -1,0 +1,351 @@
+"""Benchmark: CAKF + CAKS time-steps/s on the ERA5-shaped synthetic workload (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl cakf|reference]
+
+One bench "step" = one full pass of the hot path: T predict /
+update / truncate steps of the filter followed by the T-step smoother sweep, on the same
+device-resident synthetic inputs.  value = time-steps processed per second over the timed
+region (whole job: summed over ranks, max-over-ranks device time).  The trace (25.6 GB at
+cfg3) is far larger than the 126 MB L2, so inputs are larger than L2 between iterations.
+
+--impl reference times the CPU oracle (oracle/mfree.py, as it stands) on a bounded sample
+of the same workload and extrapolates to time-steps/s (sample described in the JSON).
+N > 1 (torchrun): this round the ranks run independent replicas of the workload
+(weak scaling, no collective on the data path; the row-sharded multi-GPU path is
+described in DESIGN.md §7).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+METRIC = "filter+smoother time-steps/sec at D=231,360 on 1/2/4/8 B200; % roofline"
+
+# ALU roofline of the kernel-evaluation pair: every pair needs one sqrt
+# and one exp2 on the MUFU (16 ops/clk/SM on B200) => 8 pairs/clk/SM.
+SMS = 148
+MUFU_PER_SM_CLK = 16
+MUFU_PER_PAIR = 2
+FP32_FLOP_PER_SM_CLK = 256  # 128 FFMA lanes x 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--impl", default="cakf", choices=["cakf", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--T", type=int, default=None, help="override T (debug only; invalidates the metric)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            mp = json.load(f)
+        return mp, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                p = [x.strip() for x in line.split(",")]
+                if len(p) < 9:
+                    continue
+                try:
+                    sm.append(float(p[1]))
+                    mx.append(float(p[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, p[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except Exception:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except Exception:
+                pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def oracle_sample(wl, budget_rows=(2048, 256, 1024)):
+    """Time the oracle's dominant operations on a bounded row slab of the workload and
+    extrapolate to one full time step (filter + smoother) of the oracle.
+
+    Per time step the oracle performs max_iter matvecs with K_TT (N x N), one
+    K(X, X_T) x [v V] product (N_X x N, 1 + max_iter columns) and one smoother product
+    K(X, X) x [x_0 x_1] (N_X x N_X, 2 (1 + r) columns).  Each is timed on its first
+    rows and scaled by the row ratio; the low-rank BLAS parts are not counted (they are
+    < 1% of the oracle's time), so the estimate is optimistic for the oracle.
+    """
+    import threadpoolctl
+    from oracle import mfree
+
+    Xn = wl.coords
+    idx = wl.obs_idx[0]
+    Xt = Xn[idx]
+    N, NX = len(idx), len(Xn)
+    rng = np.random.default_rng(0)
+    r = max(wl.max_rank, 0)
+    C_post, C_sm = 1 + wl.max_iter, 2 * (1 + r)
+    a, b, c = (min(x, y) for x, y in zip(budget_rows, (N, NX, NX)))
+    s = rng.standard_normal(N)
+    t0 = time.perf_counter()
+    mfree.gram_apply(Xt, Xt, s, wl.nu_x, wl.ell_x, chunk=1024, rows=(0, a))
+    t1 = time.perf_counter()
+    mfree.gram_apply(Xn, Xn, rng.standard_normal((NX, C_sm)), wl.nu_x, wl.ell_x, chunk=256, rows=(0, b))
+    t2 = time.perf_counter()
+    mfree.gram_apply(Xn, Xt, rng.standard_normal((N, C_post)), wl.nu_x, wl.ell_x, chunk=1024, rows=(0, c))
+    t3 = time.perf_counter()
+    per_step = wl.max_iter * (t1 - t0) * N / a + (t2 - t1) * NX / b + (t3 - t2) * NX / c
+    info = threadpoolctl.threadpool_info()
+    threads = max([p.get("num_threads", 1) for p in info] + [1])
+    sample = (f"oracle/mfree.gram_apply on {wl.name}: rows [0,{a}) of K_TT s ({a}x{N}), rows [0,{b}) of "
+              f"K_XX [x0 x1] ({b}x{NX}x{C_sm}), rows [0,{c}) of K_XT [v V] ({c}x{N}x{C_post}); scaled by "
+              f"row ratios to one time step ({wl.max_iter} matvecs + post-loop + smoother)")
+    return {"sec_per_timestep": per_step, "sample_sec": t3 - t0, "threads": threads, "sample": sample}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores, bounded samples."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from synth import make_workload
+    wl = make_workload(args.config)
+    for _ in range(args.warmup):
+        oracle_sample(wl, budget_rows=(256, 32, 128))
+    secs = []
+    last = None
+    for _ in range(args.steps):
+        last = oracle_sample(wl)
+        secs.append(last["sec_per_timestep"])
+    per_step = statistics.median(secs)
+    value = 1.0 / per_step
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "time-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step * wl.T * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "D": wl.D, "N_X": wl.n_space, "N": wl.n_obs(1), "T": wl.T,
+                   "policy": wl.policy, "max_iter": wl.max_iter, "max_rank": wl.max_rank},
+        "cpu_baseline": {"value": value, "unit": "time-steps/s", "cores": last["threads"], "kind": "oracle",
+                         "sample": last["sample"]},
+        "e2e": {"value": value, "unit": "time-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_08971_b200 import CAKF_SMOOTH, binding, runner
+    from synth import make_workload
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    kw = {} if args.T is None else {"T": args.T}
+    wl = make_workload(args.config, **kw)
+    trans, _ = runner.transitions(wl)
+    stream = torch.cuda.current_stream()
+    h = runner.make_handle(wl, args.dtype, stream=stream.cuda_stream)
+    inputs = runner.stage_inputs(wl, args.dtype)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        runner.run(h, trans, inputs, smooth=True)
+    barrier()
+    # ---------------- timed region (device-resident inputs)
+    h.profile(True)
+    h.profile_read(reset=True)
+    launches0 = binding.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            runner.run(h, trans, inputs, smooth=True)
+        ev1.record(stream)
+        barrier()
+    launches = binding.kernel_launches() - launches0
+    prof = h.profile_read(reset=True)
+    h.profile(False)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_timesteps = args.steps * wl.T * world
+    value = total_timesteps / (ms / 1e3)
+    clocks = clk.summary()
+
+    # ---------------- end to end through the C-ABI with pinned HOST buffers
+    npdt = np.float32 if args.dtype == "f32" else np.float64
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    host_in = []
+    h2d = 0
+    for (idx, y, nv, order) in runner.host_inputs(wl, args.dtype):
+        ti = torch.from_numpy(idx).pin_memory()
+        ty = torch.from_numpy(y).pin_memory()
+        tn = torch.from_numpy(nv).pin_memory()
+        to = None if order is None else torch.from_numpy(order).pin_memory()
+        host_in.append((ti, ty, tn, to))
+        h2d += idx.nbytes + y.nbytes + nv.nbytes + (0 if order is None else order.nbytes)
+    outm = [torch.empty(wl.D, dtype=tdt).pin_memory() for _ in range(wl.T + 1)]
+    outv = [torch.empty(wl.D, dtype=tdt).pin_memory() for _ in range(wl.T + 1)]
+    d2h = 2 * (wl.T + 1) * wl.D * np.dtype(npdt).itemsize
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        runner.run(h, trans, host_in, smooth=True)
+        for k in range(wl.T + 1):
+            h.get(k, CAKF_SMOOTH, outm[k], outv[k])
+    e1.record(stream)
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = {"value": args.e2e_steps * wl.T * world / (ms_e2e / 1e3), "unit": "time-steps/s",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---------------- roofline of the dominant kernel (live CUDA-event timings)
+    mp, src = peaks()
+    clock_hz = float(mp.get("sm_max_mhz", 1965.0)) * 1e6
+    N = wl.n_obs(1)
+    cat_ms = {c: prof[c][0] for c in ("k1_matvec", "k2_post", "k2_smooth")}
+    dom = max(cat_ms, key=cat_ms.get)
+    tot, nl = prof[dom]
+    avg_s = tot / max(nl, 1) / 1e3
+    traffic = None
+    try:
+        with open(TRAFFIC) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    if dom == "k1_matvec":
+        pairs = float(N) * float(N)
+        achieved = pairs / avg_s / 1e9
+        peak = SMS * MUFU_PER_SM_CLK / MUFU_PER_PAIR * clock_hz / 1e9
+        roof = {"bound": "alu", "kernel": "k1_matvec (fused Matern-3/2 eval x vector)", "achieved": achieved,
+                "peak": peak, "unit": "Gpair/s", "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_per_launch": f"{pairs:.4g} pairs",
+                "peak_source": f"derived: {SMS} SMs x {MUFU_PER_SM_CLK} MUFU/clk / {MUFU_PER_PAIR} MUFU per pair "
+                               f"x {clock_hz/1e6:.0f} MHz (sm_max_mhz, {src})"}
+    else:
+        M = wl.n_space
+        Kd = N if dom == "k2_post" else wl.n_space
+        C = (1 + wl.max_iter) if dom == "k2_post" else wl.d_time * (1 + max(wl.max_rank, 0))
+        flops = 2.0 * M * Kd * C
+        achieved = flops / avg_s / 1e12
+        peak = SMS * FP32_FLOP_PER_SM_CLK * clock_hz / 1e12
+        roof = {"bound": "alu", "kernel": f"{dom} (fused kernel-eval GEMM, SIMT fp32)", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_per_launch": f"{flops:.4g} flop",
+                "peak_source": f"derived: {SMS} SMs x 128 FFMA x 2 x {clock_hz/1e6:.0f} MHz ({src})"}
+    step_ms = ms / args.steps
+    breakdown = {c: round(prof[c][0] / args.steps, 3) for c in prof}
+    out = {
+        "metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": args.config, "D": wl.D, "N_X": wl.n_space, "N": N, "T": wl.T,
+                   "policy": wl.policy, "max_iter": wl.max_iter, "max_rank": wl.max_rank,
+                   "step": "one full CAKF (T predict/update/truncate) + CAKS (T smoother steps) pass",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (trace 25.6 GB vs 126 MB L2)"},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+        "roofline": roof,
+        "phase_ms_per_step": breakdown,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        smp = oracle_sample(wl)
+        out["cpu_baseline"] = {"value": 1.0 / smp["sec_per_timestep"], "unit": "time-steps/s",
+                               "cores": smp["threads"], "kind": "oracle", "sample": smp["sample"],
+                               "sample_sec": round(smp["sample_sec"], 2)}
+    if rank == 0:
+        print(json.dumps(out))
+    h.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

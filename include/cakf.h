@@ -1,0 +1,214 @@
+/*
+ * cakf.h — C-ABI of the B200-native computation-aware Kalman filter / RTS smoother
+ * (CAKF / CAKS, Pförtner et al., arXiv 2405.08971).
+ *
+ * Citations "P:<line>" refer to the paper's LaTeX source; "R<n>" to the
+ * readings listed in DESIGN.md §3.
+ *
+ * Problem statement (Def. A.1; Lemma B.1):
+ *   u_k = A_{k-1} u_{k-1} + q_{k-1},  q ~ N(0, Q_{k-1}),  u_0 ~ N(mu_0, Sigma_0)
+ *   y_k = H_k u_k + eps_k,            eps ~ N(0, Lambda_k)
+ * for a space-time separable Gauss-Markov prior:
+ *   A = A^t (x) I_{N_X},  Q = Q^t (x) Sigma^x(X, X),  Sigma_k = Sigma^t_k (x) Sigma^x(X, X)
+ * with D' x D' temporal factors (D' = d_time) and an N_X-point spatial Matérn kernel
+ * Sigma^x evaluated on the fly (never stored).  The state is derivative-major:
+ * u = (f_0(t, X); f_1(t, X); ...), D = D' * N_X.  H_k picks the rows obs_idx of
+ * block 0; Lambda_k is diagonal (R22).
+ *
+ * Call sequence (alg:mfkf P:276-299, alg:mfks P:386-410):
+ *   cakf_create
+ *   repeat T times: cakf_predict -> cakf_update -> cakf_truncate
+ *   caks_smooth
+ *   cakf_get / cakf_get_stats (any time after the step exists)
+ *   cakf_reset (start a new run on the same handle) ... cakf_destroy
+ * Out-of-order calls return CAKF_E_STATE and leave the handle unchanged.
+ *
+ * Memory and ownership: every pointer argument is borrowed for the duration of
+ * the call.  Array arguments may be host or device (CUDA UVA) pointers; they are
+ * copied (stream-ordered) before the call returns to the caller's control of the
+ * stream.  The handle owns all device state (trace, workspaces); outputs are
+ * written to caller buffers.  All device work is enqueued on cfg.stream (or on a
+ * stream the handle creates when cfg.stream is NULL); cakf_get, cakf_get_stats
+ * and cakf_sync synchronise that stream.
+ *
+ * Errors: every function returns 0 (CAKF_OK) or a negative code; the message of
+ * the last failure on the calling thread is available from cakf_last_error().
+ * CAKF_E_ARG / CAKF_E_STATE leave the handle unchanged.  CAKF_E_CUDA and
+ * CAKF_E_NUMERIC mark the handle failed: only get_stats, reset and destroy stay
+ * valid.  Rejected (G-degenerate) actions are NOT errors (R2): they are counted
+ * in cakf_step_stats.rejected.
+ *
+ * Concurrency: one handle is used by one host thread at a time.
+ */
+#ifndef CAKF_H
+#define CAKF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAKF_VERSION 1
+
+enum cakf_status {
+  CAKF_OK = 0,
+  CAKF_E_ARG = -1,         /* NULL / out-of-range / inconsistent argument        */
+  CAKF_E_STATE = -2,       /* call out of order (see call sequence)              */
+  CAKF_E_UNSUPPORTED = -3, /* kernel family, d_time or policy outside the build  */
+  CAKF_E_NUMERIC = -4,     /* non-finite values or failed eigendecomposition     */
+  CAKF_E_CUDA = -5,        /* CUDA / cuBLAS / cuSOLVER failure                   */
+  CAKF_E_NCCL = -6,        /* multi-GPU communication failure                    */
+  CAKF_E_NOMEM = -7        /* device allocation failed                           */
+};
+
+enum cakf_dtype { CAKF_F32 = 0, CAKF_F64 = 1 };
+
+/* Spatial Matérn family: Sigma^x(x, x') = Matern_nu(|x - x'| / ell_x), unit output
+ * scale (the output scale lives in Sigma^t).  Value = 2 nu. */
+enum cakf_kernel { CAKF_MATERN12 = 1, CAKF_MATERN32 = 3, CAKF_MATERN52 = 5 };
+
+/* Policy (Sec. 3.3, App. C.3):
+ *   CAKF_POLICY_CG     s_i = current residual r^(i)           (R1; the paper's choice)
+ *   CAKF_POLICY_COORD  s_i = e_{order[i-1]}                    (coordinate actions)
+ *   CAKF_POLICY_RANDOM s_i ~ N(0, I) by Philox4x32-10 (R16)    (randomized actions) */
+enum cakf_policy { CAKF_POLICY_CG = 0, CAKF_POLICY_COORD = 1, CAKF_POLICY_RANDOM = 2 };
+
+/* which-selector of cakf_get */
+enum cakf_which { CAKF_PRED = 0, CAKF_FILTER = 1, CAKF_SMOOTH = 2 };
+
+typedef struct cakf_s* cakf_t;
+
+typedef struct {
+  int32_t dtype;            /* CAKF_F32 or CAKF_F64: arithmetic type of all device math      */
+  int32_t d_time;           /* D' (1..3); 2 = Matérn-3/2 temporal prior                      */
+  int64_t n_space;          /* N_X >= 1                                                       */
+  int32_t space_dim;        /* 1..3 (sphere grids are passed already embedded in R^3)        */
+  const double* coords;     /* n_space * space_dim, row-major; host or device; copied         */
+  int32_t spatial_kernel;   /* enum cakf_kernel                                              */
+  double ell_x;             /* spatial lengthscale (coordinate units), > 0                    */
+  const double* sigma_t0;   /* D' x D' row-major Sigma^t(t_0, t_0); Sigma_0 = sigma_t0 (x) K  */
+  const double* mu0;        /* D (derivative-major) or NULL for a zero prior mean             */
+  int32_t policy;           /* enum cakf_policy                                              */
+  int32_t max_iter;         /* N^max: iterations (actions) per update, >= 0                   */
+  int32_t max_rank;         /* truncation cap r for M (filter) and W^s (smoother); < 0 = never */
+  double rtol;              /* stop once ||r|| <= rtol ||r0||; 0 = count-only (R2, default)   */
+  int32_t reorth;           /* 1 = second Gram-Schmidt pass d -= V V^T G d (CGS2, R19); 0 = the
+                               single classical pass of alg:update_pls line 11 as printed      */
+  uint64_t seed;            /* Philox key of CAKF_POLICY_RANDOM                               */
+  int32_t max_steps;        /* T: number of time steps the trace is sized for                */
+  int64_t max_obs;          /* max N_k over the run (0 = n_space)                            */
+  int32_t rank;             /* multi-GPU rank (0 for a single GPU)                           */
+  int32_t world;            /* number of ranks; 1 = single GPU (only value in this build)    */
+  const void* nccl_id;      /* 128-byte ncclUniqueId when world > 1, else NULL               */
+  void* stream;             /* cudaStream_t to enqueue on, or NULL                           */
+} cakf_config;
+
+typedef struct {
+  int32_t k;                /* step index                                                     */
+  int32_t iters;            /* iterations executed (including rejected actions)              */
+  int32_t rejected;         /* actions rejected by the eta floor (R2)                         */
+  int32_t rank_in;          /* columns of M^-_k                                               */
+  int32_t cols;             /* columns of M_k = rank_in + iters                               */
+  int32_t rank_out;         /* columns of M~_k after Truncate                                 */
+  int32_t smoother_rank;    /* columns of W^s_k after the smoother's Truncate                 */
+  int32_t missing;          /* 1 if the step had no observations (IsMissing)                  */
+  double res0;              /* ||r^(0)||_2                                                    */
+  double res_final;         /* ||r^(iters)||_2 (recurrence)                                   */
+  double eta_min;           /* smallest accepted eta                                          */
+  double dropped_mass;      /* sum of dropped Gram eigenvalues = tr(N N^T) (Sec. 3.2)         */
+} cakf_step_stats;
+
+/* Create a handle: copies coords (prescaled), allocates the trace for max_steps
+ * steps and all workspaces.  Returns CAKF_E_NOMEM if the trace does not fit. */
+int cakf_create(const cakf_config* cfg, cakf_t* out);
+
+/* Discard all steps and start again at k = 0 with the same configuration and buffers. */
+int cakf_reset(cakf_t h);
+
+/* Predict step k-1 -> k (alg:mfkf lines 4-5; Prop A.3):
+ *   Sigma^t_k = A^t Sigma^t_{k-1} A^tT + Q^t         (host, fp64)
+ *   m^-_k = (A^t (x) I) m_{k-1} + b,  M^-_k = (A^t (x) I) M~_{k-1}
+ * A_t, Q_t: D' x D' row-major (host or device).  b: D or NULL (zero, R9). */
+int cakf_predict(cakf_t h, const double* A_t, const double* Q_t, const void* b);
+
+/* Update step k (alg:update_pls), or IsMissing when n_obs == 0
+ * (P:283-294).  obs_idx: n_obs int64 spatial indices (f_0 rows of H_k), unique;
+ * y, noise_var: n_obs values of the handle's dtype (noise_var = diag Lambda_k);
+ * coord_order: for CAKF_POLICY_COORD, >= min(max_iter, n_obs) int64 positions into
+ * obs_idx (j(i) of App. C.3), else NULL.  Iterations = min(max_iter, n_obs). */
+int cakf_update(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* y,
+                const void* noise_var, const int64_t* coord_order);
+
+/* Truncate step k (Sec. 3.2; R3/R4): keep the top min(max_rank, cols)
+ * eigen-directions of M_k^T M_k, M~_k = M_k Q_r (eigendecomposition on device). */
+int cakf_truncate(cakf_t h);
+
+/* Backward CAKS sweep k = T-1 .. 0 (alg:mfks; R6, R7) over the steps
+ * filtered so far.  Produces smoother means and marginal variances for k = 0..T. */
+int caks_smooth(cakf_t h);
+
+/* Copy the mean and/or marginal variance (D values each, dtype of the handle,
+ * derivative-major) of state k in {0..T} to mean_D / var_D (host or device; either
+ * may be NULL).  which: CAKF_PRED (m^-_k, diag P^-_k), CAKF_FILTER (m_k, diag P_k),
+ * CAKF_SMOOTH (m^s_k, diag P^s_k; requires caks_smooth).  Synchronises. */
+int cakf_get(cakf_t h, int32_t k, int32_t which, void* mean_D, void* var_D);
+
+/* Per-step statistics (synchronises). */
+int cakf_get_stats(cakf_t h, int32_t k, cakf_step_stats* out);
+
+/* Kept Gram eigenvalues of the filter truncation at step k, descending
+ * (min(max_rank, cols) values) into vals (host, double); n_out receives the count. */
+int cakf_get_kept_eigs(cakf_t h, int32_t k, double* vals, int32_t cap, int32_t* n_out);
+
+/* Wait for all work enqueued by the handle. */
+int cakf_sync(cakf_t h);
+
+/* Kernel timing by category with CUDA events recorded on the handle's stream around
+ * every launch of that category (for bench.py's live roofline).  enable = 0 stops
+ * recording.  cakf_profile_read synchronises, adds the elapsed times recorded since
+ * the last reset into ms[CAKF_PROF_NCAT] and launches[CAKF_PROF_NCAT], and clears the
+ * record when reset != 0. */
+enum cakf_prof_category {
+  CAKF_PROF_K1 = 0,         /* fused kernel-eval matvec of the inner loop (a4)         */
+  CAKF_PROF_K2_POST = 1,    /* fused kernel-eval x [v V] of the post-loop update (a7)  */
+  CAKF_PROF_K2_SMOOTH = 2,  /* fused kernel-eval x [x_0 x_1] of the smoother (a9)      */
+  CAKF_PROF_STAGES = 3,     /* inner-loop reduction / update stages (a5, a6)           */
+  CAKF_PROF_TRUNCATE = 4,   /* Gram + eigendecomposition + M Q_r (a8, smoother too)    */
+  CAKF_PROF_LOWRANK = 5,    /* low-rank fp64-accumulated contractions (a7, a9)         */
+  CAKF_PROF_NCAT = 6
+};
+int cakf_profile(cakf_t h, int32_t enable);
+int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset);
+
+/* Number of libcakf kernels launched by this process so far (all handles). */
+int64_t cakf_kernel_launches(void);
+
+/* Free everything the handle owns. */
+int cakf_destroy(cakf_t h);
+
+/* Thread-local message for the last non-zero status. */
+const char* cakf_last_error(void);
+
+int cakf_version(void);
+
+/* Stationary Matérn(nu2/2) temporal SDE, closed forms (Remark B.2; R10):
+ * A = expm(F dt) (D' x D', row-major), Q = Sinf - A Sinf A^T, Sinf the stationary
+ * covariance, D' = (nu2 + 1) / 2.  Any output pointer may be NULL (host pointers). */
+int cakf_matern_transition(int32_t nu2, double ell_t, double sigma, double dt,
+                           double* A, double* Q, double* Sinf);
+
+/* Standalone fused kernel-evaluation x matrix product (the "Gramian x matrix" op of
+ * P:644-647; a4/a7/a9 of SURVEY §8a):
+ *   Y[i, c] = alpha * sum_j Matern_nu(|xr_i - xc_j| / ell) * X[j, c]
+ * xr: n_rows x space_dim, xc: n_cols x space_dim (row-major, device, dtype);
+ * X: n_cols x n_rhs column-major (ld = n_cols), Y: n_rows x n_rhs column-major
+ * (ld = n_rows), both device.  stream may be NULL. */
+int cakf_gram_matmul(int32_t dtype, int32_t spatial_kernel, double ell, int32_t space_dim,
+                     int64_t n_rows, const void* xr, int64_t n_cols, const void* xc,
+                     int32_t n_rhs, const void* X, double alpha, void* Y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAKF_H */

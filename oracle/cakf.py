@@ -10,12 +10,18 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 Covariances are formed DENSELY here (P^- = Sigma - M^- M^-T as a D x D array),
 which is exactly what the matrix-free device path must never do.  Readings:
-  R1  the CG policy uses the residual at the current iterate,
-      r^(i) = r^(0) - G v^(i-1) (explicit form).
+  R1  the CG policy uses the residual at the current iterate r^(i) = r^(0) - G v^(i-1)
+      (P:1518), evaluated by the recurrence
+      r^(i+1) = r^(i) - (alpha_i/eta_i) G d_i (identical in exact arithmetic; both sides
+      use it so that ill-conditioned CG runs stay comparable).
+  R19 Gram-Schmidt: line 11 as printed is one classical pass; with reorth=True (default)
+      a second pass d <- d - V (V^T G d) follows (CGS2).  Identical in exact arithmetic;
+      the single pass loses G-orthogonality of V in fp32 on ERA5-shaped problems.
   R2  StoppingCriterion: i = min(N^max, N_k) iterations (int count); if rtol > 0
       also stop once ||r^(i)|| <= rtol ||r^(0)||.  An action with
-      eta <= 64 eps |s^T G s| is rejected (not appended), counted, and the
-      iteration still counts.
+      eta <= 64 eps |s^T G s| is rejected: v is not updated, V gets a zero column
+      (so M_k always has rank_in + iters columns and ranks are integer functions of
+      (r, N^max, k)), it is counted, and the iteration still counts.
   R3/R4  Truncate keeps the top min(r, cols) eigen-directions of M^T M:
       M~ = M Q_r (same subspace as the thin SVD).
   R6  the smoother truncates W^s_k with the same procedure and cap.
@@ -73,7 +79,7 @@ class UpdateResult:
 
 
 def update_iterative(m_pred, M_pred, Sigma, H, lam_diag, y, policy, k, max_iter,
-                     rtol=0.0, eps=np.finfo(np.float64).eps, cgs2=False) -> UpdateResult:
+                     rtol=0.0, eps=np.finfo(np.float64).eps, cgs2=True) -> UpdateResult:
     """alg:update_pls (P:1507-1545), dense."""
     P_pred = Sigma - M_pred @ M_pred.T                        # line 2
     G = H @ P_pred @ H.T + np.diag(lam_diag)                  # line 3
@@ -86,11 +92,10 @@ def update_iterative(m_pred, M_pred, Sigma, H, lam_diag, y, policy, k, max_iter,
     eta_min = np.inf
     coord_idx = []
     res0 = float(np.linalg.norm(r0))
-    r = r0
+    r = r0.copy()                                             # line 9 at i = 1
     nmax = min(int(max_iter), N)
     i = 0
     while i < nmax:                                           # line 7, R2
-        r = r0 - G @ v                                        # line 9 (R1: before Policy)
         if rtol > 0 and np.linalg.norm(r) <= rtol * res0:
             break
         i += 1
@@ -104,14 +109,16 @@ def update_iterative(m_pred, M_pred, Sigma, H, lam_diag, y, policy, k, max_iter,
             d = d - V @ (V.T @ (G @ d))
         Gd = G @ d
         eta = s @ Gd                                          # line 12
-        if eta <= 64.0 * eps * abs(s @ Gs):                   # R2 rejection
+        if eta <= 64.0 * eps * abs(s @ Gs):                   # R2 rejection: zero column
             rejected += 1
+            V = np.hstack([V, np.zeros((N, 1))])
             continue
         eta_min = min(eta_min, eta)
         v = v + (alpha / eta) * d                             # line 13
         V = np.hstack([V, (d / np.sqrt(eta))[:, None]])       # line 14
+        r = r - (alpha / eta) * Gd                            # line 9 for i + 1 (R1)
         S.append(s)
-    r_final = r0 - G @ v
+    r_final = r
     w = H.T @ v                                               # line 16
     W = H.T @ V                                               # line 17
     m = m_pred + P_pred @ w                                   # line 18
@@ -178,7 +185,7 @@ class StepRecord:
 
 
 def cakf_filter(ssm: SSM, policy_kind="cg", max_iter=64, max_rank=-1, coord_order=None,
-                action_seed=1, rtol=0.0, eps=np.finfo(np.float64).eps, cgs2=False):
+                action_seed=1, rtol=0.0, eps=np.finfo(np.float64).eps, cgs2=True):
     """alg:mfkf: predict, Update unless IsMissing, Truncate."""
     policy = make_policy(policy_kind, coord_order, action_seed)
     D = ssm.D
@@ -243,6 +250,6 @@ def run_workload(wl, dtype_round=None, max_rank=None, smoother=True):
     ssm = ssm_from_workload(wl, dtype_round=dtype_round)
     mr = wl.max_rank if max_rank is None else max_rank
     tr = cakf_filter(ssm, wl.policy, wl.max_iter, mr, coord_order=wl.coord_order,
-                     action_seed=wl.action_seed, rtol=wl.rtol)
+                     action_seed=wl.action_seed, rtol=wl.rtol, cgs2=wl.reorth)
     sm = caks_smoother(ssm, tr, mr) if smoother else None
     return ssm, tr, sm

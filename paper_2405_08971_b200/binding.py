@@ -1,0 +1,252 @@
+"""Thin ctypes binding of libcakf.so — argument marshalling only.
+
+Every step of the CAKF/CAKS path runs in libcakf's CUDA kernels; this module only
+converts Python / numpy / torch arguments into the C-ABI of ``include/cakf.h``
+(same function names).  There is no CPU fallback: if the shared library or a CUDA
+device is missing, calls raise ``CakfError``.
+
+Arrays may be numpy arrays (host) or CUDA torch tensors (device); the library
+copies either kind (UVA).  Torch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcakf.so")
+
+CAKF_F32, CAKF_F64 = 0, 1
+CAKF_MATERN12, CAKF_MATERN32, CAKF_MATERN52 = 1, 3, 5
+CAKF_POLICY_CG, CAKF_POLICY_COORD, CAKF_POLICY_RANDOM = 0, 1, 2
+CAKF_PRED, CAKF_FILTER, CAKF_SMOOTH = 0, 1, 2
+POLICIES = {"cg": CAKF_POLICY_CG, "coord": CAKF_POLICY_COORD, "random": CAKF_POLICY_RANDOM}
+KERNELS = {0.5: CAKF_MATERN12, 1.5: CAKF_MATERN32, 2.5: CAKF_MATERN52}
+DTYPES = {"f32": CAKF_F32, "f64": CAKF_F64, np.float32: CAKF_F32, np.float64: CAKF_F64}
+
+
+class CakfError(RuntimeError):
+    pass
+
+
+class cakf_config(ctypes.Structure):
+    _fields_ = [
+        ("dtype", ctypes.c_int32), ("d_time", ctypes.c_int32), ("n_space", ctypes.c_int64),
+        ("space_dim", ctypes.c_int32), ("coords", ctypes.c_void_p), ("spatial_kernel", ctypes.c_int32),
+        ("ell_x", ctypes.c_double), ("sigma_t0", ctypes.c_void_p), ("mu0", ctypes.c_void_p),
+        ("policy", ctypes.c_int32), ("max_iter", ctypes.c_int32), ("max_rank", ctypes.c_int32),
+        ("rtol", ctypes.c_double), ("reorth", ctypes.c_int32), ("seed", ctypes.c_uint64), ("max_steps", ctypes.c_int32),
+        ("max_obs", ctypes.c_int64), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
+    ]
+
+
+class cakf_step_stats(ctypes.Structure):
+    _fields_ = [
+        ("k", ctypes.c_int32), ("iters", ctypes.c_int32), ("rejected", ctypes.c_int32),
+        ("rank_in", ctypes.c_int32), ("cols", ctypes.c_int32), ("rank_out", ctypes.c_int32),
+        ("smoother_rank", ctypes.c_int32), ("missing", ctypes.c_int32), ("res0", ctypes.c_double),
+        ("res_final", ctypes.c_double), ("eta_min", ctypes.c_double), ("dropped_mass", ctypes.c_double),
+    ]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+EXPORTS = [
+    "cakf_create", "cakf_reset", "cakf_predict", "cakf_update", "cakf_truncate", "caks_smooth", "cakf_get",
+    "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
+    "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
+]
+PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank"]
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libcakf.so (raises CakfError if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise CakfError(f"{path} not built: run `python -m paper_2405_08971_b200.build`")
+    lib = ctypes.CDLL(path)
+    vp, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    lib.cakf_create.argtypes = [ctypes.POINTER(cakf_config), ctypes.POINTER(vp)]
+    lib.cakf_reset.argtypes = [vp]
+    lib.cakf_predict.argtypes = [vp, vp, vp, vp]
+    lib.cakf_update.argtypes = [vp, i64, vp, vp, vp, vp]
+    lib.cakf_truncate.argtypes = [vp]
+    lib.caks_smooth.argtypes = [vp]
+    lib.cakf_get.argtypes = [vp, i32, i32, vp, vp]
+    lib.cakf_get_stats.argtypes = [vp, i32, ctypes.POINTER(cakf_step_stats)]
+    lib.cakf_get_kept_eigs.argtypes = [vp, i32, vp, i32, ctypes.POINTER(i32)]
+    lib.cakf_sync.argtypes = [vp]
+    lib.cakf_destroy.argtypes = [vp]
+    lib.cakf_last_error.restype = ctypes.c_char_p
+    lib.cakf_matern_transition.argtypes = [i32, f64, f64, f64, vp, vp, vp]
+    lib.cakf_gram_matmul.argtypes = [i32, i32, f64, i32, i64, vp, i64, vp, i32, vp, f64, vp, vp]
+    lib.cakf_profile.argtypes = [vp, i32]
+    lib.cakf_profile_read.argtypes = [vp, vp, vp, i32]
+    lib.cakf_kernel_launches.restype = ctypes.c_int64
+    for name in EXPORTS:
+        if name not in ("cakf_last_error", "cakf_version", "cakf_kernel_launches"):
+            getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = load().cakf_last_error().decode(errors="replace")
+        raise CakfError(f"libcakf status {rc}: {msg}")
+
+
+def _ptr(x):
+    """(pointer, keepalive) for numpy / torch / None."""
+    if x is None:
+        return None, None
+    if hasattr(x, "data_ptr"):  # torch tensor
+        if not x.is_contiguous():
+            x = x.contiguous()
+        return x.data_ptr(), x
+    a = np.ascontiguousarray(x)
+    return a.ctypes.data, a
+
+
+def kernel_launches() -> int:
+    """Number of libcakf kernels launched by this process so far."""
+    return int(load().cakf_kernel_launches())
+
+
+def matern_transition(nu: float, ell_t: float, sigma: float, dt: float):
+    """(A^t(dt), Q^t(dt), Sigma_inf) from the library's closed forms (R10)."""
+    lib = load()
+    nu2 = int(round(2 * nu))
+    n = (nu2 + 1) // 2
+    A = np.zeros((n, n))
+    Q = np.zeros((n, n))
+    S = np.zeros((n, n))
+    _check(lib.cakf_matern_transition(nu2, float(ell_t), float(sigma), float(dt), A.ctypes.data, Q.ctypes.data,
+                                      S.ctypes.data))
+    return A, Q, S
+
+
+def gram_matmul(xr, xc, X, nu: float, ell: float, alpha: float = 1.0, out=None, stream=None):
+    """Y = alpha * K(xr, xc) X on the device (torch CUDA tensors, dtype f32/f64)."""
+    import torch
+    lib = load()
+    dtype = CAKF_F32 if xr.dtype == torch.float32 else CAKF_F64
+    n_rhs = 1 if X.dim() == 1 else X.shape[1]
+    Xc = X.reshape(-1, n_rhs).t().contiguous()  # column-major n_cols x n_rhs
+    Y = torch.empty((n_rhs, xr.shape[0]), dtype=xr.dtype, device=xr.device)
+    _check(lib.cakf_gram_matmul(dtype, KERNELS[nu], float(ell), xr.shape[1], xr.shape[0], xr.contiguous().data_ptr(),
+                                xc.shape[0], xc.contiguous().data_ptr(), n_rhs, Xc.data_ptr(), float(alpha),
+                                Y.data_ptr(), stream))
+    Y = Y.t()
+    return Y[:, 0] if X.dim() == 1 else Y
+
+
+class Cakf:
+    """One CAKF/CAKS handle (``cakf_t``).  Methods map 1:1 onto the C-ABI."""
+
+    def __init__(self, coords, ell_x, sigma_t0, *, dtype="f32", d_time=2, nu_x=1.5, mu0=None, policy="cg",
+                 max_iter=64, max_rank=-1, seed=1, max_steps=48, max_obs=0, reorth=True, stream=None):
+        self.lib = load()
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        if coords.ndim == 1:
+            coords = coords[:, None]
+        self.np_dtype = np.float32 if DTYPES[dtype] == CAKF_F32 else np.float64
+        self.n_space, self.space_dim = coords.shape
+        self.d_time = d_time
+        self.D = d_time * self.n_space
+        st0 = np.ascontiguousarray(sigma_t0, dtype=np.float64)
+        mu = None if mu0 is None else np.ascontiguousarray(mu0, dtype=np.float64)
+        cfg = cakf_config(dtype=DTYPES[dtype], d_time=d_time, n_space=self.n_space, space_dim=self.space_dim,
+                          coords=coords.ctypes.data, spatial_kernel=KERNELS[nu_x], ell_x=float(ell_x),
+                          sigma_t0=st0.ctypes.data, mu0=None if mu is None else mu.ctypes.data,
+                          policy=POLICIES[policy] if isinstance(policy, str) else int(policy),
+                          max_iter=int(max_iter), max_rank=int(max_rank), rtol=0.0, reorth=int(bool(reorth)),
+                          seed=int(seed),
+                          max_steps=int(max_steps), max_obs=int(max_obs), rank=0, world=1, nccl_id=None,
+                          stream=stream)
+        h = ctypes.c_void_p()
+        _check(self.lib.cakf_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self.h = h
+
+    # --- the C-ABI, 1:1
+    def reset(self):
+        _check(self.lib.cakf_reset(self.h))
+
+    def predict(self, A_t, Q_t, b=None):
+        A = np.ascontiguousarray(A_t, dtype=np.float64)
+        Q = np.ascontiguousarray(Q_t, dtype=np.float64)
+        pb, kb = _ptr(b)
+        _check(self.lib.cakf_predict(self.h, A.ctypes.data, Q.ctypes.data, pb))
+
+    def update(self, obs_idx, y, noise_var, coord_order=None):
+        n = 0 if obs_idx is None else int(len(obs_idx))
+        if n == 0:
+            _check(self.lib.cakf_update(self.h, 0, None, None, None, None))
+            return
+        pi, ki = _ptr(obs_idx if hasattr(obs_idx, "data_ptr") else np.asarray(obs_idx, dtype=np.int64))
+        py, ky = _ptr(y if hasattr(y, "data_ptr") else np.asarray(y, dtype=self.np_dtype))
+        pn, kn = _ptr(noise_var if hasattr(noise_var, "data_ptr") else np.asarray(noise_var, dtype=self.np_dtype))
+        po, ko = _ptr(None if coord_order is None else (coord_order if hasattr(coord_order, "data_ptr")
+                                                        else np.asarray(coord_order, dtype=np.int64)))
+        _check(self.lib.cakf_update(self.h, n, pi, py, pn, po))
+
+    def truncate(self):
+        _check(self.lib.cakf_truncate(self.h))
+
+    def smooth(self):
+        _check(self.lib.caks_smooth(self.h))
+
+    def get(self, k: int, which: int = CAKF_FILTER, mean=None, var=None):
+        """Returns (mean, var); numpy arrays unless device buffers are passed in."""
+        if mean is None and var is None:
+            mean = np.empty(self.D, dtype=self.np_dtype)
+            var = np.empty(self.D, dtype=self.np_dtype)
+        pm, km = _ptr(mean)
+        pv, kv = _ptr(var)
+        _check(self.lib.cakf_get(self.h, int(k), int(which), pm, pv))
+        return mean, var
+
+    def get_stats(self, k: int) -> dict:
+        s = cakf_step_stats()
+        _check(self.lib.cakf_get_stats(self.h, int(k), ctypes.byref(s)))
+        return s.as_dict()
+
+    def get_kept_eigs(self, k: int, cap: int = 4096) -> np.ndarray:
+        vals = np.zeros(cap)
+        n = ctypes.c_int32(0)
+        _check(self.lib.cakf_get_kept_eigs(self.h, int(k), vals.ctypes.data, cap, ctypes.byref(n)))
+        return vals[: n.value].copy()
+
+    def sync(self):
+        _check(self.lib.cakf_sync(self.h))
+
+    def profile(self, enable: bool = True):
+        _check(self.lib.cakf_profile(self.h, int(bool(enable))))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        """{category: (total_ms, launches)} of the launches recorded since the last reset."""
+        n = len(PROF_CATEGORIES)
+        ms = np.zeros(n)
+        cnt = np.zeros(n, dtype=np.int64)
+        _check(self.lib.cakf_profile_read(self.h, ms.ctypes.data, cnt.ctypes.data, int(bool(reset))))
+        return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(PROF_CATEGORIES)}
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            self.lib.cakf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass

@@ -1,0 +1,939 @@
+// cakf_api.cu — runtime (handle, trace arena, step scheduler) and the C-ABI of libcakf.
+//
+// One CAKF/CAKS run on one B200 (cfg.world == 1).  Device layout:
+//   coords      N_X x {x,y,z,w} (dtype), prescaled by sqrt(2 nu)/ell_x
+//   per step k  m^-_k, m_k, var_k, m^s_k, var^s_k (D each)
+//               M_k = [M^-_k | B_k]  D x (rin_k + iters_k), column-major, ld = D
+//               obs idx (N_k int32), XV = [v | V]  N_k x (1 + N^max), column-major
+//               IterCtl (stats), kept Gram eigenvalues
+//   workspaces  inner loop (r, s, g, g', d, Gd, Z, HM, K1 partials, fp64 block partials),
+//               post-loop (Y, U, tmp), truncation (Gram, eig, Q_r, M~), smoother (X, Y, y, W^s)
+// Everything is enqueued on one stream without host synchronisation between the
+// calls (iteration counts and ranks are host-known integers, R2/R3).
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cakf.h"
+#include "internal.h"
+#include "step.h"
+
+using namespace cakf;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CK_CUDA(expr)                                                                           \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess) {                                                                    \
+      failed_ = true;                                                                           \
+      return fail(e_ == cudaErrorMemoryAllocation ? CAKF_E_NOMEM : CAKF_E_CUDA,                 \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                          \
+    }                                                                                           \
+  } while (0)
+#define CK_BLAS(expr)                                                                           \
+  do {                                                                                          \
+    cublasStatus_t s_ = (expr);                                                                 \
+    if (s_ != CUBLAS_STATUS_SUCCESS) {                                                          \
+      failed_ = true;                                                                           \
+      return fail(CAKF_E_CUDA, std::string(#expr) + ": cublas status " + std::to_string(s_));   \
+    }                                                                                           \
+  } while (0)
+#define CK_SOLVER(expr)                                                                         \
+  do {                                                                                          \
+    cusolverStatus_t s_ = (expr);                                                               \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) {                                                        \
+      failed_ = true;                                                                           \
+      return fail(CAKF_E_CUDA, std::string(#expr) + ": cusolver status " + std::to_string(s_)); \
+    }                                                                                           \
+  } while (0)
+#define CK(expr)              \
+  do {                        \
+    int rc_ = (expr);         \
+    if (rc_ != 0) return rc_; \
+  } while (0)
+
+Mat3 mat_from(const double* a, int n) {
+  Mat3 m{};
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) m.a[i][j] = a[i * n + j];
+  return m;
+}
+Mat3 mat_abat_plus_q(const Mat3& A, const Mat3& S, const Mat3& Q, int n) {
+  Mat3 AS{}, R{};
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int t = 0; t < n; ++t) AS.a[i][j] += A.a[i][t] * S.a[t][j];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double acc = Q.a[i][j];
+      for (int t = 0; t < n; ++t) acc += AS.a[i][t] * A.a[j][t];
+      R.a[i][j] = acc;
+    }
+  return R;
+}
+
+// host copy of a small host-or-device array of doubles
+bool fetch_doubles(const double* src, size_t n, std::vector<double>& out) {
+  out.resize(n);
+  if (!n) return true;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, src) == cudaSuccess &&
+      (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged)) {
+    return cudaMemcpy(out.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  cudaGetLastError();
+  std::memcpy(out.data(), src, n * sizeof(double));
+  return true;
+}
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <typename T> struct Blas;
+template <> struct Blas<float> {
+  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k,
+                             float alpha, const float* A, int lda, const float* B, int ldb, float beta, float* C,
+                             int ldc) {
+    return cublasSgemm(h, ta, tb, m, n, k, &alpha, A, lda, B, ldb, &beta, C, ldc);
+  }
+  static cublasStatus_t axpy(cublasHandle_t h, int n, float a, const float* x, float* y) {
+    return cublasSaxpy(h, n, &a, x, 1, y, 1);
+  }
+};
+template <> struct Blas<double> {
+  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k,
+                             double alpha, const double* A, int lda, const double* B, int ldb, double beta, double* C,
+                             int ldc) {
+    return cublasDgemm(h, ta, tb, m, n, k, &alpha, A, lda, B, ldb, &beta, C, ldc);
+  }
+  static cublasStatus_t axpy(cublasHandle_t h, int n, double a, const double* x, double* y) {
+    return cublasDaxpy(h, n, &a, x, 1, y, 1);
+  }
+};
+
+struct ImplBase {
+  virtual ~ImplBase() = default;
+  virtual int init(const cakf_config& cfg) = 0;
+  virtual int reset() = 0;
+  virtual int predict(const double* A, const double* Q, const void* b) = 0;
+  virtual int update(int64_t n, const int64_t* idx, const void* y, const void* nv, const int64_t* order) = 0;
+  virtual int truncate() = 0;
+  virtual int smooth() = 0;
+  virtual int get(int k, int which, void* mean, void* var) = 0;
+  virtual int stats(int k, cakf_step_stats* out) = 0;
+  virtual int kept_eigs(int k, double* vals, int cap, int* n_out) = 0;
+  virtual int sync() = 0;
+  virtual int profile(bool on) = 0;
+  virtual int prof_read(double* ms, int64_t* n, bool reset) = 0;
+};
+
+template <typename T>
+struct Impl final : ImplBase {
+  // ---------------- configuration
+  int Dp = 2, dim = 3, nu2 = 3, policy = 0, nhat = 0, rcap = -1, Tmax = 0;
+  int64_t NX = 0, D = 0, Nmax = 0;
+  double rtol = 0.0, ell = 1.0;
+  uint64_t seed = 0;
+  Mat3 sig_t0{};
+  bool own_stream = false, failed_ = false;
+  cudaStream_t st = nullptr;
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t sol = nullptr;
+
+  // ---------------- device memory
+  char* arena = nullptr;
+  size_t arena_bytes = 0, arena_off = 0;
+  V4<T>* coords = nullptr;
+  T* mu0 = nullptr;
+  struct Step {
+    T *m_pred, *m, *var, *ms, *vs, *Mk, *XV;
+    int* idx;
+    double* kept;
+    int cap_cols = 0;
+    int rin = 0, cols = 0, n = 0, N = 0, rank_out = 0, smoother_rank = 0;
+    bool missing = true, truncated = false;
+    Mat3 sig_t{}, A_next{};
+  };
+  std::vector<Step> steps;
+  IterCtl* ctl = nullptr;  // [Tmax + 1]
+  IterCtl* ctl_init_host = nullptr;
+
+  // inner loop
+  V4<T>* xcs = nullptr;
+  T *r = nullptr, *s = nullptr, *g = nullptr, *gp = nullptr, *d = nullptr, *Gd = nullptr, *Z = nullptr, *HM = nullptr;
+  T *ybuf = nullptr, *lam2 = nullptr, *partial = nullptr;
+  size_t partial_cap = 0;
+  int64_t* stage64 = nullptr;
+  int* order32 = nullptr;
+  double *part = nullptr, *redA = nullptr, *redB = nullptr, *redC = nullptr;
+  bool reorth = true;
+  unsigned* cnt = nullptr;
+  int W = 0, rin_max = 0, qmax = 0, cmax = 0;
+  // post-loop
+  T *Yb = nullptr, *Ub = nullptr, *tmp = nullptr;
+  // truncation
+  double *gpart = nullptr, *Gm = nullptr, *eigw = nullptr, *work = nullptr;
+  int* info = nullptr;
+  int lwork = 0, nsplit_max = 16;
+  T* Mtil = nullptr;
+  double* QrD = nullptr;
+  // fp64 scratch of the low-rank contractions (fp32 storage, fp64 accumulation)
+  double *dA = nullptr, *dB = nullptr, *dC = nullptr;
+  size_t dscr = 0;
+  // smoother
+  T *X = nullptr, *Yk = nullptr, *yb = nullptr, *Tm = nullptr, *Hy = nullptr, *tt = nullptr, *R = nullptr;
+  T *Wf = nullptr, *Ws = nullptr, *ws = nullptr, *pvar = nullptr;
+
+  // ---------------- profiling: CUDA events around launches of one category (cakf_profile)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> ev_done;  // (category, index of the start event)
+  double prof_ms[CAKF_PROF_NCAT] = {0};
+  int64_t prof_n[CAKF_PROF_NCAT] = {0};
+  size_t prof_begin() {
+    if (!prof_on) return SIZE_MAX;
+    while (ev_pool.size() < ev_used + 2) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return SIZE_MAX;
+      ev_pool.push_back(e);
+    }
+    const size_t i = ev_used;
+    ev_used += 2;
+    cudaEventRecord(ev_pool[i], st);
+    return i;
+  }
+  void prof_end(int cat, size_t i) {
+    if (i == SIZE_MAX) return;
+    cudaEventRecord(ev_pool[i + 1], st);
+    ev_done.emplace_back(cat, i);
+  }
+  int prof_read(double* ms, int64_t* n, bool reset_) override {
+    CK_CUDA(cudaStreamSynchronize(st));
+    for (auto& pr : ev_done) {
+      float t = 0.f;
+      CK_CUDA(cudaEventElapsedTime(&t, ev_pool[pr.second], ev_pool[pr.second + 1]));
+      prof_ms[pr.first] += t;
+      prof_n[pr.first] += 1;
+    }
+    ev_done.clear();
+    ev_used = 0;
+    for (int c = 0; c < CAKF_PROF_NCAT; ++c) {
+      if (ms) ms[c] = prof_ms[c];
+      if (n) n[c] = prof_n[c];
+      if (reset_) { prof_ms[c] = 0.0; prof_n[c] = 0; }
+    }
+    return CAKF_OK;
+  }
+
+  int kcur = 0, phase = 0;  // phase: 0 ready (expect predict), 1 predicted, 2 updated
+  bool smoothed = false;
+
+  ~Impl() override {
+    if (st) cudaStreamSynchronize(st);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    if (arena) cudaFree(arena);
+    if (ctl_init_host) cudaFreeHost(ctl_init_host);
+    if (blas) cublasDestroy(blas);
+    if (sol) cusolverDnDestroy(sol);
+    if (own_stream && st) cudaStreamDestroy(st);
+  }
+
+  template <typename U>
+  U* carve(size_t count) {
+    const size_t bytes = ((count * sizeof(U) + 255) / 256) * 256;
+    if (arena) {
+      U* p = reinterpret_cast<U*>(arena + arena_off);
+      arena_off += bytes;
+      return p;
+    }
+    arena_off += bytes;
+    return nullptr;
+  }
+
+  int step_cap_cols(int k) const {
+    if (k == 0) return 0;
+    const long grow = (long)(k - 1) * nhat;
+    const long rin = rcap >= 0 ? std::min<long>(rcap, grow) : grow;
+    return (int)(rin + nhat);
+  }
+
+  void layout() {
+    arena_off = 0;
+    coords = carve<V4<T>>(NX);
+    mu0 = carve<T>(D);
+    steps.resize(Tmax + 1);
+    for (int k = 0; k <= Tmax; ++k) {
+      Step& S = steps[k];
+      S.cap_cols = step_cap_cols(k);
+      S.m_pred = carve<T>(D);
+      S.m = carve<T>(D);
+      S.var = carve<T>(D);
+      S.ms = carve<T>(D);
+      S.vs = carve<T>(D);
+      S.Mk = carve<T>((size_t)D * S.cap_cols);
+      S.XV = k ? carve<T>((size_t)Nmax * (1 + nhat)) : nullptr;
+      S.idx = k ? carve<int>(Nmax) : nullptr;
+      S.kept = rcap > 0 ? carve<double>(rcap) : nullptr;
+    }
+    ctl = carve<IterCtl>(Tmax + 1);
+    rin_max = rcap >= 0 ? rcap : std::max(0, (Tmax - 1) * nhat);
+    qmax = rcap >= 0 ? rcap : Tmax * nhat;
+    cmax = std::max(rin_max + nhat, nhat + qmax);
+    W = std::max(rin_max, nhat) + 8;
+    xcs = carve<V4<T>>(Nmax);
+    r = carve<T>(Nmax); s = carve<T>(Nmax); g = carve<T>(Nmax); gp = carve<T>(Nmax);
+    d = carve<T>(Nmax); Gd = carve<T>(Nmax);
+    ybuf = carve<T>(Nmax); lam2 = carve<T>(Nmax);
+    Z = carve<T>((size_t)Nmax * std::max(nhat, 1));
+    HM = carve<T>((size_t)Nmax * std::max(rin_max, 1));
+    const int nch = matvec_chunks((int)Nmax, (int)Nmax, sizeof(T));
+    partial_cap = (size_t)std::max<int64_t>(nch, 64) * Nmax;
+    partial = carve<T>(partial_cap);
+    stage64 = carve<int64_t>(std::max<int64_t>(Nmax, NX));
+    order32 = carve<int>(std::max(nhat, 1));
+    part = carve<double>((size_t)320 * W);
+    redA = carve<double>(W);
+    redB = carve<double>(W);
+    redC = carve<double>(W);
+    cnt = carve<unsigned>(16);
+    Yb = carve<T>((size_t)NX * (1 + nhat));
+    Ub = carve<T>((size_t)std::max(rin_max, 1) * (1 + nhat));
+    tmp = carve<T>((size_t)D * (1 + nhat));
+    if (rcap >= 0) {
+      gpart = carve<double>((size_t)nsplit_max * cmax * cmax);
+      Gm = carve<double>((size_t)cmax * cmax);
+      eigw = carve<double>(cmax);
+      work = carve<double>(std::max(lwork, 1));
+      info = carve<int>(4);
+      QrD = carve<double>((size_t)cmax * std::max(rcap, 1));
+      Mtil = carve<T>((size_t)D * std::max(rcap, 1));
+    }
+    if (sizeof(T) == 4) {
+      const size_t C1 = (size_t)(1 + qmax);
+      dscr = std::max<size_t>({(size_t)D * (size_t)(std::max(cmax, 1 + qmax) + 1), (size_t)Nmax * C1,
+                               (size_t)std::max(rin_max, 1) * C1, (size_t)std::max(nhat, 1) * C1,
+                               (size_t)cmax * (size_t)std::max(rcap, 1), (size_t)Nmax * (size_t)(1 + nhat),
+                               (size_t)std::max(rin_max, 1) * (size_t)(1 + nhat)});
+      dA = carve<double>(dscr);
+      dB = carve<double>(dscr);
+      dC = carve<double>(dscr);
+    }
+    const size_t C = 1 + qmax;
+    X = carve<T>((size_t)D * C);
+    Yk = carve<T>((size_t)D * C);
+    yb = carve<T>((size_t)D * C);
+    Tm = carve<T>((size_t)std::max(rin_max, 1) * C);
+    Hy = carve<T>((size_t)Nmax * C);
+    tt = carve<T>((size_t)std::max(nhat, 1) * C);
+    R = carve<T>((size_t)Nmax * C);
+    Wf = carve<T>((size_t)D * (nhat + qmax));
+    Ws = carve<T>((size_t)D * (nhat + qmax));
+    ws = carve<T>(D);
+    pvar = carve<T>(D);
+  }
+
+  int init(const cakf_config& c) override {
+    Dp = c.d_time; dim = c.space_dim; nu2 = c.spatial_kernel; policy = c.policy;
+    nhat = c.max_iter; rcap = c.max_rank; Tmax = c.max_steps; NX = c.n_space; D = NX * Dp;
+    Nmax = c.max_obs > 0 ? std::min<int64_t>(c.max_obs, NX) : NX;
+    rtol = c.rtol; ell = c.ell_x; seed = c.seed; reorth = c.reorth != 0;
+    if (rtol != 0.0) return fail(CAKF_E_UNSUPPORTED, "rtol != 0 is not supported by the device path (R2)");
+    std::vector<double> st0;
+    if (!fetch_doubles(c.sigma_t0, (size_t)Dp * Dp, st0)) return fail(CAKF_E_ARG, "cannot read sigma_t0");
+    sig_t0 = mat_from(st0.data(), Dp);
+    if (c.stream) st = (cudaStream_t)c.stream;
+    else {
+      CK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      own_stream = true;
+    }
+    if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) return fail(CAKF_E_CUDA, "cublasCreate failed");
+    CK_BLAS(cublasSetStream(blas, st));
+    if (c.max_rank >= 0) {
+      if (cusolverDnCreate(&sol) != CUSOLVER_STATUS_SUCCESS) return fail(CAKF_E_CUDA, "cusolverDnCreate failed");
+      CK_SOLVER(cusolverDnSetStream(sol, st));
+    }
+    // size pass, then workspace query, then the real allocation
+    layout();
+    if (rcap >= 0 && cmax > 0) {
+      CK_SOLVER(cusolverDnDsyevd_bufferSize(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, cmax, nullptr, cmax,
+                                            nullptr, &lwork));
+    }
+    layout();
+    arena_bytes = arena_off;
+    cudaError_t e = cudaMalloc(&arena, arena_bytes);
+    if (e != cudaSuccess) {
+      arena = nullptr;
+      return fail(CAKF_E_NOMEM, "trace arena of " + std::to_string(arena_bytes) + " bytes: " + cudaGetErrorString(e));
+    }
+    layout();
+    CK_CUDA(cudaMemsetAsync(cnt, 0, 16 * sizeof(unsigned), st));
+    CK_CUDA(cudaMallocHost(&ctl_init_host, sizeof(IterCtl)));
+    std::memset(ctl_init_host, 0, sizeof(IterCtl));
+    ctl_init_host->eta_min = INFINITY;
+    // coordinates: copy (host or device doubles) and prescale by sqrt(2 nu)/ell
+    double* dxyz = reinterpret_cast<double*>(stage64);
+    CK_CUDA(cudaMemcpyAsync(dxyz, c.coords, (size_t)NX * dim * sizeof(double), cudaMemcpyDefault, st));
+    CK_CUDA(launch_prescale_coords<T>((int)NX, dim, dxyz, std::sqrt((double)nu2) / ell, coords, st));
+    std::vector<T> mu(D, T(0));
+    if (c.mu0) {
+      std::vector<double> m0;
+      if (!fetch_doubles(c.mu0, D, m0)) return fail(CAKF_E_ARG, "cannot read mu0");
+      for (int64_t i = 0; i < D; ++i) mu[i] = (T)m0[i];
+    }
+    CK_CUDA(cudaMemcpyAsync(mu0, mu.data(), D * sizeof(T), cudaMemcpyHostToDevice, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+    return reset();
+  }
+
+  int reset() override {
+    Step& S0 = steps[0];
+    S0.sig_t = sig_t0;
+    S0.rin = S0.cols = S0.n = S0.N = S0.rank_out = 0;
+    S0.missing = true;
+    S0.truncated = false;
+    CK_CUDA(cudaMemcpyAsync(S0.m_pred, mu0, D * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(S0.m, mu0, D * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    CK_CUDA(StepKernels<T>::rowvar((int)NX, Dp, S0.sig_t, nullptr, S0.Mk, D, 0, S0.var, st));
+    CK_CUDA(cudaMemcpyAsync(&ctl[0], ctl_init_host, sizeof(IterCtl), cudaMemcpyHostToDevice, st));
+    kcur = 0;
+    phase = 0;
+    smoothed = false;
+    failed_ = false;
+    return CAKF_OK;
+  }
+
+  int predict(const double* A_t, const double* Q_t, const void* b) override {
+    if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
+    if (phase != 0) return fail(CAKF_E_STATE, "predict: expected after create/reset/truncate");
+    if (kcur >= Tmax) return fail(CAKF_E_ARG, "predict: max_steps exhausted");
+    if (!A_t || !Q_t) return fail(CAKF_E_ARG, "predict: A_t and Q_t are required");
+    std::vector<double> a, q;
+    if (!fetch_doubles(A_t, (size_t)Dp * Dp, a) || !fetch_doubles(Q_t, (size_t)Dp * Dp, q))
+      return fail(CAKF_E_ARG, "predict: cannot read A_t/Q_t");
+    Step& P = steps[kcur];
+    Step& S = steps[kcur + 1];
+    const Mat3 A = mat_from(a.data(), Dp), Q = mat_from(q.data(), Dp);
+    P.A_next = A;
+    S.sig_t = mat_abat_plus_q(A, P.sig_t, Q, Dp);                     // Sigma^t_k
+    CK_CUDA(StepKernels<T>::mix((int)NX, Dp, 1, A, false, P.m, D, S.m_pred, D, st));   // m^- = A m
+    if (b) {
+      CK_CUDA(cudaMemcpyAsync(tmp, b, D * sizeof(T), cudaMemcpyDefault, st));
+      CK_BLAS(Blas<T>::axpy(blas, (int)D, T(1), tmp, S.m_pred));
+    }
+    const T* src = P.truncated ? Mtil : P.Mk;
+    const int rin = P.truncated ? P.rank_out : P.cols;
+    S.rin = rin;                                                      // M^- = A M~   (Prop A.3)
+    if (rin) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, rin, A, false, src, D, S.Mk, D, st));
+    S.cols = rin;
+    S.n = S.N = 0;
+    S.missing = true;
+    S.truncated = false;
+    S.rank_out = rin;
+    CK_CUDA(cudaMemcpyAsync(&ctl[kcur + 1], ctl_init_host, sizeof(IterCtl), cudaMemcpyHostToDevice, st));
+    kcur += 1;
+    phase = 1;
+    smoothed = false;
+    return CAKF_OK;
+  }
+
+  int update(int64_t n_obs, const int64_t* obs_idx, const void* y, const void* noise_var,
+             const int64_t* coord_order) override {
+    if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
+    if (phase != 1) return fail(CAKF_E_STATE, "update: expected after predict");
+    if (n_obs < 0 || n_obs > Nmax) return fail(CAKF_E_ARG, "update: n_obs outside [0, max_obs]");
+    Step& S = steps[kcur];
+    const int k = kcur;
+    const int N = (int)n_obs;
+    if (N == 0) {                                                     // IsMissing
+      CK_CUDA(cudaMemcpyAsync(S.m, S.m_pred, D * sizeof(T), cudaMemcpyDeviceToDevice, st));
+      S.cols = S.rin;
+      S.n = 0;
+      S.N = 0;
+      S.missing = true;
+      CK_CUDA(StepKernels<T>::rowvar((int)NX, Dp, S.sig_t, nullptr, S.Mk, D, S.cols, S.var, st));
+      phase = 2;
+      return CAKF_OK;
+    }
+    if (!obs_idx || !y || !noise_var) return fail(CAKF_E_ARG, "update: obs_idx, y and noise_var are required");
+    const int niter = std::min<int>(nhat, N);
+    if (policy == CAKF_POLICY_COORD && niter > 0 && !coord_order)
+      return fail(CAKF_E_ARG, "update: coordinate policy needs coord_order");
+    if (!is_device_ptr(obs_idx)) {
+      for (int i = 0; i < N; ++i)
+        if (obs_idx[i] < 0 || obs_idx[i] >= NX) return fail(CAKF_E_ARG, "update: obs_idx out of range");
+    }
+    if (policy == CAKF_POLICY_COORD && niter > 0 && !is_device_ptr(coord_order)) {
+      for (int i = 0; i < niter; ++i)
+        if (coord_order[i] < 0 || coord_order[i] >= N) return fail(CAKF_E_ARG, "update: coord_order out of range");
+    }
+    S.N = N;
+    S.n = niter;
+    S.missing = false;
+    // ---- stage inputs (host or device pointers)
+    CK_CUDA(cudaMemcpyAsync(stage64, obs_idx, (size_t)N * sizeof(int64_t), cudaMemcpyDefault, st));
+    CK_CUDA(idx64_to32(N, stage64, S.idx, st));
+    CK_CUDA(cudaMemcpyAsync(ybuf, y, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
+    CK_CUDA(cudaMemcpyAsync(lam2, noise_var, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
+    if (policy == CAKF_POLICY_COORD && niter > 0) {
+      CK_CUDA(cudaMemcpyAsync(stage64, coord_order, (size_t)niter * sizeof(int64_t), cudaMemcpyDefault, st));
+      CK_CUDA(idx64_to32(niter, stage64, order32, st));
+    }
+    const int rin = S.rin;
+    IterCtl* C = &ctl[k];
+    // ---- H M^- (N x rin) and r^(0), first action
+    if (rin) CK_CUDA(StepKernels<T>::gather_rows(N, rin, S.idx, S.Mk, D, HM, N, st));
+    CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, S.m_pred, policy, order32, seed, k, r, s, S.XV, xcs, st));
+    const double sig00 = S.sig_t.a[0][0];
+    const double eps = sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON;
+    const int nch = std::max(1, std::min<int>(matvec_chunks(N, N, sizeof(T)), (int)(partial_cap / N)));
+    T* V = S.XV + N;
+    for (int i = 1; i <= niter; ++i) {
+      // G s  (matrix-free: kernel rows on the fly + low-rank downdate + noise)
+      size_t pk = prof_begin();
+      CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
+      prof_end(CAKF_PROF_K1, pk);
+      pk = prof_begin();
+      CK_CUDA(StepKernels<T>::stageA(N, nch, partial, sig00, lam2, s, r, gp, HM, rin, part, W, redA, cnt + 0, st));
+      CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 1, st));
+      if (reorth && i > 1) {  // CGS2 (R19): d = s - V c, then d -= V (V^T G d)
+        CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W, redC,
+                                       cnt + 2, C, eps, i, 1, st));
+        CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redC, d, Gd, d, Gd, s, redA, rin, redB + (i - 1), part, W,
+                                       nullptr, cnt + 2, C, eps, i, 0, st));
+      } else {
+        CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W,
+                                       nullptr, cnt + 2, C, eps, i, 0, st));
+      }
+      CK_CUDA(StepKernels<T>::stageD(N, i, niter, C, d, Gd, S.XV, Z, r, s, xcs, policy, order32, seed, k, st));
+      prof_end(CAKF_PROF_STAGES, pk);
+    }
+    CK_CUDA(StepKernels<T>::dot(N, r, r, part, &C->res_sq, cnt + 3, st));
+    // ---- post-loop: [P^- w, P^- W] = Sigma H^T [v V] - M^- (H M^-)^T [v V]
+    const int Cc = 1 + niter;
+    size_t pk = prof_begin();
+    CK_CUDA(launch_gram_gemm<T>(nu2, coords, (int)NX, xcs, N, S.XV, N, Cc, Yb, NX, 1.0, st));
+    prof_end(CAKF_PROF_K2_POST, pk);
+    if (rin) {
+      pk = prof_begin();
+      CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rin, Cc, N, 1.0, HM, N, S.XV, N, 0.0, Ub, rin));
+      CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, Cc, rin, 1.0, S.Mk, (int)D, Ub, rin, 0.0, tmp, (int)D));
+      prof_end(CAKF_PROF_LOWRANK, pk);
+    }
+    CK_CUDA(StepKernels<T>::post_combine((int)NX, Dp, Cc, S.sig_t, Yb, rin ? tmp : nullptr, S.m_pred, S.m, S.Mk, rin,
+                                         st));
+    S.cols = rin + niter;
+    CK_CUDA(StepKernels<T>::rowvar((int)NX, Dp, S.sig_t, nullptr, S.Mk, D, S.cols, S.var, st));
+    phase = 2;
+    return CAKF_OK;
+  }
+
+  // C = alpha op(A) op(B) + beta C with fp64 accumulation for both dtypes (B optionally already fp64).
+  int gemm_impl(cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, double alpha, const T* A, int lda,
+                const T* B, const double* Bd, int ldb, double beta, T* C, int ldc) {
+    if (m <= 0 || n <= 0) return CAKF_OK;
+    if constexpr (sizeof(T) == 8) {
+      const double* Bp = Bd ? Bd : reinterpret_cast<const double*>(B);
+      CK_BLAS(cublasDgemm(blas, ta, tb, m, n, k, &alpha, reinterpret_cast<const double*>(A), lda, Bp, ldb, &beta,
+                          reinterpret_cast<double*>(C), ldc));
+    } else {
+      const int ar = ta == CUBLAS_OP_N ? m : k, ac = ta == CUBLAS_OP_N ? k : m;
+      const int br = tb == CUBLAS_OP_N ? k : n, bc = tb == CUBLAS_OP_N ? n : k;
+      if ((size_t)ar * ac > dscr || (size_t)br * bc > dscr || (size_t)m * n > dscr)
+        return fail(CAKF_E_ARG, "gemm: fp64 scratch too small");
+      CK_CUDA((convert<float, double>)(ar, ac, reinterpret_cast<const float*>(A), lda, dA, ar, st));
+      const double* Bp = Bd;
+      int ldbp = ldb;
+      if (!Bd) {
+        CK_CUDA((convert<float, double>)(br, bc, reinterpret_cast<const float*>(B), ldb, dB, br, st));
+        Bp = dB;
+        ldbp = br;
+      }
+      if (beta != 0.0) CK_CUDA((convert<float, double>)(m, n, reinterpret_cast<const float*>(C), ldc, dC, m, st));
+      if (k > 0) {
+        CK_BLAS(cublasDgemm(blas, ta, tb, m, n, k, &alpha, dA, ar, Bp, ldbp, &beta, dC, m));
+      } else {
+        CK_CUDA(cudaMemsetAsync(dC, 0, (size_t)m * n * sizeof(double), st));
+      }
+      CK_CUDA((convert<double, float>)(m, n, dC, m, reinterpret_cast<float*>(C), ldc, st));
+    }
+    return CAKF_OK;
+  }
+  int gemm(cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, double alpha, const T* A, int lda,
+           const T* B, int ldb, double beta, T* C, int ldc) {
+    return gemm_impl(ta, tb, m, n, k, alpha, A, lda, B, nullptr, ldb, beta, C, ldc);
+  }
+
+  // Truncate a D x c factor F (ld D) to its top-r Gram eigen-directions: out = F Q_r.
+  int truncate_factor(const T* F, int c, int rkeep, T* out, double* kept, double* dropped) {
+    const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit_max, D / 4096));
+    const size_t pk = prof_begin();
+    CK_CUDA(StepKernels<T>::gram(D, c, F, D, gpart, nsplit, Gm, st));
+    CK_SOLVER(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, c, Gm, c, eigw, work, lwork, info));
+    CK_CUDA(StepKernels<double>::take_top(c, rkeep, Gm, eigw, QrD, kept, dropped, st));
+    CK(gemm_impl(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, QrD, c, 0.0, out, (int)D));
+    prof_end(CAKF_PROF_TRUNCATE, pk);
+    return CAKF_OK;
+  }
+
+  int truncate() override {
+    if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
+    if (phase == 1) CK(update(0, nullptr, nullptr, nullptr, nullptr));
+    if (phase != 2) return fail(CAKF_E_STATE, "truncate: expected after update");
+    Step& S = steps[kcur];
+    if (rcap < 0 || S.cols <= rcap) {
+      S.truncated = false;
+      S.rank_out = S.cols;
+    } else {
+      CK(truncate_factor(S.Mk, S.cols, rcap, Mtil, S.kept, &ctl[kcur].dropped));   // Sec. 3.2
+      S.truncated = true;
+      S.rank_out = rcap;
+    }
+    phase = 0;
+    return CAKF_OK;
+  }
+
+  int smooth() override {
+    if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
+    if (phase != 0 || kcur < 1) return fail(CAKF_E_STATE, "caks_smooth: expected after >= 1 truncated step");
+    const int T_ = kcur;
+    Step& ST = steps[T_];
+    CK_CUDA(cudaMemcpyAsync(ST.ms, ST.m, D * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(ST.vs, ST.var, D * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    // w^s_T = H^T v_T, W^s_T = H^T V_T  (alg:mfks lines 2-3)
+    int q = ST.n;
+    CK_CUDA(StepKernels<T>::fill(D, T(0), X, st));
+    CK_CUDA(StepKernels<T>::fill((size_t)std::max(ST.N, 1), T(0), R, st));
+    CK_CUDA(StepKernels<T>::ws_build(ST.N, D, ST.n, 0, ST.idx, X, ST.XV, R, Ws, ws, st));
+    ST.smoother_rank = q;
+    for (int k = T_ - 1; k >= 0; --k) {
+      Step& S = steps[k];
+      const int C = 1 + q;
+      // x = A_k^T [w^s_{k+1}, W^s_{k+1}]
+      CK_CUDA(StepKernels<T>::mix((int)NX, Dp, 1, S.A_next, true, ws, D, X, D, st));
+      if (q) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, q, S.A_next, true, Ws, D, X + D, D, st));
+      // Sigma_k x = (Sigma^t_k (x) K) x : K applied to all D' blocks of all C columns at once
+      size_t pk = prof_begin();
+      CK_CUDA(launch_gram_gemm<T>(nu2, coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX, 1.0, st));
+      prof_end(CAKF_PROF_K2_SMOOTH, pk);
+      CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, C, S.sig_t, Yk, yb, st));
+      const int rin = S.rin, n = S.n, N = S.N;
+      // y = P^-_k x = Sigma x - M^- (M^-^T x)
+      pk = prof_begin();
+      if (rin) {
+        CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rin, C, (int)D, 1.0, S.Mk, (int)D, X, (int)D, 0.0, Tm, rin));
+        CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, C, rin, -1.0, S.Mk, (int)D, Tm, rin, 1.0, yb, (int)D));
+      }
+      // P_k x = y - B_k (V^T H y);  R = V (V^T H y)
+      if (n) {
+        T* Vk = S.XV + N;
+        CK_CUDA(StepKernels<T>::gather_rows(N, C, S.idx, yb, D, Hy, N, st));
+        CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, n, C, N, 1.0, Vk, N, Hy, N, 0.0, tt, n));
+        CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, C, n, -1.0, S.Mk + (size_t)rin * D, (int)D, tt, n, 1.0, yb, (int)D));
+        CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, N, C, n, 1.0, Vk, N, tt, n, 0.0, R, N));
+      }
+      prof_end(CAKF_PROF_LOWRANK, pk);
+      // m^s_k = m_k + P_k A^T w^s ;  var^s_k = var_k - rowsumsq(P_k A^T W^s)   (lines 5-6)
+      CK_CUDA(StepKernels<T>::smooth_out(D, C, S.m, S.var, yb, S.ms, S.vs, st));
+      // w^s_k, W^s_k = [W_k, (I - W W^T P^-) A^T W^s]   (lines 7-8)
+      CK_CUDA(StepKernels<T>::ws_build(n ? N : 0, D, n, q, S.idx, X, S.XV, R, Wf, ws, st));
+      const int qn = n + q;
+      if (rcap >= 0 && qn > rcap) {                                   // line 9 (R6)
+        CK(truncate_factor(Wf, qn, rcap, Ws, nullptr, nullptr));
+        q = rcap;
+      } else {
+        std::swap(Wf, Ws);
+        q = qn;
+      }
+      S.smoother_rank = q;
+    }
+    smoothed = true;
+    return CAKF_OK;
+  }
+
+  int get(int k, int which, void* mean, void* var) override {
+    if (k < 0 || k > kcur) return fail(CAKF_E_ARG, "get: step index out of range");
+    Step& S = steps[k];
+    const T *pm = nullptr, *pv = nullptr;
+    if (which == CAKF_PRED) {
+      pm = S.m_pred;
+      if (var) {
+        CK_CUDA(StepKernels<T>::rowvar((int)NX, Dp, S.sig_t, nullptr, S.Mk, D, S.rin, pvar, st));
+        pv = pvar;
+      }
+    } else if (which == CAKF_FILTER) {
+      if (k == kcur && phase == 1) return fail(CAKF_E_STATE, "get: step not updated yet");
+      pm = S.m;
+      pv = S.var;
+    } else if (which == CAKF_SMOOTH) {
+      if (!smoothed) return fail(CAKF_E_STATE, "get: caks_smooth has not run");
+      pm = S.ms;
+      pv = S.vs;
+    } else {
+      return fail(CAKF_E_ARG, "get: bad which");
+    }
+    if (mean) CK_CUDA(cudaMemcpyAsync(mean, pm, D * sizeof(T), cudaMemcpyDefault, st));
+    if (var) CK_CUDA(cudaMemcpyAsync(var, pv, D * sizeof(T), cudaMemcpyDefault, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+    return CAKF_OK;
+  }
+
+  int stats(int k, cakf_step_stats* out) override {
+    if (k < 0 || k > kcur) return fail(CAKF_E_ARG, "get_stats: step index out of range");
+    IterCtl c{};
+    CK_CUDA(cudaMemcpyAsync(&c, &ctl[k], sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+    const Step& S = steps[k];
+    out->k = k;
+    out->iters = S.n;
+    out->rejected = c.rejected;
+    out->rank_in = S.rin;
+    out->cols = S.cols;
+    out->rank_out = S.rank_out;
+    out->smoother_rank = smoothed ? S.smoother_rank : -1;
+    out->missing = S.missing ? 1 : 0;
+    out->res0 = std::sqrt(c.res0_sq);
+    out->res_final = std::sqrt(c.res_sq);
+    out->eta_min = c.eta_min;
+    out->dropped_mass = c.dropped;
+    if (c.nonfinite) return fail(CAKF_E_NUMERIC, "non-finite eta/alpha in step " + std::to_string(k));
+    return CAKF_OK;
+  }
+
+  int kept_eigs(int k, double* vals, int cap, int* n_out) override {
+    if (k < 0 || k > kcur) return fail(CAKF_E_ARG, "get_kept_eigs: step index out of range");
+    const Step& S = steps[k];
+    const int n = S.truncated ? S.rank_out : 0;
+    if (n_out) *n_out = n;
+    if (n && vals) {
+      CK_CUDA(cudaMemcpyAsync(vals, S.kept, (size_t)std::min(n, cap) * sizeof(double), cudaMemcpyDefault, st));
+      CK_CUDA(cudaStreamSynchronize(st));
+    }
+    return CAKF_OK;
+  }
+
+  int profile(bool on) override {
+    prof_on = on;
+    return CAKF_OK;
+  }
+
+  int sync() override {
+    CK_CUDA(cudaStreamSynchronize(st));
+    return CAKF_OK;
+  }
+};
+
+}  // namespace
+
+struct cakf_s {
+  ImplBase* impl = nullptr;
+};
+
+extern "C" {
+
+const char* cakf_last_error(void) { return g_last_error.c_str(); }
+int cakf_version(void) { return CAKF_VERSION; }
+
+int cakf_create(const cakf_config* cfg, cakf_t* out) {
+  if (!cfg || !out) return fail(CAKF_E_ARG, "cakf_create: NULL argument");
+  *out = nullptr;
+  if (cfg->world != 1 && cfg->world != 0) return fail(CAKF_E_UNSUPPORTED, "cakf_create: world > 1 not in this build");
+  if (cfg->dtype != CAKF_F32 && cfg->dtype != CAKF_F64) return fail(CAKF_E_ARG, "cakf_create: bad dtype");
+  if (cfg->d_time < 1 || cfg->d_time > 3) return fail(CAKF_E_UNSUPPORTED, "cakf_create: d_time must be 1..3");
+  if (cfg->n_space < 1 || cfg->n_space > (int64_t)1 << 30) return fail(CAKF_E_ARG, "cakf_create: bad n_space");
+  if (cfg->space_dim < 1 || cfg->space_dim > 3) return fail(CAKF_E_ARG, "cakf_create: space_dim must be 1..3");
+  if (!cfg->coords || !cfg->sigma_t0) return fail(CAKF_E_ARG, "cakf_create: coords and sigma_t0 are required");
+  if (cfg->spatial_kernel != 1 && cfg->spatial_kernel != 3 && cfg->spatial_kernel != 5)
+    return fail(CAKF_E_UNSUPPORTED, "cakf_create: spatial_kernel must be MATERN12/32/52");
+  if (!(cfg->ell_x > 0)) return fail(CAKF_E_ARG, "cakf_create: ell_x must be > 0");
+  if (cfg->policy < 0 || cfg->policy > 2) return fail(CAKF_E_UNSUPPORTED, "cakf_create: unknown policy");
+  if (cfg->max_iter < 0 || cfg->max_steps < 1) return fail(CAKF_E_ARG, "cakf_create: bad max_iter / max_steps");
+  ImplBase* impl = nullptr;
+  if (cfg->dtype == CAKF_F32) impl = new Impl<float>();
+  else impl = new Impl<double>();
+  const int rc = impl->init(*cfg);
+  if (rc != CAKF_OK) {
+    const std::string msg = g_last_error;
+    delete impl;
+    g_last_error = msg;
+    return rc;
+  }
+  cakf_s* h = new cakf_s;
+  h->impl = impl;
+  *out = h;
+  return CAKF_OK;
+}
+
+#define HANDLE_CHECK(h) \
+  if (!(h) || !(h)->impl) return fail(CAKF_E_ARG, "NULL handle")
+
+int cakf_reset(cakf_t h) { HANDLE_CHECK(h); return h->impl->reset(); }
+int cakf_predict(cakf_t h, const double* A_t, const double* Q_t, const void* b) {
+  HANDLE_CHECK(h);
+  return h->impl->predict(A_t, Q_t, b);
+}
+int cakf_update(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* y, const void* noise_var,
+                const int64_t* coord_order) {
+  HANDLE_CHECK(h);
+  return h->impl->update(n_obs, obs_idx, y, noise_var, coord_order);
+}
+int cakf_truncate(cakf_t h) { HANDLE_CHECK(h); return h->impl->truncate(); }
+int caks_smooth(cakf_t h) { HANDLE_CHECK(h); return h->impl->smooth(); }
+int cakf_get(cakf_t h, int32_t k, int32_t which, void* mean_D, void* var_D) {
+  HANDLE_CHECK(h);
+  return h->impl->get(k, which, mean_D, var_D);
+}
+int cakf_get_stats(cakf_t h, int32_t k, cakf_step_stats* out) {
+  HANDLE_CHECK(h);
+  if (!out) return fail(CAKF_E_ARG, "NULL stats");
+  return h->impl->stats(k, out);
+}
+int cakf_get_kept_eigs(cakf_t h, int32_t k, double* vals, int32_t cap, int32_t* n_out) {
+  HANDLE_CHECK(h);
+  return h->impl->kept_eigs(k, vals, cap, n_out);
+}
+int cakf_sync(cakf_t h) { HANDLE_CHECK(h); return h->impl->sync(); }
+int cakf_profile(cakf_t h, int32_t enable) { HANDLE_CHECK(h); return h->impl->profile(enable != 0); }
+int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset) {
+  HANDLE_CHECK(h);
+  return h->impl->prof_read(ms, launches, reset != 0);
+}
+int64_t cakf_kernel_launches(void) { return (int64_t)launch_counter(); }
+int cakf_destroy(cakf_t h) {
+  if (!h) return CAKF_OK;
+  delete h->impl;
+  delete h;
+  return CAKF_OK;
+}
+
+int cakf_matern_transition(int32_t nu2, double ell_t, double sigma, double dt, double* A, double* Q, double* Sinf) {
+  // Closed forms of the companion-form SDE (R10); lam = sqrt(2 nu)/ell, e = exp(-lam dt).
+  if (!(ell_t > 0) || dt < 0) return fail(CAKF_E_ARG, "cakf_matern_transition: bad ell/dt");
+  const double lam = std::sqrt((double)nu2) / ell_t, s2 = sigma * sigma, e = std::exp(-lam * dt);
+  double a[9] = {0}, si[9] = {0};
+  int n = 0;
+  if (nu2 == 1) {
+    n = 1;
+    a[0] = e;
+    si[0] = s2;
+  } else if (nu2 == 3) {
+    n = 2;
+    const double x = lam * dt;
+    a[0] = e * (1 + x); a[1] = e * dt;
+    a[2] = -e * lam * lam * dt; a[3] = e * (1 - x);
+    si[0] = s2; si[3] = s2 * lam * lam;
+  } else if (nu2 == 5) {
+    n = 3;
+    const double t = dt, l = lam, l2 = l * l, l3 = l2 * l, t2 = t * t;
+    // expm of F = [[0,1,0],[0,0,1],[-l^3,-3l^2,-3l]]  (triple eigenvalue -l)
+    a[0] = e * (1 + l * t + 0.5 * l2 * t2); a[1] = e * (t + l * t2); a[2] = e * 0.5 * t2;
+    a[3] = -e * 0.5 * l3 * t2; a[4] = e * (1 + l * t - l2 * t2); a[5] = e * (t - 0.5 * l * t2);
+    a[6] = -e * l3 * (t - 0.5 * l * t2); a[7] = -e * l2 * (3 * t - l * t2); a[8] = e * (1 - 2 * l * t + 0.5 * l2 * t2);
+    si[0] = s2; si[2] = -s2 * l2 / 3.0; si[4] = s2 * l2 / 3.0; si[6] = -s2 * l2 / 3.0; si[8] = s2 * l2 * l2;
+  } else {
+    return fail(CAKF_E_UNSUPPORTED, "cakf_matern_transition: nu2 must be 1, 3 or 5");
+  }
+  if (A) std::memcpy(A, a, sizeof(double) * n * n);
+  if (Sinf) std::memcpy(Sinf, si, sizeof(double) * n * n);
+  if (Q) {
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        double acc = si[i * n + j];
+        for (int p = 0; p < n; ++p)
+          for (int q = 0; q < n; ++q) acc -= a[i * n + p] * si[p * n + q] * a[j * n + q];
+        Q[i * n + j] = acc;
+      }
+  }
+  return CAKF_OK;
+}
+
+int cakf_gram_matmul(int32_t dtype, int32_t spatial_kernel, double ell, int32_t space_dim, int64_t n_rows,
+                     const void* xr, int64_t n_cols, const void* xc, int32_t n_rhs, const void* X, double alpha,
+                     void* Y, void* stream) {
+  if (!xr || !xc || !X || !Y || n_rows < 0 || n_cols < 0 || n_rhs < 0 || space_dim < 1 || space_dim > 3 || !(ell > 0))
+    return fail(CAKF_E_ARG, "cakf_gram_matmul: bad argument");
+  if (spatial_kernel != 1 && spatial_kernel != 3 && spatial_kernel != 5)
+    return fail(CAKF_E_UNSUPPORTED, "cakf_gram_matmul: spatial_kernel");
+  cudaStream_t st = (cudaStream_t)stream;
+  const double scale = std::sqrt((double)spatial_kernel) / ell;
+  auto run = [&](auto tag) -> int {
+    using T = decltype(tag);
+    V4<T>*cr = nullptr, *cc = nullptr;
+    double* dxyz = nullptr;
+    T* part = nullptr;
+    bool failed_ = false;
+    (void)failed_;
+    const size_t nmax = (size_t)std::max(n_rows, n_cols);
+    std::vector<double> hx;
+    cudaError_t e = cudaMallocAsync(&dxyz, nmax * space_dim * sizeof(double), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&cr, (size_t)std::max<int64_t>(n_rows, 1) * sizeof(V4<T>), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&cc, (size_t)std::max<int64_t>(n_cols, 1) * sizeof(V4<T>), st);
+    // device coordinates of the handle dtype -> double staging
+    auto stage = [&](const void* src, int64_t n, V4<T>* dst) -> cudaError_t {
+      if (n == 0) return cudaSuccess;
+      std::vector<T> h((size_t)n * space_dim);
+      cudaError_t ee = cudaMemcpyAsync(h.data(), src, h.size() * sizeof(T), cudaMemcpyDefault, st);
+      if (ee != cudaSuccess) return ee;
+      ee = cudaStreamSynchronize(st);
+      if (ee != cudaSuccess) return ee;
+      std::vector<double> hd(h.begin(), h.end());
+      ee = cudaMemcpyAsync(dxyz, hd.data(), hd.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+      if (ee != cudaSuccess) return ee;
+      ee = launch_prescale_coords<T>((int)n, space_dim, dxyz, scale, dst, st);
+      if (ee != cudaSuccess) return ee;
+      return cudaStreamSynchronize(st);
+    };
+    if (e == cudaSuccess) e = stage(xr, n_rows, cr);
+    if (e == cudaSuccess) e = stage(xc, n_cols, cc);
+    if (e == cudaSuccess && n_rhs == 1 && n_rows > 0 && n_cols > 0) {
+      // K1 path: X is the column vector; pack it into .w of the column coordinates
+      std::vector<V4<T>> hc((size_t)n_cols);
+      std::vector<T> hxv((size_t)n_cols);
+      e = cudaMemcpyAsync(hc.data(), cc, hc.size() * sizeof(V4<T>), cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(hxv.data(), X, hxv.size() * sizeof(T), cudaMemcpyDefault, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      for (size_t j = 0; j < hc.size(); ++j) hc[j].w = hxv[j];
+      if (e == cudaSuccess) e = cudaMemcpyAsync(cc, hc.data(), hc.size() * sizeof(V4<T>), cudaMemcpyHostToDevice, st);
+      const int nch = matvec_chunks((int)n_rows, (int)n_cols, sizeof(T));
+      if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)nch * n_rows * sizeof(T), st);
+      if (e == cudaSuccess) e = launch_matvec_partial<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, nch, part, st);
+      if (e == cudaSuccess) e = launch_sum_partials<T>((int)n_rows, nch, part, alpha, (T*)Y, st);
+    } else if (e == cudaSuccess) {
+      e = launch_gram_gemm<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, (const T*)X, (size_t)n_cols, n_rhs,
+                              (T*)Y, (size_t)n_rows, alpha, st);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFreeAsync(dxyz, st);
+    cudaFreeAsync(cr, st);
+    cudaFreeAsync(cc, st);
+    if (part) cudaFreeAsync(part, st);
+    cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(CAKF_E_CUDA, std::string("cakf_gram_matmul: ") + cudaGetErrorString(e));
+    return CAKF_OK;
+  };
+  if (dtype == CAKF_F32) return run(float{});
+  if (dtype == CAKF_F64) return run(double{});
+  return fail(CAKF_E_ARG, "cakf_gram_matmul: bad dtype");
+}
+
+}  // extern "C"

@@ -1,0 +1,30 @@
+// internal.h — host launchers of libcakf's device kernels (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace cakf {
+
+// ---- K1: kernel matvec partials  partial[ch][i] = sum_{j in chunk ch} k(xr_i, xc_j) * xc_j.w
+template <typename T>
+cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<T>* xc, int ncols,
+                                  int nchunks, T* partial, cudaStream_t st);
+// choose the number of column chunks for a matvec of this shape (fills the GPU in whole waves)
+int matvec_chunks(int nrows, int ncols, int elem_bytes);
+// reduce partials: y[i] = alpha * sum_ch partial[ch][i]
+template <typename T>
+cudaError_t launch_sum_partials(int nrows, int nchunks, const T* partial, double alpha, T* y, cudaStream_t st);
+
+// ---- K2: kernel x matrix  Y[i, c] = alpha * sum_j k(xr_i, xc_j) B[j, c]  (column-major)
+template <typename T>
+cudaError_t launch_gram_gemm(int nu2, const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb,
+                             int C, T* Y, size_t ldy, double alpha, cudaStream_t st);
+
+// ---- coordinates
+template <typename T>
+cudaError_t launch_prescale_coords(int n, int dim, const double* xyz, double scale, V4<T>* out, cudaStream_t st);
+
+}  // namespace cakf

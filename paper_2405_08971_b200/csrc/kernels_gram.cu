@@ -1,0 +1,256 @@
+// kernels_gram.cu — fused kernel-evaluation x vector / x matrix products (sm_100a).
+//
+// The paper's bottleneck: products with the spatial Gram matrix
+// Sigma^x(X, X) that is never materialised.  Two shapes occur on the hot path:
+//   K1  single right-hand side (the inner-loop matvec G s):
+//       ALU bound (FP32 pipe + MUFU sqrt/ex2 per pair) — register-blocked rows,
+//       column chunk staged once in shared memory, broadcast LDS.128 reads.
+//   K2  many right-hand sides (post-loop a7, smoother a9): a GEMM whose A operand
+//       is generated on the fly; SIMT register-tiled version (8x8 per thread).
+#include <algorithm>
+
+#include "internal.h"
+
+namespace cakf {
+
+namespace {
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <typename T> constexpr int kRowsPerThread = sizeof(T) == 4 ? 4 : 2;
+constexpr int kMvThreads = 256;
+template <typename T> constexpr int kMaxChunk = sizeof(T) == 4 ? 2048 : 1024;
+
+// ------------------------------------------------------------------ K1
+template <typename T, int NU2, int R>
+__global__ void __launch_bounds__(kMvThreads)
+matvec_partial_kernel(const V4<T>* __restrict__ xr, int nrows, const V4<T>* __restrict__ xc, int ncols,
+                      int chunk, T* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V4<T>* sc = reinterpret_cast<V4<T>*>(smem_raw);
+  const int ch = blockIdx.y;
+  const int j0 = ch * chunk;
+  const int n = min(chunk, ncols - j0);
+  for (int j = threadIdx.x; j < n; j += kMvThreads) sc[j] = xc[j0 + j];
+
+  T px[R], py[R], pz[R], acc[R];
+  const int base = blockIdx.x * (kMvThreads * R) + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int row = base + k * kMvThreads;
+    V4<T> p{};
+    if (row < nrows) p = xr[row];
+    px[k] = p.x; py[k] = p.y; pz[k] = p.z;
+    acc[k] = T(0);
+  }
+  __syncthreads();
+#pragma unroll 2
+  for (int j = 0; j < n; ++j) {
+    const V4<T> c = sc[j];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const T dx = px[k] - c.x, dy = py[k] - c.y, dz = pz[k] - c.z;
+      const T d2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      acc[k] = fma(matern_from_d2<NU2>(d2), c.w, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int row = base + k * kMvThreads;
+    if (row < nrows) partial[(size_t)ch * nrows + row] = acc[k];
+  }
+}
+
+template <typename T>
+__global__ void sum_partials_kernel(int nrows, int nch, const T* __restrict__ partial, double alpha, T* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  double acc = 0.0;
+  for (int c = 0; c < nch; ++c) acc += (double)partial[(size_t)c * nrows + i];
+  y[i] = (T)(alpha * acc);
+}
+
+// ------------------------------------------------------------------ K2 (SIMT)
+template <typename T, int NU2, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+gram_gemm_kernel(const V4<T>* __restrict__ xr, int M, const V4<T>* __restrict__ xc, int K,
+                 const T* __restrict__ B, size_t ldb, int C, T* __restrict__ Y, size_t ldy, T alpha) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  static_assert(NT % BM == 0, "thread count must be a multiple of BM");
+  constexpr int KSTEP = NT / BM;
+  constexpr int AG = BK / KSTEP;
+  __shared__ __align__(16) T As[BK][BM];
+  __shared__ __align__(16) T Bs[BK][BN];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int tid = threadIdx.x;
+  const int arow = tid % BM, akk0 = tid / BM;
+  V4<T> xa{};
+  if (m0 + arow < M) xa = xr[m0 + arow];
+  const int ty = tid / (BN / TN), tx = tid % (BN / TN);
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) acc[i][c] = T(0);
+
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int q = 0; q < AG; ++q) {
+      const int kk = akk0 + q * KSTEP;
+      const int j = k0 + kk;
+      T v = T(0);
+      if (j < K) {
+        const V4<T> c = xc[j];
+        v = matern_from_d2<NU2>(dist2<T>(xa, c));
+      }
+      As[kk][arow] = v;
+    }
+    for (int e = tid; e < BK * BN; e += NT) {
+      const int kk = e % BK, nn = e / BK;
+      const int j = k0 + kk, n = n0 + nn;
+      Bs[kk][nn] = (j < K && n < C) ? B[j + (size_t)n * ldb] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int c = 0; c < TN; ++c) b[c] = Bs[kk][tx * TN + c];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) acc[i][c] = fma(a[i], b[c], acc[i][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int c = 0; c < TN; ++c) {
+    const int n = n0 + tx * TN + c;
+    if (n >= C) continue;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int m = m0 + ty * TM + i;
+      if (m < M) Y[m + (size_t)n * ldy] = alpha * acc[i][c];
+    }
+  }
+}
+
+template <typename T>
+__global__ void prescale_kernel(int n, int dim, const double* __restrict__ xyz, double scale, V4<T>* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double c[3] = {0.0, 0.0, 0.0};
+  for (int d = 0; d < dim; ++d) c[d] = xyz[(size_t)i * dim + d] * scale;
+  V4<T> v;
+  v.x = (T)c[0]; v.y = (T)c[1]; v.z = (T)c[2]; v.w = T(0);
+  out[i] = v;
+}
+
+template <typename T, int NU2>
+cudaError_t matvec_partial_nu(const V4<T>* xr, int nrows, const V4<T>* xc, int ncols, int nchunks, T* partial,
+                              cudaStream_t st) {
+  constexpr int R = kRowsPerThread<T>;
+  const int chunk = (ncols + nchunks - 1) / nchunks;
+  dim3 grid((nrows + kMvThreads * R - 1) / (kMvThreads * R), nchunks);
+  const size_t smem = (size_t)chunk * sizeof(V4<T>);
+  matvec_partial_kernel<T, NU2, R><<<grid, kMvThreads, smem, st>>>(xr, nrows, xc, ncols, chunk, partial);
+  return note_launch_err();
+}
+
+template <typename T, int NU2>
+cudaError_t gram_gemm_nu(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y,
+                         size_t ldy, double alpha, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (C <= 64) {
+      dim3 grid((M + 127) / 128, (C + 63) / 64);
+      gram_gemm_kernel<T, NU2, 128, 64, 16, 8, 4><<<grid, 256, 0, st>>>(xr, M, xc, K, B, ldb, C, Y, ldy, (T)alpha);
+    } else {
+      dim3 grid((M + 127) / 128, (C + 127) / 128);
+      gram_gemm_kernel<T, NU2, 128, 128, 16, 8, 8><<<grid, 256, 0, st>>>(xr, M, xc, K, B, ldb, C, Y, ldy, (T)alpha);
+    }
+  } else {
+    dim3 grid((M + 63) / 64, (C + 63) / 64);
+    gram_gemm_kernel<T, NU2, 64, 64, 16, 4, 4><<<grid, 256, 0, st>>>(xr, M, xc, K, B, ldb, C, Y, ldy, (T)alpha);
+  }
+  return note_launch_err();
+}
+
+}  // namespace
+
+int matvec_chunks(int nrows, int ncols, int elem_bytes) {
+  const int R = elem_bytes == 4 ? kRowsPerThread<float> : kRowsPerThread<double>;
+  const int maxchunk = elem_bytes == 4 ? kMaxChunk<float> : kMaxChunk<double>;
+  const long tiles = (nrows + kMvThreads * R - 1) / (kMvThreads * R);
+  const long slots = (long)num_sms() * (2048 / kMvThreads);  // resident CTAs per wave
+  const double pairs = (double)nrows * (double)ncols;
+  long waves = std::max(1L, (long)(pairs / ((double)slots * 262144.0)));
+  waves = std::min(waves, std::max(1L, 128L * tiles / slots));
+  long ch = std::max(1L, waves * slots / tiles);
+  const long ch_max = std::max(1L, (long)(ncols + 31) / 32);
+  const long ch_min = (ncols + maxchunk - 1) / maxchunk;
+  ch = std::min(ch, ch_max);
+  ch = std::max(ch, std::max(1L, ch_min));
+  return (int)ch;
+}
+
+template <typename T>
+cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<T>* xc, int ncols, int nchunks,
+                                  T* partial, cudaStream_t st) {
+  if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+  switch (nu2) {
+    case 1: return matvec_partial_nu<T, 1>(xr, nrows, xc, ncols, nchunks, partial, st);
+    case 3: return matvec_partial_nu<T, 3>(xr, nrows, xc, ncols, nchunks, partial, st);
+    case 5: return matvec_partial_nu<T, 5>(xr, nrows, xc, ncols, nchunks, partial, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t launch_sum_partials(int nrows, int nchunks, const T* partial, double alpha, T* y, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  sum_partials_kernel<T><<<(nrows + 255) / 256, 256, 0, st>>>(nrows, nchunks, partial, alpha, y);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t launch_gram_gemm(int nu2, const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C,
+                             T* Y, size_t ldy, double alpha, cudaStream_t st) {
+  if (M <= 0 || C <= 0) return cudaSuccess;
+  switch (nu2) {
+    case 1: return gram_gemm_nu<T, 1>(xr, M, xc, K, B, ldb, C, Y, ldy, alpha, st);
+    case 3: return gram_gemm_nu<T, 3>(xr, M, xc, K, B, ldb, C, Y, ldy, alpha, st);
+    case 5: return gram_gemm_nu<T, 5>(xr, M, xc, K, B, ldb, C, Y, ldy, alpha, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t launch_prescale_coords(int n, int dim, const double* xyz, double scale, V4<T>* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  prescale_kernel<T><<<(n + 255) / 256, 256, 0, st>>>(n, dim, xyz, scale, out);
+  return note_launch_err();
+}
+
+#define INST(T)                                                                                           \
+  template cudaError_t launch_matvec_partial<T>(int, const V4<T>*, int, const V4<T>*, int, int, T*,       \
+                                                cudaStream_t);                                            \
+  template cudaError_t launch_sum_partials<T>(int, int, const T*, double, T*, cudaStream_t);              \
+  template cudaError_t launch_gram_gemm<T>(int, const V4<T>*, int, const V4<T>*, int, const T*, size_t,   \
+                                           int, T*, size_t, double, cudaStream_t);                        \
+  template cudaError_t launch_prescale_coords<T>(int, int, const double*, double, V4<T>*, cudaStream_t);
+INST(float)
+INST(double)
+#undef INST
+
+}  // namespace cakf

@@ -1,0 +1,614 @@
+// kernels_step.cu — streaming kernels of one CAKF/CAKS time step (sm_100a).
+//
+// Inner loop of alg:update_pls per iteration i, with
+// G s = Sigma^t_00 K_TT s + Lambda s - (H M^-)((H M^-)^T s):
+//   [K1 matvec partials]                       kernels_gram.cu
+//   stage A  g' = sig00 * sum(partials) + lam2 .* s ;  u = (HM)^T s ; alpha = s^T r
+//   stage B  g  = g' - HM u ;  c = V^T g ;  s^T g
+//   stage C  d  = s - V c ;  Gd = g - Z c (Z = G V kept, R18) ; eta = s^T Gd ; accept (R2)
+//   stage D  v += (alpha/eta) d ; V_i = d/sqrt(eta) ; Z_i = Gd/sqrt(eta) ;
+//            r -= (alpha/eta) Gd ; next action s (policy) packed into the column coords
+// Each reduction writes per-block partials (fp64); the last block to arrive sums them
+// in block order (deterministic, no float atomics).
+#include "internal.h"
+#include "step.h"
+
+namespace cakf {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void block_rows(int N, int rb, int& r0, int& r1) {
+  r0 = blockIdx.x * rb;
+  r1 = min(N, r0 + rb);
+}
+
+// out[j] = sum_{rows in [r0, r1)} A[row + j*ld] * v[row]  (warp per column, fp32/64 lane sums, fp64 warp sums)
+template <typename T>
+__device__ void block_cols_dot(const T* __restrict__ A, size_t ld, int ncols, const T* __restrict__ v, int r0, int r1,
+                               double* __restrict__ out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < ncols; j += nw) {
+    const T* col = A + (size_t)j * ld;
+    T acc = T(0);
+    for (int row = r0 + lane; row < r1; row += 32) acc = fma(col[row], v[row], acc);
+    const double s = warp_sum((double)acc);
+    if (lane == 0) out[j] = s;
+  }
+}
+
+__device__ void finalize_sum(int nb, int W, int n, const double* part, double* red) {
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += __ldcg(part + (size_t)b * W + j);
+    red[j] = s;
+  }
+}
+
+// ------------------------------------------------------------------ update prologue
+template <typename T>
+__global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __restrict__ coords, const T* __restrict__ y,
+                            const T* __restrict__ mpred, int policy, const int* __restrict__ order, uint64_t seed, int k,
+                            T* __restrict__ r, T* __restrict__ s, T* __restrict__ v, V4<T>* __restrict__ xcs) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= N) return;
+  const int p = idx[row];
+  const T r0 = y[row] - mpred[p];                      // r^(0) = y - H m^-   
+  T s0;
+  if (policy == 0) s0 = r0;                            // CG: s_1 = r^(1) = r^(0)  (R1)
+  else if (policy == 1) s0 = (order[0] == row) ? T(1) : T(0);
+  else s0 = (T)philox_normal(seed, (uint32_t)k, 1u, (uint32_t)row);
+  r[row] = r0;
+  s[row] = s0;
+  v[row] = T(0);
+  V4<T> c = coords[p];
+  c.w = s0;
+  xcs[row] = c;
+}
+
+// ------------------------------------------------------------------ stage A
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+stageA_kernel(int N, int rb, int nch, const T* __restrict__ partial, double sig00, const T* __restrict__ lam2,
+              const T* __restrict__ s, const T* __restrict__ r, T* __restrict__ gp, const T* __restrict__ HM, int rin,
+              double* __restrict__ part, int W, double* __restrict__ red, unsigned* cnt) {
+  __shared__ double scratch[32 * 3];
+  int r0, r1;
+  block_rows(N, rb, r0, r1);
+  double a[3] = {0.0, 0.0, 0.0};  // s.r, s.g', r.r
+  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < nch; ++c) acc += (double)partial[(size_t)c * N + row];
+    const T si = s[row], ri = r[row];
+    const T g = (T)(sig00 * acc) + lam2[row] * si;
+    gp[row] = g;
+    a[0] += (double)si * (double)ri;
+    a[1] += (double)si * (double)g;
+    a[2] += (double)ri * (double)ri;
+  }
+  block_sum<3>(a, scratch);
+  double* slot = part + (size_t)blockIdx.x * W;
+  if (threadIdx.x == 0) { slot[rin] = a[0]; slot[rin + 1] = a[1]; slot[rin + 2] = a[2]; }
+  block_cols_dot(HM, (size_t)N, rin, s, r0, r1, slot);          // u = (HM)^T s
+  if (arrive_last(cnt)) {
+    finalize_sum(gridDim.x, W, rin + 3, part, red);
+    if (threadIdx.x == 0) *cnt = 0u;
+  }
+}
+
+// ------------------------------------------------------------------ stage B
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+stageB_kernel(int N, int rb, const T* __restrict__ HM, int rin, const double* __restrict__ ured,
+              const T* __restrict__ gp, const T* __restrict__ s, T* __restrict__ g, const T* __restrict__ V, int nV,
+              double* __restrict__ part, int W, double* __restrict__ red, unsigned* cnt) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  double* u = reinterpret_cast<double*>(sm_raw);
+  __shared__ double scratch[32];
+  for (int j = threadIdx.x; j < rin; j += blockDim.x) u[j] = ured[j];
+  __syncthreads();
+  int r0, r1;
+  block_rows(N, rb, r0, r1);
+  double a[1] = {0.0};
+  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
+    double acc = 0.0;                                             // fp64: rin can be ~1e3
+    for (int j = 0; j < rin; ++j) acc = fma((double)HM[row + (size_t)j * N], (double)u[j], acc);
+    const T gi = (T)((double)gp[row] - acc);                      // G s
+    g[row] = gi;
+    a[0] += (double)s[row] * (double)gi;
+  }
+  block_sum<1>(a, scratch);
+  double* slot = part + (size_t)blockIdx.x * W;
+  if (threadIdx.x == 0) slot[nV] = a[0];
+  block_cols_dot(V, (size_t)N, nV, g, r0, r1, slot);             // c = V^T G s
+  if (arrive_last(cnt)) {
+    finalize_sum(gridDim.x, W, nV + 1, part, red);
+    if (threadIdx.x == 0) *cnt = 0u;
+  }
+}
+
+// ------------------------------------------------------------------ stage C
+// d = sin - V c ; Gd = gin - Z c  (line 11; Z = G V so G d needs no second matvec, R18).
+// pass == 1 (first pass of CGS2, R19): also c2 = V^T Gd -> red[0..nV).
+// pass == 0 (final pass): eta = s^T Gd (line 12) and the accept / reject decision (R2).
+// sin/gin may alias d/Gd (second pass runs in place), hence no __restrict__ on them.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+stageC_kernel(int N, int rb, const T* __restrict__ V, const T* __restrict__ Z, int nV, const double* __restrict__ cred,
+              const T* sin, const T* gin, T* d, T* Gd, const T* __restrict__ s_eta, const double* __restrict__ ared,
+              int rin, const double* __restrict__ sgs, double* __restrict__ part, int W, double* __restrict__ red,
+              unsigned* cnt, IterCtl* ctl, double eps, int iter, int pass) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  double* c = reinterpret_cast<double*>(sm_raw);
+  __shared__ double scratch[32];
+  for (int j = threadIdx.x; j < nV; j += blockDim.x) c[j] = cred[j];
+  __syncthreads();
+  int r0, r1;
+  block_rows(N, rb, r0, r1);
+  double a[1] = {0.0};
+  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
+    double dv = (double)sin[row], gd = (double)gin[row];
+    for (int j = 0; j < nV; ++j) {
+      const double cj = c[j];
+      dv = fma(-(double)V[row + (size_t)j * N], cj, dv);         // d = (I - V V^T G) s   (line 11)
+      gd = fma(-(double)Z[row + (size_t)j * N], cj, gd);         // G d = G s - Z c
+    }
+    d[row] = (T)dv;
+    Gd[row] = (T)gd;
+    a[0] += (double)s_eta[row] * gd;                              // eta = s^T G d        (line 12)
+  }
+  if (pass == 1) {
+    __syncthreads();                                              // Gd of this block's rows visible
+    block_cols_dot(V, (size_t)N, nV, Gd, r0, r1, part + (size_t)blockIdx.x * W);   // c2 = V^T G d
+    if (arrive_last(cnt)) {
+      finalize_sum(gridDim.x, W, nV, part, red);
+      if (threadIdx.x == 0) *cnt = 0u;
+    }
+    return;
+  }
+  block_sum<1>(a, scratch);
+  if (threadIdx.x == 0) part[(size_t)blockIdx.x * W] = a[0];
+  if (arrive_last(cnt)) {
+    if (threadIdx.x == 0) {
+      double eta = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) eta += __ldcg(part + (size_t)b * W);
+      const double alpha = ared[rin];
+      const double sGs = *sgs;
+      const double floor_ = 64.0 * eps * fabs(sGs);
+      const bool accept = eta > floor_ && isfinite(eta);
+      ctl->eta = eta;
+      ctl->alpha = alpha;
+      ctl->gamma = accept ? alpha / eta : 0.0;
+      ctl->inv_sqrt_eta = accept ? 1.0 / sqrt(eta) : 0.0;
+      if (iter == 1) ctl->res0_sq = ared[rin + 2];
+      if (accept) {
+        ctl->n_acc += 1;
+        ctl->eta_min = fmin(ctl->eta_min, eta);
+      } else {
+        ctl->rejected += 1;
+      }
+      if (!isfinite(eta) || !isfinite(alpha)) ctl->nonfinite = 1;
+      *cnt = 0u;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ stage D
+template <typename T>
+__global__ void stageD_kernel(int N, int iter, int niter, const IterCtl* __restrict__ ctl, const T* __restrict__ d,
+                              const T* __restrict__ Gd, T* __restrict__ XV, T* __restrict__ Z, T* __restrict__ r,
+                              T* __restrict__ s, V4<T>* __restrict__ xcs, int policy, const int* __restrict__ order,
+                              uint64_t seed, int k) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= N) return;
+  const T gamma = (T)ctl->gamma, isq = (T)ctl->inv_sqrt_eta;
+  const T di = d[row], gdi = Gd[row];
+  XV[row] = fma(gamma, di, XV[row]);                              // v += alpha/eta d   (line 13)
+  XV[row + (size_t)iter * N] = di * isq;                          // V_i = d / sqrt(eta) (line 14)
+  Z[row + (size_t)(iter - 1) * N] = gdi * isq;
+  const T rn = fma(-gamma, gdi, r[row]);                          // r^(i+1) = r^(i) - alpha/eta G d
+  r[row] = rn;
+  if (iter < niter) {
+    T sn;
+    if (policy == 0) sn = rn;
+    else if (policy == 1) sn = (order[iter] == row) ? T(1) : T(0);
+    else sn = (T)philox_normal(seed, (uint32_t)k, (uint32_t)(iter + 1), (uint32_t)row);
+    s[row] = sn;
+    xcs[row].w = sn;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+dot_final_kernel(int N, int rb, const T* __restrict__ a_, const T* __restrict__ b_, double* part, double* out,
+                 unsigned* cnt) {
+  __shared__ double scratch[32];
+  int r0, r1;
+  block_rows(N, rb, r0, r1);
+  double a[1] = {0.0};
+  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) a[0] += (double)a_[row] * (double)b_[row];
+  block_sum<1>(a, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = a[0];
+  if (arrive_last(cnt)) {
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(part + b);
+      *out = t;
+      *cnt = 0u;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ gathers / mixing
+// HM[row + j*N] = M[idx[row] + j*ldm]   (rows of block 0 picked by H)
+template <typename T>
+__global__ void gather_rows_kernel(int N, int C, const int* __restrict__ idx, const T* __restrict__ M, size_t ldm,
+                                   T* __restrict__ out, size_t ldo) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N * C) return;
+  const int row = (int)(e % N), j = (int)(e / N);
+  out[row + (size_t)j * ldo] = M[idx[row] + (size_t)j * ldm];
+}
+
+// out = (A (x) I) in  or (A^T (x) I) in, column by column (Lemma B.1 structure)
+template <typename T>
+__global__ void mix_kernel(int NX, int Dp, int C, Mat3 A, int transpose, const T* __restrict__ in, size_t ldi,
+                           T* __restrict__ out, size_t ldo) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)NX * C) return;
+  const int q = (int)(e % NX), j = (int)(e / NX);
+  double x[3] = {0.0, 0.0, 0.0};
+  for (int t = 0; t < Dp; ++t) x[t] = (double)in[q + (size_t)t * NX + (size_t)j * ldi];
+  for (int dd = 0; dd < Dp; ++dd) {
+    double acc = 0.0;
+    for (int t = 0; t < Dp; ++t) acc += (transpose ? A.a[t][dd] : A.a[dd][t]) * x[t];
+    out[q + (size_t)dd * NX + (size_t)j * ldo] = (T)acc;
+  }
+}
+
+// post-loop: out[p, j] = Sigma^t_{d,0} Y[q, j] - tmp[p, j]  (p = d*NX + q)
+template <typename T>
+__global__ void post_combine_kernel(int NX, int Dp, int C, Mat3 S, const T* __restrict__ Y, const T* __restrict__ tmp,
+                                    const T* __restrict__ mpred, T* __restrict__ m, T* __restrict__ Mk, int rin) {
+  const size_t D = (size_t)NX * Dp;
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= D * C) return;
+  const size_t p = e % D;
+  const int j = (int)(e / D);
+  const int dd = (int)(p / NX), q = (int)(p % NX);
+  T val = (T)S.a[dd][0] * Y[q + (size_t)j * NX];
+  if (tmp) val -= tmp[p + (size_t)j * D];
+  if (j == 0) m[p] = mpred[p] + val;                              // m = m^- + P^- w
+  else Mk[p + (size_t)(rin + j - 1) * D] = val;                   // B = P^- W
+}
+
+// var[p] = base[p] - sum_c M[p + c*ld]^2 ; base = Sigma^t_{dd} when base_vec == nullptr
+template <typename T>
+__global__ void rowvar_kernel(int NX, int Dp, Mat3 S, const T* __restrict__ base_vec, const T* __restrict__ M,
+                              size_t ld, int cols, T* __restrict__ var) {
+  const size_t D = (size_t)NX * Dp;
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= D) return;
+  double acc = 0.0;
+  for (int c = 0; c < cols; ++c) {
+    const double x = (double)M[p + (size_t)c * ld];
+    acc += x * x;
+  }
+  const double base = base_vec ? (double)base_vec[p] : S.a[p / NX][p / NX];
+  var[p] = (T)(base - acc);
+}
+
+// ------------------------------------------------------------------ Gram (fp64 accumulation)
+// part[z][a + b*c] = sum_{rows in split z} M[row, a] M[row, b], 32x32 tiles, upper tiles only
+template <typename T>
+__global__ void __launch_bounds__(256)
+gram_partial_kernel(size_t D, int c, const T* __restrict__ M, size_t ld, size_t rows_per_split, double* __restrict__ part) {
+  const int ti = blockIdx.x, tj = blockIdx.y;
+  if (tj < ti) return;
+  __shared__ double As[32][33];
+  __shared__ double Bs[32][33];
+  const size_t row_lo = (size_t)blockIdx.z * rows_per_split;
+  const size_t row_hi = min(D, row_lo + rows_per_split);
+  const int a0 = ti * 32, b0 = tj * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // ty in [0, 8)
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (size_t r = row_lo; r < row_hi; r += 32) {
+    for (int q = ty; q < 32; q += 8) {
+      const size_t row = r + tx;
+      const int ca = a0 + q, cb = b0 + q;
+      As[q][tx] = (row < row_hi && ca < c) ? (double)M[row + (size_t)ca * ld] : 0.0;
+      Bs[q][tx] = (row < row_hi && cb < c) ? (double)M[row + (size_t)cb * ld] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const double b = Bs[tx][rr];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][rr], b, acc[q]);
+    }
+    __syncthreads();
+  }
+  double* out = part + (size_t)blockIdx.z * c * c;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int a = a0 + ty + 8 * q, b = b0 + tx;
+    if (a < c && b < c) out[a + (size_t)b * c] = acc[q];
+  }
+}
+
+__global__ void gram_reduce_kernel(int c, int nsplit, const double* __restrict__ part, double* __restrict__ G) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)c * c) return;
+  const int a = (int)(e % c), b = (int)(e / c);
+  const int lo = min(a, b), hi = max(a, b);
+  const int tlo = lo / 32, thi = hi / 32;
+  // element (lo, hi) lives in tile (tlo, thi) which is an upper tile (tlo <= thi)
+  double s = 0.0;
+  if (tlo <= thi) {
+    for (int z = 0; z < nsplit; ++z) s += part[(size_t)z * c * c + lo + (size_t)hi * c];
+  }
+  G[e] = s;
+}
+
+// Qr[a + j*c] = evec[a + (c-1-j)*c]  (descending eigenvalue order), kept[j] = w[c-1-j]
+template <typename T>
+__global__ void take_top_kernel(int c, int r, const double* __restrict__ evec, const double* __restrict__ w,
+                                T* __restrict__ Qr, double* __restrict__ kept, double* dropped_mass) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < (size_t)c * r) {
+    const int a = (int)(e % c), j = (int)(e / c);
+    Qr[a + (size_t)j * c] = (T)evec[a + (size_t)(c - 1 - j) * c];
+  }
+  if (e < (size_t)r && kept) kept[e] = w[c - 1 - e];
+  if (e == 0 && dropped_mass) {
+    double s = 0.0;
+    for (int i = 0; i < c - r; ++i) s += w[i];
+    *dropped_mass = s;
+  }
+}
+
+// ------------------------------------------------------------------ smoother helpers
+// Sigma_k x: y[d*NX + q, j] = sum_e S[d][e] Y[q, j*Dp + e]
+template <typename T>
+__global__ void sigma_apply_kernel(int NX, int Dp, int C, Mat3 S, const T* __restrict__ Y, T* __restrict__ y) {
+  const size_t D = (size_t)NX * Dp;
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= D * C) return;
+  const size_t p = e % D;
+  const int j = (int)(e / D);
+  const int dd = (int)(p / NX), q = (int)(p % NX);
+  double acc = 0.0;
+  for (int t = 0; t < Dp; ++t) acc += S.a[dd][t] * (double)Y[q + (size_t)(j * Dp + t) * NX];
+  y[e] = (T)acc;
+}
+
+// smoother state: ms = m + y[:,0]; var = var_f - rowsumsq(y[:, 1:C])
+template <typename T>
+__global__ void smooth_out_kernel(size_t D, int C, const T* __restrict__ m, const T* __restrict__ varf,
+                                  const T* __restrict__ y, T* __restrict__ ms, T* __restrict__ vs) {
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= D) return;
+  ms[p] = m[p] + y[p];
+  double acc = 0.0;
+  for (int j = 1; j < C; ++j) {
+    const double x = (double)y[p + (size_t)j * D];
+    acc += x * x;
+  }
+  vs[p] = (T)((double)varf[p] - acc);
+}
+
+// W^s_full = [H^T V, x[:,1:] - H^T R[:,1:]],  w^s = H^T v + x[:,0] - H^T R[:,0]
+// step 1: dense part (copy x columns, zero the H^T V block)
+template <typename T>
+__global__ void ws_dense_kernel(size_t D, int n, int q, const T* __restrict__ X, T* __restrict__ Wf, T* __restrict__ ws) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t total = D * (size_t)(n + q + 1);
+  if (e >= total) return;
+  const size_t p = e % D;
+  const int j = (int)(e / D);
+  if (j == 0) ws[p] = X[p];
+  else if (j <= n) Wf[p + (size_t)(j - 1) * D] = T(0);
+  else Wf[p + (size_t)(j - 1) * D] = X[p + (size_t)(j - n) * D];
+}
+// step 2: scatter the observation-space terms into the train rows of block 0
+template <typename T>
+__global__ void ws_scatter_kernel(int N, size_t D, int n, int q, const int* __restrict__ idx, const T* __restrict__ XV,
+                                  const T* __restrict__ R, T* __restrict__ Wf, T* __restrict__ ws) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t total = (size_t)N * (n + q + 1);
+  if (e >= total) return;
+  const int row = (int)(e % N), j = (int)(e / N);
+  const size_t p = idx[row];
+  if (j == 0) ws[p] += XV[row] - R[row];                          // H^T v - H^T V t_0
+  else if (j <= n) Wf[p + (size_t)(j - 1) * D] = XV[row + (size_t)j * N];   // H^T V
+  else Wf[p + (size_t)(j - 1) * D] -= R[row + (size_t)(j - n) * N];         // - H^T V t_{1:}
+}
+
+template <typename S, typename D_>
+__global__ void convert_kernel(int rows, int cols, const S* __restrict__ src, size_t lds, D_* __restrict__ dst, size_t ldd) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)rows * cols) return;
+  const int i = (int)(e % rows), j = (int)(e / rows);
+  dst[i + (size_t)j * ldd] = (D_)src[i + (size_t)j * lds];
+}
+
+template <typename T>
+__global__ void fill_kernel(size_t n, T val, T* __restrict__ out) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) out[e] = val;
+}
+
+template <typename T>
+__global__ void idx64_to32_kernel(int n, const int64_t* __restrict__ in, int* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) out[e] = (int)in[e];
+}
+
+inline unsigned nblk(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+int rows_per_block(int N) {
+  int rb = (N + 295) / 296;
+  rb = ((rb + 31) / 32) * 32;
+  return rb < 32 ? 32 : rb;
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::prep(int N, const int* idx, const V4<T>* coords, const T* y, const T* mpred, int policy,
+                                 const int* order, uint64_t seed, int k, T* r, T* s, T* v, V4<T>* xcs, cudaStream_t st) {
+  if (N <= 0) return cudaSuccess;
+  prep_kernel<T><<<nblk(N), 256, 0, st>>>(N, idx, coords, y, mpred, policy, order, seed, k, r, s, v, xcs);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s,
+                                   const T* r, T* gp, const T* HM, int rin, double* part, int W, double* red,
+                                   unsigned* cnt, cudaStream_t st) {
+  const int rb = rows_per_block(N);
+  stageA_kernel<T><<<nblk(N, rb), kThreads, 0, st>>>(N, rb, nch, partial, sig00, lam2, s, r, gp, HM, rin, part, W,
+                                                     red, cnt);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g,
+                                   const T* V, int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st) {
+  const int rb = rows_per_block(N);
+  stageB_kernel<T><<<nblk(N, rb), kThreads, sizeof(double) * (rin > 0 ? rin : 1), st>>>(N, rb, HM, rin, ured, gp, s, g, V,
+                                                                                   nV, part, W, red, cnt);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::stageC(int N, const T* V, const T* Z, int nV, const double* cred, const T* sin,
+                                   const T* gin, T* d, T* Gd, const T* s_eta, const double* ared, int rin,
+                                   const double* sgs, double* part, int W, double* red, unsigned* cnt, IterCtl* ctl,
+                                   double eps, int iter, int pass, cudaStream_t st) {
+  const int rb = rows_per_block(N);
+  stageC_kernel<T><<<nblk(N, rb), kThreads, sizeof(double) * (nV > 0 ? nV : 1), st>>>(
+      N, rb, V, Z, nV, cred, sin, gin, d, Gd, s_eta, ared, rin, sgs, part, W, red, cnt, ctl, eps, iter, pass);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::stageD(int N, int iter, int niter, const IterCtl* ctl, const T* d, const T* Gd, T* XV,
+                                   T* Z, T* r, T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k,
+                                   cudaStream_t st) {
+  stageD_kernel<T><<<nblk(N), 256, 0, st>>>(N, iter, niter, ctl, d, Gd, XV, Z, r, s, xcs, policy, order, seed, k);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::dot(int N, const T* a, const T* b, double* part, double* out, unsigned* cnt,
+                                cudaStream_t st) {
+  const int rb = rows_per_block(N);
+  dot_final_kernel<T><<<nblk(N, rb), kThreads, 0, st>>>(N, rb, a, b, part, out, cnt);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::gather_rows(int N, int C, const int* idx, const T* M, size_t ldm, T* out, size_t ldo,
+                                        cudaStream_t st) {
+  if ((size_t)N * C == 0) return cudaSuccess;
+  gather_rows_kernel<T><<<nblk((size_t)N * C), 256, 0, st>>>(N, C, idx, M, ldm, out, ldo);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::mix(int NX, int Dp, int C, const Mat3& A, bool transpose, const T* in, size_t ldi, T* out,
+                                size_t ldo, cudaStream_t st) {
+  if ((size_t)NX * C == 0) return cudaSuccess;
+  mix_kernel<T><<<nblk((size_t)NX * C), 256, 0, st>>>(NX, Dp, C, A, transpose ? 1 : 0, in, ldi, out, ldo);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::post_combine(int NX, int Dp, int C, const Mat3& S, const T* Y, const T* tmp,
+                                         const T* mpred, T* m, T* Mk, int rin, cudaStream_t st) {
+  const size_t D = (size_t)NX * Dp;
+  post_combine_kernel<T><<<nblk(D * C), 256, 0, st>>>(NX, Dp, C, S, Y, tmp, mpred, m, Mk, rin);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::rowvar(int NX, int Dp, const Mat3& S, const T* base, const T* M, size_t ld, int cols,
+                                   T* var, cudaStream_t st) {
+  const size_t D = (size_t)NX * Dp;
+  rowvar_kernel<T><<<nblk(D), 256, 0, st>>>(NX, Dp, S, base, M, ld, cols, var);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::gram(size_t D, int c, const T* M, size_t ld, double* part, int nsplit, double* G,
+                                 cudaStream_t st) {
+  const size_t rps = (D + nsplit - 1) / nsplit;
+  const int nt = (c + 31) / 32;
+  dim3 grid(nt, nt, nsplit);
+  gram_partial_kernel<T><<<grid, 256, 0, st>>>(D, c, M, ld, rps, part);
+  cudaError_t e = note_launch_err();
+  if (e != cudaSuccess) return e;
+  gram_reduce_kernel<<<nblk((size_t)c * c), 256, 0, st>>>(c, nsplit, part, G);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::take_top(int c, int r, const double* evec, const double* w, T* Qr, double* kept,
+                                     double* dropped, cudaStream_t st) {
+  take_top_kernel<T><<<nblk((size_t)c * r > 0 ? (size_t)c * r : 1), 256, 0, st>>>(c, r, evec, w, Qr, kept, dropped);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::sigma_apply(int NX, int Dp, int C, const Mat3& S, const T* Y, T* y, cudaStream_t st) {
+  const size_t D = (size_t)NX * Dp;
+  sigma_apply_kernel<T><<<nblk(D * C), 256, 0, st>>>(NX, Dp, C, S, Y, y);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::smooth_out(size_t D, int C, const T* m, const T* varf, const T* y, T* ms, T* vs,
+                                       cudaStream_t st) {
+  smooth_out_kernel<T><<<nblk(D), 256, 0, st>>>(D, C, m, varf, y, ms, vs);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::ws_build(int N, size_t D, int n, int q, const int* idx, const T* X, const T* XV,
+                                     const T* R, T* Wf, T* ws, cudaStream_t st) {
+  ws_dense_kernel<T><<<nblk(D * (n + q + 1)), 256, 0, st>>>(D, n, q, X, Wf, ws);
+  cudaError_t e = note_launch_err();
+  if (e != cudaSuccess || N == 0) return e;
+  ws_scatter_kernel<T><<<nblk((size_t)N * (n + q + 1)), 256, 0, st>>>(N, D, n, q, idx, XV, R, Wf, ws);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::fill(size_t n, T val, T* out, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  fill_kernel<T><<<nblk(n), 256, 0, st>>>(n, val, out);
+  return note_launch_err();
+}
+
+template <typename S, typename D_>
+cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_t ldd, cudaStream_t st) {
+  if ((size_t)rows * cols == 0) return cudaSuccess;
+  convert_kernel<S, D_><<<nblk((size_t)rows * cols), 256, 0, st>>>(rows, cols, src, lds, dst, ldd);
+  return note_launch_err();
+}
+template cudaError_t convert<float, double>(int, int, const float*, size_t, double*, size_t, cudaStream_t);
+template cudaError_t convert<double, float>(int, int, const double*, size_t, float*, size_t, cudaStream_t);
+template cudaError_t convert<double, double>(int, int, const double*, size_t, double*, size_t, cudaStream_t);
+
+cudaError_t idx64_to32(int n, const int64_t* in, int* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  idx64_to32_kernel<int><<<nblk(n), 256, 0, st>>>(n, in, out);
+  return note_launch_err();
+}
+
+template struct StepKernels<float>;
+template struct StepKernels<double>;
+
+}  // namespace cakf

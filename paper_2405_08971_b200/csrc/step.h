@@ -1,0 +1,60 @@
+// step.h — launchers of the per-step streaming kernels (kernels_step.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace cakf {
+
+struct Mat3 {
+  double a[3][3];
+};
+
+// Device-resident control block of one update's inner loop.
+struct IterCtl {
+  double alpha, eta, gamma, inv_sqrt_eta;
+  double eta_min, res0_sq, res_sq, dropped;
+  int n_acc, rejected, nonfinite, pad;
+};
+
+int rows_per_block(int N);
+cudaError_t idx64_to32(int n, const int64_t* in, int* out, cudaStream_t st);
+template <typename S, typename D_>
+cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_t ldd, cudaStream_t st);
+
+template <typename T>
+struct StepKernels {
+  static cudaError_t prep(int N, const int* idx, const V4<T>* coords, const T* y, const T* mpred, int policy,
+                          const int* order, uint64_t seed, int k, T* r, T* s, T* v, V4<T>* xcs, cudaStream_t st);
+  static cudaError_t stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s, const T* r,
+                            T* gp, const T* HM, int rin, double* part, int W, double* red, unsigned* cnt,
+                            cudaStream_t st);
+  static cudaError_t stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g, const T* V,
+                            int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st);
+  static cudaError_t stageC(int N, const T* V, const T* Z, int nV, const double* cred, const T* sin, const T* gin,
+                            T* d, T* Gd, const T* s_eta, const double* ared, int rin, const double* sgs, double* part,
+                            int W, double* red, unsigned* cnt, IterCtl* ctl, double eps, int iter, int pass,
+                            cudaStream_t st);
+  static cudaError_t stageD(int N, int iter, int niter, const IterCtl* ctl, const T* d, const T* Gd, T* XV, T* Z, T* r,
+                            T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k, cudaStream_t st);
+  static cudaError_t dot(int N, const T* a, const T* b, double* part, double* out, unsigned* cnt, cudaStream_t st);
+  static cudaError_t gather_rows(int N, int C, const int* idx, const T* M, size_t ldm, T* out, size_t ldo,
+                                 cudaStream_t st);
+  static cudaError_t mix(int NX, int Dp, int C, const Mat3& A, bool transpose, const T* in, size_t ldi, T* out,
+                         size_t ldo, cudaStream_t st);
+  static cudaError_t post_combine(int NX, int Dp, int C, const Mat3& S, const T* Y, const T* tmp, const T* mpred, T* m,
+                                  T* Mk, int rin, cudaStream_t st);
+  static cudaError_t rowvar(int NX, int Dp, const Mat3& S, const T* base, const T* M, size_t ld, int cols, T* var,
+                            cudaStream_t st);
+  static cudaError_t gram(size_t D, int c, const T* M, size_t ld, double* part, int nsplit, double* G, cudaStream_t st);
+  static cudaError_t take_top(int c, int r, const double* evec, const double* w, T* Qr, double* kept, double* dropped,
+                              cudaStream_t st);
+  static cudaError_t sigma_apply(int NX, int Dp, int C, const Mat3& S, const T* Y, T* y, cudaStream_t st);
+  static cudaError_t smooth_out(size_t D, int C, const T* m, const T* varf, const T* y, T* ms, T* vs, cudaStream_t st);
+  static cudaError_t ws_build(int N, size_t D, int n, int q, const int* idx, const T* X, const T* XV, const T* R,
+                              T* Wf, T* ws, cudaStream_t st);
+  static cudaError_t fill(size_t n, T val, T* out, cudaStream_t st);
+};
+
+}  // namespace cakf

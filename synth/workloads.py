@@ -68,6 +68,7 @@ class Workload:
     coord_order: Optional[list] = None  # per step: int64 positions into obs_idx (coord policy)
     action_seed: int = 1          # Philox key for the random policy (R16)
     rtol: float = 0.0
+    reorth: bool = True           # second Gram-Schmidt pass (CGS2, reading R19)
 
     @property
     def n_space(self) -> int:
