@@ -280,7 +280,7 @@ def main():
         t = torch.tensor([ms_e2e], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
-    e2e = {"value": args.e2e_steps * wl.T * world / (ms_e2e / 1e3), "unit": "time-steps/s",
+    e2e = {"value": args.e2e_steps * wl.T * world / max(ms_e2e / 1e3, 1e-9), "unit": "time-steps/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     # ---------------- roofline of the dominant kernel (live CUDA-event timings)

@@ -203,6 +203,18 @@ struct Impl final : ImplBase {
   // smoother
   T *X = nullptr, *Yk = nullptr, *yb = nullptr, *Tm = nullptr, *Hy = nullptr, *tt = nullptr, *R = nullptr;
   T *Wf = nullptr, *Ws = nullptr, *ws = nullptr, *pvar = nullptr;
+  float* tcw = nullptr;  // tf32 hi/lo planes of the K2 right-hand sides
+
+  // K2: Y = K(xr, xc) B — tcgen05 3xTF32 for fp32, SIMT for fp64 (or CAKF_K2_SIMT=1)
+  cudaError_t k2(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y, size_t ldy) {
+    if constexpr (sizeof(T) == 4) {
+      if (use_tc_k2())
+        return launch_gram_gemm_tc(nu2, reinterpret_cast<const float4*>(xr), M, reinterpret_cast<const float4*>(xc), K,
+                                   reinterpret_cast<const float*>(B), ldb, C, reinterpret_cast<float*>(Y), ldy, 1.0,
+                                   tcw, st);
+    }
+    return launch_gram_gemm<T>(nu2, xr, M, xc, K, B, ldb, C, Y, ldy, 1.0, st);
+  }
 
   // ---------------- profiling: CUDA events around launches of one category (cakf_profile)
   bool prof_on = false;
@@ -308,7 +320,7 @@ struct Impl final : ImplBase {
     Z = carve<T>((size_t)Nmax * std::max(nhat, 1));
     HM = carve<T>((size_t)Nmax * std::max(rin_max, 1));
     const int nch = matvec_chunks((int)Nmax, (int)Nmax, sizeof(T));
-    partial_cap = (size_t)std::max<int64_t>(nch, 64) * Nmax;
+    partial_cap = (size_t)std::max<int64_t>({(int64_t)nch, (int64_t)64, (int64_t)matvec_sym_tiles((int)Nmax)}) * Nmax;
     partial = carve<T>(partial_cap);
     stage64 = carve<int64_t>(std::max<int64_t>(Nmax, NX));
     order32 = carve<int>(std::max(nhat, 1));
@@ -351,6 +363,11 @@ struct Impl final : ImplBase {
     Ws = carve<T>((size_t)D * (nhat + qmax));
     ws = carve<T>(D);
     pvar = carve<T>(D);
+    if (sizeof(T) == 4) {
+      const size_t wb = std::max(gram_gemm_tc_workspace((int)Nmax, 1 + nhat),
+                                 gram_gemm_tc_workspace((int)NX, Dp * (1 + qmax)));
+      tcw = carve<float>(wb / sizeof(float) + 64);
+    }
   }
 
   int init(const cakf_config& c) override {
@@ -506,12 +523,19 @@ struct Impl final : ImplBase {
     CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, S.m_pred, policy, order32, seed, k, r, s, S.XV, xcs, st));
     const double sig00 = S.sig_t.a[0][0];
     const double eps = sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON;
-    const int nch = std::max(1, std::min<int>(matvec_chunks(N, N, sizeof(T)), (int)(partial_cap / N)));
+    const bool sym = sizeof(T) == 4 && use_sym_k1();
+    const int nch = sym ? matvec_sym_tiles(N)
+                        : std::max(1, std::min<int>(matvec_chunks(N, N, sizeof(T)), (int)(partial_cap / N)));
     T* V = S.XV + N;
     for (int i = 1; i <= niter; ++i) {
       // G s  (matrix-free: kernel rows on the fly + low-rank downdate + noise)
       size_t pk = prof_begin();
-      CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
+      if constexpr (sizeof(T) == 4) {
+        if (sym) CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial), st));
+        else CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
+      } else {
+        CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
+      }
       prof_end(CAKF_PROF_K1, pk);
       pk = prof_begin();
       CK_CUDA(StepKernels<T>::stageA(N, nch, partial, sig00, lam2, s, r, gp, HM, rin, part, W, redA, cnt + 0, st));
@@ -532,7 +556,7 @@ struct Impl final : ImplBase {
     // ---- post-loop: [P^- w, P^- W] = Sigma H^T [v V] - M^- (H M^-)^T [v V]
     const int Cc = 1 + niter;
     size_t pk = prof_begin();
-    CK_CUDA(launch_gram_gemm<T>(nu2, coords, (int)NX, xcs, N, S.XV, N, Cc, Yb, NX, 1.0, st));
+    CK_CUDA(k2(coords, (int)NX, xcs, N, S.XV, N, Cc, Yb, NX));
     prof_end(CAKF_PROF_K2_POST, pk);
     if (rin) {
       pk = prof_begin();
@@ -634,7 +658,7 @@ struct Impl final : ImplBase {
       if (q) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, q, S.A_next, true, Ws, D, X + D, D, st));
       // Sigma_k x = (Sigma^t_k (x) K) x : K applied to all D' blocks of all C columns at once
       size_t pk = prof_begin();
-      CK_CUDA(launch_gram_gemm<T>(nu2, coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX, 1.0, st));
+      CK_CUDA(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX));
       prof_end(CAKF_PROF_K2_SMOOTH, pk);
       CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, C, S.sig_t, Yk, yb, st));
       const int rin = S.rin, n = S.n, N = S.N;
@@ -919,8 +943,22 @@ int cakf_gram_matmul(int32_t dtype, int32_t spatial_kernel, double ell, int32_t 
       if (e == cudaSuccess) e = launch_matvec_partial<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, nch, part, st);
       if (e == cudaSuccess) e = launch_sum_partials<T>((int)n_rows, nch, part, alpha, (T*)Y, st);
     } else if (e == cudaSuccess) {
-      e = launch_gram_gemm<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, (const T*)X, (size_t)n_cols, n_rhs,
-                              (T*)Y, (size_t)n_rows, alpha, st);
+      if constexpr (sizeof(T) == 4) {
+        if (use_tc_k2()) {
+          float* w = nullptr;
+          e = cudaMallocAsync(&w, gram_gemm_tc_workspace((int)n_cols, n_rhs), st);
+          if (e == cudaSuccess)
+            e = launch_gram_gemm_tc(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, (const float*)X, (size_t)n_cols,
+                                    n_rhs, (float*)Y, (size_t)n_rows, alpha, w, st);
+          if (w) cudaFreeAsync(w, st);
+        } else {
+          e = launch_gram_gemm<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, (const T*)X, (size_t)n_cols, n_rhs,
+                                  (T*)Y, (size_t)n_rows, alpha, st);
+        }
+      } else {
+        e = launch_gram_gemm<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, (const T*)X, (size_t)n_cols, n_rhs,
+                                (T*)Y, (size_t)n_rows, alpha, st);
+      }
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFreeAsync(dxyz, st);

@@ -14,6 +14,10 @@ cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<
                                   int nchunks, T* partial, cudaStream_t st);
 // choose the number of column chunks for a matvec of this shape (fills the GPU in whole waves)
 int matvec_chunks(int nrows, int ncols, int elem_bytes);
+// symmetric K1 (fp32, one RHS with rows == cols): partial[c][i] for c < matvec_sym_tiles(n)
+int matvec_sym_tiles(int n);
+cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, cudaStream_t st);
+bool use_sym_k1();  // false if CAKF_K1_DENSE=1
 // reduce partials: y[i] = alpha * sum_ch partial[ch][i]
 template <typename T>
 cudaError_t launch_sum_partials(int nrows, int nchunks, const T* partial, double alpha, T* y, cudaStream_t st);
@@ -22,6 +26,13 @@ cudaError_t launch_sum_partials(int nrows, int nchunks, const T* partial, double
 template <typename T>
 cudaError_t launch_gram_gemm(int nu2, const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb,
                              int C, T* Y, size_t ldy, double alpha, cudaStream_t st);
+
+// ---- K2 on tcgen05 tensor cores (fp32 via 3xTF32): workspace = gram_gemm_tc_workspace(K, C) bytes
+size_t gram_gemm_tc_workspace(int K, int C);
+cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* xc, int K, const float* B, size_t ldb,
+                                int C, float* Y, size_t ldy, double alpha, float* work, cudaStream_t st);
+// true unless CAKF_K2_SIMT=1 is set in the environment
+bool use_tc_k2();
 
 // ---- coordinates
 template <typename T>

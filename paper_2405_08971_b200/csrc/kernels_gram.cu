@@ -8,6 +8,7 @@
 //   K2  many right-hand sides (post-loop a7, smoother a9): a GEMM whose A operand
 //       is generated on the fly; SIMT register-tiled version (8x8 per thread).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -67,6 +68,88 @@ matvec_partial_kernel(const V4<T>* __restrict__ xr, int nrows, const V4<T>* __re
   for (int k = 0; k < R; ++k) {
     const int row = base + k * kMvThreads;
     if (row < nrows) partial[(size_t)ch * nrows + row] = acc[k];
+  }
+}
+
+// ------------------------------------------------------------------ K1, symmetric (fp32)
+// K_TT is symmetric: each unordered pair of 128-point tiles (I <= J) is evaluated once.
+// The 16 x 16 threads own 8 x 8 micro-tiles; row sums go to tile I, column sums to tile J:
+//   partial[J][i in I] = sum_{j in J} k_ij s_j      partial[I][j in J] = sum_{i in I} k_ij s_i
+// so row r of tile t receives exactly one partial per tile c (c = 0..nt-1) and stage A's
+// fixed-order sum over c reduces it (deterministic, no atomics).
+constexpr int SYM_T = 128;
+template <int NU2>
+__global__ void __launch_bounds__(256)
+matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, long long npairs, float* __restrict__ partial) {
+  __shared__ float4 si[SYM_T], sj[SYM_T];
+  __shared__ float colred[16][SYM_T + 4];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (long long p = blockIdx.x; p < npairs; p += gridDim.x) {
+    // p -> (I, J), I <= J, row-major over the upper triangle
+    const double b = 2.0 * nt + 1.0;
+    int I = (int)floor((b - sqrt(b * b - 8.0 * (double)p)) * 0.5);
+    while ((long long)I * nt - (long long)I * (I - 1) / 2 > p) --I;
+    while ((long long)(I + 1) * nt - (long long)(I + 1) * I / 2 <= p) ++I;
+    const int J = I + (int)(p - ((long long)I * nt - (long long)I * (I - 1) / 2));
+    __syncthreads();
+    if (tid < SYM_T) {
+      const int gi = I * SYM_T + tid;
+      float4 v = gi < n ? x[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+      si[tid] = v;
+    } else {
+      const int gj = J * SYM_T + tid - SYM_T;
+      float4 v = gj < n ? x[gj] : make_float4(0.f, 0.f, 0.f, 0.f);
+      sj[tid - SYM_T] = v;
+    }
+    __syncthreads();
+    float rx[8], ry[8], rz[8], rs[8], cx[8], cy[8], cz[8], cs[8], racc[8], cacc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 a = si[ty * 8 + q];
+      rx[q] = a.x; ry[q] = a.y; rz[q] = a.z; rs[q] = a.w; racc[q] = 0.f;
+      const float4 c = sj[tx * 8 + q];
+      cx[q] = c.x; cy[q] = c.y; cz[q] = c.z; cs[q] = c.w; cacc[q] = 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float dx = rx[r] - cx[c], dy = ry[r] - cy[c], dz = rz[r] - cz[c];
+        const float k = matern_from_d2<NU2>(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+        racc[r] = fmaf(k, cs[c], racc[r]);
+        cacc[c] = fmaf(k, rs[r], cacc[c]);
+      }
+    }
+    // row sums: reduce over tx (16 lanes of a half-warp)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      float v = racc[r];
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      racc[r] = v;
+    }
+    if (tx == 0) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int gi = I * SYM_T + ty * 8 + r;
+        if (gi < n) partial[(size_t)J * n + gi] = racc[r];
+      }
+    }
+    if (I != J) {
+      // column sums: reduce over ty through shared memory
+#pragma unroll
+      for (int c = 0; c < 8; ++c) colred[ty][tx * 8 + c] = cacc[c];
+      __syncthreads();
+      if (tid < SYM_T) {
+        float v = 0.f;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) v += colred[t][tid];
+        const int gj = J * SYM_T + tid;
+        if (gj < n) partial[(size_t)I * n + gj] = v;
+      }
+    }
   }
 }
 
@@ -214,6 +297,31 @@ cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<
     case 5: return matvec_partial_nu<T, 5>(xr, nrows, xc, ncols, nchunks, partial, st);
   }
   return cudaErrorInvalidValue;
+}
+
+int matvec_sym_tiles(int n) { return (n + SYM_T - 1) / SYM_T; }
+
+bool use_sym_k1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAKF_K1_DENSE");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int nt = matvec_sym_tiles(n);
+  const long long npairs = (long long)nt * (nt + 1) / 2;
+  const long long grid = std::min<long long>(npairs, (long long)num_sms() * 8);
+  switch (nu2) {
+    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, 0, st>>>(x, n, nt, npairs, partial); break;
+    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, 0, st>>>(x, n, nt, npairs, partial); break;
+    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, 0, st>>>(x, n, nt, npairs, partial); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return note_launch_err();
 }
 
 template <typename T>

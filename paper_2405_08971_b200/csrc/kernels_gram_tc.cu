@@ -1,0 +1,353 @@
+// kernels_gram_tc.cu — K2 on the 5th-generation tensor cores (tcgen05, sm_100a).
+//
+//   Y[i, c] = alpha * sum_j k(x_i, x_j) B[j, c]        (the "Gramian x matrix" of P:644-647)
+//
+// The smoother's Sigma_k x (N_X x N_X x 2(r+1)) and the post-loop
+// Sigma_k H^T [v V] (a7) are dense contractions whose A operand (kernel values) is
+// generated on the fly.  fp32 accuracy from bf16 tensor cores ("3 x BF16"):
+//   every fp32 value is split EXACTLY into three bf16 pieces by bit masking,
+//   a = a1 + a2 + a3 (8 + 8 + 8 significand bits), and the product is accumulated as
+//   a1b1 + a1b2 + a2b1 + a2b2 + a1b3 + a3b1 (dropped terms ~2^-24 relative) in fp32 TMEM.
+// Six kind::f16 MMAs cost the same tensor time as three kind::tf32 MMAs, and the B planes
+// take 6 bytes per element instead of 8.
+//
+// Per CTA: a 128-row x N_TILE (<= 256) output tile in TMEM.  Per K-block of 32:
+//   * 256 threads evaluate the 128 x 32 Matérn block (FP32 pipe + MUFU), split it and store
+//     the three planes in the K-major SWIZZLE_64B canonical layout;
+//   * the three B planes (precomputed, K-major) arrive by cp.async two blocks ahead;
+//   * one thread issues 2 k-steps x 6 tcgen05.mma.kind::f16 and commits to the stage mbarrier;
+//   * three stages: generation of block kb overlaps the MMAs of kb-1 and the loads of kb+2.
+// Epilogue: tcgen05.ld (32x32b) -> registers -> coalesced column-major stores.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdlib>
+
+#include "internal.h"
+
+namespace cakf {
+
+namespace {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 32;                        // 32 bf16 = one 64-byte swizzle atom row
+constexpr int TC_THREADS = 256;
+constexpr int TC_MAXN = 256;
+constexpr int TC_STAGES = 3;
+constexpr int A_PLANE = TC_BM * TC_BK * 2;       // 8 KB
+constexpr int B_PLANE = TC_MAXN * TC_BK * 2;     // 16 KB
+constexpr int STAGE_BYTES = 3 * A_PLANE + 3 * B_PLANE;   // 72 KB
+constexpr int TC_SMEM = TC_STAGES * STAGE_BYTES + 1024 + 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// exact 3-way bf16 split by truncation: returns the three bf16 bit patterns (low 16 bits)
+__device__ __forceinline__ void split3(float a, uint32_t& p1, uint32_t& p2, uint32_t& p3) {
+  const uint32_t u = __float_as_uint(a);
+  const uint32_t h1 = u & 0xFFFF0000u;
+  const float r1 = a - __uint_as_float(h1);
+  const uint32_t h2 = __float_as_uint(r1) & 0xFFFF0000u;
+  const float r2 = r1 - __uint_as_float(h2);
+  p1 = h1 >> 16;
+  p2 = h2 >> 16;
+  p3 = __float_as_uint(r2) >> 16;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// Shared-memory matrix descriptor: K-major, SWIZZLE_64B, 8-row groups 512 B apart (sm_100 version 1).
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);        // start address  [0, 14)
+  d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;               // SBO = 512 B
+  d |= (uint64_t)1 << 46;                        // version = 1
+  d |= (uint64_t)4 << 61;                        // layout = SWIZZLE_64B
+  return d;
+}
+
+// Instruction descriptor: kind::f16, D = f32, A = B = bf16, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+// byte offset of 16-byte chunk c (0..3) of row r in a K-major SWIZZLE_64B tile
+__device__ __forceinline__ uint32_t sw64_off(int r, int c) {
+  return (uint32_t)((r >> 3) * 512 + (r & 7) * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+}
+
+template <int NU2>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const float4* __restrict__ xc, int K,
+                    const uint16_t* __restrict__ Bp, size_t ldp, size_t plane, int C, int ntile,
+                    float* __restrict__ Y, size_t ldy, float alpha) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char* sbase = smem_raw + (base - raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + TC_STAGES * STAGE_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + TC_STAGES * STAGE_BYTES + 64);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.x * TC_BM, n0 = blockIdx.y * ntile;
+  // two accumulators: D_big = sum a1 b1 (the exact leading products) and D_small = the five
+  // correction products; summed in fp32 round-to-nearest in the epilogue (tensor-core
+  // accumulation truncates, so keeping the small terms apart cuts the biased error ~6x)
+  const uint32_t acc_cols = ntile <= 32 ? 32 : ntile <= 64 ? 64 : ntile <= 128 ? 128 : 256;
+  const uint32_t tmem_cols = 2 * acc_cols;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < TC_STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  const int arow = tid & (TC_BM - 1), khalf = tid >> 7;
+  float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (m0 + arow < M) xa = xr[m0 + arow];
+  const uint32_t idesc = idesc_bf16(TC_BM, ntile);
+  const int nk = (K + TC_BK - 1) / TC_BK;
+  const int nchunks = ntile * 4;                   // 16-byte chunks per B plane per K-block
+
+  auto stage_addr = [&](int s) { return smem_u32(sbase + s * STAGE_BYTES); };
+  auto load_b = [&](int kb) {
+    const int s = kb % TC_STAGES;
+    const uint32_t b0 = stage_addr(s) + 3 * A_PLANE;
+    const int k0 = kb * TC_BK;
+    for (int e = tid; e < 3 * nchunks; e += TC_THREADS) {
+      const int pl = e / nchunks;
+      const int rem = e - pl * nchunks;
+      const int n = rem >> 2, c = rem & 3;
+      const bool ok = (n0 + n) < C;
+      const uint16_t* src = Bp + pl * plane + (size_t)(ok ? n0 + n : 0) * ldp + k0 + 8 * c;
+      cp_async16(b0 + pl * B_PLANE + sw64_off(n, c), src, ok ? 16u : 0u);
+    }
+  };
+
+  // prologue: B for blocks 0 and 1
+  if (nk > 0) load_b(0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  if (nk > 1) load_b(1);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+
+  for (int kb = 0; kb < nk; ++kb) {
+    const int s = kb % TC_STAGES;
+    const uint32_t a0 = stage_addr(s);
+    // ---- A planes: Matérn values of row arow, columns k0 + 16*khalf + [0, 16)
+    {
+      const int k0 = kb * TC_BK + 16 * khalf;
+      uint32_t p1[8], p2[8], p3[8];   // bf16x2 packed
+#pragma unroll
+      for (int q = 0; q < 16; q += 2) {
+        float kv[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int j = k0 + q + t;
+          float v = 0.f;
+          if (j < K) {
+            const float4 c = __ldg(&xc[j]);
+            const float dx = xa.x - c.x, dy = xa.y - c.y, dz = xa.z - c.z;
+            v = matern_from_d2<NU2>(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+          }
+          kv[t] = v;
+        }
+        uint32_t a1, a2, a3, b1, b2, b3;
+        split3(kv[0], a1, a2, a3);
+        split3(kv[1], b1, b2, b3);
+        p1[q >> 1] = a1 | (b1 << 16);
+        p2[q >> 1] = a2 | (b2 << 16);
+        p3[q >> 1] = a3 | (b3 << 16);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t off = sw64_off(arow, 2 * khalf + h);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0 + off), "r"(p1[4 * h]), "r"(p1[4 * h + 1]),
+                     "r"(p1[4 * h + 2]), "r"(p1[4 * h + 3])
+                     : "memory");
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0 + A_PLANE + off), "r"(p2[4 * h]),
+                     "r"(p2[4 * h + 1]), "r"(p2[4 * h + 2]), "r"(p2[4 * h + 3])
+                     : "memory");
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0 + 2 * A_PLANE + off), "r"(p3[4 * h]),
+                     "r"(p3[4 * h + 1]), "r"(p3[4 * h + 2]), "r"(p3[4 * h + 3])
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.wait_group 1;" ::: "memory");          // B(kb) landed (B(kb+1) may be in flight)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t bb = a0 + 3 * A_PLANE;
+#pragma unroll
+      for (int j = 0; j < TC_BK / 16; ++j) {
+        const uint64_t A1 = sdesc_sw64(a0 + 32 * j), A2 = sdesc_sw64(a0 + A_PLANE + 32 * j),
+                       A3 = sdesc_sw64(a0 + 2 * A_PLANE + 32 * j);
+        const uint64_t B1 = sdesc_sw64(bb + 32 * j), B2 = sdesc_sw64(bb + B_PLANE + 32 * j),
+                       B3 = sdesc_sw64(bb + 2 * B_PLANE + 32 * j);
+        const uint32_t first = (kb | j) ? 1u : 0u;
+        mma_bf16(tmem, A1, B1, idesc, first);
+        mma_bf16(tmem + acc_cols, A1, B2, idesc, first);
+        mma_bf16(tmem + acc_cols, A2, B1, idesc, 1u);
+        mma_bf16(tmem + acc_cols, A2, B2, idesc, 1u);
+        mma_bf16(tmem + acc_cols, A1, B3, idesc, 1u);
+        mma_bf16(tmem + acc_cols, A3, B1, idesc, 1u);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&bars[s]))
+                   : "memory");
+    }
+    // B(kb+2) goes into the stage MMA(kb-1) used: wait for it (it precedes MMA(kb) on the tensor pipe)
+    if (kb + 2 < nk) {
+      if (kb >= 1) mbar_wait(smem_u32(&bars[(kb - 1) % TC_STAGES]), ((kb - 1) / TC_STAGES) & 1);
+      load_b(kb + 2);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // ---- epilogue
+  if (nk > 0) mbar_wait(smem_u32(&bars[(nk - 1) % TC_STAGES]), ((nk - 1) / TC_STAGES) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int quarter = warp & 3;
+  const int row = m0 + quarter * 32 + lane;
+  const int half_cols = ((ntile / 2) + 15) / 16 * 16;
+  const int c_begin = (warp >> 2) * half_cols;
+  const int c_end = (warp >> 2) ? ntile : half_cols;
+  for (int cb = c_begin; cb < c_end; cb += 16) {
+    uint32_t r[16], q[16];
+    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]), "=r"(q[8]),
+          "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
+        : "r"(taddr + acc_cols));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < M) {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int n = n0 + cb + t;
+        const float v = __uint_as_float(r[t]) + __uint_as_float(q[t]);
+        if (cb + t < c_end && n < C) Y[row + (size_t)n * ldy] = nk > 0 ? alpha * v : 0.f;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+  }
+}
+
+// B (K x C column-major, ldb) -> three bf16 planes, each C x Kp K-major (row n = column n of B),
+// zero-padded for k >= K.  Exact split (see split3).
+__global__ void split_bf16x3_kernel(int K, int C, int Kp, const float* __restrict__ B, size_t ldb,
+                                    uint16_t* __restrict__ planes, size_t plane) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)Kp * C) return;
+  const int k = (int)(e % Kp), n = (int)(e / Kp);
+  const float v = k < K ? B[k + (size_t)n * ldb] : 0.f;
+  uint32_t p1, p2, p3;
+  split3(v, p1, p2, p3);
+  planes[e] = (uint16_t)p1;
+  planes[plane + e] = (uint16_t)p2;
+  planes[2 * plane + e] = (uint16_t)p3;
+}
+
+template <int NU2>
+cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const uint16_t* planes, size_t ldp,
+                         size_t plane, int C, int ntile, float* Y, size_t ldy, float alpha, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((M + TC_BM - 1) / TC_BM, (C + ntile - 1) / ntile);
+  gram_gemm_tc_kernel<NU2><<<grid, TC_THREADS, TC_SMEM, st>>>(xr, M, xc, K, planes, ldp, plane, C, ntile, Y, ldy, alpha);
+  return note_launch_err();
+}
+
+}  // namespace
+
+bool use_tc_k2() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAKF_K2_SIMT");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+size_t gram_gemm_tc_workspace(int K, int C) {
+  const size_t Kp = ((size_t)K + TC_BK - 1) / TC_BK * TC_BK;
+  return 3 * Kp * (size_t)C * sizeof(uint16_t) + 256;
+}
+
+cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* xc, int K, const float* B, size_t ldb,
+                                int C, float* Y, size_t ldy, double alpha, float* work, cudaStream_t st) {
+  if (M <= 0 || C <= 0) return cudaSuccess;
+  const int Kp = (K + TC_BK - 1) / TC_BK * TC_BK;
+  uint16_t* planes = reinterpret_cast<uint16_t*>(work);
+  const size_t plane = (size_t)Kp * C;
+  if (plane > 0) {
+    split_bf16x3_kernel<<<(unsigned)((plane + 255) / 256), 256, 0, st>>>(K, C, Kp, B, ldb, planes, plane);
+    cudaError_t e = note_launch_err();
+    if (e != cudaSuccess) return e;
+  }
+  // N tile: fewest tiles of <= 256 columns, balanced, multiple of 16 (kind::f16, M = 128)
+  const int ntiles = (C + TC_MAXN - 1) / TC_MAXN;
+  int ntile = (C + ntiles - 1) / ntiles;
+  ntile = ((ntile + 15) / 16) * 16;
+  switch (nu2) {
+    case 1: return launch_tc_nu<1>(xr, M, xc, K, planes, Kp, plane, C, ntile, Y, ldy, (float)alpha, st);
+    case 3: return launch_tc_nu<3>(xr, M, xc, K, planes, Kp, plane, C, ntile, Y, ldy, (float)alpha, st);
+    case 5: return launch_tc_nu<5>(xr, M, xc, K, planes, Kp, plane, C, ntile, Y, ldy, (float)alpha, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace cakf

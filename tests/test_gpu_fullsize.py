@@ -1,0 +1,49 @@
+"""Full-size parity on sampled outputs: the fused kernel operators at BASELINE.json's
+cfg3 shapes (N_X = 115,680 points, N = 87,120 training points), launched exactly as the
+bench launches them, checked row by row against the oracle's chunked kernel rows."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import mfree  # noqa: E402
+from paper_2405_08971_b200 import binding  # noqa: E402
+from synth import make_workload  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return make_workload("cfg3", T=1)
+
+
+def _rel_err(got, ref, X, xr, xc, nu, ell):
+    scale = np.abs(mfree.gram_apply(xr, xc, np.abs(X), nu, ell, chunk=256))
+    return float(np.max(np.abs(got - ref) / np.maximum(scale, 1e-300)))
+
+
+@pytest.mark.parametrize("ncols", [1, 65, 1026])
+def test_gram_operator_cfg3_sampled_rows(cfg3, ncols):
+    """K1 (ncols = 1, rows x train) and K2 (post-loop 65 / smoother 1026 columns, rows x all):
+    the first 256 and last 128 rows (ragged tail) of the full-size product vs the oracle."""
+    wl = cfg3
+    rng = np.random.default_rng(ncols)
+    X_all = wl.coords
+    cols = X_all[wl.obs_idx[0]] if ncols == 1 else X_all
+    B = rng.standard_normal((len(cols), ncols))
+    dev = "cuda"
+    rows = np.concatenate([np.arange(256), np.arange(len(X_all) - 128, len(X_all))])
+    xr = torch.tensor(X_all[rows].astype(np.float32), device=dev)
+    xc = torch.tensor(cols.astype(np.float32), device=dev)
+    Bt = torch.tensor(B.astype(np.float32), device=dev)
+    Y = binding.gram_matmul(xr, xc, Bt[:, 0] if ncols == 1 else Bt, wl.nu_x, wl.ell_x)
+    Y = Y.double().cpu().numpy().reshape(len(rows), -1)
+    xr64 = X_all[rows].astype(np.float32).astype(np.float64)
+    xc64 = cols.astype(np.float32).astype(np.float64)
+    B64 = B.astype(np.float32).astype(np.float64)
+    ref = mfree.gram_apply(xr64, xc64, B64, wl.nu_x, wl.ell_x, chunk=64)
+    err = _rel_err(Y, ref, B64, xr64, xc64, wl.nu_x, wl.ell_x)
+    print("cfg3 sampled rows, ncols", ncols, "max rel err", err)
+    assert err < 2e-5

@@ -76,7 +76,7 @@ def compare(wl, dtype, tol_m, tol_v, on_device=True):
 @pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-12), (torch.float32, 2e-5)])
 @pytest.mark.parametrize("nu", [0.5, 1.5, 2.5])
 @pytest.mark.parametrize("shape", [(1, 1, 1), (333, 517, 1), (1300, 2100, 1), (777, 901, 3), (513, 1029, 65),
-                                   (300, 300, 130)])
+                                   (300, 300, 130), (1000, 2000, 257), (129, 33, 16), (260, 95, 514), (5, 7, 2)])
 def test_gram_matmul_vs_dense(dtype, tol, nu, shape):
     """K1 (n_rhs = 1) and K2 (n_rhs > 1) vs the oracle's dense Sigma^x(X, Y) @ B."""
     nr, nc, nrhs = shape
