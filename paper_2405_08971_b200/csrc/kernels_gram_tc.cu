@@ -14,7 +14,10 @@
 // Per CTA: a 128-row x N_TILE (<= 256) output tile in TMEM.  Per K-block of 32:
 //   * 256 threads evaluate the 128 x 32 Matérn block (FP32 pipe + MUFU), split it and store
 //     the three planes in the K-major SWIZZLE_64B canonical layout;
-//   * the three B planes (precomputed, K-major) arrive by cp.async two blocks ahead;
+//   * the three B planes (precomputed, K-major) and the block's column coordinates arrive by
+//     cp.async two blocks ahead;
+//   (Tried: A as the TMEM operand written with tcgen05.st ("TS" mode) — correct but 2.5x slower
+//    on B200, the stores serialise against the in-flight MMAs.)
 //   * one thread issues 2 k-steps x 6 tcgen05.mma.kind::f16 and commits to the stage mbarrier;
 //   * three stages: generation of block kb overlaps the MMAs of kb-1 and the loads of kb+2.
 // Epilogue: tcgen05.ld (32x32b) -> registers -> coalesced column-major stores.
@@ -36,7 +39,7 @@ constexpr int TC_MAXN = 256;
 constexpr int TC_STAGES = 3;
 constexpr int A_PLANE = TC_BM * TC_BK * 2;       // 8 KB
 constexpr int B_PLANE = TC_MAXN * TC_BK * 2;     // 16 KB
-constexpr int STAGE_BYTES = 3 * A_PLANE + 3 * B_PLANE;   // 72 KB
+constexpr int STAGE_BYTES = 3 * A_PLANE + 3 * B_PLANE + 1024;   // 72 KB + the K-block's column coordinates
 constexpr int TC_SMEM = TC_STAGES * STAGE_BYTES + 1024 + 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -110,7 +113,7 @@ template <int NU2>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const float4* __restrict__ xc, int K,
                     const uint16_t* __restrict__ Bp, size_t ldp, size_t plane, int C, int ntile,
-                    float* __restrict__ Y, size_t ldy, float alpha) {
+                    float* __restrict__ Y, size_t ldy, float alpha, int diag_nogen) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -153,13 +156,18 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const float4* __restri
     const int s = kb % TC_STAGES;
     const uint32_t b0 = stage_addr(s) + 3 * A_PLANE;
     const int k0 = kb * TC_BK;
-    for (int e = tid; e < 3 * nchunks; e += TC_THREADS) {
-      const int pl = e / nchunks;
-      const int rem = e - pl * nchunks;
-      const int n = rem >> 2, c = rem & 3;
-      const bool ok = (n0 + n) < C;
-      const uint16_t* src = Bp + pl * plane + (size_t)(ok ? n0 + n : 0) * ldp + k0 + 8 * c;
-      cp_async16(b0 + pl * B_PLANE + sw64_off(n, c), src, ok ? 16u : 0u);
+#pragma unroll
+    for (int pl = 0; pl < 3; ++pl) {
+      for (int e = tid; e < nchunks; e += TC_THREADS) {
+        const int n = e >> 2, c = e & 3;
+        const bool ok = (n0 + n) < C;
+        const uint16_t* src = Bp + pl * plane + (size_t)(ok ? n0 + n : 0) * ldp + k0 + 8 * c;
+        cp_async16(b0 + pl * B_PLANE + sw64_off(n, c), src, ok ? 16u : 0u);
+      }
+    }
+    if (tid < TC_BK) {   // column coordinates of this K-block (zero beyond K: B is zero there)
+      const int j = k0 + tid;
+      cp_async16(b0 + 3 * B_PLANE + 16 * tid, &xc[j < K ? j : 0], j < K ? 16u : 0u);
     }
   };
 
@@ -172,23 +180,22 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const float4* __restri
   for (int kb = 0; kb < nk; ++kb) {
     const int s = kb % TC_STAGES;
     const uint32_t a0 = stage_addr(s);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");          // B(kb) + coords(kb) landed
+    __syncthreads();
     // ---- A planes: Matérn values of row arow, columns k0 + 16*khalf + [0, 16)
     {
-      const int k0 = kb * TC_BK + 16 * khalf;
+      const float4* sxc = reinterpret_cast<const float4*>(sbase + s * STAGE_BYTES + 3 * A_PLANE + 3 * B_PLANE) +
+                          16 * khalf;
       uint32_t p1[8], p2[8], p3[8];   // bf16x2 packed
 #pragma unroll
       for (int q = 0; q < 16; q += 2) {
         float kv[2];
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-          const int j = k0 + q + t;
-          float v = 0.f;
-          if (j < K) {
-            const float4 c = __ldg(&xc[j]);
-            const float dx = xa.x - c.x, dy = xa.y - c.y, dz = xa.z - c.z;
-            v = matern_from_d2<NU2>(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
-          }
-          kv[t] = v;
+          const float4 c = sxc[q + t];
+          const float dx = xa.x - c.x, dy = xa.y - c.y, dz = xa.z - c.z;
+          const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          kv[t] = diag_nogen ? d2 : matern_from_d2<NU2>(d2);   // diag_nogen: timing experiment only
         }
         uint32_t a1, a2, a3, b1, b2, b3;
         split3(kv[0], a1, a2, a3);
@@ -211,7 +218,6 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const float4* __restri
                      : "memory");
       }
     }
-    asm volatile("cp.async.wait_group 1;" ::: "memory");          // B(kb) landed (B(kb+1) may be in flight)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> tensor core
     __syncthreads();
     if (tid == 0) {
@@ -307,7 +313,9 @@ cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const
     configured = true;
   }
   dim3 grid((M + TC_BM - 1) / TC_BM, (C + ntile - 1) / ntile);
-  gram_gemm_tc_kernel<NU2><<<grid, TC_THREADS, TC_SMEM, st>>>(xr, M, xc, K, planes, ldp, plane, C, ntile, Y, ldy, alpha);
+  static const int nogen = [] { const char* e = getenv("CAKF_TC_DIAG_NOGEN"); return (e && e[0] == '1') ? 1 : 0; }();
+  gram_gemm_tc_kernel<NU2><<<grid, TC_THREADS, TC_SMEM, st>>>(xr, M, xc, K, planes, ldp, plane, C, ntile, Y, ldy, alpha,
+                                                              nogen);
   return note_launch_err();
 }
 
