@@ -938,9 +938,18 @@ int cakf_gram_matmul(int32_t dtype, int32_t spatial_kernel, double ell, int32_t 
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       for (size_t j = 0; j < hc.size(); ++j) hc[j].w = hxv[j];
       if (e == cudaSuccess) e = cudaMemcpyAsync(cc, hc.data(), hc.size() * sizeof(V4<T>), cudaMemcpyHostToDevice, st);
-      const int nch = matvec_chunks((int)n_rows, (int)n_cols, sizeof(T));
+      // symmetric path when the row and column point sets are the same array (K_TT s of the inner loop)
+      const bool sym = sizeof(T) == 4 && xr == xc && n_rows == n_cols && use_sym_k1();
+      const int nch = sym ? matvec_sym_tiles((int)n_rows) : matvec_chunks((int)n_rows, (int)n_cols, sizeof(T));
       if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)nch * n_rows * sizeof(T), st);
-      if (e == cudaSuccess) e = launch_matvec_partial<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, nch, part, st);
+      if (e == cudaSuccess) {
+        if constexpr (sizeof(T) == 4) {
+          if (sym) e = launch_matvec_sym(spatial_kernel, cc, (int)n_rows, (float*)part, st);
+          else e = launch_matvec_partial<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, nch, part, st);
+        } else {
+          e = launch_matvec_partial<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, nch, part, st);
+        }
+      }
       if (e == cudaSuccess) e = launch_sum_partials<T>((int)n_rows, nch, part, alpha, (T*)Y, st);
     } else if (e == cudaSuccess) {
       if constexpr (sizeof(T) == 4) {

@@ -72,82 +72,102 @@ matvec_partial_kernel(const V4<T>* __restrict__ xr, int nrows, const V4<T>* __re
 }
 
 // ------------------------------------------------------------------ K1, symmetric (fp32)
-// K_TT is symmetric: each unordered pair of 128-point tiles (I <= J) is evaluated once.
-// The 16 x 16 threads own 8 x 8 micro-tiles; row sums go to tile I, column sums to tile J:
-//   partial[J][i in I] = sum_{j in J} k_ij s_j      partial[I][j in J] = sum_{i in I} k_ij s_i
-// so row r of tile t receives exactly one partial per tile c (c = 0..nt-1) and stage A's
-// fixed-order sum over c reduces it (deterministic, no atomics).
+// K_TT is symmetric: each unordered pair of 128-point tiles is evaluated once.  Tiles are
+// grouped into blocks of SYM_S tiles; a work unit is one block pair (bi <= bj), whose
+// 2 * SYM_S tiles are staged once in shared memory.  The 16 x 16 threads own 8 x 8
+// micro-tiles of each 128 x 128 tile pair; row sums accumulate in registers across the
+// unit's J tiles, column sums in shared memory, and the unit writes
+//   partial[bj][rows of its I tiles]  and  partial[bi][rows of its J tiles]
+// (for a diagonal unit both go to partial[bi], summed), so every row receives exactly one
+// partial per block and stage A's fixed-order sum over the nb blocks reduces them
+// (deterministic, no atomics).
 constexpr int SYM_T = 128;
+constexpr int SYM_S = 8;
 template <int NU2>
 __global__ void __launch_bounds__(256)
-matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, long long npairs, float* __restrict__ partial) {
-  __shared__ float4 si[SYM_T], sj[SYM_T];
-  __shared__ float colred[16][SYM_T + 4];
+matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long nunits, float* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
+  float4* tJ = tI + SYM_S * SYM_T;                                    // [SYM_S][128]
+  float* rowacc = reinterpret_cast<float*>(tJ + SYM_S * SYM_T);       // [SYM_S][128]
+  float* colacc = rowacc + SYM_S * SYM_T;                             // [SYM_S][128]
+  float* colred = colacc + SYM_S * SYM_T;                             // [16][132]
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  for (long long p = blockIdx.x; p < npairs; p += gridDim.x) {
-    // p -> (I, J), I <= J, row-major over the upper triangle
-    const double b = 2.0 * nt + 1.0;
-    int I = (int)floor((b - sqrt(b * b - 8.0 * (double)p)) * 0.5);
-    while ((long long)I * nt - (long long)I * (I - 1) / 2 > p) --I;
-    while ((long long)(I + 1) * nt - (long long)(I + 1) * I / 2 <= p) ++I;
-    const int J = I + (int)(p - ((long long)I * nt - (long long)I * (I - 1) / 2));
+  for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+    // u -> (bi, bj), bi <= bj, row-major over the upper triangle of blocks
+    const double bb = 2.0 * nb + 1.0;
+    int bi = (int)floor((bb - sqrt(bb * bb - 8.0 * (double)u)) * 0.5);
+    while ((long long)bi * nb - (long long)bi * (bi - 1) / 2 > u) --bi;
+    while ((long long)(bi + 1) * nb - (long long)(bi + 1) * bi / 2 <= u) ++bi;
+    const int bj = bi + (int)(u - ((long long)bi * nb - (long long)bi * (bi - 1) / 2));
+    const bool diag = bi == bj;
+    const int na = min(SYM_S, nt - bi * SYM_S), nbj = min(SYM_S, nt - bj * SYM_S);
     __syncthreads();
-    if (tid < SYM_T) {
-      const int gi = I * SYM_T + tid;
-      float4 v = gi < n ? x[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
-      si[tid] = v;
-    } else {
-      const int gj = J * SYM_T + tid - SYM_T;
-      float4 v = gj < n ? x[gj] : make_float4(0.f, 0.f, 0.f, 0.f);
-      sj[tid - SYM_T] = v;
+    for (int e = tid; e < SYM_S * SYM_T; e += 256) {
+      const int gi = bi * SYM_S * SYM_T + e, gj = bj * SYM_S * SYM_T + e;
+      tI[e] = gi < n ? x[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!diag) tJ[e] = gj < n ? x[gj] : make_float4(0.f, 0.f, 0.f, 0.f);
+      rowacc[e] = 0.f;
+      colacc[e] = 0.f;
     }
+    const float4* sJ = diag ? tI : tJ;
     __syncthreads();
-    float rx[8], ry[8], rz[8], rs[8], cx[8], cy[8], cz[8], cs[8], racc[8], cacc[8];
+    for (int a = 0; a < na; ++a) {
+      float rx[8], ry[8], rz[8], rs[8], racc[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 a = si[ty * 8 + q];
-      rx[q] = a.x; ry[q] = a.y; rz[q] = a.z; rs[q] = a.w; racc[q] = 0.f;
-      const float4 c = sj[tx * 8 + q];
-      cx[q] = c.x; cy[q] = c.y; cz[q] = c.z; cs[q] = c.w; cacc[q] = 0.f;
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float dx = rx[r] - cx[c], dy = ry[r] - cy[c], dz = rz[r] - cz[c];
-        const float k = matern_from_d2<NU2>(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
-        racc[r] = fmaf(k, cs[c], racc[r]);
-        cacc[c] = fmaf(k, rs[r], cacc[c]);
+      for (int q = 0; q < 8; ++q) {
+        const float4 v = tI[a * SYM_T + ty * 8 + q];
+        rx[q] = v.x; ry[q] = v.y; rz[q] = v.z; rs[q] = v.w; racc[q] = 0.f;
       }
-    }
-    // row sums: reduce over tx (16 lanes of a half-warp)
+      for (int b = diag ? a : 0; b < nbj; ++b) {
+        const bool offdiag = !(diag && a == b);
+        float cx[8], cy[8], cz[8], cs[8], cacc[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      float v = racc[r];
-      v += __shfl_xor_sync(0xffffffffu, v, 8);
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      racc[r] = v;
-    }
-    if (tx == 0) {
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = sJ[b * SYM_T + tx * 8 + q];
+          cx[q] = v.x; cy[q] = v.y; cz[q] = v.z; cs[q] = v.w; cacc[q] = 0.f;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float dx = rx[r] - cx[c], dy = ry[r] - cy[c], dz = rz[r] - cz[c];
+            const float k = matern_from_d2<NU2>(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+            racc[r] = fmaf(k, cs[c], racc[r]);
+            cacc[c] = fmaf(k, rs[r], cacc[c]);
+          }
+        }
+        if (offdiag) {   // column sums of this tile pair -> colacc[b] (fixed order over ty)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) colred[ty * 132 + tx * 8 + c] = cacc[c];
+          __syncthreads();
+          if (tid < SYM_T) {
+            float v = 0.f;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v += colred[t * 132 + tid];
+            colacc[b * SYM_T + tid] += v;
+          }
+          __syncthreads();
+        }
+      }
+      // row sums over the unit's J tiles: reduce over tx (16 lanes of a half-warp)
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const int gi = I * SYM_T + ty * 8 + r;
-        if (gi < n) partial[(size_t)J * n + gi] = racc[r];
+        float v = racc[r];
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (tx == 0) rowacc[a * SYM_T + ty * 8 + r] += v;
       }
     }
-    if (I != J) {
-      // column sums: reduce over ty through shared memory
-#pragma unroll
-      for (int c = 0; c < 8; ++c) colred[ty][tx * 8 + c] = cacc[c];
-      __syncthreads();
-      if (tid < SYM_T) {
-        float v = 0.f;
-#pragma unroll
-        for (int t = 0; t < 16; ++t) v += colred[t][tid];
-        const int gj = J * SYM_T + tid;
-        if (gj < n) partial[(size_t)I * n + gj] = v;
+    __syncthreads();
+    for (int e = tid; e < SYM_S * SYM_T; e += 256) {
+      const int gi = bi * SYM_S * SYM_T + e;
+      if (gi < n) partial[(size_t)bj * n + gi] = rowacc[e] + (diag ? colacc[e] : 0.f);
+      if (!diag) {
+        const int gj = bj * SYM_S * SYM_T + e;
+        if (gj < n) partial[(size_t)bi * n + gj] = colacc[e];
       }
     }
   }
@@ -299,7 +319,7 @@ cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<
   return cudaErrorInvalidValue;
 }
 
-int matvec_sym_tiles(int n) { return (n + SYM_T - 1) / SYM_T; }
+int matvec_sym_tiles(int n) { return ((n + SYM_T - 1) / SYM_T + SYM_S - 1) / SYM_S; }   // = partials per row
 
 bool use_sym_k1() {
   static int v = -1;
@@ -312,13 +332,23 @@ bool use_sym_k1() {
 
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  const int nt = matvec_sym_tiles(n);
-  const long long npairs = (long long)nt * (nt + 1) / 2;
-  const long long grid = std::min<long long>(npairs, (long long)num_sms() * 8);
+  const int nt = (n + SYM_T - 1) / SYM_T;
+  const int nb = (nt + SYM_S - 1) / SYM_S;
+  const long long nunits = (long long)nb * (nb + 1) / 2;
+  const long long grid = std::min<long long>(nunits, (long long)num_sms() * 3);
+  const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)2 * SYM_S * SYM_T * sizeof(float) +
+                      (size_t)16 * 132 * sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(matvec_sym_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(matvec_sym_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(matvec_sym_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
   switch (nu2) {
-    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, 0, st>>>(x, n, nt, npairs, partial); break;
-    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, 0, st>>>(x, n, nt, npairs, partial); break;
-    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, 0, st>>>(x, n, nt, npairs, partial); break;
+    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, nunits, partial); break;
+    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, nunits, partial); break;
+    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, nunits, partial); break;
     default: return cudaErrorInvalidValue;
   }
   return note_launch_err();

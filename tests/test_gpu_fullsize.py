@@ -47,3 +47,26 @@ def test_gram_operator_cfg3_sampled_rows(cfg3, ncols):
     err = _rel_err(Y, ref, B64, xr64, xc64, wl.nu_x, wl.ell_x)
     print("cfg3 sampled rows, ncols", ncols, "max rel err", err)
     assert err < 2e-5
+
+
+def test_symmetric_k1_cfg3(cfg3):
+    """The inner-loop matvec K_TT s (symmetric tile-pair kernel, N = 87,120) at full size:
+    sampled rows vs the oracle, and all rows vs the dense-kernel path."""
+    wl = cfg3
+    rng = np.random.default_rng(7)
+    Xt = wl.coords[wl.obs_idx[0]]
+    s = rng.standard_normal(len(Xt))
+    xt = torch.tensor(Xt.astype(np.float32), device="cuda")
+    st = torch.tensor(s.astype(np.float32), device="cuda")
+    y = binding.gram_matmul(xt, xt, st, wl.nu_x, wl.ell_x).double().cpu().numpy()      # xr is xc: symmetric
+    y_dense = binding.gram_matmul(xt, xt.clone(), st, wl.nu_x, wl.ell_x).double().cpu().numpy()
+    rows = np.concatenate([np.arange(200), np.arange(len(Xt) - 77, len(Xt))])
+    X64 = Xt.astype(np.float32).astype(np.float64)
+    s64 = s.astype(np.float32).astype(np.float64)
+    ref = mfree.gram_apply(X64[rows], X64, s64, wl.nu_x, wl.ell_x, chunk=64)
+    scale = mfree.gram_apply(X64[rows], X64, np.abs(s64), wl.nu_x, wl.ell_x, chunk=64)
+    err = float(np.max(np.abs(y[rows] - ref) / scale))
+    err_all = float(np.max(np.abs(y - y_dense) / np.maximum(np.abs(y_dense), 1e-30)))
+    print("symmetric K1 cfg3: sampled rel err", err, "vs dense kernel", err_all)
+    assert err < 1e-6
+    assert np.max(np.abs(y - y_dense)) < 1e-5 * np.max(np.abs(y_dense))
