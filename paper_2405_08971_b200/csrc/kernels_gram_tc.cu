@@ -12,15 +12,19 @@
 // take 6 bytes per element instead of 8.
 //
 // Per CTA: a 128-row x N_TILE (<= 256) output tile in TMEM.  Per K-block of 32:
-//   * 256 threads evaluate the 128 x 32 Matérn block (FP32 pipe + MUFU), split it and store
-//     the three planes in the K-major SWIZZLE_64B canonical layout;
-//   * the three B planes (precomputed, K-major) and the block's column coordinates arrive by
-//     cp.async two blocks ahead;
+//   * warp-specialised: 8 producer warps evaluate the 128 x 32 Matérn block (FP32 pipe +
+//     MUFU), split it and store the three planes in the K-major SWIZZLE_64B canonical layout;
+//     a 9th warp issues the MMAs; the two sides meet only at full / empty mbarriers;
+//   * a loader warp brings the three B planes (precomputed, K-major) and the block's column
+//     coordinates with TMA (cp.async.bulk.tensor, 64B swizzle = the UMMA canonical layout,
+//     zero fill out of bounds), up to three blocks ahead;
 //   (Tried: A as the TMEM operand written with tcgen05.st ("TS" mode) — correct but 2.5x slower
 //    on B200, the stores serialise against the in-flight MMAs.)
-//   * one thread issues 2 k-steps x 6 tcgen05.mma.kind::f16 and commits to the stage mbarrier;
-//   * three stages: generation of block kb overlaps the MMAs of kb-1 and the loads of kb+2.
+//   * the MMA warp issues 2 k-steps x 6 tcgen05.mma.kind::f16 per block and commits to the
+//     stage's empty barrier; with three stages the producers run up to two blocks ahead.
 // Epilogue: tcgen05.ld (32x32b) -> registers -> coalesced column-major stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -35,12 +39,16 @@ namespace {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;                        // 32 bf16 = one 64-byte swizzle atom row
 constexpr int TC_THREADS = 256;
-constexpr int TC_MAXN = 256;
-constexpr int TC_STAGES = 3;
+constexpr int TC_MAXN = 208;
+constexpr int A_STAGES = 2;                      // generated operand ring
+constexpr int B_STAGES = 4;                      // TMA operand ring (loads run 3 blocks ahead)
+constexpr int TC_STAGES = B_STAGES;
 constexpr int A_PLANE = TC_BM * TC_BK * 2;       // 8 KB
-constexpr int B_PLANE = TC_MAXN * TC_BK * 2;     // 16 KB
-constexpr int STAGE_BYTES = 3 * A_PLANE + 3 * B_PLANE + 1024;   // 72 KB + the K-block's column coordinates
-constexpr int TC_SMEM = TC_STAGES * STAGE_BYTES + 1024 + 128;
+constexpr int B_PLANE = TC_MAXN * TC_BK * 2;     // 13 KB (multiple of the 512 B SW64 atom)
+constexpr int XC_BYTES = TC_BK * 16;             // the K-block's 32 column coordinates
+constexpr int A_STAGE_BYTES = 3 * A_PLANE;                                   // 24 KB
+constexpr int B_STAGE_BYTES = (3 * B_PLANE + XC_BYTES + 1023) / 1024 * 1024;  // 40 KB
+constexpr int TC_SMEM = A_STAGES * A_STAGE_BYTES + B_STAGES * B_STAGE_BYTES + 1024 + 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -110,16 +118,22 @@ __device__ __forceinline__ uint32_t sw64_off(int r, int c) {
 }
 
 template <int NU2>
-__global__ void __launch_bounds__(TC_THREADS, 1)
-gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const float4* __restrict__ xc, int K,
-                    const uint16_t* __restrict__ Bp, size_t ldp, size_t plane, int C, int ntile,
+__global__ void __launch_bounds__(TC_THREADS + 64, 1)
+gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmX, int K, int C, int ntile,
                     float* __restrict__ Y, size_t ldy, float alpha, int diag_nogen) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   unsigned char* sbase = smem_raw + (base - raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + TC_STAGES * STAGE_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + TC_STAGES * STAGE_BYTES + 64);
+  unsigned char* a_base = sbase;                                   // A ring
+  unsigned char* b_base = sbase + A_STAGES * A_STAGE_BYTES;        // B ring (+ coordinates)
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(b_base + B_STAGES * B_STAGE_BYTES);   // producers -> MMA
+  uint64_t* emptyA = fullA + A_STAGES;                                                 // MMA -> producers
+  uint64_t* fullB = emptyA + A_STAGES;                                                 // TMA -> producers
+  uint64_t* emptyB = fullB + B_STAGES;                                                 // MMA -> loader
+  uint64_t* done = emptyB + B_STAGES;                                                  // last MMA -> epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.x * TC_BM, n0 = blockIdx.y * ntile;
@@ -128,64 +142,109 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const float4* __restri
   // accumulation truncates, so keeping the small terms apart cuts the biased error ~6x)
   const uint32_t acc_cols = ntile <= 32 ? 32 : ntile <= 64 ? 64 : ntile <= 128 ? 128 : 256;
   const uint32_t tmem_cols = 2 * acc_cols;
+  const int nk = (K + TC_BK - 1) / TC_BK;
 
-  if (warp == 0) {
+  if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (tid == 32) {
-    for (int s = 0; s < TC_STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
+  if (tid == 0) {
+    for (int s = 0; s < A_STAGES; ++s) {
+      mbar_init(smem_u32(&fullA[s]), TC_THREADS);
+      mbar_init(smem_u32(&emptyA[s]), 1);
+    }
+    for (int s = 0; s < B_STAGES; ++s) {
+      mbar_init(smem_u32(&fullB[s]), 1);
+      mbar_init(smem_u32(&emptyB[s]), 1);
+    }
+    mbar_init(smem_u32(done), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  auto a_addr = [&](int s) { return smem_u32(a_base + s * A_STAGE_BYTES); };
+  auto b_addr = [&](int s) { return smem_u32(b_base + s * B_STAGE_BYTES); };
 
-  const int arow = tid & (TC_BM - 1), khalf = tid >> 7;
-  float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (m0 + arow < M) xa = xr[m0 + arow];
-  const uint32_t idesc = idesc_bf16(TC_BM, ntile);
-  const int nk = (K + TC_BK - 1) / TC_BK;
-  const int nchunks = ntile * 4;                   // 16-byte chunks per B plane per K-block
-
-  auto stage_addr = [&](int s) { return smem_u32(sbase + s * STAGE_BYTES); };
-  auto load_b = [&](int kb) {
-    const int s = kb % TC_STAGES;
-    const uint32_t b0 = stage_addr(s) + 3 * A_PLANE;
-    const int k0 = kb * TC_BK;
+  if (warp == 8) {
+    // ===== MMA issuer: one elected lane, back-to-back over the stage ring
+    const uint32_t idesc = idesc_bf16(TC_BM, ntile);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int sa = kb % A_STAGES, sb = kb % B_STAGES;
+      mbar_wait(smem_u32(&fullA[sa]), (kb / A_STAGES) & 1);
+      mbar_wait(smem_u32(&fullB[sb]), (kb / B_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+        const uint32_t a0 = a_addr(sa), bb = b_addr(sb);
 #pragma unroll
-    for (int pl = 0; pl < 3; ++pl) {
-      for (int e = tid; e < nchunks; e += TC_THREADS) {
-        const int n = e >> 2, c = e & 3;
-        const bool ok = (n0 + n) < C;
-        const uint16_t* src = Bp + pl * plane + (size_t)(ok ? n0 + n : 0) * ldp + k0 + 8 * c;
-        cp_async16(b0 + pl * B_PLANE + sw64_off(n, c), src, ok ? 16u : 0u);
+        for (int j = 0; j < TC_BK / 16; ++j) {
+          const uint64_t A1 = sdesc_sw64(a0 + 32 * j), A2 = sdesc_sw64(a0 + A_PLANE + 32 * j),
+                         A3 = sdesc_sw64(a0 + 2 * A_PLANE + 32 * j);
+          const uint64_t B1 = sdesc_sw64(bb + 32 * j), B2 = sdesc_sw64(bb + B_PLANE + 32 * j),
+                         B3 = sdesc_sw64(bb + 2 * B_PLANE + 32 * j);
+          const uint32_t first = (kb | j) ? 1u : 0u;
+          mma_bf16(tmem, A1, B1, idesc, first);
+          mma_bf16(tmem + acc_cols, A1, B2, idesc, first);
+          mma_bf16(tmem + acc_cols, A2, B1, idesc, 1u);
+          mma_bf16(tmem + acc_cols, A2, B2, idesc, 1u);
+          mma_bf16(tmem + acc_cols, A1, B3, idesc, 1u);
+          mma_bf16(tmem + acc_cols, A3, B1, idesc, 1u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&emptyA[sa]))
+                     : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&emptyB[sb]))
+                     : "memory");
+        if (kb == nk - 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(done))
+                       : "memory");
+      }
+      __syncwarp();
+    }
+  } else if (warp == 9) {
+    // ===== TMA loader: the three B planes (64B-swizzled boxes, zero-filled beyond C / K) and the
+    // block's 32 column coordinates, up to TC_STAGES blocks ahead of the MMAs
+    if (lane == 0) {
+      const uint32_t bytes = 3u * (uint32_t)ntile * 64u + (uint32_t)XC_BYTES;
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % B_STAGES;
+        if (kb >= B_STAGES) mbar_wait(smem_u32(&emptyB[s]), ((kb / B_STAGES) - 1) & 1);
+        const uint32_t bar = smem_u32(&fullB[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        const uint32_t b0 = b_addr(s);
+        const int k0 = kb * TC_BK;
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl) {
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+              "[%5];" ::"r"(b0 + pl * B_PLANE),
+              "l"(&tmB), "r"(k0), "r"(n0), "r"(pl), "r"(bar)
+              : "memory");
+        }
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                b0 + 3 * B_PLANE),
+            "l"(&tmX), "r"(0), "r"(k0), "r"(bar)
+            : "memory");
       }
     }
-    if (tid < TC_BK) {   // column coordinates of this K-block (zero beyond K: B is zero there)
-      const int j = k0 + tid;
-      cp_async16(b0 + 3 * B_PLANE + 16 * tid, &xc[j < K ? j : 0], j < K ? 16u : 0u);
-    }
-  };
-
-  // prologue: B for blocks 0 and 1
-  if (nk > 0) load_b(0);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  if (nk > 1) load_b(1);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-
-  for (int kb = 0; kb < nk; ++kb) {
-    const int s = kb % TC_STAGES;
-    const uint32_t a0 = stage_addr(s);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");          // B(kb) + coords(kb) landed
-    __syncthreads();
-    // ---- A planes: Matérn values of row arow, columns k0 + 16*khalf + [0, 16)
-    {
-      const float4* sxc = reinterpret_cast<const float4*>(sbase + s * STAGE_BYTES + 3 * A_PLANE + 3 * B_PLANE) +
-                          16 * khalf;
+    __syncwarp();
+  } else {
+    // ===== producers (warps 0-7): A generation from the staged column coordinates
+    const int arow = tid & (TC_BM - 1), khalf = tid >> 7;
+    float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (m0 + arow < M) xa = xr[m0 + arow];
+    for (int kb = 0; kb < nk; ++kb) {
+      const int sa = kb % A_STAGES, sb = kb % B_STAGES;
+      mbar_wait(smem_u32(&fullB[sb]), (kb / B_STAGES) & 1);                       // coords(kb) landed
+      if (kb >= A_STAGES) mbar_wait(smem_u32(&emptyA[sa]), ((kb / A_STAGES) - 1) & 1);   // MMA(kb - 2) done
+      const uint32_t a0 = a_addr(sa);
+      const float4* sxc = reinterpret_cast<const float4*>(b_base + sb * B_STAGE_BYTES + 3 * B_PLANE) + 16 * khalf;
       uint32_t p1[8], p2[8], p3[8];   // bf16x2 packed
 #pragma unroll
       for (int q = 0; q < 16; q += 2) {
@@ -217,73 +276,46 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const float4* __restri
                      "r"(p3[4 * h + 1]), "r"(p3[4 * h + 2]), "r"(p3[4 * h + 3])
                      : "memory");
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> tensor core
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fullA[sa])) : "memory");
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> tensor core
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t bb = a0 + 3 * A_PLANE;
+    // ===== epilogue: D = D_big + D_small (fp32 round-to-nearest)
+    if (nk > 0) mbar_wait(smem_u32(done), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quarter = warp & 3;
+    const int row = m0 + quarter * 32 + lane;
+    const int half_cols = ((ntile / 2) + 15) / 16 * 16;
+    const int c_begin = (warp >> 2) * half_cols;
+    const int c_end = (warp >> 2) ? ntile : half_cols;
+    for (int cb = c_begin; cb < c_end; cb += 16) {
+      uint32_t r[16], q[16];
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+          "%14, %15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+          "%14, %15}, [%16];"
+          : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
+            "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
+          : "r"(taddr + acc_cols));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < M) {
 #pragma unroll
-      for (int j = 0; j < TC_BK / 16; ++j) {
-        const uint64_t A1 = sdesc_sw64(a0 + 32 * j), A2 = sdesc_sw64(a0 + A_PLANE + 32 * j),
-                       A3 = sdesc_sw64(a0 + 2 * A_PLANE + 32 * j);
-        const uint64_t B1 = sdesc_sw64(bb + 32 * j), B2 = sdesc_sw64(bb + B_PLANE + 32 * j),
-                       B3 = sdesc_sw64(bb + 2 * B_PLANE + 32 * j);
-        const uint32_t first = (kb | j) ? 1u : 0u;
-        mma_bf16(tmem, A1, B1, idesc, first);
-        mma_bf16(tmem + acc_cols, A1, B2, idesc, first);
-        mma_bf16(tmem + acc_cols, A2, B1, idesc, 1u);
-        mma_bf16(tmem + acc_cols, A2, B2, idesc, 1u);
-        mma_bf16(tmem + acc_cols, A1, B3, idesc, 1u);
-        mma_bf16(tmem + acc_cols, A3, B1, idesc, 1u);
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(&bars[s]))
-                   : "memory");
-    }
-    // B(kb+2) goes into the stage MMA(kb-1) used: wait for it (it precedes MMA(kb) on the tensor pipe)
-    if (kb + 2 < nk) {
-      if (kb >= 1) mbar_wait(smem_u32(&bars[(kb - 1) % TC_STAGES]), ((kb - 1) / TC_STAGES) & 1);
-      load_b(kb + 2);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  // ---- epilogue
-  if (nk > 0) mbar_wait(smem_u32(&bars[(nk - 1) % TC_STAGES]), ((nk - 1) / TC_STAGES) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int quarter = warp & 3;
-  const int row = m0 + quarter * 32 + lane;
-  const int half_cols = ((ntile / 2) + 15) / 16 * 16;
-  const int c_begin = (warp >> 2) * half_cols;
-  const int c_end = (warp >> 2) ? ntile : half_cols;
-  for (int cb = c_begin; cb < c_end; cb += 16) {
-    uint32_t r[16], q[16];
-    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];"
-        : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]), "=r"(q[8]),
-          "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
-        : "r"(taddr + acc_cols));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < M) {
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int n = n0 + cb + t;
-        const float v = __uint_as_float(r[t]) + __uint_as_float(q[t]);
-        if (cb + t < c_end && n < C) Y[row + (size_t)n * ldy] = nk > 0 ? alpha * v : 0.f;
+        for (int t = 0; t < 16; ++t) {
+          const int n = n0 + cb + t;
+          const float v = __uint_as_float(r[t]) + __uint_as_float(q[t]);
+          if (cb + t < c_end && n < C) Y[row + (size_t)n * ldy] = nk > 0 ? alpha * v : 0.f;
+        }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 8) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
   }
 }
@@ -303,19 +335,49 @@ __global__ void split_bf16x3_kernel(int K, int C, int Kp, const float* __restric
   planes[2 * plane + e] = (uint16_t)p3;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
 template <int NU2>
-cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const uint16_t* planes, size_t ldp,
-                         size_t plane, int C, int ntile, float* Y, size_t ldy, float alpha, cudaStream_t st) {
+cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const uint16_t* planes, int Kp, int C,
+                         int ntile, float* Y, size_t ldy, float alpha, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((M + TC_BM - 1) / TC_BM, (C + ntile - 1) / ntile);
+  auto enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  // B planes: 3 x [C rows] x [Kp bf16], K innermost; boxes of 32 K x ntile rows, 64B swizzle
+  CUtensorMap tmB, tmX;
+  const cuuint64_t gdB[3] = {(cuuint64_t)Kp, (cuuint64_t)C, 3};
+  const cuuint64_t gsB[2] = {(cuuint64_t)Kp * 2, (cuuint64_t)Kp * C * 2};
+  const cuuint32_t boxB[3] = {TC_BK, (cuuint32_t)ntile, 1};
+  const cuuint32_t es3[3] = {1, 1, 1};
+  if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, (void*)planes, gdB, gsB, boxB, es3, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  // column coordinates: [K rows] x [4 floats]; boxes of 32 rows, zero beyond K
+  const cuuint64_t gdX[2] = {4, (cuuint64_t)K};
+  const cuuint64_t gsX[1] = {16};
+  const cuuint32_t boxX[2] = {4, TC_BK};
+  const cuuint32_t es2[2] = {1, 1};
+  if (enc(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)xc, gdX, gsX, boxX, es2, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
   static const int nogen = [] { const char* e = getenv("CAKF_TC_DIAG_NOGEN"); return (e && e[0] == '1') ? 1 : 0; }();
-  gram_gemm_tc_kernel<NU2><<<grid, TC_THREADS, TC_SMEM, st>>>(xr, M, xc, K, planes, ldp, plane, C, ntile, Y, ldy, alpha,
-                                                              nogen);
+  dim3 grid((M + TC_BM - 1) / TC_BM, (C + ntile - 1) / ntile);
+  gram_gemm_tc_kernel<NU2><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha, nogen);
   return note_launch_err();
 }
 
@@ -351,9 +413,9 @@ cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* 
   int ntile = (C + ntiles - 1) / ntiles;
   ntile = ((ntile + 15) / 16) * 16;
   switch (nu2) {
-    case 1: return launch_tc_nu<1>(xr, M, xc, K, planes, Kp, plane, C, ntile, Y, ldy, (float)alpha, st);
-    case 3: return launch_tc_nu<3>(xr, M, xc, K, planes, Kp, plane, C, ntile, Y, ldy, (float)alpha, st);
-    case 5: return launch_tc_nu<5>(xr, M, xc, K, planes, Kp, plane, C, ntile, Y, ldy, (float)alpha, st);
+    case 1: return launch_tc_nu<1>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st);
+    case 3: return launch_tc_nu<3>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st);
+    case 5: return launch_tc_nu<5>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st);
   }
   return cudaErrorInvalidValue;
 }
