@@ -10,9 +10,9 @@ cfg3) is far larger than the 126 MB L2, so inputs are larger than L2 between ite
 
 --impl reference times the CPU oracle (oracle/mfree.py, as it stands) on a bounded sample
 of the same workload and extrapolates to time-steps/s (sample described in the JSON).
-N > 1 (torchrun): this round the ranks run independent replicas of the workload
-(weak scaling, no collective on the data path; the row-sharded multi-GPU path is
-described in DESIGN.md §7).
+N > 1 (torchrun): one problem, the two Gram products sharded over the ranks (K1 by
+symmetric tile-block units + NCCL all-reduce, K2 by output-row slices + NCCL all-gather),
+the rest replicated; strong scaling.
 """
 from __future__ import annotations
 
@@ -218,7 +218,12 @@ def main():
     wl = make_workload(args.config, **kw)
     trans, _ = runner.transitions(wl)
     stream = torch.cuda.current_stream()
-    h = runner.make_handle(wl, args.dtype, stream=stream.cuda_stream)
+    nccl_id = None
+    if world > 1:
+        obj = [binding.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    h = runner.make_handle(wl, args.dtype, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id)
     inputs = runner.stage_inputs(wl, args.dtype)
 
     def barrier():
@@ -249,7 +254,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_timesteps = args.steps * wl.T * world
+    total_timesteps = args.steps * wl.T            # one problem sharded over all ranks (strong scaling)
     value = total_timesteps / (ms / 1e3)
     clocks = clk.summary()
 
@@ -282,7 +287,7 @@ def main():
         t = torch.tensor([ms_e2e], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
-    e2e = {"value": args.e2e_steps * wl.T * world / max(ms_e2e / 1e3, 1e-9), "unit": "time-steps/s",
+    e2e = {"value": args.e2e_steps * wl.T / max(ms_e2e / 1e3, 1e-9), "unit": "time-steps/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     # ---------------- roofline of the dominant kernel (live CUDA-event timings)
@@ -328,12 +333,14 @@ def main():
     breakdown = {c: round(prof[c][0] / args.steps, 3) for c in prof}
     out = {
         "metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": args.config, "D": wl.D, "N_X": wl.n_space, "N": N, "T": wl.T,
                    "policy": wl.policy, "max_iter": wl.max_iter, "max_rank": wl.max_rank,
                    "step": "one full CAKF (T predict/update/truncate) + CAKS (T smoother steps) pass",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"row-sharded Gram products x{world} (NCCL all-reduce / all-gather)"
+                                   if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2 (trace 25.6 GB vs 126 MB L2)"},
         "clocks": clocks,
         "gpu_launches": int(launches),

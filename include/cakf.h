@@ -184,6 +184,25 @@ int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset);
 /* Number of libcakf kernels launched by this process so far (all handles). */
 int64_t cakf_kernel_launches(void);
 
+/* ---- multi-GPU (the spatial rows of the covariance operator are sharded) ----
+ * With cfg.world > 1 every rank calls the same sequence with the same full inputs; the two
+ * Gram products are sharded and exchanged with NCCL on cfg.stream, everything else is
+ * computed identically (deterministically) on every rank:
+ *   K1 (inner-loop K_TT s): rank p evaluates symmetric tile-block units [u_lo, u_hi) and the
+ *       reduced N-vector is all-reduced (ncclAllReduce, sum);
+ *   K2 (post-loop / smoother K(X, .) B): rank p computes output rows [row_lo, row_hi) (128-row
+ *       aligned slices) and the slices are all-gathered (ncclAllGather).
+ * cakf_nccl_unique_id writes the 128-byte ncclUniqueId rank 0 creates (broadcast it to all ranks
+ * and pass it as cfg.nccl_id). */
+int cakf_nccl_unique_id(void* out128);
+
+/* Host-only: the shard of rank `rank` of `world`: out[0..5] = {row_lo, row_hi, u_lo, u_hi,
+ * n_units, slice_rows} for n_space points and n_obs observations. */
+int cakf_shard_plan(int64_t n_space, int64_t n_obs, int32_t world, int32_t rank, int64_t* out);
+
+/* Host-only mirror of the symmetric K1's unit -> (tile block i, tile block j) map, i <= j. */
+int cakf_sym_unit_blocks(int64_t n_obs, int64_t unit, int32_t* bi, int32_t* bj);
+
 /* Free everything the handle owns. */
 int cakf_destroy(cakf_t h);
 

@@ -60,6 +60,7 @@ EXPORTS = [
     "cakf_create", "cakf_reset", "cakf_predict", "cakf_update", "cakf_truncate", "caks_smooth", "cakf_get",
     "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
+    "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks",
 ]
 PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank"]
 
@@ -92,6 +93,9 @@ def load(path: str = LIB_PATH):
     lib.cakf_profile.argtypes = [vp, i32]
     lib.cakf_profile_read.argtypes = [vp, vp, vp, i32]
     lib.cakf_kernel_launches.restype = ctypes.c_int64
+    lib.cakf_nccl_unique_id.argtypes = [vp]
+    lib.cakf_shard_plan.argtypes = [i64, i64, i32, i32, vp]
+    lib.cakf_sym_unit_blocks.argtypes = [i64, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     for name in EXPORTS:
         if name not in ("cakf_last_error", "cakf_version", "cakf_kernel_launches"):
             getattr(lib, name).restype = ctypes.c_int
@@ -120,6 +124,27 @@ def _ptr(x):
 def kernel_launches() -> int:
     """Number of libcakf kernels launched by this process so far."""
     return int(load().cakf_kernel_launches())
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (create on rank 0, broadcast, pass as nccl_id)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().cakf_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_plan(n_space: int, n_obs: int, world: int, rank: int) -> dict:
+    """Rows of the K2 output and units of the symmetric K1 owned by `rank` (host-only)."""
+    out = np.zeros(6, dtype=np.int64)
+    _check(load().cakf_shard_plan(int(n_space), int(n_obs), int(world), int(rank), out.ctypes.data))
+    return dict(zip(["row_lo", "row_hi", "u_lo", "u_hi", "n_units", "slice_rows"], (int(v) for v in out)))
+
+
+def sym_unit_blocks(n_obs: int, unit: int):
+    """(bi, bj) tile blocks of a symmetric K1 unit (host mirror of the device map)."""
+    bi, bj = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(load().cakf_sym_unit_blocks(int(n_obs), int(unit), ctypes.byref(bi), ctypes.byref(bj)))
+    return bi.value, bj.value
 
 
 def matern_transition(nu: float, ell_t: float, sigma: float, dt: float):
@@ -154,7 +179,8 @@ class Cakf:
     """One CAKF/CAKS handle (``cakf_t``).  Methods map 1:1 onto the C-ABI."""
 
     def __init__(self, coords, ell_x, sigma_t0, *, dtype="f32", d_time=2, nu_x=1.5, mu0=None, policy="cg",
-                 max_iter=64, max_rank=-1, seed=1, max_steps=48, max_obs=0, reorth=True, stream=None):
+                 max_iter=64, max_rank=-1, seed=1, max_steps=48, max_obs=0, reorth=True, stream=None,
+                 rank=0, world=1, nccl_id=None):
         self.lib = load()
         coords = np.ascontiguousarray(coords, dtype=np.float64)
         if coords.ndim == 1:
@@ -171,8 +197,12 @@ class Cakf:
                           policy=POLICIES[policy] if isinstance(policy, str) else int(policy),
                           max_iter=int(max_iter), max_rank=int(max_rank), rtol=0.0, reorth=int(bool(reorth)),
                           seed=int(seed),
-                          max_steps=int(max_steps), max_obs=int(max_obs), rank=0, world=1, nccl_id=None,
-                          stream=stream)
+                          max_steps=int(max_steps), max_obs=int(max_obs), rank=int(rank), world=int(world),
+                          nccl_id=None, stream=stream)
+        self._nccl_id = None
+        if world > 1:
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         h = ctypes.c_void_p()
         _check(self.lib.cakf_create(ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h

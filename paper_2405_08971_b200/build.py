@@ -15,6 +15,11 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcakf.so")
 SOURCES = ["kernels_gram.cu", "kernels_gram_tc.cu", "kernels_step.cu", "cakf_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+try:  # NCCL as bundled with torch (nvidia-nccl wheel): headers + libnccl.so.2
+    import nvidia.nccl as _nccl
+    NCCL_DIR = os.path.dirname(_nccl.__file__) if _nccl.__file__ else list(_nccl.__path__)[0]
+except Exception:  # pragma: no cover
+    NCCL_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl"
 
 
 def nvcc() -> str:
@@ -39,7 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     build_dir = os.path.join(HERE, "build")
     os.makedirs(build_dir, exist_ok=True)
     common = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
-              "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v" if verbose else "-O3"]
+              "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL_DIR, "include"),
+              "-Xptxas", "-v" if verbose else "-O3"]
     procs = []
     for src in SOURCES:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
@@ -53,8 +59,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out:
             print(out)
     tmp = LIB + ".tmp"
-    link = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcublas", "-lcusolver",
-            "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    nccl_lib = os.path.join(NCCL_DIR, "lib")
+    link = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcublas", "-lcusolver", "-L", nccl_lib, "-l:libnccl.so.2",
+            "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-Xlinker", "-rpath," + nccl_lib]
     r = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + " ".join(link) + "\n" + r.stdout)

@@ -12,6 +12,7 @@
 // calls (iteration counts and ranks are host-known integers, R2/R3).
 #include <cublas_v2.h>
 #include <cusolverDn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -59,6 +60,14 @@ int fail(int code, const std::string& msg) {
     if (s_ != CUSOLVER_STATUS_SUCCESS) {                                                        \
       failed_ = true;                                                                           \
       return fail(CAKF_E_CUDA, std::string(#expr) + ": cusolver status " + std::to_string(s_)); \
+    }                                                                                           \
+  } while (0)
+#define CK_NCCL(expr)                                                                           \
+  do {                                                                                          \
+    ncclResult_t r_ = (expr);                                                                   \
+    if (r_ != ncclSuccess) {                                                                    \
+      failed_ = true;                                                                           \
+      return fail(CAKF_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_));             \
     }                                                                                           \
   } while (0)
 #define CK(expr)              \
@@ -203,10 +212,22 @@ struct Impl final : ImplBase {
   // smoother
   T *X = nullptr, *Yk = nullptr, *yb = nullptr, *Tm = nullptr, *Hy = nullptr, *tt = nullptr, *R = nullptr;
   T *Wf = nullptr, *Ws = nullptr, *ws = nullptr, *pvar = nullptr;
-  float* tcw = nullptr;  // tf32 hi/lo planes of the K2 right-hand sides
+  float* tcw = nullptr;  // bf16 planes of the K2 right-hand sides
 
-  // K2: Y = K(xr, xc) B — tcgen05 3xTF32 for fp32, SIMT for fp64 (or CAKF_K2_SIMT=1)
-  cudaError_t k2(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y, size_t ldy) {
+  // ---------------- multi-GPU: the Gram products are sharded, the rest replicated
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  T *yloc = nullptr, *yred = nullptr;      // K1: this rank's reduced partial, all-reduced vector
+  T *yslice = nullptr, *ygath = nullptr;   // K2: this rank's output row slice, all-gathered slices
+  size_t k2_cmax = 0;
+
+  static int k2_slice_rows(int M, int world_) {
+    const int per = (M + world_ - 1) / world_;
+    return ((per + 127) / 128) * 128;
+  }
+
+  cudaError_t k2_local(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y,
+                       size_t ldy) {
     if constexpr (sizeof(T) == 4) {
       if (use_tc_k2())
         return launch_gram_gemm_tc(nu2, reinterpret_cast<const float4*>(xr), M, reinterpret_cast<const float4*>(xc), K,
@@ -214,6 +235,23 @@ struct Impl final : ImplBase {
                                    tcw, st);
     }
     return launch_gram_gemm<T>(nu2, xr, M, xc, K, B, ldb, C, Y, ldy, 1.0, st);
+  }
+
+  // K2: Y = K(xr, xc) B — tcgen05 3xBF16 for fp32, SIMT for fp64 (or CAKF_K2_SIMT=1).
+  // world > 1: rank p computes output rows [p*slice, (p+1)*slice) and the slices are all-gathered.
+  int k2(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y, size_t ldy) {
+    if (world == 1) {
+      CK_CUDA(k2_local(xr, M, xc, K, B, ldb, C, Y, ldy));
+      return CAKF_OK;
+    }
+    if ((size_t)C > k2_cmax) return fail(CAKF_E_ARG, "k2: too many right-hand sides for the shard buffers");
+    const int slice = k2_slice_rows(M, world);
+    const int lo = rank * slice;
+    const int mloc = std::max(0, std::min(slice, M - lo));
+    if (mloc > 0) CK_CUDA(k2_local(xr + lo, mloc, xc, K, B, ldb, C, yslice, (size_t)slice));
+    CK_NCCL(ncclAllGather(yslice, ygath, (size_t)slice * C, sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, comm, st));
+    CK_CUDA(StepKernels<T>::assemble_slices(M, C, slice, ygath, Y, ldy, st));
+    return CAKF_OK;
   }
 
   // ---------------- profiling: CUDA events around launches of one category (cakf_profile)
@@ -266,6 +304,7 @@ struct Impl final : ImplBase {
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (arena) cudaFree(arena);
     if (ctl_init_host) cudaFreeHost(ctl_init_host);
+    if (comm) ncclCommDestroy(comm);
     if (blas) cublasDestroy(blas);
     if (sol) cusolverDnDestroy(sol);
     if (own_stream && st) cudaStreamDestroy(st);
@@ -363,6 +402,14 @@ struct Impl final : ImplBase {
     Ws = carve<T>((size_t)D * (nhat + qmax));
     ws = carve<T>(D);
     pvar = carve<T>(D);
+    if (world > 1) {
+      yloc = carve<T>(Nmax);
+      yred = carve<T>(Nmax);
+      k2_cmax = std::max<size_t>((size_t)(1 + nhat), (size_t)Dp * (1 + qmax));
+      const size_t slice = (size_t)k2_slice_rows((int)NX, world);
+      yslice = carve<T>(slice * k2_cmax);
+      ygath = carve<T>(slice * k2_cmax * world);
+    }
     if (sizeof(T) == 4) {
       const size_t wb = std::max(gram_gemm_tc_workspace((int)Nmax, 1 + nhat),
                                  gram_gemm_tc_workspace((int)NX, Dp * (1 + qmax)));
@@ -375,6 +422,14 @@ struct Impl final : ImplBase {
     nhat = c.max_iter; rcap = c.max_rank; Tmax = c.max_steps; NX = c.n_space; D = NX * Dp;
     Nmax = c.max_obs > 0 ? std::min<int64_t>(c.max_obs, NX) : NX;
     rtol = c.rtol; ell = c.ell_x; seed = c.seed; reorth = c.reorth != 0;
+    world = std::max(1, c.world); rank = c.rank;
+    if (world > 1) {
+      if (!c.nccl_id || rank < 0 || rank >= world) return fail(CAKF_E_ARG, "multi-GPU: nccl_id and 0 <= rank < world needed");
+      ncclUniqueId id;
+      std::memcpy(&id, c.nccl_id, sizeof(id));
+      const ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+      if (r != ncclSuccess) return fail(CAKF_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
     if (rtol != 0.0) return fail(CAKF_E_UNSUPPORTED, "rtol != 0 is not supported by the device path (R2)");
     std::vector<double> st0;
     if (!fetch_doubles(c.sigma_t0, (size_t)Dp * Dp, st0)) return fail(CAKF_E_ARG, "cannot read sigma_t0");
@@ -530,15 +585,33 @@ struct Impl final : ImplBase {
     for (int i = 1; i <= niter; ++i) {
       // G s  (matrix-free: kernel rows on the fly + low-rank downdate + noise)
       size_t pk = prof_begin();
+      // multi-GPU: this rank evaluates its share of the kernel work (sym units / column chunks),
+      // the rest of the partial buffer is zero, and the reduced vector is all-reduced
+      if (world > 1) CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)nch * N * sizeof(T), st));
       if constexpr (sizeof(T) == 4) {
-        if (sym) CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial), st));
-        else CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
+        if (sym) {
+          const long long U = matvec_sym_units(N);
+          CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
+                                    U * rank / world, U * (rank + 1) / world, st));
+        } else {
+          CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st, nch * rank / world,
+                                           nch * (rank + 1) / world));
+        }
       } else {
-        CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
+        CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st, nch * rank / world,
+                                         nch * (rank + 1) / world));
+      }
+      const T* kpart = partial;
+      int kch = nch;
+      if (world > 1) {
+        CK_CUDA(launch_sum_partials<T>(N, nch, partial, 1.0, yloc, st));
+        CK_NCCL(ncclAllReduce(yloc, yred, (size_t)N, sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, ncclSum, comm, st));
+        kpart = yred;
+        kch = 1;
       }
       prof_end(CAKF_PROF_K1, pk);
       pk = prof_begin();
-      CK_CUDA(StepKernels<T>::stageA(N, nch, partial, sig00, lam2, s, r, gp, HM, rin, part, W, redA, cnt + 0, st));
+      CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, HM, rin, part, W, redA, cnt + 0, st));
       CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 1, st));
       if (reorth && i > 1) {  // CGS2 (R19): d = s - V c, then d -= V (V^T G d)
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W, redC,
@@ -556,7 +629,7 @@ struct Impl final : ImplBase {
     // ---- post-loop: [P^- w, P^- W] = Sigma H^T [v V] - M^- (H M^-)^T [v V]
     const int Cc = 1 + niter;
     size_t pk = prof_begin();
-    CK_CUDA(k2(coords, (int)NX, xcs, N, S.XV, N, Cc, Yb, NX));
+    CK(k2(coords, (int)NX, xcs, N, S.XV, N, Cc, Yb, NX));
     prof_end(CAKF_PROF_K2_POST, pk);
     if (rin) {
       pk = prof_begin();
@@ -658,7 +731,7 @@ struct Impl final : ImplBase {
       if (q) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, q, S.A_next, true, Ws, D, X + D, D, st));
       // Sigma_k x = (Sigma^t_k (x) K) x : K applied to all D' blocks of all C columns at once
       size_t pk = prof_begin();
-      CK_CUDA(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX));
+      CK(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX));
       prof_end(CAKF_PROF_K2_SMOOTH, pk);
       CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, C, S.sig_t, Yk, yb, st));
       const int rin = S.rin, n = S.n, N = S.N;
@@ -781,7 +854,7 @@ int cakf_version(void) { return CAKF_VERSION; }
 int cakf_create(const cakf_config* cfg, cakf_t* out) {
   if (!cfg || !out) return fail(CAKF_E_ARG, "cakf_create: NULL argument");
   *out = nullptr;
-  if (cfg->world != 1 && cfg->world != 0) return fail(CAKF_E_UNSUPPORTED, "cakf_create: world > 1 not in this build");
+  if (cfg->world < 0 || cfg->world > 64) return fail(CAKF_E_ARG, "cakf_create: bad world");
   if (cfg->dtype != CAKF_F32 && cfg->dtype != CAKF_F64) return fail(CAKF_E_ARG, "cakf_create: bad dtype");
   if (cfg->d_time < 1 || cfg->d_time > 3) return fail(CAKF_E_UNSUPPORTED, "cakf_create: d_time must be 1..3");
   if (cfg->n_space < 1 || cfg->n_space > (int64_t)1 << 30) return fail(CAKF_E_ARG, "cakf_create: bad n_space");
@@ -843,6 +916,43 @@ int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset) {
   return h->impl->prof_read(ms, launches, reset != 0);
 }
 int64_t cakf_kernel_launches(void) { return (int64_t)launch_counter(); }
+
+int cakf_nccl_unique_id(void* out) {
+  if (!out) return fail(CAKF_E_ARG, "cakf_nccl_unique_id: NULL");
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(CAKF_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  std::memcpy(out, &id, sizeof(id));
+  return CAKF_OK;
+}
+
+int cakf_shard_plan(int64_t n_space, int64_t n_obs, int32_t world, int32_t rank, int64_t* out) {
+  if (!out || world < 1 || rank < 0 || rank >= world || n_space < 0 || n_obs < 0)
+    return fail(CAKF_E_ARG, "cakf_shard_plan: bad argument");
+  const int64_t per = (n_space + world - 1) / world;
+  const int64_t slice = ((per + 127) / 128) * 128;
+  out[0] = std::min<int64_t>(n_space, slice * rank);
+  out[1] = std::min<int64_t>(n_space, slice * (rank + 1));
+  const long long U = n_obs > 0 ? matvec_sym_units((int)n_obs) : 0;
+  out[2] = U * rank / world;
+  out[3] = U * (rank + 1) / world;
+  out[4] = U;
+  out[5] = slice;
+  return CAKF_OK;
+}
+
+int cakf_sym_unit_blocks(int64_t n_obs, int64_t u, int32_t* bi_out, int32_t* bj_out) {
+  // host mirror of the device unit -> (bi, bj) map of the symmetric K1 (tests of the shard plan)
+  const long long nt = (n_obs + 127) / 128, nb = (nt + 7) / 8;
+  if (u < 0 || u >= nb * (nb + 1) / 2 || !bi_out || !bj_out) return fail(CAKF_E_ARG, "cakf_sym_unit_blocks: bad unit");
+  const double bb = 2.0 * nb + 1.0;
+  long long bi = (long long)std::floor((bb - std::sqrt(bb * bb - 8.0 * (double)u)) * 0.5);
+  while (bi * nb - bi * (bi - 1) / 2 > u) --bi;
+  while ((bi + 1) * nb - (bi + 1) * bi / 2 <= u) ++bi;
+  *bi_out = (int32_t)bi;
+  *bj_out = (int32_t)(bi + (u - (bi * nb - bi * (bi - 1) / 2)));
+  return CAKF_OK;
+}
 int cakf_destroy(cakf_t h) {
   if (!h) return CAKF_OK;
   delete h->impl;
@@ -944,7 +1054,7 @@ int cakf_gram_matmul(int32_t dtype, int32_t spatial_kernel, double ell, int32_t 
       if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)nch * n_rows * sizeof(T), st);
       if (e == cudaSuccess) {
         if constexpr (sizeof(T) == 4) {
-          if (sym) e = launch_matvec_sym(spatial_kernel, cc, (int)n_rows, (float*)part, st);
+          if (sym) e = launch_matvec_sym(spatial_kernel, cc, (int)n_rows, (float*)part, 0, matvec_sym_units((int)n_rows), st);
           else e = launch_matvec_partial<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, nch, part, st);
         } else {
           e = launch_matvec_partial<T>(spatial_kernel, cr, (int)n_rows, cc, (int)n_cols, nch, part, st);

@@ -9,14 +9,17 @@
 namespace cakf {
 
 // ---- K1: kernel matvec partials  partial[ch][i] = sum_{j in chunk ch} k(xr_i, xc_j) * xc_j.w
+// (ch0, ch1): compute only column chunks [ch0, ch1) (multi-GPU shard); ch1 < 0 = all
 template <typename T>
 cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<T>* xc, int ncols,
-                                  int nchunks, T* partial, cudaStream_t st);
+                                  int nchunks, T* partial, cudaStream_t st, int ch0 = 0, int ch1 = -1);
 // choose the number of column chunks for a matvec of this shape (fills the GPU in whole waves)
 int matvec_chunks(int nrows, int ncols, int elem_bytes);
 // symmetric K1 (fp32, one RHS with rows == cols): partial[c][i] for c < matvec_sym_tiles(n)
 int matvec_sym_tiles(int n);
-cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, cudaStream_t st);
+long long matvec_sym_units(int n);   // number of symmetric tile-block work units
+cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
+                              cudaStream_t st);
 bool use_sym_k1();  // false if CAKF_K1_DENSE=1
 // reduce partials: y[i] = alpha * sum_ch partial[ch][i]
 template <typename T>

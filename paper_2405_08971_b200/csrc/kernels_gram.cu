@@ -35,10 +35,10 @@ template <typename T> constexpr int kMaxChunk = sizeof(T) == 4 ? 2048 : 1024;
 template <typename T, int NU2, int R>
 __global__ void __launch_bounds__(kMvThreads)
 matvec_partial_kernel(const V4<T>* __restrict__ xr, int nrows, const V4<T>* __restrict__ xc, int ncols,
-                      int chunk, T* __restrict__ partial) {
+                      int chunk, int ch0, T* __restrict__ partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V4<T>* sc = reinterpret_cast<V4<T>*>(smem_raw);
-  const int ch = blockIdx.y;
+  const int ch = ch0 + blockIdx.y;
   const int j0 = ch * chunk;
   const int n = min(chunk, ncols - j0);
   for (int j = threadIdx.x; j < n; j += kMvThreads) sc[j] = xc[j0 + j];
@@ -85,15 +85,16 @@ constexpr int SYM_T = 128;
 constexpr int SYM_S = 8;
 template <int NU2>
 __global__ void __launch_bounds__(256)
-matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long nunits, float* __restrict__ partial) {
+matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
+                  float* __restrict__ partial) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
   float4* tJ = tI + SYM_S * SYM_T;                                    // [SYM_S][128]
   float* rowacc = reinterpret_cast<float*>(tJ + SYM_S * SYM_T);       // [SYM_S][128]
-  float* colacc = rowacc + SYM_S * SYM_T;                             // [SYM_S][128]
-  float* colred = colacc + SYM_S * SYM_T;                             // [16][132]
+  float* colp = rowacc + SYM_S * SYM_T;                               // [16 ty][SYM_S][128] private slots
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+  float* mycol = colp + ty * SYM_S * SYM_T + tx * 8;                  // this thread's 8 columns of each J tile
+  for (long long u = u_begin + blockIdx.x; u < u_end; u += gridDim.x) {
     // u -> (bi, bj), bi <= bj, row-major over the upper triangle of blocks
     const double bb = 2.0 * nb + 1.0;
     int bi = (int)floor((bb - sqrt(bb * bb - 8.0 * (double)u)) * 0.5);
@@ -108,8 +109,11 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
       tI[e] = gi < n ? x[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
       if (!diag) tJ[e] = gj < n ? x[gj] : make_float4(0.f, 0.f, 0.f, 0.f);
       rowacc[e] = 0.f;
-      colacc[e] = 0.f;
     }
+#pragma unroll
+    for (int b = 0; b < SYM_S; ++b)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) mycol[b * SYM_T + c] = 0.f;
     const float4* sJ = diag ? tI : tJ;
     __syncthreads();
     for (int a = 0; a < na; ++a) {
@@ -137,17 +141,13 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
             cacc[c] = fmaf(k, rs[r], cacc[c]);
           }
         }
-        if (offdiag) {   // column sums of this tile pair -> colacc[b] (fixed order over ty)
-#pragma unroll
-          for (int c = 0; c < 8; ++c) colred[ty * 132 + tx * 8 + c] = cacc[c];
-          __syncthreads();
-          if (tid < SYM_T) {
-            float v = 0.f;
-#pragma unroll
-            for (int t = 0; t < 16; ++t) v += colred[t * 132 + tid];
-            colacc[b * SYM_T + tid] += v;
-          }
-          __syncthreads();
+        if (offdiag) {   // column sums of this tile pair into this thread's private slots (no barrier)
+          float4* m4 = reinterpret_cast<float4*>(mycol + b * SYM_T);
+          float4 u0 = m4[0], u1 = m4[1];
+          u0.x += cacc[0]; u0.y += cacc[1]; u0.z += cacc[2]; u0.w += cacc[3];
+          u1.x += cacc[4]; u1.y += cacc[5]; u1.z += cacc[6]; u1.w += cacc[7];
+          m4[0] = u0;
+          m4[1] = u1;
         }
       }
       // row sums over the unit's J tiles: reduce over tx (16 lanes of a half-warp)
@@ -163,11 +163,14 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
     }
     __syncthreads();
     for (int e = tid; e < SYM_S * SYM_T; e += 256) {
+      float cs_ = 0.f;                       // column sums: fixed-order reduction over the 16 ty slots
+#pragma unroll
+      for (int t = 0; t < 16; ++t) cs_ += colp[t * SYM_S * SYM_T + e];
       const int gi = bi * SYM_S * SYM_T + e;
-      if (gi < n) partial[(size_t)bj * n + gi] = rowacc[e] + (diag ? colacc[e] : 0.f);
+      if (gi < n) partial[(size_t)bj * n + gi] = rowacc[e] + (diag ? cs_ : 0.f);
       if (!diag) {
         const int gj = bj * SYM_S * SYM_T + e;
-        if (gj < n) partial[(size_t)bi * n + gj] = colacc[e];
+        if (gj < n) partial[(size_t)bi * n + gj] = cs_;
       }
     }
   }
@@ -261,13 +264,14 @@ __global__ void prescale_kernel(int n, int dim, const double* __restrict__ xyz, 
 }
 
 template <typename T, int NU2>
-cudaError_t matvec_partial_nu(const V4<T>* xr, int nrows, const V4<T>* xc, int ncols, int nchunks, T* partial,
-                              cudaStream_t st) {
+cudaError_t matvec_partial_nu(const V4<T>* xr, int nrows, const V4<T>* xc, int ncols, int nchunks, int ch0, int ch1,
+                              T* partial, cudaStream_t st) {
   constexpr int R = kRowsPerThread<T>;
   const int chunk = (ncols + nchunks - 1) / nchunks;
-  dim3 grid((nrows + kMvThreads * R - 1) / (kMvThreads * R), nchunks);
+  if (ch1 <= ch0) return cudaSuccess;
+  dim3 grid((nrows + kMvThreads * R - 1) / (kMvThreads * R), ch1 - ch0);
   const size_t smem = (size_t)chunk * sizeof(V4<T>);
-  matvec_partial_kernel<T, NU2, R><<<grid, kMvThreads, smem, st>>>(xr, nrows, xc, ncols, chunk, partial);
+  matvec_partial_kernel<T, NU2, R><<<grid, kMvThreads, smem, st>>>(xr, nrows, xc, ncols, chunk, ch0, partial);
   return note_launch_err();
 }
 
@@ -309,12 +313,13 @@ int matvec_chunks(int nrows, int ncols, int elem_bytes) {
 
 template <typename T>
 cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<T>* xc, int ncols, int nchunks,
-                                  T* partial, cudaStream_t st) {
+                                  T* partial, cudaStream_t st, int ch0, int ch1) {
   if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+  if (ch1 < 0) ch1 = nchunks;
   switch (nu2) {
-    case 1: return matvec_partial_nu<T, 1>(xr, nrows, xc, ncols, nchunks, partial, st);
-    case 3: return matvec_partial_nu<T, 3>(xr, nrows, xc, ncols, nchunks, partial, st);
-    case 5: return matvec_partial_nu<T, 5>(xr, nrows, xc, ncols, nchunks, partial, st);
+    case 1: return matvec_partial_nu<T, 1>(xr, nrows, xc, ncols, nchunks, ch0, ch1, partial, st);
+    case 3: return matvec_partial_nu<T, 3>(xr, nrows, xc, ncols, nchunks, ch0, ch1, partial, st);
+    case 5: return matvec_partial_nu<T, 5>(xr, nrows, xc, ncols, nchunks, ch0, ch1, partial, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -330,14 +335,20 @@ bool use_sym_k1() {
   return v == 1;
 }
 
-cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
+long long matvec_sym_units(int n) {
+  const long long nt = (n + SYM_T - 1) / SYM_T;
+  const long long nb = (nt + SYM_S - 1) / SYM_S;
+  return nb * (nb + 1) / 2;
+}
+
+cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
+                              cudaStream_t st) {
+  if (n <= 0 || u_end <= u_begin) return cudaSuccess;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
-  const long long nunits = (long long)nb * (nb + 1) / 2;
-  const long long grid = std::min<long long>(nunits, (long long)num_sms() * 3);
-  const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)2 * SYM_S * SYM_T * sizeof(float) +
-                      (size_t)16 * 132 * sizeof(float);
+  const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * 2);
+  const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)SYM_S * SYM_T * sizeof(float) +
+                      (size_t)16 * SYM_S * SYM_T * sizeof(float);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(matvec_sym_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -346,9 +357,9 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, c
     configured = true;
   }
   switch (nu2) {
-    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, nunits, partial); break;
-    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, nunits, partial); break;
-    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, nunits, partial); break;
+    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial); break;
+    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial); break;
+    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial); break;
     default: return cudaErrorInvalidValue;
   }
   return note_launch_err();
@@ -382,7 +393,7 @@ cudaError_t launch_prescale_coords(int n, int dim, const double* xyz, double sca
 
 #define INST(T)                                                                                           \
   template cudaError_t launch_matvec_partial<T>(int, const V4<T>*, int, const V4<T>*, int, int, T*,       \
-                                                cudaStream_t);                                            \
+                                                cudaStream_t, int, int);                                  \
   template cudaError_t launch_sum_partials<T>(int, int, const T*, double, T*, cudaStream_t);              \
   template cudaError_t launch_gram_gemm<T>(int, const V4<T>*, int, const V4<T>*, int, const T*, size_t,   \
                                            int, T*, size_t, double, cudaStream_t);                        \

@@ -425,6 +425,16 @@ __global__ void ws_scatter_kernel(int N, size_t D, int n, int q, const int* __re
   else Wf[p + (size_t)(j - 1) * D] -= R[row + (size_t)(j - n) * N];         // - H^T V t_{1:}
 }
 
+// Y[row + c*ldy] = G[p][(row - p*slice) + c*slice] with p = row / slice (all-gathered K2 row slices)
+template <typename T>
+__global__ void assemble_slices_kernel(int M, int C, int slice, const T* __restrict__ G, T* __restrict__ Y, size_t ldy) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)M * C) return;
+  const int row = (int)(e % M), c = (int)(e / M);
+  const int p = row / slice;
+  Y[row + (size_t)c * ldy] = G[(size_t)p * slice * C + (row - (size_t)p * slice) + (size_t)c * slice];
+}
+
 template <typename S, typename D_>
 __global__ void convert_kernel(int rows, int cols, const S* __restrict__ src, size_t lds, D_* __restrict__ dst, size_t ldd) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -582,6 +592,13 @@ cudaError_t StepKernels<T>::ws_build(int N, size_t D, int n, int q, const int* i
   cudaError_t e = note_launch_err();
   if (e != cudaSuccess || N == 0) return e;
   ws_scatter_kernel<T><<<nblk((size_t)N * (n + q + 1)), 256, 0, st>>>(N, D, n, q, idx, XV, R, Wf, ws);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::assemble_slices(int M, int C, int slice, const T* G, T* Y, size_t ldy, cudaStream_t st) {
+  if ((size_t)M * C == 0) return cudaSuccess;
+  assemble_slices_kernel<T><<<nblk((size_t)M * C), 256, 0, st>>>(M, C, slice, G, Y, ldy);
   return note_launch_err();
 }
 

@@ -55,6 +55,7 @@ struct StepKernels {
   static cudaError_t ws_build(int N, size_t D, int n, int q, const int* idx, const T* X, const T* XV, const T* R,
                               T* Wf, T* ws, cudaStream_t st);
   static cudaError_t fill(size_t n, T val, T* out, cudaStream_t st);
+  static cudaError_t assemble_slices(int M, int C, int slice, const T* G, T* Y, size_t ldy, cudaStream_t st);
 };
 
 }  // namespace cakf
