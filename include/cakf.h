@@ -99,7 +99,7 @@ typedef struct {
   int32_t max_steps;        /* T: number of time steps the trace is sized for                */
   int64_t max_obs;          /* max N_k over the run (0 = n_space)                            */
   int32_t rank;             /* multi-GPU rank (0 for a single GPU)                           */
-  int32_t world;            /* number of ranks; 1 = single GPU (only value in this build)    */
+  int32_t world;            /* number of ranks (1 = single GPU); > 1 shards the Gram products */
   const void* nccl_id;      /* 128-byte ncclUniqueId when world > 1, else NULL               */
   void* stream;             /* cudaStream_t to enqueue on, or NULL                           */
 } cakf_config;
@@ -176,7 +176,10 @@ enum cakf_prof_category {
   CAKF_PROF_STAGES = 3,     /* inner-loop reduction / update stages (a5, a6)           */
   CAKF_PROF_TRUNCATE = 4,   /* Gram + eigendecomposition + M Q_r (a8, smoother too)    */
   CAKF_PROF_LOWRANK = 5,    /* low-rank fp64-accumulated contractions (a7, a9)         */
-  CAKF_PROF_NCAT = 6
+  CAKF_PROF_TRUNC_GRAM = 6, /* ... of which: the Gram matrix F^T F                      */
+  CAKF_PROF_TRUNC_EIG = 7,  /* ... of which: the symmetric eigendecomposition            */
+  CAKF_PROF_TRUNC_GEMM = 8, /* ... of which: F Q_r                                       */
+  CAKF_PROF_NCAT = 9
 };
 int cakf_profile(cakf_t h, int32_t enable);
 int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset);
@@ -196,8 +199,9 @@ int64_t cakf_kernel_launches(void);
  * and pass it as cfg.nccl_id). */
 int cakf_nccl_unique_id(void* out128);
 
-/* Host-only: the shard of rank `rank` of `world`: out[0..5] = {row_lo, row_hi, u_lo, u_hi,
- * n_units, slice_rows} for n_space points and n_obs observations. */
+/* Host-only: the shard of rank `rank` of `world`: out[0..6] = {row_lo, row_hi, u_lo, u_hi,
+ * n_units, slice_rows, block_points} for n_space points and n_obs observations (a K1 unit is a
+ * pair of blocks of block_points consecutive observations). */
 int cakf_shard_plan(int64_t n_space, int64_t n_obs, int32_t world, int32_t rank, int64_t* out);
 
 /* Host-only mirror of the symmetric K1's unit -> (tile block i, tile block j) map, i <= j. */

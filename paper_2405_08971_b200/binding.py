@@ -62,7 +62,8 @@ EXPORTS = [
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
     "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks",
 ]
-PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank"]
+PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank", "trunc_gram",
+                   "trunc_eig", "trunc_gemm"]
 
 _lib = None
 
@@ -135,9 +136,10 @@ def nccl_unique_id() -> bytes:
 
 def shard_plan(n_space: int, n_obs: int, world: int, rank: int) -> dict:
     """Rows of the K2 output and units of the symmetric K1 owned by `rank` (host-only)."""
-    out = np.zeros(6, dtype=np.int64)
+    out = np.zeros(7, dtype=np.int64)
     _check(load().cakf_shard_plan(int(n_space), int(n_obs), int(world), int(rank), out.ctypes.data))
-    return dict(zip(["row_lo", "row_hi", "u_lo", "u_hi", "n_units", "slice_rows"], (int(v) for v in out)))
+    return dict(zip(["row_lo", "row_hi", "u_lo", "u_hi", "n_units", "slice_rows", "block_points"],
+                    (int(v) for v in out)))
 
 
 def sym_unit_blocks(n_obs: int, unit: int):

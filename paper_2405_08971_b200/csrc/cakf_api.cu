@@ -18,6 +18,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -214,6 +215,42 @@ struct Impl final : ImplBase {
   T *Wf = nullptr, *Ws = nullptr, *ws = nullptr, *pvar = nullptr;
   float* tcw = nullptr;  // bf16 planes of the K2 right-hand sides
 
+  // ---------------- internal point order (spatially compact tiles for the fused kernels)
+  int *perm_d = nullptr, *invperm_d = nullptr;   // internal -> user, user -> internal
+  int *posof = nullptr, *obs_cnt = nullptr, *sigma = nullptr, *sigma_inv = nullptr;
+  T *ybuf_user = nullptr, *lam2_user = nullptr, *outm = nullptr, *outv = nullptr;
+  std::vector<int> perm_h;
+
+  // Morton (Z-order) of the quantised coordinates: consecutive points are spatially close, so
+  // 128-point tiles of the Gram kernels are compact (CAKF_NO_REORDER=1 keeps the user order).
+  void make_perm(const std::vector<double>& xyz) {
+    perm_h.resize(NX);
+    for (int64_t i = 0; i < NX; ++i) perm_h[i] = (int)i;
+    const char* e = getenv("CAKF_NO_REORDER");
+    if (e && e[0] == '1') return;
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int d = 0; d < dim; ++d) {
+      lo[d] = hi[d] = xyz[d];
+      for (int64_t i = 0; i < NX; ++i) {
+        lo[d] = std::min(lo[d], xyz[i * dim + d]);
+        hi[d] = std::max(hi[d], xyz[i * dim + d]);
+      }
+    }
+    std::vector<uint64_t> key(NX);
+    for (int64_t i = 0; i < NX; ++i) {
+      uint64_t k = 0;
+      uint32_t q[3] = {0, 0, 0};
+      for (int d = 0; d < dim; ++d) {
+        const double span = hi[d] - lo[d];
+        q[d] = span > 0 ? (uint32_t)std::min(2097151.0, (xyz[i * dim + d] - lo[d]) / span * 2097151.0) : 0u;
+      }
+      for (int b = 20; b >= 0; --b)
+        for (int d = 0; d < 3; ++d) k = (k << 1) | ((q[d] >> b) & 1u);
+      key[i] = k;
+    }
+    std::stable_sort(perm_h.begin(), perm_h.end(), [&](int a, int b) { return key[a] < key[b]; });
+  }
+
   // ---------------- multi-GPU: the Gram products are sharded, the rest replicated
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -402,6 +439,16 @@ struct Impl final : ImplBase {
     Ws = carve<T>((size_t)D * (nhat + qmax));
     ws = carve<T>(D);
     pvar = carve<T>(D);
+    perm_d = carve<int>(NX);
+    invperm_d = carve<int>(NX);
+    posof = carve<int>(NX);
+    obs_cnt = carve<int>((NX + 1023) / 1024 + 1);
+    sigma = carve<int>(Nmax);
+    sigma_inv = carve<int>(Nmax);
+    ybuf_user = carve<T>(Nmax);
+    lam2_user = carve<T>(Nmax);
+    outm = carve<T>(D);
+    outv = carve<T>(D);
     if (world > 1) {
       yloc = carve<T>(Nmax);
       yred = carve<T>(Nmax);
@@ -464,14 +511,26 @@ struct Impl final : ImplBase {
     std::memset(ctl_init_host, 0, sizeof(IterCtl));
     ctl_init_host->eta_min = INFINITY;
     // coordinates: copy (host or device doubles) and prescale by sqrt(2 nu)/ell
+    std::vector<double> xyz;
+    if (!fetch_doubles(c.coords, (size_t)NX * dim, xyz)) return fail(CAKF_E_ARG, "cannot read coords");
+    make_perm(xyz);
+    std::vector<int> inv(NX);
+    std::vector<double> xyz_int((size_t)NX * dim);
+    for (int64_t i = 0; i < NX; ++i) {
+      inv[perm_h[i]] = (int)i;
+      for (int d = 0; d < dim; ++d) xyz_int[i * dim + d] = xyz[(size_t)perm_h[i] * dim + d];
+    }
+    CK_CUDA(cudaMemcpyAsync(perm_d, perm_h.data(), NX * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(invperm_d, inv.data(), NX * sizeof(int), cudaMemcpyHostToDevice, st));
     double* dxyz = reinterpret_cast<double*>(stage64);
-    CK_CUDA(cudaMemcpyAsync(dxyz, c.coords, (size_t)NX * dim * sizeof(double), cudaMemcpyDefault, st));
+    CK_CUDA(cudaMemcpyAsync(dxyz, xyz_int.data(), (size_t)NX * dim * sizeof(double), cudaMemcpyHostToDevice, st));
     CK_CUDA(launch_prescale_coords<T>((int)NX, dim, dxyz, std::sqrt((double)nu2) / ell, coords, st));
     std::vector<T> mu(D, T(0));
     if (c.mu0) {
       std::vector<double> m0;
       if (!fetch_doubles(c.mu0, D, m0)) return fail(CAKF_E_ARG, "cannot read mu0");
-      for (int64_t i = 0; i < D; ++i) mu[i] = (T)m0[i];
+      for (int d = 0; d < Dp; ++d)
+        for (int64_t i = 0; i < NX; ++i) mu[d * NX + i] = (T)m0[d * NX + perm_h[i]];
     }
     CK_CUDA(cudaMemcpyAsync(mu0, mu.data(), D * sizeof(T), cudaMemcpyHostToDevice, st));
     CK_CUDA(cudaStreamSynchronize(st));
@@ -509,8 +568,9 @@ struct Impl final : ImplBase {
     P.A_next = A;
     S.sig_t = mat_abat_plus_q(A, P.sig_t, Q, Dp);                     // Sigma^t_k
     CK_CUDA(StepKernels<T>::mix((int)NX, Dp, 1, A, false, P.m, D, S.m_pred, D, st));   // m^- = A m
-    if (b) {
-      CK_CUDA(cudaMemcpyAsync(tmp, b, D * sizeof(T), cudaMemcpyDefault, st));
+    if (b) {   // user point order -> internal order (unpermute with the inverse permutation)
+      CK_CUDA(cudaMemcpyAsync(outm, b, D * sizeof(T), cudaMemcpyDefault, st));
+      CK_CUDA(unpermute<T>((int)NX, Dp, invperm_d, outm, tmp, st));
       CK_BLAS(Blas<T>::axpy(blas, (int)D, T(1), tmp, S.m_pred));
     }
     const T* src = P.truncated ? Mtil : P.Mk;
@@ -563,19 +623,23 @@ struct Impl final : ImplBase {
     S.n = niter;
     S.missing = false;
     // ---- stage inputs (host or device pointers)
+    // observations in internal point order: S.idx ascending, sigma[j] = the user's position
     CK_CUDA(cudaMemcpyAsync(stage64, obs_idx, (size_t)N * sizeof(int64_t), cudaMemcpyDefault, st));
-    CK_CUDA(idx64_to32(N, stage64, S.idx, st));
-    CK_CUDA(cudaMemcpyAsync(ybuf, y, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
-    CK_CUDA(cudaMemcpyAsync(lam2, noise_var, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
+    CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, S.idx, sigma, sigma_inv, st));
+    CK_CUDA(cudaMemcpyAsync(ybuf_user, y, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
+    CK_CUDA(cudaMemcpyAsync(lam2_user, noise_var, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
+    CK_CUDA(gather_vec<T>(N, sigma, ybuf_user, ybuf, st));
+    CK_CUDA(gather_vec<T>(N, sigma, lam2_user, lam2, st));
     if (policy == CAKF_POLICY_COORD && niter > 0) {
       CK_CUDA(cudaMemcpyAsync(stage64, coord_order, (size_t)niter * sizeof(int64_t), cudaMemcpyDefault, st));
-      CK_CUDA(idx64_to32(niter, stage64, order32, st));
+      CK_CUDA(map_order(niter, stage64, sigma_inv, order32, st));
     }
     const int rin = S.rin;
     IterCtl* C = &ctl[k];
     // ---- H M^- (N x rin) and r^(0), first action
     if (rin) CK_CUDA(StepKernels<T>::gather_rows(N, rin, S.idx, S.Mk, D, HM, N, st));
-    CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, S.m_pred, policy, order32, seed, k, r, s, S.XV, xcs, st));
+    CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, S.m_pred, policy, order32, seed, k, sigma, r, s, S.XV, xcs,
+                                 st));
     const double sig00 = S.sig_t.a[0][0];
     const double eps = sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON;
     const bool sym = sizeof(T) == 4 && use_sym_k1();
@@ -622,7 +686,7 @@ struct Impl final : ImplBase {
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W,
                                        nullptr, cnt + 2, C, eps, i, 0, st));
       }
-      CK_CUDA(StepKernels<T>::stageD(N, i, niter, C, d, Gd, S.XV, Z, r, s, xcs, policy, order32, seed, k, st));
+      CK_CUDA(StepKernels<T>::stageD(N, i, niter, C, d, Gd, S.XV, Z, r, s, xcs, policy, order32, seed, k, sigma, st));
       prof_end(CAKF_PROF_STAGES, pk);
     }
     CK_CUDA(StepKernels<T>::dot(N, r, r, part, &C->res_sq, cnt + 3, st));
@@ -683,12 +747,31 @@ struct Impl final : ImplBase {
 
   // Truncate a D x c factor F (ld D) to its top-r Gram eigen-directions: out = F Q_r.
   int truncate_factor(const T* F, int c, int rkeep, T* out, double* kept, double* dropped) {
-    const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit_max, D / 4096));
     const size_t pk = prof_begin();
-    CK_CUDA(StepKernels<T>::gram(D, c, F, D, gpart, nsplit, Gm, st));
+    // fp64 copy of F (fp32 storage) feeds both the Gram (DSYRK, fp64 tensor cores) and M Q_r (DGEMM)
+    const double* Fd = reinterpret_cast<const double*>(F);
+    if constexpr (sizeof(T) == 4) {
+      if ((size_t)D * c > dscr) return fail(CAKF_E_ARG, "truncate: fp64 scratch too small");
+      CK_CUDA((convert<float, double>)((int)D, c, reinterpret_cast<const float*>(F), D, dA, D, st));
+      Fd = dA;
+    }
+    const double one = 1.0, zero = 0.0;
+    size_t ps = prof_begin();
+    CK_BLAS(cublasDsyrk(blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, c, (int)D, &one, Fd, (int)D, &zero, Gm, c));
+    prof_end(CAKF_PROF_TRUNC_GRAM, ps);
+    ps = prof_begin();
     CK_SOLVER(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, c, Gm, c, eigw, work, lwork, info));
     CK_CUDA(StepKernels<double>::take_top(c, rkeep, Gm, eigw, QrD, kept, dropped, st));
-    CK(gemm_impl(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, QrD, c, 0.0, out, (int)D));
+    prof_end(CAKF_PROF_TRUNC_EIG, ps);
+    ps = prof_begin();
+    if constexpr (sizeof(T) == 4) {
+      CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one, Fd, (int)D, QrD, c, &zero, dC, (int)D));
+      CK_CUDA((convert<double, float>)((int)D, rkeep, dC, D, reinterpret_cast<float*>(out), D, st));
+    } else {
+      CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one, Fd, (int)D, QrD, c, &zero,
+                          reinterpret_cast<double*>(out), (int)D));
+    }
+    prof_end(CAKF_PROF_TRUNC_GEMM, ps);
     prof_end(CAKF_PROF_TRUNCATE, pk);
     return CAKF_OK;
   }
@@ -789,8 +872,15 @@ struct Impl final : ImplBase {
     } else {
       return fail(CAKF_E_ARG, "get: bad which");
     }
-    if (mean) CK_CUDA(cudaMemcpyAsync(mean, pm, D * sizeof(T), cudaMemcpyDefault, st));
-    if (var) CK_CUDA(cudaMemcpyAsync(var, pv, D * sizeof(T), cudaMemcpyDefault, st));
+    // internal -> user point order
+    if (mean) {
+      CK_CUDA(unpermute<T>((int)NX, Dp, perm_d, pm, outm, st));
+      CK_CUDA(cudaMemcpyAsync(mean, outm, D * sizeof(T), cudaMemcpyDefault, st));
+    }
+    if (var) {
+      CK_CUDA(unpermute<T>((int)NX, Dp, perm_d, pv, outv, st));
+      CK_CUDA(cudaMemcpyAsync(var, outv, D * sizeof(T), cudaMemcpyDefault, st));
+    }
     CK_CUDA(cudaStreamSynchronize(st));
     return CAKF_OK;
   }
@@ -938,12 +1028,13 @@ int cakf_shard_plan(int64_t n_space, int64_t n_obs, int32_t world, int32_t rank,
   out[3] = U * (rank + 1) / world;
   out[4] = U;
   out[5] = slice;
+  out[6] = matvec_sym_block_points();
   return CAKF_OK;
 }
 
 int cakf_sym_unit_blocks(int64_t n_obs, int64_t u, int32_t* bi_out, int32_t* bj_out) {
   // host mirror of the device unit -> (bi, bj) map of the symmetric K1 (tests of the shard plan)
-  const long long nt = (n_obs + 127) / 128, nb = (nt + 7) / 8;
+  const long long bp = matvec_sym_block_points(), nb = (n_obs + bp - 1) / bp;
   if (u < 0 || u >= nb * (nb + 1) / 2 || !bi_out || !bj_out) return fail(CAKF_E_ARG, "cakf_sym_unit_blocks: bad unit");
   const double bb = 2.0 * nb + 1.0;
   long long bi = (long long)std::floor((bb - std::sqrt(bb * bb - 8.0 * (double)u)) * 0.5);

@@ -18,6 +18,7 @@ int matvec_chunks(int nrows, int ncols, int elem_bytes);
 // symmetric K1 (fp32, one RHS with rows == cols): partial[c][i] for c < matvec_sym_tiles(n)
 int matvec_sym_tiles(int n);
 long long matvec_sym_units(int n);   // number of symmetric tile-block work units
+int matvec_sym_block_points();       // points per tile block of the symmetric K1
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
                               cudaStream_t st);
 bool use_sym_k1();  // false if CAKF_K1_DENSE=1

@@ -82,7 +82,7 @@ matvec_partial_kernel(const V4<T>* __restrict__ xr, int nrows, const V4<T>* __re
 // partial per block and stage A's fixed-order sum over the nb blocks reduces them
 // (deterministic, no atomics).
 constexpr int SYM_T = 128;
-constexpr int SYM_S = 8;
+constexpr int SYM_S = 4;
 template <int NU2>
 __global__ void __launch_bounds__(256)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
@@ -335,6 +335,8 @@ bool use_sym_k1() {
   return v == 1;
 }
 
+int matvec_sym_block_points() { return SYM_S * SYM_T; }
+
 long long matvec_sym_units(int n) {
   const long long nt = (n + SYM_T - 1) / SYM_T;
   const long long nb = (nt + SYM_S - 1) / SYM_S;
@@ -346,7 +348,7 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
   if (n <= 0 || u_end <= u_begin) return cudaSuccess;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
-  const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * 2);
+  const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * 3);
   const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)SYM_S * SYM_T * sizeof(float) +
                       (size_t)16 * SYM_S * SYM_T * sizeof(float);
   static bool configured = false;

@@ -29,12 +29,38 @@ template <typename T>
 __device__ void block_cols_dot(const T* __restrict__ A, size_t ld, int ncols, const T* __restrict__ v, int r0, int r1,
                                double* __restrict__ out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = warp; j < ncols; j += nw) {
-    const T* col = A + (size_t)j * ld;
+  // four columns per warp pass: 4 independent accumulators keep 4x the loads in flight
+  int j = 4 * warp;
+  for (; j + 3 < ncols; j += 4 * nw) {
+    const T* c0 = A + (size_t)j * ld;
+    const T* c1 = c0 + ld;
+    const T* c2 = c1 + ld;
+    const T* c3 = c2 + ld;
+    T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+    for (int row = r0 + lane; row < r1; row += 32) {
+      const T x = v[row];
+      a0 = fma(c0[row], x, a0);
+      a1 = fma(c1[row], x, a1);
+      a2 = fma(c2[row], x, a2);
+      a3 = fma(c3[row], x, a3);
+    }
+    const double s0 = warp_sum((double)a0), s1 = warp_sum((double)a1);
+    const double s2 = warp_sum((double)a2), s3 = warp_sum((double)a3);
+    if (lane == 0) {
+      out[j] = s0;
+      out[j + 1] = s1;
+      out[j + 2] = s2;
+      out[j + 3] = s3;
+    }
+  }
+  // remaining columns (ncols % 4), one per warp
+  const int jt = ncols & ~3;
+  for (int jj = jt + warp; jj < ncols; jj += nw) {
+    const T* col = A + (size_t)jj * ld;
     T acc = T(0);
     for (int row = r0 + lane; row < r1; row += 32) acc = fma(col[row], v[row], acc);
     const double s = warp_sum((double)acc);
-    if (lane == 0) out[j] = s;
+    if (lane == 0) out[jj] = s;
   }
 }
 
@@ -50,7 +76,8 @@ __device__ void finalize_sum(int nb, int W, int n, const double* part, double* r
 template <typename T>
 __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __restrict__ coords, const T* __restrict__ y,
                             const T* __restrict__ mpred, int policy, const int* __restrict__ order, uint64_t seed, int k,
-                            T* __restrict__ r, T* __restrict__ s, T* __restrict__ v, V4<T>* __restrict__ xcs) {
+                            const int* __restrict__ sigma, T* __restrict__ r, T* __restrict__ s, T* __restrict__ v,
+                            V4<T>* __restrict__ xcs) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= N) return;
   const int p = idx[row];
@@ -58,7 +85,7 @@ __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __r
   T s0;
   if (policy == 0) s0 = r0;                            // CG: s_1 = r^(1) = r^(0)  (R1)
   else if (policy == 1) s0 = (order[0] == row) ? T(1) : T(0);
-  else s0 = (T)philox_normal(seed, (uint32_t)k, 1u, (uint32_t)row);
+  else s0 = (T)philox_normal(seed, (uint32_t)k, 1u, (uint32_t)(sigma ? sigma[row] : row));   // R16: user position
   r[row] = r0;
   s[row] = s0;
   v[row] = T(0);
@@ -199,7 +226,7 @@ template <typename T>
 __global__ void stageD_kernel(int N, int iter, int niter, const IterCtl* __restrict__ ctl, const T* __restrict__ d,
                               const T* __restrict__ Gd, T* __restrict__ XV, T* __restrict__ Z, T* __restrict__ r,
                               T* __restrict__ s, V4<T>* __restrict__ xcs, int policy, const int* __restrict__ order,
-                              uint64_t seed, int k) {
+                              uint64_t seed, int k, const int* __restrict__ sigma) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= N) return;
   const T gamma = (T)ctl->gamma, isq = (T)ctl->inv_sqrt_eta;
@@ -213,7 +240,7 @@ __global__ void stageD_kernel(int N, int iter, int niter, const IterCtl* __restr
     T sn;
     if (policy == 0) sn = rn;
     else if (policy == 1) sn = (order[iter] == row) ? T(1) : T(0);
-    else sn = (T)philox_normal(seed, (uint32_t)k, (uint32_t)(iter + 1), (uint32_t)row);
+    else sn = (T)philox_normal(seed, (uint32_t)k, (uint32_t)(iter + 1), (uint32_t)(sigma ? sigma[row] : row));
     s[row] = sn;
     xcs[row].w = sn;
   }
@@ -435,6 +462,74 @@ __global__ void assemble_slices_kernel(int M, int C, int slice, const T* __restr
   Y[row + (size_t)c * ldy] = G[(size_t)p * slice * C + (row - (size_t)p * slice) + (size_t)c * slice];
 }
 
+// ---- observation sort: internal index order (spatially compact tiles), fully on device
+__global__ void obs_mark_kernel(int N, const int64_t* __restrict__ obs, const int* __restrict__ invperm,
+                                int* __restrict__ posof) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < N) posof[invperm[obs[j]]] = j;
+}
+__global__ void obs_count_kernel(int NX, const int* __restrict__ posof, int* __restrict__ counts) {
+  __shared__ int wsum[32];
+  const int i = blockIdx.x * 1024 + threadIdx.x;
+  const unsigned b = __ballot_sync(0xffffffffu, i < NX && posof[i] >= 0);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 32; ++w) t += wsum[w];
+    counts[blockIdx.x] = t;
+  }
+}
+__global__ void obs_scan_kernel(int nb, int* __restrict__ counts) {   // one thread: exclusive scan, nb <= ~1k
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int run = 0;
+  for (int b = 0; b < nb; ++b) {
+    const int c = counts[b];
+    counts[b] = run;
+    run += c;
+  }
+}
+__global__ void obs_scatter_kernel(int NX, const int* __restrict__ posof, const int* __restrict__ offsets,
+                                   int* __restrict__ idx_out, int* __restrict__ sigma, int* __restrict__ sigma_inv) {
+  __shared__ int wpre[33];
+  const int i = blockIdx.x * 1024 + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int p = i < NX ? posof[i] : -1;
+  const unsigned b = __ballot_sync(0xffffffffu, p >= 0);
+  if (lane == 0) wpre[w + 1] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    wpre[0] = 0;
+    for (int k = 1; k <= 32; ++k) wpre[k] += wpre[k - 1];
+  }
+  __syncthreads();
+  if (p >= 0) {
+    const int dst = offsets[blockIdx.x] + wpre[w] + __popc(b & ((1u << lane) - 1u));
+    idx_out[dst] = i;
+    sigma[dst] = p;
+    sigma_inv[p] = dst;
+  }
+}
+template <typename T>
+__global__ void gather_vec_kernel(int N, const int* __restrict__ sigma, const T* __restrict__ in, T* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < N) out[j] = in[sigma[j]];
+}
+__global__ void map_order_kernel(int n, const int64_t* __restrict__ order_user, const int* __restrict__ sigma_inv,
+                                 int* __restrict__ order_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) order_out[i] = sigma_inv[order_user[i]];
+}
+// out[d*NX + perm[i]] = in[d*NX + i]   (internal -> user point order)
+template <typename T>
+__global__ void unpermute_kernel(int NX, int Dp, const int* __restrict__ perm, const T* __restrict__ in,
+                                 T* __restrict__ out) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)NX * Dp) return;
+  const int i = (int)(e % NX), d = (int)(e / NX);
+  out[(size_t)d * NX + perm[i]] = in[e];
+}
+
 template <typename S, typename D_>
 __global__ void convert_kernel(int rows, int cols, const S* __restrict__ src, size_t lds, D_* __restrict__ dst, size_t ldd) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -467,9 +562,10 @@ int rows_per_block(int N) {
 
 template <typename T>
 cudaError_t StepKernels<T>::prep(int N, const int* idx, const V4<T>* coords, const T* y, const T* mpred, int policy,
-                                 const int* order, uint64_t seed, int k, T* r, T* s, T* v, V4<T>* xcs, cudaStream_t st) {
+                                 const int* order, uint64_t seed, int k, const int* sigma, T* r, T* s, T* v, V4<T>* xcs,
+                                 cudaStream_t st) {
   if (N <= 0) return cudaSuccess;
-  prep_kernel<T><<<nblk(N), 256, 0, st>>>(N, idx, coords, y, mpred, policy, order, seed, k, r, s, v, xcs);
+  prep_kernel<T><<<nblk(N), 256, 0, st>>>(N, idx, coords, y, mpred, policy, order, seed, k, sigma, r, s, v, xcs);
   return note_launch_err();
 }
 
@@ -506,8 +602,9 @@ cudaError_t StepKernels<T>::stageC(int N, const T* V, const T* Z, int nV, const 
 template <typename T>
 cudaError_t StepKernels<T>::stageD(int N, int iter, int niter, const IterCtl* ctl, const T* d, const T* Gd, T* XV,
                                    T* Z, T* r, T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k,
-                                   cudaStream_t st) {
-  stageD_kernel<T><<<nblk(N), 256, 0, st>>>(N, iter, niter, ctl, d, Gd, XV, Z, r, s, xcs, policy, order, seed, k);
+                                   const int* sigma, cudaStream_t st) {
+  stageD_kernel<T><<<nblk(N), 256, 0, st>>>(N, iter, niter, ctl, d, Gd, XV, Z, r, s, xcs, policy, order, seed, k,
+                                            sigma);
   return note_launch_err();
 }
 
@@ -618,6 +715,45 @@ cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_
 template cudaError_t convert<float, double>(int, int, const float*, size_t, double*, size_t, cudaStream_t);
 template cudaError_t convert<double, float>(int, int, const double*, size_t, float*, size_t, cudaStream_t);
 template cudaError_t convert<double, double>(int, int, const double*, size_t, double*, size_t, cudaStream_t);
+
+cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int* posof, int* counts, int* idx_out,
+                     int* sigma, int* sigma_inv, cudaStream_t st) {
+  if (N <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(posof, 0xff, (size_t)NX * sizeof(int), st);   // -1
+  if (e != cudaSuccess) return e;
+  obs_mark_kernel<<<nblk(N), 256, 0, st>>>(N, obs, invperm, posof);
+  if ((e = note_launch_err()) != cudaSuccess) return e;
+  const int nb = (NX + 1023) / 1024;
+  obs_count_kernel<<<nb, 1024, 0, st>>>(NX, posof, counts);
+  if ((e = note_launch_err()) != cudaSuccess) return e;
+  obs_scan_kernel<<<1, 32, 0, st>>>(nb, counts);
+  if ((e = note_launch_err()) != cudaSuccess) return e;
+  obs_scatter_kernel<<<nb, 1024, 0, st>>>(NX, posof, counts, idx_out, sigma, sigma_inv);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t gather_vec(int N, const int* sigma, const T* in, T* out, cudaStream_t st) {
+  if (N <= 0) return cudaSuccess;
+  gather_vec_kernel<T><<<nblk(N), 256, 0, st>>>(N, sigma, in, out);
+  return note_launch_err();
+}
+template cudaError_t gather_vec<float>(int, const int*, const float*, float*, cudaStream_t);
+template cudaError_t gather_vec<double>(int, const int*, const double*, double*, cudaStream_t);
+
+cudaError_t map_order(int n, const int64_t* order_user, const int* sigma_inv, int* order_out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  map_order_kernel<<<nblk(n), 256, 0, st>>>(n, order_user, sigma_inv, order_out);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t unpermute(int NX, int Dp, const int* perm, const T* in, T* out, cudaStream_t st) {
+  unpermute_kernel<T><<<nblk((size_t)NX * Dp), 256, 0, st>>>(NX, Dp, perm, in, out);
+  return note_launch_err();
+}
+template cudaError_t unpermute<float>(int, int, const int*, const float*, float*, cudaStream_t);
+template cudaError_t unpermute<double>(int, int, const int*, const double*, double*, cudaStream_t);
 
 cudaError_t idx64_to32(int n, const int64_t* in, int* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

@@ -20,13 +20,22 @@ struct IterCtl {
 
 int rows_per_block(int N);
 cudaError_t idx64_to32(int n, const int64_t* in, int* out, cudaStream_t st);
+// observations -> internal point order: idx_out ascending, sigma[j] = user position, sigma_inv inverse
+cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int* posof, int* counts, int* idx_out,
+                     int* sigma, int* sigma_inv, cudaStream_t st);
+template <typename T>
+cudaError_t gather_vec(int N, const int* sigma, const T* in, T* out, cudaStream_t st);
+cudaError_t map_order(int n, const int64_t* order_user, const int* sigma_inv, int* order_out, cudaStream_t st);
+template <typename T>
+cudaError_t unpermute(int NX, int Dp, const int* perm, const T* in, T* out, cudaStream_t st);
 template <typename S, typename D_>
 cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_t ldd, cudaStream_t st);
 
 template <typename T>
 struct StepKernels {
   static cudaError_t prep(int N, const int* idx, const V4<T>* coords, const T* y, const T* mpred, int policy,
-                          const int* order, uint64_t seed, int k, T* r, T* s, T* v, V4<T>* xcs, cudaStream_t st);
+                          const int* order, uint64_t seed, int k, const int* sigma, T* r, T* s, T* v, V4<T>* xcs,
+                          cudaStream_t st);
   static cudaError_t stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s, const T* r,
                             T* gp, const T* HM, int rin, double* part, int W, double* red, unsigned* cnt,
                             cudaStream_t st);
@@ -37,7 +46,8 @@ struct StepKernels {
                             int W, double* red, unsigned* cnt, IterCtl* ctl, double eps, int iter, int pass,
                             cudaStream_t st);
   static cudaError_t stageD(int N, int iter, int niter, const IterCtl* ctl, const T* d, const T* Gd, T* XV, T* Z, T* r,
-                            T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k, cudaStream_t st);
+                            T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k, const int* sigma,
+                            cudaStream_t st);
   static cudaError_t dot(int N, const T* a, const T* b, double* part, double* out, unsigned* cnt, cudaStream_t st);
   static cudaError_t gather_rows(int N, int C, const int* idx, const T* M, size_t ldm, T* out, size_t ldo,
                                  cudaStream_t st);

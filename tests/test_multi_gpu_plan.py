@@ -39,9 +39,11 @@ def test_shard_plan_covers_everything_once(n_space, n_obs, world):
 
 @pytest.mark.parametrize("n_obs", [1, 1024, 1025, 5580, 87120])
 def test_sym_units_enumerate_block_pairs_once(n_obs):
-    nt = (n_obs + 127) // 128
-    nb = (nt + 7) // 8
-    U = binding.shard_plan(1, n_obs, 1, 0)["n_units"]
+    plan = binding.shard_plan(1, n_obs, 1, 0)
+    bp = plan["block_points"]
+    assert bp % 128 == 0
+    nb = (n_obs + bp - 1) // bp
+    U = plan["n_units"]
     assert U == nb * (nb + 1) // 2
     seen = set()
     for u in range(U):
@@ -66,11 +68,11 @@ def _worker(rank, world, port, X, s, B, nu, ell, out_q):
     plan = binding.shard_plan(n, n, world, rank)
     # K1: this rank's symmetric units -> partial N-vector, then all-reduce
     y = np.zeros(n)
-    T, S = 128, 8
+    bp = plan["block_points"]
     for u in range(plan["u_lo"], plan["u_hi"]):
         bi, bj = binding.sym_unit_blocks(n, u)
-        I = slice(bi * S * T, min(n, (bi + 1) * S * T))
-        J = slice(bj * S * T, min(n, (bj + 1) * S * T))
+        I = slice(bi * bp, min(n, (bi + 1) * bp))
+        J = slice(bj * bp, min(n, (bj + 1) * bp))
         if bi == bj:
             y[I] += mfree.gram_apply(X[I], X[I], s[I], nu, ell)
         else:
