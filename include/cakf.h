@@ -95,6 +95,9 @@ typedef struct {
   double rtol;              /* stop once ||r|| <= rtol ||r0||; 0 = count-only (R2, default)   */
   int32_t reorth;           /* 1 = second Gram-Schmidt pass d -= V V^T G d (CGS2, R19); 0 = the
                                single classical pass of alg:update_pls line 11 as printed      */
+  int32_t cull_zero;        /* 1 = exact-zero culling (fp32 only): skip kernel tiles whose every
+                               value underflows to exactly 0 in fp32 (bounding-sphere distance in
+                               prescaled units > 88); results are bit-identical to 0 */
   uint64_t seed;            /* Philox key of CAKF_POLICY_RANDOM                               */
   int32_t max_steps;        /* T: number of time steps the trace is sized for                */
   int64_t max_obs;          /* max N_k over the run (0 = n_space)                            */
@@ -186,6 +189,12 @@ int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset);
 
 /* Number of libcakf kernels launched by this process so far (all handles). */
 int64_t cakf_kernel_launches(void);
+
+/* Exact-zero culling statistics of the handle so far: frac3[0] = fraction of the symmetric K1's
+ * 128x128 tile pairs evaluated, frac3[1] = fraction of the post-loop K2's 128x32 tiles evaluated,
+ * frac3[2] = same for the smoother's K2 (all 1.0 when culling is off).  Synchronises the handle's
+ * stream.  Errors: CAKF_E_HANDLE, CAKF_E_ARG (NULL frac3), CAKF_E_CUDA. */
+int cakf_cull_stats(cakf_t h, double* frac3);
 
 /* ---- multi-GPU (the spatial rows of the covariance operator are sharded) ----
  * With cfg.world > 1 every rank calls the same sequence with the same full inputs; the two

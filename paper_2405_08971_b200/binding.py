@@ -38,7 +38,7 @@ class cakf_config(ctypes.Structure):
         ("space_dim", ctypes.c_int32), ("coords", ctypes.c_void_p), ("spatial_kernel", ctypes.c_int32),
         ("ell_x", ctypes.c_double), ("sigma_t0", ctypes.c_void_p), ("mu0", ctypes.c_void_p),
         ("policy", ctypes.c_int32), ("max_iter", ctypes.c_int32), ("max_rank", ctypes.c_int32),
-        ("rtol", ctypes.c_double), ("reorth", ctypes.c_int32), ("seed", ctypes.c_uint64), ("max_steps", ctypes.c_int32),
+        ("rtol", ctypes.c_double), ("reorth", ctypes.c_int32), ("cull_zero", ctypes.c_int32), ("seed", ctypes.c_uint64), ("max_steps", ctypes.c_int32),
         ("max_obs", ctypes.c_int64), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
     ]
@@ -60,7 +60,7 @@ EXPORTS = [
     "cakf_create", "cakf_reset", "cakf_predict", "cakf_update", "cakf_truncate", "caks_smooth", "cakf_get",
     "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
-    "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks",
+    "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats",
 ]
 PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank", "trunc_gram",
                    "trunc_eig", "trunc_gemm"]
@@ -182,7 +182,7 @@ class Cakf:
 
     def __init__(self, coords, ell_x, sigma_t0, *, dtype="f32", d_time=2, nu_x=1.5, mu0=None, policy="cg",
                  max_iter=64, max_rank=-1, seed=1, max_steps=48, max_obs=0, reorth=True, stream=None,
-                 rank=0, world=1, nccl_id=None):
+                 rank=0, world=1, nccl_id=None, cull_zero=True):
         self.lib = load()
         coords = np.ascontiguousarray(coords, dtype=np.float64)
         if coords.ndim == 1:
@@ -198,7 +198,7 @@ class Cakf:
                           sigma_t0=st0.ctypes.data, mu0=None if mu is None else mu.ctypes.data,
                           policy=POLICIES[policy] if isinstance(policy, str) else int(policy),
                           max_iter=int(max_iter), max_rank=int(max_rank), rtol=0.0, reorth=int(bool(reorth)),
-                          seed=int(seed),
+                          cull_zero=int(bool(cull_zero)), seed=int(seed),
                           max_steps=int(max_steps), max_obs=int(max_obs), rank=int(rank), world=int(world),
                           nccl_id=None, stream=stream)
         self._nccl_id = None
@@ -271,6 +271,12 @@ class Cakf:
         cnt = np.zeros(n, dtype=np.int64)
         _check(self.lib.cakf_profile_read(self.h, ms.ctypes.data, cnt.ctypes.data, int(bool(reset))))
         return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(PROF_CATEGORIES)}
+
+    def cull_stats(self) -> dict:
+        """Fractions of the dense kernel work evaluated under exact-zero culling (1.0 = none culled)."""
+        out = np.zeros(3)
+        _check(self.lib.cakf_cull_stats(self.h, out.ctypes.data))
+        return {"k1_matvec": float(out[0]), "k2_post": float(out[1]), "k2_smooth": float(out[2])}
 
     def destroy(self):
         if getattr(self, "h", None):

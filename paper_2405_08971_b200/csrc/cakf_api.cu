@@ -155,6 +155,7 @@ struct ImplBase {
   virtual int sync() = 0;
   virtual int profile(bool on) = 0;
   virtual int prof_read(double* ms, int64_t* n, bool reset) = 0;
+  virtual int cull_stats(double* out) = 0;
 };
 
 template <typename T>
@@ -215,6 +216,16 @@ struct Impl final : ImplBase {
   T *Wf = nullptr, *Ws = nullptr, *ws = nullptr, *pvar = nullptr;
   float* tcw = nullptr;  // bf16 planes of the K2 right-hand sides
 
+  // ---------------- exact-zero culling (fp32 only): tile bounding spheres and, per 128-row
+  // output tile of K2, the ascending list of 32-column K-blocks not entirely below the fp32 underflow
+  bool cull = false;
+  float4 *sph_x128 = nullptr, *sph_x32 = nullptr, *sph_o128 = nullptr, *sph_o32 = nullptr;
+  int *act_cnt_sm = nullptr, *act_list_sm = nullptr, *act_cnt_po = nullptr, *act_list_po = nullptr;
+  int act_stride_sm = 0, act_stride_po = 0;
+  unsigned long long* cull_ctr = nullptr;  // [0] K1 tile pairs done, [1] K2-post blocks, [2] K2-smooth blocks
+  double k1_pairs_dense = 0, k2_post_dense = 0, k2_sm_dense = 0;
+  int64_t k2_sm_launches = 0;
+
   // ---------------- internal point order (spatially compact tiles for the fused kernels)
   int *perm_d = nullptr, *invperm_d = nullptr;   // internal -> user, user -> internal
   int *posof = nullptr, *obs_cnt = nullptr, *sigma = nullptr, *sigma_inv = nullptr;
@@ -264,28 +275,32 @@ struct Impl final : ImplBase {
   }
 
   cudaError_t k2_local(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y,
-                       size_t ldy) {
+                       size_t ldy, const int* acnt, const int* alist, int astride) {
     if constexpr (sizeof(T) == 4) {
       if (use_tc_k2())
         return launch_gram_gemm_tc(nu2, reinterpret_cast<const float4*>(xr), M, reinterpret_cast<const float4*>(xc), K,
                                    reinterpret_cast<const float*>(B), ldb, C, reinterpret_cast<float*>(Y), ldy, 1.0,
-                                   tcw, st);
+                                   tcw, st, acnt, alist, astride);
     }
     return launch_gram_gemm<T>(nu2, xr, M, xc, K, B, ldb, C, Y, ldy, 1.0, st);
   }
 
   // K2: Y = K(xr, xc) B — tcgen05 3xBF16 for fp32, SIMT for fp64 (or CAKF_K2_SIMT=1).
   // world > 1: rank p computes output rows [p*slice, (p+1)*slice) and the slices are all-gathered.
-  int k2(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y, size_t ldy) {
+  // acnt/alist: exact-zero culling lists of the 128-row tiles of xr (nullable)
+  int k2(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y, size_t ldy,
+         const int* acnt = nullptr, const int* alist = nullptr, int astride = 0) {
     if (world == 1) {
-      CK_CUDA(k2_local(xr, M, xc, K, B, ldb, C, Y, ldy));
+      CK_CUDA(k2_local(xr, M, xc, K, B, ldb, C, Y, ldy, acnt, alist, astride));
       return CAKF_OK;
     }
     if ((size_t)C > k2_cmax) return fail(CAKF_E_ARG, "k2: too many right-hand sides for the shard buffers");
     const int slice = k2_slice_rows(M, world);
     const int lo = rank * slice;
     const int mloc = std::max(0, std::min(slice, M - lo));
-    if (mloc > 0) CK_CUDA(k2_local(xr + lo, mloc, xc, K, B, ldb, C, yslice, (size_t)slice));
+    if (mloc > 0)
+      CK_CUDA(k2_local(xr + lo, mloc, xc, K, B, ldb, C, yslice, (size_t)slice, acnt ? acnt + lo / 128 : nullptr,
+                       alist ? alist + (size_t)(lo / 128) * astride : nullptr, astride));
     CK_NCCL(ncclAllGather(yslice, ygath, (size_t)slice * C, sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, comm, st));
     CK_CUDA(StepKernels<T>::assemble_slices(M, C, slice, ygath, Y, ldy, st));
     return CAKF_OK;
@@ -315,6 +330,20 @@ struct Impl final : ImplBase {
     cudaEventRecord(ev_pool[i + 1], st);
     ev_done.emplace_back(cat, i);
   }
+  // fractions of the dense work performed: [K1 tile pairs, K2-post K-blocks, K2-smooth K-blocks] (1 = no culling)
+  int cull_stats(double* out) override {
+    out[0] = out[1] = out[2] = 1.0;
+    if (!cull) return CAKF_OK;
+    unsigned long long h[4];
+    CK_CUDA(cudaMemcpyAsync(h, cull_ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+    const double nx128 = (double)((NX + 127) / 128), nx32 = (double)((NX + 31) / 32);
+    if (k1_pairs_dense > 0) out[0] = (double)h[0] / k1_pairs_dense;
+    if (k2_post_dense > 0) out[1] = (double)h[1] / k2_post_dense;
+    out[2] = (double)h[2] / (nx128 * nx32);
+    return CAKF_OK;
+  }
+
   int prof_read(double* ms, int64_t* n, bool reset_) override {
     CK_CUDA(cudaStreamSynchronize(st));
     for (auto& pr : ev_done) {
@@ -462,6 +491,16 @@ struct Impl final : ImplBase {
                                  gram_gemm_tc_workspace((int)NX, Dp * (1 + qmax)));
       tcw = carve<float>(wb / sizeof(float) + 64);
     }
+    if (cull) {
+      const int nx128 = (int)((NX + 127) / 128), nx32 = (int)((NX + 31) / 32);
+      const int no128 = (int)((Nmax + 127) / 128), no32 = (int)((Nmax + 31) / 32);
+      sph_x128 = carve<float4>(nx128); sph_x32 = carve<float4>(nx32);
+      sph_o128 = carve<float4>(no128); sph_o32 = carve<float4>(no32);
+      act_stride_sm = nx32; act_stride_po = no32;
+      act_cnt_sm = carve<int>(nx128); act_list_sm = carve<int>((size_t)nx128 * nx32);
+      act_cnt_po = carve<int>(nx128); act_list_po = carve<int>((size_t)nx128 * no32);
+      cull_ctr = carve<unsigned long long>(4);
+    }
   }
 
   int init(const cakf_config& c) override {
@@ -469,6 +508,7 @@ struct Impl final : ImplBase {
     nhat = c.max_iter; rcap = c.max_rank; Tmax = c.max_steps; NX = c.n_space; D = NX * Dp;
     Nmax = c.max_obs > 0 ? std::min<int64_t>(c.max_obs, NX) : NX;
     rtol = c.rtol; ell = c.ell_x; seed = c.seed; reorth = c.reorth != 0;
+    cull = c.cull_zero != 0 && sizeof(T) == 4;
     world = std::max(1, c.world); rank = c.rank;
     if (world > 1) {
       if (!c.nccl_id || rank < 0 || rank >= world) return fail(CAKF_E_ARG, "multi-GPU: nccl_id and 0 <= rank < world needed");
@@ -525,6 +565,15 @@ struct Impl final : ImplBase {
     double* dxyz = reinterpret_cast<double*>(stage64);
     CK_CUDA(cudaMemcpyAsync(dxyz, xyz_int.data(), (size_t)NX * dim * sizeof(double), cudaMemcpyHostToDevice, st));
     CK_CUDA(launch_prescale_coords<T>((int)NX, dim, dxyz, std::sqrt((double)nu2) / ell, coords, st));
+    if (cull) {  // the smoother's K2 lists depend on the (fixed) grid only
+      const float4* xf = reinterpret_cast<const float4*>(coords);
+      const int nx128 = (int)((NX + 127) / 128), nx32 = (int)((NX + 31) / 32);
+      CK_CUDA(cudaMemsetAsync(cull_ctr, 0, 4 * sizeof(unsigned long long), st));
+      CK_CUDA(launch_tile_spheres(xf, (int)NX, 128, sph_x128, st));
+      CK_CUDA(launch_tile_spheres(xf, (int)NX, 32, sph_x32, st));
+      CK_CUDA(launch_k2_active(sph_x128, nx128, sph_x32, nx32, kCullCut, act_cnt_sm, act_list_sm, act_stride_sm,
+                               cull_ctr + 2, st));
+    }
     std::vector<T> mu(D, T(0));
     if (c.mu0) {
       std::vector<double> m0;
@@ -643,6 +692,14 @@ struct Impl final : ImplBase {
     const double sig00 = S.sig_t.a[0][0];
     const double eps = sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON;
     const bool sym = sizeof(T) == 4 && use_sym_k1();
+    if (cull && N > 0) {  // spheres of the sorted observation tiles; K2-post lists against them
+      const float4* xf = reinterpret_cast<const float4*>(xcs);
+      CK_CUDA(launch_tile_spheres(xf, N, 128, sph_o128, st));
+      CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st));
+      CK_CUDA(launch_k2_active(sph_x128, (int)((NX + 127) / 128), sph_o32, (N + 31) / 32, kCullCut, act_cnt_po,
+                               act_list_po, act_stride_po, cull_ctr + 1, st));
+      k2_post_dense += (double)((NX + 127) / 128) * ((N + 31) / 32);
+    }
     const int nch = sym ? matvec_sym_tiles(N)
                         : std::max(1, std::min<int>(matvec_chunks(N, N, sizeof(T)), (int)(partial_cap / N)));
     T* V = S.XV + N;
@@ -656,7 +713,12 @@ struct Impl final : ImplBase {
         if (sym) {
           const long long U = matvec_sym_units(N);
           CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
-                                    U * rank / world, U * (rank + 1) / world, st));
+                                    U * rank / world, U * (rank + 1) / world, st, cull ? sph_o128 : nullptr,
+                                    kCullCut, cull ? cull_ctr : nullptr));
+          if (cull) {
+            const double nt = (double)((N + 127) / 128);
+            k1_pairs_dense += nt * (nt + 1) / 2 / world;
+          }
         } else {
           CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st, nch * rank / world,
                                            nch * (rank + 1) / world));
@@ -693,7 +755,7 @@ struct Impl final : ImplBase {
     // ---- post-loop: [P^- w, P^- W] = Sigma H^T [v V] - M^- (H M^-)^T [v V]
     const int Cc = 1 + niter;
     size_t pk = prof_begin();
-    CK(k2(coords, (int)NX, xcs, N, S.XV, N, Cc, Yb, NX));
+    CK(k2(coords, (int)NX, xcs, N, S.XV, N, Cc, Yb, NX, cull ? act_cnt_po : nullptr, act_list_po, act_stride_po));
     prof_end(CAKF_PROF_K2_POST, pk);
     if (rin) {
       pk = prof_begin();
@@ -814,7 +876,9 @@ struct Impl final : ImplBase {
       if (q) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, q, S.A_next, true, Ws, D, X + D, D, st));
       // Sigma_k x = (Sigma^t_k (x) K) x : K applied to all D' blocks of all C columns at once
       size_t pk = prof_begin();
-      CK(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX));
+      CK(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX, cull ? act_cnt_sm : nullptr, act_list_sm,
+            act_stride_sm));
+      ++k2_sm_launches;
       prof_end(CAKF_PROF_K2_SMOOTH, pk);
       CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, C, S.sig_t, Yk, yb, st));
       const int rin = S.rin, n = S.n, N = S.N;
@@ -1006,6 +1070,11 @@ int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset) {
   return h->impl->prof_read(ms, launches, reset != 0);
 }
 int64_t cakf_kernel_launches(void) { return (int64_t)launch_counter(); }
+int cakf_cull_stats(cakf_t h, double* frac3) {
+  HANDLE_CHECK(h);
+  if (!frac3) return fail(CAKF_E_ARG, "NULL output");
+  return h->impl->cull_stats(frac3);
+}
 
 int cakf_nccl_unique_id(void* out) {
   if (!out) return fail(CAKF_E_ARG, "cakf_nccl_unique_id: NULL");

@@ -19,8 +19,15 @@ int matvec_chunks(int nrows, int ncols, int elem_bytes);
 int matvec_sym_tiles(int n);
 long long matvec_sym_units(int n);   // number of symmetric tile-block work units
 int matvec_sym_block_points();       // points per tile block of the symmetric K1
+// sph != nullptr: skip tile pairs whose bounding spheres are > cut apart (all values exactly 0),
+// counting the evaluated 128 x 128 tile pairs in *done_pairs (nullable)
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
-                              cudaStream_t st);
+                              cudaStream_t st, const float4* sph = nullptr, float cut = 0.f,
+                              unsigned long long* done_pairs = nullptr);
+// bounding spheres (x, y, z, radius) of consecutive tiles of `tile` points
+cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st);
+// fp32 exact-zero cut: a prescaled distance above which ex2.approx.ftz(-a log2 e) flushes to 0
+constexpr float kCullCut = 88.0f;
 bool use_sym_k1();  // false if CAKF_K1_DENSE=1
 // reduce partials: y[i] = alpha * sum_ch partial[ch][i]
 template <typename T>
@@ -33,8 +40,15 @@ cudaError_t launch_gram_gemm(int nu2, const V4<T>* xr, int M, const V4<T>* xc, i
 
 // ---- K2 on tcgen05 tensor cores (fp32 via 3xTF32): workspace = gram_gemm_tc_workspace(K, C) bytes
 size_t gram_gemm_tc_workspace(int K, int C);
+// act_cnt / act_list (nullable): per 128-row output tile, the ascending list of 32-column K-blocks that
+// are not entirely exactly-zero (exact-zero culling); act_stride = list stride per tile
 cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* xc, int K, const float* B, size_t ldb,
-                                int C, float* Y, size_t ldy, double alpha, float* work, cudaStream_t st);
+                                int C, float* Y, size_t ldy, double alpha, float* work, cudaStream_t st,
+                                const int* act_cnt = nullptr, const int* act_list = nullptr, int act_stride = 0);
+// build the active K-block lists from M-tile (128) and K-block (32) spheres
+// (*total += number of active K-blocks, for the cull statistics)
+cudaError_t launch_k2_active(const float4* sphM, int nmt, const float4* sphK, int nkb, float cut, int* act_cnt,
+                             int* act_list, int act_stride, unsigned long long* total, cudaStream_t st);
 // true unless CAKF_K2_SIMT=1 is set in the environment
 bool use_tc_k2();
 

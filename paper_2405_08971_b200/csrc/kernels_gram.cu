@@ -86,7 +86,8 @@ constexpr int SYM_S = 4;
 template <int NU2>
 __global__ void __launch_bounds__(256)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
-                  float* __restrict__ partial) {
+                  float* __restrict__ partial, const float4* __restrict__ sph, float cut,
+                  unsigned long long* __restrict__ done_pairs) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
   float4* tJ = tI + SYM_S * SYM_T;                                    // [SYM_S][128]
@@ -124,6 +125,12 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
         rx[q] = v.x; ry[q] = v.y; rz[q] = v.z; rs[q] = v.w; racc[q] = 0.f;
       }
       for (int b = diag ? a : 0; b < nbj; ++b) {
+        if (sph) {   // exact-zero culling: every kernel value of this tile pair underflows to 0 in fp32
+          const float4 A = sph[bi * SYM_S + a], B = sph[bj * SYM_S + b];
+          const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
+          if (sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut) continue;
+          if (tid == 0 && done_pairs) atomicAdd(done_pairs, 1ull);
+        }
         const bool offdiag = !(diag && a == b);
         float cx[8], cy[8], cz[8], cs[8], cacc[8];
 #pragma unroll
@@ -173,6 +180,44 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
         if (gj < n) partial[(size_t)bi * n + gj] = cs_;
       }
     }
+  }
+}
+
+// Bounding sphere (center, radius inflated for rounding) of each tile of `tile` consecutive points.
+__global__ void tile_spheres_kernel(const float4* __restrict__ x, int n, int tile, float4* __restrict__ out) {
+  __shared__ double red[4][32];
+  __shared__ double cen[3];
+  const int t0 = blockIdx.x * tile, t1 = min(n, t0 + tile);
+  double sx = 0, sy = 0, sz = 0;
+  for (int i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+    const float4 p = x[i];
+    sx += p.x; sy += p.y; sz += p.z;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  sx = warp_sum(sx); sy = warp_sum(sy); sz = warp_sum(sz);
+  if (lane == 0) { red[0][w] = sx; red[1][w] = sy; red[2][w] = sz; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0, c = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { a += red[0][q]; b += red[1][q]; c += red[2][q]; }
+    const double cnt = (double)max(1, t1 - t0);
+    cen[0] = a / cnt; cen[1] = b / cnt; cen[2] = c / cnt;
+  }
+  __syncthreads();
+  double r = 0;
+  for (int i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+    const float4 p = x[i];
+    const double dx = p.x - cen[0], dy = p.y - cen[1], dz = p.z - cen[2];
+    r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+  if (lane == 0) red[3][w] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = fmax(m, red[3][q]);
+    out[blockIdx.x] = make_float4((float)cen[0], (float)cen[1], (float)cen[2], (float)(m * (1.0 + 1e-5) + 1e-3));
   }
 }
 
@@ -324,6 +369,12 @@ cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  tile_spheres_kernel<<<(n + tile - 1) / tile, 128, 0, st>>>(x, n, tile, out);
+  return note_launch_err();
+}
+
 int matvec_sym_tiles(int n) { return ((n + SYM_T - 1) / SYM_T + SYM_S - 1) / SYM_S; }   // = partials per row
 
 bool use_sym_k1() {
@@ -344,7 +395,7 @@ long long matvec_sym_units(int n) {
 }
 
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
-                              cudaStream_t st) {
+                              cudaStream_t st, const float4* sph, float cut, unsigned long long* done_pairs) {
   if (n <= 0 || u_end <= u_begin) return cudaSuccess;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
@@ -359,9 +410,12 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
     configured = true;
   }
   switch (nu2) {
-    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial); break;
-    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial); break;
-    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial); break;
+    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
+                                                                         done_pairs); break;
+    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
+                                                                         done_pairs); break;
+    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
+                                                                         done_pairs); break;
     default: return cudaErrorInvalidValue;
   }
   return note_launch_err();

@@ -121,7 +121,8 @@ template <int NU2>
 __global__ void __launch_bounds__(TC_THREADS + 64, 1)
 gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmX, int K, int C, int ntile,
-                    float* __restrict__ Y, size_t ldy, float alpha, int diag_nogen) {
+                    float* __restrict__ Y, size_t ldy, float alpha, int diag_nogen,
+                    const int* __restrict__ act_cnt, const int* __restrict__ act_list, int act_stride) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -142,7 +143,9 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
   // accumulation truncates, so keeping the small terms apart cuts the biased error ~6x)
   const uint32_t acc_cols = ntile <= 32 ? 32 : ntile <= 64 ? 64 : ntile <= 128 ? 128 : 256;
   const uint32_t tmem_cols = 2 * acc_cols;
-  const int nk = (K + TC_BK - 1) / TC_BK;
+  // exact-zero culling: only this tile's active K-blocks (ascending), else all of them
+  const int nk = act_cnt ? act_cnt[blockIdx.x] : (K + TC_BK - 1) / TC_BK;
+  const int* my_list = act_cnt ? act_list + (size_t)blockIdx.x * act_stride : nullptr;
 
   if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -217,7 +220,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
         const uint32_t bar = smem_u32(&fullB[s]);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
         const uint32_t b0 = b_addr(s);
-        const int k0 = kb * TC_BK;
+        const int k0 = (my_list ? my_list[kb] : kb) * TC_BK;
 #pragma unroll
         for (int pl = 0; pl < 3; ++pl) {
           asm volatile(
@@ -349,7 +352,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 template <int NU2>
 cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const uint16_t* planes, int Kp, int C,
-                         int ntile, float* Y, size_t ldy, float alpha, cudaStream_t st) {
+                         int ntile, float* Y, size_t ldy, float alpha, cudaStream_t st, const int* act_cnt,
+                         const int* act_list, int act_stride) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
@@ -377,11 +381,50 @@ cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const
     return cudaErrorInvalidValue;
   static const int nogen = [] { const char* e = getenv("CAKF_TC_DIAG_NOGEN"); return (e && e[0] == '1') ? 1 : 0; }();
   dim3 grid((M + TC_BM - 1) / TC_BM, (C + ntile - 1) / ntile);
-  gram_gemm_tc_kernel<NU2><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha, nogen);
+  gram_gemm_tc_kernel<NU2><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha, nogen,
+                                                                   act_cnt, act_list, act_stride);
   return note_launch_err();
 }
 
 }  // namespace
+
+// one block per 128-row output tile: ascending list of the 32-column K-blocks within the cut
+__global__ void k2_active_kernel(const float4* __restrict__ sphM, const float4* __restrict__ sphK, int nkb, float cut,
+                                 int* __restrict__ act_cnt, int* __restrict__ act_list, int act_stride,
+                                 unsigned long long* __restrict__ total) {
+  __shared__ int wcount[8];
+  __shared__ int base;
+  const float4 A = sphM[blockIdx.x];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int k0 = 0; k0 < nkb; k0 += 256) {
+    const int kb = k0 + threadIdx.x;
+    bool on = false;
+    if (kb < nkb) {
+      const float4 B = sphK[kb];
+      const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
+      on = !(sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) wcount[w] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int q = 0; q < w; ++q) off += wcount[q];
+    if (on) act_list[(size_t)blockIdx.x * act_stride + off + __popc(bal & ((1u << lane) - 1u))] = kb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int q = 0; q < 8; ++q) t += wcount[q];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    act_cnt[blockIdx.x] = base;
+    if (total) atomicAdd(total, (unsigned long long)base);
+  }
+}
 
 bool use_tc_k2() {
   static int v = -1;
@@ -392,13 +435,21 @@ bool use_tc_k2() {
   return v == 1;
 }
 
+cudaError_t launch_k2_active(const float4* sphM, int nmt, const float4* sphK, int nkb, float cut, int* act_cnt,
+                             int* act_list, int act_stride, unsigned long long* total, cudaStream_t st) {
+  if (nmt <= 0) return cudaSuccess;
+  k2_active_kernel<<<nmt, 256, 0, st>>>(sphM, sphK, nkb, cut, act_cnt, act_list, act_stride, total);
+  return note_launch_err();
+}
+
 size_t gram_gemm_tc_workspace(int K, int C) {
   const size_t Kp = ((size_t)K + TC_BK - 1) / TC_BK * TC_BK;
   return 3 * Kp * (size_t)C * sizeof(uint16_t) + 256;
 }
 
 cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* xc, int K, const float* B, size_t ldb,
-                                int C, float* Y, size_t ldy, double alpha, float* work, cudaStream_t st) {
+                                int C, float* Y, size_t ldy, double alpha, float* work, cudaStream_t st,
+                                const int* act_cnt, const int* act_list, int act_stride) {
   if (M <= 0 || C <= 0) return cudaSuccess;
   const int Kp = (K + TC_BK - 1) / TC_BK * TC_BK;
   uint16_t* planes = reinterpret_cast<uint16_t*>(work);
@@ -413,9 +464,12 @@ cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* 
   int ntile = (C + ntiles - 1) / ntiles;
   ntile = ((ntile + 15) / 16) * 16;
   switch (nu2) {
-    case 1: return launch_tc_nu<1>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st);
-    case 3: return launch_tc_nu<3>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st);
-    case 5: return launch_tc_nu<5>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st);
+    case 1: return launch_tc_nu<1>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st, act_cnt, act_list,
+                                   act_stride);
+    case 3: return launch_tc_nu<3>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st, act_cnt, act_list,
+                                   act_stride);
+    case 5: return launch_tc_nu<5>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st, act_cnt, act_list,
+                                   act_stride);
   }
   return cudaErrorInvalidValue;
 }

@@ -70,3 +70,29 @@ def test_symmetric_k1_cfg3(cfg3):
     print("symmetric K1 cfg3: sampled rel err", err, "vs dense kernel", err_all)
     assert err < 1e-6
     assert np.max(np.abs(y - y_dense)) < 1e-5 * np.max(np.abs(y_dense))
+
+
+def test_exact_zero_culling_is_bit_identical_cfg3():
+    """Exact-zero culling skips only kernel tiles whose every fp32 value is exactly 0,
+    so the filter and smoother outputs with culling on and off must be bit-identical, while a
+    real share of the K1 / K2 tiles is skipped at cfg3's lengthscale."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2405_08971_b200 import runner
+    wl = make_workload("cfg3", T=3, max_iter=24, max_rank=48)
+    trans = runner.transitions(wl)[0]
+    inputs = runner.stage_inputs(wl, "f32")
+    outs, fracs = [], []
+    for cull in (False, True):
+        h = runner.make_handle(wl, "f32", cull_zero=cull)
+        runner.run(h, trans, inputs)
+        h.sync()
+        outs.append([runner.collect(h, wl.T, w) for w in (0, 1)])
+        fracs.append(h.cull_stats())
+        h.destroy()
+    for a, b in zip(outs[0], outs[1]):
+        for ka, kb in zip(a[0] + a[1], b[0] + b[1]):
+            assert np.array_equal(ka, kb)
+    assert fracs[0] == {"k1_matvec": 1.0, "k2_post": 1.0, "k2_smooth": 1.0}
+    print("cull fractions", fracs[1])
+    assert all(0.0 < f < 0.9 for f in fracs[1].values())
