@@ -222,6 +222,7 @@ struct Impl final : ImplBase {
   float4 *sph_x128 = nullptr, *sph_x32 = nullptr, *sph_o128 = nullptr, *sph_o32 = nullptr;
   int *act_cnt_sm = nullptr, *act_list_sm = nullptr, *act_cnt_po = nullptr, *act_list_po = nullptr;
   int act_stride_sm = 0, act_stride_po = 0;
+  int *k1_list = nullptr, *k1_count = nullptr;  // active symmetric K1 units of this update
   unsigned long long* cull_ctr = nullptr;  // [0] K1 tile pairs done, [1] K2-post blocks, [2] K2-smooth blocks
   double k1_pairs_dense = 0, k2_post_dense = 0, k2_sm_dense = 0;
   int64_t k2_sm_launches = 0;
@@ -427,13 +428,13 @@ struct Impl final : ImplBase {
     const int nch = matvec_chunks((int)Nmax, (int)Nmax, sizeof(T));
     partial_cap = (size_t)std::max<int64_t>({(int64_t)nch, (int64_t)64, (int64_t)matvec_sym_tiles((int)Nmax)}) * Nmax;
     partial = carve<T>(partial_cap);
-    stage64 = carve<int64_t>(std::max<int64_t>(Nmax, NX));
+    stage64 = carve<int64_t>(std::max<int64_t>(Nmax, 3 * NX));   // also the 3 x NX staged coordinates
     order32 = carve<int>(std::max(nhat, 1));
-    part = carve<double>((size_t)320 * W);
+    part = carve<double>((size_t)(stage_blocks((int)Nmax) + 33) * W);   // block rows + group rows
     redA = carve<double>(W);
     redB = carve<double>(W);
     redC = carve<double>(W);
-    cnt = carve<unsigned>(16);
+    cnt = carve<unsigned>(4 * 64);   // per reduction: [0] top, [1..32] group counters
     Yb = carve<T>((size_t)NX * (1 + nhat));
     Ub = carve<T>((size_t)std::max(rin_max, 1) * (1 + nhat));
     tmp = carve<T>((size_t)D * (1 + nhat));
@@ -500,6 +501,8 @@ struct Impl final : ImplBase {
       act_cnt_sm = carve<int>(nx128); act_list_sm = carve<int>((size_t)nx128 * nx32);
       act_cnt_po = carve<int>(nx128); act_list_po = carve<int>((size_t)nx128 * no32);
       cull_ctr = carve<unsigned long long>(4);
+      k1_list = carve<int>((size_t)matvec_sym_units((int)Nmax) + 1);
+      k1_count = carve<int>(1);
     }
   }
 
@@ -546,7 +549,7 @@ struct Impl final : ImplBase {
       return fail(CAKF_E_NOMEM, "trace arena of " + std::to_string(arena_bytes) + " bytes: " + cudaGetErrorString(e));
     }
     layout();
-    CK_CUDA(cudaMemsetAsync(cnt, 0, 16 * sizeof(unsigned), st));
+    CK_CUDA(cudaMemsetAsync(cnt, 0, 4 * 64 * sizeof(unsigned), st));
     CK_CUDA(cudaMallocHost(&ctl_init_host, sizeof(IterCtl)));
     std::memset(ctl_init_host, 0, sizeof(IterCtl));
     ctl_init_host->eta_min = INFINITY;
@@ -699,6 +702,12 @@ struct Impl final : ImplBase {
       CK_CUDA(launch_k2_active(sph_x128, (int)((NX + 127) / 128), sph_o32, (N + 31) / 32, kCullCut, act_cnt_po,
                                act_list_po, act_stride_po, cull_ctr + 1, st));
       k2_post_dense += (double)((NX + 127) / 128) * ((N + 31) / 32);
+      if (sym) {  // active K1 units of this rank; the skipped units' partial slots stay zero
+        const long long U = matvec_sym_units(N);
+        CK_CUDA(launch_k1_active_units(sph_o128, N, U * rank / world, U * (rank + 1) / world, kCullCut, k1_list,
+                                       k1_count, st));
+        CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)matvec_sym_tiles(N) * N * sizeof(T), st));
+      }
     }
     const int nch = sym ? matvec_sym_tiles(N)
                         : std::max(1, std::min<int>(matvec_chunks(N, N, sizeof(T)), (int)(partial_cap / N)));
@@ -714,7 +723,7 @@ struct Impl final : ImplBase {
           const long long U = matvec_sym_units(N);
           CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
                                     U * rank / world, U * (rank + 1) / world, st, cull ? sph_o128 : nullptr,
-                                    kCullCut, cull ? cull_ctr : nullptr));
+                                    kCullCut, cull ? cull_ctr : nullptr, cull ? k1_list : nullptr, k1_count));
           if (cull) {
             const double nt = (double)((N + 127) / 128);
             k1_pairs_dense += nt * (nt + 1) / 2 / world;
@@ -737,21 +746,21 @@ struct Impl final : ImplBase {
       }
       prof_end(CAKF_PROF_K1, pk);
       pk = prof_begin();
-      CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, HM, rin, part, W, redA, cnt + 0, st));
-      CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 1, st));
+      CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, HM, rin, part, W, redA, cnt, st));
+      CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 64, st));
       if (reorth && i > 1) {  // CGS2 (R19): d = s - V c, then d -= V (V^T G d)
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W, redC,
-                                       cnt + 2, C, eps, i, 1, st));
+                                       cnt + 128, C, eps, i, 1, st));
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redC, d, Gd, d, Gd, s, redA, rin, redB + (i - 1), part, W,
-                                       nullptr, cnt + 2, C, eps, i, 0, st));
+                                       nullptr, cnt + 128, C, eps, i, 0, st));
       } else {
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W,
-                                       nullptr, cnt + 2, C, eps, i, 0, st));
+                                       nullptr, cnt + 128, C, eps, i, 0, st));
       }
       CK_CUDA(StepKernels<T>::stageD(N, i, niter, C, d, Gd, S.XV, Z, r, s, xcs, policy, order32, seed, k, sigma, st));
       prof_end(CAKF_PROF_STAGES, pk);
     }
-    CK_CUDA(StepKernels<T>::dot(N, r, r, part, &C->res_sq, cnt + 3, st));
+    CK_CUDA(StepKernels<T>::dot(N, r, r, part, &C->res_sq, cnt + 192, st));
     // ---- post-loop: [P^- w, P^- W] = Sigma H^T [v V] - M^- (H M^-)^T [v V]
     const int Cc = 1 + niter;
     size_t pk = prof_begin();

@@ -23,7 +23,11 @@ int matvec_sym_block_points();       // points per tile block of the symmetric K
 // counting the evaluated 128 x 128 tile pairs in *done_pairs (nullable)
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
                               cudaStream_t st, const float4* sph = nullptr, float cut = 0.f,
-                              unsigned long long* done_pairs = nullptr);
+                              unsigned long long* done_pairs = nullptr, const int* ulist = nullptr,
+                              const int* ucount = nullptr);
+// compact ascending list of the sym units in [u_lo, u_hi) with a tile pair within `cut` (device count)
+cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
+                                   int* count, cudaStream_t st);
 // bounding spheres (x, y, z, radius) of consecutive tiles of `tile` points
 cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st);
 // fp32 exact-zero cut: a prescaled distance above which ex2.approx.ftz(-a log2 e) flushes to 0

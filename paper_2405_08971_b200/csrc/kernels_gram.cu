@@ -83,11 +83,20 @@ matvec_partial_kernel(const V4<T>* __restrict__ xr, int nrows, const V4<T>* __re
 // (deterministic, no atomics).
 constexpr int SYM_T = 128;
 constexpr int SYM_S = 4;
+__device__ __forceinline__ void sym_unit_decode(long long u, int nb, int& bi, int& bj) {
+  const double bb = 2.0 * nb + 1.0;
+  bi = (int)floor((bb - sqrt(bb * bb - 8.0 * (double)u)) * 0.5);
+  while ((long long)bi * nb - (long long)bi * (bi - 1) / 2 > u) --bi;
+  while ((long long)(bi + 1) * nb - (long long)(bi + 1) * bi / 2 <= u) ++bi;
+  bj = bi + (int)(u - ((long long)bi * nb - (long long)bi * (bi - 1) / 2));
+}
+
 template <int NU2>
 __global__ void __launch_bounds__(256)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
                   float* __restrict__ partial, const float4* __restrict__ sph, float cut,
-                  unsigned long long* __restrict__ done_pairs) {
+                  unsigned long long* __restrict__ done_pairs, const int* __restrict__ ulist,
+                  const int* __restrict__ ucount) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
   float4* tJ = tI + SYM_S * SYM_T;                                    // [SYM_S][128]
@@ -95,13 +104,14 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
   float* colp = rowacc + SYM_S * SYM_T;                               // [16 ty][SYM_S][128] private slots
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   float* mycol = colp + ty * SYM_S * SYM_T + tx * 8;                  // this thread's 8 columns of each J tile
-  for (long long u = u_begin + blockIdx.x; u < u_end; u += gridDim.x) {
+  // ulist: compact ascending list of the units with an active tile pair (exact-zero culling); the
+  // skipped units' partial slots were zeroed once per update
+  const long long nwork = ulist ? (long long)*ucount : u_end - u_begin;
+  for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const long long u = ulist ? (long long)ulist[w] : u_begin + w;
     // u -> (bi, bj), bi <= bj, row-major over the upper triangle of blocks
-    const double bb = 2.0 * nb + 1.0;
-    int bi = (int)floor((bb - sqrt(bb * bb - 8.0 * (double)u)) * 0.5);
-    while ((long long)bi * nb - (long long)bi * (bi - 1) / 2 > u) --bi;
-    while ((long long)(bi + 1) * nb - (long long)(bi + 1) * bi / 2 <= u) ++bi;
-    const int bj = bi + (int)(u - ((long long)bi * nb - (long long)bi * (bi - 1) / 2));
+    int bi, bj;
+    sym_unit_decode(u, nb, bi, bj);
     const bool diag = bi == bj;
     const int na = min(SYM_S, nt - bi * SYM_S), nbj = min(SYM_S, nt - bj * SYM_S);
     __syncthreads();
@@ -394,8 +404,56 @@ long long matvec_sym_units(int n) {
   return nb * (nb + 1) / 2;
 }
 
+// one block: ascending compact list of the units in [u_lo, u_hi) with at least one tile pair within the cut
+__global__ void k1_active_units_kernel(const float4* __restrict__ sph, int nt, int nb, long long u_lo, long long u_hi,
+                                       float cut, int* __restrict__ list, int* __restrict__ count) {
+  __shared__ int wcount[32];
+  __shared__ int base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (long long c0 = u_lo; c0 < u_hi; c0 += blockDim.x) {
+    const long long u = c0 + threadIdx.x;
+    bool on = false;
+    if (u < u_hi) {
+      int bi, bj;
+      sym_unit_decode(u, nb, bi, bj);
+      const int na = min(SYM_S, nt - bi * SYM_S), nbj = min(SYM_S, nt - bj * SYM_S);
+      for (int a = 0; a < na && !on; ++a)
+        for (int b = (bi == bj) ? a : 0; b < nbj && !on; ++b) {
+          const float4 A = sph[bi * SYM_S + a], B = sph[bj * SYM_S + b];
+          const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
+          on = !(sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut);
+        }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) wcount[wid] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int q = 0; q < wid; ++q) off += wcount[q];
+    if (on) list[off + __popc(bal & ((1u << lane) - 1u))] = (int)u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int q = 0; q < nw; ++q) t += wcount[q];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base;
+}
+
+cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
+                                   int* count, cudaStream_t st) {
+  const int nt = (n + SYM_T - 1) / SYM_T;
+  const int nb = (nt + SYM_S - 1) / SYM_S;
+  k1_active_units_kernel<<<1, 1024, 0, st>>>(sph, nt, nb, u_lo, u_hi, cut, list, count);
+  return note_launch_err();
+}
+
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
-                              cudaStream_t st, const float4* sph, float cut, unsigned long long* done_pairs) {
+                              cudaStream_t st, const float4* sph, float cut, unsigned long long* done_pairs,
+                              const int* ulist, const int* ucount) {
   if (n <= 0 || u_end <= u_begin) return cudaSuccess;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
@@ -411,11 +469,11 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
   }
   switch (nu2) {
     case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
-                                                                         done_pairs); break;
+                                                                         done_pairs, ulist, ucount); break;
     case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
-                                                                         done_pairs); break;
+                                                                         done_pairs, ulist, ucount); break;
     case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
-                                                                         done_pairs); break;
+                                                                         done_pairs, ulist, ucount); break;
     default: return cudaErrorInvalidValue;
   }
   return note_launch_err();

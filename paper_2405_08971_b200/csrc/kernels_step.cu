@@ -18,58 +18,117 @@ namespace cakf {
 namespace {
 
 constexpr int kThreads = 256;
+// stage kernels: one 128-row tile per block, one row per thread (row-wise ops), 4 warps splitting the
+// columns of the column dots; per-block partial rows reduced in two deterministic levels
+constexpr int kTile = 128;
 
-__device__ __forceinline__ void block_rows(int N, int rb, int& r0, int& r1) {
-  r0 = blockIdx.x * rb;
-  r1 = min(N, r0 + rb);
-}
-
-// out[j] = sum_{rows in [r0, r1)} A[row + j*ld] * v[row]  (warp per column, fp32/64 lane sums, fp64 warp sums)
+// out[j] = sum_{rows of this tile} A[row + j*ld] * v[row]: each lane owns 4 rows; 8 columns per warp pass
+// (32 independent loads in flight per lane), lane sums fp32/fp64, cross-lane sums fp64 by a multi-value
+// butterfly (9 shuffles for 8 columns)
 template <typename T>
-__device__ void block_cols_dot(const T* __restrict__ A, size_t ld, int ncols, const T* __restrict__ v, int r0, int r1,
-                               double* __restrict__ out) {
+__device__ void tile_cols_dot(const T* __restrict__ A, size_t ld, int ncols, const T* __restrict__ v, int r0, int r1,
+                              double* __restrict__ out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  // four columns per warp pass: 4 independent accumulators keep 4x the loads in flight
-  int j = 4 * warp;
-  for (; j + 3 < ncols; j += 4 * nw) {
-    const T* c0 = A + (size_t)j * ld;
-    const T* c1 = c0 + ld;
-    const T* c2 = c1 + ld;
-    const T* c3 = c2 + ld;
-    T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
-    for (int row = r0 + lane; row < r1; row += 32) {
-      const T x = v[row];
-      a0 = fma(c0[row], x, a0);
-      a1 = fma(c1[row], x, a1);
-      a2 = fma(c2[row], x, a2);
-      a3 = fma(c3[row], x, a3);
-    }
-    const double s0 = warp_sum((double)a0), s1 = warp_sum((double)a1);
-    const double s2 = warp_sum((double)a2), s3 = warp_sum((double)a3);
-    if (lane == 0) {
-      out[j] = s0;
-      out[j + 1] = s1;
-      out[j + 2] = s2;
-      out[j + 3] = s3;
-    }
+  if (r1 <= r0) {
+    for (int j = threadIdx.x; j < ncols; j += blockDim.x) out[j] = 0.0;
+    return;
   }
-  // remaining columns (ncols % 4), one per warp
-  const int jt = ncols & ~3;
-  for (int jj = jt + warp; jj < ncols; jj += nw) {
-    const T* col = A + (size_t)jj * ld;
-    T acc = T(0);
-    for (int row = r0 + lane; row < r1; row += 32) acc = fma(col[row], v[row], acc);
-    const double s = warp_sum((double)acc);
-    if (lane == 0) out[jj] = s;
+  T x[4];
+  int rr[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int row = r0 + lane + 32 * q;
+    x[q] = row < r1 ? v[row] : T(0);
+    rr[q] = row < r1 ? row : r0;
+  }
+  for (int j = warp * 8; j < ncols; j += nw * 8) {
+    double w8[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      T acc = T(0);
+      if (j + c < ncols) {
+        const T* col = A + (size_t)(j + c) * ld;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc = fma(col[rr[q]], x[q], acc);
+      }
+      w8[c] = (double)acc;
+    }
+    // 8 -> 4 -> 2 -> 1 values per lane, then a 4-lane sum; lane holds column ((l>>4)&1)*4+((l>>3)&1)*2+((l>>2)&1)
+    double w4[4], w2[2];
+    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double send = h16 ? w8[c] : w8[c + 4], keep = h16 ? w8[c + 4] : w8[c];
+      w4[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const double send = h8 ? w4[c] : w4[c + 2], keep = h8 ? w4[c + 2] : w4[c];
+      w2[c] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    double t = (h4 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? w2[0] : w2[1], 4);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    const int col = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+    if ((lane & 3) == 0 && j + col < ncols) out[j + col] = t;
   }
 }
 
-__device__ void finalize_sum(int nb, int W, int n, const double* part, double* red) {
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += __ldcg(part + (size_t)b * W + j);
-    red[j] = s;
+// sum_j A[row + j*ld] c[j] in fp64 (c in shared memory); 16 independent loads in flight per thread
+template <typename T>
+__device__ __forceinline__ double row_gemv(const T* __restrict__ A, size_t ld, int ncols, const double* c, int row) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int j = 0;
+  for (; j + 16 <= ncols; j += 16) {
+    T x[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = A[row + (size_t)(j + q) * ld];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q & 3] = fma((double)x[q], c[j + q], acc[q & 3]);
   }
+  for (; j < ncols; ++j) acc[0] = fma((double)A[row + (size_t)j * ld], c[j], acc[0]);
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// Two-level deterministic reduction of the per-block partial rows part[b*W + j], j < n (no float atomics):
+// the last block of each group of gs consecutive blocks sums its group (ascending) into the group row
+// part[(nb + g)*W + j]; the last group sums the group rows (ascending) into red.  cnt[0] = top counter,
+// cnt[1 + g] = group counters (<= 32 groups), reset by their finalisers.  Returns true in exactly one block,
+// with red[0..n) written by that block (visible to it after the return).
+__device__ bool reduce_blocks(int n, int W, double* part, unsigned* cnt, double* red) {
+  __shared__ unsigned s_flag;
+  const int nb = gridDim.x;
+  const int gs = max(8, (nb + 31) / 32);
+  const int g = blockIdx.x / gs, ng = (nb + gs - 1) / gs;
+  const int b0 = g * gs, b1 = min(nb, b0 + gs);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_flag = atomicAdd(cnt + 1 + g, 1u) == (unsigned)(b1 - b0 - 1);
+  __syncthreads();
+  if (!s_flag) return false;
+  __threadfence();
+  double* grow = ng == 1 ? red : part + (size_t)(nb + g) * W;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double sum = 0.0;
+    for (int b = b0; b < b1; ++b) sum += __ldcg(part + (size_t)b * W + j);
+    grow[j] = sum;
+  }
+  if (threadIdx.x == 0) cnt[1 + g] = 0u;
+  __threadfence();
+  __syncthreads();
+  if (ng == 1) return true;
+  if (threadIdx.x == 0) s_flag = atomicAdd(cnt, 1u) == (unsigned)(ng - 1);
+  __syncthreads();
+  if (!s_flag) return false;
+  __threadfence();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double sum = 0.0;
+    for (int q = 0; q < ng; ++q) sum += __ldcg(part + (size_t)(nb + q) * W + j);
+    red[j] = sum;
+  }
+  if (threadIdx.x == 0) cnt[0] = 0u;
+  __syncthreads();
+  return true;
 }
 
 // ------------------------------------------------------------------ update prologue
@@ -96,63 +155,64 @@ __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __r
 
 // ------------------------------------------------------------------ stage A
 template <typename T>
-__global__ void __launch_bounds__(kThreads)
-stageA_kernel(int N, int rb, int nch, const T* __restrict__ partial, double sig00, const T* __restrict__ lam2,
+__global__ void __launch_bounds__(kTile)
+stageA_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const T* __restrict__ lam2,
               const T* __restrict__ s, const T* __restrict__ r, T* __restrict__ gp, const T* __restrict__ HM, int rin,
               double* __restrict__ part, int W, double* __restrict__ red, unsigned* cnt) {
   __shared__ double scratch[32 * 3];
-  int r0, r1;
-  block_rows(N, rb, r0, r1);
+  const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[3] = {0.0, 0.0, 0.0};  // s.r, s.g', r.r
-  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < nch; ++c) acc += (double)partial[(size_t)c * N + row];
+  if (row < r1) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    for (; c + 8 <= nch; c += 8) {
+      T x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = partial[(size_t)(c + q) * N + row];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q & 3] += (double)x[q];
+    }
+    for (; c < nch; ++c) acc[0] += (double)partial[(size_t)c * N + row];
+    const double ksum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     const T si = s[row], ri = r[row];
-    const T g = (T)(sig00 * acc) + lam2[row] * si;
+    const T g = (T)(sig00 * ksum) + lam2[row] * si;
     gp[row] = g;
-    a[0] += (double)si * (double)ri;
-    a[1] += (double)si * (double)g;
-    a[2] += (double)ri * (double)ri;
+    a[0] = (double)si * (double)ri;
+    a[1] = (double)si * (double)g;
+    a[2] = (double)ri * (double)ri;
   }
   block_sum<3>(a, scratch);
   double* slot = part + (size_t)blockIdx.x * W;
   if (threadIdx.x == 0) { slot[rin] = a[0]; slot[rin + 1] = a[1]; slot[rin + 2] = a[2]; }
-  block_cols_dot(HM, (size_t)N, rin, s, r0, r1, slot);          // u = (HM)^T s
-  if (arrive_last(cnt)) {
-    finalize_sum(gridDim.x, W, rin + 3, part, red);
-    if (threadIdx.x == 0) *cnt = 0u;
-  }
+  tile_cols_dot(HM, (size_t)N, rin, s, r0, r1, slot);            // u = (HM)^T s
+  reduce_blocks(rin + 3, W, part, cnt, red);
 }
 
 // ------------------------------------------------------------------ stage B
 template <typename T>
-__global__ void __launch_bounds__(kThreads)
-stageB_kernel(int N, int rb, const T* __restrict__ HM, int rin, const double* __restrict__ ured,
-              const T* __restrict__ gp, const T* __restrict__ s, T* __restrict__ g, const T* __restrict__ V, int nV,
-              double* __restrict__ part, int W, double* __restrict__ red, unsigned* cnt) {
+__global__ void __launch_bounds__(kTile)
+stageB_kernel(int N, const T* __restrict__ HM, int rin, const double* __restrict__ ured, const T* __restrict__ gp,
+              const T* __restrict__ s, T* __restrict__ g, const T* __restrict__ V, int nV, double* __restrict__ part,
+              int W, double* __restrict__ red, unsigned* cnt) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   double* u = reinterpret_cast<double*>(sm_raw);
   __shared__ double scratch[32];
+  __shared__ T gs_[kTile];
   for (int j = threadIdx.x; j < rin; j += blockDim.x) u[j] = ured[j];
   __syncthreads();
-  int r0, r1;
-  block_rows(N, rb, r0, r1);
+  const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[1] = {0.0};
-  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
-    double acc = 0.0;                                             // fp64: rin can be ~1e3
-    for (int j = 0; j < rin; ++j) acc = fma((double)HM[row + (size_t)j * N], (double)u[j], acc);
+  if (row < r1) {
+    const double acc = row_gemv(HM, (size_t)N, rin, u, row);     // fp64: rin can be ~1e3
     const T gi = (T)((double)gp[row] - acc);                      // G s
     g[row] = gi;
-    a[0] += (double)s[row] * (double)gi;
+    a[0] = (double)s[row] * (double)gi;
   }
   block_sum<1>(a, scratch);
   double* slot = part + (size_t)blockIdx.x * W;
   if (threadIdx.x == 0) slot[nV] = a[0];
-  block_cols_dot(V, (size_t)N, nV, g, r0, r1, slot);             // c = V^T G s
-  if (arrive_last(cnt)) {
-    finalize_sum(gridDim.x, W, nV + 1, part, red);
-    if (threadIdx.x == 0) *cnt = 0u;
-  }
+  tile_cols_dot(V, (size_t)N, nV, g, r0, r1, slot);               // c = V^T G s (g rows of this tile: own writes)
+  reduce_blocks(nV + 1, W, part, cnt, red);
 }
 
 // ------------------------------------------------------------------ stage C
@@ -161,8 +221,8 @@ stageB_kernel(int N, int rb, const T* __restrict__ HM, int rin, const double* __
 // pass == 0 (final pass): eta = s^T Gd (line 12) and the accept / reject decision (R2).
 // sin/gin may alias d/Gd (second pass runs in place), hence no __restrict__ on them.
 template <typename T>
-__global__ void __launch_bounds__(kThreads)
-stageC_kernel(int N, int rb, const T* __restrict__ V, const T* __restrict__ Z, int nV, const double* __restrict__ cred,
+__global__ void __launch_bounds__(kTile)
+stageC_kernel(int N, const T* __restrict__ V, const T* __restrict__ Z, int nV, const double* __restrict__ cred,
               const T* sin, const T* gin, T* d, T* Gd, const T* __restrict__ s_eta, const double* __restrict__ ared,
               int rin, const double* __restrict__ sgs, double* __restrict__ part, int W, double* __restrict__ red,
               unsigned* cnt, IterCtl* ctl, double eps, int iter, int pass) {
@@ -171,40 +231,30 @@ stageC_kernel(int N, int rb, const T* __restrict__ V, const T* __restrict__ Z, i
   __shared__ double scratch[32];
   for (int j = threadIdx.x; j < nV; j += blockDim.x) c[j] = cred[j];
   __syncthreads();
-  int r0, r1;
-  block_rows(N, rb, r0, r1);
+  const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[1] = {0.0};
-  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
-    double dv = (double)sin[row], gd = (double)gin[row];
-    for (int j = 0; j < nV; ++j) {
-      const double cj = c[j];
-      dv = fma(-(double)V[row + (size_t)j * N], cj, dv);         // d = (I - V V^T G) s   (line 11)
-      gd = fma(-(double)Z[row + (size_t)j * N], cj, gd);         // G d = G s - Z c
-    }
+  if (row < r1) {
+    const double dv = (double)sin[row] - row_gemv(V, (size_t)N, nV, c, row);   // d = (I - V V^T G) s  (line 11)
+    const double gd = (double)gin[row] - row_gemv(Z, (size_t)N, nV, c, row);   // G d = G s - Z c
     d[row] = (T)dv;
     Gd[row] = (T)gd;
-    a[0] += (double)s_eta[row] * gd;                              // eta = s^T G d        (line 12)
+    a[0] = (double)s_eta[row] * gd;                               // eta = s^T G d        (line 12)
   }
   if (pass == 1) {
-    __syncthreads();                                              // Gd of this block's rows visible
-    block_cols_dot(V, (size_t)N, nV, Gd, r0, r1, part + (size_t)blockIdx.x * W);   // c2 = V^T G d
-    if (arrive_last(cnt)) {
-      finalize_sum(gridDim.x, W, nV, part, red);
-      if (threadIdx.x == 0) *cnt = 0u;
-    }
+    __syncthreads();                                              // Gd of this tile visible to the block
+    tile_cols_dot(V, (size_t)N, nV, Gd, r0, r1, part + (size_t)blockIdx.x * W);   // c2 = V^T G d
+    reduce_blocks(nV, W, part, cnt, red);
     return;
   }
   block_sum<1>(a, scratch);
   if (threadIdx.x == 0) part[(size_t)blockIdx.x * W] = a[0];
-  if (arrive_last(cnt)) {
+  if (reduce_blocks(1, W, part, cnt, &ctl->eta)) {
     if (threadIdx.x == 0) {
-      double eta = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) eta += __ldcg(part + (size_t)b * W);
+      const double eta = ctl->eta;
       const double alpha = ared[rin];
       const double sGs = *sgs;
       const double floor_ = 64.0 * eps * fabs(sGs);
       const bool accept = eta > floor_ && isfinite(eta);
-      ctl->eta = eta;
       ctl->alpha = alpha;
       ctl->gamma = accept ? alpha / eta : 0.0;
       ctl->inv_sqrt_eta = accept ? 1.0 / sqrt(eta) : 0.0;
@@ -216,7 +266,6 @@ stageC_kernel(int N, int rb, const T* __restrict__ V, const T* __restrict__ Z, i
         ctl->rejected += 1;
       }
       if (!isfinite(eta) || !isfinite(alpha)) ctl->nonfinite = 1;
-      *cnt = 0u;
     }
   }
 }
@@ -247,24 +296,14 @@ __global__ void stageD_kernel(int N, int iter, int niter, const IterCtl* __restr
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads)
-dot_final_kernel(int N, int rb, const T* __restrict__ a_, const T* __restrict__ b_, double* part, double* out,
-                 unsigned* cnt) {
+__global__ void __launch_bounds__(kTile)
+dot_final_kernel(int N, const T* __restrict__ a_, const T* __restrict__ b_, double* part, double* out, unsigned* cnt) {
   __shared__ double scratch[32];
-  int r0, r1;
-  block_rows(N, rb, r0, r1);
-  double a[1] = {0.0};
-  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) a[0] += (double)a_[row] * (double)b_[row];
+  const int row = blockIdx.x * kTile + threadIdx.x;
+  double a[1] = {row < N ? (double)a_[row] * (double)b_[row] : 0.0};
   block_sum<1>(a, scratch);
   if (threadIdx.x == 0) part[blockIdx.x] = a[0];
-  if (arrive_last(cnt)) {
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(part + b);
-      *out = t;
-      *cnt = 0u;
-    }
-  }
+  reduce_blocks(1, 1, part, cnt, out);
 }
 
 // ------------------------------------------------------------------ gathers / mixing
@@ -554,11 +593,7 @@ inline unsigned nblk(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t)
 
 }  // namespace
 
-int rows_per_block(int N) {
-  int rb = (N + 295) / 296;
-  rb = ((rb + 31) / 32) * 32;
-  return rb < 32 ? 32 : rb;
-}
+int stage_blocks(int N) { return N > 0 ? (N + kTile - 1) / kTile : 1; }
 
 template <typename T>
 cudaError_t StepKernels<T>::prep(int N, const int* idx, const V4<T>* coords, const T* y, const T* mpred, int policy,
@@ -573,18 +608,16 @@ template <typename T>
 cudaError_t StepKernels<T>::stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s,
                                    const T* r, T* gp, const T* HM, int rin, double* part, int W, double* red,
                                    unsigned* cnt, cudaStream_t st) {
-  const int rb = rows_per_block(N);
-  stageA_kernel<T><<<nblk(N, rb), kThreads, 0, st>>>(N, rb, nch, partial, sig00, lam2, s, r, gp, HM, rin, part, W,
-                                                     red, cnt);
+  stageA_kernel<T><<<stage_blocks(N), kTile, 0, st>>>(N, nch, partial, sig00, lam2, s, r, gp, HM, rin, part, W, red,
+                                                      cnt);
   return note_launch_err();
 }
 
 template <typename T>
 cudaError_t StepKernels<T>::stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g,
                                    const T* V, int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st) {
-  const int rb = rows_per_block(N);
-  stageB_kernel<T><<<nblk(N, rb), kThreads, sizeof(double) * (rin > 0 ? rin : 1), st>>>(N, rb, HM, rin, ured, gp, s, g, V,
-                                                                                   nV, part, W, red, cnt);
+  stageB_kernel<T><<<stage_blocks(N), kTile, sizeof(double) * (rin > 0 ? rin : 1), st>>>(N, HM, rin, ured, gp, s, g,
+                                                                                       V, nV, part, W, red, cnt);
   return note_launch_err();
 }
 
@@ -593,9 +626,8 @@ cudaError_t StepKernels<T>::stageC(int N, const T* V, const T* Z, int nV, const 
                                    const T* gin, T* d, T* Gd, const T* s_eta, const double* ared, int rin,
                                    const double* sgs, double* part, int W, double* red, unsigned* cnt, IterCtl* ctl,
                                    double eps, int iter, int pass, cudaStream_t st) {
-  const int rb = rows_per_block(N);
-  stageC_kernel<T><<<nblk(N, rb), kThreads, sizeof(double) * (nV > 0 ? nV : 1), st>>>(
-      N, rb, V, Z, nV, cred, sin, gin, d, Gd, s_eta, ared, rin, sgs, part, W, red, cnt, ctl, eps, iter, pass);
+  stageC_kernel<T><<<stage_blocks(N), kTile, sizeof(double) * (nV > 0 ? nV : 1), st>>>(
+      N, V, Z, nV, cred, sin, gin, d, Gd, s_eta, ared, rin, sgs, part, W, red, cnt, ctl, eps, iter, pass);
   return note_launch_err();
 }
 
@@ -611,8 +643,7 @@ cudaError_t StepKernels<T>::stageD(int N, int iter, int niter, const IterCtl* ct
 template <typename T>
 cudaError_t StepKernels<T>::dot(int N, const T* a, const T* b, double* part, double* out, unsigned* cnt,
                                 cudaStream_t st) {
-  const int rb = rows_per_block(N);
-  dot_final_kernel<T><<<nblk(N, rb), kThreads, 0, st>>>(N, rb, a, b, part, out, cnt);
+  dot_final_kernel<T><<<stage_blocks(N), kTile, 0, st>>>(N, a, b, part, out, cnt);
   return note_launch_err();
 }
 

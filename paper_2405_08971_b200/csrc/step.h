@@ -18,7 +18,7 @@ struct IterCtl {
   int n_acc, rejected, nonfinite, pad;
 };
 
-int rows_per_block(int N);
+int stage_blocks(int N);   // blocks (128-row tiles) of the stage kernels
 cudaError_t idx64_to32(int n, const int64_t* in, int* out, cudaStream_t st);
 // observations -> internal point order: idx_out ascending, sigma[j] = user position, sigma_inv inverse
 cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int* posof, int* counts, int* idx_out,
