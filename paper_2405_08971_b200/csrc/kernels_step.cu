@@ -41,17 +41,33 @@ __device__ void tile_cols_dot(const T* __restrict__ A, size_t ld, int ncols, con
     x[q] = row < r1 ? v[row] : T(0);
     rr[q] = row < r1 ? row : r0;
   }
+  const int nfull = ncols & ~7;
   for (int j = warp * 8; j < ncols; j += nw * 8) {
     double w8[8];
+    if (j < nfull) {   // full group: all 32 loads issued before the first use
+      T xv[8][4];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      T acc = T(0);
-      if (j + c < ncols) {
-        const T* col = A + (size_t)(j + c) * ld;
+      for (int c = 0; c < 8; ++c)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc = fma(col[rr[q]], x[q], acc);
+        for (int q = 0; q < 4; ++q) xv[c][q] = A[(size_t)(j + c) * ld + rr[q]];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        T acc = T(0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc = fma(xv[c][q], x[q], acc);
+        w8[c] = (double)acc;
       }
-      w8[c] = (double)acc;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        T acc = T(0);
+        if (j + c < ncols) {
+          const T* col = A + (size_t)(j + c) * ld;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc = fma(col[rr[q]], x[q], acc);
+        }
+        w8[c] = (double)acc;
+      }
     }
     // 8 -> 4 -> 2 -> 1 values per lane, then a 4-lane sum; lane holds column ((l>>4)&1)*4+((l>>3)&1)*2+((l>>2)&1)
     double w4[4], w2[2];
@@ -79,12 +95,19 @@ template <typename T>
 __device__ __forceinline__ double row_gemv(const T* __restrict__ A, size_t ld, int ncols, const double* c, int row) {
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   int j = 0;
-  for (; j + 16 <= ncols; j += 16) {
-    T x[16];
+  for (; j + 32 <= ncols; j += 32) {
+    T x[32];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) x[q] = A[row + (size_t)(j + q) * ld];
+    for (int q = 0; q < 32; ++q) x[q] = A[row + (size_t)(j + q) * ld];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q & 3] = fma((double)x[q], c[j + q], acc[q & 3]);
+    for (int q = 0; q < 32; ++q) acc[q & 3] = fma((double)x[q], c[j + q], acc[q & 3]);
+  }
+  for (; j + 8 <= ncols; j += 8) {
+    T x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = A[row + (size_t)(j + q) * ld];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q & 3] = fma((double)x[q], c[j + q], acc[q & 3]);
   }
   for (; j < ncols; ++j) acc[0] = fma((double)A[row + (size_t)j * ld], c[j], acc[0]);
   return (acc[0] + acc[1]) + (acc[2] + acc[3]);
@@ -165,12 +188,12 @@ stageA_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const
   if (row < r1) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     int c = 0;
-    for (; c + 8 <= nch; c += 8) {
-      T x[8];
+    for (; c + 16 <= nch; c += 16) {
+      T x[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) x[q] = partial[(size_t)(c + q) * N + row];
+      for (int q = 0; q < 16; ++q) x[q] = partial[(size_t)(c + q) * N + row];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q & 3] += (double)x[q];
+      for (int q = 0; q < 16; ++q) acc[q & 3] += (double)x[q];
     }
     for (; c < nch; ++c) acc[0] += (double)partial[(size_t)c * N + row];
     const double ksum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
