@@ -48,6 +48,23 @@ template <int NU2> __device__ __forceinline__ float matern_from_d2(float d2) {
   else if constexpr (NU2 == 3) return fmaf(a, e, e);
   else return e * fmaf(a, fmaf(a, 1.0f / 3.0f, 1.0f), 1.0f);
 }
+// packed pair version (sm_100 f32x2 FMA-pipe ops; the two MUFU ops per value stay scalar).  Same
+// arithmetic as matern_from_d2<NU2>(float) value by value.
+template <int NU2> __device__ __forceinline__ float2 matern2_from_d2(float2 d2) {
+  float2 a, e;
+  a.x = sqrt_approx(d2.x);
+  a.y = sqrt_approx(d2.y);
+  const float2 t = __fmul2_rn(a, make_float2(-kLog2e, -kLog2e));
+  e.x = ex2_approx(t.x);
+  e.y = ex2_approx(t.y);
+  if constexpr (NU2 == 1) return e;
+  else if constexpr (NU2 == 3) return __ffma2_rn(a, e, e);
+  else {
+    const float2 p = __ffma2_rn(a, __ffma2_rn(a, make_float2(1.0f / 3.0f, 1.0f / 3.0f), make_float2(1.f, 1.f)),
+                                make_float2(1.f, 1.f));
+    return __fmul2_rn(e, p);
+  }
+}
 template <int NU2> __device__ __forceinline__ double matern_from_d2(double d2) {
   const double a = sqrt(d2);
   const double e = exp(-a);

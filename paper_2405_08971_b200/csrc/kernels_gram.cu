@@ -115,12 +115,21 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
     const bool diag = bi == bj;
     const int na = min(SYM_S, nt - bi * SYM_S), nbj = min(SYM_S, nt - bj * SYM_S);
     __syncthreads();
-    for (int e = tid; e < SYM_S * SYM_T; e += 256) {
-      const int gi = bi * SYM_S * SYM_T + e, gj = bj * SYM_S * SYM_T + e;
-      tI[e] = gi < n ? x[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (!diag) tJ[e] = gj < n ? x[gj] : make_float4(0.f, 0.f, 0.f, 0.f);
-      rowacc[e] = 0.f;
+    // tiles stored as point pairs {x0,x1,y0,y1},{z0,z1,s0,s1} so the packed f32x2 operands load ready-paired
+    for (int e = tid; e < SYM_S * SYM_T / 2; e += 256) {
+      const int gi = bi * SYM_S * SYM_T + 2 * e, gj = bj * SYM_S * SYM_T + 2 * e;
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 p0 = gi < n ? x[gi] : z4, p1 = gi + 1 < n ? x[gi + 1] : z4;
+      tI[2 * e] = make_float4(p0.x, p1.x, p0.y, p1.y);
+      tI[2 * e + 1] = make_float4(p0.z, p1.z, p0.w, p1.w);
+      if (!diag) {
+        p0 = gj < n ? x[gj] : z4;
+        p1 = gj + 1 < n ? x[gj + 1] : z4;
+        tJ[2 * e] = make_float4(p0.x, p1.x, p0.y, p1.y);
+        tJ[2 * e + 1] = make_float4(p0.z, p1.z, p0.w, p1.w);
+      }
     }
+    for (int e = tid; e < SYM_S * SYM_T; e += 256) rowacc[e] = 0.f;
 #pragma unroll
     for (int b = 0; b < SYM_S; ++b)
 #pragma unroll
@@ -128,12 +137,17 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
     const float4* sJ = diag ? tI : tJ;
     __syncthreads();
     for (int a = 0; a < na; ++a) {
-      float rx[8], ry[8], rz[8], rs[8], racc[8];
+      // rows kept negated (d = c - r) as scalars: the packed f32x2 ops broadcast a scalar operand
+      float nrx[8], nry[8], nrz[8], rs[8];
+      float2 racc2[8];   // per row: even / odd column partial sums
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 v = tI[a * SYM_T + ty * 8 + q];
-        rx[q] = v.x; ry[q] = v.y; rz[q] = v.z; rs[q] = v.w; racc[q] = 0.f;
+      for (int h = 0; h < 4; ++h) {
+        const float4 A = tI[(a * SYM_T / 2 + ty * 4 + h) * 2], B = tI[(a * SYM_T / 2 + ty * 4 + h) * 2 + 1];
+        nrx[2 * h] = -A.x; nrx[2 * h + 1] = -A.y; nry[2 * h] = -A.z; nry[2 * h + 1] = -A.w;
+        nrz[2 * h] = -B.x; nrz[2 * h + 1] = -B.y; rs[2 * h] = B.z; rs[2 * h + 1] = B.w;
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) racc2[q] = make_float2(0.f, 0.f);
       for (int b = diag ? a : 0; b < nbj; ++b) {
         if (sph) {   // exact-zero culling: every kernel value of this tile pair underflows to 0 in fp32
           const float4 A = sph[bi * SYM_S + a], B = sph[bj * SYM_S + b];
@@ -142,22 +156,32 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
           if (tid == 0 && done_pairs) atomicAdd(done_pairs, 1ull);
         }
         const bool offdiag = !(diag && a == b);
-        float cx[8], cy[8], cz[8], cs[8], cacc[8];
+        // 8 columns as 4 packed pairs: every elementwise op below is one FADD2 / FMUL2 / FFMA2 for two
+        // pairs, leaving the two MUFU ops per pair (sqrt, ex2) as the only scalar work
+        float2 cx2[4], cy2[4], cz2[4], cs2[4], cacc2[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 v = sJ[b * SYM_T + tx * 8 + q];
-          cx[q] = v.x; cy[q] = v.y; cz[q] = v.z; cs[q] = v.w; cacc[q] = 0.f;
+        for (int q = 0; q < 4; ++q) {
+          const float4 A = sJ[(b * SYM_T / 2 + tx * 4 + q) * 2], B = sJ[(b * SYM_T / 2 + tx * 4 + q) * 2 + 1];
+          cx2[q] = make_float2(A.x, A.y); cy2[q] = make_float2(A.z, A.w);
+          cz2[q] = make_float2(B.x, B.y); cs2[q] = make_float2(B.z, B.w);
+          cacc2[q] = make_float2(0.f, 0.f);
         }
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float dx = rx[r] - cx[c], dy = ry[r] - cy[c], dz = rz[r] - cz[c];
-            const float k = matern_from_d2<NU2>(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
-            racc[r] = fmaf(k, cs[c], racc[r]);
-            cacc[c] = fmaf(k, rs[r], cacc[c]);
+          for (int q = 0; q < 4; ++q) {
+            const float2 dx = __fadd2_rn(cx2[q], make_float2(nrx[r], nrx[r]));
+            const float2 dy = __fadd2_rn(cy2[q], make_float2(nry[r], nry[r]));
+            const float2 dz = __fadd2_rn(cz2[q], make_float2(nrz[r], nrz[r]));
+            const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+            const float2 k = matern2_from_d2<NU2>(d2);
+            racc2[r] = __ffma2_rn(k, cs2[q], racc2[r]);
+            cacc2[q] = __ffma2_rn(k, make_float2(rs[r], rs[r]), cacc2[q]);
           }
         }
+        float cacc[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { cacc[2 * q] = cacc2[q].x; cacc[2 * q + 1] = cacc2[q].y; }
         if (offdiag) {   // column sums of this tile pair into this thread's private slots (no barrier)
           float4* m4 = reinterpret_cast<float4*>(mycol + b * SYM_T);
           float4 u0 = m4[0], u1 = m4[1];
@@ -170,7 +194,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
       // row sums over the unit's J tiles: reduce over tx (16 lanes of a half-warp)
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        float v = racc[r];
+        float v = racc2[r].x + racc2[r].y;
         v += __shfl_xor_sync(0xffffffffu, v, 8);
         v += __shfl_xor_sync(0xffffffffu, v, 4);
         v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -457,7 +481,7 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
   if (n <= 0 || u_end <= u_begin) return cudaSuccess;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
-  const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * 3);
+  static int per_sm = 0;   // resident CTAs per SM (one full wave; the units are strided over it)
   const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)SYM_S * SYM_T * sizeof(float) +
                       (size_t)16 * SYM_S * SYM_T * sizeof(float);
   static bool configured = false;
@@ -465,8 +489,15 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
     cudaFuncSetAttribute(matvec_sym_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(matvec_sym_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(matvec_sym_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(matvec_sym_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(matvec_sym_kernel<3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(matvec_sym_kernel<5>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, matvec_sym_kernel<3>, 256, smem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
     configured = true;
   }
+  const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);
   switch (nu2) {
     case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
                                                                          done_pairs, ulist, ucount); break;
