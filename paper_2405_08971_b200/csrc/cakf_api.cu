@@ -222,7 +222,8 @@ struct Impl final : ImplBase {
   float4 *sph_x128 = nullptr, *sph_x32 = nullptr, *sph_o128 = nullptr, *sph_o32 = nullptr;
   int *act_cnt_sm = nullptr, *act_list_sm = nullptr, *act_cnt_po = nullptr, *act_list_po = nullptr;
   int act_stride_sm = 0, act_stride_po = 0;
-  int *k1_list = nullptr, *k1_count = nullptr;  // active symmetric K1 units of this update
+  int *k1_list = nullptr, *k1_count = nullptr;
+  unsigned short* k1_mask = nullptr;  // active symmetric K1 units of this update
   unsigned long long* cull_ctr = nullptr;  // [0] K1 tile pairs done, [1] K2-post blocks, [2] K2-smooth blocks
   double k1_pairs_dense = 0, k2_post_dense = 0, k2_sm_dense = 0;
   int64_t k2_sm_launches = 0;
@@ -502,6 +503,7 @@ struct Impl final : ImplBase {
       act_cnt_po = carve<int>(nx128); act_list_po = carve<int>((size_t)nx128 * no32);
       cull_ctr = carve<unsigned long long>(4);
       k1_list = carve<int>((size_t)matvec_sym_units((int)Nmax) + 1);
+      k1_mask = carve<unsigned short>((size_t)matvec_sym_units((int)Nmax) + 1);
       k1_count = carve<int>(1);
     }
   }
@@ -705,7 +707,7 @@ struct Impl final : ImplBase {
       if (sym) {  // active K1 units of this rank; the skipped units' partial slots stay zero
         const long long U = matvec_sym_units(N);
         CK_CUDA(launch_k1_active_units(sph_o128, N, U * rank / world, U * (rank + 1) / world, kCullCut, k1_list,
-                                       k1_count, st));
+                                       k1_mask, k1_count, st));
         CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)matvec_sym_tiles(N) * N * sizeof(T), st));
       }
     }
@@ -722,8 +724,8 @@ struct Impl final : ImplBase {
         if (sym) {
           const long long U = matvec_sym_units(N);
           CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
-                                    U * rank / world, U * (rank + 1) / world, st, cull ? sph_o128 : nullptr,
-                                    kCullCut, cull ? cull_ctr : nullptr, cull ? k1_list : nullptr, k1_count));
+                                    U * rank / world, U * (rank + 1) / world, st, cull ? cull_ctr : nullptr,
+                                    cull ? k1_list : nullptr, k1_count, k1_mask));
           if (cull) {
             const double nt = (double)((N + 127) / 128);
             k1_pairs_dense += nt * (nt + 1) / 2 / world;

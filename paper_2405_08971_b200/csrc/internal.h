@@ -19,15 +19,15 @@ int matvec_chunks(int nrows, int ncols, int elem_bytes);
 int matvec_sym_tiles(int n);
 long long matvec_sym_units(int n);   // number of symmetric tile-block work units
 int matvec_sym_block_points();       // points per tile block of the symmetric K1
-// sph != nullptr: skip tile pairs whose bounding spheres are > cut apart (all values exactly 0),
-// counting the evaluated 128 x 128 tile pairs in *done_pairs (nullable)
+// ulist != nullptr (exact-zero culling): evaluate only the *ucount units ulist[w] (ascending), and in each
+// only the tile pairs set in umask[w] (bit a*4+b); the skipped units' partial slots must hold zeros.
+// done_pairs (nullable) accumulates the evaluated 128 x 128 tile pairs.
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
-                              cudaStream_t st, const float4* sph = nullptr, float cut = 0.f,
-                              unsigned long long* done_pairs = nullptr, const int* ulist = nullptr,
-                              const int* ucount = nullptr);
-// compact ascending list of the sym units in [u_lo, u_hi) with a tile pair within `cut` (device count)
+                              cudaStream_t st, unsigned long long* done_pairs = nullptr, const int* ulist = nullptr,
+                              const int* ucount = nullptr, const unsigned short* umask = nullptr);
+// compact ascending list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
-                                   int* count, cudaStream_t st);
+                                   unsigned short* mask, int* count, cudaStream_t st);
 // bounding spheres (x, y, z, radius) of consecutive tiles of `tile` points
 cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st);
 // fp32 exact-zero cut: a prescaled distance above which ex2.approx.ftz(-a log2 e) flushes to 0

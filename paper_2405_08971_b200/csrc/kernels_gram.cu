@@ -94,9 +94,9 @@ __device__ __forceinline__ void sym_unit_decode(long long u, int nb, int& bi, in
 template <int NU2>
 __global__ void __launch_bounds__(256)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
-                  float* __restrict__ partial, const float4* __restrict__ sph, float cut,
+                  float* __restrict__ partial,
                   unsigned long long* __restrict__ done_pairs, const int* __restrict__ ulist,
-                  const int* __restrict__ ucount) {
+                  const int* __restrict__ ucount, const unsigned short* __restrict__ umask) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
   float4* tJ = tI + SYM_S * SYM_T;                                    // [SYM_S][128]
@@ -109,6 +109,9 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
   const long long nwork = ulist ? (long long)*ucount : u_end - u_begin;
   for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
     const long long u = ulist ? (long long)ulist[w] : u_begin + w;
+    // active tile pairs of this unit, bit a*SYM_S+b (exact-zero culling; all ones without)
+    const unsigned amask = ulist ? (unsigned)umask[w] : 0xFFFFu;
+    if (tid == 0 && done_pairs) atomicAdd(done_pairs, (unsigned long long)__popc(amask));
     // u -> (bi, bj), bi <= bj, row-major over the upper triangle of blocks
     int bi, bj;
     sym_unit_decode(u, nb, bi, bj);
@@ -149,12 +152,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
 #pragma unroll
       for (int q = 0; q < 8; ++q) racc2[q] = make_float2(0.f, 0.f);
       for (int b = diag ? a : 0; b < nbj; ++b) {
-        if (sph) {   // exact-zero culling: every kernel value of this tile pair underflows to 0 in fp32
-          const float4 A = sph[bi * SYM_S + a], B = sph[bj * SYM_S + b];
-          const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
-          if (sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut) continue;
-          if (tid == 0 && done_pairs) atomicAdd(done_pairs, 1ull);
-        }
+        if (!((amask >> (a * SYM_S + b)) & 1u)) continue;   // every value of this tile pair is exactly 0
         const bool offdiag = !(diag && a == b);
         // 8 columns as 4 packed pairs: every elementwise op below is one FADD2 / FMUL2 / FFMA2 for two
         // pairs, leaving the two MUFU ops per pair (sqrt, ex2) as the only scalar work
@@ -428,56 +426,66 @@ long long matvec_sym_units(int n) {
   return nb * (nb + 1) / 2;
 }
 
-// one block: ascending compact list of the units in [u_lo, u_hi) with at least one tile pair within the cut
+// tile-pair activity mask of unit u (bit a*SYM_S+b): pairs whose bounding spheres are within `cut`
+__device__ unsigned sym_unit_mask(const float4* __restrict__ sph, int nt, int nb, long long u, float cut) {
+  int bi, bj;
+  sym_unit_decode(u, nb, bi, bj);
+  const int na = min(SYM_S, nt - bi * SYM_S), nbj = min(SYM_S, nt - bj * SYM_S);
+  unsigned m = 0;
+  for (int a = 0; a < na; ++a)
+    for (int b = (bi == bj) ? a : 0; b < nbj; ++b) {
+      const float4 A = sph[bi * SYM_S + a], B = sph[bj * SYM_S + b];
+      const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
+      if (!(sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut)) m |= 1u << (a * SYM_S + b);
+    }
+  return m;
+}
+
+// one block: compact list of the units in [u_lo, u_hi) with at least one active tile pair, ordered by
+// decreasing number of active pairs (longest first, so the strided assignment of the K1 grid balances);
+// the order inside a bucket is arbitrary, which cannot change any result (each unit owns its partial slots)
 __global__ void k1_active_units_kernel(const float4* __restrict__ sph, int nt, int nb, long long u_lo, long long u_hi,
-                                       float cut, int* __restrict__ list, int* __restrict__ count) {
-  __shared__ int wcount[32];
-  __shared__ int base;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (threadIdx.x == 0) base = 0;
+                                       float cut, int* __restrict__ list, unsigned short* __restrict__ mask,
+                                       int* __restrict__ count) {
+  __shared__ int bucket[SYM_S * SYM_S + 1];
+  if (threadIdx.x <= SYM_S * SYM_S) bucket[threadIdx.x] = 0;
   __syncthreads();
-  for (long long c0 = u_lo; c0 < u_hi; c0 += blockDim.x) {
-    const long long u = c0 + threadIdx.x;
-    bool on = false;
-    if (u < u_hi) {
-      int bi, bj;
-      sym_unit_decode(u, nb, bi, bj);
-      const int na = min(SYM_S, nt - bi * SYM_S), nbj = min(SYM_S, nt - bj * SYM_S);
-      for (int a = 0; a < na && !on; ++a)
-        for (int b = (bi == bj) ? a : 0; b < nbj && !on; ++b) {
-          const float4 A = sph[bi * SYM_S + a], B = sph[bj * SYM_S + b];
-          const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
-          on = !(sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut);
-        }
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, on);
-    if (lane == 0) wcount[wid] = __popc(bal);
-    __syncthreads();
-    int off = base;
-    for (int q = 0; q < wid; ++q) off += wcount[q];
-    if (on) list[off + __popc(bal & ((1u << lane) - 1u))] = (int)u;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int q = 0; q < nw; ++q) t += wcount[q];
-      base += t;
-    }
-    __syncthreads();
+  for (long long u = u_lo + threadIdx.x; u < u_hi; u += blockDim.x) {
+    const unsigned m = sym_unit_mask(sph, nt, nb, u, cut);
+    if (m) atomicAdd(&bucket[__popc(m)], 1);
   }
-  if (threadIdx.x == 0) *count = base;
+  __syncthreads();
+  if (threadIdx.x == 0) {   // exclusive offsets, 16 active pairs first
+    int run = 0;
+    for (int c = SYM_S * SYM_S; c >= 1; --c) {
+      const int t = bucket[c];
+      bucket[c] = run;
+      run += t;
+    }
+    *count = run;
+  }
+  __syncthreads();
+  for (long long u = u_lo + threadIdx.x; u < u_hi; u += blockDim.x) {
+    const unsigned m = sym_unit_mask(sph, nt, nb, u, cut);
+    if (m) {
+      const int pos = atomicAdd(&bucket[__popc(m)], 1);
+      list[pos] = (int)u;
+      mask[pos] = (unsigned short)m;
+    }
+  }
 }
 
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
-                                   int* count, cudaStream_t st) {
+                                   unsigned short* mask, int* count, cudaStream_t st) {
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
-  k1_active_units_kernel<<<1, 1024, 0, st>>>(sph, nt, nb, u_lo, u_hi, cut, list, count);
+  k1_active_units_kernel<<<1, 1024, 0, st>>>(sph, nt, nb, u_lo, u_hi, cut, list, mask, count);
   return note_launch_err();
 }
 
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
-                              cudaStream_t st, const float4* sph, float cut, unsigned long long* done_pairs,
-                              const int* ulist, const int* ucount) {
+                              cudaStream_t st, unsigned long long* done_pairs, const int* ulist,
+                              const int* ucount, const unsigned short* umask) {
   if (n <= 0 || u_end <= u_begin) return cudaSuccess;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
@@ -499,12 +507,12 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
   }
   const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);
   switch (nu2) {
-    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
-                                                                         done_pairs, ulist, ucount); break;
-    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
-                                                                         done_pairs, ulist, ucount); break;
-    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, sph, cut,
-                                                                         done_pairs, ulist, ucount); break;
+    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
+                                                                         done_pairs, ulist, ucount, umask); break;
+    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
+                                                                         done_pairs, ulist, ucount, umask); break;
+    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
+                                                                         done_pairs, ulist, ucount, umask); break;
     default: return cudaErrorInvalidValue;
   }
   return note_launch_err();
