@@ -215,6 +215,14 @@ struct Impl final : ImplBase {
   T *X = nullptr, *Yk = nullptr, *yb = nullptr, *Tm = nullptr, *Hy = nullptr, *tt = nullptr, *R = nullptr;
   T *Wf = nullptr, *Ws = nullptr, *ws = nullptr, *pvar = nullptr;
   float* tcw = nullptr;  // bf16 planes of the K2 right-hand sides
+  // low-rank contractions on tcgen05 (kernels_gemm_tc.cu): operand planes, split-K work, fp32 Q_r
+  // (truncation always; the post-loop / smoother contractions only with CAKF_LOWRANK_TC=1 — fp32
+  // accumulation there misses the cfg1 1e-4 bound under the variance cancellation)
+  bool lowrank_tc = [] { const char* e = getenv("CAKF_LOWRANK_TC"); return e && e[0] == '1'; }();
+  bool gram_tc = [] { const char* e = getenv("CAKF_GRAM_TC"); return e && e[0] == '1'; }();
+  uint16_t *gpA = nullptr, *gpB = nullptr;
+  size_t gp_elems = 0;
+  float *gwork = nullptr, *Qf = nullptr;
 
   // ---------------- exact-zero culling (fp32 only): tile bounding spheres and, per 128-row
   // output tile of K2, the ascending list of 32-column K-blocks not entirely below the fp32 underflow
@@ -454,9 +462,11 @@ struct Impl final : ImplBase {
                                (size_t)std::max(rin_max, 1) * C1, (size_t)std::max(nhat, 1) * C1,
                                (size_t)cmax * (size_t)std::max(rcap, 1), (size_t)Nmax * (size_t)(1 + nhat),
                                (size_t)std::max(rin_max, 1) * (size_t)(1 + nhat)});
-      dA = carve<double>(dscr);
-      dB = carve<double>(dscr);
-      dC = carve<double>(dscr);
+      {   // fp64 staging of the DGEMM contractions
+        dA = carve<double>(dscr);
+        dB = carve<double>(dscr);
+        dC = carve<double>(dscr);
+      }
     }
     const size_t C = 1 + qmax;
     X = carve<T>((size_t)D * C);
@@ -492,6 +502,11 @@ struct Impl final : ImplBase {
       const size_t wb = std::max(gram_gemm_tc_workspace((int)Nmax, 1 + nhat),
                                  gram_gemm_tc_workspace((int)NX, Dp * (1 + qmax)));
       tcw = carve<float>(wb / sizeof(float) + 64);
+      gp_elems = 3 * (dscr + 8 * (size_t)std::max<int64_t>({D, Nmax, (int64_t)cmax}) + 64);
+      gpA = carve<uint16_t>(gp_elems);
+      gpB = carve<uint16_t>(gp_elems);
+      gwork = carve<float>(kGemmWorkFloats);
+      if (rcap >= 0) Qf = carve<float>((size_t)cmax * std::max(rcap, 1));
     }
     if (cull) {
       const int nx128 = (int)((NX + 127) / 128), nx32 = (int)((NX + 31) / 32);
@@ -790,6 +805,15 @@ struct Impl final : ImplBase {
       const double* Bp = Bd ? Bd : reinterpret_cast<const double*>(B);
       CK_BLAS(cublasDgemm(blas, ta, tb, m, n, k, &alpha, reinterpret_cast<const double*>(A), lda, Bp, ldb, &beta,
                           reinterpret_cast<double*>(C), ldc));
+    } else if (lowrank_tc) {
+      // tcgen05 3xBF16 (kernels_gemm_tc.cu): op(A) rows m and op(B)^T rows n as K-major planes
+      if (Bd) return fail(CAKF_E_ARG, "gemm: fp64 right operand on the tensor-core path");
+      if (gemm_tc_plane_bytes(m, k) > gp_elems * 2 || gemm_tc_plane_bytes(n, k) > gp_elems * 2)
+        return fail(CAKF_E_ARG, "gemm: operand planes too small");
+      CK_CUDA(gemm_tc_split(reinterpret_cast<const float*>(A), m, k, (size_t)lda, ta == CUBLAS_OP_T, gpA, st));
+      CK_CUDA(gemm_tc_split(reinterpret_cast<const float*>(B), n, k, (size_t)ldb, tb == CUBLAS_OP_N, gpB, st));
+      CK_CUDA(gemm_tc_run(gpA, m, gpB, n, k, alpha, beta, reinterpret_cast<float*>(C), nullptr, (size_t)ldc, gwork,
+                          kGemmWorkFloats, st));
     } else {
       const int ar = ta == CUBLAS_OP_N ? m : k, ac = ta == CUBLAS_OP_N ? k : m;
       const int br = tb == CUBLAS_OP_N ? k : n, bc = tb == CUBLAS_OP_N ? n : k;
@@ -818,9 +842,41 @@ struct Impl final : ImplBase {
     return gemm_impl(ta, tb, m, n, k, alpha, A, lda, B, nullptr, ldb, beta, C, ldc);
   }
 
+  // fp32 truncation on tcgen05: Gram F^T F (3xBF16, K split, fp64 reduction) -> fp64 eig -> F Q_r
+  int truncate_factor_tc(const float* F, int c, int rkeep, float* out, double* kept, double* dropped, size_t pk) {
+    size_t ps = prof_begin();
+    if (gemm_tc_plane_bytes((int)D, c) > gp_elems * 2) return fail(CAKF_E_ARG, "truncate: operand planes too small");
+    if (gram_tc) {
+      CK_CUDA(gemm_tc_split(F, c, (int)D, (size_t)D, true, gpA, st));          // F^T rows (K = D contiguous)
+      CK_CUDA(gemm_tc_run(gpA, c, gpA, c, (int)D, 1.0, 0.0, nullptr, Gm, (size_t)c, gwork, kGemmWorkFloats, st));
+    } else {   // the Gram decides the kept subspace: fp32 products, fp64 accumulation (DGEMM)
+      if ((size_t)D * c > dscr) return fail(CAKF_E_ARG, "truncate: fp64 scratch too small");
+      CK_CUDA((convert<float, double>)((int)D, c, F, D, dA, D, st));
+      const double one = 1.0, zero = 0.0;
+      CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c, c, (int)D, &one, dA, (int)D, dA, (int)D, &zero, Gm, c));
+    }
+    prof_end(CAKF_PROF_TRUNC_GRAM, ps);
+    ps = prof_begin();
+    CK_SOLVER(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, c, Gm, c, eigw, work, lwork, info));
+    CK_CUDA(StepKernels<double>::take_top(c, rkeep, Gm, eigw, QrD, kept, dropped, st));
+    prof_end(CAKF_PROF_TRUNC_EIG, ps);
+    ps = prof_begin();
+    CK_CUDA((convert<double, float>)(c, rkeep, QrD, c, Qf, c, st));
+    CK_CUDA(gemm_tc_split(F, (int)D, c, (size_t)D, false, gpA, st));           // F rows (K = c, transposed)
+    CK_CUDA(gemm_tc_split(Qf, rkeep, c, (size_t)c, true, gpB, st));           // Q_r columns
+    CK_CUDA(gemm_tc_run(gpA, (int)D, gpB, rkeep, c, 1.0, 0.0, out, nullptr, (size_t)D, gwork, kGemmWorkFloats, st));
+    prof_end(CAKF_PROF_TRUNC_GEMM, ps);
+    prof_end(CAKF_PROF_TRUNCATE, pk);
+    return CAKF_OK;
+  }
+
   // Truncate a D x c factor F (ld D) to its top-r Gram eigen-directions: out = F Q_r.
   int truncate_factor(const T* F, int c, int rkeep, T* out, double* kept, double* dropped) {
     const size_t pk = prof_begin();
+    if constexpr (sizeof(T) == 4) {
+      if (use_tc_gemm()) return truncate_factor_tc(reinterpret_cast<const float*>(F), c, rkeep,
+                                                   reinterpret_cast<float*>(out), kept, dropped, pk);
+    }
     // fp64 copy of F (fp32 storage) feeds both the Gram (DSYRK, fp64 tensor cores) and M Q_r (DGEMM)
     const double* Fd = reinterpret_cast<const double*>(F);
     if constexpr (sizeof(T) == 4) {
@@ -830,7 +886,8 @@ struct Impl final : ImplBase {
     }
     const double one = 1.0, zero = 0.0;
     size_t ps = prof_begin();
-    CK_BLAS(cublasDsyrk(blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, c, (int)D, &one, Fd, (int)D, &zero, Gm, c));
+    // full Gram through DGEMM: on this shape (K = D >> c) cuBLAS DSYRK reaches ~12 TF/s, DGEMM ~36
+    CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c, c, (int)D, &one, Fd, (int)D, Fd, (int)D, &zero, Gm, c));
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
     CK_SOLVER(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, c, Gm, c, eigw, work, lwork, info));

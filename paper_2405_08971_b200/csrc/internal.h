@@ -60,4 +60,17 @@ bool use_tc_k2();
 template <typename T>
 cudaError_t launch_prescale_coords(int n, int dim, const double* xyz, double scale, V4<T>* out, cudaStream_t st);
 
+// ---- low-rank contractions on tcgen05 (kernels_gemm_tc.cu): fp32 operands as exact bf16x3 planes
+int gemm_tc_kp(int K);                              // padded K of the planes (multiple of 8)
+size_t gemm_tc_plane_bytes(int rows, int K);        // bytes of the three planes of a rows x K operand
+// planes[3][R][Kp] of the R x K operand whose (r, k) element is src[k + r ld] (k_contig) or src[r + k ld]
+cudaError_t gemm_tc_split(const float* src, int R, int K, size_t ld, bool k_contig, uint16_t* planes,
+                          cudaStream_t st);
+// C (M x N, column-major ldc) = alpha A B^T-of-planes + beta C, i.e. sum_k Ap[m][k] Bp[n][k];
+// output fp32 C or fp64 Cd (exactly one non-null); K splits reduced in fp64 through work (floats)
+cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, int K, double alpha, double beta,
+                        float* C, double* Cd, size_t ldc, float* work, size_t work_floats, cudaStream_t st);
+bool use_tc_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM instead
+constexpr size_t kGemmWorkFloats = (size_t)32 << 20;
+
 }  // namespace cakf
