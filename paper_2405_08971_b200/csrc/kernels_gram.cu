@@ -92,7 +92,7 @@ __device__ __forceinline__ void sym_unit_decode(long long u, int nb, int& bi, in
 }
 
 template <int NU2>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
                   float* __restrict__ partial,
                   unsigned long long* __restrict__ done_pairs, const int* __restrict__ ulist,
