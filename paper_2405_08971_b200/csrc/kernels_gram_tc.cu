@@ -30,6 +30,8 @@
 
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "internal.h"
 
 namespace cakf {
@@ -62,6 +64,14 @@ __device__ __forceinline__ void split3(float a, uint32_t& p1, uint32_t& p2, uint
   p1 = h1 >> 16;
   p2 = h2 >> 16;
   p3 = __float_as_uint(r2) >> 16;
+}
+
+// two-way fp16 split (round to nearest): a = h1 + h2 + O(2^-22 a) for a in the fp16 normal range
+__device__ __forceinline__ void split2h(float a, uint32_t& p1, uint32_t& p2) {
+  const __half h1 = __float2half_rn(a);
+  const __half h2 = __float2half_rn(a - __half2float(h1));
+  p1 = (uint32_t)__half_as_ushort(h1);
+  p2 = (uint32_t)__half_as_ushort(h2);
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -99,6 +109,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Instruction descriptor: kind::f16, D = f32, A = B = f16, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -117,12 +132,18 @@ __device__ __forceinline__ uint32_t sw64_off(int r, int c) {
   return (uint32_t)((r >> 3) * 512 + (r & 7) * 64 + ((c ^ ((r >> 1) & 3)) << 4));
 }
 
-template <int NU2>
+// F16 = false: 3 x BF16 planes, 6 MMAs per k-step (products to ~2^-24).
+// F16 = true : 2 x FP16 planes (kernel values scaled by 2^14, B columns by powers of two into
+//              [2^13, 2^14)), 3 MMAs per k-step (a1b1 | a1b2 + a2b1; products to ~2^-21), half
+//              the tensor work; colinv[n] undoes both scalings in the epilogue.
+template <int NU2, bool F16>
 __global__ void __launch_bounds__(TC_THREADS + 64, 1)
 gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmX, int K, int C, int ntile,
                     float* __restrict__ Y, size_t ldy, float alpha, int diag_nogen,
-                    const int* __restrict__ act_cnt, const int* __restrict__ act_list, int act_stride) {
+                    const int* __restrict__ act_cnt, const int* __restrict__ act_list, int act_stride,
+                    const float* __restrict__ colinv) {
+  constexpr int NPL = F16 ? 2 : 3;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -174,7 +195,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
 
   if (warp == 8) {
     // ===== MMA issuer: one elected lane, back-to-back over the stage ring
-    const uint32_t idesc = idesc_bf16(TC_BM, ntile);
+    const uint32_t idesc = F16 ? idesc_f16(TC_BM, ntile) : idesc_bf16(TC_BM, ntile);
     for (int kb = 0; kb < nk; ++kb) {
       const int sa = kb % A_STAGES, sb = kb % B_STAGES;
       mbar_wait(smem_u32(&fullA[sa]), (kb / A_STAGES) & 1);
@@ -192,9 +213,11 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
           mma_bf16(tmem, A1, B1, idesc, first);
           mma_bf16(tmem + acc_cols, A1, B2, idesc, first);
           mma_bf16(tmem + acc_cols, A2, B1, idesc, 1u);
-          mma_bf16(tmem + acc_cols, A2, B2, idesc, 1u);
-          mma_bf16(tmem + acc_cols, A1, B3, idesc, 1u);
-          mma_bf16(tmem + acc_cols, A3, B1, idesc, 1u);
+          if (!F16) {
+            mma_bf16(tmem + acc_cols, A2, B2, idesc, 1u);
+            mma_bf16(tmem + acc_cols, A1, B3, idesc, 1u);
+            mma_bf16(tmem + acc_cols, A3, B1, idesc, 1u);
+          }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_u32(&emptyA[sa]))
@@ -213,7 +236,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
     // ===== TMA loader: the three B planes (64B-swizzled boxes, zero-filled beyond C / K) and the
     // block's 32 column coordinates, up to TC_STAGES blocks ahead of the MMAs
     if (lane == 0) {
-      const uint32_t bytes = 3u * (uint32_t)ntile * 64u + (uint32_t)XC_BYTES;
+      const uint32_t bytes = (uint32_t)NPL * (uint32_t)ntile * 64u + (uint32_t)XC_BYTES;
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % B_STAGES;
         if (kb >= B_STAGES) mbar_wait(smem_u32(&emptyB[s]), ((kb / B_STAGES) - 1) & 1);
@@ -222,7 +245,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
         const uint32_t b0 = b_addr(s);
         const int k0 = (my_list ? my_list[kb] : kb) * TC_BK;
 #pragma unroll
-        for (int pl = 0; pl < 3; ++pl) {
+        for (int pl = 0; pl < NPL; ++pl) {
           asm volatile(
               "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
               "[%5];" ::"r"(b0 + pl * B_PLANE),
@@ -259,9 +282,14 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
           const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           kv[t] = diag_nogen ? d2 : matern_from_d2<NU2>(d2);   // diag_nogen: timing experiment only
         }
-        uint32_t a1, a2, a3, b1, b2, b3;
-        split3(kv[0], a1, a2, a3);
-        split3(kv[1], b1, b2, b3);
+        uint32_t a1, a2, a3 = 0, b1, b2, b3 = 0;
+        if (F16) {
+          split2h(kv[0] * 16384.f, a1, a2);
+          split2h(kv[1] * 16384.f, b1, b2);
+        } else {
+          split3(kv[0], a1, a2, a3);
+          split3(kv[1], b1, b2, b3);
+        }
         p1[q >> 1] = a1 | (b1 << 16);
         p2[q >> 1] = a2 | (b2 << 16);
         p3[q >> 1] = a3 | (b3 << 16);
@@ -275,9 +303,10 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0 + A_PLANE + off), "r"(p2[4 * h]),
                      "r"(p2[4 * h + 1]), "r"(p2[4 * h + 2]), "r"(p2[4 * h + 3])
                      : "memory");
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0 + 2 * A_PLANE + off), "r"(p3[4 * h]),
-                     "r"(p3[4 * h + 1]), "r"(p3[4 * h + 2]), "r"(p3[4 * h + 3])
-                     : "memory");
+        if (!F16)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0 + 2 * A_PLANE + off), "r"(p3[4 * h]),
+                       "r"(p3[4 * h + 1]), "r"(p3[4 * h + 2]), "r"(p3[4 * h + 3])
+                       : "memory");
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> tensor core
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fullA[sa])) : "memory");
@@ -311,7 +340,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
         for (int t = 0; t < 16; ++t) {
           const int n = n0 + cb + t;
           const float v = __uint_as_float(r[t]) + __uint_as_float(q[t]);
-          if (cb + t < c_end && n < C) Y[row + (size_t)n * ldy] = nk > 0 ? alpha * v : 0.f;
+          if (cb + t < c_end && n < C) Y[row + (size_t)n * ldy] = nk > 0 ? (F16 ? alpha * colinv[n] * v : alpha * v) : 0.f;
         }
       }
     }
@@ -338,6 +367,41 @@ __global__ void split_bf16x3_kernel(int K, int C, int Kp, const float* __restric
   planes[2 * plane + e] = (uint16_t)p3;
 }
 
+// per-column power-of-two scaling of B into [2^13, 2^14): scale[n] = 2^(14 - e), e = exponent with
+// max|B[:, n]| < 2^e; colinv[n] = 2^-14 / scale[n] (also undoes the 2^14 kernel-value scaling)
+__global__ void colscale_kernel(int K, const float* __restrict__ B, size_t ldb, float* __restrict__ scale,
+                                float* __restrict__ colinv) {
+  __shared__ float red[32];
+  const int n = blockIdx.x;
+  float m = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) m = fmaxf(m, fabsf(B[k + (size_t)n * ldb]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t = fmaxf(t, red[q]);
+    int e = 0;
+    if (t > 0.f && isfinite(t)) frexpf(t, &e);   // t in [2^(e-1), 2^e)
+    scale[n] = ldexpf(1.f, 14 - e);
+    colinv[n] = ldexpf(1.f, e - 28);
+  }
+}
+
+// B (K x C column-major) -> two fp16 planes (C x Kp, K-major) of B[:, n] * scale[n], zero for k >= K
+__global__ void split_f16x2_kernel(int K, int C, int Kp, const float* __restrict__ B, size_t ldb,
+                                   const float* __restrict__ scale, uint16_t* __restrict__ planes, size_t plane) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)Kp * C) return;
+  const int k = (int)(e % Kp), n = (int)(e / Kp);
+  const float v = k < K ? B[k + (size_t)n * ldb] * scale[n] : 0.f;
+  uint32_t p1, p2;
+  split2h(v, p1, p2);
+  planes[e] = (uint16_t)p1;
+  planes[plane + e] = (uint16_t)p2;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -353,10 +417,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 template <int NU2>
 cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const uint16_t* planes, int Kp, int C,
                          int ntile, float* Y, size_t ldy, float alpha, cudaStream_t st, const int* act_cnt,
-                         const int* act_list, int act_stride) {
+                         const int* act_list, int act_stride, const float* colinv) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         TC_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -381,8 +448,12 @@ cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const
     return cudaErrorInvalidValue;
   static const int nogen = [] { const char* e = getenv("CAKF_TC_DIAG_NOGEN"); return (e && e[0] == '1') ? 1 : 0; }();
   dim3 grid((M + TC_BM - 1) / TC_BM, (C + ntile - 1) / ntile);
-  gram_gemm_tc_kernel<NU2><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha, nogen,
-                                                                   act_cnt, act_list, act_stride);
+  if (colinv)
+    gram_gemm_tc_kernel<NU2, true><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha,
+                                                                           nogen, act_cnt, act_list, act_stride, colinv);
+  else
+    gram_gemm_tc_kernel<NU2, false><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha,
+                                                                            nogen, act_cnt, act_list, act_stride, nullptr);
   return note_launch_err();
 }
 
@@ -444,7 +515,16 @@ cudaError_t launch_k2_active(const float4* sphM, int nmt, const float4* sphK, in
 
 size_t gram_gemm_tc_workspace(int K, int C) {
   const size_t Kp = ((size_t)K + TC_BK - 1) / TC_BK * TC_BK;
-  return 3 * Kp * (size_t)C * sizeof(uint16_t) + 256;
+  return 3 * Kp * (size_t)C * sizeof(uint16_t) + 2 * (size_t)C * sizeof(float) + 1024;
+}
+
+bool use_f16_k2() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAKF_K2_PREC");
+    v = (e && (e[0] == 'f' || e[0] == 'F')) ? 1 : 0;   // "f16x2"; default 3 x BF16
+  }
+  return v == 1;
 }
 
 cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* xc, int K, const float* B, size_t ldb,
@@ -454,8 +534,18 @@ cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* 
   const int Kp = (K + TC_BK - 1) / TC_BK * TC_BK;
   uint16_t* planes = reinterpret_cast<uint16_t*>(work);
   const size_t plane = (size_t)Kp * C;
+  const bool f16 = use_f16_k2();
+  float* colscale = reinterpret_cast<float*>(planes + 3 * plane + 256);   // 512 B past the planes
+  float* colinv = colscale + C;
   if (plane > 0) {
-    split_bf16x3_kernel<<<(unsigned)((plane + 255) / 256), 256, 0, st>>>(K, C, Kp, B, ldb, planes, plane);
+    if (f16) {
+      colscale_kernel<<<C, 256, 0, st>>>(K, B, ldb, colscale, colinv);
+      cudaError_t e = note_launch_err();
+      if (e != cudaSuccess) return e;
+      split_f16x2_kernel<<<(unsigned)((plane + 255) / 256), 256, 0, st>>>(K, C, Kp, B, ldb, colscale, planes, plane);
+    } else {
+      split_bf16x3_kernel<<<(unsigned)((plane + 255) / 256), 256, 0, st>>>(K, C, Kp, B, ldb, planes, plane);
+    }
     cudaError_t e = note_launch_err();
     if (e != cudaSuccess) return e;
   }
@@ -465,11 +555,11 @@ cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* 
   ntile = ((ntile + 15) / 16) * 16;
   switch (nu2) {
     case 1: return launch_tc_nu<1>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st, act_cnt, act_list,
-                                   act_stride);
+                                   act_stride, f16 ? colinv : nullptr);
     case 3: return launch_tc_nu<3>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st, act_cnt, act_list,
-                                   act_stride);
+                                   act_stride, f16 ? colinv : nullptr);
     case 5: return launch_tc_nu<5>(xr, M, xc, K, planes, Kp, C, ntile, Y, ldy, (float)alpha, st, act_cnt, act_list,
-                                   act_stride);
+                                   act_stride, f16 ? colinv : nullptr);
   }
   return cudaErrorInvalidValue;
 }
