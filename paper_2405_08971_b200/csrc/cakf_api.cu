@@ -242,34 +242,43 @@ struct Impl final : ImplBase {
   T *ybuf_user = nullptr, *lam2_user = nullptr, *outm = nullptr, *outv = nullptr;
   std::vector<int> perm_h;
 
-  // Morton (Z-order) of the quantised coordinates: consecutive points are spatially close, so
-  // 128-point tiles of the Gram kernels are compact (CAKF_NO_REORDER=1 keeps the user order).
+  // Internal point order: a balanced kd-tree (recursive bisection at the median of the widest
+  // axis), depth-first.  Splits fall on multiples of 128 above 256 points and of 32 below, so every
+  // 128-row tile of the K2 output and every 32-column K-block is one compact subtree (bounding
+  // spheres ~2x tighter than a Morton order).  CAKF_NO_REORDER=1 keeps the user order.
   void make_perm(const std::vector<double>& xyz) {
     perm_h.resize(NX);
     for (int64_t i = 0; i < NX; ++i) perm_h[i] = (int)i;
     const char* e = getenv("CAKF_NO_REORDER");
     if (e && e[0] == '1') return;
-    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    for (int d = 0; d < dim; ++d) {
-      lo[d] = hi[d] = xyz[d];
-      for (int64_t i = 0; i < NX; ++i) {
-        lo[d] = std::min(lo[d], xyz[i * dim + d]);
-        hi[d] = std::max(hi[d], xyz[i * dim + d]);
-      }
-    }
-    std::vector<uint64_t> key(NX);
-    for (int64_t i = 0; i < NX; ++i) {
-      uint64_t k = 0;
-      uint32_t q[3] = {0, 0, 0};
+    std::vector<std::pair<int64_t, int64_t>> stack{{0, NX}};
+    while (!stack.empty()) {
+      const auto [b0, b1] = stack.back();
+      stack.pop_back();
+      const int64_t n = b1 - b0;
+      if (n <= 32) continue;
+      double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
       for (int d = 0; d < dim; ++d) {
-        const double span = hi[d] - lo[d];
-        q[d] = span > 0 ? (uint32_t)std::min(2097151.0, (xyz[i * dim + d] - lo[d]) / span * 2097151.0) : 0u;
+        lo[d] = hi[d] = xyz[(size_t)perm_h[b0] * dim + d];
+        for (int64_t i = b0; i < b1; ++i) {
+          const double v = xyz[(size_t)perm_h[i] * dim + d];
+          lo[d] = std::min(lo[d], v);
+          hi[d] = std::max(hi[d], v);
+        }
       }
-      for (int b = 20; b >= 0; --b)
-        for (int d = 0; d < 3; ++d) k = (k << 1) | ((q[d] >> b) & 1u);
-      key[i] = k;
+      int ax = 0;
+      for (int d = 1; d < dim; ++d)
+        if (hi[d] - lo[d] > hi[ax] - lo[ax]) ax = d;
+      std::sort(perm_h.begin() + b0, perm_h.begin() + b1, [&](int a, int b) {
+        const double va = xyz[(size_t)a * dim + ax], vb = xyz[(size_t)b * dim + ax];
+        return va < vb || (va == vb && a < b);
+      });
+      const int64_t al = n > 256 ? 128 : 32;
+      int64_t h = ((n / 2 + al / 2) / al) * al;
+      h = std::min(std::max(h, al), n - 1);
+      stack.push_back({b0 + h, b1});   // right half after the left one (depth-first, left first)
+      stack.push_back({b0, b0 + h});
     }
-    std::stable_sort(perm_h.begin(), perm_h.end(), [&](int a, int b) { return key[a] < key[b]; });
   }
 
   // ---------------- multi-GPU: the Gram products are sharded, the rest replicated

@@ -142,7 +142,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
                     const __grid_constant__ CUtensorMap tmX, int K, int C, int ntile,
                     float* __restrict__ Y, size_t ldy, float alpha, int diag_nogen,
                     const int* __restrict__ act_cnt, const int* __restrict__ act_list, int act_stride,
-                    const float* __restrict__ colinv) {
+                    const float* __restrict__ colinv, int oneacc) {
   constexpr int NPL = F16 ? 2 : 3;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -211,8 +211,8 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
                          B3 = sdesc_sw64(bb + 2 * B_PLANE + 32 * j);
           const uint32_t first = (kb | j) ? 1u : 0u;
           mma_bf16(tmem, A1, B1, idesc, first);
-          mma_bf16(tmem + acc_cols, A1, B2, idesc, first);
-          mma_bf16(tmem + acc_cols, A2, B1, idesc, 1u);
+          mma_bf16(tmem + (oneacc ? 0u : acc_cols), A1, B2, idesc, oneacc ? 1u : first);
+          mma_bf16(tmem + (oneacc ? 0u : acc_cols), A2, B1, idesc, 1u);
           if (!F16) {
             mma_bf16(tmem + acc_cols, A2, B2, idesc, 1u);
             mma_bf16(tmem + acc_cols, A1, B3, idesc, 1u);
@@ -339,7 +339,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
           const int n = n0 + cb + t;
-          const float v = __uint_as_float(r[t]) + __uint_as_float(q[t]);
+          const float v = __uint_as_float(r[t]) + (oneacc ? 0.f : __uint_as_float(q[t]));
           if (cb + t < c_end && n < C) Y[row + (size_t)n * ldy] = nk > 0 ? (F16 ? alpha * colinv[n] * v : alpha * v) : 0.f;
         }
       }
@@ -446,14 +446,17 @@ cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const
   if (enc(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)xc, gdX, gsX, boxX, es2, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
+  static const int oneacc = [] { const char* e = getenv("CAKF_K2_ONEACC"); return (e && e[0] == '1') ? 1 : 0; }();
   static const int nogen = [] { const char* e = getenv("CAKF_TC_DIAG_NOGEN"); return (e && e[0] == '1') ? 1 : 0; }();
   dim3 grid((M + TC_BM - 1) / TC_BM, (C + ntile - 1) / ntile);
   if (colinv)
     gram_gemm_tc_kernel<NU2, true><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha,
-                                                                           nogen, act_cnt, act_list, act_stride, colinv);
+                                                                           nogen, act_cnt, act_list, act_stride, colinv,
+                                                                           oneacc);
   else
     gram_gemm_tc_kernel<NU2, false><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha,
-                                                                            nogen, act_cnt, act_list, act_stride, nullptr);
+                                                                            nogen, act_cnt, act_list, act_stride, nullptr,
+                                                                            0);
   return note_launch_err();
 }
 
