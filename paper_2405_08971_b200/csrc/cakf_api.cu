@@ -241,6 +241,11 @@ struct Impl final : ImplBase {
   int *posof = nullptr, *obs_cnt = nullptr, *sigma = nullptr, *sigma_inv = nullptr;
   T *ybuf_user = nullptr, *lam2_user = nullptr, *outm = nullptr, *outv = nullptr;
   std::vector<int> perm_h;
+  // per-update kd order of the observations (kd_order.cu); CAKF_NO_REORDER=1 keeps the sorted order
+  bool kd_obs = [] { const char* e = getenv("CAKF_NO_REORDER"); return !(e && e[0] == '1'); }();
+  int *idx_tmp = nullptr, *sig_tmp = nullptr;
+  void* kd_ws = nullptr;
+  size_t kd_ws_bytes = 0;
 
   // Internal point order: a balanced kd-tree (recursive bisection at the median of the widest
   // axis), depth-first.  Splits fall on multiples of 128 above 256 points and of 32 below, so every
@@ -495,6 +500,10 @@ struct Impl final : ImplBase {
     obs_cnt = carve<int>((NX + 1023) / 1024 + 1);
     sigma = carve<int>(Nmax);
     sigma_inv = carve<int>(Nmax);
+    idx_tmp = carve<int>(Nmax);
+    sig_tmp = carve<int>(Nmax);
+    kd_ws_bytes = kd_obs_workspace((int)Nmax);
+    kd_ws = carve<unsigned char>(kd_ws_bytes);
     ybuf_user = carve<T>(Nmax);
     lam2_user = carve<T>(Nmax);
     outm = carve<T>(D);
@@ -703,7 +712,12 @@ struct Impl final : ImplBase {
     // ---- stage inputs (host or device pointers)
     // observations in internal point order: S.idx ascending, sigma[j] = the user's position
     CK_CUDA(cudaMemcpyAsync(stage64, obs_idx, (size_t)N * sizeof(int64_t), cudaMemcpyDefault, st));
-    CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, S.idx, sigma, sigma_inv, st));
+    if (kd_obs) {   // internal order, then the per-update kd order over the observed points
+      CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, sigma_inv, st));
+      CK_CUDA(kd_obs_order<T>(N, idx_tmp, coords, sigma, sigma_inv, S.idx, sig_tmp, kd_ws, kd_ws_bytes, st));
+    } else {
+      CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, S.idx, sigma, sigma_inv, st));
+    }
     CK_CUDA(cudaMemcpyAsync(ybuf_user, y, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
     CK_CUDA(cudaMemcpyAsync(lam2_user, noise_var, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
     CK_CUDA(gather_vec<T>(N, sigma, ybuf_user, ybuf, st));

@@ -73,4 +73,12 @@ cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, in
 bool use_tc_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM instead
 constexpr size_t kGemmWorkFloats = (size_t)32 << 20;
 
+// ---- per-update kd-tree order of the observed points (kd_order.cu)
+size_t kd_obs_workspace(int Nmax);
+// idx/sig_in_sorted: the observations in internal point order (obs_sort); writes idx_out, sig_out
+// (user position of each row) and sig_inv in the kd order
+template <typename T>
+cudaError_t kd_obs_order(int N, const int* idx, const V4<T>* coords, int* sig_out, int* sig_inv, int* idx_out,
+                         const int* sig_in_sorted, void* ws, size_t ws_bytes, cudaStream_t st);
+
 }  // namespace cakf
