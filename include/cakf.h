@@ -191,7 +191,7 @@ int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset);
 int64_t cakf_kernel_launches(void);
 
 /* Exact-zero culling statistics of the handle so far: frac3[0] = fraction of the symmetric K1's
- * 128x128 tile pairs evaluated, frac3[1] = fraction of the post-loop K2's 128x32 tiles evaluated,
+ * pairs evaluated (counted in 16 x 128 warp blocks of its 128 x 128 tile pairs), frac3[1] = fraction of the post-loop K2's 128x32 tiles evaluated,
  * frac3[2] = same for the smoother's K2 (all 1.0 when culling is off).  Synchronises the handle's
  * stream.  Errors: CAKF_E_HANDLE, CAKF_E_ARG (NULL frac3), CAKF_E_CUDA. */
 int cakf_cull_stats(cakf_t h, double* frac3);

@@ -227,7 +227,7 @@ struct Impl final : ImplBase {
   // ---------------- exact-zero culling (fp32 only): tile bounding spheres and, per 128-row
   // output tile of K2, the ascending list of 32-column K-blocks not entirely below the fp32 underflow
   bool cull = false;
-  float4 *sph_x128 = nullptr, *sph_x32 = nullptr, *sph_o128 = nullptr, *sph_o32 = nullptr;
+  float4 *sph_x128 = nullptr, *sph_x32 = nullptr, *sph_o128 = nullptr, *sph_o32 = nullptr, *sph_o16 = nullptr;
   int *act_cnt_sm = nullptr, *act_list_sm = nullptr, *act_cnt_po = nullptr, *act_list_po = nullptr;
   int act_stride_sm = 0, act_stride_po = 0;
   int *k1_list = nullptr, *k1_count = nullptr;
@@ -531,6 +531,7 @@ struct Impl final : ImplBase {
       const int no128 = (int)((Nmax + 127) / 128), no32 = (int)((Nmax + 31) / 32);
       sph_x128 = carve<float4>(nx128); sph_x32 = carve<float4>(nx32);
       sph_o128 = carve<float4>(no128); sph_o32 = carve<float4>(no32);
+      sph_o16 = carve<float4>((Nmax + 15) / 16 + 1);
       act_stride_sm = nx32; act_stride_po = no32;
       act_cnt_sm = carve<int>(nx128); act_list_sm = carve<int>((size_t)nx128 * nx32);
       act_cnt_po = carve<int>(nx128); act_list_po = carve<int>((size_t)nx128 * no32);
@@ -739,6 +740,7 @@ struct Impl final : ImplBase {
       const float4* xf = reinterpret_cast<const float4*>(xcs);
       CK_CUDA(launch_tile_spheres(xf, N, 128, sph_o128, st));
       CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st));
+      CK_CUDA(launch_tile_spheres(xf, N, 16, sph_o16, st));
       CK_CUDA(launch_k2_active(sph_x128, (int)((NX + 127) / 128), sph_o32, (N + 31) / 32, kCullCut, act_cnt_po,
                                act_list_po, act_stride_po, cull_ctr + 1, st));
       k2_post_dense += (double)((NX + 127) / 128) * ((N + 31) / 32);
@@ -763,10 +765,10 @@ struct Impl final : ImplBase {
           const long long U = matvec_sym_units(N);
           CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
                                     U * rank / world, U * (rank + 1) / world, st, cull ? cull_ctr : nullptr,
-                                    cull ? k1_list : nullptr, k1_count, k1_mask));
+                                    cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128, kCullCut));
           if (cull) {
             const double nt = (double)((N + 127) / 128);
-            k1_pairs_dense += nt * (nt + 1) / 2 / world;
+            k1_pairs_dense += 8.0 * nt * (nt + 1) / 2 / world;   // in 16 x 128 warp blocks
           }
         } else {
           CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st, nch * rank / world,

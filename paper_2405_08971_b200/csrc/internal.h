@@ -20,11 +20,13 @@ int matvec_sym_tiles(int n);
 long long matvec_sym_units(int n);   // number of symmetric tile-block work units
 int matvec_sym_block_points();       // points per tile block of the symmetric K1
 // ulist != nullptr (exact-zero culling): evaluate only the *ucount units ulist[w] (ascending), and in each
-// only the tile pairs set in umask[w] (bit a*4+b); the skipped units' partial slots must hold zeros.
+// only the tile pairs set in umask[w] (bit a*4+b), and in those only the warps whose 16-row group sphere
+// (sph16) is within cut of the J tile sphere (sph128); the skipped units' partial slots must hold zeros.
 // done_pairs (nullable) accumulates the evaluated 128 x 128 tile pairs.
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
                               cudaStream_t st, unsigned long long* done_pairs = nullptr, const int* ulist = nullptr,
-                              const int* ucount = nullptr, const unsigned short* umask = nullptr);
+                              const int* ucount = nullptr, const unsigned short* umask = nullptr,
+                              const float4* sph16 = nullptr, const float4* sph128 = nullptr, float cut = 0.f);
 // compact ascending list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
                                    unsigned short* mask, int* count, cudaStream_t st);

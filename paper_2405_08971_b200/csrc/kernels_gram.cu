@@ -96,8 +96,11 @@ __global__ void __launch_bounds__(256, 3)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
                   float* __restrict__ partial,
                   unsigned long long* __restrict__ done_pairs, const int* __restrict__ ulist,
-                  const int* __restrict__ ucount, const unsigned short* __restrict__ umask) {
+                  const int* __restrict__ ucount, const unsigned short* __restrict__ umask,
+                  const float4* __restrict__ sph16, const float4* __restrict__ sph128, float cut) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
+  __shared__ float4 s16[SYM_S * 8], s128[SYM_S];   // this unit's 16-row group / J tile spheres
+  __shared__ unsigned s_done;                        // evaluated 16 x 128 warp blocks of this unit
   float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
   float4* tJ = tI + SYM_S * SYM_T;                                    // [SYM_S][128]
   float* rowacc = reinterpret_cast<float*>(tJ + SYM_S * SYM_T);       // [SYM_S][128]
@@ -111,7 +114,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
     const long long u = ulist ? (long long)ulist[w] : u_begin + w;
     // active tile pairs of this unit, bit a*SYM_S+b (exact-zero culling; all ones without)
     const unsigned amask = ulist ? (unsigned)umask[w] : 0xFFFFu;
-    if (tid == 0 && done_pairs) atomicAdd(done_pairs, (unsigned long long)__popc(amask));
+    if (tid == 0) s_done = 0u;
     // u -> (bi, bj), bi <= bj, row-major over the upper triangle of blocks
     int bi, bj;
     sym_unit_decode(u, nb, bi, bj);
@@ -138,6 +141,15 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
 #pragma unroll
       for (int c = 0; c < 8; ++c) mycol[b * SYM_T + c] = 0.f;
     const float4* sJ = diag ? tI : tJ;
+    if (ulist) {
+      if (tid < SYM_S * 8) {
+        const int g = bi * SYM_S * 8 + tid;
+        s16[tid] = g < (n + 15) / 16 ? sph16[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if (tid < SYM_S * 8 + SYM_S) {
+        const int t = bj * SYM_S + tid - SYM_S * 8;
+        s128[tid - SYM_S * 8] = t < nt ? sph128[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
     __syncthreads();
     for (int a = 0; a < na; ++a) {
       // rows kept negated (d = c - r) as scalars: the packed f32x2 ops broadcast a scalar operand
@@ -153,6 +165,12 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
       for (int q = 0; q < 8; ++q) racc2[q] = make_float2(0.f, 0.f);
       for (int b = diag ? a : 0; b < nbj; ++b) {
         if (!((amask >> (a * SYM_S + b)) & 1u)) continue;   // every value of this tile pair is exactly 0
+        if (ulist) {   // same test for this warp's 16 rows against the J tile (warp-uniform)
+          const float4 A = s16[a * 8 + (tid >> 5)], B = s128[b];
+          const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
+          if (sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut) continue;
+          if ((tid & 31) == 0) atomicAdd(&s_done, 1u);
+        }
         const bool offdiag = !(diag && a == b);
         // 8 columns as 4 packed pairs: every elementwise op below is one FADD2 / FMUL2 / FFMA2 for two
         // pairs, leaving the two MUFU ops per pair (sqrt, ex2) as the only scalar work
@@ -201,6 +219,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
       }
     }
     __syncthreads();
+    if (tid == 0 && done_pairs && ulist) atomicAdd(done_pairs, (unsigned long long)s_done);
     for (int e = tid; e < SYM_S * SYM_T; e += 256) {
       float cs_ = 0.f;                       // column sums: fixed-order reduction over the 16 ty slots
 #pragma unroll
@@ -485,7 +504,8 @@ cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, lon
 
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
                               cudaStream_t st, unsigned long long* done_pairs, const int* ulist,
-                              const int* ucount, const unsigned short* umask) {
+                              const int* ucount, const unsigned short* umask, const float4* sph16,
+                              const float4* sph128, float cut) {
   if (n <= 0 || u_end <= u_begin) return cudaSuccess;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
@@ -508,11 +528,14 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
   const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);
   switch (nu2) {
     case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
-                                                                         done_pairs, ulist, ucount, umask); break;
+                                                                         done_pairs, ulist, ucount, umask, sph16,
+                                                                         sph128, cut); break;
     case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
-                                                                         done_pairs, ulist, ucount, umask); break;
+                                                                         done_pairs, ulist, ucount, umask, sph16,
+                                                                         sph128, cut); break;
     case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
-                                                                         done_pairs, ulist, ucount, umask); break;
+                                                                         done_pairs, ulist, ucount, umask, sph16,
+                                                                         sph128, cut); break;
     default: return cudaErrorInvalidValue;
   }
   return note_launch_err();
