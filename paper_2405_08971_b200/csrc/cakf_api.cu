@@ -168,6 +168,11 @@ struct Impl final : ImplBase {
   Mat3 sig_t0{};
   bool own_stream = false, failed_ = false;
   cudaStream_t st = nullptr;
+  // side stream: u = (HM^-)^T s (HBM-bound) overlaps K1 (MUFU-bound) in every inner iteration
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  double* part2 = nullptr;
+  bool side = [] { const char* e = getenv("CAKF_NO_SIDE_STREAM"); return !(e && e[0] == '1'); }();
   cublasHandle_t blas = nullptr;
   cusolverDnHandle_t sol = nullptr;
 
@@ -398,6 +403,9 @@ struct Impl final : ImplBase {
     if (blas) cublasDestroy(blas);
     if (sol) cusolverDnDestroy(sol);
     if (own_stream && st) cudaStreamDestroy(st);
+    if (st2) cudaStreamDestroy(st2);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
   }
 
   template <typename U>
@@ -457,7 +465,8 @@ struct Impl final : ImplBase {
     redA = carve<double>(W);
     redB = carve<double>(W);
     redC = carve<double>(W);
-    cnt = carve<unsigned>(4 * 64);   // per reduction: [0] top, [1..32] group counters
+    cnt = carve<unsigned>(5 * 64);   // per reduction: [0] top, [1..32] group counters
+    part2 = carve<double>((size_t)(stage_blocks((int)Nmax) + 33) * W);
     Yb = carve<T>((size_t)NX * (1 + nhat));
     Ub = carve<T>((size_t)std::max(rin_max, 1) * (1 + nhat));
     tmp = carve<T>((size_t)D * (1 + nhat));
@@ -585,7 +594,12 @@ struct Impl final : ImplBase {
       return fail(CAKF_E_NOMEM, "trace arena of " + std::to_string(arena_bytes) + " bytes: " + cudaGetErrorString(e));
     }
     layout();
-    CK_CUDA(cudaMemsetAsync(cnt, 0, 4 * 64 * sizeof(unsigned), st));
+    CK_CUDA(cudaMemsetAsync(cnt, 0, 5 * 64 * sizeof(unsigned), st));
+    if (side) {
+      CK_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+      CK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      CK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
     CK_CUDA(cudaMallocHost(&ctl_init_host, sizeof(IterCtl)));
     std::memset(ctl_init_host, 0, sizeof(IterCtl));
     ctl_init_host->eta_min = INFINITY;
@@ -756,6 +770,13 @@ struct Impl final : ImplBase {
     T* V = S.XV + N;
     for (int i = 1; i <= niter; ++i) {
       // G s  (matrix-free: kernel rows on the fly + low-rank downdate + noise)
+      const bool fork = side && rin > 0;
+      if (fork) {   // u = HM^T s on the side stream, concurrently with K1 (joined before stage B)
+        CK_CUDA(cudaEventRecord(ev_fork, st));
+        CK_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
+        CK_CUDA(StepKernels<T>::hmts(N, HM, rin, s, part2, W, redA, cnt + 256, st2));
+        CK_CUDA(cudaEventRecord(ev_join, st2));
+      }
       size_t pk = prof_begin();
       // multi-GPU: this rank evaluates its share of the kernel work (sym units / column chunks),
       // the rest of the partial buffer is zero, and the reduced vector is all-reduced
@@ -788,7 +809,9 @@ struct Impl final : ImplBase {
       }
       prof_end(CAKF_PROF_K1, pk);
       pk = prof_begin();
-      CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, HM, rin, part, W, redA, cnt, st));
+      CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, fork ? nullptr : HM, rin, part, W, redA,
+                                     cnt, st));
+      if (fork) CK_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
       CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 64, st));
       if (reorth && i > 1) {  // CGS2 (R19): d = s - V c, then d -= V (V^T G d)
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W, redC,

@@ -523,6 +523,7 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, matvec_sym_kernel<3>, 256, smem) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
+    if (const char* e = getenv("CAKF_K1_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
     configured = true;
   }
   const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);

@@ -206,9 +206,25 @@ stageA_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const
   }
   block_sum<3>(a, scratch);
   double* slot = part + (size_t)blockIdx.x * W;
+  if (!HM) {   // u = (HM)^T s runs concurrently on the side stream (hmts_kernel) into red[0, rin)
+    if (threadIdx.x == 0) { slot[0] = a[0]; slot[1] = a[1]; slot[2] = a[2]; }
+    reduce_blocks(3, W, part, cnt, red + rin);
+    return;
+  }
   if (threadIdx.x == 0) { slot[rin] = a[0]; slot[rin + 1] = a[1]; slot[rin + 2] = a[2]; }
   tile_cols_dot(HM, (size_t)N, rin, s, r0, r1, slot);            // u = (HM)^T s
   reduce_blocks(rin + 3, W, part, cnt, red);
+}
+
+// u = (HM^-)^T s alone (red[0, rin)): the HBM-bound half of stage A, launched on a side stream so it
+// overlaps the MUFU-bound K1 of the same iteration (both only need s)
+template <typename T>
+__global__ void __launch_bounds__(kTile)
+hmts_kernel(int N, const T* __restrict__ HM, int rin, const T* __restrict__ s, double* __restrict__ part, int W,
+            double* __restrict__ red, unsigned* cnt) {
+  const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile);
+  tile_cols_dot(HM, (size_t)N, rin, s, r0, r1, part + (size_t)blockIdx.x * W);
+  reduce_blocks(rin, W, part, cnt, red);
 }
 
 // ------------------------------------------------------------------ stage B
@@ -633,6 +649,14 @@ cudaError_t StepKernels<T>::stageA(int N, int nch, const T* partial, double sig0
                                    unsigned* cnt, cudaStream_t st) {
   stageA_kernel<T><<<stage_blocks(N), kTile, 0, st>>>(N, nch, partial, sig00, lam2, s, r, gp, HM, rin, part, W, red,
                                                       cnt);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::hmts(int N, const T* HM, int rin, const T* s, double* part, int W, double* red,
+                                 unsigned* cnt, cudaStream_t st) {
+  if (rin <= 0 || N <= 0) return cudaSuccess;
+  hmts_kernel<T><<<stage_blocks(N), kTile, 0, st>>>(N, HM, rin, s, part, W, red, cnt);
   return note_launch_err();
 }
 

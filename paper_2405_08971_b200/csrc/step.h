@@ -39,6 +39,9 @@ struct StepKernels {
   static cudaError_t stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s, const T* r,
                             T* gp, const T* HM, int rin, double* part, int W, double* red, unsigned* cnt,
                             cudaStream_t st);
+  // HM == nullptr in stageA: u = HM^T s is computed by hmts (side stream) into red[0, rin)
+  static cudaError_t hmts(int N, const T* HM, int rin, const T* s, double* part, int W, double* red, unsigned* cnt,
+                          cudaStream_t st);
   static cudaError_t stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g, const T* V,
                             int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st);
   static cudaError_t stageC(int N, const T* V, const T* Z, int nV, const double* cred, const T* sin, const T* gin,
