@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--impl", default="cakf", choices=["cakf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cull", action="store_true", help="disable exact-zero culling (results are bit-identical)")
+    ap.add_argument("--no-dense", action="store_true", help="skip the reference timing with culling off")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--T", type=int, default=None, help="override T (debug only; invalidates the metric)")
     return ap.parse_args()
@@ -241,11 +242,17 @@ def main():
     h.profile_read(reset=True)
     launches0 = binding.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = []
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
-        for _ in range(args.steps):
-            runner.run(h, trans, inputs, smooth=True)
+        for _ in range(args.steps):   # filter and smoother bracketed separately (two extra events)
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            runner.run(h, trans, inputs, smooth=False)
+            ea.record(stream)
+            h.smooth()
+            eb.record(stream)
+            evs.append((ea, eb))
         ev1.record(stream)
         barrier()
     launches = binding.kernel_launches() - launches0
@@ -256,6 +263,8 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    smoother_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    filter_ms = ms / args.steps - smoother_ms
     total_timesteps = args.steps * wl.T            # one problem sharded over all ranks (strong scaling)
     value = total_timesteps / (ms / 1e3)
     clocks = clk.summary()
@@ -357,7 +366,40 @@ def main():
         "e2e": e2e,
         "roofline": roof,
         "phase_ms_per_step": breakdown,
+        "filter_ms_per_step": round(filter_ms, 3), "smoother_ms_per_step": round(smoother_ms, 3),
+        "filter_time_steps_per_s": wl.T / (filter_ms / 1e3), "smoother_time_steps_per_s": wl.T / (smoother_ms / 1e3),
     }
+    h.destroy()
+    if not args.no_cull and not args.no_dense and args.dtype == "f32":
+        # the same pass with exact-zero culling off (bit-identical results): the dense-work rate and
+        # K1's roofline fraction on the full N(N+1)/2 pairs, reported separately
+        hd = runner.make_handle(wl, args.dtype, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id,
+                                cull_zero=False)
+        runner.run(hd, trans, inputs, smooth=True)
+        barrier()
+        hd.profile(True)
+        hd.profile_read(reset=True)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        runner.run(hd, trans, inputs, smooth=True)
+        d1.record(stream)
+        barrier()
+        dprof = hd.profile_read(reset=True)
+        dms = d0.elapsed_time(d1)
+        if world > 1:
+            t = torch.tensor([dms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dms = float(t.item())
+        k1_ms, k1_n = dprof["k1_matvec"]
+        pairs = float(N) * (float(N) + 1.0) / 2.0
+        k1_rate = pairs / (k1_ms / max(k1_n, 1) / 1e3) / 1e9
+        out["dense"] = {"value": wl.T / (dms / 1e3), "unit": "time-steps/s", "ms_per_step": dms, "steps": 1,
+                        "warmup": 1, "cull_zero": False,
+                        "k1_roofline": {"achieved": k1_rate, "peak": roof.get("peak") if dom == "k1_matvec" else None,
+                                        "unit": "Gpair/s", "frac": (k1_rate / roof["peak"]) if dom == "k1_matvec" else None,
+                                        "algorithmic_per_launch": f"{pairs:.4g} unique pairs N(N+1)/2"},
+                        "phase_ms_per_step": {c: round(dprof[c][0], 3) for c in dprof}}
+        hd.destroy()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = oracle_sample(wl)
         out["cpu_baseline"] = {"value": 1.0 / smp["sec_per_timestep"], "unit": "time-steps/s",
@@ -365,7 +407,6 @@ def main():
                                "sample_sec": round(smp["sample_sec"], 2)}
     if rank == 0:
         print(json.dumps(out))
-    h.destroy()
     if world > 1:
         dist.destroy_process_group()
     return 0
