@@ -222,6 +222,9 @@ def caks_smoother(ssm: SSM, trace, max_rank=-1):
     ranks = [0] * (T + 1)
     ws = trace[T].w                                           # line 2
     Ws = trace[T].W                                           # line 3
+    ws_k = [None] * (T + 1)                                   # carriers kept for interpolation
+    Ws_k = [None] * (T + 1)                                   # (alg:caks-interpolation)
+    ws_k[T], Ws_k[T] = ws, Ws
     ms[T] = trace[T].m
     Ms[T] = trace[T].M
     var[T] = trace[T].var
@@ -241,7 +244,8 @@ def caks_smoother(ssm: SSM, trace, max_rank=-1):
         Ws_full = np.hstack([rec.W, proj @ (A.T @ Ws)])       # line 8
         Ws, _ = truncate(Ws_full, max_rank)                   # line 9 (R6)
         ranks[k] = Ws.shape[1]
-    return {"m": ms, "var": var, "M": Ms, "rank": ranks}
+        ws_k[k], Ws_k[k] = ws, Ws
+    return {"m": ms, "var": var, "M": Ms, "rank": ranks, "ws": ws_k, "Ws": Ws_k}
 
 
 def run_workload(wl, dtype_round=None, max_rank=None, smoother=True):
