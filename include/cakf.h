@@ -98,6 +98,9 @@ typedef struct {
   int32_t cull_zero;        /* 1 = exact-zero culling (fp32 only): skip kernel tiles whose every
                                value underflows to exactly 0 in fp32 (bounding-sphere distance in
                                prescaled units > 88); results are bit-identical to 0 */
+  int32_t keep_carriers;    /* 1 = keep the smoother carriers w^s_k, W^s_k of every step (an extra
+                               (T+1) x D x (1 + r) values) so cakf_interpolate can return smoother
+                               states between steps (Cor. A.10); 0 = filter interpolation only */
   uint64_t seed;            /* Philox key of CAKF_POLICY_RANDOM                               */
   int32_t max_steps;        /* T: number of time steps the trace is sized for                */
   int64_t max_obs;          /* max N_k over the run (0 = n_space)                            */
@@ -189,6 +192,23 @@ int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset);
 
 /* Number of libcakf kernels launched by this process so far (all handles). */
 int64_t cakf_kernel_launches(void);
+
+/* Temporal interpolation (Cor. A.10 P:1386-1437; alg:cakf-interpolation P:1445-1469,
+ * alg:caks-interpolation P:1470-1499): the filter (which = CAKF_FILTER) or smoother
+ * (CAKF_SMOOTH) marginal mean and variance at an off-grid time t with t_k <= t < t_{k+1}
+ * (k = T: t >= t_T), from the stored step-k state — no data is revisited:
+ *   m(t) = (A1 (x) I) m_k, M(t) = (A1 (x) I) M~_k, P(t) = Sigma(t) - M(t) M(t)^T,
+ *   Sigma(t) = (A1 Sigma^t_k A1^T + Q1) (x) K_X;  smoother (k < T): m^s(t) = m(t) +
+ *   P(t) (A2 (x) I)^T w^s_{k+1}, var^s(t) = var(t) - rowsumsq(P(t) (A2 (x) I)^T W^s_{k+1}).
+ * A1 = A^t(t, t_k), Q1 = Q^t(t, t_k), A2 = A^t(t_{k+1}, t): D' x D' row-major doubles, host or
+ * device (e.g. cakf_matern_transition with dt = t - t_k and t_{k+1} - t); A2 is ignored for the
+ * filter and for k = T.  mean_D / var_D: D values (dtype), user point order, host or device,
+ * either may be NULL.  Synchronises the handle's stream.
+ * Errors: CAKF_E_ARG (k outside [1, steps done], bad which, NULL matrices), CAKF_E_STATE (step k
+ * not truncated yet; smoother query before caks_smooth or without keep_carriers), CAKF_E_NUMERIC
+ * (singular A_{k+1}), CAKF_E_CUDA. */
+int cakf_interpolate(cakf_t h, int32_t k, const double* A1, const double* Q1, const double* A2, int32_t which,
+                     void* mean_D, void* var_D);
 
 /* Exact-zero culling statistics of the handle so far: frac3[0] = fraction of the symmetric K1's
  * pairs evaluated (counted in 16 x 128 warp blocks of its 128 x 128 tile pairs), frac3[1] = fraction of the post-loop K2's 128x32 tiles evaluated,

@@ -38,7 +38,7 @@ class cakf_config(ctypes.Structure):
         ("space_dim", ctypes.c_int32), ("coords", ctypes.c_void_p), ("spatial_kernel", ctypes.c_int32),
         ("ell_x", ctypes.c_double), ("sigma_t0", ctypes.c_void_p), ("mu0", ctypes.c_void_p),
         ("policy", ctypes.c_int32), ("max_iter", ctypes.c_int32), ("max_rank", ctypes.c_int32),
-        ("rtol", ctypes.c_double), ("reorth", ctypes.c_int32), ("cull_zero", ctypes.c_int32), ("seed", ctypes.c_uint64), ("max_steps", ctypes.c_int32),
+        ("rtol", ctypes.c_double), ("reorth", ctypes.c_int32), ("cull_zero", ctypes.c_int32), ("keep_carriers", ctypes.c_int32), ("seed", ctypes.c_uint64), ("max_steps", ctypes.c_int32),
         ("max_obs", ctypes.c_int64), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
     ]
@@ -60,7 +60,7 @@ EXPORTS = [
     "cakf_create", "cakf_reset", "cakf_predict", "cakf_update", "cakf_truncate", "caks_smooth", "cakf_get",
     "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
-    "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats",
+    "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats", "cakf_interpolate",
 ]
 PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank", "trunc_gram",
                    "trunc_eig", "trunc_gemm"]
@@ -96,6 +96,8 @@ def load(path: str = LIB_PATH):
     lib.cakf_kernel_launches.restype = ctypes.c_int64
     lib.cakf_nccl_unique_id.argtypes = [vp]
     lib.cakf_shard_plan.argtypes = [i64, i64, i32, i32, vp]
+    lib.cakf_cull_stats.argtypes = [vp, vp]
+    lib.cakf_interpolate.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp]
     lib.cakf_sym_unit_blocks.argtypes = [i64, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     for name in EXPORTS:
         if name not in ("cakf_last_error", "cakf_version", "cakf_kernel_launches"):
@@ -182,7 +184,7 @@ class Cakf:
 
     def __init__(self, coords, ell_x, sigma_t0, *, dtype="f32", d_time=2, nu_x=1.5, mu0=None, policy="cg",
                  max_iter=64, max_rank=-1, seed=1, max_steps=48, max_obs=0, reorth=True, stream=None,
-                 rank=0, world=1, nccl_id=None, cull_zero=True):
+                 rank=0, world=1, nccl_id=None, cull_zero=True, keep_carriers=False):
         self.lib = load()
         coords = np.ascontiguousarray(coords, dtype=np.float64)
         if coords.ndim == 1:
@@ -198,7 +200,7 @@ class Cakf:
                           sigma_t0=st0.ctypes.data, mu0=None if mu is None else mu.ctypes.data,
                           policy=POLICIES[policy] if isinstance(policy, str) else int(policy),
                           max_iter=int(max_iter), max_rank=int(max_rank), rtol=0.0, reorth=int(bool(reorth)),
-                          cull_zero=int(bool(cull_zero)), seed=int(seed),
+                          cull_zero=int(bool(cull_zero)), keep_carriers=int(bool(keep_carriers)), seed=int(seed),
                           max_steps=int(max_steps), max_obs=int(max_obs), rank=int(rank), world=int(world),
                           nccl_id=None, stream=stream)
         self._nccl_id = None
@@ -271,6 +273,18 @@ class Cakf:
         cnt = np.zeros(n, dtype=np.int64)
         _check(self.lib.cakf_profile_read(self.h, ms.ctypes.data, cnt.ctypes.data, int(bool(reset))))
         return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(PROF_CATEGORIES)}
+
+    def interpolate(self, k: int, A1, Q1, A2=None, which: int = CAKF_SMOOTH):
+        """Mean and variance (numpy, user point order) at t in [t_k, t_{k+1}) (cakf_interpolate)."""
+        a1 = np.ascontiguousarray(A1, dtype=np.float64)
+        q1 = np.ascontiguousarray(Q1, dtype=np.float64)
+        a2 = None if A2 is None else np.ascontiguousarray(A2, dtype=np.float64)
+        mean = np.empty(self.D, dtype=self.np_dtype)
+        var = np.empty(self.D, dtype=self.np_dtype)
+        _check(self.lib.cakf_interpolate(self.h, int(k), a1.ctypes.data, q1.ctypes.data,
+                                         None if a2 is None else a2.ctypes.data, int(which),
+                                         mean.ctypes.data, var.ctypes.data))
+        return mean, var
 
     def cull_stats(self) -> dict:
         """Fractions of the dense kernel work evaluated under exact-zero culling (1.0 = none culled)."""

@@ -97,6 +97,40 @@ Mat3 mat_abat_plus_q(const Mat3& A, const Mat3& S, const Mat3& Q, int n) {
   return R;
 }
 
+Mat3 mat_mul(const Mat3& A, const Mat3& B, int n) {
+  Mat3 R{};
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int t = 0; t < n; ++t) R.a[i][j] += A.a[i][t] * B.a[t][j];
+  return R;
+}
+// Gauss-Jordan with partial pivoting (n <= 3); false if singular
+bool mat_inv(const Mat3& A, int n, Mat3& out) {
+  double M[3][6] = {};
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < n; ++j) M[i][j] = A.a[i][j];
+    M[i][n + i] = 1.0;
+  }
+  for (int c = 0; c < n; ++c) {
+    int p = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(M[r][c]) > std::fabs(M[p][c])) p = r;
+    if (M[p][c] == 0.0) return false;
+    for (int j = 0; j < 2 * n; ++j) std::swap(M[c][j], M[p][j]);
+    const double d = M[c][c];
+    for (int j = 0; j < 2 * n; ++j) M[c][j] /= d;
+    for (int r = 0; r < n; ++r)
+      if (r != c) {
+        const double f = M[r][c];
+        for (int j = 0; j < 2 * n; ++j) M[r][j] -= f * M[c][j];
+      }
+  }
+  out = Mat3{};
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) out.a[i][j] = M[i][n + j];
+  return true;
+}
+
 // host copy of a small host-or-device array of doubles
 bool fetch_doubles(const double* src, size_t n, std::vector<double>& out) {
   out.resize(n);
@@ -156,6 +190,8 @@ struct ImplBase {
   virtual int profile(bool on) = 0;
   virtual int prof_read(double* ms, int64_t* n, bool reset) = 0;
   virtual int cull_stats(double* out) = 0;
+  virtual int interpolate(int k, const double* A1, const double* Q1, const double* A2, int which, void* mean,
+                          void* var) = 0;
 };
 
 template <typename T>
@@ -246,6 +282,9 @@ struct Impl final : ImplBase {
   int *posof = nullptr, *obs_cnt = nullptr, *sigma = nullptr, *sigma_inv = nullptr;
   T *ybuf_user = nullptr, *lam2_user = nullptr, *outm = nullptr, *outv = nullptr;
   std::vector<int> perm_h;
+  // temporal interpolation (Cor. A.10): smoother carriers w^s_k, W^s_k kept per step
+  bool keep = false;
+  T *ws_st = nullptr, *Ws_st = nullptr, *ip_m = nullptr, *ip_v = nullptr, *ip_ms = nullptr, *ip_vs = nullptr;
   // per-update kd order of the observations (kd_order.cu); CAKF_NO_REORDER=1 keeps the sorted order
   bool kd_obs = [] { const char* e = getenv("CAKF_NO_REORDER"); return !(e && e[0] == '1'); }();
   int *idx_tmp = nullptr, *sig_tmp = nullptr;
@@ -509,6 +548,11 @@ struct Impl final : ImplBase {
     obs_cnt = carve<int>((NX + 1023) / 1024 + 1);
     sigma = carve<int>(Nmax);
     sigma_inv = carve<int>(Nmax);
+    ip_m = carve<T>(D); ip_v = carve<T>(D); ip_ms = carve<T>(D); ip_vs = carve<T>(D);
+    if (keep) {
+      ws_st = carve<T>((size_t)(Tmax + 1) * D);
+      Ws_st = carve<T>((size_t)(Tmax + 1) * D * std::max(qmax, 1));
+    }
     idx_tmp = carve<int>(Nmax);
     sig_tmp = carve<int>(Nmax);
     kd_ws_bytes = kd_obs_workspace((int)Nmax);
@@ -556,6 +600,7 @@ struct Impl final : ImplBase {
     nhat = c.max_iter; rcap = c.max_rank; Tmax = c.max_steps; NX = c.n_space; D = NX * Dp;
     Nmax = c.max_obs > 0 ? std::min<int64_t>(c.max_obs, NX) : NX;
     rtol = c.rtol; ell = c.ell_x; seed = c.seed; reorth = c.reorth != 0;
+    keep = c.keep_carriers != 0;
     cull = c.cull_zero != 0 && sizeof(T) == 4;
     world = std::max(1, c.world); rank = c.rank;
     if (world > 1) {
@@ -984,6 +1029,7 @@ struct Impl final : ImplBase {
     CK_CUDA(StepKernels<T>::fill((size_t)std::max(ST.N, 1), T(0), R, st));
     CK_CUDA(StepKernels<T>::ws_build(ST.N, D, ST.n, 0, ST.idx, X, ST.XV, R, Ws, ws, st));
     ST.smoother_rank = q;
+    CK(keep_carriers(T_, q));
     for (int k = T_ - 1; k >= 0; --k) {
       Step& S = steps[k];
       const int C = 1 + q;
@@ -1026,8 +1072,88 @@ struct Impl final : ImplBase {
         q = qn;
       }
       S.smoother_rank = q;
+      CK(keep_carriers(k, q));
     }
     smoothed = true;
+    return CAKF_OK;
+  }
+
+  int keep_carriers(int k, int q) {
+    if (!keep) return CAKF_OK;
+    if (q > std::max(qmax, 1)) return fail(CAKF_E_ARG, "smoother carrier rank exceeds the kept capacity");
+    CK_CUDA(cudaMemcpyAsync(ws_st + (size_t)k * D, ws, D * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    if (q)
+      CK_CUDA(cudaMemcpyAsync(Ws_st + (size_t)k * D * std::max(qmax, 1), Ws, (size_t)D * q * sizeof(T),
+                              cudaMemcpyDeviceToDevice, st));
+    return CAKF_OK;
+  }
+
+  // Cor. A.10 / alg:cakf-interpolation / alg:caks-interpolation: the filter (and
+  // smoother) state at t in [t_k, t_{k+1}) from the stored step-k filter state, the filter factor
+  // M~_k and the step-(k+1) smoother carriers; A1 = A(t, t_k), Q1 = Q(t, t_k), A2 = A(t_{k+1}, t).
+  // M~_k = (A_{k+1}^-1 (x) I) M^-_{k+1} for k < T (already stored), else the last truncation output.
+  int interpolate(int k, const double* A1p, const double* Q1p, const double* A2p, int which, void* mean,
+                  void* var) override {
+    if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
+    if (k < 1 || k > kcur) return fail(CAKF_E_ARG, "interpolate: k outside [1, steps done]");
+    if (k == kcur && phase != 0) return fail(CAKF_E_STATE, "interpolate: step k not truncated yet");
+    if (which != CAKF_FILTER && which != CAKF_SMOOTH) return fail(CAKF_E_ARG, "interpolate: bad which");
+    const bool smooth_q = which == CAKF_SMOOTH;
+    if (smooth_q && !smoothed) return fail(CAKF_E_STATE, "interpolate: caks_smooth has not run");
+    if (smooth_q && k < kcur && !keep) return fail(CAKF_E_STATE, "interpolate: create with keep_carriers = 1");
+    if (!A1p || !Q1p || (smooth_q && k < kcur && !A2p))
+      return fail(CAKF_E_ARG, "interpolate: A1, Q1 (and A2) are required");
+    std::vector<double> a1, q1, a2;
+    if (!fetch_doubles(A1p, (size_t)Dp * Dp, a1) || !fetch_doubles(Q1p, (size_t)Dp * Dp, q1))
+      return fail(CAKF_E_ARG, "interpolate: cannot read A1/Q1");
+    const Mat3 A1 = mat_from(a1.data(), Dp), Q1 = mat_from(q1.data(), Dp);
+    Step& S = steps[k];
+    const Mat3 sig_t = mat_abat_plus_q(A1, S.sig_t, Q1, Dp);          // Sigma^t(t)
+    CK_CUDA(StepKernels<T>::mix((int)NX, Dp, 1, A1, false, S.m, D, ip_m, D, st));   // m(t) = A1 m_k
+    // M(t) = A1 M~_k, into the smoother scratch Wf
+    int rt = 0;
+    if (k < kcur) {
+      const Step& S1 = steps[k + 1];
+      Mat3 Ainv{};
+      if (!mat_inv(S.A_next, Dp, Ainv)) return fail(CAKF_E_NUMERIC, "interpolate: singular A_{k+1}");
+      rt = S1.rin;
+      if (rt) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, rt, mat_mul(A1, Ainv, Dp), false, S1.Mk, D, Wf, D, st));
+    } else {
+      rt = S.truncated ? S.rank_out : S.cols;
+      if (rt) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, rt, A1, false, S.truncated ? Mtil : S.Mk, D, Wf, D, st));
+    }
+    CK_CUDA(StepKernels<T>::rowvar((int)NX, Dp, sig_t, nullptr, Wf, D, rt, ip_v, st));
+    const T *pm = ip_m, *pv = ip_v;
+    if (smooth_q && k < kcur) {
+      if (!fetch_doubles(A2p, (size_t)Dp * Dp, a2)) return fail(CAKF_E_ARG, "interpolate: cannot read A2");
+      const Mat3 A2 = mat_from(a2.data(), Dp);
+      const int q = steps[k + 1].smoother_rank, C = 1 + q;
+      const T* wsk = ws_st + (size_t)(k + 1) * D;
+      const T* Wsk = Ws_st + (size_t)(k + 1) * D * std::max(qmax, 1);
+      // x = A2^T [w^s_{k+1}, W^s_{k+1}];  y = P(t) x = Sigma(t) x - M(t) (M(t)^T x)
+      CK_CUDA(StepKernels<T>::mix((int)NX, Dp, 1, A2, true, wsk, D, X, D, st));
+      if (q) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, q, A2, true, Wsk, D, X + D, D, st));
+      CK(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX, cull ? act_cnt_sm : nullptr, act_list_sm,
+            act_stride_sm));
+      CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, C, sig_t, Yk, yb, st));
+      if (rt) {
+        CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rt, C, (int)D, 1.0, Wf, (int)D, X, (int)D, 0.0, Tm, rt));
+        CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, C, rt, -1.0, Wf, (int)D, Tm, rt, 1.0, yb, (int)D));
+      }
+      // m^s(t) = m(t) + y_0 ; var^s(t) = var(t) - rowsumsq(y_{1:})
+      CK_CUDA(StepKernels<T>::smooth_out(D, C, ip_m, ip_v, yb, ip_ms, ip_vs, st));
+      pm = ip_ms;
+      pv = ip_vs;
+    }
+    if (mean) {
+      CK_CUDA(unpermute<T>((int)NX, Dp, perm_d, pm, outm, st));
+      CK_CUDA(cudaMemcpyAsync(mean, outm, D * sizeof(T), cudaMemcpyDefault, st));
+    }
+    if (var) {
+      CK_CUDA(unpermute<T>((int)NX, Dp, perm_d, pv, outv, st));
+      CK_CUDA(cudaMemcpyAsync(var, outv, D * sizeof(T), cudaMemcpyDefault, st));
+    }
+    CK_CUDA(cudaStreamSynchronize(st));
     return CAKF_OK;
   }
 
@@ -1186,6 +1312,11 @@ int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset) {
   return h->impl->prof_read(ms, launches, reset != 0);
 }
 int64_t cakf_kernel_launches(void) { return (int64_t)launch_counter(); }
+int cakf_interpolate(cakf_t h, int32_t k, const double* A1, const double* Q1, const double* A2, int32_t which,
+                     void* mean_D, void* var_D) {
+  HANDLE_CHECK(h);
+  return h->impl->interpolate(k, A1, Q1, A2, which, mean_D, var_D);
+}
 int cakf_cull_stats(cakf_t h, double* frac3) {
   HANDLE_CHECK(h);
   if (!frac3) return fail(CAKF_E_ARG, "NULL output");

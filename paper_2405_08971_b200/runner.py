@@ -27,14 +27,15 @@ def transitions(problem):
     return out, Sinf
 
 
-def make_handle(problem, dtype="f32", stream=None, max_steps=None, rank=0, world=1, nccl_id=None, cull_zero=True):
+def make_handle(problem, dtype="f32", stream=None, max_steps=None, rank=0, world=1, nccl_id=None, cull_zero=True,
+                keep_carriers=False):
     _, Sinf = transitions(problem)
     max_obs = max((len(i) for i in problem.obs_idx), default=0)
     return Cakf(problem.coords, problem.ell_x, Sinf, dtype=dtype, d_time=problem.d_time, nu_x=problem.nu_x,
                 policy=problem.policy, max_iter=problem.max_iter, max_rank=problem.max_rank,
                 seed=problem.action_seed, max_steps=max_steps or problem.T, max_obs=max(max_obs, 1),
                 reorth=getattr(problem, "reorth", True), stream=stream, rank=rank, world=world, nccl_id=nccl_id,
-                cull_zero=cull_zero)
+                cull_zero=cull_zero, keep_carriers=keep_carriers)
 
 
 def stage_inputs(problem, dtype="f32", device="cuda"):
