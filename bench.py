@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cull", action="store_true", help="disable exact-zero culling (results are bit-identical)")
     ap.add_argument("--no-dense", action="store_true", help="skip the reference timing with culling off")
+    ap.add_argument("--no-interp", action="store_true", help="skip the temporal-interpolation query timing")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--T", type=int, default=None, help="override T (debug only; invalidates the metric)")
     return ap.parse_args()
@@ -400,6 +401,31 @@ def main():
                                         "algorithmic_per_launch": f"{pairs:.4g} unique pairs N(N+1)/2"},
                         "phase_ms_per_step": {c: round(dprof[c][0], 3) for c in dprof}}
         hd.destroy()
+    if world == 1 and not args.no_interp:
+        # temporal interpolation (Cor. A.10): one pass with the smoother carriers
+        # kept, then filter / smoother queries at mid-interval times, device-timed per query
+        from paper_2405_08971_b200 import CAKF_FILTER
+        hi = runner.make_handle(wl, args.dtype, stream=stream.cuda_stream, cull_zero=not args.no_cull,
+                                keep_carriers=True)
+        runner.run(hi, trans, inputs, smooth=True)
+        barrier()
+        q = {}
+        for which, name in ((CAKF_FILTER, "filter"), (CAKF_SMOOTH, "smoother")):
+            times_ms = []
+            for k in (wl.T // 4, wl.T // 2, (3 * wl.T) // 4):
+                dt = float(wl.dts[k])
+                A1, Q1, _ = binding.matern_transition(wl.nu_t, wl.ell_t, wl.sigma, 0.5 * dt)
+                A2 = binding.matern_transition(wl.nu_t, wl.ell_t, wl.sigma, 0.5 * dt)[0]
+                q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                q0.record(stream)
+                hi.interpolate(k, A1, Q1, A2, which)      # synchronises (device -> host copy of the result)
+                q1.record(stream)
+                q1.synchronize()
+                times_ms.append(q0.elapsed_time(q1))
+            q[name] = round(statistics.median(times_ms), 3)
+        out["interpolation_ms_per_query"] = dict(q, note="cakf_interpolate at t = (t_k + t_k+1)/2, k = T/4, T/2, "
+                                                 "3T/4; includes the D2H copy of mean and variance")
+        hi.destroy()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = oracle_sample(wl)
         out["cpu_baseline"] = {"value": 1.0 / smp["sec_per_timestep"], "unit": "time-steps/s",
