@@ -78,7 +78,7 @@ def test_exact_zero_culling_is_bit_identical_cfg3():
     real share of the K1 / K2 tiles is skipped at cfg3's lengthscale."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    from paper_2405_08971_b200 import runner
+    from paper_2405_08971_b200 import CAKF_FILTER, CAKF_SMOOTH, runner
     wl = make_workload("cfg3", T=3, max_iter=24, max_rank=48)
     trans = runner.transitions(wl)[0]
     inputs = runner.stage_inputs(wl, "f32")
@@ -87,7 +87,7 @@ def test_exact_zero_culling_is_bit_identical_cfg3():
         h = runner.make_handle(wl, "f32", cull_zero=cull)
         runner.run(h, trans, inputs)
         h.sync()
-        outs.append([runner.collect(h, wl.T, w) for w in (0, 1)])
+        outs.append([runner.collect(h, wl.T, w) for w in (CAKF_FILTER, CAKF_SMOOTH)])
         fracs.append(h.cull_stats())
         h.destroy()
     for a, b in zip(outs[0], outs[1]):
@@ -96,3 +96,39 @@ def test_exact_zero_culling_is_bit_identical_cfg3():
     assert fracs[0] == {"k1_matvec": 1.0, "k2_post": 1.0, "k2_smooth": 1.0}
     print("cull fractions", fracs[1])
     assert all(0.0 < f < 0.9 for f in fracs[1].values())
+
+
+def test_cfg4_maximum_size():
+    """The largest configuration (BASELINE cfg4: N_X = 501,000, D = 1,002,000, N = 376,500,
+    r = 1024) on one GPU: the symmetric K1 at N = 376,500 on sampled rows vs the oracle, and a
+    3-step filter + smoother pass whose outputs are finite and within [0, prior] variance."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2405_08971_b200 import CAKF_FILTER, CAKF_SMOOTH, runner
+    wl = make_workload("cfg4", T=3)
+    Xt = wl.coords[wl.obs_idx[0]]
+    rng = np.random.default_rng(4)
+    s = rng.standard_normal(len(Xt))
+    xt = torch.tensor(Xt.astype(np.float32), device="cuda")
+    y = binding.gram_matmul(xt, xt, torch.tensor(s.astype(np.float32), device="cuda"), wl.nu_x,
+                            wl.ell_x).double().cpu().numpy()
+    rows = np.concatenate([np.arange(128), np.arange(len(Xt) - 61, len(Xt))])
+    X64 = Xt.astype(np.float32).astype(np.float64)
+    s64 = s.astype(np.float32).astype(np.float64)
+    ref = mfree.gram_apply(X64[rows], X64, s64, wl.nu_x, wl.ell_x, chunk=32)
+    scale = mfree.gram_apply(X64[rows], X64, np.abs(s64), wl.nu_x, wl.ell_x, chunk=32)
+    assert float(np.max(np.abs(y[rows] - ref) / scale)) < 1e-6
+    del xt
+    trans, Sinf = runner.transitions(wl)
+    h = runner.make_handle(wl, "f32")
+    runner.run(h, trans, runner.stage_inputs(wl, "f32"))
+    h.sync()
+    prior = np.repeat(np.diag(Sinf), wl.n_space)
+    for k in range(wl.T + 1):
+        for which in (CAKF_FILTER, CAKF_SMOOTH):
+            m, v = h.get(k, which)
+            assert np.all(np.isfinite(m)) and np.all(np.isfinite(v))
+            assert np.all(v <= prior * (1 + 1e-5)) and np.all(v >= -1e-3 * prior)
+    assert [h.get_stats(k)["rank_out"] for k in range(1, wl.T + 1)] == [64, 128, 192]
+    assert 0.0 < h.cull_stats()["k1_matvec"] < 0.2
+    h.destroy()
