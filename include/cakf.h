@@ -210,6 +210,24 @@ int64_t cakf_kernel_launches(void);
 int cakf_interpolate(cakf_t h, int32_t k, const double* A1, const double* Q1, const double* A2, int32_t which,
                      void* mean_D, void* var_D);
 
+/* Posterior sampler (alg:cakf-caks-sampler P:1336-1358; Matheron's rule P:1150-1216, Prop A.9
+ * P:1290-1313): S samples of the CAKF (which = CAKF_FILTER) or CAKS (CAKF_SMOOTH) posterior
+ * at every step k = 0..T from the stored filter trace, given the caller's prior draws (the
+ * random numbers the method consumes are inputs; the smoother does not have to have run):
+ *   forward  x^-_k = A_{k-1} x_{k-1} + q_{k-1};  w_k = H_k^T V_k V_k^T (y_k - H_k x^-_k - eps_k);
+ *            x_k = x^-_k + P^-_k w_k
+ *   backward x^s_k = x_k + P_k A_k^T w^s_{k+1};  w^s_k = w_k + (I - W_k W_k^T P^-_k) A_k^T w^s_{k+1}
+ * (R25: eps_k is a full-space draw of N(0, Lambda_k), equivalent to the paper's projected noise).
+ *   x0  : D x S column-major draws of N(mu_0, Sigma_0), user point order, dtype
+ *   q   : T blocks of D x S, block k-1 = draws of N(0, Q^t_{k-1} (x) K_X) into step k
+ *   eps : for k = 1..T, an N_k x S block of N(0, Lambda_k) draws in the observation order passed
+ *         to cakf_update at step k (missing steps contribute no block)
+ *   out : (T+1) blocks of D x S, user point order.  All host or device.  1 <= S <= 1 + max_iter.
+ * Valid after the last cakf_truncate.  Synchronises the handle's stream.
+ * Errors: CAKF_E_ARG, CAKF_E_STATE, CAKF_E_CUDA, CAKF_E_NOMEM (workspace). */
+int cakf_sample(cakf_t h, int32_t n_samples, const void* x0, const void* q, const void* eps, int32_t which,
+                void* out);
+
 /* Exact-zero culling statistics of the handle so far: frac3[0] = fraction of the symmetric K1's
  * pairs evaluated (counted in 16 x 128 warp blocks of its 128 x 128 tile pairs), frac3[1] = fraction of the post-loop K2's 128x32 tiles evaluated,
  * frac3[2] = same for the smoother's K2 (all 1.0 when culling is off).  Synchronises the handle's

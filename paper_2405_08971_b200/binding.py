@@ -60,7 +60,7 @@ EXPORTS = [
     "cakf_create", "cakf_reset", "cakf_predict", "cakf_update", "cakf_truncate", "caks_smooth", "cakf_get",
     "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
-    "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats", "cakf_interpolate",
+    "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats", "cakf_interpolate", "cakf_sample",
 ]
 PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank", "trunc_gram",
                    "trunc_eig", "trunc_gemm"]
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH):
     lib.cakf_shard_plan.argtypes = [i64, i64, i32, i32, vp]
     lib.cakf_cull_stats.argtypes = [vp, vp]
     lib.cakf_interpolate.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp]
+    lib.cakf_sample.argtypes = [vp, i32, vp, vp, vp, i32, vp]
     lib.cakf_sym_unit_blocks.argtypes = [i64, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     for name in EXPORTS:
         if name not in ("cakf_last_error", "cakf_version", "cakf_kernel_launches"):
@@ -285,6 +286,24 @@ class Cakf:
                                          None if a2 is None else a2.ctypes.data, int(which),
                                          mean.ctypes.data, var.ctypes.data))
         return mean, var
+
+    def sample(self, x0, q, eps, which: int = CAKF_SMOOTH) -> np.ndarray:
+        """Posterior samples (cakf_sample).  x0: D x S; q: list of T arrays D x S; eps: list of
+        N_k x S arrays for the non-missing steps.  Returns (T+1) x D x S (numpy, user order)."""
+        x0 = np.asarray(x0, dtype=self.np_dtype)
+        if x0.ndim == 1:
+            x0 = x0[:, None]
+        S = x0.shape[1]
+        x0f = np.asfortranarray(x0)
+        qf = np.concatenate([np.asfortranarray(np.asarray(a, dtype=self.np_dtype).reshape(self.D, S)).ravel(order="F")
+                             for a in q])
+        ef = np.concatenate([np.asfortranarray(np.asarray(a, dtype=self.np_dtype).reshape(-1, S)).ravel(order="F")
+                             for a in eps] or [np.zeros(1, dtype=self.np_dtype)])
+        T = len(q)
+        out = np.empty((T + 1) * self.D * S, dtype=self.np_dtype)
+        _check(self.lib.cakf_sample(self.h, int(S), x0f.ctypes.data, qf.ctypes.data, ef.ctypes.data, int(which),
+                                    out.ctypes.data))
+        return out.reshape(T + 1, S, self.D).transpose(0, 2, 1)
 
     def cull_stats(self) -> dict:
         """Fractions of the dense kernel work evaluated under exact-zero culling (1.0 = none culled)."""

@@ -192,6 +192,7 @@ struct ImplBase {
   virtual int cull_stats(double* out) = 0;
   virtual int interpolate(int k, const double* A1, const double* Q1, const double* A2, int which, void* mean,
                           void* var) = 0;
+  virtual int sample(int S, const void* x0, const void* q, const void* eps, int which, void* out) = 0;
 };
 
 template <typename T>
@@ -284,6 +285,9 @@ struct Impl final : ImplBase {
   std::vector<int> perm_h;
   // temporal interpolation (Cor. A.10): smoother carriers w^s_k, W^s_k kept per step
   bool keep = false;
+  // per-step observations (internal row order) and their user positions, for the sampler
+  T* y_st = nullptr;
+  int* sig_st = nullptr;
   T *ws_st = nullptr, *Ws_st = nullptr, *ip_m = nullptr, *ip_v = nullptr, *ip_ms = nullptr, *ip_vs = nullptr;
   // per-update kd order of the observations (kd_order.cu); CAKF_NO_REORDER=1 keeps the sorted order
   bool kd_obs = [] { const char* e = getenv("CAKF_NO_REORDER"); return !(e && e[0] == '1'); }();
@@ -553,6 +557,8 @@ struct Impl final : ImplBase {
       ws_st = carve<T>((size_t)(Tmax + 1) * D);
       Ws_st = carve<T>((size_t)(Tmax + 1) * D * std::max(qmax, 1));
     }
+    y_st = carve<T>((size_t)(Tmax + 1) * Nmax);
+    sig_st = carve<int>((size_t)(Tmax + 1) * Nmax);
     idx_tmp = carve<int>(Nmax);
     sig_tmp = carve<int>(Nmax);
     kd_ws_bytes = kd_obs_workspace((int)Nmax);
@@ -782,6 +788,8 @@ struct Impl final : ImplBase {
     CK_CUDA(cudaMemcpyAsync(lam2_user, noise_var, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
     CK_CUDA(gather_vec<T>(N, sigma, ybuf_user, ybuf, st));
     CK_CUDA(gather_vec<T>(N, sigma, lam2_user, lam2, st));
+    CK_CUDA(cudaMemcpyAsync(y_st + (size_t)k * Nmax, ybuf, (size_t)N * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(sig_st + (size_t)k * Nmax, sigma, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
     if (policy == CAKF_POLICY_COORD && niter > 0) {
       CK_CUDA(cudaMemcpyAsync(stage64, coord_order, (size_t)niter * sizeof(int64_t), cudaMemcpyDefault, st));
       CK_CUDA(map_order(niter, stage64, sigma_inv, order32, st));
@@ -1157,6 +1165,124 @@ struct Impl final : ImplBase {
     return CAKF_OK;
   }
 
+  // alg:cakf-caks-sampler: S posterior samples from the stored filter trace and the
+  // caller's prior draws (x0 ~ N(mu_0, Sigma_0), q_{k-1} ~ N(0, Q_{k-1}), eps_k ~ N(0, Lambda_k)).
+  // Forward: x^-_k = A x_{k-1} + q_{k-1}; w_k = H^T V_k V_k^T (y_k - H x^-_k - eps_k) (R25);
+  // x_k = x^-_k + P^-_k w_k.  Backward: x^s_k = x_k + P_k A_k^T w^s_{k+1};
+  // w^s_k = w_k + (I - W_k W_k^T P^-_k) A_k^T w^s_{k+1}.  Same kernels as the update / smoother.
+  int sample(int S, const void* x0, const void* q, const void* eps, int which, void* out) override {
+    if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
+    if (phase != 0 || kcur < 1) return fail(CAKF_E_STATE, "sample: expected after the last truncate");
+    if (S < 1 || S > 1 + std::min(nhat, qmax)) return fail(CAKF_E_ARG, "sample: n_samples outside [1, 1 + max_iter]");
+    if (which != CAKF_FILTER && which != CAKF_SMOOTH) return fail(CAKF_E_ARG, "sample: bad which");
+    if (!x0 || !q || !out || !eps) return fail(CAKF_E_ARG, "sample: x0, q, eps and out are required");
+    const int T_ = kcur;
+    const size_t DS = (size_t)D * S;
+    // device workspace: forward samples x_0..x_T, their w_k (as u_k = V V^T res, N_k x S), staging
+    size_t n_obs_total = 0;
+    for (int k = 1; k <= T_; ++k) n_obs_total += (size_t)steps[k].N;
+    T* xs = nullptr;
+    const size_t bytes = ((size_t)(T_ + 1) * DS + 3 * DS + n_obs_total * S * 2 + 1024) * sizeof(T);
+    CK_CUDA(cudaMallocAsync(&xs, bytes, st));
+    T* xtmp = xs + (size_t)(T_ + 1) * DS;   // D x S scratch (user order staging)
+    T* wsv = xtmp + DS;                     // w^s (D x S)
+    T* xsm = wsv + DS;                      // one smoother sample (D x S)
+    T* ust = xsm + DS;                      // u_k per step (N_k x S)
+    T* epsd = ust + n_obs_total * S;        // eps of all steps (device copy)
+    std::vector<size_t> uoff(T_ + 2, 0);
+    for (int k = 1; k <= T_; ++k) uoff[k + 1] = uoff[k] + (size_t)steps[k].N * S;
+    auto cleanup = [&]() { cudaFreeAsync(xs, st); };
+    auto run = [&]() -> int {
+      CK_CUDA(cudaMemcpyAsync(epsd, eps, n_obs_total * S * sizeof(T), cudaMemcpyDefault, st));
+      // x_0 (user order) -> internal
+      CK_CUDA(cudaMemcpyAsync(xtmp, x0, DS * sizeof(T), cudaMemcpyDefault, st));
+      CK_CUDA(sampler_ops<T>::permute_cols((int)NX, Dp, S, invperm_d, xtmp, D, xs, D, st));
+      for (int k = 1; k <= T_; ++k) {
+        Step& P = steps[k - 1];
+        Step& K = steps[k];
+        T* xk = xs + (size_t)k * DS;
+        // x^-_k = A x_{k-1} + q_{k-1}
+        CK_CUDA(StepKernels<T>::mix((int)NX, Dp, S, P.A_next, false, xs + (size_t)(k - 1) * DS, D, xk, D, st));
+        CK_CUDA(cudaMemcpyAsync(xtmp, static_cast<const T*>(q) + (size_t)(k - 1) * DS, DS * sizeof(T),
+                                cudaMemcpyDefault, st));
+        CK_CUDA(sampler_ops<T>::permute_cols((int)NX, Dp, S, invperm_d, xtmp, D, xsm, D, st));
+        CK_BLAS(Blas<T>::axpy(blas, (int)DS, T(1), xsm, xk));
+        const int N = K.N, n = K.n, rin = K.rin;
+        if (K.missing || N == 0) continue;
+        // u = V V^T (y - H x^- - eps)
+        T* res = R;                                         // N x S
+        CK_CUDA(sampler_ops<T>::residual(N, S, y_st + (size_t)k * Nmax, K.idx, sig_st + (size_t)k * Nmax, xk, D,
+                                         epsd + uoff[k], res, st));
+        T* u = ust + uoff[k];
+        if (n) {
+          const T* Vk = K.XV + N;
+          CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, n, S, N, 1.0, Vk, N, res, N, 0.0, tt, n));
+          CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, N, S, n, 1.0, Vk, N, tt, n, 0.0, u, N));
+        } else {
+          CK_CUDA(cudaMemsetAsync(u, 0, (size_t)N * S * sizeof(T), st));
+        }
+        // x_k = x^-_k + Sigma_k H^T u - M^- (H M^-)^T u
+        CK_CUDA(sampler_ops<T>::gather_coords(N, K.idx, coords, xcs, st));
+        CK(k2(coords, (int)NX, xcs, N, u, N, S, Yb, NX));
+        const T* tmpp = nullptr;
+        if (rin) {
+          CK_CUDA(StepKernels<T>::gather_rows(N, rin, K.idx, K.Mk, D, HM, N, st));
+          CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rin, S, N, 1.0, HM, N, u, N, 0.0, Ub, rin));
+          CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, S, rin, 1.0, K.Mk, (int)D, Ub, rin, 0.0, tmp, (int)D));
+          tmpp = tmp;
+        }
+        CK_CUDA(sampler_ops<T>::combine((int)NX, Dp, S, K.sig_t, Yb, tmpp, xk, xk, st));
+      }
+      const T* res_out = xs;   // filter samples
+      if (which == CAKF_SMOOTH) {
+        // w^s_T = w_T = H^T u_T
+        CK_CUDA(cudaMemsetAsync(wsv, 0, DS * sizeof(T), st));
+        if (!steps[T_].missing && steps[T_].N)
+          CK_CUDA(sampler_ops<T>::scatter_rows(steps[T_].N, S, steps[T_].idx, ust + uoff[T_], T(1), wsv, D, st));
+        for (int k = T_ - 1; k >= 0; --k) {
+          Step& K = steps[k];
+          const int N = K.N, n = K.n, rin = K.rin;
+          // z = A_k^T w^s_{k+1};  y = P^-_k z = Sigma_k z - M^- (M^-^T z)
+          CK_CUDA(StepKernels<T>::mix((int)NX, Dp, S, K.A_next, true, wsv, D, X, D, st));
+          CK(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * S, Yk, NX, cull ? act_cnt_sm : nullptr, act_list_sm,
+                act_stride_sm));
+          CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, S, K.sig_t, Yk, yb, st));
+          if (rin) {
+            CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rin, S, (int)D, 1.0, K.Mk, (int)D, X, (int)D, 0.0, Tm, rin));
+            CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, S, rin, -1.0, K.Mk, (int)D, Tm, rin, 1.0, yb, (int)D));
+          }
+          // w^s_k = w_k + z - H^T V (V^T H y);  P_k z = y - B_k (V^T H y)
+          CK_CUDA(cudaMemcpyAsync(wsv, X, DS * sizeof(T), cudaMemcpyDeviceToDevice, st));
+          if (!K.missing && N) {
+            CK_CUDA(sampler_ops<T>::scatter_rows(N, S, K.idx, ust + uoff[k], T(1), wsv, D, st));
+            if (n) {
+              const T* Vk = K.XV + N;
+              CK_CUDA(StepKernels<T>::gather_rows(N, S, K.idx, yb, D, Hy, N, st));
+              CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, n, S, N, 1.0, Vk, N, Hy, N, 0.0, tt, n));
+              CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, N, S, n, 1.0, Vk, N, tt, n, 0.0, R, N));
+              CK_CUDA(sampler_ops<T>::scatter_rows(N, S, K.idx, R, T(-1), wsv, D, st));
+              CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, S, n, -1.0, K.Mk + (size_t)rin * D, (int)D, tt, n, 1.0, yb,
+                      (int)D));
+            }
+          }
+          // x^s_k = x_k + P_k z  (in place over the forward sample: the forward x_k is not needed again)
+          CK_BLAS(Blas<T>::axpy(blas, (int)DS, T(1), yb, xs + (size_t)k * DS));
+        }
+      }
+      // internal -> user order, to the caller's buffer: (T+1) x D x S
+      for (int k = 0; k <= T_; ++k) {
+        CK_CUDA(sampler_ops<T>::permute_cols((int)NX, Dp, S, perm_d, res_out + (size_t)k * DS, D, xtmp, D, st));
+        CK_CUDA(cudaMemcpyAsync(static_cast<T*>(out) + (size_t)k * DS, xtmp, DS * sizeof(T), cudaMemcpyDefault, st));
+      }
+      CK_CUDA(cudaStreamSynchronize(st));
+      return CAKF_OK;
+    };
+    const int rc = run();
+    cleanup();
+    if (rc == CAKF_OK) CK_CUDA(cudaStreamSynchronize(st));
+    return rc;
+  }
+
   int get(int k, int which, void* mean, void* var) override {
     if (k < 0 || k > kcur) return fail(CAKF_E_ARG, "get: step index out of range");
     Step& S = steps[k];
@@ -1316,6 +1442,11 @@ int cakf_interpolate(cakf_t h, int32_t k, const double* A1, const double* Q1, co
                      void* mean_D, void* var_D) {
   HANDLE_CHECK(h);
   return h->impl->interpolate(k, A1, Q1, A2, which, mean_D, var_D);
+}
+int cakf_sample(cakf_t h, int32_t n_samples, const void* x0, const void* q, const void* eps, int32_t which,
+                void* out) {
+  HANDLE_CHECK(h);
+  return h->impl->sample(n_samples, x0, q, eps, which, out);
 }
 int cakf_cull_stats(cakf_t h, double* frac3) {
   HANDLE_CHECK(h);

@@ -540,6 +540,61 @@ __global__ void assemble_slices_kernel(int M, int C, int slice, const T* __restr
   Y[row + (size_t)c * ldy] = G[(size_t)p * slice * C + (row - (size_t)p * slice) + (size_t)c * slice];
 }
 
+// ---- posterior sampler (alg:cakf-caks-sampler), S samples as columns
+// out[d*NX + map[i] + s*ldo] = in[d*NX + i + s*ldi]
+template <typename T>
+__global__ void permute_cols_kernel(int NX, int Dp, int S, const int* __restrict__ map, const T* __restrict__ in,
+                                    size_t ldi, T* __restrict__ out, size_t ldo) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t D = (size_t)NX * Dp;
+  if (e >= D * S) return;
+  const size_t s = e / D, r = e % D;
+  const int d = (int)(r / NX), i = (int)(r % NX);
+  out[(size_t)d * NX + map[i] + s * ldo] = in[r + s * ldi];
+}
+// res[j, s] = y[j] - x^-[idx[j], s] - eps_user[sigma[j], s]   (R25: full-space noise draws)
+template <typename T>
+__global__ void sample_residual_kernel(int N, int S, const T* __restrict__ y, const int* __restrict__ idx,
+                                       const int* __restrict__ sigma, const T* __restrict__ xp, size_t D,
+                                       const T* __restrict__ eps, T* __restrict__ res) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N * S) return;
+  const int j = (int)(e % N), s = (int)(e / N);
+  res[e] = y[j] - xp[idx[j] + (size_t)s * D] - eps[sigma[j] + (size_t)s * N];
+}
+// x[p, s] = x^-[p, s] + Sigma^t_{d,0} Y[q, s] - tmp[p, s]   (p = d*NX + q): x^- + P^- w for w in block 0
+template <typename T>
+__global__ void sample_combine_kernel(int NX, int Dp, int S, Mat3 Sg, const T* __restrict__ Y,
+                                      const T* __restrict__ tmp, int has_tmp, const T* __restrict__ xp,
+                                      T* __restrict__ x) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t D = (size_t)NX * Dp;
+  if (e >= D * S) return;
+  const size_t s = e / D, p = e % D;
+  const int d = (int)(p / NX), q = (int)(p % NX);
+  T v = xp[e] + (T)Sg.a[d][0] * Y[q + s * NX];
+  if (has_tmp) v -= tmp[e];
+  x[e] = v;
+}
+// w[idx[j], s] += sign * R[j, s]  (H^T R into the block-0 rows)
+template <typename T>
+__global__ void scatter_rows_kernel(int N, int S, const int* __restrict__ idx, const T* __restrict__ R, T sign,
+                                    T* __restrict__ w, size_t D) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N * S) return;
+  const int j = (int)(e % N), s = (int)(e / N);
+  w[idx[j] + (size_t)s * D] += sign * R[e];
+}
+template <typename T>
+__global__ void gather_coords_kernel(int N, const int* __restrict__ idx, const V4<T>* __restrict__ coords,
+                                     V4<T>* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  V4<T> c = coords[idx[j]];
+  c.w = T(0);
+  out[j] = c;
+}
+
 // ---- observation sort: internal index order (spatially compact tiles), fully on device
 __global__ void obs_mark_kernel(int N, const int64_t* __restrict__ obs, const int* __restrict__ invperm,
                                 int* __restrict__ posof) {
@@ -793,6 +848,45 @@ cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_
 template cudaError_t convert<float, double>(int, int, const float*, size_t, double*, size_t, cudaStream_t);
 template cudaError_t convert<double, float>(int, int, const double*, size_t, float*, size_t, cudaStream_t);
 template cudaError_t convert<double, double>(int, int, const double*, size_t, double*, size_t, cudaStream_t);
+
+template <typename T>
+cudaError_t sampler_ops<T>::permute_cols(int NX, int Dp, int S, const int* map, const T* in, size_t ldi, T* out,
+                                         size_t ldo, cudaStream_t st) {
+  const size_t n = (size_t)NX * Dp * S;
+  if (!n) return cudaSuccess;
+  permute_cols_kernel<T><<<nblk(n), 256, 0, st>>>(NX, Dp, S, map, in, ldi, out, ldo);
+  return note_launch_err();
+}
+template <typename T>
+cudaError_t sampler_ops<T>::residual(int N, int S, const T* y, const int* idx, const int* sigma, const T* xp, size_t D,
+                                     const T* eps, T* res, cudaStream_t st) {
+  if ((size_t)N * S == 0) return cudaSuccess;
+  sample_residual_kernel<T><<<nblk((size_t)N * S), 256, 0, st>>>(N, S, y, idx, sigma, xp, D, eps, res);
+  return note_launch_err();
+}
+template <typename T>
+cudaError_t sampler_ops<T>::combine(int NX, int Dp, int S, const Mat3& Sg, const T* Y, const T* tmp, const T* xp, T* x,
+                                    cudaStream_t st) {
+  const size_t n = (size_t)NX * Dp * S;
+  if (!n) return cudaSuccess;
+  sample_combine_kernel<T><<<nblk(n), 256, 0, st>>>(NX, Dp, S, Sg, Y, tmp, tmp ? 1 : 0, xp, x);
+  return note_launch_err();
+}
+template <typename T>
+cudaError_t sampler_ops<T>::scatter_rows(int N, int S, const int* idx, const T* R, T sign, T* w, size_t D,
+                                         cudaStream_t st) {
+  if ((size_t)N * S == 0) return cudaSuccess;
+  scatter_rows_kernel<T><<<nblk((size_t)N * S), 256, 0, st>>>(N, S, idx, R, sign, w, D);
+  return note_launch_err();
+}
+template <typename T>
+cudaError_t sampler_ops<T>::gather_coords(int N, const int* idx, const V4<T>* coords, V4<T>* out, cudaStream_t st) {
+  if (N <= 0) return cudaSuccess;
+  gather_coords_kernel<T><<<nblk(N), 256, 0, st>>>(N, idx, coords, out);
+  return note_launch_err();
+}
+template struct sampler_ops<float>;
+template struct sampler_ops<double>;
 
 cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int* posof, int* counts, int* idx_out,
                      int* sigma, int* sigma_inv, cudaStream_t st) {

@@ -71,4 +71,17 @@ struct StepKernels {
   static cudaError_t assemble_slices(int M, int C, int slice, const T* G, T* Y, size_t ldy, cudaStream_t st);
 };
 
+// posterior sampler helpers (alg:cakf-caks-sampler); S samples as columns
+template <typename T>
+struct sampler_ops {
+  static cudaError_t permute_cols(int NX, int Dp, int S, const int* map, const T* in, size_t ldi, T* out, size_t ldo,
+                                  cudaStream_t st);
+  static cudaError_t residual(int N, int S, const T* y, const int* idx, const int* sigma, const T* xp, size_t D,
+                              const T* eps, T* res, cudaStream_t st);
+  static cudaError_t combine(int NX, int Dp, int S, const Mat3& Sg, const T* Y, const T* tmp, const T* xp, T* x,
+                             cudaStream_t st);
+  static cudaError_t scatter_rows(int N, int S, const int* idx, const T* R, T sign, T* w, size_t D, cudaStream_t st);
+  static cudaError_t gather_coords(int N, const int* idx, const V4<T>* coords, V4<T>* out, cudaStream_t st);
+};
+
 }  // namespace cakf
