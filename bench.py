@@ -425,6 +425,26 @@ def main():
             q[name] = round(statistics.median(times_ms), 3)
         out["interpolation_ms_per_query"] = dict(q, note="cakf_interpolate at t = (t_k + t_k+1)/2, k = T/4, T/2, "
                                                  "3T/4; includes the D2H copy of mean and variance")
+        # posterior sampler (alg:cakf-caks-sampler): S joint samples of all T+1
+        # states; the draws are standard normal here (timing only: the cost does not depend on them)
+        S = 4
+        rng = np.random.default_rng(0)
+        npdt = np.float32 if args.dtype == "f32" else np.float64
+        x0 = torch.from_numpy(rng.standard_normal((S, wl.D)).astype(npdt)).cuda().T.contiguous().T
+        qd = torch.from_numpy(rng.standard_normal((wl.T, S, wl.D)).astype(npdt)).cuda()
+        ed = torch.from_numpy(rng.standard_normal(sum(len(i) for i in wl.obs_idx) * S).astype(npdt)).cuda()
+        outd = torch.empty(((wl.T + 1) * S * wl.D,), dtype=qd.dtype, device="cuda")
+        smp = {}
+        for which, name in ((CAKF_FILTER, "filter"), (CAKF_SMOOTH, "smoother")):
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            binding._check(hi.lib.cakf_sample(hi.h, S, x0.data_ptr(), qd.data_ptr(), ed.data_ptr(), which,
+                                              outd.data_ptr()))
+            s1.record(stream)
+            s1.synchronize()
+            smp[name] = round(s0.elapsed_time(s1), 3)
+        out["sampler_ms_per_call"] = dict(smp, samples=S, note="cakf_sample: S joint samples of the T+1 states "
+                                          "(device buffers; standard-normal draws for timing)")
         hi.destroy()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = oracle_sample(wl)

@@ -1223,7 +1223,12 @@ struct Impl final : ImplBase {
         }
         // x_k = x^-_k + Sigma_k H^T u - M^- (H M^-)^T u
         CK_CUDA(sampler_ops<T>::gather_coords(N, K.idx, coords, xcs, st));
-        CK(k2(coords, (int)NX, xcs, N, u, N, S, Yb, NX));
+        if (cull) {   // this step's active K-block lists (as in its update)
+          CK_CUDA(launch_tile_spheres(reinterpret_cast<const float4*>(xcs), N, 32, sph_o32, st));
+          CK_CUDA(launch_k2_active(sph_x128, (int)((NX + 127) / 128), sph_o32, (N + 31) / 32, kCullCut, act_cnt_po,
+                                   act_list_po, act_stride_po, nullptr, st));
+        }
+        CK(k2(coords, (int)NX, xcs, N, u, N, S, Yb, NX, cull ? act_cnt_po : nullptr, act_list_po, act_stride_po));
         const T* tmpp = nullptr;
         if (rin) {
           CK_CUDA(StepKernels<T>::gather_rows(N, rin, K.idx, K.Mk, D, HM, N, st));
