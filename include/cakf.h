@@ -98,6 +98,11 @@ typedef struct {
   int32_t cull_zero;        /* 1 = exact-zero culling (fp32 only): skip kernel tiles whose every
                                value underflows to exactly 0 in fp32 (bounding-sphere distance in
                                prescaled units > 88); results are bit-identical to 0 */
+  int32_t block_actions;    /* b >= 1: the non-adaptive policies (random, coordinate) evaluate the
+                               kernel part of G s for b consecutive actions with one multi-RHS
+                               product (K2, tensor cores); same arithmetic as b sequential
+                               iterations.  1 = one K1 matvec per iteration.  Ignored
+                               for CG (each action depends on the previous residual)              */
   int32_t keep_carriers;    /* 1 = keep the smoother carriers w^s_k, W^s_k of every step (an extra
                                (T+1) x D x (1 + r) values) so cakf_interpolate can return smoother
                                states between steps (Cor. A.10); 0 = filter interpolation only */

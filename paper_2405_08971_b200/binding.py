@@ -38,7 +38,7 @@ class cakf_config(ctypes.Structure):
         ("space_dim", ctypes.c_int32), ("coords", ctypes.c_void_p), ("spatial_kernel", ctypes.c_int32),
         ("ell_x", ctypes.c_double), ("sigma_t0", ctypes.c_void_p), ("mu0", ctypes.c_void_p),
         ("policy", ctypes.c_int32), ("max_iter", ctypes.c_int32), ("max_rank", ctypes.c_int32),
-        ("rtol", ctypes.c_double), ("reorth", ctypes.c_int32), ("cull_zero", ctypes.c_int32), ("keep_carriers", ctypes.c_int32), ("seed", ctypes.c_uint64), ("max_steps", ctypes.c_int32),
+        ("rtol", ctypes.c_double), ("reorth", ctypes.c_int32), ("cull_zero", ctypes.c_int32), ("block_actions", ctypes.c_int32), ("keep_carriers", ctypes.c_int32), ("seed", ctypes.c_uint64), ("max_steps", ctypes.c_int32),
         ("max_obs", ctypes.c_int64), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
     ]
@@ -185,7 +185,7 @@ class Cakf:
 
     def __init__(self, coords, ell_x, sigma_t0, *, dtype="f32", d_time=2, nu_x=1.5, mu0=None, policy="cg",
                  max_iter=64, max_rank=-1, seed=1, max_steps=48, max_obs=0, reorth=True, stream=None,
-                 rank=0, world=1, nccl_id=None, cull_zero=True, keep_carriers=False):
+                 rank=0, world=1, nccl_id=None, cull_zero=True, keep_carriers=False, block_actions=1):
         self.lib = load()
         coords = np.ascontiguousarray(coords, dtype=np.float64)
         if coords.ndim == 1:
@@ -201,7 +201,8 @@ class Cakf:
                           sigma_t0=st0.ctypes.data, mu0=None if mu is None else mu.ctypes.data,
                           policy=POLICIES[policy] if isinstance(policy, str) else int(policy),
                           max_iter=int(max_iter), max_rank=int(max_rank), rtol=0.0, reorth=int(bool(reorth)),
-                          cull_zero=int(bool(cull_zero)), keep_carriers=int(bool(keep_carriers)), seed=int(seed),
+                          cull_zero=int(bool(cull_zero)), keep_carriers=int(bool(keep_carriers)), block_actions=int(block_actions),
+                          seed=int(seed),
                           max_steps=int(max_steps), max_obs=int(max_obs), rank=int(rank), world=int(world),
                           nccl_id=None, stream=stream)
         self._nccl_id = None

@@ -285,6 +285,9 @@ struct Impl final : ImplBase {
   std::vector<int> perm_h;
   // temporal interpolation (Cor. A.10): smoother carriers w^s_k, W^s_k kept per step
   bool keep = false;
+  // block execution of the non-adaptive policies: b actions' G s per K2 launch
+  int blk = 1;
+  int *act_cnt_tt = nullptr, *act_list_tt = nullptr;
   // per-step observations (internal row order) and their user positions, for the sampler
   T* y_st = nullptr;
   int* sig_st = nullptr;
@@ -597,6 +600,8 @@ struct Impl final : ImplBase {
       cull_ctr = carve<unsigned long long>(4);
       k1_list = carve<int>((size_t)matvec_sym_units((int)Nmax) + 1);
       k1_mask = carve<unsigned short>((size_t)matvec_sym_units((int)Nmax) + 1);
+      act_cnt_tt = carve<int>(no128);
+      act_list_tt = carve<int>((size_t)no128 * no32);
       k1_count = carve<int>(1);
     }
   }
@@ -607,6 +612,7 @@ struct Impl final : ImplBase {
     Nmax = c.max_obs > 0 ? std::min<int64_t>(c.max_obs, NX) : NX;
     rtol = c.rtol; ell = c.ell_x; seed = c.seed; reorth = c.reorth != 0;
     keep = c.keep_carriers != 0;
+    blk = std::max(1, std::min<int>(c.block_actions, std::max(1, 1 + nhat)));
     cull = c.cull_zero != 0 && sizeof(T) == 4;
     world = std::max(1, c.world); rank = c.rank;
     if (world > 1) {
@@ -821,6 +827,18 @@ struct Impl final : ImplBase {
     const int nch = sym ? matvec_sym_tiles(N)
                         : std::max(1, std::min<int>(matvec_chunks(N, N, sizeof(T)), (int)(partial_cap / N)));
     T* V = S.XV + N;
+    // Non-adaptive policies (random, coordinate) with block_actions = b > 1: the actions of b
+    // consecutive iterations are known in advance, so K_TT [s_i .. s_{i+b-1}] is one multi-RHS K2
+    // product (tensor cores, each kernel value evaluated once for b columns) and the b iterations
+    // then run the unchanged stage kernels on its columns — the same arithmetic as b sequential
+    // iterations up to summation order (iterative = projected update for the same S).
+    const bool blocked = blk > 1 && policy != CAKF_POLICY_CG && niter > 0;
+    if (blocked && cull) {
+      CK_CUDA(launch_k2_active(sph_o128, (N + 127) / 128, sph_o32, (N + 31) / 32, kCullCut, act_cnt_tt, act_list_tt,
+                               act_stride_po, nullptr, st));
+    }
+    T* Sblk = tmp;   // N x b actions   (post-loop scratch, free during the loop)
+    T* Yblk = Yb;    // N x b   K_TT S
     for (int i = 1; i <= niter; ++i) {
       // G s  (matrix-free: kernel rows on the fly + low-rank downdate + noise)
       const bool fork = side && rin > 0;
@@ -831,6 +849,24 @@ struct Impl final : ImplBase {
         CK_CUDA(cudaEventRecord(ev_join, st2));
       }
       size_t pk = prof_begin();
+      const T* kpart = partial;
+      int kch = nch;
+      if (policy == CAKF_POLICY_COORD) {
+        // K_TT e_j: the kernel columns of the chosen points (N evaluations each), b at a time
+        const int j = (i - 1) % blk;
+        if (j == 0) CK_CUDA(launch_kernel_columns<T>(nu2, xcs, N, order32, i, std::min(blk, niter - i + 1), Yblk, N, st));
+        kpart = Yblk + (size_t)j * N;
+        kch = 1;
+      } else if (blocked) {
+        const int j = (i - 1) % blk;
+        if (j == 0) {
+          const int nb = std::min(blk, niter - i + 1);
+          CK_CUDA(StepKernels<T>::gen_actions(N, i, nb, policy, order32, seed, k, sigma, Sblk, N, st));
+          CK(k2(xcs, N, xcs, N, Sblk, N, nb, Yblk, N, cull ? act_cnt_tt : nullptr, act_list_tt, act_stride_po));
+        }
+        kpart = Yblk + (size_t)j * N;
+        kch = 1;
+      } else {
       // multi-GPU: this rank evaluates its share of the kernel work (sym units / column chunks),
       // the rest of the partial buffer is zero, and the reduced vector is all-reduced
       if (world > 1) CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)nch * N * sizeof(T), st));
@@ -852,13 +888,12 @@ struct Impl final : ImplBase {
         CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st, nch * rank / world,
                                          nch * (rank + 1) / world));
       }
-      const T* kpart = partial;
-      int kch = nch;
       if (world > 1) {
         CK_CUDA(launch_sum_partials<T>(N, nch, partial, 1.0, yloc, st));
         CK_NCCL(ncclAllReduce(yloc, yred, (size_t)N, sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, ncclSum, comm, st));
         kpart = yred;
         kch = 1;
+      }
       }
       prof_end(CAKF_PROF_K1, pk);
       pk = prof_begin();

@@ -83,4 +83,9 @@ template <typename T>
 cudaError_t kd_obs_order(int N, const int* idx, const V4<T>* coords, int* sig_out, int* sig_inv, int* idx_out,
                          const int* sig_in_sorted, void* ws, size_t ws_bytes, cudaStream_t st);
 
+// columns k(X, x_{order[i0-1+c]}), c < nb, of the kernel matrix (coordinate actions)
+template <typename T>
+cudaError_t launch_kernel_columns(int nu2, const V4<T>* x, int N, const int* order, int i0, int nb, T* out, size_t ldo,
+                                  cudaStream_t st);
+
 }  // namespace cakf

@@ -234,6 +234,17 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
   }
 }
 
+// Coordinate actions: K_TT e_j is column j of the kernel matrix — N evaluations instead of N^2
+// (SURVEY §8a a4).  out[row + c*ldo] = k(x_row, x_{order[i0 - 1 + c]}) for c < nb.
+template <typename T, int NU2>
+__global__ void kernel_columns_kernel(const V4<T>* __restrict__ x, int N, const int* __restrict__ order, int i0, int nb,
+                                      T* __restrict__ out, size_t ldo) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N * nb) return;
+  const int row = (int)(e % N), c = (int)(e / N);
+  out[row + (size_t)c * ldo] = matern_from_d2<NU2>(dist2<T>(x[row], x[order[i0 - 1 + c]]));
+}
+
 // Bounding sphere (center, radius inflated for rounding) of each tile of `tile` consecutive points.
 __global__ void tile_spheres_kernel(const float4* __restrict__ x, int n, int tile, float4* __restrict__ out) {
   __shared__ double red[4][32];
@@ -425,6 +436,25 @@ cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, c
   tile_spheres_kernel<<<(n + tile - 1) / tile, 128, 0, st>>>(x, n, tile, out);
   return note_launch_err();
 }
+
+template <typename T>
+cudaError_t launch_kernel_columns(int nu2, const V4<T>* x, int N, const int* order, int i0, int nb, T* out, size_t ldo,
+                                  cudaStream_t st) {
+  const size_t n = (size_t)N * nb;
+  if (!n) return cudaSuccess;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  switch (nu2) {
+    case 1: kernel_columns_kernel<T, 1><<<g, 256, 0, st>>>(x, N, order, i0, nb, out, ldo); break;
+    case 3: kernel_columns_kernel<T, 3><<<g, 256, 0, st>>>(x, N, order, i0, nb, out, ldo); break;
+    case 5: kernel_columns_kernel<T, 5><<<g, 256, 0, st>>>(x, N, order, i0, nb, out, ldo); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return note_launch_err();
+}
+template cudaError_t launch_kernel_columns<float>(int, const V4<float>*, int, const int*, int, int, float*, size_t,
+                                                  cudaStream_t);
+template cudaError_t launch_kernel_columns<double>(int, const V4<double>*, int, const int*, int, int, double*, size_t,
+                                                   cudaStream_t);
 
 int matvec_sym_tiles(int n) { return ((n + SYM_T - 1) / SYM_T + SYM_S - 1) / SYM_S; }   // = partials per row
 

@@ -176,6 +176,21 @@ __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __r
   xcs[row] = c;
 }
 
+// actions s_{i0} .. s_{i0+nb-1} of a non-adaptive policy at once (block execution): the same
+// formulas as prep / stageD — coordinate e_{order[i-1]}, random Philox(seed; j = user position, i, k)
+template <typename T>
+__global__ void gen_actions_kernel(int N, int i0, int nb, int policy, const int* __restrict__ order, uint64_t seed,
+                                   int k, const int* __restrict__ sigma, T* __restrict__ S, size_t ldS) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N * nb) return;
+  const int row = (int)(e % N), j = (int)(e / N);
+  const int i = i0 + j;
+  T v;
+  if (policy == 1) v = (order[i - 1] == row) ? T(1) : T(0);
+  else v = (T)philox_normal(seed, (uint32_t)k, (uint32_t)i, (uint32_t)(sigma ? sigma[row] : row));
+  S[row + (size_t)j * ldS] = v;
+}
+
 // ------------------------------------------------------------------ stage A
 template <typename T>
 __global__ void __launch_bounds__(kTile)
@@ -695,6 +710,14 @@ cudaError_t StepKernels<T>::prep(int N, const int* idx, const V4<T>* coords, con
                                  cudaStream_t st) {
   if (N <= 0) return cudaSuccess;
   prep_kernel<T><<<nblk(N), 256, 0, st>>>(N, idx, coords, y, mpred, policy, order, seed, k, sigma, r, s, v, xcs);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::gen_actions(int N, int i0, int nb, int policy, const int* order, uint64_t seed, int k,
+                                        const int* sigma, T* S, size_t ldS, cudaStream_t st) {
+  if ((size_t)N * nb == 0) return cudaSuccess;
+  gen_actions_kernel<T><<<nblk((size_t)N * nb), 256, 0, st>>>(N, i0, nb, policy, order, seed, k, sigma, S, ldS);
   return note_launch_err();
 }
 

@@ -39,6 +39,8 @@ struct StepKernels {
   static cudaError_t stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s, const T* r,
                             T* gp, const T* HM, int rin, double* part, int W, double* red, unsigned* cnt,
                             cudaStream_t st);
+  static cudaError_t gen_actions(int N, int i0, int nb, int policy, const int* order, uint64_t seed, int k,
+                                 const int* sigma, T* S, size_t ldS, cudaStream_t st);
   // HM == nullptr in stageA: u = HM^T s is computed by hmts (side stream) into red[0, rin)
   static cudaError_t hmts(int N, const T* HM, int rin, const T* s, double* part, int W, double* red, unsigned* cnt,
                           cudaStream_t st);

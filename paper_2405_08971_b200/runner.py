@@ -35,7 +35,8 @@ def make_handle(problem, dtype="f32", stream=None, max_steps=None, rank=0, world
                 policy=problem.policy, max_iter=problem.max_iter, max_rank=problem.max_rank,
                 seed=problem.action_seed, max_steps=max_steps or problem.T, max_obs=max(max_obs, 1),
                 reorth=getattr(problem, "reorth", True), stream=stream, rank=rank, world=world, nccl_id=nccl_id,
-                cull_zero=cull_zero, keep_carriers=keep_carriers)
+                cull_zero=cull_zero, keep_carriers=keep_carriers,
+                block_actions=getattr(problem, "block_actions", 1))
 
 
 def stage_inputs(problem, dtype="f32", device="cuda"):

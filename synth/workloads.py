@@ -69,6 +69,7 @@ class Workload:
     action_seed: int = 1          # Philox key for the random policy (R16)
     rtol: float = 0.0
     reorth: bool = True           # second Gram-Schmidt pass (CGS2, reading R19)
+    block_actions: int = 1      # block execution of non-adaptive policies (b actions per K2 product)
 
     @property
     def n_space(self) -> int:

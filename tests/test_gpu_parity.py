@@ -234,3 +234,20 @@ def test_state_machine_errors():
         h.predict(*trans[0])
     with pytest.raises(binding.CakfError):
         h.update(np.array([0, 99], dtype=np.int64), np.zeros(2), np.ones(2))
+
+
+@pytest.mark.parametrize("policy,b", [("random", 4), ("random", 5), ("random", 16), ("coord", 8)])
+def test_block_actions_fp64(policy, b):
+    """Block execution of a non-adaptive policy (block_actions = b: one multi-RHS K2 for b
+    consecutive actions) is the sequential algorithm — same oracle, 1e-9."""
+    wl = make_workload("sphere48", policy=policy, max_iter=16, max_rank=24, T=4, block_actions=b)
+    if policy == "coord":
+        from synth.workloads import farthest_point_order
+        o = farthest_point_order(wl.coords[wl.obs_idx[0]], 16)
+        wl.coord_order = [o.copy() for _ in range(wl.T)]
+    compare(wl, "f64", 1e-9, 1e-9)
+
+
+def test_block_actions_fp32():
+    wl = make_workload("sphere48", policy="random", max_iter=16, max_rank=24, T=4, block_actions=8)
+    compare_fp32_cancellation(wl)
