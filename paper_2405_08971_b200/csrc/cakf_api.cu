@@ -493,7 +493,7 @@ struct Impl final : ImplBase {
     }
     ctl = carve<IterCtl>(Tmax + 1);
     rin_max = rcap >= 0 ? rcap : std::max(0, (Tmax - 1) * nhat);
-    qmax = rcap >= 0 ? rcap : Tmax * nhat;
+    qmax = rcap >= 0 ? std::max(rcap, nhat) : Tmax * nhat;   // W^s_T = W_T keeps n <= nhat columns (R6)
     cmax = std::max(rin_max + nhat, nhat + qmax);
     W = std::max(rin_max, nhat) + 8;
     xcs = carve<V4<T>>(Nmax);
