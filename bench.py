@@ -412,8 +412,8 @@ def main():
         q = {}
         for which, name in ((CAKF_FILTER, "filter"), (CAKF_SMOOTH, "smoother")):
             times_ms = []
-            for k in (wl.T // 4, wl.T // 2, (3 * wl.T) // 4):
-                dt = float(wl.dts[k])
+            for k in sorted({max(1, min(wl.T - 1, x)) for x in (wl.T // 4, wl.T // 2, (3 * wl.T) // 4)}):
+                dt = float(wl.dts[min(k, wl.T - 1)])
                 A1, Q1, _ = binding.matern_transition(wl.nu_t, wl.ell_t, wl.sigma, 0.5 * dt)
                 A2 = binding.matern_transition(wl.nu_t, wl.ell_t, wl.sigma, 0.5 * dt)[0]
                 q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
