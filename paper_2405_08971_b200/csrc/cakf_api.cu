@@ -295,6 +295,13 @@ struct Impl final : ImplBase {
   // per-update kd order of the observations (kd_order.cu); CAKF_NO_REORDER=1 keeps the sorted order
   bool kd_obs = [] { const char* e = getenv("CAKF_NO_REORDER"); return !(e && e[0] == '1'); }();
   int *idx_tmp = nullptr, *sig_tmp = nullptr;
+  // observation-order cache: an update whose obs_idx equals the previous one's reuses that order
+  // (idx, sigma, sigma_inv are a pure function of obs_idx; bit-identical to recomputing it)
+  int64_t obs_cache_n = -1;
+  std::vector<int64_t> obs_cache_h;    // host copy (host-pointer callers)
+  int64_t* obs_cache_d = nullptr;      // device copy (device-pointer callers)
+  int *idx_cache = nullptr, *sig_cache = nullptr, *siginv_cache = nullptr, *neq_d = nullptr;
+  int* neq_h = nullptr;                // pinned
   void* kd_ws = nullptr;
   size_t kd_ws_bytes = 0;
 
@@ -445,6 +452,7 @@ struct Impl final : ImplBase {
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (arena) cudaFree(arena);
     if (ctl_init_host) cudaFreeHost(ctl_init_host);
+    if (neq_h) cudaFreeHost(neq_h);
     if (comm) ncclCommDestroy(comm);
     if (blas) cublasDestroy(blas);
     if (sol) cusolverDnDestroy(sol);
@@ -564,6 +572,11 @@ struct Impl final : ImplBase {
     sig_st = carve<int>((size_t)(Tmax + 1) * Nmax);
     idx_tmp = carve<int>(Nmax);
     sig_tmp = carve<int>(Nmax);
+    obs_cache_d = carve<int64_t>(Nmax);
+    idx_cache = carve<int>(Nmax);
+    sig_cache = carve<int>(Nmax);
+    siginv_cache = carve<int>(Nmax);
+    neq_d = carve<int>(1);
     kd_ws_bytes = kd_obs_workspace((int)Nmax);
     kd_ws = carve<unsigned char>(kd_ws_bytes);
     ybuf_user = carve<T>(Nmax);
@@ -658,6 +671,7 @@ struct Impl final : ImplBase {
       CK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
     CK_CUDA(cudaMallocHost(&ctl_init_host, sizeof(IterCtl)));
+    if (!neq_h) CK_CUDA(cudaMallocHost(&neq_h, sizeof(int)));
     std::memset(ctl_init_host, 0, sizeof(IterCtl));
     ctl_init_host->eta_min = INFINITY;
     // coordinates: copy (host or device doubles) and prescale by sqrt(2 nu)/ell
@@ -784,11 +798,36 @@ struct Impl final : ImplBase {
     // ---- stage inputs (host or device pointers)
     // observations in internal point order: S.idx ascending, sigma[j] = the user's position
     CK_CUDA(cudaMemcpyAsync(stage64, obs_idx, (size_t)N * sizeof(int64_t), cudaMemcpyDefault, st));
-    if (kd_obs) {   // internal order, then the per-update kd order over the observed points
-      CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, sigma_inv, st));
-      CK_CUDA(kd_obs_order<T>(N, idx_tmp, coords, sigma, sigma_inv, S.idx, sig_tmp, kd_ws, kd_ws_bytes, st));
+    const bool obs_host = !is_device_ptr(obs_idx);
+    bool same_obs = false;
+    if (obs_cache_n == N) {   // same observation set as the cached update (ERA5-style fixed stations)
+      if (obs_host && obs_cache_h.size() == (size_t)N) {
+        same_obs = std::memcmp(obs_idx, obs_cache_h.data(), (size_t)N * sizeof(int64_t)) == 0;
+      } else {
+        CK_CUDA(obs_neq(N, stage64, obs_cache_d, neq_d, st));
+        CK_CUDA(cudaMemcpyAsync(neq_h, neq_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK_CUDA(cudaStreamSynchronize(st));
+        same_obs = *neq_h == 0;
+      }
+    }
+    if (same_obs) {
+      CK_CUDA(cudaMemcpyAsync(S.idx, idx_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(sigma, sig_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(sigma_inv, siginv_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
     } else {
-      CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, S.idx, sigma, sigma_inv, st));
+      if (kd_obs) {   // internal order, then the per-update kd order over the observed points
+        CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, sigma_inv, st));
+        CK_CUDA(kd_obs_order<T>(N, idx_tmp, coords, sigma, sigma_inv, S.idx, sig_tmp, kd_ws, kd_ws_bytes, st));
+      } else {
+        CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, S.idx, sigma, sigma_inv, st));
+      }
+      CK_CUDA(cudaMemcpyAsync(idx_cache, S.idx, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(sig_cache, sigma, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(siginv_cache, sigma_inv, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(obs_cache_d, stage64, (size_t)N * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      if (obs_host) obs_cache_h.assign(obs_idx, obs_idx + N);
+      else obs_cache_h.clear();
+      obs_cache_n = N;
     }
     CK_CUDA(cudaMemcpyAsync(ybuf_user, y, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
     CK_CUDA(cudaMemcpyAsync(lam2_user, noise_var, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
@@ -978,6 +1017,27 @@ struct Impl final : ImplBase {
     return gemm_impl(ta, tb, m, n, k, alpha, A, lda, B, nullptr, ldb, beta, C, ldc);
   }
 
+  // Lower triangle of the Gram Gm = F^T F (fp64 F, D x c, ld D; Gm ld c) — all the eigensolver reads
+  // (CUBLAS_FILL_MODE_LOWER).  On this shape (K = D >> c) cuBLAS DSYRK reaches ~12 TF/s and DGEMM ~36,
+  // so the lower triangle is three DGEMMs over a 2 x 2 column split: F0^T F0, F1^T F0, F1^T F1
+  // (3/4 of the full product's flops).  CAKF_GRAM_FULL=1: one full DGEMM.
+  int gram_lower(const double* Fd, int c) {
+    static const bool full = [] { const char* e = getenv("CAKF_GRAM_FULL"); return e && e[0] == '1'; }();
+    const double one = 1.0, zero = 0.0;
+    const int c0 = std::min(c, ((c + 1) / 2 + 31) / 32 * 32), c1 = c - c0;
+    if (full || c1 <= 0) {
+      CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c, c, (int)D, &one, Fd, (int)D, Fd, (int)D, &zero, Gm, c));
+      return CAKF_OK;
+    }
+    const double* F1 = Fd + (size_t)c0 * D;
+    CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c0, c0, (int)D, &one, Fd, (int)D, Fd, (int)D, &zero, Gm, c));
+    CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c1, c0, (int)D, &one, F1, (int)D, Fd, (int)D, &zero, Gm + c0,
+                        c));
+    CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c1, c1, (int)D, &one, F1, (int)D, F1, (int)D, &zero,
+                        Gm + c0 + (size_t)c0 * c, c));
+    return CAKF_OK;
+  }
+
   // fp32 truncation on tcgen05: Gram F^T F (3xBF16, K split, fp64 reduction) -> fp64 eig -> F Q_r
   int truncate_factor_tc(const float* F, int c, int rkeep, float* out, double* kept, double* dropped, size_t pk) {
     size_t ps = prof_begin();
@@ -988,8 +1048,7 @@ struct Impl final : ImplBase {
     } else {   // the Gram decides the kept subspace: fp32 products, fp64 accumulation (DGEMM)
       if ((size_t)D * c > dscr) return fail(CAKF_E_ARG, "truncate: fp64 scratch too small");
       CK_CUDA((convert<float, double>)((int)D, c, F, D, dA, D, st));
-      const double one = 1.0, zero = 0.0;
-      CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c, c, (int)D, &one, dA, (int)D, dA, (int)D, &zero, Gm, c));
+      CK(gram_lower(dA, c));
     }
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
@@ -1022,8 +1081,7 @@ struct Impl final : ImplBase {
     }
     const double one = 1.0, zero = 0.0;
     size_t ps = prof_begin();
-    // full Gram through DGEMM: on this shape (K = D >> c) cuBLAS DSYRK reaches ~12 TF/s, DGEMM ~36
-    CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c, c, (int)D, &one, Fd, (int)D, Fd, (int)D, &zero, Gm, c));
+    CK(gram_lower(Fd, c));
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
     CK_SOLVER(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, c, Gm, c, eigw, work, lwork, info));

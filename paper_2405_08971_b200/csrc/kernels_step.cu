@@ -927,6 +927,19 @@ cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int*
   return note_launch_err();
 }
 
+// obs_equal: neq_out = 1 if a[0:n] != b[0:n] (the observation-order cache of cakf_update)
+__global__ void obs_neq_kernel(int n, const int64_t* __restrict__ a, const int64_t* __restrict__ b,
+                               int* __restrict__ neq) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n && a[j] != b[j]) *neq = 1;
+}
+cudaError_t obs_neq(int n, const int64_t* a, const int64_t* b, int* neq, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(neq, 0, sizeof(int), st);
+  if (e != cudaSuccess || n <= 0) return e;
+  obs_neq_kernel<<<nblk(n), 256, 0, st>>>(n, a, b, neq);
+  return note_launch_err();
+}
+
 template <typename T>
 cudaError_t gather_vec(int N, const int* sigma, const T* in, T* out, cudaStream_t st) {
   if (N <= 0) return cudaSuccess;

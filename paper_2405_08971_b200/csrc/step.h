@@ -23,6 +23,8 @@ cudaError_t idx64_to32(int n, const int64_t* in, int* out, cudaStream_t st);
 // observations -> internal point order: idx_out ascending, sigma[j] = user position, sigma_inv inverse
 cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int* posof, int* counts, int* idx_out,
                      int* sigma, int* sigma_inv, cudaStream_t st);
+// *neq = (a[0:n] != b[0:n]) (device buffers)
+cudaError_t obs_neq(int n, const int64_t* a, const int64_t* b, int* neq, cudaStream_t st);
 template <typename T>
 cudaError_t gather_vec(int N, const int* sigma, const T* in, T* out, cudaStream_t st);
 cudaError_t map_order(int n, const int64_t* order_user, const int* sigma_inv, int* order_out, cudaStream_t st);
