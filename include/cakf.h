@@ -283,6 +283,18 @@ int cakf_gram_matmul(int32_t dtype, int32_t spatial_kernel, double ell, int32_t 
                      int64_t n_rows, const void* xr, int64_t n_cols, const void* xc,
                      int32_t n_rhs, const void* X, double alpha, void* Y, void* stream);
 
+/* Standalone low-rank contraction of the fp32 path (a7 post-loop P:1532-1541, a8 truncation Gram
+ * and M Q_r Sec. 3.2, a9 smoother products alg:mfks P:388-409):
+ *   C = alpha * op(A) op(B) + beta * C,   op(X) = X (trans = 0) or X^T (trans = 1),
+ * A, B, C fp32, column-major (BLAS convention: op(A) m x k, op(B) k x n, C m x n, leading
+ * dimensions lda / ldb / ldc), device pointers.  Computed on the INT8 tensor cores with exact
+ * slice products and fp64 sums (kernels_gemm_i8.cu): the result equals the fp64 product of
+ * the fp32 inputs to ~2^-33 relative to sum_k |a||b| per chunk maximum.  k >= 1.
+ * Workspaces are allocated on `stream` (may be NULL) and freed before return; synchronises. */
+int cakf_lowrank_gemm(int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k, double alpha,
+                      const float* A, int64_t lda, const float* B, int64_t ldb, double beta, float* C,
+                      int64_t ldc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,7 @@ EXPORTS = [
     "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
     "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats", "cakf_interpolate", "cakf_sample",
+    "cakf_lowrank_gemm",
 ]
 PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank", "trunc_gram",
                    "trunc_eig", "trunc_gemm"]
@@ -91,6 +92,7 @@ def load(path: str = LIB_PATH):
     lib.cakf_last_error.restype = ctypes.c_char_p
     lib.cakf_matern_transition.argtypes = [i32, f64, f64, f64, vp, vp, vp]
     lib.cakf_gram_matmul.argtypes = [i32, i32, f64, i32, i64, vp, i64, vp, i32, vp, f64, vp, vp]
+    lib.cakf_lowrank_gemm.argtypes = [i32, i32, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64, vp]
     lib.cakf_profile.argtypes = [vp, i32]
     lib.cakf_profile_read.argtypes = [vp, vp, vp, i32]
     lib.cakf_kernel_launches.restype = ctypes.c_int64
@@ -178,6 +180,25 @@ def gram_matmul(xr, xc, X, nu: float, ell: float, alpha: float = 1.0, out=None, 
                                 Y.data_ptr(), stream))
     Y = Y.t()
     return Y[:, 0] if X.dim() == 1 else Y
+
+
+def lowrank_gemm(A, B, transa=False, transb=False, alpha=1.0, beta=0.0, C=None, stream=None):
+    """alpha op(A) @ op(B) + beta C for fp32 CUDA tensors (fp64-accurate, INT8 tensor cores).
+
+    torch tensors are row-major; a row-major (r, c) tensor is the column-major (c, r) matrix, so
+    the call computes C^T = op(B)^T op(A)^T in the library's column-major convention."""
+    import torch
+    lib = load()
+    Am, Bm = A.contiguous(), B.contiguous()
+    m = Am.shape[1] if transa else Am.shape[0]
+    k = Am.shape[0] if transa else Am.shape[1]
+    n = Bm.shape[0] if transb else Bm.shape[1]
+    out = torch.zeros((m, n), dtype=torch.float32, device=A.device) if C is None else C
+    assert out.is_contiguous() and out.shape == (m, n) and out.dtype == torch.float32
+    _check(lib.cakf_lowrank_gemm(1 if transb else 0, 1 if transa else 0, n, m, k, float(alpha),
+                                 Bm.data_ptr(), Bm.shape[1], Am.data_ptr(), Am.shape[1], float(beta),
+                                 out.data_ptr(), n, stream))
+    return out
 
 
 class Cakf:

@@ -265,6 +265,13 @@ struct Impl final : ImplBase {
   uint16_t *gpA = nullptr, *gpB = nullptr;
   size_t gp_elems = 0;
   float *gwork = nullptr, *Qf = nullptr;
+  int *gexA = nullptr, *gexB = nullptr;   // INT8-slice GEMM: per-(row, K chunk) exponents
+  // contractions with K >= i8_min_k (the D- and N-long reductions: truncation Gram, M^T x, (HM)^T [v V])
+  // run on the INT8-slice GEMM, the short-K ones through DGEMM: measured in the bench, the INT8 kernel
+  // does not win on D x 513 x 512 in place (scripts/gemm_i8_bench.py); CAKF_I8_MIN_K overrides
+  int i8_min_k = [] { const char* e = getenv("CAKF_I8_MIN_K"); return e ? std::atoi(e) : 8192; }();
+  bool i8_mqr = [] { const char* e = getenv("CAKF_I8_MQR"); return e && e[0] == '1'; }();
+  size_t gex_elems = 0;
 
   // ---------------- exact-zero culling (fp32 only): tile bounding spheres and, per 128-row
   // output tile of K2, the ascending list of 32-column K-blocks not entirely below the fp32 underflow
@@ -599,6 +606,9 @@ struct Impl final : ImplBase {
       gpA = carve<uint16_t>(gp_elems);
       gpB = carve<uint16_t>(gp_elems);
       gwork = carve<float>(kGemmWorkFloats);
+      gex_elems = (size_t)std::max<int64_t>({D, Nmax, (int64_t)cmax}) + gp_elems / 4096 + 1024;
+      gexA = carve<int>(gex_elems);
+      gexB = carve<int>(gex_elems);
       if (rcap >= 0) Qf = carve<float>((size_t)cmax * std::max(rcap, 1));
     }
     if (cull) {
@@ -980,6 +990,9 @@ struct Impl final : ImplBase {
       const double* Bp = Bd ? Bd : reinterpret_cast<const double*>(B);
       CK_BLAS(cublasDgemm(blas, ta, tb, m, n, k, &alpha, reinterpret_cast<const double*>(A), lda, Bp, ldb, &beta,
                           reinterpret_cast<double*>(C), ldc));
+    } else if (!lowrank_tc && !Bd && k >= i8_min_k && use_i8_gemm()) {
+      CK(gemm_i8_f32(ta, tb, m, n, k, alpha, reinterpret_cast<const float*>(A), lda,
+                     reinterpret_cast<const float*>(B), ldb, beta, reinterpret_cast<float*>(C), nullptr, ldc));
     } else if (lowrank_tc) {
       // tcgen05 3xBF16 (kernels_gemm_tc.cu): op(A) rows m and op(B)^T rows n as K-major planes
       if (Bd) return fail(CAKF_E_ARG, "gemm: fp64 right operand on the tensor-core path");
@@ -1012,6 +1025,28 @@ struct Impl final : ImplBase {
     }
     return CAKF_OK;
   }
+  // fp32 operands, fp64-accurate product on the INT8 tensor cores (kernels_gemm_i8.cu): op(A) rows m and
+  // op(B)^T rows n sliced into K-major planes; fp32 C or fp64 Cd; lower: only n <= m needed (Gram);
+  // Bq (nullable) replaces B by an fp64 operand with the same layout
+  int gemm_i8_f32(cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, double alpha, const float* A,
+                  int lda, const float* B, int ldb, double beta, float* C, double* Cd, int ldc, bool lower = false,
+                  const double* Bq = nullptr) {
+    const size_t cap = gp_elems * 2;
+    const size_t nch = (size_t)gemm_i8_nchunk(k);
+    if (gemm_i8_plane_bytes(m, k) > cap || gemm_i8_plane_bytes(n, k) > cap || (size_t)m * nch > gex_elems ||
+        (size_t)n * nch > gex_elems)
+      return fail(CAKF_E_ARG, "gemm: INT8 slice planes too small");
+    int8_t* pa = reinterpret_cast<int8_t*>(gpA);
+    int8_t* pb = reinterpret_cast<int8_t*>(gpB);
+    CK_CUDA(gemm_i8_split<float>(A, m, k, (size_t)lda, ta == CUBLAS_OP_T, pa, gexA, st));
+    const bool same = B == A && tb != ta && ldb == lda && m == n && !Bq;   // A^T A: one set of planes
+    if (Bq) CK_CUDA(gemm_i8_split<double>(Bq, n, k, (size_t)ldb, tb == CUBLAS_OP_N, pb, gexB, st));
+    else if (!same) CK_CUDA(gemm_i8_split<float>(B, n, k, (size_t)ldb, tb == CUBLAS_OP_N, pb, gexB, st));
+    CK_CUDA(gemm_i8_run(pa, gexA, m, same ? pa : pb, same ? gexA : gexB, n, k, alpha, beta, C, Cd, (size_t)ldc,
+                        lower, reinterpret_cast<double*>(gwork), kGemmWorkFloats / 2, st));
+    return CAKF_OK;
+  }
+
   int gemm(cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, double alpha, const T* A, int lda,
            const T* B, int ldb, double beta, T* C, int ldc) {
     return gemm_impl(ta, tb, m, n, k, alpha, A, lda, B, nullptr, ldb, beta, C, ldc);
@@ -1042,9 +1077,12 @@ struct Impl final : ImplBase {
   int truncate_factor_tc(const float* F, int c, int rkeep, float* out, double* kept, double* dropped, size_t pk) {
     size_t ps = prof_begin();
     if (gemm_tc_plane_bytes((int)D, c) > gp_elems * 2) return fail(CAKF_E_ARG, "truncate: operand planes too small");
+    const bool i8 = use_i8_gemm();
     if (gram_tc) {
       CK_CUDA(gemm_tc_split(F, c, (int)D, (size_t)D, true, gpA, st));          // F^T rows (K = D contiguous)
       CK_CUDA(gemm_tc_run(gpA, c, gpA, c, (int)D, 1.0, 0.0, nullptr, Gm, (size_t)c, gwork, kGemmWorkFloats, st));
+    } else if (i8) {   // exact products, fp64 sums: lower triangle of F^T F on the INT8 tensor cores
+      CK(gemm_i8_f32(CUBLAS_OP_T, CUBLAS_OP_N, c, c, (int)D, 1.0, F, (int)D, F, (int)D, 0.0, nullptr, Gm, c, true));
     } else {   // the Gram decides the kept subspace: fp32 products, fp64 accumulation (DGEMM)
       if ((size_t)D * c > dscr) return fail(CAKF_E_ARG, "truncate: fp64 scratch too small");
       CK_CUDA((convert<float, double>)((int)D, c, F, D, dA, D, st));
@@ -1056,10 +1094,16 @@ struct Impl final : ImplBase {
     CK_CUDA(StepKernels<double>::take_top(c, rkeep, Gm, eigw, QrD, kept, dropped, st));
     prof_end(CAKF_PROF_TRUNC_EIG, ps);
     ps = prof_begin();
-    CK_CUDA((convert<double, float>)(c, rkeep, QrD, c, Qf, c, st));
-    CK_CUDA(gemm_tc_split(F, (int)D, c, (size_t)D, false, gpA, st));           // F rows (K = c, transposed)
-    CK_CUDA(gemm_tc_split(Qf, rkeep, c, (size_t)c, true, gpB, st));           // Q_r columns
-    CK_CUDA(gemm_tc_run(gpA, (int)D, gpB, rkeep, c, 1.0, 0.0, out, nullptr, (size_t)D, gwork, kGemmWorkFloats, st));
+    if (i8 && i8_mqr) {   // M~ = F Q_r with the fp64 eigenvectors sliced directly
+      CK(gemm_i8_f32(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, c, 0.0, out, nullptr,
+                     (int)D, false, QrD));
+    } else {
+      CK_CUDA((convert<double, float>)(c, rkeep, QrD, c, Qf, c, st));
+      CK_CUDA(gemm_tc_split(F, (int)D, c, (size_t)D, false, gpA, st));           // F rows (K = c, transposed)
+      CK_CUDA(gemm_tc_split(Qf, rkeep, c, (size_t)c, true, gpB, st));           // Q_r columns
+      CK_CUDA(gemm_tc_run(gpA, (int)D, gpB, rkeep, c, 1.0, 0.0, out, nullptr, (size_t)D, gwork, kGemmWorkFloats,
+                          st));
+    }
     prof_end(CAKF_PROF_TRUNC_GEMM, ps);
     prof_end(CAKF_PROF_TRUNCATE, pk);
     return CAKF_OK;
@@ -1727,6 +1771,47 @@ int cakf_gram_matmul(int32_t dtype, int32_t spatial_kernel, double ell, int32_t 
   if (dtype == CAKF_F32) return run(float{});
   if (dtype == CAKF_F64) return run(double{});
   return fail(CAKF_E_ARG, "cakf_gram_matmul: bad dtype");
+}
+
+int cakf_lowrank_gemm(int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
+                      int64_t lda, const float* B, int64_t ldb, double beta, float* C, int64_t ldc, void* stream) {
+  if (!A || !B || !C || m < 0 || n < 0 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX ||
+      (transa != 0 && transa != 1) || (transb != 0 && transb != 1) || ldc < std::max<int64_t>(m, 1) ||
+      lda < std::max<int64_t>(transa ? k : m, 1) || ldb < std::max<int64_t>(transb ? n : k, 1))
+    return fail(CAKF_E_ARG, "cakf_lowrank_gemm: bad argument");
+  if (m == 0 || n == 0) return CAKF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  static bool pool_kept = [] {   // keep the stream-ordered pool's memory between calls (repeated calls)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    return true;
+  }();
+  (void)pool_kept;
+  int8_t *pa = nullptr, *pb = nullptr;
+  int *ea = nullptr, *eb = nullptr;
+  double* work = nullptr;
+  const size_t nch = (size_t)gemm_i8_nchunk((int)k);
+  const size_t work_doubles = (size_t)m * n * nch;
+  cudaError_t e = cudaMallocAsync(&pa, gemm_i8_plane_bytes((int)m, (int)k), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&pb, gemm_i8_plane_bytes((int)n, (int)k), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&ea, (size_t)m * nch * sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&eb, (size_t)n * nch * sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&work, work_doubles * sizeof(double), st);
+  if (e == cudaSuccess) e = gemm_i8_split<float>(A, (int)m, (int)k, (size_t)lda, transa == 1, pa, ea, st);
+  if (e == cudaSuccess) e = gemm_i8_split<float>(B, (int)n, (int)k, (size_t)ldb, transb == 0, pb, eb, st);
+  if (e == cudaSuccess)
+    e = gemm_i8_run(pa, ea, (int)m, pb, eb, (int)n, (int)k, alpha, beta, C, nullptr, (size_t)ldc, false, work,
+                    work_doubles, st);
+  for (void* p : {(void*)pa, (void*)pb, (void*)ea, (void*)eb, (void*)work})
+    if (p) cudaFreeAsync(p, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return fail(CAKF_E_CUDA, std::string("cakf_lowrank_gemm: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+  return CAKF_OK;
 }
 
 }  // extern "C"

@@ -75,6 +75,23 @@ cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, in
 bool use_tc_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM instead
 constexpr size_t kGemmWorkFloats = (size_t)32 << 20;
 
+// ---- fp64-accurate contractions of fp32 factors on the INT8 tensor cores (kernels_gemm_i8.cu, Ozaki
+// splitting into 7-bit slices with per-(row, K chunk) power-of-two scales; exact int32 accumulation)
+int gemm_i8_kp(int K);                              // padded K of the planes (multiple of 16)
+int gemm_i8_nchunk(int K);                          // K chunks (one exponent per row and chunk)
+size_t gemm_i8_plane_bytes(int rows, int K);        // bytes of the slice planes of a rows x K operand
+// planes[S][R][Kp] + exponents ex[R][nchunk] of the R x K operand (r, k) = src[k + r ld] (k_contig) or src[r + k ld]
+template <typename Src>
+cudaError_t gemm_i8_split(const Src* src, int R, int K, size_t ld, bool k_contig, int8_t* planes, int* ex,
+                          cudaStream_t st);
+// C (M x N, column-major ldc) = alpha sum_k A(m, k) B(n, k) + beta C from the planes of both operands;
+// output fp32 C or fp64 Cd (exactly one non-null); lower: only n <= m is required (symmetric Gram);
+// K splits accumulate in fp64 through work (doubles), reduced in a fixed order
+cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* Bp, const int* expB, int N, int K,
+                        double alpha, double beta, float* C, double* Cd, size_t ldc, bool lower, double* work,
+                        size_t work_doubles, cudaStream_t st);
+bool use_i8_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM instead
+
 // ---- per-update kd-tree order of the observed points (kd_order.cu)
 size_t kd_obs_workspace(int Nmax);
 // idx/sig_in_sorted: the observations in internal point order (obs_sort); writes idx_out, sig_out
