@@ -924,10 +924,10 @@ struct Impl final : ImplBase {
           const long long U = matvec_sym_units(N);
           CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
                                     U * rank / world, U * (rank + 1) / world, st, cull ? cull_ctr : nullptr,
-                                    cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128, kCullCut));
+                                    cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128, sph_o32, kCullCut));
           if (cull) {
             const double nt = (double)((N + 127) / 128);
-            k1_pairs_dense += 8.0 * nt * (nt + 1) / 2 / world;   // in 16 x 128 warp blocks
+            k1_pairs_dense += (double)matvec_sym_blocks_per_tile_pair() * nt * (nt + 1) / 2 / world;   // warp blocks
           }
         } else {
           CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st, nch * rank / world,

@@ -23,10 +23,14 @@ int matvec_sym_block_points();       // points per tile block of the symmetric K
 // only the tile pairs set in umask[w] (bit a*4+b), and in those only the warps whose 16-row group sphere
 // (sph16) is within cut of the J tile sphere (sph128); the skipped units' partial slots must hold zeros.
 // done_pairs (nullable) accumulates the evaluated 128 x 128 tile pairs.
+// With the 32-column sub-tile test (default; CAKF_K1_SUB=0 for the 128-column one) the warp test uses
+// sph32 (32-point spheres of the observations) and done_pairs counts 16 x 32 blocks.
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
                               cudaStream_t st, unsigned long long* done_pairs = nullptr, const int* ulist = nullptr,
                               const int* ucount = nullptr, const unsigned short* umask = nullptr,
-                              const float4* sph16 = nullptr, const float4* sph128 = nullptr, float cut = 0.f);
+                              const float4* sph16 = nullptr, const float4* sph128 = nullptr,
+                              const float4* sph32 = nullptr, float cut = 0.f);
+int matvec_sym_blocks_per_tile_pair();   // warp blocks per 128 x 128 tile pair counted by done_pairs
 // compact ascending list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
                                    unsigned short* mask, int* count, cudaStream_t st);

@@ -91,15 +91,19 @@ __device__ __forceinline__ void sym_unit_decode(long long u, int nb, int& bi, in
   bj = bi + (int)(u - ((long long)bi * nb - (long long)bi * (bi - 1) / 2));
 }
 
-template <int NU2>
+// SUB: the exact-zero test and the work run per 16-row group x 32-column sub-tile (sphJ = 32-point
+// spheres; each lane owns one packed column pair of the sub-tile), else per 16-row group x 128-column
+// J tile (sphJ = 128-point spheres; each lane owns 8 columns).  Row -> lane mapping is the same.
+template <int NU2, bool SUB>
 __global__ void __launch_bounds__(256, 3)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
                   float* __restrict__ partial,
                   unsigned long long* __restrict__ done_pairs, const int* __restrict__ ulist,
                   const int* __restrict__ ucount, const unsigned short* __restrict__ umask,
-                  const float4* __restrict__ sph16, const float4* __restrict__ sph128, float cut) {
+                  const float4* __restrict__ sph16, const float4* __restrict__ sphJ, float cut) {
+  constexpr int NJS = SUB ? SYM_S * 4 : SYM_S;   // J spheres per unit
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  __shared__ float4 s16[SYM_S * 8], s128[SYM_S];   // this unit's 16-row group / J tile spheres
+  __shared__ float4 s16[SYM_S * 8], s128[NJS];   // this unit's 16-row group / J (sub-)tile spheres
   __shared__ unsigned s_done;                        // evaluated 16 x 128 warp blocks of this unit
   float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
   float4* tJ = tI + SYM_S * SYM_T;                                    // [SYM_S][128]
@@ -145,9 +149,9 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
       if (tid < SYM_S * 8) {
         const int g = bi * SYM_S * 8 + tid;
         s16[tid] = g < (n + 15) / 16 ? sph16[g] : make_float4(0.f, 0.f, 0.f, 0.f);
-      } else if (tid < SYM_S * 8 + SYM_S) {
-        const int t = bj * SYM_S + tid - SYM_S * 8;
-        s128[tid - SYM_S * 8] = t < nt ? sph128[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if (tid < SYM_S * 8 + NJS) {
+        const int t = bj * NJS + tid - SYM_S * 8;
+        s128[tid - SYM_S * 8] = t < (SUB ? (n + 31) / 32 : nt) ? sphJ[t] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
     __syncthreads();
@@ -165,13 +169,93 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
       for (int q = 0; q < 8; ++q) racc2[q] = make_float2(0.f, 0.f);
       for (int b = diag ? a : 0; b < nbj; ++b) {
         if (!((amask >> (a * SYM_S + b)) & 1u)) continue;   // every value of this tile pair is exactly 0
+        const bool offdiag = !(diag && a == b);
+        if constexpr (SUB) {
+          // 4 sub-tiles of 32 columns; lane tx owns the packed column pairs q4*32 + 2tx, +1 (q4 < 4).
+          // act: sub-tiles of this warp's 16 rows with a possibly nonzero value (warp-uniform).  A fully
+          // active J tile runs all four pairs at once; otherwise the active sub-tiles run one by one in
+          // the same order, so every accumulator sees the same operation sequence (skipped = exact zeros).
+          unsigned act = 0u;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const bool live = bj * SYM_S * SYM_T + b * SYM_T + q4 * 32 < n;   // beyond: only padding
+            bool on = live;
+            if (ulist && live) {
+              const float4 A = s16[a * 8 + (tid >> 5)], B = s128[b * 4 + q4];
+              const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
+              on = sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w <= cut;
+            }
+            act |= on ? (1u << q4) : 0u;
+          }
+          if (!act) continue;
+          if (ulist && (tid & 31) == 0) atomicAdd(&s_done, (unsigned)__popc(act));
+          if (act == 0xFu) {
+            float2 cx2[4], cy2[4], cz2[4], cs2[4], cacc2[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 P = sJ[(b * SYM_T / 2 + q * 16 + tx) * 2], Q = sJ[(b * SYM_T / 2 + q * 16 + tx) * 2 + 1];
+              cx2[q] = make_float2(P.x, P.y); cy2[q] = make_float2(P.z, P.w);
+              cz2[q] = make_float2(Q.x, Q.y); cs2[q] = make_float2(Q.z, Q.w);
+              cacc2[q] = make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 dx = __fadd2_rn(cx2[q], make_float2(nrx[r], nrx[r]));
+                const float2 dy = __fadd2_rn(cy2[q], make_float2(nry[r], nry[r]));
+                const float2 dz = __fadd2_rn(cz2[q], make_float2(nrz[r], nrz[r]));
+                const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+                const float2 k = matern2_from_d2<NU2>(d2);
+                racc2[r] = __ffma2_rn(k, cs2[q], racc2[r]);
+                cacc2[q] = __ffma2_rn(k, make_float2(rs[r], rs[r]), cacc2[q]);
+              }
+            }
+            if (offdiag) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float2* m2 = reinterpret_cast<float2*>(colp + ty * SYM_S * SYM_T + b * SYM_T + q * 32 + 2 * tx);
+                float2 u = *m2;
+                u.x += cacc2[q].x;
+                u.y += cacc2[q].y;
+                *m2 = u;
+              }
+            }
+            continue;
+          }
+#pragma unroll 1
+          for (int q4 = 0; q4 < 4; ++q4) {
+            if (!((act >> q4) & 1u)) continue;
+            const float4 P = sJ[(b * SYM_T / 2 + q4 * 16 + tx) * 2], Q = sJ[(b * SYM_T / 2 + q4 * 16 + tx) * 2 + 1];
+            const float2 cx2 = make_float2(P.x, P.y), cy2 = make_float2(P.z, P.w);
+            const float2 cz2 = make_float2(Q.x, Q.y), cs2 = make_float2(Q.z, Q.w);
+            float2 cacc2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const float2 dx = __fadd2_rn(cx2, make_float2(nrx[r], nrx[r]));
+              const float2 dy = __fadd2_rn(cy2, make_float2(nry[r], nry[r]));
+              const float2 dz = __fadd2_rn(cz2, make_float2(nrz[r], nrz[r]));
+              const float2 d2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+              const float2 k = matern2_from_d2<NU2>(d2);
+              racc2[r] = __ffma2_rn(k, cs2, racc2[r]);
+              cacc2 = __ffma2_rn(k, make_float2(rs[r], rs[r]), cacc2);
+            }
+            if (offdiag) {   // column sums into this thread's private slots (no barrier)
+              float2* m2 = reinterpret_cast<float2*>(colp + ty * SYM_S * SYM_T + b * SYM_T + q4 * 32 + 2 * tx);
+              float2 u = *m2;
+              u.x += cacc2.x;
+              u.y += cacc2.y;
+              *m2 = u;
+            }
+          }
+          continue;
+        }
         if (ulist) {   // same test for this warp's 16 rows against the J tile (warp-uniform)
           const float4 A = s16[a * 8 + (tid >> 5)], B = s128[b];
           const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
           if (sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut) continue;
           if ((tid & 31) == 0) atomicAdd(&s_done, 1u);
         }
-        const bool offdiag = !(diag && a == b);
         // 8 columns as 4 packed pairs: every elementwise op below is one FADD2 / FMUL2 / FFMA2 for two
         // pairs, leaving the two MUFU ops per pair (sqrt, ex2) as the only scalar work
         float2 cx2[4], cy2[4], cz2[4], cs2[4], cacc2[4];
@@ -532,45 +616,65 @@ cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, lon
   return note_launch_err();
 }
 
-cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
-                              cudaStream_t st, unsigned long long* done_pairs, const int* ulist,
-                              const int* ucount, const unsigned short* umask, const float4* sph16,
-                              const float4* sph128, float cut) {
-  if (n <= 0 || u_end <= u_begin) return cudaSuccess;
-  const int nt = (n + SYM_T - 1) / SYM_T;
-  const int nb = (nt + SYM_S - 1) / SYM_S;
+bool use_k1_sub() {   // CAKF_K1_SUB=0: exact-zero test per 128-column J tile instead of per 32-column sub-tile
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAKF_K1_SUB");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int NU2, bool SUB>
+cudaError_t launch_sym_t(const float4* x, int n, int nt, int nb, float* partial, long long u_begin, long long u_end,
+                         cudaStream_t st, unsigned long long* done_pairs, const int* ulist, const int* ucount,
+                         const unsigned short* umask, const float4* sph16, const float4* sphJ, float cut) {
   static int per_sm = 0;   // resident CTAs per SM (one full wave; the units are strided over it)
   const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)SYM_S * SYM_T * sizeof(float) +
                       (size_t)16 * SYM_S * SYM_T * sizeof(float);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(matvec_sym_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(matvec_sym_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(matvec_sym_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(matvec_sym_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(matvec_sym_kernel<3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(matvec_sym_kernel<5>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, matvec_sym_kernel<3>, 256, smem) != cudaSuccess ||
+    cudaFuncSetAttribute(matvec_sym_kernel<NU2, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(matvec_sym_kernel<NU2, SUB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, matvec_sym_kernel<NU2, SUB>, 256, smem) !=
+            cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
     if (const char* e = getenv("CAKF_K1_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
     configured = true;
   }
   const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);
-  switch (nu2) {
-    case 1: matvec_sym_kernel<1><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
-                                                                         done_pairs, ulist, ucount, umask, sph16,
-                                                                         sph128, cut); break;
-    case 3: matvec_sym_kernel<3><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
-                                                                         done_pairs, ulist, ucount, umask, sph16,
-                                                                         sph128, cut); break;
-    case 5: matvec_sym_kernel<5><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial,
-                                                                         done_pairs, ulist, ucount, umask, sph16,
-                                                                         sph128, cut); break;
-    default: return cudaErrorInvalidValue;
-  }
+  matvec_sym_kernel<NU2, SUB><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, done_pairs,
+                                                                  ulist, ucount, umask, sph16, sphJ, cut);
   return note_launch_err();
 }
+
+cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
+                              cudaStream_t st, unsigned long long* done_pairs, const int* ulist,
+                              const int* ucount, const unsigned short* umask, const float4* sph16,
+                              const float4* sph128, const float4* sph32, float cut) {
+  if (n <= 0 || u_end <= u_begin) return cudaSuccess;
+  const int nt = (n + SYM_T - 1) / SYM_T;
+  const int nb = (nt + SYM_S - 1) / SYM_S;
+  const bool sub = use_k1_sub();
+  if (ulist && sub && !sph32) return cudaErrorInvalidValue;
+  switch (nu2) {
+#define CAKF_SYM_CASE(NU)                                                                                           \
+  case NU:                                                                                                         \
+    return sub ? launch_sym_t<NU, true>(x, n, nt, nb, partial, u_begin, u_end, st, done_pairs, ulist, ucount,    \
+                                        umask, sph16, sph32, cut)                                                 \
+               : launch_sym_t<NU, false>(x, n, nt, nb, partial, u_begin, u_end, st, done_pairs, ulist, ucount,   \
+                                         umask, sph16, sph128, cut);
+    CAKF_SYM_CASE(1)
+    CAKF_SYM_CASE(3)
+    CAKF_SYM_CASE(5)
+#undef CAKF_SYM_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// dense-equivalent work units counted by done_pairs per 128 x 128 tile pair
+int matvec_sym_blocks_per_tile_pair() { return use_k1_sub() ? 32 : 8; }
 
 template <typename T>
 cudaError_t launch_sum_partials(int nrows, int nchunks, const T* partial, double alpha, T* y, cudaStream_t st) {
