@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcakf.so")
+LIB_PATH = os.environ.get("CAKF_LIB") or os.path.join(HERE, "libcakf.so")   # CAKF_LIB: experiment builds
 
 CAKF_F32, CAKF_F64 = 0, 1
 CAKF_MATERN12, CAKF_MATERN32, CAKF_MATERN52 = 1, 3, 5

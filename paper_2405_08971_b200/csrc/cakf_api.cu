@@ -209,6 +209,7 @@ struct Impl final : ImplBase {
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* part2 = nullptr;
+  double* hmw = nullptr;   // HM u (fp64 rows), formed on the side stream
   bool side = [] { const char* e = getenv("CAKF_NO_SIDE_STREAM"); return !(e && e[0] == '1'); }();
   cublasHandle_t blas = nullptr;
   cusolverDnHandle_t sol = nullptr;
@@ -266,10 +267,10 @@ struct Impl final : ImplBase {
   size_t gp_elems = 0;
   float *gwork = nullptr, *Qf = nullptr;
   int *gexA = nullptr, *gexB = nullptr;   // INT8-slice GEMM: per-(row, K chunk) exponents
-  // contractions with K >= i8_min_k (the D- and N-long reductions: truncation Gram, M^T x, (HM)^T [v V])
-  // run on the INT8-slice GEMM, the short-K ones through DGEMM: measured in the bench, the INT8 kernel
-  // does not win on D x 513 x 512 in place (scripts/gemm_i8_bench.py); CAKF_I8_MIN_K overrides
-  int i8_min_k = [] { const char* e = getenv("CAKF_I8_MIN_K"); return e ? std::atoi(e) : 8192; }();
+  // contractions with K >= i8_min_k (the D- and N-long reductions: truncation Gram, M^T x, (HM)^T [v V],
+  // and the K = r products M (M^T x), M U) run on the INT8-slice GEMM; K = N^ = 64 (B_k t) through DGEMM
+  // (A/B in the bench, scripts/gemm_i8_bench.py); CAKF_I8_MIN_K overrides
+  int i8_min_k = [] { const char* e = getenv("CAKF_I8_MIN_K"); return e ? std::atoi(e) : 512; }();
   bool i8_mqr = [] { const char* e = getenv("CAKF_I8_MQR"); return e && e[0] == '1'; }();
   size_t gex_elems = 0;
 
@@ -528,6 +529,7 @@ struct Impl final : ImplBase {
     redC = carve<double>(W);
     cnt = carve<unsigned>(5 * 64);   // per reduction: [0] top, [1..32] group counters
     part2 = carve<double>((size_t)(stage_blocks((int)Nmax) + 33) * W);
+    hmw = carve<double>((size_t)Nmax);
     Yb = carve<T>((size_t)NX * (1 + nhat));
     Ub = carve<T>((size_t)std::max(rin_max, 1) * (1 + nhat));
     tmp = carve<T>((size_t)D * (1 + nhat));
@@ -895,6 +897,7 @@ struct Impl final : ImplBase {
         CK_CUDA(cudaEventRecord(ev_fork, st));
         CK_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
         CK_CUDA(StepKernels<T>::hmts(N, HM, rin, s, part2, W, redA, cnt + 256, st2));
+        CK_CUDA(StepKernels<T>::hmu(N, HM, rin, redA, hmw, st2));
         CK_CUDA(cudaEventRecord(ev_join, st2));
       }
       size_t pk = prof_begin();
@@ -949,7 +952,8 @@ struct Impl final : ImplBase {
       CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, fork ? nullptr : HM, rin, part, W, redA,
                                      cnt, st));
       if (fork) CK_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
-      CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 64, st));
+      CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 64, st,
+                                     fork ? hmw : nullptr));
       if (reorth && i > 1) {  // CGS2 (R19): d = s - V c, then d -= V (V^T G d)
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W, redC,
                                        cnt + 128, C, eps, i, 1, st));

@@ -94,8 +94,11 @@ __device__ __forceinline__ void sym_unit_decode(long long u, int nb, int& bi, in
 // SUB: the exact-zero test and the work run per 16-row group x 32-column sub-tile (sphJ = 32-point
 // spheres; each lane owns one packed column pair of the sub-tile), else per 16-row group x 128-column
 // J tile (sphJ = 128-point spheres; each lane owns 8 columns).  Row -> lane mapping is the same.
+#ifndef CAKF_K1_MINB
+#define CAKF_K1_MINB 3
+#endif
 template <int NU2, bool SUB>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, CAKF_K1_MINB)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
                   float* __restrict__ partial,
                   unsigned long long* __restrict__ done_pairs, const int* __restrict__ ulist,

@@ -242,22 +242,36 @@ hmts_kernel(int N, const T* __restrict__ HM, int rin, const T* __restrict__ s, d
   reduce_blocks(rin, W, part, cnt, red);
 }
 
+// w = HM u (fp64 rows) on the side stream right after hmts, so stage B's second HM pass also overlaps K1
+template <typename T>
+__global__ void __launch_bounds__(kTile)
+hmu_kernel(int N, const T* __restrict__ HM, int rin, const double* __restrict__ ured, double* __restrict__ w) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  double* u = reinterpret_cast<double*>(sm_raw);
+  for (int j = threadIdx.x; j < rin; j += blockDim.x) u[j] = ured[j];
+  __syncthreads();
+  const int row = blockIdx.x * kTile + threadIdx.x;
+  if (row < N) w[row] = row_gemv(HM, (size_t)N, rin, u, row);
+}
+
 // ------------------------------------------------------------------ stage B
+// wpre (nullable): HM u already formed by hmu_kernel (same fp64 row sums), else formed here
 template <typename T>
 __global__ void __launch_bounds__(kTile)
 stageB_kernel(int N, const T* __restrict__ HM, int rin, const double* __restrict__ ured, const T* __restrict__ gp,
               const T* __restrict__ s, T* __restrict__ g, const T* __restrict__ V, int nV, double* __restrict__ part,
-              int W, double* __restrict__ red, unsigned* cnt) {
+              int W, double* __restrict__ red, unsigned* cnt, const double* __restrict__ wpre) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   double* u = reinterpret_cast<double*>(sm_raw);
   __shared__ double scratch[32];
   __shared__ T gs_[kTile];
-  for (int j = threadIdx.x; j < rin; j += blockDim.x) u[j] = ured[j];
+  if (!wpre)
+    for (int j = threadIdx.x; j < rin; j += blockDim.x) u[j] = ured[j];
   __syncthreads();
   const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[1] = {0.0};
   if (row < r1) {
-    const double acc = row_gemv(HM, (size_t)N, rin, u, row);     // fp64: rin can be ~1e3
+    const double acc = wpre ? wpre[row] : row_gemv(HM, (size_t)N, rin, u, row);   // fp64: rin ~1e3
     const T gi = (T)((double)gp[row] - acc);                      // G s
     g[row] = gi;
     a[0] = (double)s[row] * (double)gi;
@@ -739,10 +753,18 @@ cudaError_t StepKernels<T>::hmts(int N, const T* HM, int rin, const T* s, double
 }
 
 template <typename T>
+cudaError_t StepKernels<T>::hmu(int N, const T* HM, int rin, const double* ured, double* w, cudaStream_t st) {
+  if (rin <= 0 || N <= 0) return cudaSuccess;
+  hmu_kernel<T><<<stage_blocks(N), kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
+  return note_launch_err();
+}
+
+template <typename T>
 cudaError_t StepKernels<T>::stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g,
-                                   const T* V, int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st) {
-  stageB_kernel<T><<<stage_blocks(N), kTile, sizeof(double) * (rin > 0 ? rin : 1), st>>>(N, HM, rin, ured, gp, s, g,
-                                                                                       V, nV, part, W, red, cnt);
+                                   const T* V, int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st,
+                                   const double* wpre) {
+  stageB_kernel<T><<<stage_blocks(N), kTile, wpre ? 8 : sizeof(double) * (rin > 0 ? rin : 1), st>>>(
+      N, HM, rin, ured, gp, s, g, V, nV, part, W, red, cnt, wpre);
   return note_launch_err();
 }
 

@@ -46,8 +46,11 @@ struct StepKernels {
   // HM == nullptr in stageA: u = HM^T s is computed by hmts (side stream) into red[0, rin)
   static cudaError_t hmts(int N, const T* HM, int rin, const T* s, double* part, int W, double* red, unsigned* cnt,
                           cudaStream_t st);
+  // w = HM u (fp64) from the reduced u = red[0, rin) (side stream, after hmts)
+  static cudaError_t hmu(int N, const T* HM, int rin, const double* ured, double* w, cudaStream_t st);
   static cudaError_t stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g, const T* V,
-                            int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st);
+                            int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st,
+                            const double* wpre = nullptr);
   static cudaError_t stageC(int N, const T* V, const T* Z, int nV, const double* cred, const T* sin, const T* gin,
                             T* d, T* Gd, const T* s_eta, const double* ared, int rin, const double* sgs, double* part,
                             int W, double* red, unsigned* cnt, IterCtl* ctl, double eps, int iter, int pass,
