@@ -40,7 +40,7 @@ namespace {
 constexpr int I_BM = 128;
 constexpr int I_BK = 64;                      // int8 per K block: one 64-byte swizzle row
 constexpr int I_S = 5;                        // 7-bit slices per operand (35 bits)
-constexpr int I_KC = 16384;                   // K elements per exact int32 chunk
+constexpr int I_KC = 8192;                    // K elements per exact int32 chunk (and per work item)
 constexpr int I_KBC = I_KC / I_BK;            // K blocks per chunk
 constexpr int I_MAXN = 96;                    // I_S accumulators of <= 96 columns in 512 TMEM columns
 constexpr int I_THREADS = 192;                // loader, MMA, 4 epilogue warps
@@ -481,11 +481,10 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  // K splits (whole chunks) until the grid covers the SMs twice; every chunk count >= 2 goes through work
-  const int tiles = mt * ntiles;
-  int splits = std::max(1, std::min(nchunk, (2 * sm_count() + tiles - 1) / tiles));
-  int cps = (nchunk + splits - 1) / splits;
-  splits = (nchunk + cps - 1) / cps;
+  // one work item per (tile, chunk) when the fp64 partials fit (the persistent CTAs then balance many
+  // small items), else whole chunks grouped per split; every chunk count >= 2 goes through work
+  int splits = nchunk;
+  int cps = 1;
   while (nchunk > 1 && (size_t)splits * M * N > work_doubles && splits > 1) {
     ++cps;
     splits = (nchunk + cps - 1) / cps;

@@ -32,13 +32,14 @@ def _check(A, B, ta, tb, alpha, beta, C0, dev, tol):
     # the fp32 output rounding is 2^-24 relative to |C|
     err = np.abs(got.astype(np.float64) - ref) - 2.0 ** -24 * np.abs(ref)
     # slicing bound (kernels_gemm_i8.cu): per product < 12 * 2^-35 * 2^(e_a + e_b) with 2^e <= 2 max|.|
-    # over the 16384-element K chunk, i.e. < 2^-29.4 * max_chunk|a| * max_chunk|b|
+    # over the 8192-element K chunk, i.e. < 2^-29.4 * max_chunk|a| * max_chunk|b|
     K = opA.shape[1]
+    KC = 8192
     bound = np.zeros_like(ref)
-    for c0 in range(0, K, 16384):
-        a = np.abs(opA[:, c0:c0 + 16384]).max(axis=1)
-        b = np.abs(opB[c0:c0 + 16384, :]).max(axis=0)
-        bound += min(16384, K - c0) * np.outer(a, b)
+    for c0 in range(0, K, KC):
+        a = np.abs(opA[:, c0:c0 + KC]).max(axis=1)
+        b = np.abs(opB[c0:c0 + KC, :]).max(axis=0)
+        bound += min(KC, K - c0) * np.outer(a, b)
     bound *= abs(alpha) * 2.0 ** -29
     assert np.all(err <= bound + 1e-300), float(np.max(err / np.maximum(bound, 1e-300)))
     worst = float(np.max(err / np.maximum(scale, 1e-300)))
@@ -51,7 +52,7 @@ def _check(A, B, ta, tb, alpha, beta, C0, dev, tol):
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
 def test_lowrank_gemm_matches_fp64(dev, m, n, k, ta, tb):
     """Shapes with ragged tiles on every axis (128-row / 96-column tiles, 64-deep K blocks) and
-    K spanning several 16384-element exact chunks; Gaussian data spanning 2^10 in magnitude
+    K spanning several 8192-element exact chunks; Gaussian data spanning 2^10 in magnitude
     (beyond 2^11 below a chunk maximum the slices drop bits, hence the max-relative bound)."""
     rng = np.random.default_rng(m * 7 + n * 3 + k)
     A = rng.standard_normal((k, m) if ta else (m, k)) * np.exp2(rng.integers(-5, 5, (k, m) if ta else (m, k)))
