@@ -10,6 +10,8 @@
 //            r -= (alpha/eta) Gd ; next action s (policy) packed into the column coords
 // Each reduction writes per-block partials (fp64); the last block to arrive sums them
 // in block order (deterministic, no float atomics).
+#include <algorithm>
+
 #include "internal.h"
 #include "step.h"
 
@@ -379,9 +381,8 @@ dot_final_kernel(int N, const T* __restrict__ a_, const T* __restrict__ b_, doub
 template <typename T>
 __global__ void gather_rows_kernel(int N, int C, const int* __restrict__ idx, const T* __restrict__ M, size_t ldm,
                                    T* __restrict__ out, size_t ldo) {
-  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (size_t)N * C) return;
-  const int row = (int)(e % N), j = (int)(e / N);
+  const int row = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;   // grid (rows, columns)
+  if (row >= N) return;
   out[row + (size_t)j * ldo] = M[idx[row] + (size_t)j * ldm];
 }
 
@@ -389,9 +390,8 @@ __global__ void gather_rows_kernel(int N, int C, const int* __restrict__ idx, co
 template <typename T>
 __global__ void mix_kernel(int NX, int Dp, int C, Mat3 A, int transpose, const T* __restrict__ in, size_t ldi,
                            T* __restrict__ out, size_t ldo) {
-  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (size_t)NX * C) return;
-  const int q = (int)(e % NX), j = (int)(e / NX);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;   // grid (points, columns)
+  if (q >= NX) return;
   double x[3] = {0.0, 0.0, 0.0};
   for (int t = 0; t < Dp; ++t) x[t] = (double)in[q + (size_t)t * NX + (size_t)j * ldi];
   for (int dd = 0; dd < Dp; ++dd) {
@@ -406,11 +406,9 @@ template <typename T>
 __global__ void post_combine_kernel(int NX, int Dp, int C, Mat3 S, const T* __restrict__ Y, const T* __restrict__ tmp,
                                     const T* __restrict__ mpred, T* __restrict__ m, T* __restrict__ Mk, int rin) {
   const size_t D = (size_t)NX * Dp;
-  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= D * C) return;
-  const size_t p = e % D;
-  const int j = (int)(e / D);
-  const int dd = (int)(p / NX), q = (int)(p % NX);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, dd = blockIdx.z;   // grid (points, cols, D')
+  if (q >= NX) return;
+  const size_t p = (size_t)dd * NX + q;
   T val = (T)S.a[dd][0] * Y[q + (size_t)j * NX];
   if (tmp) val -= tmp[p + (size_t)j * D];
   if (j == 0) m[p] = mpred[p] + val;                              // m = m^- + P^- w
@@ -507,14 +505,11 @@ __global__ void take_top_kernel(int c, int r, const double* __restrict__ evec, c
 template <typename T>
 __global__ void sigma_apply_kernel(int NX, int Dp, int C, Mat3 S, const T* __restrict__ Y, T* __restrict__ y) {
   const size_t D = (size_t)NX * Dp;
-  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= D * C) return;
-  const size_t p = e % D;
-  const int j = (int)(e / D);
-  const int dd = (int)(p / NX), q = (int)(p % NX);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, dd = blockIdx.z;   // grid (points, cols, D')
+  if (q >= NX) return;
   double acc = 0.0;
   for (int t = 0; t < Dp; ++t) acc += S.a[dd][t] * (double)Y[q + (size_t)(j * Dp + t) * NX];
-  y[e] = (T)acc;
+  y[(size_t)dd * NX + q + (size_t)j * D] = (T)acc;
 }
 
 // smoother state: ms = m + y[:,0]; var = var_f - rowsumsq(y[:, 1:C])
@@ -536,11 +531,9 @@ __global__ void smooth_out_kernel(size_t D, int C, const T* __restrict__ m, cons
 // step 1: dense part (copy x columns, zero the H^T V block)
 template <typename T>
 __global__ void ws_dense_kernel(size_t D, int n, int q, const T* __restrict__ X, T* __restrict__ Wf, T* __restrict__ ws) {
-  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t total = D * (size_t)(n + q + 1);
-  if (e >= total) return;
-  const size_t p = e % D;
-  const int j = (int)(e / D);
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;   // grid (rows, n + q + 1 columns)
+  const int j = blockIdx.y;
+  if (p >= D) return;
   if (j == 0) ws[p] = X[p];
   else if (j <= n) Wf[p + (size_t)(j - 1) * D] = T(0);
   else Wf[p + (size_t)(j - 1) * D] = X[p + (size_t)(j - n) * D];
@@ -694,9 +687,8 @@ __global__ void unpermute_kernel(int NX, int Dp, const int* __restrict__ perm, c
 
 template <typename S, typename D_>
 __global__ void convert_kernel(int rows, int cols, const S* __restrict__ src, size_t lds, D_* __restrict__ dst, size_t ldd) {
-  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (size_t)rows * cols) return;
-  const int i = (int)(e % rows), j = (int)(e / rows);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;   // grid (rows, columns)
+  if (i >= rows) return;
   dst[i + (size_t)j * ldd] = (D_)src[i + (size_t)j * lds];
 }
 
@@ -798,7 +790,8 @@ template <typename T>
 cudaError_t StepKernels<T>::gather_rows(int N, int C, const int* idx, const T* M, size_t ldm, T* out, size_t ldo,
                                         cudaStream_t st) {
   if ((size_t)N * C == 0) return cudaSuccess;
-  gather_rows_kernel<T><<<nblk((size_t)N * C), 256, 0, st>>>(N, C, idx, M, ldm, out, ldo);
+  if (N <= 0 || C <= 0) return cudaSuccess;
+  gather_rows_kernel<T><<<dim3(nblk(N), C), 256, 0, st>>>(N, C, idx, M, ldm, out, ldo);
   return note_launch_err();
 }
 
@@ -806,7 +799,8 @@ template <typename T>
 cudaError_t StepKernels<T>::mix(int NX, int Dp, int C, const Mat3& A, bool transpose, const T* in, size_t ldi, T* out,
                                 size_t ldo, cudaStream_t st) {
   if ((size_t)NX * C == 0) return cudaSuccess;
-  mix_kernel<T><<<nblk((size_t)NX * C), 256, 0, st>>>(NX, Dp, C, A, transpose ? 1 : 0, in, ldi, out, ldo);
+  if (NX <= 0 || C <= 0) return cudaSuccess;
+  mix_kernel<T><<<dim3(nblk(NX), C), 256, 0, st>>>(NX, Dp, C, A, transpose ? 1 : 0, in, ldi, out, ldo);
   return note_launch_err();
 }
 
@@ -814,7 +808,8 @@ template <typename T>
 cudaError_t StepKernels<T>::post_combine(int NX, int Dp, int C, const Mat3& S, const T* Y, const T* tmp,
                                          const T* mpred, T* m, T* Mk, int rin, cudaStream_t st) {
   const size_t D = (size_t)NX * Dp;
-  post_combine_kernel<T><<<nblk(D * C), 256, 0, st>>>(NX, Dp, C, S, Y, tmp, mpred, m, Mk, rin);
+  if (D == 0 || C <= 0) return cudaSuccess;
+  post_combine_kernel<T><<<dim3(nblk(NX), C, Dp), 256, 0, st>>>(NX, Dp, C, S, Y, tmp, mpred, m, Mk, rin);
   return note_launch_err();
 }
 
@@ -849,7 +844,8 @@ cudaError_t StepKernels<T>::take_top(int c, int r, const double* evec, const dou
 template <typename T>
 cudaError_t StepKernels<T>::sigma_apply(int NX, int Dp, int C, const Mat3& S, const T* Y, T* y, cudaStream_t st) {
   const size_t D = (size_t)NX * Dp;
-  sigma_apply_kernel<T><<<nblk(D * C), 256, 0, st>>>(NX, Dp, C, S, Y, y);
+  if (NX <= 0 || C <= 0) return cudaSuccess;
+  sigma_apply_kernel<T><<<dim3(nblk(NX), C, Dp), 256, 0, st>>>(NX, Dp, C, S, Y, y);
   return note_launch_err();
 }
 
@@ -863,7 +859,7 @@ cudaError_t StepKernels<T>::smooth_out(size_t D, int C, const T* m, const T* var
 template <typename T>
 cudaError_t StepKernels<T>::ws_build(int N, size_t D, int n, int q, const int* idx, const T* X, const T* XV,
                                      const T* R, T* Wf, T* ws, cudaStream_t st) {
-  ws_dense_kernel<T><<<nblk(D * (n + q + 1)), 256, 0, st>>>(D, n, q, X, Wf, ws);
+  ws_dense_kernel<T><<<dim3(nblk(D), n + q + 1), 256, 0, st>>>(D, n, q, X, Wf, ws);
   cudaError_t e = note_launch_err();
   if (e != cudaSuccess || N == 0) return e;
   ws_scatter_kernel<T><<<nblk((size_t)N * (n + q + 1)), 256, 0, st>>>(N, D, n, q, idx, XV, R, Wf, ws);
@@ -887,7 +883,15 @@ cudaError_t StepKernels<T>::fill(size_t n, T val, T* out, cudaStream_t st) {
 template <typename S, typename D_>
 cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_t ldd, cudaStream_t st) {
   if ((size_t)rows * cols == 0) return cudaSuccess;
-  convert_kernel<S, D_><<<nblk((size_t)rows * cols), 256, 0, st>>>(rows, cols, src, lds, dst, ldd);
+  for (int j0 = 0; j0 < cols; j0 += 65535) {   // grid.y <= 65535 columns per launch
+    const int nc = std::min(65535, cols - j0);
+    convert_kernel<S, D_><<<dim3(nblk(rows), nc), 256, 0, st>>>(rows, nc, src + (size_t)j0 * lds, lds,
+                                                                 dst + (size_t)j0 * ldd, ldd);
+    if (j0 + nc < cols) {
+      const cudaError_t e = note_launch_err();
+      if (e != cudaSuccess) return e;
+    }
+  }
   return note_launch_err();
 }
 template cudaError_t convert<float, double>(int, int, const float*, size_t, double*, size_t, cudaStream_t);
