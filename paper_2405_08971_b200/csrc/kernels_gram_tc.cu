@@ -272,12 +272,36 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
       const uint32_t a0 = a_addr(sa);
       const float4* sxc = reinterpret_cast<const float4*>(b_base + sb * B_STAGE_BYTES + 3 * B_PLANE) + 16 * khalf;
       uint32_t p1[8], p2[8], p3[8];   // bf16x2 packed
+      if (!F16 && !diag_nogen) {
+        // two columns per step on the packed f32x2 FMA-pipe ops (MUFU sqrt / ex2 stay scalar), then the
+        // exact truncation split of both values at once: h1 = top 16 bits, r1 = v - h1, h2 = top of r1,
+        // r2 = r1 - h2 (both subtractions exact); each plane's bf16x2 word is one byte permute of the
+        // two values' high halves — the same planes as split3 + pack, in about half the instructions
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+          const float4 c0 = sxc[q], c1 = sxc[q + 1];   // {x, x', y, y'}, {z, z', w, w'} of points k, k+1
+          const float2 dx = __fadd2_rn(make_float2(c0.x, c0.y), make_float2(-xa.x, -xa.x));
+          const float2 dy = __fadd2_rn(make_float2(c0.z, c0.w), make_float2(-xa.y, -xa.y));
+          const float2 dz = __fadd2_rn(make_float2(c1.x, c1.y), make_float2(-xa.z, -xa.z));
+          const float2 kv = matern2_from_d2<NU2>(__ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx))));
+          const uint32_t ua = __float_as_uint(kv.x), ub = __float_as_uint(kv.y);
+          const float2 h1 = make_float2(__uint_as_float(ua & 0xFFFF0000u), __uint_as_float(ub & 0xFFFF0000u));
+          const float2 r1 = __fadd2_rn(kv, make_float2(-h1.x, -h1.y));
+          const uint32_t va = __float_as_uint(r1.x), vb = __float_as_uint(r1.y);
+          const float2 h2 = make_float2(__uint_as_float(va & 0xFFFF0000u), __uint_as_float(vb & 0xFFFF0000u));
+          const float2 r2 = __fadd2_rn(r1, make_float2(-h2.x, -h2.y));
+          p1[q >> 1] = __byte_perm(ua, ub, 0x7632);
+          p2[q >> 1] = __byte_perm(va, vb, 0x7632);
+          p3[q >> 1] = __byte_perm(__float_as_uint(r2.x), __float_as_uint(r2.y), 0x7632);
+        }
+      } else {
 #pragma unroll
       for (int q = 0; q < 16; q += 2) {
         float kv[2];
+        const float4 cA = sxc[q], cB = sxc[q + 1];   // pair-packed {x, x', y, y'}, {z, z', w, w'}
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-          const float4 c = sxc[q + t];
+          const float4 c = t == 0 ? make_float4(cA.x, cA.z, cB.x, 0.f) : make_float4(cA.y, cA.w, cB.y, 0.f);
           const float dx = xa.x - c.x, dy = xa.y - c.y, dz = xa.z - c.z;
           const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           kv[t] = diag_nogen ? d2 : matern_from_d2<NU2>(d2);   // diag_nogen: timing experiment only
@@ -293,6 +317,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
         p1[q >> 1] = a1 | (b1 << 16);
         p2[q >> 1] = a2 | (b2 << 16);
         p3[q >> 1] = a3 | (b3 << 16);
+      }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -414,6 +439,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// column coordinates as point pairs: out[2j] = {x_2j, x_2j+1, y_2j, y_2j+1}, out[2j+1] = {z.., w..}
+// (zero partner for an odd count), so the producers' packed f32x2 operands load ready-paired
+__global__ void pack_pairs_kernel(int K, const float4* __restrict__ xc, float4* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * j >= K) return;
+  const float4 a = xc[2 * j], b = 2 * j + 1 < K ? xc[2 * j + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+  out[2 * j] = make_float4(a.x, b.x, a.y, b.y);
+  out[2 * j + 1] = make_float4(a.z, b.z, a.w, b.w);
+}
+
 template <int NU2>
 cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const uint16_t* planes, int Kp, int C,
                          int ntile, float* Y, size_t ldy, float alpha, cudaStream_t st, const int* act_cnt,
@@ -438,8 +473,8 @@ cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const
   if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, (void*)planes, gdB, gsB, boxB, es3, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  // column coordinates: [K rows] x [4 floats]; boxes of 32 rows, zero beyond K
-  const cuuint64_t gdX[2] = {4, (cuuint64_t)K};
+  // column coordinates, pair-packed (pack_pairs_kernel): [K2 rows] x [4 floats]; boxes of 32 rows, zero beyond
+  const cuuint64_t gdX[2] = {4, (cuuint64_t)((K + 1) / 2 * 2)};
   const cuuint64_t gsX[1] = {16};
   const cuuint32_t boxX[2] = {4, TC_BK};
   const cuuint32_t es2[2] = {1, 1};
@@ -518,7 +553,8 @@ cudaError_t launch_k2_active(const float4* sphM, int nmt, const float4* sphK, in
 
 size_t gram_gemm_tc_workspace(int K, int C) {
   const size_t Kp = ((size_t)K + TC_BK - 1) / TC_BK * TC_BK;
-  return 3 * Kp * (size_t)C * sizeof(uint16_t) + 2 * (size_t)C * sizeof(float) + 1024;
+  // planes, column scales, and the pair-packed column coordinates (K rounded up to even) + alignment
+  return 3 * Kp * (size_t)C * sizeof(uint16_t) + 2 * (size_t)C * sizeof(float) + ((size_t)K + 2) * 16 + 2048;
 }
 
 bool use_f16_k2() {
@@ -540,6 +576,13 @@ cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* 
   const bool f16 = use_f16_k2();
   float* colscale = reinterpret_cast<float*>(planes + 3 * plane + 256);   // 512 B past the planes
   float* colinv = colscale + C;
+  float4* xpair = reinterpret_cast<float4*>(((uintptr_t)(colinv + C) + 255) & ~(uintptr_t)255);
+  if (K > 0) {
+    pack_pairs_kernel<<<(unsigned)(((K + 1) / 2 + 255) / 256), 256, 0, st>>>(K, xc, xpair);
+    const cudaError_t e = note_launch_err();
+    if (e != cudaSuccess) return e;
+  }
+  xc = xpair;
   if (plane > 0) {
     if (f16) {
       colscale_kernel<<<C, 256, 0, st>>>(K, B, ldb, colscale, colinv);
