@@ -354,6 +354,7 @@ struct Impl final : ImplBase {
 
   // ---------------- multi-GPU: the Gram products are sharded, the rest replicated
   int world = 1, rank = 0;
+  bool coll = false;   // sharded data path with collectives (world > 1, or CAKF_FORCE_COLLECTIVES=1 at world 1)
   ncclComm_t comm = nullptr;
   T *yloc = nullptr, *yred = nullptr;      // K1: this rank's reduced partial, all-reduced vector
   T *yslice = nullptr, *ygath = nullptr;   // K2: this rank's output row slice, all-gathered slices
@@ -380,7 +381,7 @@ struct Impl final : ImplBase {
   // acnt/alist: exact-zero culling lists of the 128-row tiles of xr (nullable)
   int k2(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y, size_t ldy,
          const int* acnt = nullptr, const int* alist = nullptr, int astride = 0) {
-    if (world == 1) {
+    if (!coll) {
       CK_CUDA(k2_local(xr, M, xc, K, B, ldb, C, Y, ldy, acnt, alist, astride));
       return CAKF_OK;
     }
@@ -592,7 +593,7 @@ struct Impl final : ImplBase {
     lam2_user = carve<T>(Nmax);
     outm = carve<T>(D);
     outv = carve<T>(D);
-    if (world > 1) {
+    if (coll) {
       yloc = carve<T>(Nmax);
       yred = carve<T>(Nmax);
       k2_cmax = std::max<size_t>((size_t)(1 + nhat), (size_t)Dp * (1 + qmax));
@@ -640,10 +641,21 @@ struct Impl final : ImplBase {
     blk = std::max(1, std::min<int>(c.block_actions, std::max(1, 1 + nhat)));
     cull = c.cull_zero != 0 && sizeof(T) == 4;
     world = std::max(1, c.world); rank = c.rank;
-    if (world > 1) {
-      if (!c.nccl_id || rank < 0 || rank >= world) return fail(CAKF_E_ARG, "multi-GPU: nccl_id and 0 <= rank < world needed");
+    {
+      const char* fc = std::getenv("CAKF_FORCE_COLLECTIVES");
+      coll = world > 1 || (fc && fc[0] == '1');
+    }
+    if (coll) {
       ncclUniqueId id;
-      std::memcpy(&id, c.nccl_id, sizeof(id));
+      if (world == 1) {
+        // single-rank communicator: the sharded path (slices, all-reduce, all-gather) runs on one GPU
+        rank = 0;
+        CK_NCCL(ncclGetUniqueId(&id));
+      } else {
+        if (!c.nccl_id || rank < 0 || rank >= world)
+          return fail(CAKF_E_ARG, "multi-GPU: nccl_id and 0 <= rank < world needed");
+        std::memcpy(&id, c.nccl_id, sizeof(id));
+      }
       const ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
       if (r != ncclSuccess) return fail(CAKF_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
@@ -921,7 +933,7 @@ struct Impl final : ImplBase {
       } else {
       // multi-GPU: this rank evaluates its share of the kernel work (sym units / column chunks),
       // the rest of the partial buffer is zero, and the reduced vector is all-reduced
-      if (world > 1) CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)nch * N * sizeof(T), st));
+      if (coll) CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)nch * N * sizeof(T), st));
       if constexpr (sizeof(T) == 4) {
         if (sym) {
           const long long U = matvec_sym_units(N);
@@ -940,7 +952,7 @@ struct Impl final : ImplBase {
         CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st, nch * rank / world,
                                          nch * (rank + 1) / world));
       }
-      if (world > 1) {
+      if (coll) {
         CK_CUDA(launch_sum_partials<T>(N, nch, partial, 1.0, yloc, st));
         CK_NCCL(ncclAllReduce(yloc, yred, (size_t)N, sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, ncclSum, comm, st));
         kpart = yred;

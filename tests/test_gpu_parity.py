@@ -251,3 +251,21 @@ def test_block_actions_fp64(policy, b):
 def test_block_actions_fp32():
     wl = make_workload("sphere48", policy="random", max_iter=16, max_rank=24, T=4, block_actions=8)
     compare_fp32_cancellation(wl)
+
+
+# ------------------------------------------------ sharded data path on one rank
+@pytest.mark.parametrize("name,dtype,policy,iters,rank", [("sphere48", "f64", "cg", 16, 24),
+                                                          ("sphere48", "f64", "random", 8, 12),
+                                                          ("sphere24", "f32", "random", 16, 24)])
+def test_collective_path_world1(monkeypatch, name, dtype, policy, iters, rank):
+    """CAKF_FORCE_COLLECTIVES=1 runs the multi-GPU data path with a one-rank NCCL communicator:
+    K1 through the per-rank unit range + partial sum + ncclAllReduce, K2 through the row slice +
+    ncclAllGather + slice reassembly.  This pool gives one GPU per call, so this is the on-device
+    check of the sharded code path (the world-2 decomposition itself is covered by
+    tests/test_multi_gpu_plan.py on gloo)."""
+    monkeypatch.setenv("CAKF_FORCE_COLLECTIVES", "1")
+    wl = make_workload(name, policy=policy, max_iter=iters, max_rank=rank, T=4)
+    if dtype == "f64":
+        compare(wl, "f64", 1e-9, 1e-9)
+    else:
+        compare_fp32_cancellation(wl)
