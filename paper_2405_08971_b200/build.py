@@ -37,15 +37,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
+    """extra / out: experiment builds (extra nvcc -D flags, a separate library path for CAKF_LIB A/B runs)."""
+    lib = out or LIB
+    if not force and not extra and not _stale():
         return LIB
     objs = []
-    build_dir = os.path.join(HERE, "build")
+    build_dir = os.path.join(HERE, "build" if not out else "build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(build_dir, exist_ok=True)
     common = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL_DIR, "include"),
-              "-Xptxas", "-v" if verbose else "-O3"]
+              "-Xptxas", "-v" if verbose else "-O3", *(extra or [])]
     procs = []
     for src in SOURCES:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
@@ -58,16 +60,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + out)
         if verbose and out:
             print(out)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     nccl_lib = os.path.join(NCCL_DIR, "lib")
     link = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcublas", "-lcusolver", "-L", nccl_lib, "-l:libnccl.so.2",
             "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-Xlinker", "-rpath," + nccl_lib]
     r = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + " ".join(link) + "\n" + r.stdout)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    _extra = [a for a in sys.argv[1:] if a.startswith("-D")]
+    _out = next((a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")), None)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, extra=_extra, out=_out))

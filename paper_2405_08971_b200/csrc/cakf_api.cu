@@ -282,6 +282,7 @@ struct Impl final : ImplBase {
   int act_stride_sm = 0, act_stride_po = 0;
   int *k1_list = nullptr, *k1_count = nullptr;
   unsigned short* k1_mask = nullptr;  // active symmetric K1 units of this update
+  unsigned* k1_sched = nullptr;                           // K1 dynamic unit scheduling counters
   unsigned long long* cull_ctr = nullptr;  // [0] K1 tile pairs done, [1] K2-post blocks, [2] K2-smooth blocks
   double k1_pairs_dense = 0, k2_post_dense = 0, k2_sm_dense = 0;
   int64_t k2_sm_launches = 0;
@@ -630,6 +631,7 @@ struct Impl final : ImplBase {
       act_list_tt = carve<int>((size_t)no128 * no32);
       k1_count = carve<int>(1);
     }
+    k1_sched = carve<unsigned>(4);
   }
 
   int init(const cakf_config& c) override {
@@ -689,8 +691,14 @@ struct Impl final : ImplBase {
     }
     layout();
     CK_CUDA(cudaMemsetAsync(cnt, 0, 5 * 64 * sizeof(unsigned), st));
+    CK_CUDA(cudaMemsetAsync(k1_sched, 0, 4 * sizeof(unsigned), st));
     if (side) {
-      CK_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+      {  // highest priority: the side HM passes take SM slots ahead of queued K1 CTAs
+        int lo = 0, hi = 0;
+        CK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const char* e = getenv("CAKF_SIDE_PRIO");
+        CK_CUDA(cudaStreamCreateWithPriority(&st2, cudaStreamNonBlocking, (e && e[0] == '0') ? lo : hi));
+      }
       CK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       CK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
@@ -939,7 +947,8 @@ struct Impl final : ImplBase {
           const long long U = matvec_sym_units(N);
           CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
                                     U * rank / world, U * (rank + 1) / world, st, cull ? cull_ctr : nullptr,
-                                    cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128, sph_o32, kCullCut));
+                                    cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128, sph_o32, kCullCut,
+                                    k1_sched));
           if (cull) {
             const double nt = (double)((N + 127) / 128);
             k1_pairs_dense += (double)matvec_sym_blocks_per_tile_pair() * nt * (nt + 1) / 2 / world;   // warp blocks

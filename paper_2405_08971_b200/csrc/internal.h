@@ -29,7 +29,8 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
                               cudaStream_t st, unsigned long long* done_pairs = nullptr, const int* ulist = nullptr,
                               const int* ucount = nullptr, const unsigned short* umask = nullptr,
                               const float4* sph16 = nullptr, const float4* sph128 = nullptr,
-                              const float4* sph32 = nullptr, float cut = 0.f);
+                              const float4* sph32 = nullptr, float cut = 0.f, unsigned* sched = nullptr);
+// sched (nullable, 2 zero-initialised counters, one per handle): dynamic unit scheduling (CAKF_K1_DYN=0: off)
 int matvec_sym_blocks_per_tile_pair();   // warp blocks per 128 x 128 tile pair counted by done_pairs
 // compact ascending list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,

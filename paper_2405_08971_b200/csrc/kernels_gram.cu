@@ -94,20 +94,24 @@ __device__ __forceinline__ void sym_unit_decode(long long u, int nb, int& bi, in
 // SUB: the exact-zero test and the work run per 16-row group x 32-column sub-tile (sphJ = 32-point
 // spheres; each lane owns one packed column pair of the sub-tile), else per 16-row group x 128-column
 // J tile (sphJ = 128-point spheres; each lane owns 8 columns).  Row -> lane mapping is the same.
-#ifndef CAKF_K1_MINB
-#define CAKF_K1_MINB 3
+// 72 registers (no spills) leave 10240 of an SM's 65536 registers beside three resident 256-thread CTAs:
+// room for one 128-thread side-stream HM CTA, so the HBM-bound HM passes overlap the MUFU-bound K1
+#ifndef CAKF_K1_MAXREG
+#define CAKF_K1_MAXREG 72
 #endif
 template <int NU2, bool SUB>
-__global__ void __launch_bounds__(256, CAKF_K1_MINB)
+__global__ void __maxnreg__(CAKF_K1_MAXREG)
 matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long u_begin, long long u_end,
                   float* __restrict__ partial,
                   unsigned long long* __restrict__ done_pairs, const int* __restrict__ ulist,
                   const int* __restrict__ ucount, const unsigned short* __restrict__ umask,
-                  const float4* __restrict__ sph16, const float4* __restrict__ sphJ, float cut) {
+                  const float4* __restrict__ sph16, const float4* __restrict__ sphJ, float cut,
+                  unsigned* __restrict__ sched) {
   constexpr int NJS = SUB ? SYM_S * 4 : SYM_S;   // J spheres per unit
   extern __shared__ __align__(16) unsigned char sm_raw[];
   __shared__ float4 s16[SYM_S * 8], s128[NJS];   // this unit's 16-row group / J (sub-)tile spheres
   __shared__ unsigned s_done;                        // evaluated 16 x 128 warp blocks of this unit
+  __shared__ unsigned s_next;                        // dynamic scheduling: this CTA's next work item
   float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
   float4* tJ = tI + SYM_S * SYM_T;                                    // [SYM_S][128]
   float* rowacc = reinterpret_cast<float*>(tJ + SYM_S * SYM_T);       // [SYM_S][128]
@@ -117,7 +121,10 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
   // ulist: compact ascending list of the units with an active tile pair (exact-zero culling); the
   // skipped units' partial slots were zeroed once per update
   const long long nwork = ulist ? (long long)*ucount : u_end - u_begin;
-  for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
+  // sched != nullptr: the first item is blockIdx.x, later ones are taken from a global counter in list
+  // order (longest first => greedy LPT balance); the assignment cannot change any result because every
+  // unit owns its partial slots.  The last CTA to finish resets the counters for the next launch.
+  for (long long w = blockIdx.x; w < nwork;) {
     const long long u = ulist ? (long long)ulist[w] : u_begin + w;
     // active tile pairs of this unit, bit a*SYM_S+b (exact-zero culling; all ones without)
     const unsigned amask = ulist ? (unsigned)umask[w] : 0xFFFFu;
@@ -317,6 +324,20 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
         const int gj = bj * SYM_S * SYM_T + e;
         if (gj < n) partial[(size_t)bi * n + gj] = cs_;
       }
+    }
+    if (sched) {
+      if (tid == 0) s_next = gridDim.x + atomicAdd(sched, 1u);
+      __syncthreads();   // the next write of s_next is behind the next unit's barriers
+      w = s_next;
+    } else {
+      w += gridDim.x;
+    }
+  }
+  if (sched && tid == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+      sched[0] = 0u;
+      sched[1] = 0u;
     }
   }
 }
@@ -619,6 +640,15 @@ cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, lon
   return note_launch_err();
 }
 
+bool use_k1_dyn() {   // CAKF_K1_DYN=0: static strided unit assignment instead of the global work counter
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAKF_K1_DYN");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 bool use_k1_sub() {   // CAKF_K1_SUB=0: exact-zero test per 128-column J tile instead of per 32-column sub-tile
   static int v = -1;
   if (v < 0) {
@@ -631,7 +661,8 @@ bool use_k1_sub() {   // CAKF_K1_SUB=0: exact-zero test per 128-column J tile in
 template <int NU2, bool SUB>
 cudaError_t launch_sym_t(const float4* x, int n, int nt, int nb, float* partial, long long u_begin, long long u_end,
                          cudaStream_t st, unsigned long long* done_pairs, const int* ulist, const int* ucount,
-                         const unsigned short* umask, const float4* sph16, const float4* sphJ, float cut) {
+                         const unsigned short* umask, const float4* sph16, const float4* sphJ, float cut,
+                         unsigned* sched) {
   static int per_sm = 0;   // resident CTAs per SM (one full wave; the units are strided over it)
   const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)SYM_S * SYM_T * sizeof(float) +
                       (size_t)16 * SYM_S * SYM_T * sizeof(float);
@@ -648,14 +679,15 @@ cudaError_t launch_sym_t(const float4* x, int n, int nt, int nb, float* partial,
   }
   const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);
   matvec_sym_kernel<NU2, SUB><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, done_pairs,
-                                                                  ulist, ucount, umask, sph16, sphJ, cut);
+                                                                  ulist, ucount, umask, sph16, sphJ, cut,
+                                                                  use_k1_dyn() ? sched : nullptr);
   return note_launch_err();
 }
 
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
                               cudaStream_t st, unsigned long long* done_pairs, const int* ulist,
                               const int* ucount, const unsigned short* umask, const float4* sph16,
-                              const float4* sph128, const float4* sph32, float cut) {
+                              const float4* sph128, const float4* sph32, float cut, unsigned* sched) {
   if (n <= 0 || u_end <= u_begin) return cudaSuccess;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
@@ -665,9 +697,9 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
 #define CAKF_SYM_CASE(NU)                                                                                           \
   case NU:                                                                                                         \
     return sub ? launch_sym_t<NU, true>(x, n, nt, nb, partial, u_begin, u_end, st, done_pairs, ulist, ucount,    \
-                                        umask, sph16, sph32, cut)                                                 \
+                                        umask, sph16, sph32, cut, sched)                                          \
                : launch_sym_t<NU, false>(x, n, nt, nb, partial, u_begin, u_end, st, done_pairs, ulist, ucount,   \
-                                         umask, sph16, sph128, cut);
+                                         umask, sph16, sph128, cut, sched);
     CAKF_SYM_CASE(1)
     CAKF_SYM_CASE(3)
     CAKF_SYM_CASE(5)

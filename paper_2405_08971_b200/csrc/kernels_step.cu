@@ -156,6 +156,15 @@ __device__ bool reduce_blocks(int n, int W, double* part, unsigned* cnt, double*
   return true;
 }
 
+bool side_slim() {   // CAKF_SIDE_SLIM=0: side-stream HM kernels without the 80-register cap (then they only fit in the K1 tail)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAKF_SIDE_SLIM");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // ------------------------------------------------------------------ update prologue
 template <typename T>
 __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __restrict__ coords, const T* __restrict__ y,
@@ -235,8 +244,11 @@ stageA_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const
 
 // u = (HM^-)^T s alone (red[0, rin)): the HBM-bound half of stage A, launched on a side stream so it
 // overlaps the MUFU-bound K1 of the same iteration (both only need s)
-template <typename T>
-__global__ void __launch_bounds__(kTile)
+// MINB = 6 caps the kernel at 80 registers so one of its CTAs fits beside three resident K1 CTAs
+// (3 x 256 x 72 = 55296 of 65536 registers): the HBM-bound HM passes then run concurrently with the
+// MUFU-bound K1 instead of only in its tail
+template <typename T, int MINB>
+__global__ void __launch_bounds__(kTile, MINB)
 hmts_kernel(int N, const T* __restrict__ HM, int rin, const T* __restrict__ s, double* __restrict__ part, int W,
             double* __restrict__ red, unsigned* cnt) {
   const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile);
@@ -245,8 +257,8 @@ hmts_kernel(int N, const T* __restrict__ HM, int rin, const T* __restrict__ s, d
 }
 
 // w = HM u (fp64 rows) on the side stream right after hmts, so stage B's second HM pass also overlaps K1
-template <typename T>
-__global__ void __launch_bounds__(kTile)
+template <typename T, int MINB>
+__global__ void __launch_bounds__(kTile, MINB)
 hmu_kernel(int N, const T* __restrict__ HM, int rin, const double* __restrict__ ured, double* __restrict__ w) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   double* u = reinterpret_cast<double*>(sm_raw);
@@ -740,14 +752,20 @@ template <typename T>
 cudaError_t StepKernels<T>::hmts(int N, const T* HM, int rin, const T* s, double* part, int W, double* red,
                                  unsigned* cnt, cudaStream_t st) {
   if (rin <= 0 || N <= 0) return cudaSuccess;
-  hmts_kernel<T><<<stage_blocks(N), kTile, 0, st>>>(N, HM, rin, s, part, W, red, cnt);
+  if (side_slim())
+    hmts_kernel<T, 6><<<stage_blocks(N), kTile, 0, st>>>(N, HM, rin, s, part, W, red, cnt);
+  else
+    hmts_kernel<T, 1><<<stage_blocks(N), kTile, 0, st>>>(N, HM, rin, s, part, W, red, cnt);
   return note_launch_err();
 }
 
 template <typename T>
 cudaError_t StepKernels<T>::hmu(int N, const T* HM, int rin, const double* ured, double* w, cudaStream_t st) {
   if (rin <= 0 || N <= 0) return cudaSuccess;
-  hmu_kernel<T><<<stage_blocks(N), kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
+  if (side_slim())
+    hmu_kernel<T, 6><<<stage_blocks(N), kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
+  else
+    hmu_kernel<T, 1><<<stage_blocks(N), kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
   return note_launch_err();
 }
 
