@@ -1040,13 +1040,15 @@ struct Impl final : ImplBase {
         Bp = dB;
         ldbp = br;
       }
-      if (beta != 0.0) CK_CUDA((convert<float, double>)(m, n, reinterpret_cast<const float*>(C), ldc, dC, m, st));
+      // beta C is added in fp64 by the fold-back kernel (no fp64 copy of C in or out of the DGEMM)
+      const double zero = 0.0;
       if (k > 0) {
-        CK_BLAS(cublasDgemm(blas, ta, tb, m, n, k, &alpha, dA, ar, Bp, ldbp, &beta, dC, m));
+        CK_BLAS(cublasDgemm(blas, ta, tb, m, n, k, &alpha, dA, ar, Bp, ldbp, &zero, dC, m));
       } else {
         CK_CUDA(cudaMemsetAsync(dC, 0, (size_t)m * n * sizeof(double), st));
       }
-      CK_CUDA((convert<double, float>)(m, n, dC, m, reinterpret_cast<float*>(C), ldc, st));
+      if (beta != 0.0) CK_CUDA(accum_d2f(m, n, beta, dC, m, reinterpret_cast<float*>(C), ldc, st));
+      else CK_CUDA((convert<double, float>)(m, n, dC, m, reinterpret_cast<float*>(C), ldc, st));
     }
     return CAKF_OK;
   }

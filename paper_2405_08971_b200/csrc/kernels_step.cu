@@ -749,6 +749,15 @@ __global__ void convert_kernel(int rows, int cols, const S* __restrict__ src, si
   dst[i + (size_t)j * ldd] = (D_)src[i + (size_t)j * lds];
 }
 
+// C = (float)(beta * C + Cd): the fp64 GEMM result folded into an fp32 C in one pass (no fp64 copy of C)
+__global__ void accum_d2f_kernel(int rows, double beta, const double* __restrict__ Cd, size_t ldcd,
+                                 float* __restrict__ C, size_t ldc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;   // grid (rows, columns)
+  if (i >= rows) return;
+  float* c = C + i + (size_t)j * ldc;
+  *c = (float)(beta * (double)*c + Cd[i + (size_t)j * ldcd]);
+}
+
 template <typename T>
 __global__ void fill_kernel(size_t n, T val, T* __restrict__ out) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -976,6 +985,19 @@ cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_
   }
   return note_launch_err();
 }
+cudaError_t accum_d2f(int rows, int cols, double beta, const double* Cd, size_t ldcd, float* C, size_t ldc,
+                      cudaStream_t st) {
+  if ((size_t)rows * cols == 0) return cudaSuccess;
+  for (int j0 = 0; j0 < cols; j0 += 65535) {
+    const int nc = std::min(65535, cols - j0);
+    accum_d2f_kernel<<<dim3(nblk(rows), nc), 256, 0, st>>>(rows, beta, Cd + (size_t)j0 * ldcd, ldcd,
+                                                          C + (size_t)j0 * ldc, ldc);
+    const cudaError_t e = note_launch_err();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 template cudaError_t convert<float, double>(int, int, const float*, size_t, double*, size_t, cudaStream_t);
 template cudaError_t convert<double, float>(int, int, const double*, size_t, float*, size_t, cudaStream_t);
 template cudaError_t convert<double, double>(int, int, const double*, size_t, double*, size_t, cudaStream_t);

@@ -32,6 +32,9 @@ template <typename T>
 cudaError_t unpermute(int NX, int Dp, const int* perm, const T* in, T* out, cudaStream_t st);
 template <typename S, typename D_>
 cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_t ldd, cudaStream_t st);
+// C = (float)(beta C + Cd) (fp64 GEMM result accumulated into fp32 C)
+cudaError_t accum_d2f(int rows, int cols, double beta, const double* Cd, size_t ldcd, float* C, size_t ldc,
+                      cudaStream_t st);
 
 template <typename T>
 struct StepKernels {
