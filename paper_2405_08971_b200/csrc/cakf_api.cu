@@ -221,6 +221,7 @@ struct Impl final : ImplBase {
   T* mu0 = nullptr;
   struct Step {
     T *m_pred, *m, *var, *ms, *vs, *Mk, *XV;
+    T* KV;   // post-loop kernel products K(X, T_k) [v V] (NX x (1 + n)), reused by the smoother
     int* idx;
     double* kept;
     int cap_cols = 0;
@@ -257,6 +258,9 @@ struct Impl final : ImplBase {
   // smoother
   T *X = nullptr, *Yk = nullptr, *yb = nullptr, *Tm = nullptr, *Hy = nullptr, *tt = nullptr, *R = nullptr;
   T *Wf = nullptr, *Ws = nullptr, *ws = nullptr, *pvar = nullptr;
+  // kernel-applied smoother carriers (I (x) K)[w^s, W^s] (and of W^s_full), K(X, T) V t
+  T *KWf = nullptr, *KWs = nullptr, *Kws = nullptr, *Zk = nullptr;
+  bool smooth_k2 = [] { const char* e = getenv("CAKF_SMOOTH_K2"); return e && e[0] == '1'; }();
   float* tcw = nullptr;  // bf16 planes of the K2 right-hand sides
   // low-rank contractions on tcgen05 (kernels_gemm_tc.cu): operand planes, split-K work, fp32 Q_r
   // (truncation always; the post-loop / smoother contractions only with CAKF_LOWRANK_TC=1 — fp32
@@ -506,6 +510,7 @@ struct Impl final : ImplBase {
       S.vs = carve<T>(D);
       S.Mk = carve<T>((size_t)D * S.cap_cols);
       S.XV = k ? carve<T>((size_t)Nmax * (1 + nhat)) : nullptr;
+      S.KV = k ? carve<T>((size_t)NX * (1 + nhat)) : nullptr;
       S.idx = k ? carve<int>(Nmax) : nullptr;
       S.kept = rcap > 0 ? carve<double>(rcap) : nullptr;
     }
@@ -567,6 +572,12 @@ struct Impl final : ImplBase {
     Wf = carve<T>((size_t)D * (nhat + qmax));
     Ws = carve<T>((size_t)D * (nhat + qmax));
     ws = carve<T>(D);
+    if (!smooth_k2) {
+      KWf = carve<T>((size_t)D * (nhat + qmax));
+      KWs = carve<T>((size_t)D * (nhat + qmax));
+      Kws = carve<T>(D);
+      Zk = carve<T>((size_t)NX * C);
+    }
     pvar = carve<T>(D);
     perm_d = carve<int>(NX);
     invperm_d = carve<int>(NX);
@@ -991,7 +1002,7 @@ struct Impl final : ImplBase {
     // ---- post-loop: [P^- w, P^- W] = Sigma H^T [v V] - M^- (H M^-)^T [v V]
     const int Cc = 1 + niter;
     size_t pk = prof_begin();
-    CK(k2(coords, (int)NX, xcs, N, S.XV, N, Cc, Yb, NX, cull ? act_cnt_po : nullptr, act_list_po, act_stride_po));
+    CK(k2(coords, (int)NX, xcs, N, S.XV, N, Cc, S.KV, NX, cull ? act_cnt_po : nullptr, act_list_po, act_stride_po));
     prof_end(CAKF_PROF_K2_POST, pk);
     if (rin) {
       pk = prof_begin();
@@ -999,7 +1010,7 @@ struct Impl final : ImplBase {
       CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, Cc, rin, 1.0, S.Mk, (int)D, Ub, rin, 0.0, tmp, (int)D));
       prof_end(CAKF_PROF_LOWRANK, pk);
     }
-    CK_CUDA(StepKernels<T>::post_combine((int)NX, Dp, Cc, S.sig_t, Yb, rin ? tmp : nullptr, S.m_pred, S.m, S.Mk, rin,
+    CK_CUDA(StepKernels<T>::post_combine((int)NX, Dp, Cc, S.sig_t, S.KV, rin ? tmp : nullptr, S.m_pred, S.m, S.Mk, rin,
                                          st));
     S.cols = rin + niter;
     CK_CUDA(StepKernels<T>::rowvar((int)NX, Dp, S.sig_t, nullptr, S.Mk, D, S.cols, S.var, st));
@@ -1101,7 +1112,8 @@ struct Impl final : ImplBase {
   }
 
   // fp32 truncation on tcgen05: Gram F^T F (3xBF16, K split, fp64 reduction) -> fp64 eig -> F Q_r
-  int truncate_factor_tc(const float* F, int c, int rkeep, float* out, double* kept, double* dropped, size_t pk) {
+  int truncate_factor_tc(const float* F, int c, int rkeep, float* out, double* kept, double* dropped, size_t pk,
+                         const float* F2, float* out2) {
     size_t ps = prof_begin();
     if (gemm_tc_plane_bytes((int)D, c) > gp_elems * 2) return fail(CAKF_E_ARG, "truncate: operand planes too small");
     const bool i8 = use_i8_gemm();
@@ -1124,24 +1136,35 @@ struct Impl final : ImplBase {
     if (i8 && i8_mqr) {   // M~ = F Q_r with the fp64 eigenvectors sliced directly
       CK(gemm_i8_f32(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, c, 0.0, out, nullptr,
                      (int)D, false, QrD));
+      if (F2)
+        CK(gemm_i8_f32(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, 1.0, F2, (int)D, nullptr, c, 0.0, out2, nullptr,
+                       (int)D, false, QrD));
     } else {
       CK_CUDA((convert<double, float>)(c, rkeep, QrD, c, Qf, c, st));
       CK_CUDA(gemm_tc_split(F, (int)D, c, (size_t)D, false, gpA, st));           // F rows (K = c, transposed)
       CK_CUDA(gemm_tc_split(Qf, rkeep, c, (size_t)c, true, gpB, st));           // Q_r columns
       CK_CUDA(gemm_tc_run(gpA, (int)D, gpB, rkeep, c, 1.0, 0.0, out, nullptr, (size_t)D, gwork, kGemmWorkFloats,
                           st));
+      if (F2) {   // same Q_r planes
+        CK_CUDA(gemm_tc_split(F2, (int)D, c, (size_t)D, false, gpA, st));
+        CK_CUDA(gemm_tc_run(gpA, (int)D, gpB, rkeep, c, 1.0, 0.0, out2, nullptr, (size_t)D, gwork, kGemmWorkFloats,
+                            st));
+      }
     }
     prof_end(CAKF_PROF_TRUNC_GEMM, ps);
     prof_end(CAKF_PROF_TRUNCATE, pk);
     return CAKF_OK;
   }
 
-  // Truncate a D x c factor F (ld D) to its top-r Gram eigen-directions: out = F Q_r.
-  int truncate_factor(const T* F, int c, int rkeep, T* out, double* kept, double* dropped) {
+  // Truncate a D x c factor F (ld D) to its top-r Gram eigen-directions: out = F Q_r; F2 (nullable, D x c)
+  // gets the same Q_r: out2 = F2 Q_r (the smoother's kernel-applied carriers).
+  int truncate_factor(const T* F, int c, int rkeep, T* out, double* kept, double* dropped, const T* F2 = nullptr,
+                      T* out2 = nullptr) {
     const size_t pk = prof_begin();
     if constexpr (sizeof(T) == 4) {
       if (use_tc_gemm()) return truncate_factor_tc(reinterpret_cast<const float*>(F), c, rkeep,
-                                                   reinterpret_cast<float*>(out), kept, dropped, pk);
+                                                   reinterpret_cast<float*>(out), kept, dropped, pk,
+                                                   reinterpret_cast<const float*>(F2), reinterpret_cast<float*>(out2));
     }
     // fp64 copy of F (fp32 storage) feeds both the Gram (DSYRK, fp64 tensor cores) and M Q_r (DGEMM)
     const double* Fd = reinterpret_cast<const double*>(F);
@@ -1162,9 +1185,19 @@ struct Impl final : ImplBase {
     if constexpr (sizeof(T) == 4) {
       CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one, Fd, (int)D, QrD, c, &zero, dC, (int)D));
       CK_CUDA((convert<double, float>)((int)D, rkeep, dC, D, reinterpret_cast<float*>(out), D, st));
+      if (F2) {
+        CK_CUDA((convert<float, double>)((int)D, c, reinterpret_cast<const float*>(F2), D, dA, D, st));
+        CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one, dA, (int)D, QrD, c, &zero, dC,
+                            (int)D));
+        CK_CUDA((convert<double, float>)((int)D, rkeep, dC, D, reinterpret_cast<float*>(out2), D, st));
+      }
     } else {
       CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one, Fd, (int)D, QrD, c, &zero,
                           reinterpret_cast<double*>(out), (int)D));
+      if (F2)
+        CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one,
+                            reinterpret_cast<const double*>(F2), (int)D, QrD, c, &zero, reinterpret_cast<double*>(out2),
+                            (int)D));
     }
     prof_end(CAKF_PROF_TRUNC_GEMM, ps);
     prof_end(CAKF_PROF_TRUNCATE, pk);
@@ -1200,6 +1233,8 @@ struct Impl final : ImplBase {
     CK_CUDA(StepKernels<T>::fill(D, T(0), X, st));
     CK_CUDA(StepKernels<T>::fill((size_t)std::max(ST.N, 1), T(0), R, st));
     CK_CUDA(StepKernels<T>::ws_build(ST.N, D, ST.n, 0, ST.idx, X, ST.XV, R, Ws, ws, st));
+    // (I (x) K) of the carriers: [K(X,T) v_T; 0], [K(X,T) V_T; 0] from the stored post-loop products
+    if (!smooth_k2) CK_CUDA(StepKernels<T>::kcar_build(NX, Dp, ST.n, 0, ST.KV, nullptr, nullptr, KWs, Kws, st));
     ST.smoother_rank = q;
     CK(keep_carriers(T_, q));
     for (int k = T_ - 1; k >= 0; --k) {
@@ -1210,9 +1245,16 @@ struct Impl final : ImplBase {
       if (q) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, q, S.A_next, true, Ws, D, X + D, D, st));
       // Sigma_k x = (Sigma^t_k (x) K) x : K applied to all D' blocks of all C columns at once
       size_t pk = prof_begin();
-      CK(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX, cull ? act_cnt_sm : nullptr, act_list_sm,
-            act_stride_sm));
-      ++k2_sm_launches;
+      if (smooth_k2) {
+        CK(k2(coords, (int)NX, coords, (int)NX, X, NX, Dp * C, Yk, NX, cull ? act_cnt_sm : nullptr, act_list_sm,
+              act_stride_sm));
+        ++k2_sm_launches;
+      } else {
+        // (I (x) K) x = (A^T (x) I) (I (x) K)[w^s, W^s]: the carriers' kernel products, kept exactly by
+        // linearity (K (F Q) = (K F) Q, K H^T V t = (K(X,T) V) t), so no kernel is evaluated here
+        CK_CUDA(StepKernels<T>::mix((int)NX, Dp, 1, S.A_next, true, Kws, D, Yk, D, st));
+        if (q) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, q, S.A_next, true, KWs, D, Yk + D, D, st));
+      }
       prof_end(CAKF_PROF_K2_SMOOTH, pk);
       CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, C, S.sig_t, Yk, yb, st));
       const int rin = S.rin, n = S.n, N = S.N;
@@ -1235,12 +1277,20 @@ struct Impl final : ImplBase {
       CK_CUDA(StepKernels<T>::smooth_out(D, C, S.m, S.var, yb, S.ms, S.vs, st));
       // w^s_k, W^s_k = [W_k, (I - W W^T P^-) A^T W^s]   (lines 7-8)
       CK_CUDA(StepKernels<T>::ws_build(n ? N : 0, D, n, q, S.idx, X, S.XV, R, Wf, ws, st));
+      if (!smooth_k2) {
+        // (I (x) K) W^s_full = [[K(X,T) V; 0], Kx[:,1:] - [K(X,T) V t[:,1:]; 0]], same for w^s with column 0
+        pk = prof_begin();
+        if (n) CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)NX, C, n, 1.0, S.KV + NX, (int)NX, tt, n, 0.0, Zk, (int)NX));
+        prof_end(CAKF_PROF_LOWRANK, pk);
+        CK_CUDA(StepKernels<T>::kcar_build(NX, Dp, n, q, S.KV, n ? Zk : nullptr, Yk, KWf, Kws, st));
+      }
       const int qn = n + q;
       if (rcap >= 0 && qn > rcap) {                                   // line 9 (R6)
-        CK(truncate_factor(Wf, qn, rcap, Ws, nullptr, nullptr));
+        CK(truncate_factor(Wf, qn, rcap, Ws, nullptr, nullptr, smooth_k2 ? nullptr : KWf, KWs));
         q = rcap;
       } else {
         std::swap(Wf, Ws);
+        if (!smooth_k2) std::swap(KWf, KWs);
         q = qn;
       }
       S.smoother_rank = q;

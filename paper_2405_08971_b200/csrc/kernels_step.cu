@@ -595,6 +595,29 @@ __global__ void ws_dense_kernel(size_t D, int n, int q, const T* __restrict__ X,
   else if (j <= n) Wf[p + (size_t)(j - 1) * D] = T(0);
   else Wf[p + (size_t)(j - 1) * D] = X[p + (size_t)(j - n) * D];
 }
+// kernel-applied carriers: (I (x) K) of ws_dense + ws_scatter, from K(X,T)[v V] and K(X,T) V t (block 0 only,
+// H = [E_train, 0]); grid (rows of D, 1 + n + q columns)
+template <typename T>
+__global__ void kcar_build_kernel(size_t NX, size_t D, int n, int q, const T* __restrict__ KV, const T* __restrict__ Z,
+                                  const T* __restrict__ Kx, T* __restrict__ KWf, T* __restrict__ Kws) {
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (p >= D) return;
+  const bool b0 = p < NX;
+  if (j == 0) {
+    T v = Kx ? Kx[p] : T(0);
+    if (b0 && n) v += Z ? KV[p] - Z[p] : KV[p];   // n = 0: no observation-space term (as ws_build)
+    Kws[p] = v;
+  } else if (j <= n) {
+    KWf[p + (size_t)(j - 1) * D] = b0 ? KV[p + (size_t)j * NX] : T(0);
+  } else {
+    const int c = j - n;
+    T v = Kx[p + (size_t)c * D];
+    if (b0 && n && Z) v -= Z[p + (size_t)c * NX];
+    KWf[p + (size_t)(j - 1) * D] = v;
+  }
+}
+
 // step 2: scatter the observation-space terms into the train rows of block 0
 template <typename T>
 __global__ void ws_scatter_kernel(int N, size_t D, int n, int q, const int* __restrict__ idx, const T* __restrict__ XV,
@@ -944,6 +967,16 @@ cudaError_t StepKernels<T>::smooth_out(size_t D, int C, const T* m, const T* var
     }
   }
   smooth_out_kernel<T><<<nblk(D), 256, 0, st>>>(D, C, m, varf, y, ms, vs);
+  return note_launch_err();
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::kcar_build(int64_t NX, int Dp, int n, int q, const T* KV, const T* Z, const T* Kx, T* KWf,
+                                       T* Kws, cudaStream_t st) {
+  const size_t D = (size_t)NX * Dp;
+  if (D == 0) return cudaSuccess;
+  if (n && !Z && (Kx || q)) return cudaErrorInvalidValue;
+  kcar_build_kernel<T><<<dim3(nblk(D), 1 + n + q), 256, 0, st>>>((size_t)NX, D, n, q, KV, Z, Kx, KWf, Kws);
   return note_launch_err();
 }
 

@@ -75,6 +75,11 @@ struct StepKernels {
                               cudaStream_t st);
   static cudaError_t sigma_apply(int NX, int Dp, int C, const Mat3& S, const T* Y, T* y, cudaStream_t st);
   static cudaError_t smooth_out(size_t D, int C, const T* m, const T* varf, const T* y, T* ms, T* vs, cudaStream_t st);
+  // kernel-applied smoother carriers: with KV = K(X,T)[v V] (NX x (1+n)), Z = K(X,T) V t (NX x C,
+  // nullable when n = 0), Kx = (I (x) K) x (D x (1+q), nullable at the first step):
+  //   Kws = [KV_0 - Z_0; 0] + Kx_0,  KWf = [[KV_1..n; 0], Kx_1..q - [Z_1..q; 0]]
+  static cudaError_t kcar_build(int64_t NX, int Dp, int n, int q, const T* KV, const T* Z, const T* Kx, T* KWf,
+                                T* Kws, cudaStream_t st);
   static cudaError_t ws_build(int N, size_t D, int n, int q, const int* idx, const T* X, const T* XV, const T* R,
                               T* Wf, T* ws, cudaStream_t st);
   static cudaError_t fill(size_t n, T val, T* out, cudaStream_t st);
