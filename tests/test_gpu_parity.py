@@ -269,3 +269,22 @@ def test_collective_path_world1(monkeypatch, name, dtype, policy, iters, rank):
         compare(wl, "f64", 1e-9, 1e-9)
     else:
         compare_fp32_cancellation(wl)
+
+
+# ------------------------------------------------ kernel-free smoother (DESIGN §6 "Smoother")
+@pytest.mark.parametrize("dtype,policy,iters,rank,tol", [("f64", "cg", 16, 24, 1e-10), ("f64", "random", 8, 12, 1e-10),
+                                                         ("f32", "random", 16, 24, 2e-5)])
+def test_propagated_smoother_equals_direct_k2(monkeypatch, dtype, policy, iters, rank, tol):
+    """The default smoother assembles Sigma_k x from the stored post-loop products K(X,T_k)[v V] by
+    linearity; CAKF_SMOOTH_K2=1 evaluates it with a K2 per step (the paper's order).  Same inputs, same
+    filter: the smoothed means / variances agree to rounding (with truncation: the same Q_r is applied
+    to both carriers), and the smoother ranks are identical."""
+    wl = make_workload("sphere48", policy=policy, max_iter=iters, max_rank=rank, T=5)
+    monkeypatch.setenv("CAKF_SMOOTH_K2", "1")
+    _, _, _, sm_d, sv_d, st_d = run_device(wl, dtype)
+    monkeypatch.delenv("CAKF_SMOOTH_K2")
+    _, _, _, sm_p, sv_p, st_p = run_device(wl, dtype)
+    for k in range(wl.T + 1):
+        assert st_p[k]["smoother_rank"] == st_d[k]["smoother_rank"]
+        assert mean_rel(sm_p[k], sm_d[k]) < tol, (k, mean_rel(sm_p[k], sm_d[k]))
+        assert var_rel(sv_p[k], sv_d[k]) < 10 * tol, (k, var_rel(sv_p[k], sv_d[k]))
