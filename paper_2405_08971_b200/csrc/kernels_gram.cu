@@ -166,6 +166,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
     }
     __syncthreads();
     for (int a = 0; a < na; ++a) {
+      if (!((amask >> (a * SYM_S)) & ((1u << SYM_S) - 1u))) continue;   // no active tile pair in this row tile
       // rows kept negated (d = c - r) as scalars: the packed f32x2 ops broadcast a scalar operand
       float nrx[8], nry[8], nrz[8], rs[8];
       float2 racc2[8];   // per row: even / odd column partial sums
@@ -301,16 +302,31 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
           m4[1] = u1;
         }
       }
-      // row sums over the unit's J tiles: reduce over tx (16 lanes of a half-warp)
+      // row sums over the unit's J tiles: reduce the 8 rows over tx (16 lanes of a half-warp) as a
+      // reduce-scatter (4 + 2 + 1 + 1 shuffles instead of 8 x 4); lane pair (tx, tx ^ 1) ends with row
+      // rsel = 4 (tx>>3 & 1) + 2 (tx>>2 & 1) + (tx>>1 & 1)
+      float v8[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        float v = racc2[r].x + racc2[r].y;
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        if (tx == 0) rowacc[a * SYM_T + ty * 8 + r] += v;
+      for (int r = 0; r < 8; ++r) v8[r] = racc2[r].x + racc2[r].y;
+      const bool h8 = tx & 8, h4 = tx & 4, h2 = tx & 2;
+      float w4[4], w2[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float send = h8 ? v8[i] : v8[i + 4], keep = h8 ? v8[i + 4] : v8[i];
+        w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
       }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float send = h4 ? w4[i] : w4[i + 2], keep = h4 ? w4[i + 2] : w4[i];
+        w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      float w1;
+      {
+        const float send = h2 ? w2[0] : w2[1], keep = h2 ? w2[1] : w2[0];
+        w1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
+      if (!(tx & 1)) rowacc[a * SYM_T + ty * 8 + (h8 ? 4 : 0) + (h4 ? 2 : 0) + (h2 ? 1 : 0)] += w1;
     }
     __syncthreads();
     if (tid == 0 && done_pairs && ulist) atomicAdd(done_pairs, (unsigned long long)s_done);
