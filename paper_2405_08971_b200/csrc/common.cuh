@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace cakf {
 
 // Count of libcakf kernel launches (host side, all handles); read by cakf_kernel_launches().
@@ -21,6 +23,32 @@ inline long long& launch_counter() {
 inline cudaError_t note_launch_err() {
   ++launch_counter();
   return cudaGetLastError();
+}
+
+// Programmatic dependent launch (PDL): the inner-loop kernels are launched with programmatic stream
+// serialisation so that a kernel's CTAs are scheduled while its predecessor drains; each such kernel
+// calls griddep_wait() before touching memory (it returns once the predecessor grid has completed and
+// its writes are visible; a no-op without a programmatic dependency).  CAKF_PDL=0 launches them plainly.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  ++launch_counter();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename T> struct V4t;

@@ -107,6 +107,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
                   const int* __restrict__ ucount, const unsigned short* __restrict__ umask,
                   const float4* __restrict__ sph16, const float4* __restrict__ sphJ, float cut,
                   unsigned* __restrict__ sched) {
+  griddep_wait();   // PDL: the actions (xcs .w) come from the preceding stage kernel
   constexpr int NJS = SUB ? SYM_S * 4 : SYM_S;   // J spheres per unit
   extern __shared__ __align__(16) unsigned char sm_raw[];
   __shared__ float4 s16[SYM_S * 8], s128[NJS];   // this unit's 16-row group / J (sub-)tile spheres
@@ -694,10 +695,9 @@ cudaError_t launch_sym_t(const float4* x, int n, int nt, int nb, float* partial,
     configured = true;
   }
   const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);
-  matvec_sym_kernel<NU2, SUB><<<(unsigned)grid, 256, smem, st>>>(x, n, nt, nb, u_begin, u_end, partial, done_pairs,
-                                                                  ulist, ucount, umask, sph16, sphJ, cut,
-                                                                  use_k1_dyn() ? sched : nullptr);
-  return note_launch_err();
+  return launch_pdl(matvec_sym_kernel<NU2, SUB>, dim3((unsigned)grid), dim3(256), smem, st, x, n, nt, nb, u_begin,
+                    u_end, partial, done_pairs, ulist, ucount, umask, sph16, sphJ, cut,
+                    use_k1_dyn() ? sched : (unsigned*)nullptr);
 }
 
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,

@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(kTile)
 stageA_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const T* __restrict__ lam2,
               const T* __restrict__ s, const T* __restrict__ r, T* __restrict__ gp, const T* __restrict__ HM, int rin,
               double* __restrict__ part, int W, double* __restrict__ red, unsigned* cnt) {
+  griddep_wait();
   __shared__ double scratch[32 * 3];
   const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[3] = {0.0, 0.0, 0.0};  // s.r, s.g', r.r
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(kTile)
 stageB_kernel(int N, const T* __restrict__ HM, int rin, const double* __restrict__ ured, const T* __restrict__ gp,
               const T* __restrict__ s, T* __restrict__ g, const T* __restrict__ V, int nV, double* __restrict__ part,
               int W, double* __restrict__ red, unsigned* cnt, const double* __restrict__ wpre) {
+  griddep_wait();
   extern __shared__ __align__(16) unsigned char sm_raw[];
   double* u = reinterpret_cast<double*>(sm_raw);
   __shared__ double scratch[32];
@@ -308,6 +310,7 @@ stageC_kernel(int N, const T* __restrict__ V, const T* __restrict__ Z, int nV, c
               const T* sin, const T* gin, T* d, T* Gd, const T* __restrict__ s_eta, const double* __restrict__ ared,
               int rin, const double* __restrict__ sgs, double* __restrict__ part, int W, double* __restrict__ red,
               unsigned* cnt, IterCtl* ctl, double eps, int iter, int pass) {
+  griddep_wait();
   extern __shared__ __align__(16) unsigned char sm_raw[];
   double* c = reinterpret_cast<double*>(sm_raw);
   __shared__ double scratch[32];
@@ -358,6 +361,7 @@ __global__ void stageD_kernel(int N, int iter, int niter, const IterCtl* __restr
                               const T* __restrict__ Gd, T* __restrict__ XV, T* __restrict__ Z, T* __restrict__ r,
                               T* __restrict__ s, V4<T>* __restrict__ xcs, int policy, const int* __restrict__ order,
                               uint64_t seed, int k, const int* __restrict__ sigma) {
+  griddep_wait();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= N) return;
   const T gamma = (T)ctl->gamma, isq = (T)ctl->inv_sqrt_eta;
@@ -820,9 +824,8 @@ template <typename T>
 cudaError_t StepKernels<T>::stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s,
                                    const T* r, T* gp, const T* HM, int rin, double* part, int W, double* red,
                                    unsigned* cnt, cudaStream_t st) {
-  stageA_kernel<T><<<stage_blocks(N), kTile, 0, st>>>(N, nch, partial, sig00, lam2, s, r, gp, HM, rin, part, W, red,
-                                                      cnt);
-  return note_launch_err();
+  return launch_pdl(stageA_kernel<T>, dim3(stage_blocks(N)), dim3(kTile), 0, st, N, nch, partial, sig00, lam2, s, r,
+                    gp, HM, rin, part, W, red, cnt);
 }
 
 template <typename T>
@@ -850,9 +853,9 @@ template <typename T>
 cudaError_t StepKernels<T>::stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g,
                                    const T* V, int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st,
                                    const double* wpre) {
-  stageB_kernel<T><<<stage_blocks(N), kTile, wpre ? 8 : sizeof(double) * (rin > 0 ? rin : 1), st>>>(
-      N, HM, rin, ured, gp, s, g, V, nV, part, W, red, cnt, wpre);
-  return note_launch_err();
+  return launch_pdl(stageB_kernel<T>, dim3(stage_blocks(N)), dim3(kTile),
+                    wpre ? 8 : sizeof(double) * (rin > 0 ? rin : 1), st, N, HM, rin, ured, gp, s, g, V, nV, part, W,
+                    red, cnt, wpre);
 }
 
 template <typename T>
@@ -860,18 +863,16 @@ cudaError_t StepKernels<T>::stageC(int N, const T* V, const T* Z, int nV, const 
                                    const T* gin, T* d, T* Gd, const T* s_eta, const double* ared, int rin,
                                    const double* sgs, double* part, int W, double* red, unsigned* cnt, IterCtl* ctl,
                                    double eps, int iter, int pass, cudaStream_t st) {
-  stageC_kernel<T><<<stage_blocks(N), kTile, sizeof(double) * (nV > 0 ? nV : 1), st>>>(
-      N, V, Z, nV, cred, sin, gin, d, Gd, s_eta, ared, rin, sgs, part, W, red, cnt, ctl, eps, iter, pass);
-  return note_launch_err();
+  return launch_pdl(stageC_kernel<T>, dim3(stage_blocks(N)), dim3(kTile), sizeof(double) * (nV > 0 ? nV : 1), st, N,
+                    V, Z, nV, cred, sin, gin, d, Gd, s_eta, ared, rin, sgs, part, W, red, cnt, ctl, eps, iter, pass);
 }
 
 template <typename T>
 cudaError_t StepKernels<T>::stageD(int N, int iter, int niter, const IterCtl* ctl, const T* d, const T* Gd, T* XV,
                                    T* Z, T* r, T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k,
                                    const int* sigma, cudaStream_t st) {
-  stageD_kernel<T><<<nblk(N), 256, 0, st>>>(N, iter, niter, ctl, d, Gd, XV, Z, r, s, xcs, policy, order, seed, k,
-                                            sigma);
-  return note_launch_err();
+  return launch_pdl(stageD_kernel<T>, dim3(nblk(N)), dim3(256), 0, st, N, iter, niter, ctl, d, Gd, XV, Z, r, s, xcs,
+                    policy, order, seed, k, sigma);
 }
 
 template <typename T>
@@ -1135,4 +1136,15 @@ cudaError_t idx64_to32(int n, const int64_t* in, int* out, cudaStream_t st) {
 template struct StepKernels<float>;
 template struct StepKernels<double>;
 
+}  // namespace cakf
+
+namespace cakf {
+bool pdl_enabled() {   // CAKF_PDL=0: plain launches for the inner-loop kernels
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAKF_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 }  // namespace cakf
