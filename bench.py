@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true", help="skip the reference timing with culling off")
     ap.add_argument("--no-interp", action="store_true", help="skip the temporal-interpolation query timing")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--serving", type=int, default=2,
+                    help="also time P independent problems per GPU on P streams (reported as 'serving'; <2: skip)")
     ap.add_argument("--T", type=int, default=None, help="override T (debug only; invalidates the metric)")
     return ap.parse_args()
 
@@ -453,6 +455,46 @@ def main():
         out["sampler_ms_per_call"] = dict(smp, samples=S, note="cakf_sample: S joint samples of the T+1 states "
                                           "(device buffers; standard-normal draws for timing)")
         hi.destroy()
+    if world == 1 and args.serving > 1:
+        # serving mode: P independent problems per GPU, one handle + stream + host thread each, so one
+        # problem's latency-bound phases (truncation eigensolver, CG stage reductions) are filled by
+        # another's K1 (scripts/concurrent_bench.py; tests/test_gpu_concurrent.py)
+        import threading
+        P = args.serving
+        sts = [torch.cuda.Stream() for _ in range(P)]
+        hs = [runner.make_handle(wl, args.dtype, stream=s.cuda_stream, cull_zero=not args.no_cull) for s in sts]
+
+        def drive(p, n):
+            for _ in range(n):
+                runner.run(hs[p], trans, inputs, smooth=True)
+
+        def run_all(n):
+            ths = [threading.Thread(target=drive, args=(p, n)) for p in range(P)]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+
+        run_all(1)
+        barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for s in sts:
+            s.wait_event(c0)
+        run_all(args.steps)
+        for s in sts:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            stream.wait_event(ev)
+        c1.record(stream)
+        barrier()
+        cms = c0.elapsed_time(c1)
+        out["serving"] = {"problems_per_gpu": P, "value": P * args.steps * wl.T / (cms / 1e3), "unit": "time-steps/s",
+                          "ms_per_pass_per_problem": cms / args.steps, "steps": args.steps, "warmup": 1,
+                          "note": "independent problems (same workload, device-resident inputs), one stream + host "
+                                  "thread each, CUDA events bracketing all streams; no profiling events"}
+        for x in hs:
+            x.destroy()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = oracle_sample(wl)
         out["cpu_baseline"] = {"value": 1.0 / smp["sec_per_timestep"], "unit": "time-steps/s",
