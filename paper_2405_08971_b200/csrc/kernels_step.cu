@@ -215,6 +215,15 @@ stageA_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const
   if (row < r1) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     int c = 0;
+    // 32 loads in flight per thread, then one 16-batch and the scalar tail: each acc[j] sees
+    // partial[c + j], partial[c + j + 4], ... in the same order as with 16-batches alone
+    for (; c + 32 <= nch; c += 32) {
+      T x[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) x[q] = partial[(size_t)(c + q) * N + row];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q & 3] += (double)x[q];
+    }
     for (; c + 16 <= nch; c += 16) {
       T x[16];
 #pragma unroll

@@ -2,7 +2,7 @@
 # A/B of env-selected variants on the cfg3 bench (no dense / interp / cpu legs): ab.sh "ENV=.. ENV2=.." ...
 mkdir -p gpurun_out
 for v in "$@"; do
-  env $v python bench.py --no-dense --no-interp --no-cpu-baseline --e2e-steps 0 > gpurun_out/ab.json 2> gpurun_out/ab.err
+  env $v python bench.py --no-dense --no-interp --no-cpu-baseline --e2e-steps 0 --serving 0 > gpurun_out/ab.json 2> gpurun_out/ab.err
   python - "$v" <<'PY'
 import json, sys
 try:
