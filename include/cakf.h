@@ -233,6 +233,16 @@ int cakf_interpolate(cakf_t h, int32_t k, const double* A1, const double* Q1, co
 int cakf_sample(cakf_t h, int32_t n_samples, const void* x0, const void* q, const void* eps, int32_t which,
                 void* out);
 
+/* Test entry point: the inner loop's kernel matvec (a4's K_TT s) launched
+ * exactly as cakf_update launches it — the per-update kd order of the observed points, the
+ * exact-zero culling lists, the symmetric tile-pair kernel with its dynamic unit scheduler and
+ * partial slots — for one vector:  out[j] = sum_l Matern(|x_{obs[j]} - x_{obs[l]}| / ell) s[l].
+ * obs_idx (n_obs spatial indices, int64), s and out (n_obs, handle dtype) in the caller's
+ * observation order, host or device.  Call between steps (not between predict and update); it
+ * overwrites the inner-loop workspaces only.  Synchronises.
+ * Errors: CAKF_E_ARG (NULL, n_obs outside [1, max_obs], index out of range), CAKF_E_STATE, CAKF_E_CUDA. */
+int cakf_debug_matvec(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* s, void* out);
+
 /* Exact-zero culling statistics of the handle so far: frac3[0] = fraction of the symmetric K1's
  * pairs evaluated (counted in 16 x 128 warp blocks of its 128 x 128 tile pairs), frac3[1] = fraction of the post-loop K2's 128x32 tiles evaluated,
  * frac3[2] = same for the smoother's K2 (all 1.0 when culling is off).  Synchronises the handle's

@@ -36,9 +36,15 @@ def gram_apply(Xr, Xc, B, nu, ell, chunk=1024, rows=None):
 
 
 class MFModel:
-    """Kronecker LGSSM accessed only through products (Lemma B.1)."""
+    """Kronecker LGSSM accessed only through products (Lemma B.1).
 
-    def __init__(self, wl, dtype_round=None, chunk=1024):
+    cache=True keeps the kernel matrices K(X_T, X_T), K(X, X_T) (per observation set) and
+    K(X, X) once generated instead of regenerating their rows for every product: the same
+    entries (``matern(cdist(.)/ell)``, as in ``gram_apply``) and the same products, only
+    stored — for D ~ 1e4 parity runs (cfg2) where regenerating rows dominates the oracle's time.
+    """
+
+    def __init__(self, wl, dtype_round=None, chunk=1024, cache=False):
         X = wl.coords
         self.ys, self.nvs = wl.y, wl.noise_var
         if dtype_round is not None:
@@ -61,6 +67,35 @@ class MFModel:
         self.Dp = Sinf.shape[0]
         self.D = self.Dp * self.NX
         self.T = len(self.At)
+        self.cache = cache
+        self._K = {}
+
+    def _kmat(self, key, Xr, Xc):
+        if key not in self._K:
+            self._K[key] = matern(self.nu, cdist(Xr, Xc) / self.ell)
+        return self._K[key]
+
+    def _obs_key(self, k):
+        return self.idx[k - 1].tobytes()
+
+    def ktt_apply(self, k, x):
+        """K(X_T, X_T) x for the observed points of step k."""
+        Xt = self.X[self.idx[k - 1]]
+        if self.cache:
+            return self._kmat(("TT", self._obs_key(k)), Xt, Xt) @ x
+        return gram_apply(Xt, Xt, x, self.nu, self.ell, self.chunk)
+
+    def kxt_apply(self, k, Vm):
+        """K(X, X_T) Vm for the observed points of step k."""
+        Xt = self.X[self.idx[k - 1]]
+        if self.cache:
+            return self._kmat(("XT", self._obs_key(k)), self.X, Xt) @ Vm
+        return gram_apply(self.X, Xt, Vm, self.nu, self.ell, self.chunk)
+
+    def kxx_apply(self, B):
+        if self.cache:
+            return self._kmat("XX", self.X, self.X) @ B
+        return gram_apply(self.X, self.X, B, self.nu, self.ell, self.chunk)
 
     def blocks(self, Xm):
         return Xm.reshape(self.Dp, self.NX, -1)
@@ -68,14 +103,14 @@ class MFModel:
     def sigma_apply(self, k, Xm):
         """(Sigma^t_k (x) K) Xm for Xm of shape D x m."""
         Bl = self.blocks(Xm)
-        KB = [gram_apply(self.X, self.X, Bl[e], self.nu, self.ell, self.chunk) for e in range(self.Dp)]
+        KB = [self.kxx_apply(Bl[e]) for e in range(self.Dp)]
         S = self.St[k]
         out = [sum(S[d, e] * KB[e] for e in range(self.Dp)) for d in range(self.Dp)]
         return np.concatenate(out, axis=0)
 
     def sigma_HT_apply(self, k, Vm):
         """Sigma_k H^T Vm (Vm: N x m): only the kernel columns of observed points."""
-        Kx = gram_apply(self.X, self.X[self.idx[k - 1]], Vm, self.nu, self.ell, self.chunk)
+        Kx = self.kxt_apply(k, Vm)
         S = self.St[k]
         return np.concatenate([S[d, 0] * Kx for d in range(self.Dp)], axis=0)
 
@@ -101,13 +136,12 @@ def _truncate(M, r):
 def update_mf(mm: MFModel, k, m_pred, M_pred, policy, max_iter, eps=np.finfo(np.float64).eps, cgs2=True):
     """alg:update_pls with matrix-free G s = sig00 K_TT s - HM (HM^T s) + Lambda s."""
     idx = mm.idx[k - 1]
-    Xt = mm.X[idx]
     y, lam = mm.ys[k - 1], mm.nvs[k - 1]
     HM = M_pred[idx]
     s00 = mm.St[k][0, 0]
 
     def G(x):
-        return s00 * gram_apply(Xt, Xt, x, mm.nu, mm.ell, mm.chunk) - HM @ (HM.T @ x) + lam * x
+        return s00 * mm.ktt_apply(k, x) - HM @ (HM.T @ x) + lam * x
 
     N = len(y)
     v = np.zeros(N)
@@ -136,10 +170,15 @@ def update_mf(mm: MFModel, k, m_pred, M_pred, policy, max_iter, eps=np.finfo(np.
     return m, M, v, V
 
 
-def run_mf(wl, dtype_round=None, smoother=True, chunk=1024):
-    """Full CAKF (+ CAKS) through matrix-free products; returns per-step means/variances."""
+def run_mf(wl, dtype_round=None, smoother=True, chunk=1024, cache=False, perturb_y=0.0):
+    """Full CAKF (+ CAKS) through matrix-free products; returns per-step means/variances.
+
+    perturb_y: relative perturbation y <- y (1 + perturb_y) of every observation (the oracle's own
+    input sensitivity, used to judge trajectory-sensitive comparisons such as fp64 CG at cfg2)."""
     from .cakf import make_policy
-    mm = MFModel(wl, dtype_round, chunk)
+    mm = MFModel(wl, dtype_round, chunk, cache=cache)
+    if perturb_y:
+        mm.ys = [y * (1.0 + perturb_y) for y in mm.ys]
     pol = make_policy(wl.policy, wl.coord_order, wl.action_seed)
     D = mm.D
     m = np.zeros(D)

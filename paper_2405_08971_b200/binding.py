@@ -61,7 +61,7 @@ EXPORTS = [
     "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
     "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats", "cakf_interpolate", "cakf_sample",
-    "cakf_lowrank_gemm",
+    "cakf_lowrank_gemm", "cakf_debug_matvec",
 ]
 PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank", "trunc_gram",
                    "trunc_eig", "trunc_gemm"]
@@ -99,6 +99,7 @@ def load(path: str = LIB_PATH):
     lib.cakf_nccl_unique_id.argtypes = [vp]
     lib.cakf_shard_plan.argtypes = [i64, i64, i32, i32, vp]
     lib.cakf_cull_stats.argtypes = [vp, vp]
+    lib.cakf_debug_matvec.argtypes = [vp, i64, vp, vp, vp]
     lib.cakf_interpolate.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp]
     lib.cakf_sample.argtypes = [vp, i32, vp, vp, vp, i32, vp]
     lib.cakf_sym_unit_blocks.argtypes = [i64, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
@@ -326,6 +327,14 @@ class Cakf:
         _check(self.lib.cakf_sample(self.h, int(S), x0f.ctypes.data, qf.ctypes.data, ef.ctypes.data, int(which),
                                     out.ctypes.data))
         return out.reshape(T + 1, S, self.D).transpose(0, 2, 1)
+
+    def debug_matvec(self, obs_idx, s):
+        """K(X_obs, X_obs) s through the inner loop's own K1 launch path (cakf_debug_matvec); numpy in/out."""
+        idx = np.ascontiguousarray(obs_idx, dtype=np.int64)
+        sv = np.ascontiguousarray(s, dtype=self.np_dtype)
+        out = np.empty(len(idx), dtype=self.np_dtype)
+        _check(self.lib.cakf_debug_matvec(self.h, len(idx), idx.ctypes.data, sv.ctypes.data, out.ctypes.data))
+        return out
 
     def cull_stats(self) -> dict:
         """Fractions of the dense kernel work evaluated under exact-zero culling (1.0 = none culled)."""

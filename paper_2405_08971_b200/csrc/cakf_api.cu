@@ -193,6 +193,7 @@ struct ImplBase {
   virtual int interpolate(int k, const double* A1, const double* Q1, const double* A2, int which, void* mean,
                           void* var) = 0;
   virtual int sample(int S, const void* x0, const void* q, const void* eps, int which, void* out) = 0;
+  virtual int debug_matvec(int64_t n, const int64_t* idx, const void* s, void* out) = 0;
 };
 
 template <typename T>
@@ -689,6 +690,9 @@ struct Impl final : ImplBase {
     }
     // size pass, then workspace query, then the real allocation
     layout();
+    // the stage kernels keep one fp64 per kept column / previous action in (default, <= 48 KB) dynamic smem
+    if (std::max(rin_max, nhat) > 6144)
+      return fail(CAKF_E_UNSUPPORTED, "max_rank (or (T-1) max_iter without a cap) and max_iter must be <= 6144");
     if (rcap >= 0 && cmax > 0) {
       CK_SOLVER(cusolverDnDsyevd_bufferSize(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, cmax, nullptr, cmax,
                                             nullptr, &lwork));
@@ -805,6 +809,91 @@ struct Impl final : ImplBase {
     return CAKF_OK;
   }
 
+  // Observations in the internal point order of this update: idx_out (kd order over the observed points),
+  // sigma[j] = the user's position of row j, sigma_inv its inverse.  An update whose obs_idx equals the
+  // previous one's reuses the cached order (a pure function of obs_idx, so bit-identical).
+  int stage_obs(int N, const int64_t* obs_idx, int* idx_out) {
+    CK_CUDA(cudaMemcpyAsync(stage64, obs_idx, (size_t)N * sizeof(int64_t), cudaMemcpyDefault, st));
+    const bool obs_host = !is_device_ptr(obs_idx);
+    bool same_obs = false;
+    if (obs_cache_n == N) {   // same observation set as the cached update (ERA5-style fixed stations)
+      if (obs_host && obs_cache_h.size() == (size_t)N) {
+        same_obs = std::memcmp(obs_idx, obs_cache_h.data(), (size_t)N * sizeof(int64_t)) == 0;
+      } else {
+        CK_CUDA(obs_neq(N, stage64, obs_cache_d, neq_d, st));
+        CK_CUDA(cudaMemcpyAsync(neq_h, neq_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK_CUDA(cudaStreamSynchronize(st));
+        same_obs = *neq_h == 0;
+      }
+    }
+    if (same_obs) {
+      CK_CUDA(cudaMemcpyAsync(idx_out, idx_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(sigma, sig_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(sigma_inv, siginv_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    } else {
+      if (kd_obs) {   // internal order, then the per-update kd order over the observed points
+        CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, sigma_inv, st));
+        CK_CUDA(kd_obs_order<T>(N, idx_tmp, coords, sigma, sigma_inv, idx_out, sig_tmp, kd_ws, kd_ws_bytes, st));
+      } else {
+        CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, idx_out, sigma, sigma_inv, st));
+      }
+      CK_CUDA(cudaMemcpyAsync(idx_cache, idx_out, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(sig_cache, sigma, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(siginv_cache, sigma_inv, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      CK_CUDA(cudaMemcpyAsync(obs_cache_d, stage64, (size_t)N * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      if (obs_host) obs_cache_h.assign(obs_idx, obs_idx + N);
+      else obs_cache_h.clear();
+      obs_cache_n = N;
+    }
+    return CAKF_OK;
+  }
+
+  // K1 exactly as the inner loop launches it (observation order, exact-zero culling lists, dynamic unit
+  // scheduler, symmetric partial slots), for one user vector s: out = K(X_obs, X_obs) s in the user's
+  // observation order.  Test entry point (cakf_debug_matvec); clobbers the inner-loop workspaces.
+  int debug_matvec(int64_t n_obs, const int64_t* obs_idx, const void* s_user, void* out_user) override {
+    if (phase == 1) return fail(CAKF_E_STATE, "debug_matvec: not between predict and update");
+    if (n_obs < 1 || n_obs > Nmax || !obs_idx || !s_user || !out_user) return fail(CAKF_E_ARG, "debug_matvec: bad argument");
+    const int N = (int)n_obs;
+    if (!is_device_ptr(obs_idx))
+      for (int i = 0; i < N; ++i)
+        if (obs_idx[i] < 0 || obs_idx[i] >= NX) return fail(CAKF_E_ARG, "debug_matvec: obs_idx out of range");
+    int* idx = sig_st;   // scratch index list: the sampler's per-step slot 0 (step 0 is never observed)
+    CK(stage_obs(N, obs_idx, idx));
+    CK_CUDA(cudaMemcpyAsync(ybuf_user, s_user, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
+    CK_CUDA(gather_vec<T>(N, sigma, ybuf_user, ybuf, st));
+    CK_CUDA(sampler_ops<T>::gather_coords(N, idx, coords, xcs, st));
+    CK_CUDA(set_w<T>(N, ybuf, xcs, st));
+    const bool sym = sizeof(T) == 4 && use_sym_k1();
+    const int nch = sym ? matvec_sym_tiles(N)
+                        : std::max(1, std::min<int>(matvec_chunks(N, N, sizeof(T)), (int)(partial_cap / N)));
+    if constexpr (sizeof(T) == 4) {
+      if (sym) {
+        if (cull) {
+          const float4* xf = reinterpret_cast<const float4*>(xcs);
+          CK_CUDA(launch_tile_spheres(xf, N, 128, sph_o128, st));
+          CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st));
+          CK_CUDA(launch_tile_spheres(xf, N, 16, sph_o16, st));
+          const long long U = matvec_sym_units(N);
+          CK_CUDA(launch_k1_active_units(sph_o128, N, 0, U, kCullCut, k1_list, k1_mask, k1_count, st));
+          CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)matvec_sym_tiles(N) * N * sizeof(T), st));
+        }
+        CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial), 0,
+                                  matvec_sym_units(N), st, nullptr, cull ? k1_list : nullptr, k1_count, k1_mask,
+                                  sph_o16, sph_o128, sph_o32, kCullCut, k1_sched));
+      } else {
+        CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
+      }
+    } else {
+      CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
+    }
+    CK_CUDA(launch_sum_partials<T>(N, nch, partial, 1.0, r, st));
+    CK_CUDA(scatter_vec<T>(N, sigma, r, ybuf_user, st));
+    CK_CUDA(cudaMemcpyAsync(out_user, ybuf_user, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+    return CAKF_OK;
+  }
+
   int update(int64_t n_obs, const int64_t* obs_idx, const void* y, const void* noise_var,
              const int64_t* coord_order) override {
     if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
@@ -839,39 +928,7 @@ struct Impl final : ImplBase {
     S.n = niter;
     S.missing = false;
     // ---- stage inputs (host or device pointers)
-    // observations in internal point order: S.idx ascending, sigma[j] = the user's position
-    CK_CUDA(cudaMemcpyAsync(stage64, obs_idx, (size_t)N * sizeof(int64_t), cudaMemcpyDefault, st));
-    const bool obs_host = !is_device_ptr(obs_idx);
-    bool same_obs = false;
-    if (obs_cache_n == N) {   // same observation set as the cached update (ERA5-style fixed stations)
-      if (obs_host && obs_cache_h.size() == (size_t)N) {
-        same_obs = std::memcmp(obs_idx, obs_cache_h.data(), (size_t)N * sizeof(int64_t)) == 0;
-      } else {
-        CK_CUDA(obs_neq(N, stage64, obs_cache_d, neq_d, st));
-        CK_CUDA(cudaMemcpyAsync(neq_h, neq_d, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK_CUDA(cudaStreamSynchronize(st));
-        same_obs = *neq_h == 0;
-      }
-    }
-    if (same_obs) {
-      CK_CUDA(cudaMemcpyAsync(S.idx, idx_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(sigma, sig_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(sigma_inv, siginv_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-    } else {
-      if (kd_obs) {   // internal order, then the per-update kd order over the observed points
-        CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, sigma_inv, st));
-        CK_CUDA(kd_obs_order<T>(N, idx_tmp, coords, sigma, sigma_inv, S.idx, sig_tmp, kd_ws, kd_ws_bytes, st));
-      } else {
-        CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, S.idx, sigma, sigma_inv, st));
-      }
-      CK_CUDA(cudaMemcpyAsync(idx_cache, S.idx, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(sig_cache, sigma, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(siginv_cache, sigma_inv, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(obs_cache_d, stage64, (size_t)N * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-      if (obs_host) obs_cache_h.assign(obs_idx, obs_idx + N);
-      else obs_cache_h.clear();
-      obs_cache_n = N;
-    }
+    CK(stage_obs(N, obs_idx, S.idx));
     CK_CUDA(cudaMemcpyAsync(ybuf_user, y, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
     CK_CUDA(cudaMemcpyAsync(lam2_user, noise_var, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
     CK_CUDA(gather_vec<T>(N, sigma, ybuf_user, ybuf, st));
@@ -1585,7 +1642,23 @@ struct Impl final : ImplBase {
 
 struct cakf_s {
   ImplBase* impl = nullptr;
+  int device = -1;   // CUDA device current at cakf_create; every entry point runs on it
 };
+
+namespace {
+// Scoped current-device switch: a handle may be driven from a host thread whose current device differs
+// from the one it was created on (serving mode); restores the caller's device on exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int cur = -1;
+    if (dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
 
 extern "C" {
 
@@ -1618,12 +1691,14 @@ int cakf_create(const cakf_config* cfg, cakf_t* out) {
   }
   cakf_s* h = new cakf_s;
   h->impl = impl;
+  cudaGetDevice(&h->device);
   *out = h;
   return CAKF_OK;
 }
 
-#define HANDLE_CHECK(h) \
-  if (!(h) || !(h)->impl) return fail(CAKF_E_ARG, "NULL handle")
+#define HANDLE_CHECK(h)                                          \
+  if (!(h) || !(h)->impl) return fail(CAKF_E_ARG, "NULL handle"); \
+  DeviceGuard device_guard_((h)->device)
 
 int cakf_reset(cakf_t h) { HANDLE_CHECK(h); return h->impl->reset(); }
 int cakf_predict(cakf_t h, const double* A_t, const double* Q_t, const void* b) {
@@ -1656,7 +1731,7 @@ int cakf_profile_read(cakf_t h, double* ms, int64_t* launches, int32_t reset) {
   HANDLE_CHECK(h);
   return h->impl->prof_read(ms, launches, reset != 0);
 }
-int64_t cakf_kernel_launches(void) { return (int64_t)launch_counter(); }
+int64_t cakf_kernel_launches(void) { return (int64_t)launch_counter().load(); }
 int cakf_interpolate(cakf_t h, int32_t k, const double* A1, const double* Q1, const double* A2, int32_t which,
                      void* mean_D, void* var_D) {
   HANDLE_CHECK(h);
@@ -1666,6 +1741,10 @@ int cakf_sample(cakf_t h, int32_t n_samples, const void* x0, const void* q, cons
                 void* out) {
   HANDLE_CHECK(h);
   return h->impl->sample(n_samples, x0, q, eps, which, out);
+}
+int cakf_debug_matvec(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* s, void* out) {
+  HANDLE_CHECK(h);
+  return h->impl->debug_matvec(n_obs, obs_idx, s, out);
 }
 int cakf_cull_stats(cakf_t h, double* frac3) {
   HANDLE_CHECK(h);
@@ -1712,6 +1791,7 @@ int cakf_sym_unit_blocks(int64_t n_obs, int64_t u, int32_t* bi_out, int32_t* bj_
 }
 int cakf_destroy(cakf_t h) {
   if (!h) return CAKF_OK;
+  DeviceGuard device_guard_(h->device);
   delete h->impl;
   delete h;
   return CAKF_OK;

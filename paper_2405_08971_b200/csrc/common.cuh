@@ -11,14 +11,49 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <cstdlib>
+#include <mutex>
 #include <utility>
 
 namespace cakf {
 
-// Count of libcakf kernel launches (host side, all handles); read by cakf_kernel_launches().
-inline long long& launch_counter() {
-  static long long n = 0;
+// Count of libcakf kernel launches (host side, all handles and host threads); read by
+// cakf_kernel_launches().
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> n{0};
   return n;
+}
+
+// One-time setup per (call site, CUDA device), thread-safe: handles on different host threads (serving
+// mode) may make their first calls concurrently, and function attributes are per device context.
+struct PerDeviceOnce {
+  static constexpr int kMaxDev = 64;
+  std::once_flag flag[kMaxDev];
+  cudaError_t result[kMaxDev] = {};
+};
+template <typename F>
+inline cudaError_t once_per_device(PerDeviceOnce& o, F&& f) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= PerDeviceOnce::kMaxDev) dev = 0;
+  std::call_once(o.flag[dev], [&] { o.result[dev] = f(); });
+  return o.result[dev];
+}
+// SM count of the first device queried (one GPU model per process), thread-safe
+inline int num_sms() {
+  static const int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+// Environment switch read once (thread-safe magic static at each call site): true iff the variable is set
+// and its first character equals `on`.
+inline bool env_is(const char* name, char on) {
+  const char* e = std::getenv(name);
+  return e && e[0] == on;
 }
 inline cudaError_t note_launch_err() {
   ++launch_counter();

@@ -48,16 +48,7 @@ constexpr int I_APLANE = I_BM * I_BK;         // 8 KB
 constexpr int I_SMEM_BUDGET = 220 * 1024;
 static_assert((long long)I_S * 127 * 127 * I_KC < (1ll << 31), "int32 accumulators must stay exact");
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sm_count() { return num_sms(); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -85,14 +76,26 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 
 // Chunk exponents, stored offset by kExpBias (0 = all-zero chunk): e = ilogb(max |src(r, k)|) + 1 over
 // chunk c, so 2^e > max.  Blocks reduce a tile and atomicMax the encoded value (order-independent).
+// A chunk holding a NaN or an Inf gets the reserved code kExpNaN (the largest, so atomicMax keeps it): its
+// slices are written as zeros and every output that reads the chunk is NaN, so non-finite factors
+// propagate instead of being sliced into finite garbage.
 constexpr int kExpBias = 512;
+constexpr int kExpNaN = 2 * kExpBias + 1;
 __device__ __forceinline__ int enc_exp(float m) {
+  if (!(m <= 3.402823466e38f)) return kExpNaN;   // Inf (NaN was mapped to Inf by nonfinite_abs)
   return m > 0.f ? min(max(ilogbf(m) + 1 + kExpBias, 1), 2 * kExpBias) : 0;
 }
 __device__ __forceinline__ int enc_exp(double m) {
+  if (!(m <= 1.7976931348623157e308)) return kExpNaN;
   return m > 0.0 ? min(max(ilogb(m) + 1 + kExpBias, 1), 2 * kExpBias) : 0;
 }
 __device__ __forceinline__ int dec_exp(int v) { return v ? v - kExpBias : 0; }
+// |x| with NaN mapped to +Inf (fmax would drop a NaN)
+template <typename Src>
+__device__ __forceinline__ Src nonfinite_abs(Src x) {
+  const Src a = fabs(x);
+  return a == a ? a : Src(INFINITY);
+}
 
 // K-major, SWIZZLE_64B smem descriptor (8-row groups 512 B apart, sm_100 version 1)
 __device__ __forceinline__ uint64_t sdesc_sw64(uint32_t addr) {
@@ -273,7 +276,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int lc = c - c0;
         mbar_wait(smem_u32(done), gc & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int ea = row < M ? dec_exp(expA[(size_t)row * nchunk + c]) : 0;
+        const int codeA = row < M ? expA[(size_t)row * nchunk + c] : 0;
+        const int ea = dec_exp(codeA);
         for (int cb = 0; cb < ntile; cb += 16) {
           uint32_t r[I_S][16];
           const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
@@ -290,8 +294,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 long long V = (int)r[0][t];
 #pragma unroll
                 for (int L = 1; L < I_S; ++L) V = (V << 7) + (long long)(int)r[L][t];
-                const int ex2 = ea + dec_exp(expB[(size_t)n * nchunk + c]) - 7 * (I_S + 1);
-                const double v = (double)V * __longlong_as_double((long long)(ex2 + 1023) << 52);
+                const int codeB = expB[(size_t)n * nchunk + c];
+                const int ex2 = ea + dec_exp(codeB) - 7 * (I_S + 1);
+                double v = (double)V * __longlong_as_double((long long)(ex2 + 1023) << 52);
+                if (codeA == kExpNaN || codeB == kExpNaN) v = __longlong_as_double(0x7ff8000000000000ll);
                 if (direct) {
                   if (Cd) {
                     double* p = Cd + row + (size_t)n * ldc;
@@ -341,7 +347,7 @@ __global__ void i8_exps_kc_kernel(const Src* __restrict__ src, int R, int K, siz
   __shared__ Src red[8];
   const int r = blockIdx.x, k0 = blockIdx.y * 2048;
   Src m = 0;
-  for (int k = k0 + threadIdx.x; k < min(K, k0 + 2048); k += 256) m = fmax(m, fabs(src[k + (size_t)r * ld]));
+  for (int k = k0 + threadIdx.x; k < min(K, k0 + 2048); k += 256) m = fmax(m, nonfinite_abs(src[k + (size_t)r * ld]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -360,7 +366,7 @@ __global__ void i8_exps_rc_kernel(const Src* __restrict__ src, int R, int K, siz
   const int r = blockIdx.x * blockDim.x + threadIdx.x, k0 = blockIdx.y * 64;
   if (r >= R) return;
   Src m = 0;
-  for (int k = k0; k < min(K, k0 + 64); ++k) m = fmax(m, fabs(src[r + (size_t)k * ld]));
+  for (int k = k0; k < min(K, k0 + 64); ++k) m = fmax(m, nonfinite_abs(src[r + (size_t)k * ld]));
   const int e = enc_exp(m);
   if (e) atomicMax(&ex[(size_t)r * nchunk + k0 / I_KC], e);
 }
@@ -388,8 +394,15 @@ __global__ void i8_planes_kernel(const Src* __restrict__ src, int R, int K, int 
   for (int i = 0; i < 4; ++i) {
     const int r = r0 + ty + 8 * i;
     if (r >= R) continue;
-    const int e = dec_exp(ex[(size_t)r * nchunk + min(k, K - 1) / I_KC]);   // 4 k never straddle a chunk
+    const int code = ex[(size_t)r * nchunk + min(k, K - 1) / I_KC];   // 4 k never straddle a chunk
+    const int e = dec_exp(code);
     uint32_t word[I_S] = {};
+    if (code == kExpNaN) {   // non-finite chunk: zero slices, the epilogue writes NaN
+      const size_t o = (size_t)r * Kp + k;
+#pragma unroll
+      for (int s_ = 0; s_ < I_S; ++s_) *reinterpret_cast<uint32_t*>(planes + s_ * plane + o) = 0u;
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       Src v;
@@ -412,14 +425,14 @@ __global__ void i8_planes_kernel(const Src* __restrict__ src, int R, int K, int 
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -475,11 +488,12 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
   const uint32_t stage_bytes = ((uint32_t)I_S * I_APLANE + (uint32_t)I_S * ntile * I_BK + 1023u) & ~1023u;
   const int stages = std::max(2, std::min(6, (int)((I_SMEM_BUDGET - 1024 - 256) / stage_bytes)));
   const size_t smem = (size_t)stages * stage_bytes + 1024 + 256;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I_SMEM_BUDGET);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = once_per_device(once, [] {
+      return cudaFuncSetAttribute(gemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I_SMEM_BUDGET);
+    });
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   // one work item per (tile, chunk) when the fp64 partials fit (the persistent CTAs then balance many
   // small items), else whole chunks grouped per split; every chunk count >= 2 goes through work
@@ -511,12 +525,8 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
 }
 
 bool use_i8_gemm() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_GEMM_F64");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = !env_is("CAKF_GEMM_F64", '1');
+  return v;
 }
 
 }  // namespace cakf

@@ -36,16 +36,7 @@ constexpr int G_THREADS = 192;           // loader, MMA, 4 epilogue warps
 constexpr int G_APLANE = G_BM * G_BK * 2;   // 8 KB
 constexpr int G_SMEM_BUDGET = 220 * 1024;
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sm_count() { return num_sms(); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -296,14 +287,14 @@ __global__ void splitk_reduce_kernel(int M, int N, int S, const float* __restric
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -348,11 +339,12 @@ cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, in
   const uint32_t stage_bytes = ((3u * G_APLANE + 3u * (uint32_t)ntile * G_BK * 2) + 1023u) & ~1023u;
   const int stages = std::max(2, std::min(6, (int)((G_SMEM_BUDGET - 1024 - 256) / stage_bytes)));
   const size_t smem = (size_t)stages * stage_bytes + 1024 + 256;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BUDGET);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = once_per_device(once, [] {
+      return cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BUDGET);
+    });
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   // split K until the grid covers the SMs (each split keeps >= 8 K blocks), fp64 output always reduces
   const int tiles = mt * ntiles;
@@ -378,12 +370,8 @@ cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, in
 }
 
 bool use_tc_gemm() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_GEMM_F64");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = !env_is("CAKF_GEMM_F64", '1');
+  return v;
 }
 
 }  // namespace cakf

@@ -16,16 +16,6 @@ namespace cakf {
 
 namespace {
 
-int g_num_sms = 0;
-int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
 
 template <typename T> constexpr int kRowsPerThread = sizeof(T) == 4 ? 4 : 2;
 constexpr int kMvThreads = 256;
@@ -584,12 +574,8 @@ template cudaError_t launch_kernel_columns<double>(int, const V4<double>*, int, 
 int matvec_sym_tiles(int n) { return ((n + SYM_T - 1) / SYM_T + SYM_S - 1) / SYM_S; }   // = partials per row
 
 bool use_sym_k1() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_K1_DENSE");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = !env_is("CAKF_K1_DENSE", '1');
+  return v;
 }
 
 int matvec_sym_block_points() { return SYM_S * SYM_T; }
@@ -658,21 +644,13 @@ cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, lon
 }
 
 bool use_k1_dyn() {   // CAKF_K1_DYN=0: static strided unit assignment instead of the global work counter
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_K1_DYN");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = !env_is("CAKF_K1_DYN", '0');
+  return v;
 }
 
 bool use_k1_sub() {   // CAKF_K1_SUB=0: exact-zero test per 128-column J tile instead of per 32-column sub-tile
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_K1_SUB");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = !env_is("CAKF_K1_SUB", '0');
+  return v;
 }
 
 template <int NU2, bool SUB>
@@ -680,20 +658,31 @@ cudaError_t launch_sym_t(const float4* x, int n, int nt, int nb, float* partial,
                          cudaStream_t st, unsigned long long* done_pairs, const int* ulist, const int* ucount,
                          const unsigned short* umask, const float4* sph16, const float4* sphJ, float cut,
                          unsigned* sched) {
-  static int per_sm = 0;   // resident CTAs per SM (one full wave; the units are strided over it)
   const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)SYM_S * SYM_T * sizeof(float) +
                       (size_t)16 * SYM_S * SYM_T * sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(matvec_sym_kernel<NU2, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(matvec_sym_kernel<NU2, SUB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, matvec_sym_kernel<NU2, SUB>, 256, smem) !=
-            cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-    if (const char* e = getenv("CAKF_K1_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
-    configured = true;
-  }
+  // resident CTAs per SM (one full wave; the units are strided over it), set up once per device (thread-safe)
+  static PerDeviceOnce once;
+  static int per_sm_dev[PerDeviceOnce::kMaxDev] = {};
+  const cudaError_t ce = once_per_device(once, [&] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= PerDeviceOnce::kMaxDev) dev = 0;
+    cudaError_t r = cudaFuncSetAttribute(matvec_sym_kernel<NU2, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(matvec_sym_kernel<NU2, SUB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int ps = 0;
+    if (r == cudaSuccess &&
+        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, matvec_sym_kernel<NU2, SUB>, 256, smem) != cudaSuccess ||
+         ps < 1))
+      ps = 1;
+    if (const char* e = getenv("CAKF_K1_CTAS")) ps = std::max(1, std::min(ps, atoi(e)));
+    per_sm_dev[dev] = ps;
+    return r;
+  });
+  if (ce != cudaSuccess) return ce;
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur < 0 || cur >= PerDeviceOnce::kMaxDev) cur = 0;
+  const int per_sm = std::max(1, per_sm_dev[cur]);
   const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);
   return launch_pdl(matvec_sym_kernel<NU2, SUB>, dim3((unsigned)grid), dim3(256), smem, st, x, n, nt, nb, u_begin,
                     u_end, partial, done_pairs, ulist, ucount, umask, sph16, sphJ, cut,

@@ -428,14 +428,14 @@ __global__ void split_f16x2_kernel(int K, int C, int Kp, const float* __restrict
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -453,14 +453,16 @@ template <int NU2>
 cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const uint16_t* planes, int Kp, int C,
                          int ntile, float* Y, size_t ldy, float alpha, cudaStream_t st, const int* act_cnt,
                          const int* act_list, int act_stride, const float* colinv) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         TC_SMEM);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = once_per_device(once, [] {
+      cudaError_t r = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2, false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(gram_gemm_tc_kernel<NU2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+      return r;
+    });
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   auto enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -536,12 +538,8 @@ __global__ void k2_active_kernel(const float4* __restrict__ sphM, const float4* 
 }
 
 bool use_tc_k2() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_K2_SIMT");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = !env_is("CAKF_K2_SIMT", '1');
+  return v;
 }
 
 cudaError_t launch_k2_active(const float4* sphM, int nmt, const float4* sphK, int nkb, float cut, int* act_cnt,
@@ -558,12 +556,8 @@ size_t gram_gemm_tc_workspace(int K, int C) {
 }
 
 bool use_f16_k2() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_K2_PREC");
-    v = (e && (e[0] == 'f' || e[0] == 'F')) ? 1 : 0;   // "f16x2"; default 3 x BF16
-  }
-  return v == 1;
+  static const bool v = env_is("CAKF_K2_PREC", 'f') || env_is("CAKF_K2_PREC", 'F');   // "f16x2"; default 3 x BF16
+  return v;
 }
 
 cudaError_t launch_gram_gemm_tc(int nu2, const float4* xr, int M, const float4* xc, int K, const float* B, size_t ldb,

@@ -157,12 +157,8 @@ __device__ bool reduce_blocks(int n, int W, double* part, unsigned* cnt, double*
 }
 
 bool side_slim() {   // CAKF_SIDE_SLIM=0: side-stream HM kernels without the 80-register cap (then they only fit in the K1 tail)
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_SIDE_SLIM");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = !env_is("CAKF_SIDE_SLIM", '0');
+  return v;
 }
 
 // ------------------------------------------------------------------ update prologue
@@ -1122,6 +1118,34 @@ cudaError_t gather_vec(int N, const int* sigma, const T* in, T* out, cudaStream_
 template cudaError_t gather_vec<float>(int, const int*, const float*, float*, cudaStream_t);
 template cudaError_t gather_vec<double>(int, const int*, const double*, double*, cudaStream_t);
 
+template <typename T>
+__global__ void scatter_vec_kernel(int N, const int* __restrict__ sigma, const T* __restrict__ in, T* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < N) out[sigma[j]] = in[j];
+}
+template <typename T>
+cudaError_t scatter_vec(int N, const int* sigma, const T* in, T* out, cudaStream_t st) {
+  if (N <= 0) return cudaSuccess;
+  scatter_vec_kernel<T><<<nblk(N), 256, 0, st>>>(N, sigma, in, out);
+  return note_launch_err();
+}
+template cudaError_t scatter_vec<float>(int, const int*, const float*, float*, cudaStream_t);
+template cudaError_t scatter_vec<double>(int, const int*, const double*, double*, cudaStream_t);
+
+template <typename T>
+__global__ void set_w_kernel(int N, const T* __restrict__ w, V4<T>* __restrict__ xc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < N) xc[j].w = w[j];
+}
+template <typename T>
+cudaError_t set_w(int N, const T* w, V4<T>* xc, cudaStream_t st) {
+  if (N <= 0) return cudaSuccess;
+  set_w_kernel<T><<<nblk(N), 256, 0, st>>>(N, w, xc);
+  return note_launch_err();
+}
+template cudaError_t set_w<float>(int, const float*, V4<float>*, cudaStream_t);
+template cudaError_t set_w<double>(int, const double*, V4<double>*, cudaStream_t);
+
 cudaError_t map_order(int n, const int64_t* order_user, const int* sigma_inv, int* order_out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   map_order_kernel<<<nblk(n), 256, 0, st>>>(n, order_user, sigma_inv, order_out);
@@ -1149,11 +1173,7 @@ template struct StepKernels<double>;
 
 namespace cakf {
 bool pdl_enabled() {   // CAKF_PDL=0: plain launches for the inner-loop kernels
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAKF_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = !env_is("CAKF_PDL", '0');
+  return v;
 }
 }  // namespace cakf

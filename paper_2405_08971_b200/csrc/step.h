@@ -27,6 +27,12 @@ cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int*
 cudaError_t obs_neq(int n, const int64_t* a, const int64_t* b, int* neq, cudaStream_t st);
 template <typename T>
 cudaError_t gather_vec(int N, const int* sigma, const T* in, T* out, cudaStream_t st);
+// out[sigma[j]] = in[j]  (internal observation order -> user order)
+template <typename T>
+cudaError_t scatter_vec(int N, const int* sigma, const T* in, T* out, cudaStream_t st);
+// xc[j].w = w[j]
+template <typename T>
+cudaError_t set_w(int N, const T* w, V4<T>* xc, cudaStream_t st);
 cudaError_t map_order(int n, const int64_t* order_user, const int* sigma_inv, int* order_out, cudaStream_t st);
 template <typename T>
 cudaError_t unpermute(int NX, int Dp, const int* perm, const T* in, T* out, cudaStream_t st);

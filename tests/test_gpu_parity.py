@@ -48,8 +48,16 @@ def run_oracle(wl, dtype):
     return ocakf.run_workload(wl, dtype_round=np.float32 if dtype == "f32" else None)
 
 
+def assert_positive_variances(fv, sv):
+    """A marginal variance of the computation-aware posterior is >= the exact posterior's > 0
+    (dominance): any value <= 0 is a defect, never rounding to be tolerated."""
+    for k, (a, b) in enumerate(zip(fv, sv)):
+        assert np.min(a) > 0 and np.min(b) > 0, (k, float(np.min(a)), float(np.min(b)))
+
+
 def compare(wl, dtype, tol_m, tol_v, on_device=True):
     h, fm, fv, sm, sv, stats = run_device(wl, dtype, on_device)
+    assert_positive_variances(fv, sv)
     ssm, tr, osm = run_oracle(wl, dtype)
     errs = {"fm": 0.0, "fv": 0.0, "sm": 0.0, "sv": 0.0}
     for k in range(wl.T + 1):
@@ -164,6 +172,7 @@ def compare_fp32_cancellation(wl, tol_m=1e-4, c_cancel=2048.0):
     eps32 * Sigma_dd absolute; measured c <= 420 with coordinate actions).
     """
     h, fm, fv, sm, sv, stats = run_device(wl, "f32")
+    assert_positive_variances(fv, sv)
     ssm, tr, osm = run_oracle(wl, "f32")
     for k in range(wl.T + 1):
         sdd = np.concatenate([np.full(wl.n_space, ssm.sigma_t(k)[d, d]) for d in range(wl.d_time)])
@@ -288,3 +297,30 @@ def test_propagated_smoother_equals_direct_k2(monkeypatch, dtype, policy, iters,
         assert st_p[k]["smoother_rank"] == st_d[k]["smoother_rank"]
         assert mean_rel(sm_p[k], sm_d[k]) < tol, (k, mean_rel(sm_p[k], sm_d[k]))
         assert var_rel(sv_p[k], sv_d[k]) < 10 * tol, (k, var_rel(sv_p[k], sv_d[k]))
+
+
+# ------------------------------------------------ the paper-literal single Gram-Schmidt pass (R19)
+def test_reorth0_cfg1_equals_exact_kf():
+    """reorth = 0 runs alg:update_pls line 11 exactly as printed (one classical pass).  With
+    full-rank unit actions and no truncation CAKF/CAKS must still equal the exact KF/RTS (P2)."""
+    from oracle import kf
+    wl = make_workload("cfg1", reorth=False)
+    compare(wl, "f64", 1e-9, 1e-9)
+    h, fm, fv, sm, sv, stats = run_device(wl, "f64")
+    ssm = omodel.ssm_from_workload(wl)
+    K = kf.kalman_filter(ssm)
+    R = kf.rts_smoother(ssm, K)
+    for k in range(wl.T + 1):
+        assert mean_rel(fm[k], K["m"][k]) < 1e-9 and var_rel(fv[k], np.diag(K["P"][k])) < 1e-9
+        assert mean_rel(sm[k], R["m"][k]) < 1e-9 and var_rel(sv[k], np.diag(R["P"][k])) < 1e-9
+
+
+@pytest.mark.parametrize("policy,iters,rank", [("cg", 16, 24), ("random", 16, 24), ("coord", 10, 15)])
+def test_reorth0_sphere48_fp64(policy, iters, rank):
+    """Single CGS pass on both sides (oracle cgs2=False), with truncation: fp64 1e-9."""
+    wl = make_workload("sphere48", policy=policy, max_iter=iters, max_rank=rank, T=5, reorth=False)
+    if policy == "coord":
+        from synth.workloads import farthest_point_order
+        o = farthest_point_order(wl.coords[wl.obs_idx[0]], iters)
+        wl.coord_order = [o.copy() for _ in range(wl.T)]
+    compare(wl, "f64", 1e-9, 1e-9)

@@ -10,10 +10,11 @@ from synth import make_workload
 @pytest.mark.parametrize("name,kw", [("line8", dict(policy="cg", max_iter=3, max_rank=4)),
                                      ("sphere48", dict(T=3, max_iter=6, max_rank=8)),
                                      ("sphere48", dict(T=2, policy="random", max_iter=5, max_rank=-1))])
-def test_mfree_equals_dense(name, kw):
+@pytest.mark.parametrize("cache", [False, True])
+def test_mfree_equals_dense(name, kw, cache):
     wl = make_workload(name, **kw)
     ssm, tr, sm = cakf.run_workload(wl)
-    out = mfree.run_mf(wl, chunk=97)
+    out = mfree.run_mf(wl, chunk=97, cache=cache)
     for k in range(wl.T + 1):
         for got, ref in ((out["fm"][k], tr[k].m), (out["sm"][k], sm["m"][k])):
             assert np.max(np.abs(got - ref)) <= 1e-9 * max(np.max(np.abs(ref)), 1.0)
