@@ -56,17 +56,24 @@ def _perturbed(wl, eps):
     return w2
 
 
-def errs(dev, ref):
+def mrel(a, b):
+    den, num = float(np.max(np.abs(b))), float(np.max(np.abs(a - b)))
+    return num / den if den > 0 else (0.0 if num == 0 else float("inf"))
+
+
+def errs(dev, ref, sdd=None):
     fm, fv, sm, sv = dev[:4]
     om, ov, osm_, osv = ref
-    mrel = lambda a, b: float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
     vrel = lambda a, b: float(np.max(np.abs(a - b) / np.abs(b)))
     T = len(fm) - 1
     return {"f_mean": max(mrel(fm[k], om[k]) for k in range(T + 1)),
             "f_var": max(vrel(fv[k], ov[k]) for k in range(T + 1)),
             "s_mean": max(mrel(sm[k], osm_[k]) for k in range(T + 1)),
             "s_var": max(vrel(sv[k], osv[k]) for k in range(T + 1)),
-            "f_var_min": float(min(np.min(v) for v in fv)), "s_var_min": float(min(np.min(v) for v in sv))}
+            "f_var_min": float(min(np.min(v) for v in fv)), "s_var_min": float(min(np.min(v) for v in sv)),
+            # downdate-cancellation constant of R20: max |dv| / (eps32 Sigma_dd)
+            "c_cancel": None if sdd is None else float(max(np.max(np.abs(a - b) / (EPS32 * sdd))
+                                                           for a, b in zip(list(fv) + list(sv), list(ov) + list(osv))))}
 
 
 def sens(a, b):
@@ -80,7 +87,8 @@ CASES = {
     + [("sphere48", dict(policy="cg", max_iter=16, max_rank=24, T=5, reorth=False), "f64", True)],
     "sphere24": [("sphere24", dict(policy=p, max_iter=16, max_rank=24, T=4), d, True)
                  for p in ("random", "coord", "cg") for d in ("f64", "f32")],
-    "cfg2": [("cfg2", dict(policy=p, T=6), d, False) for p in ("random", "coord", "cg") for d in ("f64", "f32")],
+    "cfg2": [("cfg2", dict(policy=p, T=6), d, False) for p in ("random", "coord", "cg") for d in ("f64", "f32")]
+    + [("cfg2", dict(policy="cg", T=6, max_iter=6, max_rank=16), d, False) for d in ("f64", "f32")],
 }
 
 
@@ -100,10 +108,11 @@ def main():
             dev = device(wl, dtype)
             t1 = time.time()
             ref = oracle(wl, dtype, dense)
+            sdd = np.concatenate([np.full(wl.n_space, wl.sigma ** 2), np.full(wl.n_space, 3 * wl.sigma ** 2 / wl.ell_t ** 2)])
             row = {"case": name, "dtype": dtype, "policy": wl.policy, "max_iter": wl.max_iter,
                    "max_rank": wl.max_rank, "T": wl.T, "D": wl.D, "reorth": bool(wl.reorth),
                    "oracle": "dense O4/O5" if dense else "matrix-free O8 (cached kernel matrices)",
-                   **errs(dev, ref), "ranks_out": [s["rank_out"] for s in dev[4][1:]],
+                   **errs(dev, ref, sdd if dtype == "f32" else None), "ranks_out": [s["rank_out"] for s in dev[4][1:]],
                    "device_s": round(t1 - t0, 2), "oracle_s": round(time.time() - t1, 2)}
             if wl.policy == "cg" and dtype == "f64":
                 ref2 = oracle(wl, dtype, dense, perturb=2.0 ** -52)

@@ -58,10 +58,26 @@ def device(policy, dtype):
     return wl, out
 
 
+def _mrel(x, y):
+    """R20: ||dm||_inf / ||m||_inf; a zero reference mean (the prior at k = 0) must be matched exactly."""
+    den = float(np.max(np.abs(y)))
+    num = float(np.max(np.abs(x - y)))
+    return num / den if den > 0 else (0.0 if num == 0 else np.inf)
+
+
 def rel_errs(a, b):
-    m = max(float(np.max(np.abs(x - y)) / np.max(np.abs(y))) for key in ("fm", "sm") for x, y in zip(a[key], b[key]))
+    m = max(_mrel(x, y) for key in ("fm", "sm") for x, y in zip(a[key], b[key]))
     v = max(float(np.max(np.abs(x - y) / np.abs(y))) for key in ("fv", "sv") for x, y in zip(a[key], b[key]))
     return m, v
+
+
+def heldout_rmse(wl, means):
+    """RMSE of the filter / smoother mean of f_0 on the held-out test subgrid vs the noise-free field."""
+    from synth.workloads import temperature_field
+    X = wl.coords[wl.test_idx]
+    lat, lon = np.arcsin(np.clip(X[:, 2], -1, 1)), np.arctan2(X[:, 1], X[:, 0])
+    errs = [means[k][wl.test_idx] - temperature_field(wl.times[k - 1], lat, lon) for k in range(1, wl.T + 1)]
+    return float(np.sqrt(np.mean(np.concatenate(errs) ** 2)))
 
 
 def check_ranks(wl, out):
@@ -107,26 +123,44 @@ def test_cfg2_fixed_actions_fp32(policy):
             assert np.all(np.abs(x - y) <= 1e-4 * y + bound_abs)
 
 
-def test_cfg2_cg_fp64_within_oracle_sensitivity():
-    wl, out = device("cg", "f64")
+def test_cfg2_cg_short_fp64():
+    """CG actions while the Krylov trajectory is still well-conditioned (6 iterations per step; the
+    oracle's 1-ulp sensitivity grows ~8x per iteration at cfg2), rank cap 16 so the
+    truncation is active from step 3: fp64 within 1e-9, integer stats bit-exact."""
+    wl = make_workload("cfg2", policy="cg", T=6, max_iter=6, max_rank=16)
+    trans, _ = runner.transitions(wl)
+    h = runner.make_handle(wl, "f64")
+    runner.run(h, trans, runner.stage_inputs(wl, "f64"), smooth=True)
+    out = {}
+    out["fm"], out["fv"] = runner.collect(h, wl.T, CAKF_FILTER)
+    out["sm"], out["sv"] = runner.collect(h, wl.T, CAKF_SMOOTH)
+    ranks = [h.get_stats(k)["rank_out"] for k in range(1, wl.T + 1)]
+    h.destroy()
+    assert ranks == [6, 12, 16, 16, 16, 16]
+    positive(out)
+    m, v = rel_errs(out, mfree.run_mf(wl, cache=True))
+    print(f"cfg2 cg (6 iterations) fp64: mean {m:.3g} var {v:.3g}")
+    assert m < 1e-9 and v < 1e-9
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_cfg2_cg_64_reported_against_oracle_sensitivity(dtype):
+    """64 CG iterations per step (the bench's policy): the oracle itself moves O(1) under a 1-ulp
+    relative perturbation of y (R20: the Krylov trajectory amplifies rounding ~8x per
+    iteration), so element-wise parity is undefined here.  Reported: device-vs-oracle error next to
+    the oracle's own 1-ulp sensitivity.  Gated: every variance positive, and the held-out RMSE of the
+    device's means (a property every valid trajectory shares) within the oracle-vs-perturbed-oracle
+    spread of the oracle's RMSE (x3, + 5 %)."""
+    wl, out = device("cg", dtype)
     check_ranks(wl, out)
     positive(out)
-    ref = oracle("cg", "f64")
-    pert = oracle("cg", "f64", perturb=2.0 ** -52)
+    ref = oracle("cg", dtype)
+    pert = oracle("cg", dtype, perturb=2.0 ** -52)
     m, v = rel_errs(out, ref)
     sm_, sv_ = rel_errs(pert, ref)
-    print(f"cfg2 cg fp64: mean {m:.3g} var {v:.3g}; oracle 1-ulp sensitivity mean {sm_:.3g} var {sv_:.3g}")
-    # a different (but equally valid) fp64 rounding sequence moves the result like O(64)
-    # independent 1-ulp input perturbations (one per Krylov step), so the device may differ from
-    # the oracle by up to 64x the oracle's own 1-ulp sensitivity, and never by more than 1e-6.
-    assert m <= max(1e-9, 64 * sm_) and v <= max(1e-9, 64 * sv_)
-    assert m < 1e-6 and v < 1e-6
-
-
-def test_cfg2_cg_fp32_reported():
-    wl, out = device("cg", "f32")
-    check_ranks(wl, out)
-    positive(out)
-    m, v = rel_errs(out, oracle("cg", "f32"))
-    print(f"cfg2 cg fp32 (reported, R20): mean {m:.3g} var {v:.3g}")
-    assert np.isfinite(m) and np.isfinite(v)
+    print(f"cfg2 cg {dtype}: device-vs-oracle mean {m:.3g} var {v:.3g}; oracle 1-ulp sensitivity "
+          f"mean {sm_:.3g} var {sv_:.3g}")
+    for key in ("fm", "sm"):
+        r_dev, r_or, r_pt = heldout_rmse(wl, out[key]), heldout_rmse(wl, ref[key]), heldout_rmse(wl, pert[key])
+        print(f"  {key} held-out RMSE: device {r_dev:.4f} oracle {r_or:.4f} perturbed oracle {r_pt:.4f}")
+        assert abs(r_dev - r_or) <= 3 * abs(r_pt - r_or) + 0.05 * r_or
