@@ -305,6 +305,16 @@ int cakf_lowrank_gemm(int32_t transa, int32_t transb, int64_t m, int64_t n, int6
                       const float* A, int64_t lda, const float* B, int64_t ldb, double beta, float* C,
                       int64_t ldc, void* stream);
 
+/* Standalone symmetric eigensolver of the truncation (a8 / a9 Truncate, Sec. 3.2; "SVD of
+ * M M^T" P:367, reading R4: eigh of the Gram M^T M), fp64, all on the device (kernels_eig.cu:
+ * cluster Householder tridiagonalisation, divide and conquer, back-transformation):
+ *   G : c x c symmetric, column-major, only the lower triangle is read (host or device)
+ *   w : c eigenvalues, ascending (nullable)
+ *   Qr: c x r column-major eigenvectors of the r LARGEST eigenvalues, in descending order (nullable)
+ * 1 <= c <= 8192, 0 <= r <= c.  Workspaces are allocated on `stream` (may be NULL); synchronises.
+ * Errors: CAKF_E_ARG, CAKF_E_NUMERIC (non-finite eigenvalue), CAKF_E_CUDA. */
+int cakf_sym_eig(int64_t c, int64_t r, const double* G, double* w, double* Qr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

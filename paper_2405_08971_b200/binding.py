@@ -61,7 +61,7 @@ EXPORTS = [
     "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
     "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats", "cakf_interpolate", "cakf_sample",
-    "cakf_lowrank_gemm", "cakf_debug_matvec",
+    "cakf_lowrank_gemm", "cakf_debug_matvec", "cakf_sym_eig",
 ]
 PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank", "trunc_gram",
                    "trunc_eig", "trunc_gemm"]
@@ -100,6 +100,7 @@ def load(path: str = LIB_PATH):
     lib.cakf_shard_plan.argtypes = [i64, i64, i32, i32, vp]
     lib.cakf_cull_stats.argtypes = [vp, vp]
     lib.cakf_debug_matvec.argtypes = [vp, i64, vp, vp, vp]
+    lib.cakf_sym_eig.argtypes = [i64, i64, vp, vp, vp, vp]
     lib.cakf_interpolate.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp]
     lib.cakf_sample.argtypes = [vp, i32, vp, vp, vp, i32, vp]
     lib.cakf_sym_unit_blocks.argtypes = [i64, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
@@ -200,6 +201,18 @@ def lowrank_gemm(A, B, transa=False, transb=False, alpha=1.0, beta=0.0, C=None, 
                                  Bm.data_ptr(), Bm.shape[1], Am.data_ptr(), Am.shape[1], float(beta),
                                  out.data_ptr(), n, stream))
     return out
+
+
+def sym_eig(G, r=None):
+    """(w ascending, Qr (c x r) eigenvectors of the r largest eigenvalues, descending) of a symmetric fp64
+    matrix through the library's device eigensolver (cakf_sym_eig); numpy in / out."""
+    Gf = np.asfortranarray(np.asarray(G, dtype=np.float64))
+    c = Gf.shape[0]
+    r = c if r is None else int(r)
+    w = np.empty(c)
+    Q = np.empty((c, max(r, 1)), order="F")
+    _check(load().cakf_sym_eig(c, r, Gf.ctypes.data, w.ctypes.data, Q.ctypes.data, None))
+    return w, Q[:, :r]
 
 
 class Cakf:

@@ -250,6 +250,10 @@ struct Impl final : ImplBase {
   // truncation
   double *gpart = nullptr, *Gm = nullptr, *eigw = nullptr, *work = nullptr;
   int* info = nullptr;
+  void* eigws = nullptr;   // own eigensolver workspace (kernels_eig.cu)
+  size_t eigws_bytes = 0;
+  // CAKF_EIG_CUSOLVER=1: cusolverDnDsyevd instead of the repo's eigensolver (A/B only)
+  bool eig_cusolver = env_is("CAKF_EIG_CUSOLVER", '1');
   int lwork = 0, nsplit_max = 16;
   T* Mtil = nullptr;
   double* QrD = nullptr;
@@ -548,6 +552,8 @@ struct Impl final : ImplBase {
       work = carve<double>(std::max(lwork, 1));
       info = carve<int>(4);
       QrD = carve<double>((size_t)cmax * std::max(rcap, 1));
+      eigws_bytes = eig_workspace_bytes(cmax);
+      eigws = carve<unsigned char>(eigws_bytes);
       Mtil = carve<T>((size_t)D * std::max(rcap, 1));
     }
     if (sizeof(T) == 4) {
@@ -684,7 +690,7 @@ struct Impl final : ImplBase {
     }
     if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) return fail(CAKF_E_CUDA, "cublasCreate failed");
     CK_BLAS(cublasSetStream(blas, st));
-    if (c.max_rank >= 0) {
+    if (c.max_rank >= 0 && eig_cusolver) {
       if (cusolverDnCreate(&sol) != CUSOLVER_STATUS_SUCCESS) return fail(CAKF_E_CUDA, "cusolverDnCreate failed");
       CK_SOLVER(cusolverDnSetStream(sol, st));
     }
@@ -693,7 +699,7 @@ struct Impl final : ImplBase {
     // the stage kernels keep one fp64 per kept column / previous action in (default, <= 48 KB) dynamic smem
     if (std::max(rin_max, nhat) > 6144)
       return fail(CAKF_E_UNSUPPORTED, "max_rank (or (T-1) max_iter without a cap) and max_iter must be <= 6144");
-    if (rcap >= 0 && cmax > 0) {
+    if (rcap >= 0 && cmax > 0 && eig_cusolver) {
       CK_SOLVER(cusolverDnDsyevd_bufferSize(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, cmax, nullptr, cmax,
                                             nullptr, &lwork));
     }
@@ -1169,8 +1175,21 @@ struct Impl final : ImplBase {
   }
 
   // fp32 truncation on tcgen05: Gram F^T F (3xBF16, K split, fp64 reduction) -> fp64 eig -> F Q_r
+  // top-rkeep eigenpairs of the Gram Gm (lower, ld c) -> QrD (c x rkeep, descending), kept, dropped mass;
+  // fail: the step's IterCtl::nonfinite (reported by cakf_get_stats)
+  int eig(int c, int rkeep, double* kept, double* dropped, int* failflag) {
+    if (eig_cusolver) {
+      CK_SOLVER(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, c, Gm, c, eigw, work, lwork,
+                                 info));
+      CK_CUDA(StepKernels<double>::take_top(c, rkeep, Gm, eigw, QrD, kept, dropped, st));
+      return CAKF_OK;
+    }
+    CK_CUDA(eig_top(c, rkeep, Gm, eigws, eigws_bytes, QrD, kept, dropped, nullptr, failflag, st));
+    return CAKF_OK;
+  }
+
   int truncate_factor_tc(const float* F, int c, int rkeep, float* out, double* kept, double* dropped, size_t pk,
-                         const float* F2, float* out2) {
+                         const float* F2, float* out2, int* failflag) {
     size_t ps = prof_begin();
     if (gemm_tc_plane_bytes((int)D, c) > gp_elems * 2) return fail(CAKF_E_ARG, "truncate: operand planes too small");
     const bool i8 = use_i8_gemm();
@@ -1186,8 +1205,7 @@ struct Impl final : ImplBase {
     }
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
-    CK_SOLVER(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, c, Gm, c, eigw, work, lwork, info));
-    CK_CUDA(StepKernels<double>::take_top(c, rkeep, Gm, eigw, QrD, kept, dropped, st));
+    CK(eig(c, rkeep, kept, dropped, failflag));
     prof_end(CAKF_PROF_TRUNC_EIG, ps);
     ps = prof_begin();
     if (i8 && i8_mqr) {   // M~ = F Q_r with the fp64 eigenvectors sliced directly
@@ -1215,13 +1233,14 @@ struct Impl final : ImplBase {
 
   // Truncate a D x c factor F (ld D) to its top-r Gram eigen-directions: out = F Q_r; F2 (nullable, D x c)
   // gets the same Q_r: out2 = F2 Q_r (the smoother's kernel-applied carriers).
-  int truncate_factor(const T* F, int c, int rkeep, T* out, double* kept, double* dropped, const T* F2 = nullptr,
-                      T* out2 = nullptr) {
+  int truncate_factor(const T* F, int c, int rkeep, T* out, double* kept, double* dropped, int* failflag,
+                      const T* F2 = nullptr, T* out2 = nullptr) {
     const size_t pk = prof_begin();
     if constexpr (sizeof(T) == 4) {
       if (use_tc_gemm()) return truncate_factor_tc(reinterpret_cast<const float*>(F), c, rkeep,
                                                    reinterpret_cast<float*>(out), kept, dropped, pk,
-                                                   reinterpret_cast<const float*>(F2), reinterpret_cast<float*>(out2));
+                                                   reinterpret_cast<const float*>(F2), reinterpret_cast<float*>(out2),
+                                                   failflag);
     }
     // fp64 copy of F (fp32 storage) feeds both the Gram (DSYRK, fp64 tensor cores) and M Q_r (DGEMM)
     const double* Fd = reinterpret_cast<const double*>(F);
@@ -1235,8 +1254,7 @@ struct Impl final : ImplBase {
     CK(gram_lower(Fd, c));
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
-    CK_SOLVER(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, c, Gm, c, eigw, work, lwork, info));
-    CK_CUDA(StepKernels<double>::take_top(c, rkeep, Gm, eigw, QrD, kept, dropped, st));
+    CK(eig(c, rkeep, kept, dropped, failflag));
     prof_end(CAKF_PROF_TRUNC_EIG, ps);
     ps = prof_begin();
     if constexpr (sizeof(T) == 4) {
@@ -1270,7 +1288,7 @@ struct Impl final : ImplBase {
       S.truncated = false;
       S.rank_out = S.cols;
     } else {
-      CK(truncate_factor(S.Mk, S.cols, rcap, Mtil, S.kept, &ctl[kcur].dropped));   // Sec. 3.2
+      CK(truncate_factor(S.Mk, S.cols, rcap, Mtil, S.kept, &ctl[kcur].dropped, &ctl[kcur].nonfinite));   // Sec. 3.2
       S.truncated = true;
       S.rank_out = rcap;
     }
@@ -1343,7 +1361,7 @@ struct Impl final : ImplBase {
       }
       const int qn = n + q;
       if (rcap >= 0 && qn > rcap) {                                   // line 9 (R6)
-        CK(truncate_factor(Wf, qn, rcap, Ws, nullptr, nullptr, smooth_k2 ? nullptr : KWf, KWs));
+        CK(truncate_factor(Wf, qn, rcap, Ws, nullptr, nullptr, &ctl[k].nonfinite, smooth_k2 ? nullptr : KWf, KWs));
         q = rcap;
       } else {
         std::swap(Wf, Ws);
@@ -1928,6 +1946,34 @@ int cakf_gram_matmul(int32_t dtype, int32_t spatial_kernel, double ell, int32_t 
   if (dtype == CAKF_F32) return run(float{});
   if (dtype == CAKF_F64) return run(double{});
   return fail(CAKF_E_ARG, "cakf_gram_matmul: bad dtype");
+}
+
+int cakf_sym_eig(int64_t c, int64_t r, const double* G, double* w, double* Qr, void* stream) {
+  if (c < 1 || c > 8192 || r < 0 || r > c || !G || (!w && !Qr)) return fail(CAKF_E_ARG, "cakf_sym_eig: bad argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t cc = (size_t)c * c, wsb = eig_workspace_bytes((int)c);
+  double *Gd = nullptr, *wd = nullptr, *Qd = nullptr;
+  int* fl = nullptr;
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&Gd, cc * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&wd, (size_t)c * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&Qd, (size_t)c * std::max<int64_t>(r, 1) * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&fl, sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&ws, wsb, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(Gd, G, cc * sizeof(double), cudaMemcpyDefault, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(fl, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = eig_top((int)c, (int)r, Gd, ws, wsb, Qd, nullptr, nullptr, wd, fl, st);
+  int hf = 0;
+  if (e == cudaSuccess && w) e = cudaMemcpyAsync(w, wd, (size_t)c * sizeof(double), cudaMemcpyDefault, st);
+  if (e == cudaSuccess && Qr && r) e = cudaMemcpyAsync(Qr, Qd, (size_t)c * r * sizeof(double), cudaMemcpyDefault, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hf, fl, sizeof(int), cudaMemcpyDeviceToHost, st);
+  for (void* p : {(void*)Gd, (void*)wd, (void*)Qd, (void*)fl, ws})
+    if (p) cudaFreeAsync(p, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return fail(CAKF_E_CUDA, std::string("cakf_sym_eig: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+  if (hf) return fail(CAKF_E_NUMERIC, "cakf_sym_eig: non-finite eigenvalue");
+  return CAKF_OK;
 }
 
 int cakf_lowrank_gemm(int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k, double alpha, const float* A,

@@ -97,6 +97,15 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
                         size_t work_doubles, cudaStream_t st);
 bool use_i8_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM instead
 
+// ---- the truncation's symmetric eigensolver (kernels_eig.cu): cluster Householder tridiagonalisation,
+// divide and conquer, back-transformation of the r wanted eigenvectors.  G: c x c fp64, lower triangle
+// (ld c).  Qr: c x r eigenvectors of the r largest eigenvalues, descending; kept (r, nullable) those
+// eigenvalues; dropped (nullable) the sum of the c - r smallest; w_all (c, nullable) all eigenvalues
+// ascending; fail (nullable device int) set to 1 on a non-finite eigenvalue.
+size_t eig_workspace_bytes(int cmax);
+cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, double* Qr, double* kept,
+                    double* dropped, double* w_all, int* fail, cudaStream_t st);
+
 // ---- per-update kd-tree order of the observed points (kd_order.cu)
 size_t kd_obs_workspace(int Nmax);
 // idx/sig_in_sorted: the observations in internal point order (obs_sort); writes idx_out, sig_out
