@@ -65,162 +65,219 @@ struct TrdArgs {
   double* tau;       // c
   double* d;         // c   diagonal of T
   double* e;         // c   sub-diagonal of T (e[j] = T[j+1][j])
-  double* vglob;     // 2 x c  broadcast of v (double-buffered by step parity)
-  double* pglob;     // c      broadcast of p
-  double* sglob;     // kTrdCluster partial dots
-  double* Aglob;     // global-memory mode: kTrdCluster slabs of L x c
+  double* pglob;     // 2 x c  p of the step (double-buffered by step parity)
+  double* colglob;   // 2 x c  the next column after all but the latest update
+  double* sglob;     // 2 x kTrdCluster partial dots p^T v
+  double* Aglob;     // global-memory mode: slabs of L x c per CTA
 };
 
-// Householder reflector of column j (owned by this CTA, local column lc): x = A[j+1:, j].
-// LAPACK dlarfg convention: H = I - tau v v^T, H x = beta e_1, v[j+1] = 1.
-__device__ void trd_householder(const TrdArgs& a, const double* Acol, int j, double* red) {
-  const int c = a.c;
-  double s2 = 0.0;
-  for (int l = j + 2 + threadIdx.x; l < c; l += blockDim.x) s2 += Acol[l] * Acol[l];
-  s2 = block_sum_d(s2, red);
-  const double alpha = Acol[j + 1];
-  double tau = 0.0, beta = alpha, scal = 0.0;
-  if (s2 > 0.0) {
-    const double nrm = sqrt(alpha * alpha + s2);
-    beta = alpha >= 0.0 ? -nrm : nrm;
-    tau = (beta - alpha) / beta;
-    scal = 1.0 / (alpha - beta);
-  }
-  double* vg = a.vglob + (size_t)(j & 1) * c;
-  for (int l = j + 1 + threadIdx.x; l < c; l += blockDim.x) {
-    const double v = l == j + 1 ? 1.0 : Acol[l] * scal;
-    vg[l] = v;
-    a.V[l + (size_t)j * c] = v;
-  }
-  if (threadIdx.x == 0) {
-    a.tau[j] = tau;
-    a.d[j] = Acol[j];
-    a.e[j] = beta;
-  }
-}
 
-template <bool SMEM>
+// Householder tridiagonalisation in one cluster of NC CTAs, ONE cluster barrier per step:
+//   step j: (a) fused pass over my columns i > j: apply update(j-1) (A -= v w^T + w v^T) to rows > j and form
+//               p_i = tau_j A[:, i] . v_j; the owner of column j+1 also publishes that column (post update(j-1));
+//           (b) cluster barrier;
+//           (c) every CTA reads p, the partial dots and column j+1 (one L2 round trip), forms w_j, applies
+//               update(j) to column j+1 and computes reflector j+1 itself (identical arithmetic in every CTA,
+//               no second barrier).  Rows are spread one per thread (loops only for c > blockDim).
+// Reflector convention (LAPACK dlarfg): H = I - tau v v^T, H x = beta e_1, v[j+1] = 1.
+template <int NC, bool SMEM>
 __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   const int q = (int)cl.block_rank();
-  const int NC = (int)cl.num_blocks();
   const int c = a.c;
   const int L = (c + NC - 1) / NC;
   extern __shared__ __align__(16) double sm[];
   double* A = SMEM ? sm : a.Aglob + (size_t)q * L * c;
-  double* vb = SMEM ? sm + (size_t)L * c : sm;   // [2][c]
-  double* wb = vb + 2 * (size_t)c;                // [2][c]
-  double* red = wb + 2 * (size_t)c;               // [64]
+  double* vb = SMEM ? sm + (size_t)L * c : sm;   // [2][c]  v_j by step parity
+  double* wb = vb + 2 * (size_t)c;                // [2][c]  w_j by step parity
+  double* pb = wb + 2 * (size_t)c;                // [c]     raw p, then the updated column j+1
+  double* red = pb + (size_t)c;                   // [64]    red[40 + parity] = tau_j
   const int nloc = q < c ? (c - q + NC - 1) / NC : 0;   // my columns i = q + NC * lc
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  // load my columns of the symmetric matrix (lower triangle mirrored)
-  for (size_t x = threadIdx.x; x < (size_t)nloc * c; x += blockDim.x) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, bd = blockDim.x;
+  const bool writer = q == 0;
+  for (size_t x = tid; x < (size_t)nloc * c; x += bd) {
     const int lc = (int)(x / c), l = (int)(x % c), i = q + NC * lc;
     A[x] = l >= i ? a.G[l + (size_t)i * c] : a.G[i + (size_t)l * c];
   }
+  if (c <= 2) {
+    if (writer && tid == 0) {
+      a.d[0] = a.G[0];
+      if (c == 2) {
+        a.d[1] = a.G[3];
+        a.e[0] = a.G[1];
+      }
+    }
+    return;
+  }
+  // reflector jr from x = xs[jr+1 .. c) (smem), into vout; tau -> red[40 + (jr & 1)]; CTA 0 writes the outputs
+  auto reflector = [&](int jr, const double* xs, double dj, double* vout) {
+    double s2 = 0.0;
+    for (int l = jr + 2 + tid; l < c; l += bd) s2 += xs[l] * xs[l];
+    s2 = warp_sum_d(s2);
+    if (lane == 0) red[warp] = s2;
+    __syncthreads();
+    double t = lane < nwarps ? red[lane] : 0.0;   // every warp reduces the partials itself (no 2nd barrier)
+    t = warp_sum_d(t);
+    const double alpha = xs[jr + 1];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (t > 0.0) {
+      const double nrm = sqrt(alpha * alpha + t);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int l = jr + 1 + tid; l < c; l += bd) {
+      const double v = l == jr + 1 ? 1.0 : xs[l] * scal;
+      vout[l] = v;
+      if (writer) a.V[l + (size_t)jr * c] = v;
+    }
+    if (tid == 0) {
+      red[40 + (jr & 1)] = tau;
+      if (writer) {
+        a.tau[jr] = tau;
+        a.d[jr] = dj;
+        a.e[jr] = beta;
+      }
+    }
+  };
+  for (int l = tid; l < c; l += bd) pb[l] = a.G[l];   // column 0 of G: no update yet
   __syncthreads();
-  if (c >= 3 && q == 0) trd_householder(a, A, 0, red);   // column 0 lives in CTA 0 (lc 0)
-  cl.sync();
+  reflector(0, pb, pb[0], vb);
+  __syncthreads();
   for (int j = 0; j + 3 <= c; ++j) {
     const int par = j & 1;
-    double* vj = vb + (size_t)par * c;
-    double* vprev = vb + (size_t)(par ^ 1) * c;
-    double* wprev = wb + (size_t)(par ^ 1) * c;
+    const double* vj = vb + (size_t)par * c;
+    const double* vprev = vb + (size_t)(par ^ 1) * c;
+    const double* wprev = wb + (size_t)(par ^ 1) * c;
     double* wj = wb + (size_t)par * c;
-    // ---- v_j from L2 (written by the owner before the barrier)
-    const double* vg = a.vglob + (size_t)par * c;
-    for (int l = j + 1 + threadIdx.x; l < c; l += blockDim.x) vj[l] = __ldcg(vg + l);
-    const double tj = __ldcg(a.tau + j);
-    __syncthreads();
-    // ---- fused pass over my columns i > j: apply update(j-1) to rows >= j+1, then p_i = tau_j A[:, i] . v_j
+    double* pg = a.pglob + (size_t)par * c;
+    double* cg_ = a.colglob + (size_t)par * c;
+    double* sg = a.sglob + (size_t)par * NC;
+    const double tj = red[40 + par];
+    // ---- (a) fused pass
     const int lc0 = q > j ? 0 : (j - q) / NC + 1;   // first local column with i > j
     double sq = 0.0;
     for (int lc = lc0 + warp; lc < nloc; lc += nwarps) {
       const int i = q + NC * lc;
       double* col = A + (size_t)lc * c;
-      double acc = 0.0;
+      double acc0 = 0.0, acc1 = 0.0;
+      int l = j + 1 + lane;
       if (j > 0) {
         const double vpi = vprev[i], wpi = wprev[i];
-        for (int l = j + 1 + lane; l < c; l += 32) {
-          const double x = col[l] - vprev[l] * wpi - wprev[l] * vpi;
-          col[l] = x;
-          acc += x * vj[l];
+        if (i == j + 1) {
+          for (; l < c; l += 32) {
+            const double x = col[l] - vprev[l] * wpi - wprev[l] * vpi;
+            col[l] = x;
+            cg_[l] = x;
+            acc0 += x * vj[l];
+          }
+        } else {
+          for (; l + 32 < c; l += 64) {
+            const double x0 = col[l] - vprev[l] * wpi - wprev[l] * vpi;
+            const double x1 = col[l + 32] - vprev[l + 32] * wpi - wprev[l + 32] * vpi;
+            col[l] = x0;
+            col[l + 32] = x1;
+            acc0 += x0 * vj[l];
+            acc1 += x1 * vj[l + 32];
+          }
+          if (l < c) {
+            const double x0 = col[l] - vprev[l] * wpi - wprev[l] * vpi;
+            col[l] = x0;
+            acc0 += x0 * vj[l];
+          }
         }
       } else {
-        for (int l = j + 1 + lane; l < c; l += 32) acc += col[l] * vj[l];
+        for (; l < c; l += 32) {
+          const double x = col[l];
+          if (i == j + 1) cg_[l] = x;
+          acc0 += x * vj[l];
+        }
       }
-      acc = warp_sum_d(acc);
+      const double acc = warp_sum_d(acc0 + acc1);
       if (lane == 0) {
         const double p = tj * acc;
-        a.pglob[i] = p;
+        pg[i] = p;
         sq += p * vj[i];
       }
     }
     if (lane == 0) red[warp] = sq;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < nwarps; ++w) t += red[w];
-      a.sglob[q] = t;
+    if (warp == 0) {
+      double t = lane < nwarps ? red[lane] : 0.0;
+      t = warp_sum_d(t);
+      if (lane == 0) sg[q] = t;
     }
+    // ---- (b)
     cl.sync();
-    // ---- w_j = p - (tau/2)(p^T v) v, every CTA, full vector
-    double K = 0.0;
-    for (int r = 0; r < NC; ++r) K += __ldcg(a.sglob + r);
-    const double hk = 0.5 * tj * K;
-    for (int l = j + 1 + threadIdx.x; l < c; l += blockDim.x) wj[l] = __ldcg(a.pglob + l) - hk * vj[l];
+    // ---- (c) raw p and column j+1 into smem, the NC partial dots (warp 0): one L2 round trip
+    double* xcol = wb + (size_t)(par ^ 1) * c;   // w_{j-1}: consumed by (a), free until step j+1 writes w_{j+1}
+    for (int l = j + 1 + tid; l < c; l += bd) {
+      pb[l] = __ldcg(pg + l);
+      xcol[l] = __ldcg(cg_ + l);
+    }
+    if (warp == 0) {
+      double t = lane < NC ? __ldcg(sg + lane) : 0.0;
+      t = warp_sum_d(t);
+      if (lane == 0) red[35] = t;
+    }
     __syncthreads();
-    // ---- owner of column j+1: apply update(j) to it now (look-ahead), then its reflector
-    const int jn = j + 1;
-    if (q == jn % NC) {
-      double* col = A + (size_t)(jn / NC) * c;
-      const double vi = vj[jn], wi = wj[jn];
-      for (int l = jn + threadIdx.x; l < c; l += blockDim.x) col[l] -= vj[l] * wi + wj[l] * vi;
-      __syncthreads();
-      if (jn + 3 <= c) trd_householder(a, col, jn, red);
+    const double hk = 0.5 * tj * red[35];
+    const double vn = vj[j + 1], wn = pb[j + 1] - hk * vn;
+    for (int l = j + 1 + tid; l < c; l += bd) {
+      const double w = pb[l] - hk * vj[l];
+      wj[l] = w;
+      xcol[l] -= vj[l] * wn + w * vn;   // update(j) of column j+1
     }
-    cl.sync();
+    if (j + 4 <= c) {
+      __syncthreads();   // the reflector reads rows of column j+1 updated by other threads
+      reflector(j + 1, xcol, xcol[j + 1], vb + (size_t)(par ^ 1) * c);
+    } else if (writer) {   // j + 1 == c - 2: the last 2 x 2 block's column c-2
+      for (int l = j + 1 + tid; l < c; l += bd) {
+        if (l == c - 2) a.d[c - 2] = xcol[l];
+        if (l == c - 1) a.e[c - 2] = xcol[l];
+      }
+    }
+    __syncthreads();
   }
-  // ---- epilogue: the last 2 x 2 block (column c-2 got update(c-3) in the loop; column c-1 gets it here)
-  if (c >= 3) {
-    const int j = c - 3, par = j & 1;
+  // ---- d[c-1]: column c-1 (owner) after update(c-3): row c-1 only
+  {
+    const int j = c - 3, par = j & 1, i = c - 1;
     const double* vj = vb + (size_t)par * c;
     const double* wj = wb + (size_t)par * c;
-    const int i = c - 1;
-    if (q == i % NC && threadIdx.x < 2) {
-      double* col = A + (size_t)(i / NC) * c;
-      const int l = c - 2 + threadIdx.x;
-      col[l] -= vj[l] * wj[i] + wj[l] * vj[i];
-    }
-    __syncthreads();
-  }
-  if (c >= 2) {
-    if (q == (c - 2) % NC && threadIdx.x == 0) {
-      const double* col = A + (size_t)((c - 2) / NC) * c;
-      a.d[c - 2] = col[c - 2];
-      a.e[c - 2] = col[c - 1];
+    if (q == i % NC && tid == 0) {
+      const double* col = A + (size_t)(i / NC) * c;
+      a.d[c - 1] = col[c - 1] - 2.0 * vj[c - 1] * wj[c - 1];
     }
   }
-  if (q == (c - 1) % NC && threadIdx.x == 0) a.d[c - 1] = A[(size_t)((c - 1) / NC) * c + (c - 1)];
 }
 
 // ------------------------------------------------------------------ divide and conquer
 // Merge m at level s (blocks of size s merged in pairs): rows/cols [o, o + n), L = [o, o + s),
 // R = [o + s, o + n), o = 2 s m, n = min(2 s, c - o); valid iff o + s < c.
+// Per merge, with P the sort permutation of the poles and G the deflation rotations:
+//   T_block = Q P G (Dhat + rho zhat zhat^T) G^T P^T Q^T,   new eigenvectors  Q P G [U | E_defl]
+// The new block is computed as Qnew = Q_block B with B = P G [U | E_defl] (n x n, built per column),
+// so no permuted copy of Q is materialised; Q and the output alternate between two buffers.
 struct DcArgs {
   int c, s;
   const double* e;     // sub-diagonal of T
   double* dl;          // c: eigenvalues of the current blocks (ascending within a block)
-  double* Q;           // c x c: eigenvectors of the current blocks (block-diagonal)
-  double* Qp;          // c x c: gathered (sorted, rotated) columns of the merge
-  double* U;           // c x c: secular eigenvectors, block (o, o)
-  double* dK;          // c: non-deflated poles (sorted), then deflated values
+  const double* Q;     // c x c: eigenvectors of the current blocks (block-diagonal)
+  double* Qn;          // c x c: eigenvectors of the merged blocks (output)
+  double* B;           // c x c: per merge, n x n block at (o, o): rows = local columns of Q
+  double* dK;          // c: non-deflated poles (sorted)
   double* zK;          // c: non-deflated weights
-  double* org_tau;     // c: tau of root t (distance to its origin pole)
+  double* org_tau;     // c: tau of root t (signed distance to its origin pole)
   double* zhat;        // c
   double* lam;         // c: merged eigenvalues in (K, deflated) order
+  double* rotc;        // c: deflation rotation cosines (per merge, in scan order)
+  double* rots;        // c: sines
+  int* rota;           // c: rotated sorted positions (pj)
+  int* rotb;           // c: (nj)
+  int* nrot;           // per merge
+  int* perm;           // c: sorted position -> local column
   int* org;            // c: origin pole index of root t
-  int* kmap;           // c: (K, deflated) order -> sorted position (column of Qp)
+  int* kmap;           // c: (K, deflated) order -> sorted position
   int* rank;           // c: (K, deflated) order -> final ascending position
   int* kcnt;           // per merge: number of non-deflated
   double* rho;         // per merge: rho * ||z||^2
@@ -252,28 +309,21 @@ __global__ void dc_init_kernel(int c, const double* __restrict__ d, const double
 
 constexpr int kDcPrepThreads = 256;
 
-// Per merge: z = Q^T u, sort the poles, deflate (dlaed2), gather the sorted columns and apply the
-// deflation rotations.  Dynamic smem: n doubles (d sorted) + n doubles (z sorted) + n ints (perm)
-// + n ints (kmap) + n x (2 ints + 2 doubles) rotations.
+// Per merge: z = Q^T u, sort the poles (merge of two ascending lists), deflate (dlaed2: negligible
+// weight; close poles -> Givens rotation).  Dynamic smem: 2 n doubles + n ints.
 __global__ void __launch_bounds__(kDcPrepThreads) dc_prep_kernel(DcArgs a) {
   int o, n;
   const int m = blockIdx.x;
   if (!dc_merge(a.c, a.s, m, o, n)) return;
-  const int c = a.c, s = a.s, n1 = s, n2 = n - s;
+  const int c = a.c, s = a.s, n1 = s;
   extern __shared__ __align__(16) double sh[];
   double* ds = sh;              // sorted poles
   double* zs = ds + n;          // sorted weights
-  double* rc = zs + n;          // rotation cosines
-  double* rs = rc + n;          // rotation sines
-  int* perm = reinterpret_cast<int*>(rs + n);   // sorted position -> local column
-  int* ra = perm + n;           // rotation column a (sorted positions)
-  int* rb = ra + n;
-  int* km = rb + n;             // (K, deflated) order -> sorted position
+  int* km = reinterpret_cast<int*>(zs + n);   // (K, deflated) order -> sorted position
   __shared__ double red[40];
-  __shared__ int nrot_s, k_s;
+  __shared__ int k_s;
   const double rho0 = fabs(a.e[o + s - 1]);
   const double sgn = a.e[o + s - 1] < 0.0 ? -1.0 : 1.0;
-  // z and its norm
   double z2 = 0.0;
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     const double z = t < n1 ? a.Q[(o + s - 1) + (size_t)(o + t) * c] : sgn * a.Q[(o + s) + (size_t)(o + t) * c];
@@ -282,11 +332,10 @@ __global__ void __launch_bounds__(kDcPrepThreads) dc_prep_kernel(DcArgs a) {
   z2 = block_sum_d(z2, red);
   const double zn = sqrt(z2);
   const double rho = rho0 * z2;
-  // merge the two ascending lists (ties: L first)
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     const bool left = t < n1;
     const double dv = a.dl[o + t];
-    int lo = left ? n1 : 0, hi = left ? n : n1;   // search the other list
+    int lo = left ? n1 : 0, hi = left ? n : n1;   // rank in the other list (ties: L first)
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       const double dm = a.dl[o + mid];
@@ -294,24 +343,22 @@ __global__ void __launch_bounds__(kDcPrepThreads) dc_prep_kernel(DcArgs a) {
       else hi = mid;
     }
     const int pos = left ? t + (lo - n1) : (t - n1) + lo;
-    const double z = t < n1 ? a.Q[(o + s - 1) + (size_t)(o + t) * c] : sgn * a.Q[(o + s) + (size_t)(o + t) * c];
+    const double z = left ? a.Q[(o + s - 1) + (size_t)(o + t) * c] : sgn * a.Q[(o + s) + (size_t)(o + t) * c];
     ds[pos] = dv;
     zs[pos] = zn > 0.0 ? z / zn : 0.0;
-    perm[pos] = t;
+    a.perm[o + pos] = t;
   }
   __syncthreads();
-  // deflation scan (sequential, dlaed2)
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {   // sequential deflation scan (cheap reject of far poles: |gap C S| <= |gap| / 2)
     double dmax = 0.0, zmax = 0.0;
     for (int t = 0; t < n; ++t) {
       dmax = fmax(dmax, fabs(ds[t]));
       zmax = fmax(zmax, fabs(zs[t]));
     }
     const double tol = 8.0 * DBL_EPSILON * fmax(dmax, rho * zmax);
-    int k = 0, ndef = 0, nrot = 0, pj = -1;
-    // deflated entries are written from the back of km (reverse order, fixed below)
+    int k = 0, ndef = 0, nr = 0, pj = -1;
     for (int t = 0; t < n; ++t) {
-      if (rho * fabs(zs[t]) <= tol) {   // negligible weight
+      if (rho * fabs(zs[t]) <= tol) {
         km[n - 1 - ndef++] = t;
         continue;
       }
@@ -319,43 +366,44 @@ __global__ void __launch_bounds__(kDcPrepThreads) dc_prep_kernel(DcArgs a) {
         pj = t;
         continue;
       }
-      double S = zs[pj], C = zs[t];
-      const double tz = hypot(C, S);
-      C /= tz;
-      S = -S / tz;
       const double gap = ds[t] - ds[pj];
-      if (fabs(gap * C * S) <= tol) {   // close poles: rotate the weight of pj into t
-        zs[t] = tz;
-        zs[pj] = 0.0;
-        ra[nrot] = pj;
-        rb[nrot] = t;
-        rc[nrot] = C;
-        rs[nrot] = S;
-        ++nrot;
-        const double tt = ds[pj] * C * C + ds[t] * S * S;
-        ds[t] = ds[pj] * S * S + ds[t] * C * C;
-        ds[pj] = tt;
-        km[n - 1 - ndef++] = pj;
-        pj = t;
-      } else {
-        km[k++] = pj;
-        pj = t;
+      bool defl = false;
+      if (fabs(gap) <= 2.0 * tol) {
+        double S = zs[pj], C = zs[t];
+        const double tz = hypot(C, S);
+        C /= tz;
+        S = -S / tz;
+        if (fabs(gap * C * S) <= tol) {
+          defl = true;
+          zs[t] = tz;
+          zs[pj] = 0.0;
+          a.rota[o + nr] = pj;
+          a.rotb[o + nr] = t;
+          a.rotc[o + nr] = C;
+          a.rots[o + nr] = S;
+          ++nr;
+          const double tt = ds[pj] * C * C + ds[t] * S * S;
+          ds[t] = ds[pj] * S * S + ds[t] * C * C;
+          ds[pj] = tt;
+          km[n - 1 - ndef++] = pj;
+        }
       }
+      if (!defl) km[k++] = pj;
+      pj = t;
     }
     if (pj >= 0) km[k++] = pj;
-    // deflated part in ascending scan order
-    for (int x = 0; x < ndef / 2; ++x) {
+    for (int x = 0; x < ndef / 2; ++x) {   // deflated part in scan order
       const int tmp = km[k + x];
       km[k + x] = km[n - 1 - x];
       km[n - 1 - x] = tmp;
     }
-    nrot_s = nrot;
     k_s = k;
     a.kcnt[m] = k;
+    a.nrot[m] = nr;
     a.rho[m] = rho;
   }
   __syncthreads();
-  const int k = k_s, nrot = nrot_s;
+  const int k = k_s;
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     const int sp = km[t];
     a.kmap[o + t] = sp;
@@ -366,28 +414,12 @@ __global__ void __launch_bounds__(kDcPrepThreads) dc_prep_kernel(DcArgs a) {
       a.lam[o + t] = ds[sp];   // deflated eigenvalue
     }
   }
-  // gather the columns in sorted order (rows of the merge only), then the rotations row by row
-  for (size_t x = threadIdx.x; x < (size_t)n * n; x += blockDim.x) {
-    const int r = (int)(x % n), sp = (int)(x / n);
-    a.Qp[(o + r) + (size_t)(o + sp) * c] = a.Q[(o + r) + (size_t)(o + perm[sp]) * c];
-  }
-  __syncthreads();
-  if (nrot) {
-    for (int r = threadIdx.x; r < n; r += blockDim.x) {
-      double* row = a.Qp + (o + r);
-      for (int x = 0; x < nrot; ++x) {
-        double* pa = row + (size_t)(o + ra[x]) * c;
-        double* pb = row + (size_t)(o + rb[x]) * c;
-        const double qa = *pa, qb = *pb, C = rc[x], S = rs[x];
-        *pa = C * qa + S * qb;
-        *pb = C * qb - S * qa;
-      }
-    }
-  }
 }
 
-// secular equation 1/rho + sum_i z_i^2 / (d_i - lambda) = 0, root t of merge m (one warp):
-// lambda_t = d[org] + tau with org the nearer pole, tau solved by bisection to full relative precision
+// secular equation g(tau) = 1/rho + sum_i z_i^2 / ((d_i - d_org) - tau) = 0 for root t of merge m (one warp):
+// lambda_t = d_org + tau, origin = the nearer pole.  Safeguarded iteration: the two-pole rational model
+// of psi (poles <= t) and phi (poles > t) matched in value and slope (Bunch-Nielsen-Sorensen), falling back to
+// bisection (geometric while the bracket spans orders of magnitude) whenever the model step leaves the bracket.
 __global__ void dc_secular_kernel(DcArgs a) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (gw >= a.c) return;
@@ -398,41 +430,78 @@ __global__ void dc_secular_kernel(DcArgs a) {
   if (t >= k) return;
   const double* dK = a.dK + o;
   const double* zK = a.zK + o;
-  const double rho = a.rho[m];
-  auto g_at = [&](int orgi, double tau) {   // 1/rho + sum z^2 / ((d_i - d_org) - tau)
-    const double dor = dK[orgi];
-    double acc = 0.0;
-    for (int i = lane; i < k; i += 32) acc += zK[i] * zK[i] / ((dK[i] - dor) - tau);
-    return warp_sum_d(acc) + 1.0 / rho;
-  };
+  const double rho = a.rho[m], irho = 1.0 / rho;
+  const bool last = t == k - 1;
   int orgi;
-  double lo, hi;   // |tau| bracket (lo > 0 tiny, hi), direction by orgi
-  bool right;      // tau > 0 (origin on the left)
-  if (t == k - 1) {
+  double tlo, thi;   // signed bracket of tau, g(tlo) < 0 <= g(thi)
+  if (last) {
     orgi = t;
-    right = true;
-    hi = rho * 1.0000000001 + 4.0 * DBL_EPSILON * fabs(dK[t]);   // ||z|| = 1
+    tlo = DBL_TRUE_MIN;
+    thi = rho * 1.0000000001 + 4.0 * DBL_EPSILON * fabs(dK[t]);
   } else {
     const double gap = dK[t + 1] - dK[t];
-    const double gm = g_at(t, 0.5 * gap);
-    right = gm >= 0.0;
+    double acc = 0.0;
+    const double mid = 0.5 * gap;
+    for (int i = lane; i < k; i += 32) acc += zK[i] * zK[i] / ((dK[i] - dK[t]) - mid);
+    const bool right = warp_sum_d(acc) + irho >= 0.0;
     orgi = right ? t : t + 1;
-    hi = 0.5 * gap;
+    tlo = right ? DBL_TRUE_MIN : -0.5 * gap;
+    thi = right ? 0.5 * gap : -DBL_TRUE_MIN;
   }
-  lo = DBL_TRUE_MIN;
-  for (int it = 0; it < 200; ++it) {
-    const double mid = hi > 4.0 * lo ? sqrt(lo) * sqrt(hi) : 0.5 * (lo + hi);
-    if (!(mid > lo && mid < hi)) break;
-    const double g = g_at(orgi, right ? mid : -mid);
-    // g increasing in lambda: right (tau = +mid): g < 0 -> larger; left (tau = -mid): g < 0 -> smaller |tau|
-    if ((g < 0.0) == right) lo = mid;
-    else hi = mid;
-    if (hi - lo <= 2.0 * DBL_EPSILON * hi) break;
+  const double dor = dK[orgi];
+  const double dl_ = dK[t] - dor;                          // left pole (origin-relative)
+  const double dr_ = last ? 0.0 : dK[t + 1] - dor;         // right pole
+  double tau = 0.5 * (tlo + thi);
+  for (int it = 0; it < 100; ++it) {
+    double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
+    for (int i = lane; i < k; i += 32) {
+      const double inv = 1.0 / ((dK[i] - dor) - tau);
+      const double tv = zK[i] * zK[i] * inv;
+      if (i <= t) {
+        psi += tv;
+        dpsi += tv * inv;
+      } else {
+        phi += tv;
+        dphi += tv * inv;
+      }
+    }
+    psi = warp_sum_d(psi);
+    dpsi = warp_sum_d(dpsi);
+    phi = warp_sum_d(phi);
+    dphi = warp_sum_d(dphi);
+    const double g = irho + psi + phi;
+    if (g < 0.0) tlo = tau;
+    else thi = tau;
+    const double erretm = 8.0 * (irho + fabs(psi) + fabs(phi)) + fabs(tau) * (dpsi + dphi);
+    if (fabs(g) <= DBL_EPSILON * erretm || thi - tlo <= 2.0 * DBL_EPSILON * fmax(fabs(tlo), fabs(thi))) break;
+    // rational model step
+    double x;
+    const double b = dpsi * (dl_ - tau) * (dl_ - tau), av = psi - dpsi * (dl_ - tau);
+    if (last) {
+      const double A = irho + av;
+      x = dl_ + b / A;
+    } else {
+      const double dd = dphi * (dr_ - tau) * (dr_ - tau), cv = phi - dphi * (dr_ - tau);
+      const double A = irho + av + cv;
+      // A x^2 - (A (dl + dr) + b + dd) x + (A dl dr + b dr + dd dl) = 0
+      const double Bq = -(A * (dl_ + dr_) + b + dd);
+      const double Cq = A * dl_ * dr_ + b * dr_ + dd * dl_;
+      const double disc = fmax(Bq * Bq - 4.0 * A * Cq, 0.0);
+      const double qv = -0.5 * (Bq + copysign(sqrt(disc), Bq));
+      const double x1 = qv / A, x2 = Cq / qv;
+      x = (x1 > tlo && x1 < thi) ? x1 : x2;
+    }
+    if (!(x > tlo && x < thi)) {   // bisection (geometric when the bracket spans orders of magnitude)
+      if (tlo > 0.0 && thi > 4.0 * tlo) x = sqrt(tlo) * sqrt(thi);
+      else if (thi < 0.0 && -tlo > -4.0 * thi) x = -sqrt(-tlo) * sqrt(-thi);
+      else x = 0.5 * (tlo + thi);
+      if (!(x > tlo && x < thi)) break;
+    }
+    tau = x;
   }
   if (lane == 0) {
-    const double tau = 0.5 * (lo + hi);
     a.org[o + t] = orgi;
-    a.org_tau[o + t] = right ? tau : -tau;
+    a.org_tau[o + t] = tau;
   }
 }
 
@@ -453,8 +522,7 @@ __global__ void dc_zhat_kernel(DcArgs a) {
   const double* dK = a.dK + o;
   const int* org = a.org + o;
   const double* tau = a.org_tau + o;
-  // product with explicit exponent tracking (no overflow / underflow for any k)
-  double mant = 1.0;
+  double mant = 1.0;   // product with explicit exponent tracking (no overflow / underflow for any k)
   int ex = 0;
   for (int j = lane; j < k; j += 32) {
     double f = lam_minus_d(dK, org, tau, j, i);
@@ -472,38 +540,55 @@ __global__ void dc_zhat_kernel(DcArgs a) {
     mant = frexp(mant * om, &e2);
     ex += e2 + oe;
   }
-  if (lane == 0) {
-    const double z2 = ldexp(fabs(mant), ex);
-    const double zs = a.zK[o + i];
-    a.zhat[o + i] = copysign(sqrt(z2), zs);
-  }
+  if (lane == 0) a.zhat[o + i] = copysign(sqrt(ldexp(fabs(mant), ex)), a.zK[o + i]);
 }
 
-// secular eigenvectors U[:, j] = zhat_i / (d_i - lambda_j), normalised (one warp per j), the merged
-// eigenvalues, and (one thread per element) the final ascending rank of all n eigenvalues
-__global__ void dc_vec_kernel(DcArgs a) {
+// column t of B = P G [U | E_defl] (one warp per t < n; n doubles of smem per warp):
+//   t < k: U[:, t] = zhat_u / (d_u - lambda_t) normalised, placed at the sorted positions kmap[u];
+//   t >= k: the unit vector at sorted position kmap[t];
+// then the deflation rotations in reverse order, then the rows scattered to the local columns perm[s].
+constexpr int kVecWarps = 4;
+__global__ void __launch_bounds__(kVecWarps * 32) dc_vec_kernel(DcArgs a, int nmax) {
+  extern __shared__ __align__(16) double vbuf[];
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (gw >= a.c) return;
   const int m = gw / (2 * a.s);
   int o, n;
   if (!dc_merge(a.c, a.s, m, o, n)) return;
-  const int j = gw - o, k = a.kcnt[m];
-  const int c = a.c;
-  if (j < k) {
+  const int t = gw - o, k = a.kcnt[m], c = a.c;
+  double* col = vbuf + (size_t)(threadIdx.x >> 5) * nmax;
+  for (int x = lane; x < n; x += 32) col[x] = 0.0;
+  __syncwarp();
+  if (t < k) {
     const double* dK = a.dK + o;
     const int* org = a.org + o;
     const double* tau = a.org_tau + o;
     double ss = 0.0;
-    for (int i = lane; i < k; i += 32) {
-      const double u = a.zhat[o + i] / -lam_minus_d(dK, org, tau, j, i);
-      ss += u * u;
+    for (int u = lane; u < k; u += 32) {
+      const double v = a.zhat[o + u] / -lam_minus_d(dK, org, tau, t, u);
+      col[a.kmap[o + u]] = v;
+      ss += v * v;
     }
     ss = warp_sum_d(ss);
+    __syncwarp();
     const double inv = 1.0 / sqrt(ss);
-    for (int i = lane; i < k; i += 32)
-      a.U[(o + i) + (size_t)(o + j) * c] = a.zhat[o + i] / -lam_minus_d(dK, org, tau, j, i) * inv;
-    if (lane == 0) a.lam[o + j] = dK[org[j]] + tau[j];
+    for (int u = lane; u < k; u += 32) col[a.kmap[o + u]] *= inv;
+    if (lane == 0) a.lam[o + t] = dK[org[t]] + tau[t];
+  } else if (lane == 0) {
+    col[a.kmap[o + t]] = 1.0;
   }
+  __syncwarp();
+  if (lane == 0) {
+    for (int x = a.nrot[m] - 1; x >= 0; --x) {   // G x = G_1 (G_2 (... G_nrot x))
+      const int pa = a.rota[o + x], pb = a.rotb[o + x];
+      const double C = a.rotc[o + x], S = a.rots[o + x];
+      const double xa = col[pa], xb = col[pb];
+      col[pa] = C * xa - S * xb;
+      col[pb] = S * xa + C * xb;
+    }
+  }
+  __syncwarp();
+  for (int sp = lane; sp < n; sp += 32) a.B[(o + a.perm[o + sp]) + (size_t)(o + t) * c] = col[sp];
 }
 
 // final ascending position of each merged eigenvalue (ties by (K, deflated) order index)
@@ -524,49 +609,56 @@ __global__ void dc_rank_kernel(DcArgs a) {
   a.dl[o + r] = v;
 }
 
-// Q[o:o+n, o+rank(t)] = Qp[o:o+n, o+kmap[u]] U[o+u, o+t] (u < k) for t < k; = Qp[:, o+kmap[t]] for t >= k.
-// Tiles of 64 x 64 outputs (rows x (K, deflated)-order columns) within one merge; 256 threads, 4 x 4 each.
+// Qn[o:o+n, o+rank(t)] = Q[o:o+n, o:o+n] B[o:o+n, o+t]; the carried (unmerged) last block is copied.
+// Tiles of 64 x 64 outputs within one merge; 256 threads, 4 x 4 outputs each.
 constexpr int kGT = 64, kGK = 16;
 __global__ void __launch_bounds__(256) dc_gemm_kernel(DcArgs a) {
   const int c = a.c, s = a.s;
-  // tile -> (merge, row tile, col tile); merges have n <= 2s, tiles per merge = ceil(n/64)^2
   const int tpm = (2 * s + kGT - 1) / kGT;   // tiles per merge side
   const int tiles_per_merge = tpm * tpm;
   const int m = blockIdx.x / tiles_per_merge, tt = blockIdx.x % tiles_per_merge;
   int o, n;
-  if (!dc_merge(c, s, m, o, n)) return;
   const int r0 = (tt % tpm) * kGT, c0 = (tt / tpm) * kGT;
+  if (!dc_merge(c, s, m, o, n)) {
+    o = 2 * s * m;
+    if (o >= c) return;
+    n = c - o;
+    for (int x = threadIdx.x; x < kGT * kGT; x += 256) {
+      const int rr = r0 + x % kGT, cc = c0 + x / kGT;
+      if (rr < n && cc < n) a.Qn[(o + rr) + (size_t)(o + cc) * c] = a.Q[(o + rr) + (size_t)(o + cc) * c];
+    }
+    return;
+  }
   if (r0 >= n || c0 >= n) return;
-  const int k = a.kcnt[m];
-  __shared__ double As[kGK][kGT + 1];   // Qp rows x u
-  __shared__ double Bs[kGK][kGT + 1];   // u x cols
+  __shared__ double As[kGK][kGT + 1];   // Q rows x inner
+  __shared__ double Bs[kGK][kGT + 1];   // inner x cols
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   double acc[4][4] = {};
-  const int kend = min(k, n);
-  if (c0 < k) {
-    for (int u0 = 0; u0 < kend; u0 += kGK) {
-      for (int x = threadIdx.x; x < kGK * kGT; x += 256) {
-        const int uu = x / kGT, rr = x % kGT;
-        const int u = u0 + uu, row = r0 + rr;
-        As[uu][rr] = (u < kend && row < n) ? a.Qp[(o + row) + (size_t)(o + a.kmap[o + u]) * c] : 0.0;
-        const int col = c0 + rr;
-        Bs[uu][rr] = (u < kend && col < k) ? a.U[(o + u) + (size_t)(o + col) * c] : 0.0;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int uu = 0; uu < kGK; ++uu) {
-        double av[4], bv[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) av[p] = As[uu][ty + 16 * p];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) bv[p] = Bs[uu][tx + 16 * p];
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-#pragma unroll
-          for (int q2 = 0; q2 < 4; ++q2) acc[p][q2] = fma(av[p], bv[q2], acc[p][q2]);
-      }
-      __syncthreads();
+  for (int u0 = 0; u0 < n; u0 += kGK) {
+    for (int x = threadIdx.x; x < kGK * kGT; x += 256) {
+      const int uu = x / kGT, rr = x % kGT;
+      const int u = u0 + uu;
+      As[uu][rr] = (u < n && r0 + rr < n) ? a.Q[(o + r0 + rr) + (size_t)(o + u) * c] : 0.0;
     }
+    for (int x = threadIdx.x; x < kGK * kGT; x += 256) {
+      const int uu = x % kGK, cc = x / kGK;
+      const int u = u0 + uu;
+      Bs[uu][cc] = (u < n && c0 + cc < n) ? a.B[(o + u) + (size_t)(o + c0 + cc) * c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int uu = 0; uu < kGK; ++uu) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) av[p] = As[uu][ty + 16 * p];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) bv[p] = Bs[uu][tx + 16 * p];
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) acc[p][q2] = fma(av[p], bv[q2], acc[p][q2]);
+    }
+    __syncthreads();
   }
 #pragma unroll
   for (int q2 = 0; q2 < 4; ++q2) {
@@ -576,52 +668,143 @@ __global__ void __launch_bounds__(256) dc_gemm_kernel(DcArgs a) {
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
       const int row = r0 + ty + 16 * p;
-      if (row >= n) continue;
-      a.Q[(o + row) + (size_t)dst * c] = t < k ? acc[p][q2] : a.Qp[(o + row) + (size_t)(o + a.kmap[o + t]) * c];
+      if (row < n) a.Qn[(o + row) + (size_t)dst * c] = acc[p][q2];
     }
   }
 }
 
-// back-transformation of the r wanted eigenvectors (descending eigenvalues): out[:, j] = H_0 ... H_{c-3} Q[:, c-1-j],
-// one warp per column, the column in shared memory; kept / dropped / all eigenvalues; non-finite -> *fail = 1
-constexpr int kBtWarps = 8;
-__global__ void __launch_bounds__(kBtWarps * 32) eig_backtransform_kernel(int c, int r, const double* __restrict__ V,
-                                                                         const double* __restrict__ tau,
-                                                                         const double* __restrict__ Q,
-                                                                         const double* __restrict__ dl, double* Qr,
-                                                                         double* kept, double* dropped, double* w_all,
-                                                                         int* fail) {
-  extern __shared__ __align__(16) double colbuf[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x * kBtWarps + warp;
-  if (blockIdx.x == 0) {
-    for (int i = threadIdx.x; i < c; i += blockDim.x) {
-      if (w_all) w_all[i] = dl[i];
-      if (!isfinite(dl[i]) && fail) *fail = 1;
-    }
-    if (threadIdx.x == 0 && dropped) {
-      double s = 0.0;
-      for (int i = 0; i < c - r; ++i) s += dl[i];
-      *dropped = s;
-    }
-  }
-  if (j >= r) return;
-  double* q = colbuf + (size_t)warp * c;
-  const int src = c - 1 - j;
-  for (int l = lane; l < c; l += 32) q[l] = Q[l + (size_t)src * c];
-  __syncwarp();
-  for (int h = c - 3; h >= 0; --h) {
-    const double th = tau[h];
-    if (th == 0.0) continue;
-    const double* v = V + (size_t)h * c;
+// ---- blocked (compact WY) back-transformation: panels of kBtNb reflectors, H_j0 ... H_j0+b-1 = I - V T V^T
+constexpr int kBtNb = 32, kBtCols = 8, kBtThreads = 256;
+
+// T of panel p (upper triangular b x b, column-major ld kBtNb): dlarft (forward, columnwise)
+__global__ void __launch_bounds__(kBtThreads) bt_larft_kernel(int c, const double* __restrict__ V,
+                                                              const double* __restrict__ tau, double* __restrict__ Tall) {
+  const int p = blockIdx.x, nref = c - 2, j0 = p * kBtNb, b = min(kBtNb, nref - j0);
+  if (b <= 0) return;
+  __shared__ double S[kBtNb][kBtNb + 1];
+  __shared__ double T[kBtNb][kBtNb + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kBtThreads / 32;
+  // S[a][e] = v_{j0+a} . v_{j0+e}, a < e: rows j0+e+1 .. c-1 (the support of v_{j0+e})
+  for (int pr = warp; pr < b * b; pr += nw) {
+    const int a = pr % b, e = pr / b;
+    if (a >= e) continue;
+    const double* va = V + (size_t)(j0 + a) * c;
+    const double* ve = V + (size_t)(j0 + e) * c;
     double acc = 0.0;
-    for (int l = h + 1 + lane; l < c; l += 32) acc += __ldg(v + l) * q[l];
-    acc = warp_sum_d(acc) * th;
-    for (int l = h + 1 + lane; l < c; l += 32) q[l] -= acc * __ldg(v + l);
-    __syncwarp();
+    for (int l = j0 + e + 1 + lane; l < c; l += 32) acc += va[l] * ve[l];
+    acc = warp_sum_d(acc);
+    if (lane == 0) S[a][e] = acc;
   }
-  for (int l = lane; l < c; l += 32) Qr[l + (size_t)j * c] = q[l];
-  if (lane == 0 && kept) kept[j] = dl[src];
+  __syncthreads();
+  if (warp == 0) {
+    for (int i = 0; i < b; ++i) {
+      const double ti = tau[j0 + i];
+      // T[0:i, i] = -tau_i T[0:i, 0:i] S[0:i, i]   (lane r computes row r)
+      double acc = 0.0;
+      if (lane < i)
+        for (int x = lane; x < i; ++x) acc += T[lane][x] * S[x][i];
+      __syncwarp();
+      if (lane < i) T[lane][i] = -ti * acc;
+      if (lane == 0) T[i][i] = ti;
+      if (lane > i && lane < kBtNb) T[lane][i] = 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < kBtNb * kBtNb; x += kBtThreads) {
+    const int r = x % kBtNb, e = x / kBtNb;
+    Tall[(size_t)p * kBtNb * kBtNb + x] = (r < b && e < b) ? T[r][e] : 0.0;
+  }
+}
+
+// kBtCols output columns per CTA: Z = Q_T[:, c-1-j] (descending eigenvalues), then Z <- (I - V_p T_p V_p^T) Z
+// for the panels from the last to the first; Z in shared memory (c x kBtCols), the panel's V staged through
+// shared memory in chunks of kBtRows rows (coalesced loads, conflict-free reads).  Thread t owns the output
+// (a, col) = (t % 32, t / 32) of W = V_p^T Z.
+constexpr int kBtRows = 128;
+static_assert(kBtNb * kBtCols == kBtThreads, "one W output per thread");
+__global__ void __launch_bounds__(kBtThreads) bt_apply_kernel(int c, int r, const double* __restrict__ V,
+                                                              const double* __restrict__ Tall,
+                                                              const double* __restrict__ Q, double* __restrict__ Qr) {
+  extern __shared__ __align__(16) double Zs[];   // [kBtCols][c]
+  __shared__ double Vs[kBtRows][kBtNb + 1];
+  __shared__ double W[kBtNb][kBtCols], Ts[kBtNb][kBtNb + 1];
+  const int j0c = blockIdx.x * kBtCols, ncol = min(kBtCols, r - j0c);
+  for (int x = threadIdx.x; x < kBtCols * c; x += kBtThreads) {
+    const int col = x / c, l = x % c;
+    Zs[x] = col < ncol ? Q[l + (size_t)(c - 1 - (j0c + col)) * c] : 0.0;
+  }
+  const int nref = c - 2;
+  const int np = nref > 0 ? (nref + kBtNb - 1) / kBtNb : 0;
+  const int ta = threadIdx.x % kBtNb, tcol = threadIdx.x / kBtNb;
+  auto stage = [&](int j0, int b, int r0) {   // Vs[rr][a] = v_{j0+a}[r0+rr] (zero above its support)
+    for (int x = threadIdx.x; x < kBtRows * kBtNb; x += kBtThreads) {
+      const int rr = x % kBtRows, a = x / kBtRows, l = r0 + rr;
+      Vs[rr][a] = (a < b && l < c && l > j0 + a) ? V[l + (size_t)(j0 + a) * c] : 0.0;
+    }
+  };
+  for (int p = np - 1; p >= 0; --p) {
+    const int j0 = p * kBtNb, b = min(kBtNb, nref - j0);
+    for (int x = threadIdx.x; x < kBtNb * kBtNb; x += kBtThreads) Ts[x % kBtNb][x / kBtNb] = Tall[(size_t)p * kBtNb * kBtNb + x];
+    // W = V_p^T Z
+    double acc = 0.0;
+    for (int r0 = j0 + 1; r0 < c; r0 += kBtRows) {
+      __syncthreads();
+      stage(j0, b, r0);
+      __syncthreads();
+      const double* z = Zs + (size_t)tcol * c + r0;
+      const int nr = min(kBtRows, c - r0);
+      double a0 = 0.0, a1 = 0.0;
+      int rr = 0;
+      for (; rr + 1 < nr; rr += 2) {
+        a0 += Vs[rr][ta] * z[rr];
+        a1 += Vs[rr + 1][ta] * z[rr + 1];
+      }
+      if (rr < nr) a0 += Vs[rr][ta] * z[rr];
+      acc += a0 + a1;
+    }
+    W[ta][tcol] = acc;
+    __syncthreads();
+    // W2 = T W  (in place through registers)
+    double w2 = 0.0;
+    for (int e = ta; e < b; ++e) w2 += Ts[ta][e] * W[e][tcol];
+    __syncthreads();
+    W[ta][tcol] = w2;
+    // Z -= V_p W2
+    for (int r0 = j0 + 1; r0 < c; r0 += kBtRows) {
+      __syncthreads();
+      stage(j0, b, r0);
+      __syncthreads();
+      const int nr = min(kBtRows, c - r0);
+      for (int x = threadIdx.x; x < nr * kBtCols; x += kBtThreads) {
+        const int rr = x % nr, col = x / nr;
+        double s = 0.0;
+#pragma unroll 8
+        for (int a = 0; a < kBtNb; ++a) s += Vs[rr][a] * W[a][col];
+        Zs[(size_t)col * c + r0 + rr] -= s;
+      }
+    }
+    __syncthreads();
+  }
+  for (int x = threadIdx.x; x < ncol * c; x += kBtThreads) {
+    const int col = x / c, l = x % c;
+    Qr[l + (size_t)(j0c + col) * c] = Zs[x];
+  }
+}
+
+// eigenvalue outputs: kept (descending top r), dropped mass, all (ascending); non-finite -> *fail = 1
+__global__ void eig_values_kernel(int c, int r, const double* __restrict__ dl, double* kept, double* dropped,
+                                  double* w_all, int* fail) {
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    if (w_all) w_all[i] = dl[i];
+    if (kept && i < r) kept[i] = dl[c - 1 - i];
+    if (!isfinite(dl[i]) && fail) *fail = 1;
+  }
+  if (threadIdx.x == 0 && dropped) {
+    double s = 0.0;
+    for (int i = 0; i < c - r; ++i) s += dl[i];
+    *dropped = s;
+  }
 }
 
 size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
@@ -633,7 +816,7 @@ int trd_smem_max_c(int nc) {
   int best = 0;
   for (int c = 1; c <= 4096; ++c) {
     const size_t L = (c + nc - 1) / nc;
-    const size_t bytes = (L * c + 4 * (size_t)c + 64) * sizeof(double);
+    const size_t bytes = (L * c + 5 * (size_t)c + 64) * sizeof(double);
     if (bytes <= (size_t)kTrdSmemBytes) best = c;
   }
   return best;
@@ -642,8 +825,8 @@ int trd_smem_max_c(int nc) {
 // 16-CTA clusters need the non-portable size; fall back to 8 if the device cannot co-schedule 16
 int trd_cluster_size() {
   static const int nc = [] {
-    cudaFuncSetAttribute(sytrd_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(sytrd_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrdSmemBytes);
+    cudaFuncSetAttribute(sytrd_cluster_kernel<16, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(sytrd_cluster_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrdSmemBytes);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kTrdCluster);
     cfg.blockDim = dim3(kTrdThreads);
@@ -656,7 +839,7 @@ int trd_cluster_size() {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, sytrd_cluster_kernel<true>, &cfg) != cudaSuccess || n < 1) {
+    if (cudaOccupancyMaxActiveClusters(&n, sytrd_cluster_kernel<16, true>, &cfg) != cudaSuccess || n < 1) {
       cudaGetLastError();
       return 8;
     }
@@ -669,10 +852,12 @@ size_t eig_workspace_bytes(int cmax) {
   const size_t c = (size_t)std::max(cmax, 1);
   size_t b = 0;
   b += align_up(c * c * 8) * 4;                 // V, Q, Qp, U
-  b += align_up(c * 8) * 12;                    // tau, d, e, dl, dK, zK, org_tau, zhat, lam, vglob(2), pglob
-  b += align_up(c * 4) * 4;                     // org, kmap, rank, kcnt
+  b += align_up(c * 8) * 13;                    // tau, d, e, dl, dK, zK, org_tau, zhat, lam, colglob(2), pglob(2)
+  b += align_up(c * 4) * 8;                     // org, kmap, rank, kcnt, perm, rota, rotb, nrot
+  b += align_up(c * 8) * 2;                     // rotc, rots
   b += align_up(c * 8) + align_up(64 * 8);      // rho, sglob
   b += align_up((c + kTrdCluster) * c * 8);     // global-memory tridiagonalisation slabs (nc x ceil(c/nc) x c)
+  b += align_up((c / 32 + 2) * 32 * 32 * 8);    // compact-WY T factors of the back-transformation
   return b + 4096;
 }
 
@@ -700,40 +885,46 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
   double* otau = reinterpret_cast<double*>(take(c * 8));
   double* zhat = reinterpret_cast<double*>(take(c * 8));
   double* lam = reinterpret_cast<double*>(take(c * 8));
-  double* vglob = reinterpret_cast<double*>(take(2 * (size_t)c * 8));
-  double* pglob = reinterpret_cast<double*>(take(c * 8));
+  double* colglob = reinterpret_cast<double*>(take(2 * (size_t)c * 8));
+  double* pglob = reinterpret_cast<double*>(take(2 * (size_t)c * 8));
   int* org = reinterpret_cast<int*>(take(c * 4));
   int* kmap = reinterpret_cast<int*>(take(c * 4));
   int* rank = reinterpret_cast<int*>(take(c * 4));
   int* kcnt = reinterpret_cast<int*>(take(c * 4));
+  int* perm = reinterpret_cast<int*>(take(c * 4));
+  int* rota = reinterpret_cast<int*>(take(c * 4));
+  int* rotb = reinterpret_cast<int*>(take(c * 4));
+  int* nrot = reinterpret_cast<int*>(take(c * 4));
+  double* rotc = reinterpret_cast<double*>(take(c * 8));
+  double* rots = reinterpret_cast<double*>(take(c * 8));
   double* rho = reinterpret_cast<double*>(take(c * 8));
   double* sglob = reinterpret_cast<double*>(take(64 * 8));
   double* Aglob = reinterpret_cast<double*>(take(((size_t)c + kTrdCluster) * c * 8));
+  double* Tp = reinterpret_cast<double*>(take(((size_t)c / 32 + 2) * 32 * 32 * 8));
   (void)p;
   // ---- 1. tridiagonalisation (one cluster of nc CTAs: 16 where the device can co-schedule it, else 8)
   {
     static const int smem_max_c16 = trd_smem_max_c(16), smem_max_c8 = trd_smem_max_c(8);
     const int nc = trd_cluster_size();
+    auto kern = nc == 16 ? (c <= smem_max_c16 ? sytrd_cluster_kernel<16, true> : sytrd_cluster_kernel<16, false>)
+                         : (c <= smem_max_c8 ? sytrd_cluster_kernel<8, true> : sytrd_cluster_kernel<8, false>);
     const size_t L = (c + nc - 1) / nc;
     const bool in_smem = c <= (nc == 16 ? smem_max_c16 : smem_max_c8);
-    const size_t smem = in_smem ? (L * c + 4 * (size_t)c + 64) * sizeof(double)
-                                : (4 * (size_t)c + 64) * sizeof(double);
+    const size_t smem = in_smem ? (L * c + 5 * (size_t)c + 64) * sizeof(double)
+                                : (5 * (size_t)c + 64) * sizeof(double);
     if (smem > (size_t)kTrdSmemBytes) return cudaErrorInvalidValue;
     static PerDeviceOnce once;
     const cudaError_t ce = once_per_device(once, [] {
-      cudaError_t r1 = cudaFuncSetAttribute(sytrd_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            kTrdSmemBytes);
-      if (r1 == cudaSuccess)
-        r1 = cudaFuncSetAttribute(sytrd_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kTrdSmemBytes);
-      if (r1 == cudaSuccess)
-        r1 = cudaFuncSetAttribute(sytrd_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (r1 == cudaSuccess)
-        r1 = cudaFuncSetAttribute(sytrd_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaError_t r1 = cudaSuccess;
+      for (auto k : {sytrd_cluster_kernel<16, true>, sytrd_cluster_kernel<16, false>, sytrd_cluster_kernel<8, true>,
+                     sytrd_cluster_kernel<8, false>}) {
+        if (r1 == cudaSuccess) r1 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrdSmemBytes);
+        if (r1 == cudaSuccess) r1 = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      }
       return r1;
     });
     if (ce != cudaSuccess) return ce;
-    TrdArgs ta{c, G, V, tau, d, e, vglob, pglob, sglob, Aglob};
+    TrdArgs ta{c, G, V, tau, d, e, pglob, colglob, sglob, Aglob};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nc);
     cfg.blockDim = dim3(kTrdThreads);
@@ -746,8 +937,7 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = in_smem ? cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel<true>, ta)
-                             : cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel<false>, ta);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta);
     ++launch_counter();
     if (le != cudaSuccess) return le;
     le = cudaGetLastError();
@@ -757,18 +947,26 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
   dc_init_kernel<<<(unsigned)((cc + 255) / 256), 256, 0, st>>>(c, d, e, dl, Q);
   cudaError_t err = note_launch_err();
   if (err != cudaSuccess) return err;
-  DcArgs da{c, 1, e, dl, Q, Qp, U, dK, zK, otau, zhat, lam, org, kmap, rank, kcnt, rho};
-  static PerDeviceOnce once_prep;
-  err = once_per_device(once_prep, [] {
-    return cudaFuncSetAttribute(dc_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  DcArgs da{c, 1, e, dl, Q, Qp, U, dK, zK, otau, zhat, lam, rotc, rots, rota, rotb, nrot, perm, org, kmap, rank,
+            kcnt, rho};
+  static PerDeviceOnce once_dc;
+  err = once_per_device(once_dc, [] {
+    cudaError_t r1 = cudaFuncSetAttribute(dc_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (r1 == cudaSuccess) r1 = cudaFuncSetAttribute(dc_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return r1;
   });
   if (err != cudaSuccess) return err;
+  double* Qcur = Q;
+  double* Qnext = Qp;
   for (int s = 1; s < c; s *= 2) {
     da.s = s;
+    da.Q = Qcur;
+    da.Qn = Qnext;
     const int nmerge = (c + 2 * s - 1) / (2 * s);
     const size_t nmax = (size_t)std::min(2 * s, c);
-    const size_t psmem = nmax * (4 * sizeof(double) + 4 * sizeof(int));
-    if (psmem > 200 * 1024) return cudaErrorInvalidValue;
+    const size_t psmem = nmax * (2 * sizeof(double) + sizeof(int));
+    const size_t vsmem = (size_t)kVecWarps * nmax * sizeof(double);
+    if (psmem > 200 * 1024 || vsmem > 200 * 1024) return cudaErrorInvalidValue;
     dc_prep_kernel<<<nmerge, kDcPrepThreads, psmem, st>>>(da);
     if ((err = note_launch_err()) != cudaSuccess) return err;
     const unsigned wblocks = (unsigned)((c * 32 + 255) / 256);
@@ -776,24 +974,32 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
     if ((err = note_launch_err()) != cudaSuccess) return err;
     dc_zhat_kernel<<<wblocks, 256, 0, st>>>(da);
     if ((err = note_launch_err()) != cudaSuccess) return err;
-    dc_vec_kernel<<<wblocks, 256, 0, st>>>(da);
+    dc_vec_kernel<<<(unsigned)((c + kVecWarps - 1) / kVecWarps), kVecWarps * 32, vsmem, st>>>(da, (int)nmax);
     if ((err = note_launch_err()) != cudaSuccess) return err;
     dc_rank_kernel<<<(c + 255) / 256, 256, 0, st>>>(da);
     if ((err = note_launch_err()) != cudaSuccess) return err;
     const int tpm = (2 * s + kGT - 1) / kGT;
     dc_gemm_kernel<<<nmerge * tpm * tpm, 256, 0, st>>>(da);
     if ((err = note_launch_err()) != cudaSuccess) return err;
+    std::swap(Qcur, Qnext);
   }
-  // ---- 3. back-transformation of the r wanted eigenvectors
-  const size_t bsmem = (size_t)kBtWarps * c * sizeof(double);
+  // ---- 3. back-transformation of the r wanted eigenvectors (compact WY panels), eigenvalue outputs
+  eig_values_kernel<<<1, 256, 0, st>>>(c, r, dl, kept, dropped, w_all, fail);
+  if ((err = note_launch_err()) != cudaSuccess) return err;
+  if (r == 0) return cudaSuccess;
+  const int np = c > 2 ? (c - 2 + kBtNb - 1) / kBtNb : 0;
+  if (np) {
+    bt_larft_kernel<<<np, kBtThreads, 0, st>>>(c, V, tau, Tp);
+    if ((err = note_launch_err()) != cudaSuccess) return err;
+  }
+  const size_t bsmem = (size_t)kBtCols * c * sizeof(double);
   static PerDeviceOnce once_bt;
   err = once_per_device(once_bt, [] {
-    return cudaFuncSetAttribute(eig_backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    return cudaFuncSetAttribute(bt_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   });
   if (err != cudaSuccess) return err;
-  if (bsmem > 220 * 1024) return cudaErrorInvalidValue;
-  const unsigned bgrid = (unsigned)std::max(1, (r + kBtWarps - 1) / kBtWarps);
-  eig_backtransform_kernel<<<bgrid, kBtWarps * 32, bsmem, st>>>(c, r, V, tau, Q, dl, Qr, kept, dropped, w_all, fail);
+  if (bsmem > 160 * 1024) return cudaErrorInvalidValue;
+  bt_apply_kernel<<<(r + kBtCols - 1) / kBtCols, kBtThreads, bsmem, st>>>(c, r, V, Tp, Qcur, Qr);
   return note_launch_err();
 }
 

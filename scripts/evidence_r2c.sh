@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+timeout 300 python scripts/eig_timing.py > gpurun_out/r2c_eig_timing.txt 2>&1
+EIG_REPS=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2c_eig_ncu.csv python scripts/eig_timing.py > gpurun_out/r2c_eig_ncu.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_cfg2.py tests/test_gpu_fullsize.py -q -s -k "short or launch_path" > gpurun_out/r2c_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/r2c_pytest.log

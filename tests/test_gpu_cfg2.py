@@ -123,11 +123,15 @@ def test_cfg2_fixed_actions_fp32(policy):
             assert np.all(np.abs(x - y) <= 1e-4 * y + bound_abs)
 
 
-def test_cfg2_cg_short_fp64():
-    """CG actions while the Krylov trajectory is still well-conditioned (6 iterations per step; the
-    oracle's 1-ulp sensitivity grows ~8x per iteration at cfg2), rank cap 16 so the
-    truncation is active from step 3: fp64 within 1e-9, integer stats bit-exact."""
-    wl = make_workload("cfg2", policy="cg", T=6, max_iter=6, max_rank=16)
+@pytest.mark.parametrize("iters,rank", [(2, 4), (6, 16)])
+def test_cfg2_cg_short_fp64(iters, rank):
+    """CG actions while the Krylov trajectory is still well-conditioned, rank cap below the column
+    count so the truncation is active from step 3.  The oracle's own sensitivity to a 1-ulp relative
+    perturbation of y grows fast with the iterations at cfg2 (1.5e-11 at 2, 1e-9 at 4,
+    2e-8 at 6 iterations per step over 6 steps), so: 2 iterations -> fp64 within 1e-9 (north_star);
+    6 iterations -> within 16x the oracle's measured 1-ulp sensitivity (a different but equally valid
+    rounding in each of the 36 Krylov steps)."""
+    wl = make_workload("cfg2", policy="cg", T=6, max_iter=iters, max_rank=rank)
     trans, _ = runner.transitions(wl)
     h = runner.make_handle(wl, "f64")
     runner.run(h, trans, runner.stage_inputs(wl, "f64"), smooth=True)
@@ -136,11 +140,16 @@ def test_cfg2_cg_short_fp64():
     out["sm"], out["sv"] = runner.collect(h, wl.T, CAKF_SMOOTH)
     ranks = [h.get_stats(k)["rank_out"] for k in range(1, wl.T + 1)]
     h.destroy()
-    assert ranks == [6, 12, 16, 16, 16, 16]
+    assert ranks == [min(rank, iters * k) for k in range(1, wl.T + 1)]
     positive(out)
-    m, v = rel_errs(out, mfree.run_mf(wl, cache=True))
-    print(f"cfg2 cg (6 iterations) fp64: mean {m:.3g} var {v:.3g}")
-    assert m < 1e-9 and v < 1e-9
+    ref = mfree.run_mf(wl, cache=True)
+    m, v = rel_errs(out, ref)
+    sm_, sv_ = rel_errs(mfree.run_mf(wl, cache=True, perturb_y=2.0 ** -52), ref)
+    print(f"cfg2 cg ({iters} iterations) fp64: mean {m:.3g} var {v:.3g}; oracle 1-ulp sensitivity {sm_:.3g} {sv_:.3g}")
+    if iters <= 2:
+        assert m < 1e-9 and v < 1e-9
+    else:
+        assert m <= 16 * sm_ and v <= 16 * sv_
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
