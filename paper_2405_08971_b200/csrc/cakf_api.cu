@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1185,6 +1186,33 @@ struct Impl final : ImplBase {
       return CAKF_OK;
     }
     CK_CUDA(eig_top(c, rkeep, Gm, eigws, eigws_bytes, QrD, kept, dropped, nullptr, failflag, st));
+    static const bool check = env_is("CAKF_EIG_CHECK", '1');
+    if (check) {   // debug: residual of the returned eigenpairs against the (lower) Gram, on the host
+      std::vector<double> G((size_t)c * c), Q((size_t)c * rkeep), w(c);
+      CK_CUDA(cudaStreamSynchronize(st));
+      CK_CUDA(cudaMemcpy(G.data(), Gm, G.size() * 8, cudaMemcpyDeviceToHost));
+      CK_CUDA(cudaMemcpy(Q.data(), QrD, Q.size() * 8, cudaMemcpyDeviceToHost));
+      double gmax = 0, res = 0, orth = 0;
+      for (int i = 0; i < c; ++i)
+        for (int j = 0; j <= i; ++j) gmax = std::max(gmax, std::fabs(G[i + (size_t)j * c]));
+      for (int t = 0; t < rkeep; ++t) {
+        const double* q = &Q[(size_t)t * c];
+        std::vector<double> gq(c, 0.0);
+        for (int i = 0; i < c; ++i)
+          for (int j = 0; j < c; ++j) gq[i] += (i >= j ? G[i + (size_t)j * c] : G[j + (size_t)i * c]) * q[j];
+        double lam = 0;
+        for (int i = 0; i < c; ++i) lam += q[i] * gq[i];
+        double rr = 0;
+        for (int i = 0; i < c; ++i) rr += (gq[i] - lam * q[i]) * (gq[i] - lam * q[i]);
+        res = std::max(res, std::sqrt(rr) / gmax);
+        for (int u = 0; u < t; ++u) {
+          double dd = 0;
+          for (int i = 0; i < c; ++i) dd += q[i] * Q[(size_t)u * c + i];
+          orth = std::max(orth, std::fabs(dd));
+        }
+      }
+      fprintf(stderr, "eig check c=%d r=%d: residual %.3e orthogonality %.3e\n", c, rkeep, res, orth);
+    }
     return CAKF_OK;
   }
 
@@ -1954,12 +1982,24 @@ int cakf_sym_eig(int64_t c, int64_t r, const double* G, double* w, double* Qr, v
   const size_t cc = (size_t)c * c, wsb = eig_workspace_bytes((int)c);
   double *Gd = nullptr, *wd = nullptr, *Qd = nullptr;
   int* fl = nullptr;
-  void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&Gd, cc * sizeof(double), st);
+  // one process-wide workspace, reused by successive calls like a handle's (grown when c grows)
+  static std::mutex ws_mu;
+  static void* ws_keep = nullptr;
+  static size_t ws_keep_bytes = 0;
+  std::lock_guard<std::mutex> lock(ws_mu);
+  cudaError_t e = cudaSuccess;
+  if (ws_keep_bytes < wsb) {
+    if (ws_keep) cudaFree(ws_keep);
+    ws_keep = nullptr;
+    ws_keep_bytes = 0;
+    e = cudaMalloc(&ws_keep, wsb);
+    if (e == cudaSuccess) ws_keep_bytes = wsb;
+  }
+  void* ws = ws_keep;
+  if (e == cudaSuccess) e = cudaMallocAsync(&Gd, cc * sizeof(double), st);
   if (e == cudaSuccess) e = cudaMallocAsync(&wd, (size_t)c * sizeof(double), st);
   if (e == cudaSuccess) e = cudaMallocAsync(&Qd, (size_t)c * std::max<int64_t>(r, 1) * sizeof(double), st);
   if (e == cudaSuccess) e = cudaMallocAsync(&fl, sizeof(int), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&ws, wsb, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(Gd, G, cc * sizeof(double), cudaMemcpyDefault, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(fl, 0, sizeof(int), st);
   if (e == cudaSuccess) e = eig_top((int)c, (int)r, Gd, ws, wsb, Qd, nullptr, nullptr, wd, fl, st);
@@ -1967,7 +2007,7 @@ int cakf_sym_eig(int64_t c, int64_t r, const double* G, double* w, double* Qr, v
   if (e == cudaSuccess && w) e = cudaMemcpyAsync(w, wd, (size_t)c * sizeof(double), cudaMemcpyDefault, st);
   if (e == cudaSuccess && Qr && r) e = cudaMemcpyAsync(Qr, Qd, (size_t)c * r * sizeof(double), cudaMemcpyDefault, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&hf, fl, sizeof(int), cudaMemcpyDeviceToHost, st);
-  for (void* p : {(void*)Gd, (void*)wd, (void*)Qd, (void*)fl, ws})
+  for (void* p : {(void*)Gd, (void*)wd, (void*)Qd, (void*)fl})
     if (p) cudaFreeAsync(p, st);
   const cudaError_t e2 = cudaStreamSynchronize(st);
   if (e != cudaSuccess || e2 != cudaSuccess)

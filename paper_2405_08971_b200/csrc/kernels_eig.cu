@@ -1,27 +1,28 @@
 // kernels_eig.cu — the truncation's symmetric eigensolver (a8 / a9 Truncate, Sec. 3.2 P:334-369,
 // "SVD of M M^T" P:367, reading R4: eigh of the c x c Gram M^T M), fp64, entirely on the device.
 //
-//   1. Householder tridiagonalisation  C = H T H^T  in ONE thread-block cluster (16 CTAs, the
-//      matrix resident in their shared memory for c <= kTrdSmemMaxC, else in L2-resident global
-//      memory): reflector j is computed by the CTA owning column j; the symmetric matvec p = tau A v
-//      is column-parallel (every CTA owns whole columns, cyclically), the rank-2 update of step j is
-//      fused into the matvec pass of step j+1 (one pass over the trailing matrix per step), v and p
-//      are exchanged through L2 between two cluster barriers per step.
-//   2. Cuppen divide and conquer on T (leaves of size 1, one level per launch group): rank-one
-//      merges with deflation (small z, close poles by Givens rotation), the secular equation solved
-//      per root by bisection in the distance to the nearest pole (full relative accuracy, one warp
-//      per root), Gu-Eisenstat recomputation of z so the merged eigenvectors are orthogonal, and
-//      the eigenvector update as an fp64 GEMM per merge.
-//   3. Back-transformation of the r wanted eigenvectors (descending eigenvalues): q <- H_0 ... H_{c-3} q,
-//      one warp per column.
+//   1. Householder tridiagonalisation  C = H T H^T  in ONE thread-block cluster (16 CTAs; the matrix
+//      resident in their shared memory for c <= ~600, else in L2-resident global memory), one cluster
+//      barrier per column: every CTA owns whole columns (cyclically); the rank-2 update of step j is
+//      fused into the matvec pass of step j+1; p is exchanged through distributed shared memory and the
+//      next column through L2; every CTA then computes the next reflector itself.
+//   2. Cuppen divide and conquer on T (leaves of size 1, six launches per level): rank-one merges with
+//      deflation (negligible weight; close poles by Givens rotation), the secular equation per root by a
+//      safeguarded two-pole rational iteration in the distance to the nearer pole, Gu-Eisenstat
+//      recomputation of z (orthogonal vectors without reorthogonalisation), and the eigenvector update
+//      Q_block B as an fp64 GEMM per merge (B = sort permutation x deflation rotations x secular vectors).
+//   3. Back-transformation of the r wanted eigenvectors (descending eigenvalues) in compact-WY panels of
+//      32 reflectors (T factors by dlarft, then Z <- (I - V T V^T) Z per panel, 4 columns per CTA).
 // The outputs replace cusolverDnDsyevd + take_top: Q_r (c x r, column-major), the kept eigenvalues
 // (descending), the dropped mass (sum of the c - r smallest) and optionally all eigenvalues ascending.
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -73,32 +74,40 @@ struct TrdArgs {
 
 
 // Householder tridiagonalisation in one cluster of NC CTAs, ONE cluster barrier per step:
-//   step j: (a) fused pass over my columns i > j: apply update(j-1) (A -= v w^T + w v^T) to rows > j and form
-//               p_i = tau_j A[:, i] . v_j; the owner of column j+1 also publishes that column (post update(j-1));
+//   step j: (a) fused pass over my columns i > j (two columns per warp, two rows per lane as double2):
+//               apply update(j-1) (A -= v w^T + w v^T) to the rows > j and form p_i = tau_j A[:, i] . v_j into
+//               my shared memory; the owner of column j+1 also publishes that column (post update(j-1)) in L2;
 //           (b) cluster barrier;
-//           (c) every CTA reads p, the partial dots and column j+1 (one L2 round trip), forms w_j, applies
-//               update(j) to column j+1 and computes reflector j+1 itself (identical arithmetic in every CTA,
-//               no second barrier).  Rows are spread one per thread (loops only for c > blockDim).
-// Reflector convention (LAPACK dlarfg): H = I - tau v v^T, H x = beta e_1, v[j+1] = 1.
+//           (c) every CTA reads p (DSMEM, from the column owners), the partial dots (DSMEM) and column j+1 (L2),
+//               forms w_j, applies update(j) to column j+1 and computes reflector j+1 itself (identical
+//               arithmetic in every CTA, no second barrier).
+// Layout: local columns with an even stride ldA >= c + 1 (the rows in [c, ldA) and the row entries of v / w
+// at and above c are zero), so the double2 pass may start one row early and run one row past the end.
+// Reflector convention (LAPACK dlarfg): H = I - tau v v^T, H x = beta e_1, v[j+1] = 1, v[j] = 0.
+__host__ __device__ constexpr int trd_ld(int c) { return (c + 2) & ~1; }
+
 template <int NC, bool SMEM>
 __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   const int q = (int)cl.block_rank();
-  const int c = a.c;
+  const int c = a.c, ld = trd_ld(c);
   const int L = (c + NC - 1) / NC;
   extern __shared__ __align__(16) double sm[];
-  double* A = SMEM ? sm : a.Aglob + (size_t)q * L * c;
-  double* vb = SMEM ? sm + (size_t)L * c : sm;   // [2][c]  v_j by step parity
-  double* wb = vb + 2 * (size_t)c;                // [2][c]  w_j by step parity
-  double* pb = wb + 2 * (size_t)c;                // [c]     raw p, then the updated column j+1
-  double* red = pb + (size_t)c;                   // [64]    red[40 + parity] = tau_j
+  double* A = SMEM ? sm : a.Aglob + (size_t)q * L * ld;
+  double* vb = SMEM ? sm + (size_t)L * ld : sm;   // [2][ld]  v_j by step parity
+  double* wb = vb + 2 * (size_t)ld;                // [2][ld]  w_j by step parity
+  double* pb = wb + 2 * (size_t)ld;                // [2][ld]  p_i of my columns by step parity (read by the cluster)
+  double* prw = pb + 2 * (size_t)ld;               // [ld]     p of every row (gathered)
+  double* xb = prw + (size_t)ld;                   // [ld]     column j+1
+  double* red = xb + (size_t)ld;                   // [64]     red[36 + parity] = my partial dot, red[40 + parity] = tau_j
   const int nloc = q < c ? (c - q + NC - 1) / NC : 0;   // my columns i = q + NC * lc
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, bd = blockDim.x;
   const bool writer = q == 0;
-  for (size_t x = tid; x < (size_t)nloc * c; x += bd) {
-    const int lc = (int)(x / c), l = (int)(x % c), i = q + NC * lc;
-    A[x] = l >= i ? a.G[l + (size_t)i * c] : a.G[i + (size_t)l * c];
+  for (size_t x = tid; x < (size_t)nloc * ld; x += bd) {
+    const int lc = (int)(x / ld), l = (int)(x % ld), i = q + NC * lc;
+    A[x] = l >= c ? 0.0 : l >= i ? a.G[l + (size_t)i * c] : a.G[i + (size_t)l * c];
   }
+  for (int x = tid; x < 8 * ld; x += bd) vb[x] = 0.0;   // v, w, p, x buffers incl. the padding rows
   if (c <= 2) {
     if (writer && tid == 0) {
       a.d[0] = a.G[0];
@@ -132,6 +141,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
       if (writer) a.V[l + (size_t)jr * c] = v;
     }
     if (tid == 0) {
+      vout[jr] = 0.0;
       red[40 + (jr & 1)] = tau;
       if (writer) {
         a.tau[jr] = tau;
@@ -140,112 +150,147 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
       }
     }
   };
-  for (int l = tid; l < c; l += bd) pb[l] = a.G[l];   // column 0 of G: no update yet
   __syncthreads();
-  reflector(0, pb, pb[0], vb);
+  for (int l = tid; l < c; l += bd) xb[l] = a.G[l];   // column 0 of G: no update yet
   __syncthreads();
+  reflector(0, xb, xb[0], vb);
+  __syncthreads();
+#ifdef CAKF_TRD_TIMING
+  long long tacc[8] = {};
+  long long tprev = clock64();
+#define TRD_T(k)                       \
+  {                                    \
+    const long long tn_ = clock64();   \
+    tacc[k] += tn_ - tprev;            \
+    tprev = tn_;                       \
+  }
+#else
+#define TRD_T(k)
+#endif
   for (int j = 0; j + 3 <= c; ++j) {
     const int par = j & 1;
-    const double* vj = vb + (size_t)par * c;
-    const double* vprev = vb + (size_t)(par ^ 1) * c;
-    const double* wprev = wb + (size_t)(par ^ 1) * c;
-    double* wj = wb + (size_t)par * c;
-    double* pg = a.pglob + (size_t)par * c;
+    const double* vj = vb + (size_t)par * ld;
+    const double* vprev = vb + (size_t)(par ^ 1) * ld;
+    const double* wprev = wb + (size_t)(par ^ 1) * ld;
+    double* wj = wb + (size_t)par * ld;
     double* cg_ = a.colglob + (size_t)par * c;
-    double* sg = a.sglob + (size_t)par * NC;
+    double* pbp = pb + (size_t)par * ld;
     const double tj = red[40 + par];
-    // ---- (a) fused pass
+    // ---- (a) fused pass: column pairs (lcA, lcA + 1) per warp, row pairs per lane
     const int lc0 = q > j ? 0 : (j - q) / NC + 1;   // first local column with i > j
+    const int r0 = (j + 1) & ~1;                     // first row pair (row j is dead: v_j[j] = 0)
     double sq = 0.0;
-    for (int lc = lc0 + warp; lc < nloc; lc += nwarps) {
-      const int i = q + NC * lc;
-      double* col = A + (size_t)lc * c;
-      double acc0 = 0.0, acc1 = 0.0;
-      int l = j + 1 + lane;
-      if (j > 0) {
-        const double vpi = vprev[i], wpi = wprev[i];
-        if (i == j + 1) {
-          for (; l < c; l += 32) {
-            const double x = col[l] - vprev[l] * wpi - wprev[l] * vpi;
-            col[l] = x;
-            cg_[l] = x;
-            acc0 += x * vj[l];
-          }
-        } else {
-          for (; l + 32 < c; l += 64) {
-            const double x0 = col[l] - vprev[l] * wpi - wprev[l] * vpi;
-            const double x1 = col[l + 32] - vprev[l + 32] * wpi - wprev[l + 32] * vpi;
-            col[l] = x0;
-            col[l + 32] = x1;
-            acc0 += x0 * vj[l];
-            acc1 += x1 * vj[l + 32];
-          }
-          if (l < c) {
-            const double x0 = col[l] - vprev[l] * wpi - wprev[l] * vpi;
-            col[l] = x0;
-            acc0 += x0 * vj[l];
-          }
+    for (int lcA = lc0 + 2 * warp; lcA < nloc; lcA += 2 * nwarps) {
+      const bool hasB = lcA + 1 < nloc;
+      const int iA = q + NC * lcA, iB = iA + NC;
+      double* colA = A + (size_t)lcA * ld;
+      double* colB = A + (size_t)(lcA + 1) * ld;
+      const double vpA = vprev[iA], wpA = wprev[iA];
+      const double vpB = hasB ? vprev[iB] : 0.0, wpB = hasB ? wprev[iB] : 0.0;
+      const bool pubA = iA == j + 1, pubB = hasB && iB == j + 1;
+      double accA = 0.0, accB = 0.0;
+      for (int r = r0 + 2 * lane; r < c; r += 64) {
+        const double2 vp = *reinterpret_cast<const double2*>(vprev + r);
+        const double2 wp = *reinterpret_cast<const double2*>(wprev + r);
+        const double2 vv = *reinterpret_cast<const double2*>(vj + r);
+        double2 xa = *reinterpret_cast<double2*>(colA + r);
+        if (j > 0) {
+          xa.x -= vp.x * wpA + wp.x * vpA;
+          xa.y -= vp.y * wpA + wp.y * vpA;
+          *reinterpret_cast<double2*>(colA + r) = xa;
         }
-      } else {
-        for (; l < c; l += 32) {
-          const double x = col[l];
-          if (i == j + 1) cg_[l] = x;
-          acc0 += x * vj[l];
+        accA += xa.x * vv.x + xa.y * vv.y;
+        if (pubA) {
+          if (r >= j + 1) cg_[r] = xa.x;
+          if (r + 1 < c) cg_[r + 1] = xa.y;
+        }
+        if (hasB) {
+          double2 xb2 = *reinterpret_cast<double2*>(colB + r);
+          if (j > 0) {
+            xb2.x -= vp.x * wpB + wp.x * vpB;
+            xb2.y -= vp.y * wpB + wp.y * vpB;
+            *reinterpret_cast<double2*>(colB + r) = xb2;
+          }
+          accB += xb2.x * vv.x + xb2.y * vv.y;
+          if (pubB) {
+            if (r >= j + 1) cg_[r] = xb2.x;
+            if (r + 1 < c) cg_[r + 1] = xb2.y;
+          }
         }
       }
-      const double acc = warp_sum_d(acc0 + acc1);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        accA += __shfl_xor_sync(0xffffffffu, accA, off);
+        accB += __shfl_xor_sync(0xffffffffu, accB, off);
+      }
       if (lane == 0) {
-        const double p = tj * acc;
-        pg[i] = p;
-        sq += p * vj[i];
+        const double pA = tj * accA;
+        pbp[iA] = pA;
+        sq += pA * vj[iA];
+        if (hasB) {
+          const double pB = tj * accB;
+          pbp[iB] = pB;
+          sq += pB * vj[iB];
+        }
       }
     }
+    TRD_T(0)
     if (lane == 0) red[warp] = sq;
     __syncthreads();
+    TRD_T(1)
     if (warp == 0) {
       double t = lane < nwarps ? red[lane] : 0.0;
       t = warp_sum_d(t);
-      if (lane == 0) sg[q] = t;
+      if (lane == 0) red[36 + par] = t;
     }
     // ---- (b)
     cl.sync();
-    // ---- (c) raw p and column j+1 into smem, the NC partial dots (warp 0): one L2 round trip
-    double* xcol = wb + (size_t)(par ^ 1) * c;   // w_{j-1}: consumed by (a), free until step j+1 writes w_{j+1}
+    TRD_T(2)
+    // ---- (c) p from the column owners (DSMEM), column j+1 (L2), the partial dots (DSMEM, warp 0)
     for (int l = j + 1 + tid; l < c; l += bd) {
-      pb[l] = __ldcg(pg + l);
-      xcol[l] = __ldcg(cg_ + l);
+      prw[l] = cl.map_shared_rank(pbp, l % NC)[l];
+      xb[l] = __ldcg(cg_ + l);
     }
     if (warp == 0) {
-      double t = lane < NC ? __ldcg(sg + lane) : 0.0;
+      double t = 0.0;
+      if (lane < NC) t = cl.map_shared_rank(red, lane)[36 + par];
       t = warp_sum_d(t);
       if (lane == 0) red[35] = t;
     }
     __syncthreads();
+    TRD_T(3)
     const double hk = 0.5 * tj * red[35];
-    const double vn = vj[j + 1], wn = pb[j + 1] - hk * vn;
+    const double vn = vj[j + 1], wn = prw[j + 1] - hk * vn;
     for (int l = j + 1 + tid; l < c; l += bd) {
-      const double w = pb[l] - hk * vj[l];
+      const double w = prw[l] - hk * vj[l];
       wj[l] = w;
-      xcol[l] -= vj[l] * wn + w * vn;   // update(j) of column j+1
+      xb[l] -= vj[l] * wn + w * vn;   // update(j) of column j+1
     }
     if (j + 4 <= c) {
-      __syncthreads();   // the reflector reads rows of column j+1 updated by other threads
-      reflector(j + 1, xcol, xcol[j + 1], vb + (size_t)(par ^ 1) * c);
-    } else if (writer) {   // j + 1 == c - 2: the last 2 x 2 block's column c-2
-      for (int l = j + 1 + tid; l < c; l += bd) {
-        if (l == c - 2) a.d[c - 2] = xcol[l];
-        if (l == c - 1) a.e[c - 2] = xcol[l];
-      }
+      __syncthreads();   // the reflector reads rows of column j+1 computed by other threads
+      TRD_T(4)
+      reflector(j + 1, xb, xb[j + 1], vb + (size_t)(par ^ 1) * ld);
+      TRD_T(5)
+    } else if (writer && tid == 0) {   // j + 1 == c - 2: the last 2 x 2 block's column c-2
+      a.d[c - 2] = xb[c - 2];
+      a.e[c - 2] = xb[c - 1];
     }
-    __syncthreads();
+    __syncthreads();   // xb / wj / vb complete before the next pass; pb, red[36..] are double-buffered
+    TRD_T(6)
   }
+#ifdef CAKF_TRD_TIMING
+  if (tid == 0 && (q == 0 || q == 1 || q == NC - 1))
+    printf("trd cta %d c %d: pass %lld sync1 %lld cl.sync %lld loads %lld xupd %lld refl %lld end %lld (cycles/step)\n", q,
+           c, tacc[0] / (c - 2), tacc[1] / (c - 2), tacc[2] / (c - 2), tacc[3] / (c - 2), tacc[4] / (c - 2),
+           tacc[5] / (c - 2), tacc[6] / (c - 2));
+#endif
   // ---- d[c-1]: column c-1 (owner) after update(c-3): row c-1 only
   {
     const int j = c - 3, par = j & 1, i = c - 1;
-    const double* vj = vb + (size_t)par * c;
-    const double* wj = wb + (size_t)par * c;
+    const double* vj = vb + (size_t)par * ld;
+    const double* wj = wb + (size_t)par * ld;
     if (q == i % NC && tid == 0) {
-      const double* col = A + (size_t)(i / NC) * c;
+      const double* col = A + (size_t)(i / NC) * ld;
       a.d[c - 1] = col[c - 1] - 2.0 * vj[c - 1] * wj[c - 1];
     }
   }
@@ -610,9 +655,10 @@ __global__ void dc_rank_kernel(DcArgs a) {
 }
 
 // Qn[o:o+n, o+rank(t)] = Q[o:o+n, o:o+n] B[o:o+n, o+t]; the carried (unmerged) last block is copied.
-// Tiles of 64 x 64 outputs within one merge; 256 threads, 4 x 4 outputs each.
-constexpr int kGT = 64, kGK = 16;
-__global__ void __launch_bounds__(256) dc_gemm_kernel(DcArgs a) {
+// 32 x 32 output tiles (many CTAs: the GEMMs are small and latency-bound), 64 threads with 4 x 4 outputs each,
+// K chunks of 32 double-buffered through registers.
+constexpr int kGT = 32, kGK = 32, kGThreads = 64;
+__global__ void __launch_bounds__(kGThreads) dc_gemm_kernel(DcArgs a) {
   const int c = a.c, s = a.s;
   const int tpm = (2 * s + kGT - 1) / kGT;   // tiles per merge side
   const int tiles_per_merge = tpm * tpm;
@@ -623,58 +669,71 @@ __global__ void __launch_bounds__(256) dc_gemm_kernel(DcArgs a) {
     o = 2 * s * m;
     if (o >= c) return;
     n = c - o;
-    for (int x = threadIdx.x; x < kGT * kGT; x += 256) {
+    for (int x = threadIdx.x; x < kGT * kGT; x += kGThreads) {
       const int rr = r0 + x % kGT, cc = c0 + x / kGT;
       if (rr < n && cc < n) a.Qn[(o + rr) + (size_t)(o + cc) * c] = a.Q[(o + rr) + (size_t)(o + cc) * c];
     }
     return;
   }
   if (r0 >= n || c0 >= n) return;
-  __shared__ double As[kGK][kGT + 1];   // Q rows x inner
-  __shared__ double Bs[kGK][kGT + 1];   // inner x cols
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  __shared__ double As[kGK][kGT + 1];   // [inner][row]
+  __shared__ double Bs[kGK][kGT + 1];   // [inner][col]
+  const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;   // 8 x 8 threads, outputs (ty + 8p, tx + 8q)
   double acc[4][4] = {};
-  for (int u0 = 0; u0 < n; u0 += kGK) {
-    for (int x = threadIdx.x; x < kGK * kGT; x += 256) {
-      const int uu = x / kGT, rr = x % kGT;
-      const int u = u0 + uu;
-      As[uu][rr] = (u < n && r0 + rr < n) ? a.Q[(o + r0 + rr) + (size_t)(o + u) * c] : 0.0;
+  double ra[16], rb[16];
+  // Q_block is block-diagonal (L = [0, s), R = [s, n)): its off-diagonal blocks are never stored (they hold
+  // stale data) and contribute zero; a row tile entirely in L (R) runs over the inner range of L (R) only
+  const int ulo = r0 >= s ? s : 0, uhi = r0 + kGT <= s ? s : n;
+  auto fetch = [&](int u0) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int x = threadIdx.x + e * kGThreads;     // 0 .. 1023
+      const int rr = x % kGT, uu = x / kGT;          // A: rows contiguous
+      const int u = u0 + uu, row = r0 + rr;
+      ra[e] = (u < uhi && row < n && ((row < s) == (u < s))) ? a.Q[(o + row) + (size_t)(o + u) * c] : 0.0;
+      const int ub = x % kGK, cc = x / kGK;          // B: inner contiguous
+      rb[e] = (u0 + ub < uhi && c0 + cc < n) ? a.B[(o + u0 + ub) + (size_t)(o + c0 + cc) * c] : 0.0;
     }
-    for (int x = threadIdx.x; x < kGK * kGT; x += 256) {
-      const int uu = x % kGK, cc = x / kGK;
-      const int u = u0 + uu;
-      Bs[uu][cc] = (u < n && c0 + cc < n) ? a.B[(o + u) + (size_t)(o + c0 + cc) * c] : 0.0;
+  };
+  fetch(ulo);
+  for (int u0 = ulo; u0 < uhi; u0 += kGK) {
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int x = threadIdx.x + e * kGThreads;
+      As[x / kGT][x % kGT] = ra[e];
+      Bs[x % kGK][x / kGK] = rb[e];
     }
     __syncthreads();
+    if (u0 + kGK < uhi) fetch(u0 + kGK);
 #pragma unroll
     for (int uu = 0; uu < kGK; ++uu) {
       double av[4], bv[4];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) av[p] = As[uu][ty + 16 * p];
+      for (int p = 0; p < 4; ++p) av[p] = As[uu][ty + 8 * p];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) bv[p] = Bs[uu][tx + 16 * p];
+      for (int p = 0; p < 4; ++p) bv[p] = Bs[uu][tx + 8 * p];
 #pragma unroll
       for (int p = 0; p < 4; ++p)
 #pragma unroll
         for (int q2 = 0; q2 < 4; ++q2) acc[p][q2] = fma(av[p], bv[q2], acc[p][q2]);
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int q2 = 0; q2 < 4; ++q2) {
-    const int t = c0 + tx + 16 * q2;
+    const int t = c0 + tx + 8 * q2;
     if (t >= n) continue;
     const int dst = o + a.rank[o + t];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      const int row = r0 + ty + 16 * p;
+      const int row = r0 + ty + 8 * p;
       if (row < n) a.Qn[(o + row) + (size_t)dst * c] = acc[p][q2];
     }
   }
 }
 
 // ---- blocked (compact WY) back-transformation: panels of kBtNb reflectors, H_j0 ... H_j0+b-1 = I - V T V^T
-constexpr int kBtNb = 32, kBtCols = 8, kBtThreads = 256;
+constexpr int kBtNb = 32, kBtCols = 4, kBtThreads = 256;
 
 // T of panel p (upper triangular b x b, column-major ld kBtNb): dlarft (forward, columnwise)
 __global__ void __launch_bounds__(kBtThreads) bt_larft_kernel(int c, const double* __restrict__ V,
@@ -718,16 +777,16 @@ __global__ void __launch_bounds__(kBtThreads) bt_larft_kernel(int c, const doubl
 }
 
 // kBtCols output columns per CTA: Z = Q_T[:, c-1-j] (descending eigenvalues), then Z <- (I - V_p T_p V_p^T) Z
-// for the panels from the last to the first; Z in shared memory (c x kBtCols), the panel's V staged through
-// shared memory in chunks of kBtRows rows (coalesced loads, conflict-free reads).  Thread t owns the output
-// (a, col) = (t % 32, t / 32) of W = V_p^T Z.
-constexpr int kBtRows = 128;
-static_assert(kBtNb * kBtCols == kBtThreads, "one W output per thread");
-__global__ void __launch_bounds__(kBtThreads) bt_apply_kernel(int c, int r, const double* __restrict__ V,
+// for the panels from the last to the first; Z in shared memory (c x kBtCols), the panel's V rows staged
+// once per panel into shared memory (in chunks of `rmax` rows only when the panel does not fit).
+// Thread t owns the output (a, col) = (t % 32, t / 32) of W = V_p^T Z.
+constexpr int kBtPad = kBtNb + 1;
+static_assert(kBtNb * kBtCols <= kBtThreads, "one W output per thread");
+__global__ void __launch_bounds__(kBtThreads) bt_apply_kernel(int c, int r, int rmax, const double* __restrict__ V,
                                                               const double* __restrict__ Tall,
                                                               const double* __restrict__ Q, double* __restrict__ Qr) {
-  extern __shared__ __align__(16) double Zs[];   // [kBtCols][c]
-  __shared__ double Vs[kBtRows][kBtNb + 1];
+  extern __shared__ __align__(16) double Zs[];   // [kBtCols][c], then Vs[rmax][kBtPad]
+  double* Vs = Zs + (size_t)kBtCols * c;
   __shared__ double W[kBtNb][kBtCols], Ts[kBtNb][kBtNb + 1];
   const int j0c = blockIdx.x * kBtCols, ncol = min(kBtCols, r - j0c);
   for (int x = threadIdx.x; x < kBtCols * c; x += kBtThreads) {
@@ -737,51 +796,60 @@ __global__ void __launch_bounds__(kBtThreads) bt_apply_kernel(int c, int r, cons
   const int nref = c - 2;
   const int np = nref > 0 ? (nref + kBtNb - 1) / kBtNb : 0;
   const int ta = threadIdx.x % kBtNb, tcol = threadIdx.x / kBtNb;
-  auto stage = [&](int j0, int b, int r0) {   // Vs[rr][a] = v_{j0+a}[r0+rr] (zero above its support)
-    for (int x = threadIdx.x; x < kBtRows * kBtNb; x += kBtThreads) {
-      const int rr = x % kBtRows, a = x / kBtRows, l = r0 + rr;
-      Vs[rr][a] = (a < b && l < c && l > j0 + a) ? V[l + (size_t)(j0 + a) * c] : 0.0;
+  const bool wown = threadIdx.x < kBtNb * kBtCols;
+  auto stage = [&](int j0, int b, int r0, int nr) {   // Vs[rr][a] = v_{j0+a}[r0+rr] (zero above its support)
+    for (int x = threadIdx.x; x < nr * kBtNb; x += kBtThreads) {
+      const int rr = x % nr, a = x / nr, l = r0 + rr;
+      Vs[(size_t)rr * kBtPad + a] = (a < b && l > j0 + a) ? __ldg(V + l + (size_t)(j0 + a) * c) : 0.0;
     }
   };
   for (int p = np - 1; p >= 0; --p) {
     const int j0 = p * kBtNb, b = min(kBtNb, nref - j0);
+    const int r00 = j0 + 1, nrows = c - r00;
+    const bool one = nrows <= rmax;
     for (int x = threadIdx.x; x < kBtNb * kBtNb; x += kBtThreads) Ts[x % kBtNb][x / kBtNb] = Tall[(size_t)p * kBtNb * kBtNb + x];
     // W = V_p^T Z
-    double acc = 0.0;
-    for (int r0 = j0 + 1; r0 < c; r0 += kBtRows) {
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int r0 = r00; r0 < c; r0 += rmax) {
+      const int nr = min(rmax, c - r0);
       __syncthreads();
-      stage(j0, b, r0);
+      stage(j0, b, r0, nr);
       __syncthreads();
-      const double* z = Zs + (size_t)tcol * c + r0;
-      const int nr = min(kBtRows, c - r0);
-      double a0 = 0.0, a1 = 0.0;
-      int rr = 0;
-      for (; rr + 1 < nr; rr += 2) {
-        a0 += Vs[rr][ta] * z[rr];
-        a1 += Vs[rr + 1][ta] * z[rr + 1];
+      if (wown) {
+        const double* z = Zs + (size_t)tcol * c + r0;
+        int rr = 0;
+        for (; rr + 1 < nr; rr += 2) {
+          acc0 += Vs[(size_t)rr * kBtPad + ta] * z[rr];
+          acc1 += Vs[(size_t)(rr + 1) * kBtPad + ta] * z[rr + 1];
+        }
+        if (rr < nr) acc0 += Vs[(size_t)rr * kBtPad + ta] * z[rr];
       }
-      if (rr < nr) a0 += Vs[rr][ta] * z[rr];
-      acc += a0 + a1;
     }
-    W[ta][tcol] = acc;
+    if (wown) W[ta][tcol] = acc0 + acc1;
     __syncthreads();
-    // W2 = T W  (in place through registers)
-    double w2 = 0.0;
-    for (int e = ta; e < b; ++e) w2 += Ts[ta][e] * W[e][tcol];
+    double w2 = 0.0;   // W2 = T W
+    if (wown)
+      for (int e = ta; e < b; ++e) w2 += Ts[ta][e] * W[e][tcol];
     __syncthreads();
-    W[ta][tcol] = w2;
+    if (wown) W[ta][tcol] = w2;
     // Z -= V_p W2
-    for (int r0 = j0 + 1; r0 < c; r0 += kBtRows) {
+    for (int r0 = r00; r0 < c; r0 += rmax) {
+      const int nr = min(rmax, c - r0);
+      if (!one) {
+        __syncthreads();
+        stage(j0, b, r0, nr);
+      }
       __syncthreads();
-      stage(j0, b, r0);
-      __syncthreads();
-      const int nr = min(kBtRows, c - r0);
       for (int x = threadIdx.x; x < nr * kBtCols; x += kBtThreads) {
         const int rr = x % nr, col = x / nr;
-        double s = 0.0;
-#pragma unroll 8
-        for (int a = 0; a < kBtNb; ++a) s += Vs[rr][a] * W[a][col];
-        Zs[(size_t)col * c + r0 + rr] -= s;
+        const double* vr = Vs + (size_t)rr * kBtPad;
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int a = 0; a < kBtNb; a += 2) {
+          s0 += vr[a] * W[a][col];
+          s1 += vr[a + 1] * W[a + 1][col];
+        }
+        Zs[(size_t)col * c + r0 + rr] -= s0 + s1;
       }
     }
     __syncthreads();
@@ -816,7 +884,8 @@ int trd_smem_max_c(int nc) {
   int best = 0;
   for (int c = 1; c <= 4096; ++c) {
     const size_t L = (c + nc - 1) / nc;
-    const size_t bytes = (L * c + 5 * (size_t)c + 64) * sizeof(double);
+    const size_t ld = trd_ld(c);
+    const size_t bytes = (L * ld + 8 * ld + 64) * sizeof(double);
     if (bytes <= (size_t)kTrdSmemBytes) best = c;
   }
   return best;
@@ -856,7 +925,7 @@ size_t eig_workspace_bytes(int cmax) {
   b += align_up(c * 4) * 8;                     // org, kmap, rank, kcnt, perm, rota, rotb, nrot
   b += align_up(c * 8) * 2;                     // rotc, rots
   b += align_up(c * 8) + align_up(64 * 8);      // rho, sglob
-  b += align_up((c + kTrdCluster) * c * 8);     // global-memory tridiagonalisation slabs (nc x ceil(c/nc) x c)
+  b += align_up((c + kTrdCluster) * (c + 2) * 8);   // global-memory tridiagonalisation slabs (nc x ceil(c/nc) x ld)
   b += align_up((c / 32 + 2) * 32 * 32 * 8);    // compact-WY T factors of the back-transformation
   return b + 4096;
 }
@@ -899,7 +968,7 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
   double* rots = reinterpret_cast<double*>(take(c * 8));
   double* rho = reinterpret_cast<double*>(take(c * 8));
   double* sglob = reinterpret_cast<double*>(take(64 * 8));
-  double* Aglob = reinterpret_cast<double*>(take(((size_t)c + kTrdCluster) * c * 8));
+  double* Aglob = reinterpret_cast<double*>(take(((size_t)c + kTrdCluster) * ((size_t)c + 2) * 8));
   double* Tp = reinterpret_cast<double*>(take(((size_t)c / 32 + 2) * 32 * 32 * 8));
   (void)p;
   // ---- 1. tridiagonalisation (one cluster of nc CTAs: 16 where the device can co-schedule it, else 8)
@@ -910,8 +979,8 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
                          : (c <= smem_max_c8 ? sytrd_cluster_kernel<8, true> : sytrd_cluster_kernel<8, false>);
     const size_t L = (c + nc - 1) / nc;
     const bool in_smem = c <= (nc == 16 ? smem_max_c16 : smem_max_c8);
-    const size_t smem = in_smem ? (L * c + 5 * (size_t)c + 64) * sizeof(double)
-                                : (5 * (size_t)c + 64) * sizeof(double);
+    const size_t ldt = trd_ld(c);
+    const size_t smem = in_smem ? (L * ldt + 8 * ldt + 64) * sizeof(double) : (8 * ldt + 64) * sizeof(double);
     if (smem > (size_t)kTrdSmemBytes) return cudaErrorInvalidValue;
     static PerDeviceOnce once;
     const cudaError_t ce = once_per_device(once, [] {
@@ -979,7 +1048,7 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
     dc_rank_kernel<<<(c + 255) / 256, 256, 0, st>>>(da);
     if ((err = note_launch_err()) != cudaSuccess) return err;
     const int tpm = (2 * s + kGT - 1) / kGT;
-    dc_gemm_kernel<<<nmerge * tpm * tpm, 256, 0, st>>>(da);
+    dc_gemm_kernel<<<nmerge * tpm * tpm, kGThreads, 0, st>>>(da);
     if ((err = note_launch_err()) != cudaSuccess) return err;
     std::swap(Qcur, Qnext);
   }
@@ -992,14 +1061,17 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
     bt_larft_kernel<<<np, kBtThreads, 0, st>>>(c, V, tau, Tp);
     if ((err = note_launch_err()) != cudaSuccess) return err;
   }
-  const size_t bsmem = (size_t)kBtCols * c * sizeof(double);
+  constexpr size_t kBtSmem = 200 * 1024;   // + ~9 KB static (W, T)
+  const size_t zbytes = (size_t)kBtCols * c * sizeof(double);
+  if (zbytes + 64 * kBtPad * sizeof(double) > kBtSmem) return cudaErrorInvalidValue;
+  const int rmax = (int)std::min<size_t>((size_t)std::max(c - 1, 1), (kBtSmem - zbytes) / (kBtPad * sizeof(double)));
+  const size_t bsmem = zbytes + (size_t)rmax * kBtPad * sizeof(double);
   static PerDeviceOnce once_bt;
   err = once_per_device(once_bt, [] {
-    return cudaFuncSetAttribute(bt_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    return cudaFuncSetAttribute(bt_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBtSmem);
   });
   if (err != cudaSuccess) return err;
-  if (bsmem > 160 * 1024) return cudaErrorInvalidValue;
-  bt_apply_kernel<<<(r + kBtCols - 1) / kBtCols, kBtThreads, bsmem, st>>>(c, r, V, Tp, Qcur, Qr);
+  bt_apply_kernel<<<(r + kBtCols - 1) / kBtCols, kBtThreads, bsmem, st>>>(c, r, rmax, V, Tp, Qcur, Qr);
   return note_launch_err();
 }
 

@@ -116,3 +116,13 @@ def test_truncation_gram_from_cakf_run_c576():
     assert err < 1e-9
     assert abs(h.get_stats(9)["dropped_mass"] - np.sort(np.linalg.eigvalsh(G))[:64].sum()) <= 1e-9 * ref[0]
     h.destroy()
+
+
+def test_workspace_reuse_across_sizes():
+    """Successive calls share one workspace (as a handle's truncations do) with changing c: nothing may
+    depend on the workspace's previous contents (e.g. the never-stored off-diagonal blocks of the
+    divide-and-conquer's block-diagonal eigenvector matrices)."""
+    rng = np.random.default_rng(77)
+    for c in (576, 16, 18, 40, 16, 333, 17, 64, 576):
+        A = rng.standard_normal((c, c))
+        check(A + A.T, max(1, c - 7))
