@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcakf.so")
 SOURCES = ["kernels_gram.cu", "kernels_gram_tc.cu", "kernels_gemm_tc.cu", "kernels_gemm_i8.cu", "kd_order.cu", "kernels_step.cu", "kernels_eig.cu",
-           "cakf_api.cu"]
+           "kernels_gemm_f64.cu", "cakf_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 try:  # NCCL as bundled with torch (nvidia-nccl wheel): headers + libnccl.so.2
     import nvidia.nccl as _nccl
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
             print(out)
     tmp = lib + ".tmp"
     nccl_lib = os.path.join(NCCL_DIR, "lib")
-    link = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcublas", "-lcusolver", "-L", nccl_lib, "-l:libnccl.so.2",
+    link = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcusolver", "-L", nccl_lib, "-l:libnccl.so.2",
             "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-Xlinker", "-rpath," + nccl_lib]
     r = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:

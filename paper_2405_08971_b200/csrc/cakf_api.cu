@@ -10,7 +10,6 @@
 //               post-loop (Y, U, tmp), truncation (Gram, eig, Q_r, M~), smoother (X, Y, y, W^s)
 // Everything is enqueued on one stream without host synchronisation between the
 // calls (iteration counts and ranks are host-known integers, R2/R3).
-#include <cublas_v2.h>
 #include <cusolverDn.h>
 #include <nccl.h>
 
@@ -46,14 +45,6 @@ int fail(int code, const std::string& msg) {
       failed_ = true;                                                                           \
       return fail(e_ == cudaErrorMemoryAllocation ? CAKF_E_NOMEM : CAKF_E_CUDA,                 \
                   std::string(#expr) + ": " + cudaGetErrorString(e_));                          \
-    }                                                                                           \
-  } while (0)
-#define CK_BLAS(expr)                                                                           \
-  do {                                                                                          \
-    cublasStatus_t s_ = (expr);                                                                 \
-    if (s_ != CUBLAS_STATUS_SUCCESS) {                                                          \
-      failed_ = true;                                                                           \
-      return fail(CAKF_E_CUDA, std::string(#expr) + ": cublas status " + std::to_string(s_));   \
     }                                                                                           \
   } while (0)
 #define CK_SOLVER(expr)                                                                         \
@@ -154,27 +145,7 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-template <typename T> struct Blas;
-template <> struct Blas<float> {
-  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k,
-                             float alpha, const float* A, int lda, const float* B, int ldb, float beta, float* C,
-                             int ldc) {
-    return cublasSgemm(h, ta, tb, m, n, k, &alpha, A, lda, B, ldb, &beta, C, ldc);
-  }
-  static cublasStatus_t axpy(cublasHandle_t h, int n, float a, const float* x, float* y) {
-    return cublasSaxpy(h, n, &a, x, 1, y, 1);
-  }
-};
-template <> struct Blas<double> {
-  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k,
-                             double alpha, const double* A, int lda, const double* B, int ldb, double beta, double* C,
-                             int ldc) {
-    return cublasDgemm(h, ta, tb, m, n, k, &alpha, A, lda, B, ldb, &beta, C, ldc);
-  }
-  static cublasStatus_t axpy(cublasHandle_t h, int n, double a, const double* x, double* y) {
-    return cublasDaxpy(h, n, &a, x, 1, y, 1);
-  }
-};
+constexpr bool OP_N = false, OP_T = true;   // op(X) = X / X^T of the low-rank contractions
 
 struct ImplBase {
   virtual ~ImplBase() = default;
@@ -213,7 +184,6 @@ struct Impl final : ImplBase {
   double* part2 = nullptr;
   double* hmw = nullptr;   // HM u (fp64 rows), formed on the side stream
   bool side = [] { const char* e = getenv("CAKF_NO_SIDE_STREAM"); return !(e && e[0] == '1'); }();
-  cublasHandle_t blas = nullptr;
   cusolverDnHandle_t sol = nullptr;
 
   // ---------------- device memory
@@ -259,8 +229,9 @@ struct Impl final : ImplBase {
   T* Mtil = nullptr;
   double* QrD = nullptr;
   // fp64 scratch of the low-rank contractions (fp32 storage, fp64 accumulation)
-  double *dA = nullptr, *dB = nullptr, *dC = nullptr;
-  size_t dscr = 0;
+  size_t dscr = 0;          // largest low-rank operand (elements): sizes the tensor-core operand planes
+  double* fwork = nullptr;  // split-K partials of the FP64-pipe GEMM
+  static constexpr size_t kF64WorkDoubles = (size_t)4 << 20;
   // smoother
   T *X = nullptr, *Yk = nullptr, *yb = nullptr, *Tm = nullptr, *Hy = nullptr, *tt = nullptr, *R = nullptr;
   T *Wf = nullptr, *Ws = nullptr, *ws = nullptr, *pvar = nullptr;
@@ -474,7 +445,6 @@ struct Impl final : ImplBase {
     if (ctl_init_host) cudaFreeHost(ctl_init_host);
     if (neq_h) cudaFreeHost(neq_h);
     if (comm) ncclCommDestroy(comm);
-    if (blas) cublasDestroy(blas);
     if (sol) cusolverDnDestroy(sol);
     if (own_stream && st) cudaStreamDestroy(st);
     if (st2) cudaStreamDestroy(st2);
@@ -563,12 +533,8 @@ struct Impl final : ImplBase {
                                (size_t)std::max(rin_max, 1) * C1, (size_t)std::max(nhat, 1) * C1,
                                (size_t)cmax * (size_t)std::max(rcap, 1), (size_t)Nmax * (size_t)(1 + nhat),
                                (size_t)std::max(rin_max, 1) * (size_t)(1 + nhat)});
-      {   // fp64 staging of the DGEMM contractions
-        dA = carve<double>(dscr);
-        dB = carve<double>(dscr);
-        dC = carve<double>(dscr);
-      }
     }
+    fwork = carve<double>(kF64WorkDoubles);
     const size_t C = 1 + qmax;
     X = carve<T>((size_t)D * C);
     Yk = carve<T>((size_t)D * C);
@@ -689,8 +655,6 @@ struct Impl final : ImplBase {
       CK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
       own_stream = true;
     }
-    if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) return fail(CAKF_E_CUDA, "cublasCreate failed");
-    CK_BLAS(cublasSetStream(blas, st));
     if (c.max_rank >= 0 && eig_cusolver) {
       if (cusolverDnCreate(&sol) != CUSOLVER_STATUS_SUCCESS) return fail(CAKF_E_CUDA, "cusolverDnCreate failed");
       CK_SOLVER(cusolverDnSetStream(sol, st));
@@ -798,7 +762,7 @@ struct Impl final : ImplBase {
     if (b) {   // user point order -> internal order (unpermute with the inverse permutation)
       CK_CUDA(cudaMemcpyAsync(outm, b, D * sizeof(T), cudaMemcpyDefault, st));
       CK_CUDA(unpermute<T>((int)NX, Dp, invperm_d, outm, tmp, st));
-      CK_BLAS(Blas<T>::axpy(blas, (int)D, T(1), tmp, S.m_pred));
+      CK_CUDA(axpy<T>((size_t)D, 1.0, tmp, S.m_pred, st));
     }
     const T* src = P.truncated ? Mtil : P.Mk;
     const int rin = P.truncated ? P.rank_out : P.cols;
@@ -1070,8 +1034,8 @@ struct Impl final : ImplBase {
     prof_end(CAKF_PROF_K2_POST, pk);
     if (rin) {
       pk = prof_begin();
-      CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rin, Cc, N, 1.0, HM, N, S.XV, N, 0.0, Ub, rin));
-      CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, Cc, rin, 1.0, S.Mk, (int)D, Ub, rin, 0.0, tmp, (int)D));
+      CK(gemm(OP_T, OP_N, rin, Cc, N, 1.0, HM, N, S.XV, N, 0.0, Ub, rin));
+      CK(gemm(OP_N, OP_N, (int)D, Cc, rin, 1.0, S.Mk, (int)D, Ub, rin, 0.0, tmp, (int)D));
       prof_end(CAKF_PROF_LOWRANK, pk);
     }
     CK_CUDA(StepKernels<T>::post_combine((int)NX, Dp, Cc, S.sig_t, S.KV, rin ? tmp : nullptr, S.m_pred, S.m, S.Mk, rin,
@@ -1082,14 +1046,17 @@ struct Impl final : ImplBase {
     return CAKF_OK;
   }
 
-  // C = alpha op(A) op(B) + beta C with fp64 accumulation for both dtypes (B optionally already fp64).
-  int gemm_impl(cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, double alpha, const T* A, int lda,
-                const T* B, const double* Bd, int ldb, double beta, T* C, int ldc) {
+  // C = alpha op(A) op(B) + beta C with fp64 accumulation for both dtypes (B optionally already fp64):
+  // fp32 with K >= i8_min_k on the INT8-slice tensor-core GEMM, everything else (short K, fp64 mode) on the
+  // FP64-pipe GEMM of kernels_gemm_f64.cu (fp32 operands converted on load, one rounding of the result)
+  int gemm_impl(bool ta, bool tb, int m, int n, int k, double alpha, const T* A, int lda, const T* B, const double* Bd,
+                int ldb, double beta, T* C, int ldc) {
     if (m <= 0 || n <= 0) return CAKF_OK;
     if constexpr (sizeof(T) == 8) {
       const double* Bp = Bd ? Bd : reinterpret_cast<const double*>(B);
-      CK_BLAS(cublasDgemm(blas, ta, tb, m, n, k, &alpha, reinterpret_cast<const double*>(A), lda, Bp, ldb, &beta,
-                          reinterpret_cast<double*>(C), ldc));
+      CK_CUDA((gemm_f64acc<double, double, double>)(ta, tb, m, n, k, alpha, reinterpret_cast<const double*>(A),
+                                                    (size_t)lda, Bp, (size_t)ldb, beta, reinterpret_cast<double*>(C),
+                                                    (size_t)ldc, fwork, kF64WorkDoubles, st));
     } else if (!lowrank_tc && !Bd && k >= i8_min_k && use_i8_gemm()) {
       CK(gemm_i8_f32(ta, tb, m, n, k, alpha, reinterpret_cast<const float*>(A), lda,
                      reinterpret_cast<const float*>(B), ldb, beta, reinterpret_cast<float*>(C), nullptr, ldc));
@@ -1098,39 +1065,25 @@ struct Impl final : ImplBase {
       if (Bd) return fail(CAKF_E_ARG, "gemm: fp64 right operand on the tensor-core path");
       if (gemm_tc_plane_bytes(m, k) > gp_elems * 2 || gemm_tc_plane_bytes(n, k) > gp_elems * 2)
         return fail(CAKF_E_ARG, "gemm: operand planes too small");
-      CK_CUDA(gemm_tc_split(reinterpret_cast<const float*>(A), m, k, (size_t)lda, ta == CUBLAS_OP_T, gpA, st));
-      CK_CUDA(gemm_tc_split(reinterpret_cast<const float*>(B), n, k, (size_t)ldb, tb == CUBLAS_OP_N, gpB, st));
+      CK_CUDA(gemm_tc_split(reinterpret_cast<const float*>(A), m, k, (size_t)lda, ta, gpA, st));
+      CK_CUDA(gemm_tc_split(reinterpret_cast<const float*>(B), n, k, (size_t)ldb, !tb, gpB, st));
       CK_CUDA(gemm_tc_run(gpA, m, gpB, n, k, alpha, beta, reinterpret_cast<float*>(C), nullptr, (size_t)ldc, gwork,
                           kGemmWorkFloats, st));
+    } else if (Bd) {
+      CK_CUDA((gemm_f64acc<float, double, float>)(ta, tb, m, n, k, alpha, reinterpret_cast<const float*>(A),
+                                                  (size_t)lda, Bd, (size_t)ldb, beta, reinterpret_cast<float*>(C),
+                                                  (size_t)ldc, fwork, kF64WorkDoubles, st));
     } else {
-      const int ar = ta == CUBLAS_OP_N ? m : k, ac = ta == CUBLAS_OP_N ? k : m;
-      const int br = tb == CUBLAS_OP_N ? k : n, bc = tb == CUBLAS_OP_N ? n : k;
-      if ((size_t)ar * ac > dscr || (size_t)br * bc > dscr || (size_t)m * n > dscr)
-        return fail(CAKF_E_ARG, "gemm: fp64 scratch too small");
-      CK_CUDA((convert<float, double>)(ar, ac, reinterpret_cast<const float*>(A), lda, dA, ar, st));
-      const double* Bp = Bd;
-      int ldbp = ldb;
-      if (!Bd) {
-        CK_CUDA((convert<float, double>)(br, bc, reinterpret_cast<const float*>(B), ldb, dB, br, st));
-        Bp = dB;
-        ldbp = br;
-      }
-      // beta C is added in fp64 by the fold-back kernel (no fp64 copy of C in or out of the DGEMM)
-      const double zero = 0.0;
-      if (k > 0) {
-        CK_BLAS(cublasDgemm(blas, ta, tb, m, n, k, &alpha, dA, ar, Bp, ldbp, &zero, dC, m));
-      } else {
-        CK_CUDA(cudaMemsetAsync(dC, 0, (size_t)m * n * sizeof(double), st));
-      }
-      if (beta != 0.0) CK_CUDA(accum_d2f(m, n, beta, dC, m, reinterpret_cast<float*>(C), ldc, st));
-      else CK_CUDA((convert<double, float>)(m, n, dC, m, reinterpret_cast<float*>(C), ldc, st));
+      CK_CUDA((gemm_f64acc<float, float, float>)(ta, tb, m, n, k, alpha, reinterpret_cast<const float*>(A),
+                                                 (size_t)lda, reinterpret_cast<const float*>(B), (size_t)ldb, beta,
+                                                 reinterpret_cast<float*>(C), (size_t)ldc, fwork, kF64WorkDoubles, st));
     }
     return CAKF_OK;
   }
   // fp32 operands, fp64-accurate product on the INT8 tensor cores (kernels_gemm_i8.cu): op(A) rows m and
   // op(B)^T rows n sliced into K-major planes; fp32 C or fp64 Cd; lower: only n <= m needed (Gram);
   // Bq (nullable) replaces B by an fp64 operand with the same layout
-  int gemm_i8_f32(cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, double alpha, const float* A,
+  int gemm_i8_f32(bool ta, bool tb, int m, int n, int k, double alpha, const float* A,
                   int lda, const float* B, int ldb, double beta, float* C, double* Cd, int ldc, bool lower = false,
                   const double* Bq = nullptr) {
     const size_t cap = gp_elems * 2;
@@ -1140,38 +1093,30 @@ struct Impl final : ImplBase {
       return fail(CAKF_E_ARG, "gemm: INT8 slice planes too small");
     int8_t* pa = reinterpret_cast<int8_t*>(gpA);
     int8_t* pb = reinterpret_cast<int8_t*>(gpB);
-    CK_CUDA(gemm_i8_split<float>(A, m, k, (size_t)lda, ta == CUBLAS_OP_T, pa, gexA, st));
+    CK_CUDA(gemm_i8_split<float>(A, m, k, (size_t)lda, ta, pa, gexA, st));
     const bool same = B == A && tb != ta && ldb == lda && m == n && !Bq;   // A^T A: one set of planes
-    if (Bq) CK_CUDA(gemm_i8_split<double>(Bq, n, k, (size_t)ldb, tb == CUBLAS_OP_N, pb, gexB, st));
-    else if (!same) CK_CUDA(gemm_i8_split<float>(B, n, k, (size_t)ldb, tb == CUBLAS_OP_N, pb, gexB, st));
+    if (Bq) CK_CUDA(gemm_i8_split<double>(Bq, n, k, (size_t)ldb, !tb, pb, gexB, st));
+    else if (!same) CK_CUDA(gemm_i8_split<float>(B, n, k, (size_t)ldb, !tb, pb, gexB, st));
     CK_CUDA(gemm_i8_run(pa, gexA, m, same ? pa : pb, same ? gexA : gexB, n, k, alpha, beta, C, Cd, (size_t)ldc,
                         lower, reinterpret_cast<double*>(gwork), kGemmWorkFloats / 2, st));
     return CAKF_OK;
   }
 
-  int gemm(cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, double alpha, const T* A, int lda,
+  int gemm(bool ta, bool tb, int m, int n, int k, double alpha, const T* A, int lda,
            const T* B, int ldb, double beta, T* C, int ldc) {
     return gemm_impl(ta, tb, m, n, k, alpha, A, lda, B, nullptr, ldb, beta, C, ldc);
   }
 
-  // Lower triangle of the Gram Gm = F^T F (fp64 F, D x c, ld D; Gm ld c) — all the eigensolver reads
-  // (CUBLAS_FILL_MODE_LOWER).  On this shape (K = D >> c) cuBLAS DSYRK reaches ~12 TF/s and DGEMM ~36,
-  // so the lower triangle is three DGEMMs over a 2 x 2 column split: F0^T F0, F1^T F0, F1^T F1
-  // (3/4 of the full product's flops).  CAKF_GRAM_FULL=1: one full DGEMM.
-  int gram_lower(const double* Fd, int c) {
-    static const bool full = [] { const char* e = getenv("CAKF_GRAM_FULL"); return e && e[0] == '1'; }();
-    const double one = 1.0, zero = 0.0;
-    const int c0 = std::min(c, ((c + 1) / 2 + 31) / 32 * 32), c1 = c - c0;
-    if (full || c1 <= 0) {
-      CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c, c, (int)D, &one, Fd, (int)D, Fd, (int)D, &zero, Gm, c));
-      return CAKF_OK;
-    }
-    const double* F1 = Fd + (size_t)c0 * D;
-    CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c0, c0, (int)D, &one, Fd, (int)D, Fd, (int)D, &zero, Gm, c));
-    CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c1, c0, (int)D, &one, F1, (int)D, Fd, (int)D, &zero, Gm + c0,
-                        c));
-    CK_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, c1, c1, (int)D, &one, F1, (int)D, F1, (int)D, &zero,
-                        Gm + c0 + (size_t)c0 * c, c));
+  // Gram Gm = F^T F in fp64 (F fp32 or fp64, D x c, ld D; Gm ld c; the eigensolver reads the lower triangle)
+  int gram_fp64(const T* F, int c) {
+    if constexpr (sizeof(T) == 8)
+      CK_CUDA((gemm_f64acc<double, double, double>)(true, false, c, c, (int)D, 1.0, reinterpret_cast<const double*>(F),
+                                                    (size_t)D, reinterpret_cast<const double*>(F), (size_t)D, 0.0, Gm,
+                                                    (size_t)c, fwork, kF64WorkDoubles, st));
+    else
+      CK_CUDA((gemm_f64acc<float, float, double>)(true, false, c, c, (int)D, 1.0, reinterpret_cast<const float*>(F),
+                                                  (size_t)D, reinterpret_cast<const float*>(F), (size_t)D, 0.0, Gm,
+                                                  (size_t)c, fwork, kF64WorkDoubles, st));
     return CAKF_OK;
   }
 
@@ -1225,11 +1170,10 @@ struct Impl final : ImplBase {
       CK_CUDA(gemm_tc_split(F, c, (int)D, (size_t)D, true, gpA, st));          // F^T rows (K = D contiguous)
       CK_CUDA(gemm_tc_run(gpA, c, gpA, c, (int)D, 1.0, 0.0, nullptr, Gm, (size_t)c, gwork, kGemmWorkFloats, st));
     } else if (i8) {   // exact products, fp64 sums: lower triangle of F^T F on the INT8 tensor cores
-      CK(gemm_i8_f32(CUBLAS_OP_T, CUBLAS_OP_N, c, c, (int)D, 1.0, F, (int)D, F, (int)D, 0.0, nullptr, Gm, c, true));
-    } else {   // the Gram decides the kept subspace: fp32 products, fp64 accumulation (DGEMM)
-      if ((size_t)D * c > dscr) return fail(CAKF_E_ARG, "truncate: fp64 scratch too small");
-      CK_CUDA((convert<float, double>)((int)D, c, F, D, dA, D, st));
-      CK(gram_lower(dA, c));
+      CK(gemm_i8_f32(OP_T, OP_N, c, c, (int)D, 1.0, F, (int)D, F, (int)D, 0.0, nullptr, Gm, c, true));
+    } else {   // the Gram decides the kept subspace: fp32 products, fp64 accumulation
+      CK_CUDA((gemm_f64acc<float, float, double>)(true, false, c, c, (int)D, 1.0, F, (size_t)D, F, (size_t)D, 0.0, Gm,
+                                                  (size_t)c, fwork, kF64WorkDoubles, st));
     }
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
@@ -1237,10 +1181,10 @@ struct Impl final : ImplBase {
     prof_end(CAKF_PROF_TRUNC_EIG, ps);
     ps = prof_begin();
     if (i8 && i8_mqr) {   // M~ = F Q_r with the fp64 eigenvectors sliced directly
-      CK(gemm_i8_f32(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, c, 0.0, out, nullptr,
+      CK(gemm_i8_f32(OP_N, OP_N, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, c, 0.0, out, nullptr,
                      (int)D, false, QrD));
       if (F2)
-        CK(gemm_i8_f32(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, 1.0, F2, (int)D, nullptr, c, 0.0, out2, nullptr,
+        CK(gemm_i8_f32(OP_N, OP_N, (int)D, rkeep, c, 1.0, F2, (int)D, nullptr, c, 0.0, out2, nullptr,
                        (int)D, false, QrD));
     } else {
       CK_CUDA((convert<double, float>)(c, rkeep, QrD, c, Qf, c, st));
@@ -1270,38 +1214,16 @@ struct Impl final : ImplBase {
                                                    reinterpret_cast<const float*>(F2), reinterpret_cast<float*>(out2),
                                                    failflag);
     }
-    // fp64 copy of F (fp32 storage) feeds both the Gram (DSYRK, fp64 tensor cores) and M Q_r (DGEMM)
-    const double* Fd = reinterpret_cast<const double*>(F);
-    if constexpr (sizeof(T) == 4) {
-      if ((size_t)D * c > dscr) return fail(CAKF_E_ARG, "truncate: fp64 scratch too small");
-      CK_CUDA((convert<float, double>)((int)D, c, reinterpret_cast<const float*>(F), D, dA, D, st));
-      Fd = dA;
-    }
-    const double one = 1.0, zero = 0.0;
+    // fp64 accumulation for the Gram and M Q_r on the FP64 pipe (CAKF_GEMM_F64=1 for fp32, and fp64 mode)
     size_t ps = prof_begin();
-    CK(gram_lower(Fd, c));
+    CK(gram_fp64(F, c));
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
     CK(eig(c, rkeep, kept, dropped, failflag));
     prof_end(CAKF_PROF_TRUNC_EIG, ps);
     ps = prof_begin();
-    if constexpr (sizeof(T) == 4) {
-      CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one, Fd, (int)D, QrD, c, &zero, dC, (int)D));
-      CK_CUDA((convert<double, float>)((int)D, rkeep, dC, D, reinterpret_cast<float*>(out), D, st));
-      if (F2) {
-        CK_CUDA((convert<float, double>)((int)D, c, reinterpret_cast<const float*>(F2), D, dA, D, st));
-        CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one, dA, (int)D, QrD, c, &zero, dC,
-                            (int)D));
-        CK_CUDA((convert<double, float>)((int)D, rkeep, dC, D, reinterpret_cast<float*>(out2), D, st));
-      }
-    } else {
-      CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one, Fd, (int)D, QrD, c, &zero,
-                          reinterpret_cast<double*>(out), (int)D));
-      if (F2)
-        CK_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, rkeep, c, &one,
-                            reinterpret_cast<const double*>(F2), (int)D, QrD, c, &zero, reinterpret_cast<double*>(out2),
-                            (int)D));
-    }
+    CK(gemm_impl(false, false, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, QrD, c, 0.0, out, (int)D));
+    if (F2) CK(gemm_impl(false, false, (int)D, rkeep, c, 1.0, F2, (int)D, nullptr, QrD, c, 0.0, out2, (int)D));
     prof_end(CAKF_PROF_TRUNC_GEMM, ps);
     prof_end(CAKF_PROF_TRUNCATE, pk);
     return CAKF_OK;
@@ -1364,16 +1286,16 @@ struct Impl final : ImplBase {
       // y = P^-_k x = Sigma x - M^- (M^-^T x)
       pk = prof_begin();
       if (rin) {
-        CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rin, C, (int)D, 1.0, S.Mk, (int)D, X, (int)D, 0.0, Tm, rin));
-        CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, C, rin, -1.0, S.Mk, (int)D, Tm, rin, 1.0, yb, (int)D));
+        CK(gemm(OP_T, OP_N, rin, C, (int)D, 1.0, S.Mk, (int)D, X, (int)D, 0.0, Tm, rin));
+        CK(gemm(OP_N, OP_N, (int)D, C, rin, -1.0, S.Mk, (int)D, Tm, rin, 1.0, yb, (int)D));
       }
       // P_k x = y - B_k (V^T H y);  R = V (V^T H y)
       if (n) {
         T* Vk = S.XV + N;
         CK_CUDA(StepKernels<T>::gather_rows(N, C, S.idx, yb, D, Hy, N, st));
-        CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, n, C, N, 1.0, Vk, N, Hy, N, 0.0, tt, n));
-        CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, C, n, -1.0, S.Mk + (size_t)rin * D, (int)D, tt, n, 1.0, yb, (int)D));
-        CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, N, C, n, 1.0, Vk, N, tt, n, 0.0, R, N));
+        CK(gemm(OP_T, OP_N, n, C, N, 1.0, Vk, N, Hy, N, 0.0, tt, n));
+        CK(gemm(OP_N, OP_N, (int)D, C, n, -1.0, S.Mk + (size_t)rin * D, (int)D, tt, n, 1.0, yb, (int)D));
+        CK(gemm(OP_N, OP_N, N, C, n, 1.0, Vk, N, tt, n, 0.0, R, N));
       }
       prof_end(CAKF_PROF_LOWRANK, pk);
       // m^s_k = m_k + P_k A^T w^s ;  var^s_k = var_k - rowsumsq(P_k A^T W^s)   (lines 5-6)
@@ -1383,7 +1305,7 @@ struct Impl final : ImplBase {
       if (!smooth_k2) {
         // (I (x) K) W^s_full = [[K(X,T) V; 0], Kx[:,1:] - [K(X,T) V t[:,1:]; 0]], same for w^s with column 0
         pk = prof_begin();
-        if (n) CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)NX, C, n, 1.0, S.KV + NX, (int)NX, tt, n, 0.0, Zk, (int)NX));
+        if (n) CK(gemm(OP_N, OP_N, (int)NX, C, n, 1.0, S.KV + NX, (int)NX, tt, n, 0.0, Zk, (int)NX));
         prof_end(CAKF_PROF_LOWRANK, pk);
         CK_CUDA(StepKernels<T>::kcar_build(NX, Dp, n, q, S.KV, n ? Zk : nullptr, Yk, KWf, Kws, st));
       }
@@ -1462,8 +1384,8 @@ struct Impl final : ImplBase {
             act_stride_sm));
       CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, C, sig_t, Yk, yb, st));
       if (rt) {
-        CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rt, C, (int)D, 1.0, Wf, (int)D, X, (int)D, 0.0, Tm, rt));
-        CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, C, rt, -1.0, Wf, (int)D, Tm, rt, 1.0, yb, (int)D));
+        CK(gemm(OP_T, OP_N, rt, C, (int)D, 1.0, Wf, (int)D, X, (int)D, 0.0, Tm, rt));
+        CK(gemm(OP_N, OP_N, (int)D, C, rt, -1.0, Wf, (int)D, Tm, rt, 1.0, yb, (int)D));
       }
       // m^s(t) = m(t) + y_0 ; var^s(t) = var(t) - rowsumsq(y_{1:})
       CK_CUDA(StepKernels<T>::smooth_out(D, C, ip_m, ip_v, yb, ip_ms, ip_vs, st));
@@ -1523,7 +1445,7 @@ struct Impl final : ImplBase {
         CK_CUDA(cudaMemcpyAsync(xtmp, static_cast<const T*>(q) + (size_t)(k - 1) * DS, DS * sizeof(T),
                                 cudaMemcpyDefault, st));
         CK_CUDA(sampler_ops<T>::permute_cols((int)NX, Dp, S, invperm_d, xtmp, D, xsm, D, st));
-        CK_BLAS(Blas<T>::axpy(blas, (int)DS, T(1), xsm, xk));
+        CK_CUDA(axpy<T>(DS, 1.0, xsm, xk, st));
         const int N = K.N, n = K.n, rin = K.rin;
         if (K.missing || N == 0) continue;
         // u = V V^T (y - H x^- - eps)
@@ -1533,8 +1455,8 @@ struct Impl final : ImplBase {
         T* u = ust + uoff[k];
         if (n) {
           const T* Vk = K.XV + N;
-          CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, n, S, N, 1.0, Vk, N, res, N, 0.0, tt, n));
-          CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, N, S, n, 1.0, Vk, N, tt, n, 0.0, u, N));
+          CK(gemm(OP_T, OP_N, n, S, N, 1.0, Vk, N, res, N, 0.0, tt, n));
+          CK(gemm(OP_N, OP_N, N, S, n, 1.0, Vk, N, tt, n, 0.0, u, N));
         } else {
           CK_CUDA(cudaMemsetAsync(u, 0, (size_t)N * S * sizeof(T), st));
         }
@@ -1549,8 +1471,8 @@ struct Impl final : ImplBase {
         const T* tmpp = nullptr;
         if (rin) {
           CK_CUDA(StepKernels<T>::gather_rows(N, rin, K.idx, K.Mk, D, HM, N, st));
-          CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rin, S, N, 1.0, HM, N, u, N, 0.0, Ub, rin));
-          CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, S, rin, 1.0, K.Mk, (int)D, Ub, rin, 0.0, tmp, (int)D));
+          CK(gemm(OP_T, OP_N, rin, S, N, 1.0, HM, N, u, N, 0.0, Ub, rin));
+          CK(gemm(OP_N, OP_N, (int)D, S, rin, 1.0, K.Mk, (int)D, Ub, rin, 0.0, tmp, (int)D));
           tmpp = tmp;
         }
         CK_CUDA(sampler_ops<T>::combine((int)NX, Dp, S, K.sig_t, Yb, tmpp, xk, xk, st));
@@ -1570,8 +1492,8 @@ struct Impl final : ImplBase {
                 act_stride_sm));
           CK_CUDA(StepKernels<T>::sigma_apply((int)NX, Dp, S, K.sig_t, Yk, yb, st));
           if (rin) {
-            CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, rin, S, (int)D, 1.0, K.Mk, (int)D, X, (int)D, 0.0, Tm, rin));
-            CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, S, rin, -1.0, K.Mk, (int)D, Tm, rin, 1.0, yb, (int)D));
+            CK(gemm(OP_T, OP_N, rin, S, (int)D, 1.0, K.Mk, (int)D, X, (int)D, 0.0, Tm, rin));
+            CK(gemm(OP_N, OP_N, (int)D, S, rin, -1.0, K.Mk, (int)D, Tm, rin, 1.0, yb, (int)D));
           }
           // w^s_k = w_k + z - H^T V (V^T H y);  P_k z = y - B_k (V^T H y)
           CK_CUDA(cudaMemcpyAsync(wsv, X, DS * sizeof(T), cudaMemcpyDeviceToDevice, st));
@@ -1580,15 +1502,15 @@ struct Impl final : ImplBase {
             if (n) {
               const T* Vk = K.XV + N;
               CK_CUDA(StepKernels<T>::gather_rows(N, S, K.idx, yb, D, Hy, N, st));
-              CK(gemm(CUBLAS_OP_T, CUBLAS_OP_N, n, S, N, 1.0, Vk, N, Hy, N, 0.0, tt, n));
-              CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, N, S, n, 1.0, Vk, N, tt, n, 0.0, R, N));
+              CK(gemm(OP_T, OP_N, n, S, N, 1.0, Vk, N, Hy, N, 0.0, tt, n));
+              CK(gemm(OP_N, OP_N, N, S, n, 1.0, Vk, N, tt, n, 0.0, R, N));
               CK_CUDA(sampler_ops<T>::scatter_rows(N, S, K.idx, R, T(-1), wsv, D, st));
-              CK(gemm(CUBLAS_OP_N, CUBLAS_OP_N, (int)D, S, n, -1.0, K.Mk + (size_t)rin * D, (int)D, tt, n, 1.0, yb,
+              CK(gemm(OP_N, OP_N, (int)D, S, n, -1.0, K.Mk + (size_t)rin * D, (int)D, tt, n, 1.0, yb,
                       (int)D));
             }
           }
           // x^s_k = x_k + P_k z  (in place over the forward sample: the forward x_k is not needed again)
-          CK_BLAS(Blas<T>::axpy(blas, (int)DS, T(1), yb, xs + (size_t)k * DS));
+          CK_CUDA(axpy<T>(DS, 1.0, yb, xs + (size_t)k * DS, st));
         }
       }
       // internal -> user order, to the caller's buffer: (T+1) x D x S

@@ -97,6 +97,18 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
                         size_t work_doubles, cudaStream_t st);
 bool use_i8_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM instead
 
+// ---- low-rank contractions with fp64 accumulation on the FP64 pipe (kernels_gemm_f64.cu):
+// C = alpha op(A) op(B) + beta C, column-major, op = transpose when trans*; fp32/fp64 operands converted on
+// load, fp64 products and sums, one rounding into C; long K split into fixed slices reduced in order through
+// work (doubles; the split shrinks to fit work_doubles)
+template <typename TA, typename TB, typename TC>
+cudaError_t gemm_f64acc(bool transa, bool transb, int m, int n, int k, double alpha, const TA* A, size_t lda,
+                        const TB* B, size_t ldb, double beta, TC* C, size_t ldc, double* work, size_t work_doubles,
+                        cudaStream_t st);
+// y += a x
+template <typename T>
+cudaError_t axpy(size_t n, double a, const T* x, T* y, cudaStream_t st);
+
 // ---- the truncation's symmetric eigensolver (kernels_eig.cu): cluster Householder tridiagonalisation,
 // divide and conquer, back-transformation of the r wanted eigenvectors.  G: c x c fp64, lower triangle
 // (ld c).  Qr: c x r eigenvectors of the r largest eigenvalues, descending; kept (r, nullable) those
