@@ -305,6 +305,12 @@ int cakf_lowrank_gemm(int32_t transa, int32_t transb, int64_t m, int64_t n, int6
                       const float* A, int64_t lda, const float* B, int64_t ldb, double beta, float* C,
                       int64_t ldc, void* stream);
 
+/* Live ALU peaks for the roofline denominators (bench.py): out3[0] = MUFU ops/s of the sqrt.approx /
+ * ex2.approx mix K1 is bound by (2 MUFU ops per kernel pair), out3[1] = fp64 tensor-core
+ * (DMMA) flop/s, out3[2] = clock64 cycles of one CTA of the MUFU test (diagnostic).  Microbenchmarks launched on
+ * `stream` (may be NULL); synchronises.  Errors: CAKF_E_ARG, CAKF_E_CUDA. */
+int cakf_alu_peaks(double* out3, void* stream);
+
 /* Standalone symmetric eigensolver of the truncation (a8 / a9 Truncate, Sec. 3.2; "SVD of
  * M M^T" P:367, reading R4: eigh of the Gram M^T M), fp64, all on the device (kernels_eig.cu:
  * cluster Householder tridiagonalisation, divide and conquer, back-transformation):

@@ -61,7 +61,7 @@ EXPORTS = [
     "cakf_get_stats", "cakf_get_kept_eigs", "cakf_sync", "cakf_destroy", "cakf_last_error", "cakf_version",
     "cakf_matern_transition", "cakf_gram_matmul", "cakf_profile", "cakf_profile_read", "cakf_kernel_launches",
     "cakf_nccl_unique_id", "cakf_shard_plan", "cakf_sym_unit_blocks", "cakf_cull_stats", "cakf_interpolate", "cakf_sample",
-    "cakf_lowrank_gemm", "cakf_debug_matvec", "cakf_sym_eig",
+    "cakf_lowrank_gemm", "cakf_debug_matvec", "cakf_sym_eig", "cakf_alu_peaks",
 ]
 PROF_CATEGORIES = ["k1_matvec", "k2_post", "k2_smooth", "loop_stages", "truncate", "lowrank", "trunc_gram",
                    "trunc_eig", "trunc_gemm"]
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH):
     lib.cakf_cull_stats.argtypes = [vp, vp]
     lib.cakf_debug_matvec.argtypes = [vp, i64, vp, vp, vp]
     lib.cakf_sym_eig.argtypes = [i64, i64, vp, vp, vp, vp]
+    lib.cakf_alu_peaks.argtypes = [vp, vp]
     lib.cakf_interpolate.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp]
     lib.cakf_sample.argtypes = [vp, i32, vp, vp, vp, i32, vp]
     lib.cakf_sym_unit_blocks.argtypes = [i64, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
@@ -201,6 +202,13 @@ def lowrank_gemm(A, B, transa=False, transb=False, alpha=1.0, beta=0.0, C=None, 
                                  Bm.data_ptr(), Bm.shape[1], Am.data_ptr(), Am.shape[1], float(beta),
                                  out.data_ptr(), n, stream))
     return out
+
+
+def alu_peaks(stream=None) -> dict:
+    """Live microbenchmarks (cakf_alu_peaks): MUFU ops/s and fp64 tensor-core flop/s."""
+    out = np.zeros(3)
+    _check(load().cakf_alu_peaks(out.ctypes.data, stream))
+    return {"mufu_ops_per_s": float(out[0]), "dmma_flop_per_s": float(out[1])}
 
 
 def sym_eig(G, r=None):

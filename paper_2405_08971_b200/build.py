@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcakf.so")
 SOURCES = ["kernels_gram.cu", "kernels_gram_tc.cu", "kernels_gemm_tc.cu", "kernels_gemm_i8.cu", "kd_order.cu", "kernels_step.cu", "kernels_eig.cu",
-           "kernels_gemm_f64.cu", "cakf_api.cu"]
+           "kernels_gemm_f64.cu", "kernels_peak.cu", "cakf_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 try:  # NCCL as bundled with torch (nvidia-nccl wheel): headers + libnccl.so.2
     import nvidia.nccl as _nccl
