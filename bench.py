@@ -347,8 +347,26 @@ def pass_roofline(wl, prof, live, nz, hbm_gbs, pass_ms):
 
 
 # ------------------------------------------------------------------ GPU arm
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a launcher: re-run this script under torch.distributed.run with N ranks on
+    this node (rendezvous on 127.0.0.1); rank 0's JSON line is relayed."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, text=True)
+    for line in r.stdout.splitlines():
+        if line.startswith("{"):
+            print(line)
+    return r.returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     import torch

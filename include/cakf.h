@@ -239,9 +239,11 @@ int cakf_sample(cakf_t h, int32_t n_samples, const void* x0, const void* q, cons
  * partial slots — for one vector:  out[j] = sum_l Matern(|x_{obs[j]} - x_{obs[l]}| / ell) s[l].
  * obs_idx (n_obs spatial indices, int64), s and out (n_obs, handle dtype) in the caller's
  * observation order, host or device.  Call between steps (not between predict and update); it
- * overwrites the inner-loop workspaces only.  Synchronises.
+ * overwrites the inner-loop workspaces only.  shares > 1 runs K1 as the multi-GPU split into `shares`
+ * contiguous unit ranges with equal active tile pairs (what rank p of `shares` ranks evaluates), one after
+ * the other into the same partial slots: the result must equal shares = 1 bit for bit.  Synchronises.
  * Errors: CAKF_E_ARG (NULL, n_obs outside [1, max_obs], index out of range), CAKF_E_STATE, CAKF_E_CUDA. */
-int cakf_debug_matvec(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* s, void* out);
+int cakf_debug_matvec(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* s, void* out, int32_t shares);
 
 /* Exact-zero culling statistics of the handle so far: frac3[0] = fraction of the symmetric K1's
  * pairs evaluated (counted in 16 x 128 warp blocks of its 128 x 128 tile pairs), frac3[1] = fraction of the post-loop K2's 128x32 tiles evaluated,
@@ -249,14 +251,21 @@ int cakf_debug_matvec(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const voi
  * stream.  Errors: CAKF_E_HANDLE, CAKF_E_ARG (NULL frac3), CAKF_E_CUDA. */
 int cakf_cull_stats(cakf_t h, double* frac3);
 
-/* ---- multi-GPU (the spatial rows of the covariance operator are sharded) ----
- * With cfg.world > 1 every rank calls the same sequence with the same full inputs; the two
- * Gram products are sharded and exchanged with NCCL on cfg.stream, everything else is
- * computed identically (deterministically) on every rank:
- *   K1 (inner-loop K_TT s): rank p evaluates symmetric tile-block units [u_lo, u_hi) and the
- *       reduced N-vector is all-reduced (ncclAllReduce, sum);
- *   K2 (post-loop / smoother K(X, .) B): rank p computes output rows [row_lo, row_hi) (128-row
- *       aligned slices) and the slices are all-gathered (ncclAllGather).
+/* ---- multi-GPU (the spatial rows of the covariance operator and of M are sharded) ----
+ * With cfg.world > 1 every rank calls the same sequence with the same full inputs.  Rank p owns the
+ * internal (kd-ordered) points [row_lo, row_hi) (128-aligned equal slices) and holds only their rows of
+ * every D-length state: m, variances, M_k = [M^-_k | B_k], the truncated factors, the smoother carriers
+ * and the post-loop kernel products K(X_p, X_T)[v V].  Exchanges, all NCCL on cfg.stream:
+ *   update   all-reduce of [H m^-, H M^-] (N x (1 + r): each rank contributes the observed rows it owns);
+ *   loop     K1 (K_TT s): rank p evaluates its share of the symmetric tile-block units (with exact-zero
+ *            culling: a contiguous unit range holding 1/world of the active tile pairs, else [u_lo, u_hi)),
+ *            then all-reduce of the N-vector; the N-length loop state is replicated;
+ *   post     none: K2 and the low-rank algebra produce this rank's rows;
+ *   truncate all-reduce of the partial Grams M_p^T M_p (c x c fp64); the eigensolver runs on every rank
+ *            on identical bits; M~_p = M_p Q_r;
+ *   smoother all-reduce of M^-T x (r x (1+q)) and V^T H y (n x (1+q));
+ *   get      all-gather of the row slices.
+ * cakf_interpolate / cakf_sample / CAKF_SMOOTH_K2 are single-GPU only (CAKF_E_UNSUPPORTED).
  * cakf_nccl_unique_id writes the 128-byte ncclUniqueId rank 0 creates (broadcast it to all ranks
  * and pass it as cfg.nccl_id). */
 int cakf_nccl_unique_id(void* out128);

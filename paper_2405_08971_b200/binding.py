@@ -99,7 +99,7 @@ def load(path: str = LIB_PATH):
     lib.cakf_nccl_unique_id.argtypes = [vp]
     lib.cakf_shard_plan.argtypes = [i64, i64, i32, i32, vp]
     lib.cakf_cull_stats.argtypes = [vp, vp]
-    lib.cakf_debug_matvec.argtypes = [vp, i64, vp, vp, vp]
+    lib.cakf_debug_matvec.argtypes = [vp, i64, vp, vp, vp, i32]
     lib.cakf_sym_eig.argtypes = [i64, i64, vp, vp, vp, vp]
     lib.cakf_alu_peaks.argtypes = [vp, vp]
     lib.cakf_interpolate.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp]
@@ -349,12 +349,14 @@ class Cakf:
                                     out.ctypes.data))
         return out.reshape(T + 1, S, self.D).transpose(0, 2, 1)
 
-    def debug_matvec(self, obs_idx, s):
-        """K(X_obs, X_obs) s through the inner loop's own K1 launch path (cakf_debug_matvec); numpy in/out."""
+    def debug_matvec(self, obs_idx, s, shares=1):
+        """K(X_obs, X_obs) s through the inner loop's own K1 launch path (cakf_debug_matvec); numpy in/out.
+        shares > 1: K1 as the multi-GPU split of `shares` ranks, run one share after the other."""
         idx = np.ascontiguousarray(obs_idx, dtype=np.int64)
         sv = np.ascontiguousarray(s, dtype=self.np_dtype)
         out = np.empty(len(idx), dtype=self.np_dtype)
-        _check(self.lib.cakf_debug_matvec(self.h, len(idx), idx.ctypes.data, sv.ctypes.data, out.ctypes.data))
+        _check(self.lib.cakf_debug_matvec(self.h, len(idx), idx.ctypes.data, sv.ctypes.data, out.ctypes.data,
+                                          int(shares)))
         return out
 
     def cull_stats(self) -> dict:

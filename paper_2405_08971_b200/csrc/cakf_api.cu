@@ -165,14 +165,18 @@ struct ImplBase {
   virtual int interpolate(int k, const double* A1, const double* Q1, const double* A2, int which, void* mean,
                           void* var) = 0;
   virtual int sample(int S, const void* x0, const void* q, const void* eps, int which, void* out) = 0;
-  virtual int debug_matvec(int64_t n, const int64_t* idx, const void* s, void* out) = 0;
+  virtual int debug_matvec(int64_t n, const int64_t* idx, const void* s, void* out, int shares) = 0;
 };
 
 template <typename T>
 struct Impl final : ImplBase {
   // ---------------- configuration
   int Dp = 2, dim = 3, nu2 = 3, policy = 0, nhat = 0, rcap = -1, Tmax = 0;
+  // Row sharding: this rank owns the internal points [plo, plo + NX) — NX and D = Dp NX are the
+  // LOCAL sizes of every D-row array (m, var, M_k, B, carriers, ...); NXf / Df are the full grid.  world = 1:
+  // plo = 0, NX = NXf.
   int64_t NX = 0, D = 0, Nmax = 0;
+  int64_t NXf = 0, Df = 0, plo = 0, pslice = 0;
   double rtol = 0.0, ell = 1.0;
   uint64_t seed = 0;
   Mat3 sig_t0{};
@@ -208,6 +212,8 @@ struct Impl final : ImplBase {
   // inner loop
   V4<T>* xcs = nullptr;
   T *r = nullptr, *s = nullptr, *g = nullptr, *gp = nullptr, *d = nullptr, *Gd = nullptr, *Z = nullptr, *HM = nullptr;
+  T* hmx = nullptr;   // [H m^- | H M^-] (N x (1 + rin)): gathered from the owners of the observed rows
+  long long* k1_range = nullptr;   // multi-GPU: this rank's K1 unit range, balanced by active tile pairs
   T *ybuf = nullptr, *lam2 = nullptr, *partial = nullptr;
   size_t partial_cap = 0;
   int64_t* stage64 = nullptr;
@@ -300,11 +306,11 @@ struct Impl final : ImplBase {
   // 128-row tile of the K2 output and every 32-column K-block is one compact subtree (bounding
   // spheres ~2x tighter than a Morton order).  CAKF_NO_REORDER=1 keeps the user order.
   void make_perm(const std::vector<double>& xyz) {
-    perm_h.resize(NX);
-    for (int64_t i = 0; i < NX; ++i) perm_h[i] = (int)i;
+    perm_h.resize(NXf);
+    for (int64_t i = 0; i < NXf; ++i) perm_h[i] = (int)i;
     const char* e = getenv("CAKF_NO_REORDER");
     if (e && e[0] == '1') return;
-    std::vector<std::pair<int64_t, int64_t>> stack{{0, NX}};
+    std::vector<std::pair<int64_t, int64_t>> stack{{0, NXf}};
     while (!stack.empty()) {
       const auto [b0, b1] = stack.back();
       stack.pop_back();
@@ -358,24 +364,19 @@ struct Impl final : ImplBase {
     return launch_gram_gemm<T>(nu2, xr, M, xc, K, B, ldb, C, Y, ldy, 1.0, st);
   }
 
-  // K2: Y = K(xr, xc) B — tcgen05 3xBF16 for fp32, SIMT for fp64 (or CAKF_K2_SIMT=1).
-  // world > 1: rank p computes output rows [p*slice, (p+1)*slice) and the slices are all-gathered.
+  // K2: Y = K(xr, xc) B — tcgen05 3xBF16 for fp32, SIMT for fp64 (or CAKF_K2_SIMT=1).  With row sharding
+  // the callers pass their local rows (coords + plo, NX) and the matching slice of the culling lists.
   // acnt/alist: exact-zero culling lists of the 128-row tiles of xr (nullable)
   int k2(const V4<T>* xr, int M, const V4<T>* xc, int K, const T* B, size_t ldb, int C, T* Y, size_t ldy,
          const int* acnt = nullptr, const int* alist = nullptr, int astride = 0) {
-    if (!coll) {
-      CK_CUDA(k2_local(xr, M, xc, K, B, ldb, C, Y, ldy, acnt, alist, astride));
-      return CAKF_OK;
-    }
-    if ((size_t)C > k2_cmax) return fail(CAKF_E_ARG, "k2: too many right-hand sides for the shard buffers");
-    const int slice = k2_slice_rows(M, world);
-    const int lo = rank * slice;
-    const int mloc = std::max(0, std::min(slice, M - lo));
-    if (mloc > 0)
-      CK_CUDA(k2_local(xr + lo, mloc, xc, K, B, ldb, C, yslice, (size_t)slice, acnt ? acnt + lo / 128 : nullptr,
-                       alist ? alist + (size_t)(lo / 128) * astride : nullptr, astride));
-    CK_NCCL(ncclAllGather(yslice, ygath, (size_t)slice * C, sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, comm, st));
-    CK_CUDA(StepKernels<T>::assemble_slices(M, C, slice, ygath, Y, ldy, st));
+    CK_CUDA(k2_local(xr, M, xc, K, B, ldb, C, Y, ldy, acnt, alist, astride));
+    return CAKF_OK;
+  }
+  // sum of a small replicated-shape partial over the ranks (no-op without collectives)
+  template <typename U>
+  int allreduce(U* buf, size_t n) {
+    if (!coll || !n) return CAKF_OK;
+    CK_NCCL(ncclAllReduce(buf, buf, n, sizeof(U) == 4 ? ncclFloat32 : ncclFloat64, ncclSum, comm, st));
     return CAKF_OK;
   }
 
@@ -473,7 +474,7 @@ struct Impl final : ImplBase {
 
   void layout() {
     arena_off = 0;
-    coords = carve<V4<T>>(NX);
+    coords = carve<V4<T>>(NXf);
     mu0 = carve<T>(D);
     steps.resize(Tmax + 1);
     for (int k = 0; k <= Tmax; ++k) {
@@ -500,11 +501,12 @@ struct Impl final : ImplBase {
     d = carve<T>(Nmax); Gd = carve<T>(Nmax);
     ybuf = carve<T>(Nmax); lam2 = carve<T>(Nmax);
     Z = carve<T>((size_t)Nmax * std::max(nhat, 1));
-    HM = carve<T>((size_t)Nmax * std::max(rin_max, 1));
+    hmx = carve<T>((size_t)Nmax * (1 + std::max(rin_max, 1)));
+    HM = hmx + Nmax;
     const int nch = matvec_chunks((int)Nmax, (int)Nmax, sizeof(T));
     partial_cap = (size_t)std::max<int64_t>({(int64_t)nch, (int64_t)64, (int64_t)matvec_sym_tiles((int)Nmax)}) * Nmax;
     partial = carve<T>(partial_cap);
-    stage64 = carve<int64_t>(std::max<int64_t>(Nmax, 3 * NX));   // also the 3 x NX staged coordinates
+    stage64 = carve<int64_t>(std::max<int64_t>(Nmax, 3 * NXf));   // also the 3 x NX staged coordinates
     order32 = carve<int>(std::max(nhat, 1));
     part = carve<double>((size_t)(stage_blocks((int)Nmax) + 33) * W);   // block rows + group rows
     redA = carve<double>(W);
@@ -513,9 +515,9 @@ struct Impl final : ImplBase {
     cnt = carve<unsigned>(5 * 64);   // per reduction: [0] top, [1..32] group counters
     part2 = carve<double>((size_t)(stage_blocks((int)Nmax) + 33) * W);
     hmw = carve<double>((size_t)Nmax);
-    Yb = carve<T>((size_t)NX * (1 + nhat));
+    Yb = carve<T>((size_t)std::max<int64_t>(NX, Nmax) * (1 + nhat));   // K2 post output or N x b action block
     Ub = carve<T>((size_t)std::max(rin_max, 1) * (1 + nhat));
-    tmp = carve<T>((size_t)D * (1 + nhat));
+    tmp = carve<T>(std::max<size_t>((size_t)D * (1 + nhat), (size_t)Nmax * blk));
     if (rcap >= 0) {
       gpart = carve<double>((size_t)nsplit_max * cmax * cmax);
       Gm = carve<double>((size_t)cmax * cmax);
@@ -553,10 +555,10 @@ struct Impl final : ImplBase {
       Zk = carve<T>((size_t)NX * C);
     }
     pvar = carve<T>(D);
-    perm_d = carve<int>(NX);
-    invperm_d = carve<int>(NX);
-    posof = carve<int>(NX);
-    obs_cnt = carve<int>((NX + 1023) / 1024 + 1);
+    perm_d = carve<int>(NXf);
+    invperm_d = carve<int>(NXf);
+    posof = carve<int>(NXf);
+    obs_cnt = carve<int>((NXf + 1023) / 1024 + 1);
     sigma = carve<int>(Nmax);
     sigma_inv = carve<int>(Nmax);
     ip_m = carve<T>(D); ip_v = carve<T>(D); ip_ms = carve<T>(D); ip_vs = carve<T>(D);
@@ -577,15 +579,14 @@ struct Impl final : ImplBase {
     kd_ws = carve<unsigned char>(kd_ws_bytes);
     ybuf_user = carve<T>(Nmax);
     lam2_user = carve<T>(Nmax);
-    outm = carve<T>(D);
-    outv = carve<T>(D);
+    outm = carve<T>(Df);
+    outv = carve<T>(Df);
     if (coll) {
       yloc = carve<T>(Nmax);
       yred = carve<T>(Nmax);
-      k2_cmax = std::max<size_t>((size_t)(1 + nhat), (size_t)Dp * (1 + qmax));
-      const size_t slice = (size_t)k2_slice_rows((int)NX, world);
-      yslice = carve<T>(slice * k2_cmax);
-      ygath = carve<T>(slice * k2_cmax * world);
+      const size_t slice = (size_t)pslice;   // cakf_get: pack + all-gather of the local D rows
+      yslice = carve<T>(slice * Dp);
+      ygath = carve<T>(slice * Dp * world);
     }
     if (sizeof(T) == 4) {
       const size_t wb = std::max(gram_gemm_tc_workspace((int)Nmax, 1 + nhat),
@@ -601,7 +602,7 @@ struct Impl final : ImplBase {
       if (rcap >= 0) Qf = carve<float>((size_t)cmax * std::max(rcap, 1));
     }
     if (cull) {
-      const int nx128 = (int)((NX + 127) / 128), nx32 = (int)((NX + 31) / 32);
+      const int nx128 = (int)((NXf + 127) / 128), nx32 = (int)((NXf + 31) / 32);
       const int no128 = (int)((Nmax + 127) / 128), no32 = (int)((Nmax + 31) / 32);
       sph_x128 = carve<float4>(nx128); sph_x32 = carve<float4>(nx32);
       sph_o128 = carve<float4>(no128); sph_o32 = carve<float4>(no32);
@@ -617,12 +618,13 @@ struct Impl final : ImplBase {
       k1_count = carve<int>(1);
     }
     k1_sched = carve<unsigned>(4);
+    k1_range = carve<long long>(2);
   }
 
   int init(const cakf_config& c) override {
     Dp = c.d_time; dim = c.space_dim; nu2 = c.spatial_kernel; policy = c.policy;
-    nhat = c.max_iter; rcap = c.max_rank; Tmax = c.max_steps; NX = c.n_space; D = NX * Dp;
-    Nmax = c.max_obs > 0 ? std::min<int64_t>(c.max_obs, NX) : NX;
+    nhat = c.max_iter; rcap = c.max_rank; Tmax = c.max_steps; NXf = c.n_space; Df = NXf * Dp;
+    Nmax = c.max_obs > 0 ? std::min<int64_t>(c.max_obs, NXf) : NXf;
     rtol = c.rtol; ell = c.ell_x; seed = c.seed; reorth = c.reorth != 0;
     keep = c.keep_carriers != 0;
     blk = std::max(1, std::min<int>(c.block_actions, std::max(1, 1 + nhat)));
@@ -646,6 +648,13 @@ struct Impl final : ImplBase {
       const ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
       if (r != ncclSuccess) return fail(CAKF_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
+    // this rank's rows: 128-aligned equal slices of the internal (kd-ordered, spatially compact) point order
+    pslice = coll ? k2_slice_rows((int)NXf, world) : NXf;
+    plo = std::min<int64_t>(NXf, (int64_t)rank * pslice);
+    NX = std::max<int64_t>(0, std::min<int64_t>(NXf, plo + pslice) - plo);
+    D = NX * Dp;
+    if (NX < 1) return fail(CAKF_E_ARG, "multi-GPU: every rank needs at least one 128-point slice of the grid");
+    if (world > 1 && smooth_k2) return fail(CAKF_E_UNSUPPORTED, "CAKF_SMOOTH_K2=1 is single-GPU only");
     if (rtol != 0.0) return fail(CAKF_E_UNSUPPORTED, "rtol != 0 is not supported by the device path (R2)");
     std::vector<double> st0;
     if (!fetch_doubles(c.sigma_t0, (size_t)Dp * Dp, st0)) return fail(CAKF_E_ARG, "cannot read sigma_t0");
@@ -694,34 +703,34 @@ struct Impl final : ImplBase {
     ctl_init_host->eta_min = INFINITY;
     // coordinates: copy (host or device doubles) and prescale by sqrt(2 nu)/ell
     std::vector<double> xyz;
-    if (!fetch_doubles(c.coords, (size_t)NX * dim, xyz)) return fail(CAKF_E_ARG, "cannot read coords");
+    if (!fetch_doubles(c.coords, (size_t)NXf * dim, xyz)) return fail(CAKF_E_ARG, "cannot read coords");
     make_perm(xyz);
-    std::vector<int> inv(NX);
-    std::vector<double> xyz_int((size_t)NX * dim);
-    for (int64_t i = 0; i < NX; ++i) {
+    std::vector<int> inv(NXf);
+    std::vector<double> xyz_int((size_t)NXf * dim);
+    for (int64_t i = 0; i < NXf; ++i) {
       inv[perm_h[i]] = (int)i;
       for (int d = 0; d < dim; ++d) xyz_int[i * dim + d] = xyz[(size_t)perm_h[i] * dim + d];
     }
-    CK_CUDA(cudaMemcpyAsync(perm_d, perm_h.data(), NX * sizeof(int), cudaMemcpyHostToDevice, st));
-    CK_CUDA(cudaMemcpyAsync(invperm_d, inv.data(), NX * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(perm_d, perm_h.data(), NXf * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(invperm_d, inv.data(), NXf * sizeof(int), cudaMemcpyHostToDevice, st));
     double* dxyz = reinterpret_cast<double*>(stage64);
-    CK_CUDA(cudaMemcpyAsync(dxyz, xyz_int.data(), (size_t)NX * dim * sizeof(double), cudaMemcpyHostToDevice, st));
-    CK_CUDA(launch_prescale_coords<T>((int)NX, dim, dxyz, std::sqrt((double)nu2) / ell, coords, st));
+    CK_CUDA(cudaMemcpyAsync(dxyz, xyz_int.data(), (size_t)NXf * dim * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK_CUDA(launch_prescale_coords<T>((int)NXf, dim, dxyz, std::sqrt((double)nu2) / ell, coords, st));
     if (cull) {  // the smoother's K2 lists depend on the (fixed) grid only
       const float4* xf = reinterpret_cast<const float4*>(coords);
-      const int nx128 = (int)((NX + 127) / 128), nx32 = (int)((NX + 31) / 32);
+      const int nx128 = (int)((NXf + 127) / 128), nx32 = (int)((NXf + 31) / 32);
       CK_CUDA(cudaMemsetAsync(cull_ctr, 0, 4 * sizeof(unsigned long long), st));
-      CK_CUDA(launch_tile_spheres(xf, (int)NX, 128, sph_x128, st));
-      CK_CUDA(launch_tile_spheres(xf, (int)NX, 32, sph_x32, st));
+      CK_CUDA(launch_tile_spheres(xf, (int)NXf, 128, sph_x128, st));
+      CK_CUDA(launch_tile_spheres(xf, (int)NXf, 32, sph_x32, st));
       CK_CUDA(launch_k2_active(sph_x128, nx128, sph_x32, nx32, kCullCut, act_cnt_sm, act_list_sm, act_stride_sm,
                                cull_ctr + 2, st));
     }
-    std::vector<T> mu(D, T(0));
+    std::vector<T> mu(D, T(0));   // this rank's rows of the prior mean, internal order
     if (c.mu0) {
       std::vector<double> m0;
-      if (!fetch_doubles(c.mu0, D, m0)) return fail(CAKF_E_ARG, "cannot read mu0");
+      if (!fetch_doubles(c.mu0, Df, m0)) return fail(CAKF_E_ARG, "cannot read mu0");
       for (int d = 0; d < Dp; ++d)
-        for (int64_t i = 0; i < NX; ++i) mu[d * NX + i] = (T)m0[d * NX + perm_h[i]];
+        for (int64_t i = 0; i < NX; ++i) mu[d * NX + i] = (T)m0[d * NXf + perm_h[plo + i]];
     }
     CK_CUDA(cudaMemcpyAsync(mu0, mu.data(), D * sizeof(T), cudaMemcpyHostToDevice, st));
     CK_CUDA(cudaStreamSynchronize(st));
@@ -759,10 +768,11 @@ struct Impl final : ImplBase {
     P.A_next = A;
     S.sig_t = mat_abat_plus_q(A, P.sig_t, Q, Dp);                     // Sigma^t_k
     CK_CUDA(StepKernels<T>::mix((int)NX, Dp, 1, A, false, P.m, D, S.m_pred, D, st));   // m^- = A m
-    if (b) {   // user point order -> internal order (unpermute with the inverse permutation)
-      CK_CUDA(cudaMemcpyAsync(outm, b, D * sizeof(T), cudaMemcpyDefault, st));
-      CK_CUDA(unpermute<T>((int)NX, Dp, invperm_d, outm, tmp, st));
-      CK_CUDA(axpy<T>((size_t)D, 1.0, tmp, S.m_pred, st));
+    if (b) {   // user point order -> internal order (unpermute with the inverse permutation), this rank's rows
+      CK_CUDA(cudaMemcpyAsync(outm, b, Df * sizeof(T), cudaMemcpyDefault, st));
+      CK_CUDA(unpermute<T>((int)NXf, Dp, invperm_d, outm, outv, st));
+      for (int d = 0; d < Dp; ++d)
+        CK_CUDA(axpy<T>((size_t)NX, 1.0, outv + (size_t)d * NXf + plo, S.m_pred + (size_t)d * NX, st));
     }
     const T* src = P.truncated ? Mtil : P.Mk;
     const int rin = P.truncated ? P.rank_out : P.cols;
@@ -803,10 +813,10 @@ struct Impl final : ImplBase {
       CK_CUDA(cudaMemcpyAsync(sigma_inv, siginv_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
     } else {
       if (kd_obs) {   // internal order, then the per-update kd order over the observed points
-        CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, sigma_inv, st));
+        CK_CUDA(obs_sort(N, (int)NXf, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, sigma_inv, st));
         CK_CUDA(kd_obs_order<T>(N, idx_tmp, coords, sigma, sigma_inv, idx_out, sig_tmp, kd_ws, kd_ws_bytes, st));
       } else {
-        CK_CUDA(obs_sort(N, (int)NX, stage64, invperm_d, posof, obs_cnt, idx_out, sigma, sigma_inv, st));
+        CK_CUDA(obs_sort(N, (int)NXf, stage64, invperm_d, posof, obs_cnt, idx_out, sigma, sigma_inv, st));
       }
       CK_CUDA(cudaMemcpyAsync(idx_cache, idx_out, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
       CK_CUDA(cudaMemcpyAsync(sig_cache, sigma, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
@@ -822,13 +832,13 @@ struct Impl final : ImplBase {
   // K1 exactly as the inner loop launches it (observation order, exact-zero culling lists, dynamic unit
   // scheduler, symmetric partial slots), for one user vector s: out = K(X_obs, X_obs) s in the user's
   // observation order.  Test entry point (cakf_debug_matvec); clobbers the inner-loop workspaces.
-  int debug_matvec(int64_t n_obs, const int64_t* obs_idx, const void* s_user, void* out_user) override {
+  int debug_matvec(int64_t n_obs, const int64_t* obs_idx, const void* s_user, void* out_user, int shares) override {
     if (phase == 1) return fail(CAKF_E_STATE, "debug_matvec: not between predict and update");
     if (n_obs < 1 || n_obs > Nmax || !obs_idx || !s_user || !out_user) return fail(CAKF_E_ARG, "debug_matvec: bad argument");
     const int N = (int)n_obs;
     if (!is_device_ptr(obs_idx))
       for (int i = 0; i < N; ++i)
-        if (obs_idx[i] < 0 || obs_idx[i] >= NX) return fail(CAKF_E_ARG, "debug_matvec: obs_idx out of range");
+        if (obs_idx[i] < 0 || obs_idx[i] >= NXf) return fail(CAKF_E_ARG, "debug_matvec: obs_idx out of range");
     int* idx = sig_st;   // scratch index list: the sampler's per-step slot 0 (step 0 is never observed)
     CK(stage_obs(N, obs_idx, idx));
     CK_CUDA(cudaMemcpyAsync(ybuf_user, s_user, (size_t)N * sizeof(T), cudaMemcpyDefault, st));
@@ -845,13 +855,25 @@ struct Impl final : ImplBase {
           CK_CUDA(launch_tile_spheres(xf, N, 128, sph_o128, st));
           CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st));
           CK_CUDA(launch_tile_spheres(xf, N, 16, sph_o16, st));
-          const long long U = matvec_sym_units(N);
-          CK_CUDA(launch_k1_active_units(sph_o128, N, 0, U, kCullCut, k1_list, k1_mask, k1_count, st));
           CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)matvec_sym_tiles(N) * N * sizeof(T), st));
         }
-        CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial), 0,
-                                  matvec_sym_units(N), st, nullptr, cull ? k1_list : nullptr, k1_count, k1_mask,
-                                  sph_o16, sph_o128, sph_o32, kCullCut, k1_sched));
+        // shares > 1: the multi-GPU split (units balanced by active tile pairs), every share in turn into the
+        // same partial slots (disjoint units: the sum is the one-launch result bit for bit)
+        const long long U = matvec_sym_units(N);
+        for (int p = 0; p < std::max(1, shares); ++p) {
+          if (cull) {
+            if (shares > 1) {
+              CK_CUDA(launch_k1_balanced_range(sph_o128, N, kCullCut, p, shares, k1_range, st));
+              CK_CUDA(launch_k1_active_units(sph_o128, N, 0, U, kCullCut, k1_list, k1_mask, k1_count, st, k1_range));
+            } else {
+              CK_CUDA(launch_k1_active_units(sph_o128, N, 0, U, kCullCut, k1_list, k1_mask, k1_count, st));
+            }
+          }
+          CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
+                                    cull ? 0 : U * p / std::max(1, shares), cull ? U : U * (p + 1) / std::max(1, shares),
+                                    st, nullptr, cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128,
+                                    sph_o32, kCullCut, k1_sched));
+        }
       } else {
         CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
       }
@@ -889,7 +911,7 @@ struct Impl final : ImplBase {
       return fail(CAKF_E_ARG, "update: coordinate policy needs coord_order");
     if (!is_device_ptr(obs_idx)) {
       for (int i = 0; i < N; ++i)
-        if (obs_idx[i] < 0 || obs_idx[i] >= NX) return fail(CAKF_E_ARG, "update: obs_idx out of range");
+        if (obs_idx[i] < 0 || obs_idx[i] >= NXf) return fail(CAKF_E_ARG, "update: obs_idx out of range");
     }
     if (policy == CAKF_POLICY_COORD && niter > 0 && !is_device_ptr(coord_order)) {
       for (int i = 0; i < niter; ++i)
@@ -912,10 +934,13 @@ struct Impl final : ImplBase {
     }
     const int rin = S.rin;
     IterCtl* C = &ctl[k];
-    // ---- H M^- (N x rin) and r^(0), first action
-    if (rin) CK_CUDA(StepKernels<T>::gather_rows(N, rin, S.idx, S.Mk, D, HM, N, st));
-    CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, S.m_pred, policy, order32, seed, k, sigma, r, s, S.XV, xcs,
-                                 st));
+    // ---- [H m^-, H M^-] (N x (1 + rin)) from the ranks owning the observed rows (zeros elsewhere, summed),
+    // then r^(0) and the first action
+    HM = hmx + N;
+    CK_CUDA(StepKernels<T>::gather_rows(N, 1, S.idx, S.m_pred, D, hmx, N, (int)plo, (int)NX, st));
+    if (rin) CK_CUDA(StepKernels<T>::gather_rows(N, rin, S.idx, S.Mk, D, HM, N, (int)plo, (int)NX, st));
+    CK(allreduce(hmx, (size_t)N * (1 + rin)));
+    CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, hmx, policy, order32, seed, k, sigma, r, s, S.XV, xcs, st));
     const double sig00 = S.sig_t.a[0][0];
     const double eps = sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON;
     const bool sym = sizeof(T) == 4 && use_sym_k1();
@@ -924,13 +949,17 @@ struct Impl final : ImplBase {
       CK_CUDA(launch_tile_spheres(xf, N, 128, sph_o128, st));
       CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st));
       CK_CUDA(launch_tile_spheres(xf, N, 16, sph_o16, st));
-      CK_CUDA(launch_k2_active(sph_x128, (int)((NX + 127) / 128), sph_o32, (N + 31) / 32, kCullCut, act_cnt_po,
-                               act_list_po, act_stride_po, cull_ctr + 1, st));
+      CK_CUDA(launch_k2_active(sph_x128 + plo / 128, (int)((NX + 127) / 128), sph_o32, (N + 31) / 32, kCullCut,
+                               act_cnt_po, act_list_po, act_stride_po, cull_ctr + 1, st));
       k2_post_dense += (double)((NX + 127) / 128) * ((N + 31) / 32);
       if (sym) {  // active K1 units of this rank; the skipped units' partial slots stay zero
         const long long U = matvec_sym_units(N);
-        CK_CUDA(launch_k1_active_units(sph_o128, N, U * rank / world, U * (rank + 1) / world, kCullCut, k1_list,
-                                       k1_mask, k1_count, st));
+        if (world > 1) {   // contiguous unit range holding 1/world of the active tile pairs (same on every rank)
+          CK_CUDA(launch_k1_balanced_range(sph_o128, N, kCullCut, rank, world, k1_range, st));
+          CK_CUDA(launch_k1_active_units(sph_o128, N, 0, U, kCullCut, k1_list, k1_mask, k1_count, st, k1_range));
+        } else {
+          CK_CUDA(launch_k1_active_units(sph_o128, N, 0, U, kCullCut, k1_list, k1_mask, k1_count, st));
+        }
         CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)matvec_sym_tiles(N) * N * sizeof(T), st));
       }
     }
@@ -984,8 +1013,10 @@ struct Impl final : ImplBase {
       if constexpr (sizeof(T) == 4) {
         if (sym) {
           const long long U = matvec_sym_units(N);
+          // culling: the unit list (this rank's balanced share) defines the work; else the unit-index range
           CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
-                                    U * rank / world, U * (rank + 1) / world, st, cull ? cull_ctr : nullptr,
+                                    cull ? 0 : U * rank / world, cull ? U : U * (rank + 1) / world, st,
+                                    cull ? cull_ctr : nullptr,
                                     cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128, sph_o32, kCullCut,
                                     k1_sched));
           if (cull) {
@@ -1030,7 +1061,8 @@ struct Impl final : ImplBase {
     // ---- post-loop: [P^- w, P^- W] = Sigma H^T [v V] - M^- (H M^-)^T [v V]
     const int Cc = 1 + niter;
     size_t pk = prof_begin();
-    CK(k2(coords, (int)NX, xcs, N, S.XV, N, Cc, S.KV, NX, cull ? act_cnt_po : nullptr, act_list_po, act_stride_po));
+    CK(k2(coords + plo, (int)NX, xcs, N, S.XV, N, Cc, S.KV, NX, cull ? act_cnt_po : nullptr, act_list_po,
+          act_stride_po));
     prof_end(CAKF_PROF_K2_POST, pk);
     if (rin) {
       pk = prof_begin();
@@ -1175,6 +1207,7 @@ struct Impl final : ImplBase {
       CK_CUDA((gemm_f64acc<float, float, double>)(true, false, c, c, (int)D, 1.0, F, (size_t)D, F, (size_t)D, 0.0, Gm,
                                                   (size_t)c, fwork, kF64WorkDoubles, st));
     }
+    CK(allreduce(Gm, (size_t)c * c));   // row-sharded factor: the Gram is the sum of the ranks' partial Grams
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
     CK(eig(c, rkeep, kept, dropped, failflag));
@@ -1217,6 +1250,7 @@ struct Impl final : ImplBase {
     // fp64 accumulation for the Gram and M Q_r on the FP64 pipe (CAKF_GEMM_F64=1 for fp32, and fp64 mode)
     size_t ps = prof_begin();
     CK(gram_fp64(F, c));
+    CK(allreduce(Gm, (size_t)c * c));   // row-sharded factor: the Gram is the sum of the ranks' partial Grams
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
     ps = prof_begin();
     CK(eig(c, rkeep, kept, dropped, failflag));
@@ -1257,7 +1291,7 @@ struct Impl final : ImplBase {
     int q = ST.n;
     CK_CUDA(StepKernels<T>::fill(D, T(0), X, st));
     CK_CUDA(StepKernels<T>::fill((size_t)std::max(ST.N, 1), T(0), R, st));
-    CK_CUDA(StepKernels<T>::ws_build(ST.N, D, ST.n, 0, ST.idx, X, ST.XV, R, Ws, ws, st));
+    CK_CUDA(StepKernels<T>::ws_build(ST.N, D, ST.n, 0, ST.idx, X, ST.XV, R, Ws, ws, (int)plo, (int)NX, st));
     // (I (x) K) of the carriers: [K(X,T) v_T; 0], [K(X,T) V_T; 0] from the stored post-loop products
     if (!smooth_k2) CK_CUDA(StepKernels<T>::kcar_build(NX, Dp, ST.n, 0, ST.KV, nullptr, nullptr, KWs, Kws, st));
     ST.smoother_rank = q;
@@ -1287,13 +1321,15 @@ struct Impl final : ImplBase {
       pk = prof_begin();
       if (rin) {
         CK(gemm(OP_T, OP_N, rin, C, (int)D, 1.0, S.Mk, (int)D, X, (int)D, 0.0, Tm, rin));
+        CK(allreduce(Tm, (size_t)rin * C));   // M^-T x over all rows: sum of the ranks' partial products
         CK(gemm(OP_N, OP_N, (int)D, C, rin, -1.0, S.Mk, (int)D, Tm, rin, 1.0, yb, (int)D));
       }
       // P_k x = y - B_k (V^T H y);  R = V (V^T H y)
       if (n) {
         T* Vk = S.XV + N;
-        CK_CUDA(StepKernels<T>::gather_rows(N, C, S.idx, yb, D, Hy, N, st));
+        CK_CUDA(StepKernels<T>::gather_rows(N, C, S.idx, yb, D, Hy, N, (int)plo, (int)NX, st));
         CK(gemm(OP_T, OP_N, n, C, N, 1.0, Vk, N, Hy, N, 0.0, tt, n));
+        CK(allreduce(tt, (size_t)n * C));     // V^T H y: each rank holds the observed rows it owns (zeros elsewhere)
         CK(gemm(OP_N, OP_N, (int)D, C, n, -1.0, S.Mk + (size_t)rin * D, (int)D, tt, n, 1.0, yb, (int)D));
         CK(gemm(OP_N, OP_N, N, C, n, 1.0, Vk, N, tt, n, 0.0, R, N));
       }
@@ -1301,7 +1337,7 @@ struct Impl final : ImplBase {
       // m^s_k = m_k + P_k A^T w^s ;  var^s_k = var_k - rowsumsq(P_k A^T W^s)   (lines 5-6)
       CK_CUDA(StepKernels<T>::smooth_out(D, C, S.m, S.var, yb, S.ms, S.vs, st));
       // w^s_k, W^s_k = [W_k, (I - W W^T P^-) A^T W^s]   (lines 7-8)
-      CK_CUDA(StepKernels<T>::ws_build(n ? N : 0, D, n, q, S.idx, X, S.XV, R, Wf, ws, st));
+      CK_CUDA(StepKernels<T>::ws_build(n ? N : 0, D, n, q, S.idx, X, S.XV, R, Wf, ws, (int)plo, (int)NX, st));
       if (!smooth_k2) {
         // (I (x) K) W^s_full = [[K(X,T) V; 0], Kx[:,1:] - [K(X,T) V t[:,1:]; 0]], same for w^s with column 0
         pk = prof_begin();
@@ -1342,6 +1378,7 @@ struct Impl final : ImplBase {
   int interpolate(int k, const double* A1p, const double* Q1p, const double* A2p, int which, void* mean,
                   void* var) override {
     if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
+    if (world > 1) return fail(CAKF_E_UNSUPPORTED, "cakf_interpolate: single-GPU handles only");
     if (k < 1 || k > kcur) return fail(CAKF_E_ARG, "interpolate: k outside [1, steps done]");
     if (k == kcur && phase != 0) return fail(CAKF_E_STATE, "interpolate: step k not truncated yet");
     if (which != CAKF_FILTER && which != CAKF_SMOOTH) return fail(CAKF_E_ARG, "interpolate: bad which");
@@ -1411,6 +1448,7 @@ struct Impl final : ImplBase {
   // w^s_k = w_k + (I - W_k W_k^T P^-_k) A_k^T w^s_{k+1}.  Same kernels as the update / smoother.
   int sample(int S, const void* x0, const void* q, const void* eps, int which, void* out) override {
     if (failed_) return fail(CAKF_E_STATE, "handle failed earlier");
+    if (world > 1) return fail(CAKF_E_UNSUPPORTED, "cakf_sample: single-GPU handles only");
     if (phase != 0 || kcur < 1) return fail(CAKF_E_STATE, "sample: expected after the last truncate");
     if (S < 1 || S > 1 + std::min(nhat, qmax)) return fail(CAKF_E_ARG, "sample: n_samples outside [1, 1 + max_iter]");
     if (which != CAKF_FILTER && which != CAKF_SMOOTH) return fail(CAKF_E_ARG, "sample: bad which");
@@ -1470,7 +1508,8 @@ struct Impl final : ImplBase {
         CK(k2(coords, (int)NX, xcs, N, u, N, S, Yb, NX, cull ? act_cnt_po : nullptr, act_list_po, act_stride_po));
         const T* tmpp = nullptr;
         if (rin) {
-          CK_CUDA(StepKernels<T>::gather_rows(N, rin, K.idx, K.Mk, D, HM, N, st));
+          HM = hmx + N;
+          CK_CUDA(StepKernels<T>::gather_rows(N, rin, K.idx, K.Mk, D, HM, N, 0, (int)NX, st));
           CK(gemm(OP_T, OP_N, rin, S, N, 1.0, HM, N, u, N, 0.0, Ub, rin));
           CK(gemm(OP_N, OP_N, (int)D, S, rin, 1.0, K.Mk, (int)D, Ub, rin, 0.0, tmp, (int)D));
           tmpp = tmp;
@@ -1501,7 +1540,7 @@ struct Impl final : ImplBase {
             CK_CUDA(sampler_ops<T>::scatter_rows(N, S, K.idx, ust + uoff[k], T(1), wsv, D, st));
             if (n) {
               const T* Vk = K.XV + N;
-              CK_CUDA(StepKernels<T>::gather_rows(N, S, K.idx, yb, D, Hy, N, st));
+              CK_CUDA(StepKernels<T>::gather_rows(N, S, K.idx, yb, D, Hy, N, 0, (int)NX, st));
               CK(gemm(OP_T, OP_N, n, S, N, 1.0, Vk, N, Hy, N, 0.0, tt, n));
               CK(gemm(OP_N, OP_N, N, S, n, 1.0, Vk, N, tt, n, 0.0, R, N));
               CK_CUDA(sampler_ops<T>::scatter_rows(N, S, K.idx, R, T(-1), wsv, D, st));
@@ -1548,16 +1587,34 @@ struct Impl final : ImplBase {
     } else {
       return fail(CAKF_E_ARG, "get: bad which");
     }
-    // internal -> user point order
+    // this rank's rows -> all rows (all-gather of the row slices) -> user point order
     if (mean) {
-      CK_CUDA(unpermute<T>((int)NX, Dp, perm_d, pm, outm, st));
-      CK_CUDA(cudaMemcpyAsync(mean, outm, D * sizeof(T), cudaMemcpyDefault, st));
+      const T* full = nullptr;
+      CK(gather_rows_all(pm, outv, &full));
+      CK_CUDA(unpermute<T>((int)NXf, Dp, perm_d, full, outm, st));
+      CK_CUDA(cudaMemcpyAsync(mean, outm, Df * sizeof(T), cudaMemcpyDefault, st));
     }
     if (var) {
-      CK_CUDA(unpermute<T>((int)NX, Dp, perm_d, pv, outv, st));
-      CK_CUDA(cudaMemcpyAsync(var, outv, D * sizeof(T), cudaMemcpyDefault, st));
+      const T* full = nullptr;
+      CK(gather_rows_all(pv, outm, &full));
+      CK_CUDA(unpermute<T>((int)NXf, Dp, perm_d, full, outv, st));
+      CK_CUDA(cudaMemcpyAsync(var, outv, Df * sizeof(T), cudaMemcpyDefault, st));
     }
     CK_CUDA(cudaStreamSynchronize(st));
+    return CAKF_OK;
+  }
+
+  // the full D vector (internal order) from the ranks' local rows: *out = local when one rank holds all rows,
+  // else the packed slices all-gathered (ncclAllGather) and unpacked into scratch (Df elements)
+  int gather_rows_all(const T* local, T* scratch, const T** out) {
+    if (NX == NXf) {
+      *out = local;
+      return CAKF_OK;
+    }
+    CK_CUDA(StepKernels<T>::pack_dslice(Dp, (int)NX, (int)pslice, local, yslice, st));
+    CK_NCCL(ncclAllGather(yslice, ygath, (size_t)Dp * pslice, sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, comm, st));
+    CK_CUDA(StepKernels<T>::unpack_dslices((int)NXf, Dp, (int)pslice, ygath, scratch, st));
+    *out = scratch;
     return CAKF_OK;
   }
 
@@ -1710,9 +1767,9 @@ int cakf_sample(cakf_t h, int32_t n_samples, const void* x0, const void* q, cons
   HANDLE_CHECK(h);
   return h->impl->sample(n_samples, x0, q, eps, which, out);
 }
-int cakf_debug_matvec(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* s, void* out) {
+int cakf_debug_matvec(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* s, void* out, int32_t shares) {
   HANDLE_CHECK(h);
-  return h->impl->debug_matvec(n_obs, obs_idx, s, out);
+  return h->impl->debug_matvec(n_obs, obs_idx, s, out, shares);
 }
 int cakf_cull_stats(cakf_t h, double* frac3) {
   HANDLE_CHECK(h);

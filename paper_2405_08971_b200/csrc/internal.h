@@ -33,8 +33,12 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
 // sched (nullable, 2 zero-initialised counters, one per handle): dynamic unit scheduling (CAKF_K1_DYN=0: off)
 int matvec_sym_blocks_per_tile_pair();   // warp blocks per 128 x 128 tile pair counted by done_pairs
 // compact ascending list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`
+// urange (nullable, device): read [u_lo, u_hi) from it instead (the balanced multi-GPU split below)
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
-                                   unsigned short* mask, int* count, cudaStream_t st);
+                                   unsigned short* mask, int* count, cudaStream_t st, const long long* urange = nullptr);
+// multi-GPU: the unit range of `rank` with an equal share of the active tile pairs (deterministic) -> urange[2]
+cudaError_t launch_k1_balanced_range(const float4* sph, int n, float cut, int rank, int world, long long* urange,
+                                     cudaStream_t st);
 // bounding spheres (x, y, z, radius) of consecutive tiles of `tile` points
 cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st);
 // fp32 exact-zero cut: a prescaled distance above which ex2.approx.ftz(-a log2 e) flushes to 0

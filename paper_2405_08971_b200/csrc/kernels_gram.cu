@@ -606,7 +606,11 @@ __device__ unsigned sym_unit_mask(const float4* __restrict__ sph, int nt, int nb
 // the order inside a bucket is arbitrary, which cannot change any result (each unit owns its partial slots)
 __global__ void k1_active_units_kernel(const float4* __restrict__ sph, int nt, int nb, long long u_lo, long long u_hi,
                                        float cut, int* __restrict__ list, unsigned short* __restrict__ mask,
-                                       int* __restrict__ count) {
+                                       int* __restrict__ count, const long long* __restrict__ urange) {
+  if (urange) {   // this rank's unit range, balanced by active tile pairs (k1_balanced_range_kernel)
+    u_lo = urange[0];
+    u_hi = urange[1];
+  }
   __shared__ int bucket[SYM_S * SYM_S + 1];
   if (threadIdx.x <= SYM_S * SYM_S) bucket[threadIdx.x] = 0;
   __syncthreads();
@@ -636,10 +640,62 @@ __global__ void k1_active_units_kernel(const float4* __restrict__ sph, int nt, i
 }
 
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
-                                   unsigned short* mask, int* count, cudaStream_t st) {
+                                   unsigned short* mask, int* count, cudaStream_t st, const long long* urange) {
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
-  k1_active_units_kernel<<<1, 1024, 0, st>>>(sph, nt, nb, u_lo, u_hi, cut, list, mask, count);
+  k1_active_units_kernel<<<1, 1024, 0, st>>>(sph, nt, nb, u_lo, u_hi, cut, list, mask, count, urange);
+  return note_launch_err();
+}
+
+// Multi-GPU split of K1 by work (not by unit index): the units in index order carry popc(mask) active tile
+// pairs each; rank p takes the contiguous unit range whose prefix work falls in [W p / world, W (p+1) / world).
+// One block, each thread a contiguous chunk of units; deterministic (the same range on every rank).
+__global__ void k1_balanced_range_kernel(const float4* __restrict__ sph, int nt, int nb, long long U, float cut,
+                                         int rank, int world, long long* __restrict__ urange) {
+  __shared__ long long csum[1025];
+  const int t = threadIdx.x, nthr = blockDim.x;
+  const long long per = (U + nthr - 1) / nthr, a = min(U, per * t), b = min(U, a + per);
+  long long w = 0;
+  for (long long u = a; u < b; ++u) w += __popc(sym_unit_mask(sph, nt, nb, u, cut));
+  csum[t + 1] = w;
+  if (t == 0) csum[0] = 0;
+  __syncthreads();
+  if (t == 0)
+    for (int x = 1; x <= nthr; ++x) csum[x] += csum[x - 1];
+  __syncthreads();
+  const long long total = csum[nthr];
+  const long long lo_w = total * rank / world, hi_w = total * (rank + 1) / world;
+  // boundary unit for a work target: the first unit whose inclusive prefix exceeds the target
+  auto boundary = [&](long long target, bool last) -> long long {
+    if (last) return U;
+    if (target <= 0) return 0;
+    // chunk containing the target, then a sequential scan inside it (only one thread calls this)
+    int lo = 0, hi = nthr;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (csum[mid + 1] <= target) lo = mid + 1;
+      else hi = mid;
+    }
+    long long acc = csum[lo], u = min(U, per * lo);
+    const long long ue = min(U, u + per);
+    for (; u < ue; ++u) {
+      acc += __popc(sym_unit_mask(sph, nt, nb, u, cut));
+      if (acc > target) return u + 1;
+    }
+    return ue;
+  };
+  if (t == 0) {
+    urange[0] = rank == 0 ? 0 : boundary(lo_w, false);
+    urange[1] = boundary(hi_w, rank == world - 1);
+  }
+}
+
+cudaError_t launch_k1_balanced_range(const float4* sph, int n, float cut, int rank, int world, long long* urange,
+                                     cudaStream_t st) {
+  const int nt = (n + SYM_T - 1) / SYM_T;
+  const int nb = (nt + SYM_S - 1) / SYM_S;
+  const long long U = (long long)nb * (nb + 1) / 2;
+  k1_balanced_range_kernel<<<1, 1024, 0, st>>>(sph, nt, nb, U, cut, rank, world, urange);
   return note_launch_err();
 }
 

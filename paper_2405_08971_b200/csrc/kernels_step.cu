@@ -170,7 +170,7 @@ __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __r
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= N) return;
   const int p = idx[row];
-  const T r0 = y[row] - mpred[p];                      // r^(0) = y - H m^-   
+  const T r0 = y[row] - mpred[row];                    // r^(0) = y - H m^-   (P:1515); mpred = H m^- (gathered)
   T s0;
   if (policy == 0) s0 = r0;                            // CG: s_1 = r^(1) = r^(0)  (R1)
   else if (policy == 1) s0 = (order[0] == row) ? T(1) : T(0);
@@ -398,13 +398,15 @@ dot_final_kernel(int N, const T* __restrict__ a_, const T* __restrict__ b_, doub
 }
 
 // ------------------------------------------------------------------ gathers / mixing
-// HM[row + j*N] = M[idx[row] + j*ldm]   (rows of block 0 picked by H)
+// HM[row + j*N] = M[idx[row] - lo + j*ldm]   (rows of block 0 picked by H) for the points this rank owns
+// (lo <= idx < lo + nl, M holds the local rows), zero for the others (summed across the ranks)
 template <typename T>
 __global__ void gather_rows_kernel(int N, int C, const int* __restrict__ idx, const T* __restrict__ M, size_t ldm,
-                                   T* __restrict__ out, size_t ldo) {
+                                   T* __restrict__ out, size_t ldo, int lo, int nl) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;   // grid (rows, columns)
   if (row >= N) return;
-  out[row + (size_t)j * ldo] = M[idx[row] + (size_t)j * ldm];
+  const int p = idx[row] - lo;
+  out[row + (size_t)j * ldo] = (p >= 0 && p < nl) ? M[p + (size_t)j * ldm] : T(0);
 }
 
 // out = (A (x) I) in  or (A^T (x) I) in, column by column (Lemma B.1 structure)
@@ -630,12 +632,14 @@ __global__ void kcar_build_kernel(size_t NX, size_t D, int n, int q, const T* __
 // step 2: scatter the observation-space terms into the train rows of block 0
 template <typename T>
 __global__ void ws_scatter_kernel(int N, size_t D, int n, int q, const int* __restrict__ idx, const T* __restrict__ XV,
-                                  const T* __restrict__ R, T* __restrict__ Wf, T* __restrict__ ws) {
+                                  const T* __restrict__ R, T* __restrict__ Wf, T* __restrict__ ws, int lo, int nl) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t total = (size_t)N * (n + q + 1);
   if (e >= total) return;
   const int row = (int)(e % N), j = (int)(e / N);
-  const size_t p = idx[row];
+  const int pl = idx[row] - lo;   // local row of the observed point (rows owned by this rank only)
+  if (pl < 0 || pl >= nl) return;
+  const size_t p = (size_t)pl;
   if (j == 0) ws[p] += XV[row] - R[row];                          // H^T v - H^T V t_0
   else if (j <= n) Wf[p + (size_t)(j - 1) * D] = XV[row + (size_t)j * N];   // H^T V
   else Wf[p + (size_t)(j - 1) * D] -= R[row + (size_t)(j - n) * N];         // - H^T V t_{1:}
@@ -889,10 +893,11 @@ cudaError_t StepKernels<T>::dot(int N, const T* a, const T* b, double* part, dou
 
 template <typename T>
 cudaError_t StepKernels<T>::gather_rows(int N, int C, const int* idx, const T* M, size_t ldm, T* out, size_t ldo,
+                                        int lo, int nl,
                                         cudaStream_t st) {
   if ((size_t)N * C == 0) return cudaSuccess;
   if (N <= 0 || C <= 0) return cudaSuccess;
-  gather_rows_kernel<T><<<dim3(nblk(N), C), 256, 0, st>>>(N, C, idx, M, ldm, out, ldo);
+  gather_rows_kernel<T><<<dim3(nblk(N), C), 256, 0, st>>>(N, C, idx, M, ldm, out, ldo, lo, nl);
   return note_launch_err();
 }
 
@@ -988,11 +993,38 @@ cudaError_t StepKernels<T>::kcar_build(int64_t NX, int Dp, int n, int q, const T
 
 template <typename T>
 cudaError_t StepKernels<T>::ws_build(int N, size_t D, int n, int q, const int* idx, const T* X, const T* XV,
-                                     const T* R, T* Wf, T* ws, cudaStream_t st) {
+                                     const T* R, T* Wf, T* ws, int lo, int nl, cudaStream_t st) {
   ws_dense_kernel<T><<<dim3(nblk(D), n + q + 1), 256, 0, st>>>(D, n, q, X, Wf, ws);
   cudaError_t e = note_launch_err();
   if (e != cudaSuccess || N == 0) return e;
-  ws_scatter_kernel<T><<<nblk((size_t)N * (n + q + 1)), 256, 0, st>>>(N, D, n, q, idx, XV, R, Wf, ws);
+  ws_scatter_kernel<T><<<nblk((size_t)N * (n + q + 1)), 256, 0, st>>>(N, D, n, q, idx, XV, R, Wf, ws, lo, nl);
+  return note_launch_err();
+}
+
+// row-sharded D vectors: pack a rank's local [d * nl + i] into [d * S + i] (zero padded), and assemble the
+// all-gathered packs into the full internal order [d * NX + p * S + i]
+template <typename T>
+__global__ void pack_dslice_kernel(int Dp, int nl, int S, const T* __restrict__ in, T* __restrict__ out) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)Dp * S) return;
+  const int d = (int)(e / S), i = (int)(e % S);
+  out[e] = i < nl ? in[(size_t)d * nl + i] : T(0);
+}
+template <typename T>
+__global__ void unpack_dslices_kernel(int NX, int Dp, int S, const T* __restrict__ G, T* __restrict__ out) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)Dp * NX) return;
+  const int d = (int)(e / NX), g = (int)(e % NX), p = g / S, i = g % S;
+  out[e] = G[(size_t)p * Dp * S + (size_t)d * S + i];
+}
+template <typename T>
+cudaError_t StepKernels<T>::pack_dslice(int Dp, int nl, int S, const T* in, T* out, cudaStream_t st) {
+  pack_dslice_kernel<T><<<nblk((size_t)Dp * S), 256, 0, st>>>(Dp, nl, S, in, out);
+  return note_launch_err();
+}
+template <typename T>
+cudaError_t StepKernels<T>::unpack_dslices(int NX, int Dp, int S, const T* G, T* out, cudaStream_t st) {
+  unpack_dslices_kernel<T><<<nblk((size_t)Dp * NX), 256, 0, st>>>(NX, Dp, S, G, out);
   return note_launch_err();
 }
 

@@ -68,7 +68,8 @@ struct StepKernels {
                             T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k, const int* sigma,
                             cudaStream_t st);
   static cudaError_t dot(int N, const T* a, const T* b, double* part, double* out, unsigned* cnt, cudaStream_t st);
-  static cudaError_t gather_rows(int N, int C, const int* idx, const T* M, size_t ldm, T* out, size_t ldo,
+  // rows of the points a rank owns (lo <= idx < lo + nl; M = local rows), zeros for the others
+  static cudaError_t gather_rows(int N, int C, const int* idx, const T* M, size_t ldm, T* out, size_t ldo, int lo, int nl,
                                  cudaStream_t st);
   static cudaError_t mix(int NX, int Dp, int C, const Mat3& A, bool transpose, const T* in, size_t ldi, T* out,
                          size_t ldo, cudaStream_t st);
@@ -86,10 +87,13 @@ struct StepKernels {
   //   Kws = [KV_0 - Z_0; 0] + Kx_0,  KWf = [[KV_1..n; 0], Kx_1..q - [Z_1..q; 0]]
   static cudaError_t kcar_build(int64_t NX, int Dp, int n, int q, const T* KV, const T* Z, const T* Kx, T* KWf,
                                 T* Kws, cudaStream_t st);
+  // D = local rows; observations of points outside [lo, lo + nl) are skipped
   static cudaError_t ws_build(int N, size_t D, int n, int q, const int* idx, const T* X, const T* XV, const T* R,
-                              T* Wf, T* ws, cudaStream_t st);
+                              T* Wf, T* ws, int lo, int nl, cudaStream_t st);
   static cudaError_t fill(size_t n, T val, T* out, cudaStream_t st);
   static cudaError_t assemble_slices(int M, int C, int slice, const T* G, T* Y, size_t ldy, cudaStream_t st);
+  static cudaError_t pack_dslice(int Dp, int nl, int S, const T* in, T* out, cudaStream_t st);
+  static cudaError_t unpack_dslices(int NX, int Dp, int S, const T* G, T* out, cudaStream_t st);
 };
 
 // posterior sampler helpers (alg:cakf-caks-sampler); S samples as columns

@@ -90,6 +90,11 @@ def test_k1_bench_launch_path_cfg3(cfg3):
         outs[cull] = h.debug_matvec(idx, s.astype(np.float32)).astype(np.float64)
         again = h.debug_matvec(idx, s.astype(np.float32)).astype(np.float64)   # cached order, same bits
         assert np.array_equal(again, outs[cull])
+        # the multi-GPU split of K1 (8 and 3 ranks' unit shares, balanced by active tile pairs with culling,
+        # by unit index without) covers every unit exactly once: the same bits as one launch
+        for shares in (8, 3):
+            assert np.array_equal(h.debug_matvec(idx, s.astype(np.float32), shares=shares).astype(np.float64),
+                                  outs[cull])
         h.destroy()
     assert np.array_equal(outs[True], outs[False])
     y = outs[True]

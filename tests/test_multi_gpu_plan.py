@@ -1,9 +1,10 @@
-"""Multi-GPU decomposition on CPU: the library's shard plan (host-only C-ABI
-functions) and a world_size-2 gloo run of the same exchange pattern the GPU path uses:
-  K1  rank p evaluates symmetric tile-block units [u_lo, u_hi), all-reduce(sum) of the N-vector;
-  K2  rank p computes output rows [row_lo, row_hi), all-gather of the row slices.
-The per-rank products here come from the oracle's chunked kernel rows, so the test checks the
-plan and the collectives, not the CUDA kernels (those are covered by the GPU parity tests)."""
+"""Multi-GPU decomposition on CPU: the library's shard plan (host-only C-ABI functions)
+and world_size 2 / 3 gloo runs of the row-sharded exchange pattern of the device path (include/cakf.h):
+rank p owns points [row_lo, row_hi) and their rows of every D-length array; [H m^-, H M^-] and K1's
+N-vector (symmetric units [u_lo, u_hi)) are all-reduced, the truncation Gram is the all-reduced sum of
+partial Grams (eig replicated), the smoother all-reduces M^-T x and V^T H y, K2 and the rest stay local.
+The per-rank products come from the oracle, so the test checks the plan and the collectives, not the
+CUDA kernels (tests/test_gpu_*: the forced-collective path at world 1, K1's balanced split emulated)."""
 import os
 import socket
 
@@ -59,14 +60,34 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, X, s, B, nu, ell, out_q):
+def _worker(rank, world, port, prob, out_q):
+    """One rank of the row-sharded exchange pattern of the device path (include/cakf.h, multi-GPU):
+    rows [row_lo, row_hi) of every D-length array (both derivative blocks), replicated N-length state."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     binding.load()
-    n = len(X)
-    plan = binding.shard_plan(n, n, world, rank)
-    # K1: this rank's symmetric units -> partial N-vector, then all-reduce
+    X, s, M, x, V, obs, nu, ell, Dp, r = (prob[k] for k in ("X", "s", "M", "x", "V", "obs", "nu", "ell", "Dp", "r"))
+    NX = len(X)
+    plan = binding.shard_plan(NX, len(obs), world, rank)
+    lo, hi = plan["row_lo"], plan["row_hi"]
+    rows = np.concatenate([np.arange(lo, hi) + d * NX for d in range(Dp)])   # this rank's D rows
+    Mp, xp = M[rows], x[rows]
+
+    def allreduce(a):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        dist.all_reduce(t)
+        return t.numpy()
+
+    out = {}
+    # update: [H m^-, H M^-] -- each rank the observed rows it owns, zeros elsewhere, summed
+    own = (obs >= lo) & (obs < hi)
+    HMp = np.zeros((len(obs), M.shape[1]))
+    HMp[own] = M[obs[own]]
+    out["HM"] = allreduce(HMp)
+    # K1: this rank's symmetric units (index split of the plan), all-reduce of the N-vector
+    Xt = X[obs]
+    n = len(obs)
     y = np.zeros(n)
     bp = plan["block_points"]
     for u in range(plan["u_lo"], plan["u_hi"]):
@@ -74,45 +95,74 @@ def _worker(rank, world, port, X, s, B, nu, ell, out_q):
         I = slice(bi * bp, min(n, (bi + 1) * bp))
         J = slice(bj * bp, min(n, (bj + 1) * bp))
         if bi == bj:
-            y[I] += mfree.gram_apply(X[I], X[I], s[I], nu, ell)
+            y[I] += mfree.gram_apply(Xt[I], Xt[I], s[I], nu, ell)
         else:
-            y[I] += mfree.gram_apply(X[I], X[J], s[J], nu, ell)
-            y[J] += mfree.gram_apply(X[J], X[I], s[I], nu, ell)
-    yt = torch.from_numpy(y)
-    dist.all_reduce(yt)
-    # K2: this rank's output row slice, then all-gather of equal-size (padded) slices
-    slice_rows = plan["slice_rows"]
-    Ys = np.zeros((slice_rows, B.shape[1]))
-    lo, hi = plan["row_lo"], plan["row_hi"]
-    if hi > lo:
-        Ys[: hi - lo] = mfree.gram_apply(X[lo:hi], X, B, nu, ell)
-    parts = [torch.zeros_like(torch.from_numpy(Ys)) for _ in range(world)]
-    dist.all_gather(parts, torch.from_numpy(Ys))
-    Y = torch.cat(parts)[:n].numpy()
-    if rank == 0:
-        out_q.put((yt.numpy(), Y))
+            y[I] += mfree.gram_apply(Xt[I], Xt[J], s[J], nu, ell)
+            y[J] += mfree.gram_apply(Xt[J], Xt[I], s[I], nu, ell)
+    out["Ks"] = allreduce(y)
+    # post-loop K2: this rank's rows of K(X, X_T) [v V] -- no exchange
+    out["KV_rows"] = (lo, hi, mfree.gram_apply(X[lo:hi], Xt, V, nu, ell))
+    # truncation: partial Grams summed, replicated eig, local rows of M Q_r
+    G = allreduce(Mp.T @ Mp)
+    lam, Q = np.linalg.eigh(G)
+    out["G"] = G
+    out["MQ_rows"] = (rows, Mp @ Q[:, -r:])
+    # smoother: M^T x partials summed, local rows of y = x - M (M^T x); V^T H y partial over owned observations
+    t = allreduce(Mp.T @ xp)
+    yl = xp - Mp @ t
+    out["y_rows"] = (rows, yl)
+    Hy = np.zeros((n, x.shape[1]))
+    pos = {g: i for i, g in enumerate(rows)}
+    for j, o in enumerate(obs):
+        if lo <= o < hi:
+            Hy[j] = yl[pos[o]]
+    out["VtHy"] = allreduce(V.T @ Hy)
+    out_q.put((rank, out))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n", [300, 2100])
-def test_sharded_products_gloo_world2(n):
-    rng = np.random.default_rng(n)
-    X = rng.standard_normal((n, 3)) * 2.0
-    s = rng.standard_normal(n)
-    B = rng.standard_normal((n, 5))
-    nu, ell = 1.5, 0.9
+@pytest.mark.parametrize("n_space,world", [(300, 2), (700, 3)])
+def test_row_sharded_exchanges_gloo(n_space, world):
+    """The row-sharded decomposition with the library's own plan (cakf_shard_plan), world 2 and 3 on gloo:
+    every exchanged quantity equals its unsharded value, every local row block reassembles the full one."""
+    rng = np.random.default_rng(n_space)
+    Dp, c, r = 2, 12, 8
+    X = rng.standard_normal((n_space, 3)) * 2.0
+    obs = np.sort(rng.choice(n_space, n_space * 3 // 4, replace=False))
+    prob = {"X": X, "s": rng.standard_normal(len(obs)), "M": rng.standard_normal((Dp * n_space, c)),
+            "x": rng.standard_normal((Dp * n_space, 5)), "V": rng.standard_normal((len(obs), 4)), "obs": obs,
+            "nu": 1.5, "ell": 0.9, "Dp": Dp, "r": r}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, X, s, B, nu, ell, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(k, world, port, prob, q)) for k in range(world)]
     for p in procs:
         p.start()
-    y, Y = q.get(timeout=300)
+    outs = dict(q.get(timeout=600) for _ in range(world))
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    ref_y = mfree.gram_apply(X, X, s, nu, ell)
-    ref_Y = mfree.gram_apply(X, X, B, nu, ell)
-    assert np.allclose(y, ref_y, rtol=1e-12, atol=1e-10)
-    assert np.allclose(Y, ref_Y, rtol=1e-12, atol=1e-10)
+    M, x, V = prob["M"], prob["x"], prob["V"]
+    Xt = X[obs]
+    G = M.T @ M
+    lam, Q = np.linalg.eigh(G)
+    y_full = x - M @ (M.T @ x)
+    KV = mfree.gram_apply(X, Xt, V, 1.5, 0.9)
+    MQ = M @ Q[:, -r:]
+    KV_got, MQ_got, y_got = np.zeros_like(KV), np.zeros_like(MQ), np.zeros_like(y_full)
+    for k, o in outs.items():
+        assert np.allclose(o["HM"], M[obs], rtol=0, atol=0)             # zeros + one value: exact
+        assert np.allclose(o["Ks"], mfree.gram_apply(Xt, Xt, prob["s"], 1.5, 0.9), rtol=1e-12, atol=1e-10)
+        assert np.allclose(o["G"], G, rtol=1e-12, atol=1e-10)
+        assert np.allclose(o["VtHy"], V.T @ y_full[obs], rtol=1e-12, atol=1e-10)
+        lo, hi, blk = o["KV_rows"]
+        KV_got[lo:hi] = blk
+        rows, blk = o["MQ_rows"]
+        MQ_got[rows] = blk
+        rows, blk = o["y_rows"]
+        y_got[rows] = blk
+    assert np.allclose(KV_got, KV, rtol=1e-12, atol=1e-10)
+    # eigenvectors: equal up to sign per column (identical Gram bits on every rank -> identical eig)
+    assert np.allclose(np.abs(MQ_got), np.abs(MQ), rtol=1e-9, atol=1e-9)
+    assert np.allclose(y_got, y_full, rtol=1e-12, atol=1e-10)
