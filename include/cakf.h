@@ -71,8 +71,14 @@ enum cakf_kernel { CAKF_MATERN12 = 1, CAKF_MATERN32 = 3, CAKF_MATERN52 = 5 };
 /* Policy (Sec. 3.3, App. C.3):
  *   CAKF_POLICY_CG     s_i = current residual r^(i)           (R1; the paper's choice)
  *   CAKF_POLICY_COORD  s_i = e_{order[i-1]}                    (coordinate actions)
- *   CAKF_POLICY_RANDOM s_i ~ N(0, I) by Philox4x32-10 (R16)    (randomized actions) */
-enum cakf_policy { CAKF_POLICY_CG = 0, CAKF_POLICY_COORD = 1, CAKF_POLICY_RANDOM = 2 };
+ *   CAKF_POLICY_RANDOM s_i ~ N(0, I) by Philox4x32-10 (R16)    (randomized actions)
+ *   CAKF_POLICY_BLOCKRES  the adaptive block policy of alg:projected_update:
+ *                      a block of b = block_actions actions is chosen at once from the residual at the
+ *                      block's start, r^(i0) restricted to b regions of the observations:
+ *                      s_{i0+j} = r^(i0) * 1[floor(u b / N) == j], u = the observation's position in the
+ *                      caller's order (contiguous index ranges: latitude bands on ERA5-shaped grids);
+ *                      b = 1 is CG.  Executed as one multi-RHS K2 per block (tensor cores). */
+enum cakf_policy { CAKF_POLICY_CG = 0, CAKF_POLICY_COORD = 1, CAKF_POLICY_RANDOM = 2, CAKF_POLICY_BLOCKRES = 3 };
 
 /* which-selector of cakf_get */
 enum cakf_which { CAKF_PRED = 0, CAKF_FILTER = 1, CAKF_SMOOTH = 2 };
@@ -102,7 +108,8 @@ typedef struct {
                                kernel part of G s for b consecutive actions with one multi-RHS
                                product (K2, tensor cores); same arithmetic as b sequential
                                iterations.  1 = one K1 matvec per iteration.  Ignored
-                               for CG (each action depends on the previous residual)              */
+                               for CG (each action depends on the previous residual); the block
+                               size of CAKF_POLICY_BLOCKRES                                       */
   int32_t keep_carriers;    /* 1 = keep the smoother carriers w^s_k, W^s_k of every step (an extra
                                (T+1) x D x (1 + r) values) so cakf_interpolate can return smoother
                                states between steps (Cor. A.10); 0 = filter interpolation only */

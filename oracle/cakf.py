@@ -40,15 +40,28 @@ from .philox import random_action
 
 
 # --------------------------------------------------------------------------- policies
-def make_policy(kind: str, coord_order=None, seed: int = 1):
+def make_policy(kind: str, coord_order=None, seed: int = 1, block: int = 1):
     """Policy(k, i, r^(i), n) -> action s (App. C.3).
 
-    cg     : s = r^(i)                    (CG/Lanczos actions)
-    coord  : s = e_{order_k[i-1]}          (coordinate actions)
-    random : s ~ N(0, I) via Philox (R16) (randomized actions)
+    cg       : s = r^(i)                    (CG/Lanczos actions)
+    coord    : s = e_{order_k[i-1]}          (coordinate actions)
+    random   : s ~ N(0, I) via Philox (R16) (randomized actions)
+    blockres : a block of b actions chosen at once from the residual at the block's start i0 = 1, 1+b, ...
+               (the batch Policy call of alg:projected_update, repeated per block):
+               s_{i0+j} = r^(i0) * 1[floor(u b / n) == j] for observation u = 0..n-1; b = 1 is CG
     """
     if kind == "cg":
         return lambda k, i, r, n: r.copy()
+    if kind == "blockres":
+        state = {}
+
+        def pol(k, i, r, n):
+            j = (i - 1) % block
+            if j == 0:
+                state["r0"] = r.copy()
+            region = (np.arange(n, dtype=np.int64) * block) // n
+            return np.where(region == j, state["r0"], 0.0)
+        return pol
     if kind == "coord":
         def pol(k, i, r, n):
             s = np.zeros(n)
@@ -185,9 +198,9 @@ class StepRecord:
 
 
 def cakf_filter(ssm: SSM, policy_kind="cg", max_iter=64, max_rank=-1, coord_order=None,
-                action_seed=1, rtol=0.0, eps=np.finfo(np.float64).eps, cgs2=True):
+                action_seed=1, rtol=0.0, eps=np.finfo(np.float64).eps, cgs2=True, block=1):
     """alg:mfkf: predict, Update unless IsMissing, Truncate."""
-    policy = make_policy(policy_kind, coord_order, action_seed)
+    policy = make_policy(policy_kind, coord_order, action_seed, block)
     D = ssm.D
     m = ssm.mu0.copy()
     Sig0 = ssm.Sigma(0)
@@ -254,6 +267,7 @@ def run_workload(wl, dtype_round=None, max_rank=None, smoother=True):
     ssm = ssm_from_workload(wl, dtype_round=dtype_round)
     mr = wl.max_rank if max_rank is None else max_rank
     tr = cakf_filter(ssm, wl.policy, wl.max_iter, mr, coord_order=wl.coord_order,
-                     action_seed=wl.action_seed, rtol=wl.rtol, cgs2=wl.reorth)
+                     action_seed=wl.action_seed, rtol=wl.rtol, cgs2=wl.reorth,
+                     block=max(1, min(getattr(wl, "block_actions", 1), 1 + wl.max_iter)))
     sm = caks_smoother(ssm, tr, mr) if smoother else None
     return ssm, tr, sm

@@ -179,7 +179,8 @@ def run_mf(wl, dtype_round=None, smoother=True, chunk=1024, cache=False, perturb
     mm = MFModel(wl, dtype_round, chunk, cache=cache)
     if perturb_y:
         mm.ys = [y * (1.0 + perturb_y) for y in mm.ys]
-    pol = make_policy(wl.policy, wl.coord_order, wl.action_seed)
+    pol = make_policy(wl.policy, wl.coord_order, wl.action_seed,
+                      max(1, min(getattr(wl, "block_actions", 1), 1 + wl.max_iter)))
     D = mm.D
     m = np.zeros(D)
     Mt = np.zeros((D, 0))

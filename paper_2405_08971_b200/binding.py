@@ -21,9 +21,10 @@ LIB_PATH = os.environ.get("CAKF_LIB") or os.path.join(HERE, "libcakf.so")   # CA
 
 CAKF_F32, CAKF_F64 = 0, 1
 CAKF_MATERN12, CAKF_MATERN32, CAKF_MATERN52 = 1, 3, 5
-CAKF_POLICY_CG, CAKF_POLICY_COORD, CAKF_POLICY_RANDOM = 0, 1, 2
+CAKF_POLICY_CG, CAKF_POLICY_COORD, CAKF_POLICY_RANDOM, CAKF_POLICY_BLOCKRES = 0, 1, 2, 3
 CAKF_PRED, CAKF_FILTER, CAKF_SMOOTH = 0, 1, 2
-POLICIES = {"cg": CAKF_POLICY_CG, "coord": CAKF_POLICY_COORD, "random": CAKF_POLICY_RANDOM}
+POLICIES = {"cg": CAKF_POLICY_CG, "coord": CAKF_POLICY_COORD, "random": CAKF_POLICY_RANDOM,
+            "blockres": CAKF_POLICY_BLOCKRES}
 KERNELS = {0.5: CAKF_MATERN12, 1.5: CAKF_MATERN32, 2.5: CAKF_MATERN52}
 DTYPES = {"f32": CAKF_F32, "f64": CAKF_F64, np.float32: CAKF_F32, np.float64: CAKF_F64}
 

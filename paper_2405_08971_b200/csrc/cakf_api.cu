@@ -213,6 +213,7 @@ struct Impl final : ImplBase {
   V4<T>* xcs = nullptr;
   T *r = nullptr, *s = nullptr, *g = nullptr, *gp = nullptr, *d = nullptr, *Gd = nullptr, *Z = nullptr, *HM = nullptr;
   T* hmx = nullptr;   // [H m^- | H M^-] (N x (1 + rin)): gathered from the owners of the observed rows
+  T* rbs = nullptr;   // CAKF_POLICY_BLOCKRES: the residual at the current block's start
   long long* k1_range = nullptr;   // multi-GPU: this rank's K1 unit range, balanced by active tile pairs
   T *ybuf = nullptr, *lam2 = nullptr, *partial = nullptr;
   size_t partial_cap = 0;
@@ -502,6 +503,7 @@ struct Impl final : ImplBase {
     ybuf = carve<T>(Nmax); lam2 = carve<T>(Nmax);
     Z = carve<T>((size_t)Nmax * std::max(nhat, 1));
     hmx = carve<T>((size_t)Nmax * (1 + std::max(rin_max, 1)));
+    rbs = carve<T>(Nmax);
     HM = hmx + Nmax;
     const int nch = matvec_chunks((int)Nmax, (int)Nmax, sizeof(T));
     partial_cap = (size_t)std::max<int64_t>({(int64_t)nch, (int64_t)64, (int64_t)matvec_sym_tiles((int)Nmax)}) * Nmax;
@@ -940,7 +942,8 @@ struct Impl final : ImplBase {
     CK_CUDA(StepKernels<T>::gather_rows(N, 1, S.idx, S.m_pred, D, hmx, N, (int)plo, (int)NX, st));
     if (rin) CK_CUDA(StepKernels<T>::gather_rows(N, rin, S.idx, S.Mk, D, HM, N, (int)plo, (int)NX, st));
     CK(allreduce(hmx, (size_t)N * (1 + rin)));
-    CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, hmx, policy, order32, seed, k, sigma, r, s, S.XV, xcs, st));
+    CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, hmx, policy, order32, seed, k, sigma, r, s, S.XV, xcs, st, blk,
+                                 rbs));
     const double sig00 = S.sig_t.a[0][0];
     const double eps = sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON;
     const bool sym = sizeof(T) == 4 && use_sym_k1();
@@ -1001,7 +1004,7 @@ struct Impl final : ImplBase {
         const int j = (i - 1) % blk;
         if (j == 0) {
           const int nb = std::min(blk, niter - i + 1);
-          CK_CUDA(StepKernels<T>::gen_actions(N, i, nb, policy, order32, seed, k, sigma, Sblk, N, st));
+          CK_CUDA(StepKernels<T>::gen_actions(N, i, nb, policy, order32, seed, k, sigma, Sblk, N, st, rbs, blk));
           CK(k2(xcs, N, xcs, N, Sblk, N, nb, Yblk, N, cull ? act_cnt_tt : nullptr, act_list_tt, act_stride_po));
         }
         kpart = Yblk + (size_t)j * N;
@@ -1054,7 +1057,8 @@ struct Impl final : ImplBase {
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W,
                                        nullptr, cnt + 128, C, eps, i, 0, st));
       }
-      CK_CUDA(StepKernels<T>::stageD(N, i, niter, C, d, Gd, S.XV, Z, r, s, xcs, policy, order32, seed, k, sigma, st));
+      CK_CUDA(StepKernels<T>::stageD(N, i, niter, C, d, Gd, S.XV, Z, r, s, xcs, policy, order32, seed, k, sigma, st, blk,
+                                     rbs));
       prof_end(CAKF_PROF_STAGES, pk);
     }
     CK_CUDA(StepKernels<T>::dot(N, r, r, part, &C->res_sq, cnt + 192, st));
@@ -1702,7 +1706,7 @@ int cakf_create(const cakf_config* cfg, cakf_t* out) {
   if (cfg->spatial_kernel != 1 && cfg->spatial_kernel != 3 && cfg->spatial_kernel != 5)
     return fail(CAKF_E_UNSUPPORTED, "cakf_create: spatial_kernel must be MATERN12/32/52");
   if (!(cfg->ell_x > 0)) return fail(CAKF_E_ARG, "cakf_create: ell_x must be > 0");
-  if (cfg->policy < 0 || cfg->policy > 2) return fail(CAKF_E_UNSUPPORTED, "cakf_create: unknown policy");
+  if (cfg->policy < 0 || cfg->policy > 3) return fail(CAKF_E_UNSUPPORTED, "cakf_create: unknown policy");
   if (cfg->max_iter < 0 || cfg->max_steps < 1) return fail(CAKF_E_ARG, "cakf_create: bad max_iter / max_steps");
   ImplBase* impl = nullptr;
   if (cfg->dtype == CAKF_F32) impl = new Impl<float>();

@@ -162,11 +162,14 @@ bool side_slim() {   // CAKF_SIDE_SLIM=0: side-stream HM kernels without the 80-
 }
 
 // ------------------------------------------------------------------ update prologue
+// BLOCKRES region of the observation at user position u: floor(u b / N)  (CAKF_POLICY_BLOCKRES)
+__device__ __forceinline__ int block_region(int u, int N, int b) { return (int)(((long long)u * b) / N); }
+
 template <typename T>
 __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __restrict__ coords, const T* __restrict__ y,
                             const T* __restrict__ mpred, int policy, const int* __restrict__ order, uint64_t seed, int k,
                             const int* __restrict__ sigma, T* __restrict__ r, T* __restrict__ s, T* __restrict__ v,
-                            V4<T>* __restrict__ xcs) {
+                            V4<T>* __restrict__ xcs, int nblk_pol, T* __restrict__ rbs) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= N) return;
   const int p = idx[row];
@@ -174,10 +177,12 @@ __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __r
   T s0;
   if (policy == 0) s0 = r0;                            // CG: s_1 = r^(1) = r^(0)  (R1)
   else if (policy == 1) s0 = (order[0] == row) ? T(1) : T(0);
+  else if (policy == 3) s0 = block_region(sigma ? sigma[row] : row, N, nblk_pol) == 0 ? r0 : T(0);   // BLOCKRES
   else s0 = (T)philox_normal(seed, (uint32_t)k, 1u, (uint32_t)(sigma ? sigma[row] : row));   // R16: user position
   r[row] = r0;
   s[row] = s0;
   v[row] = T(0);
+  if (rbs) rbs[row] = r0;   // BLOCKRES: residual at the block's start
   V4<T> c = coords[p];
   c.w = s0;
   xcs[row] = c;
@@ -187,13 +192,15 @@ __global__ void prep_kernel(int N, const int* __restrict__ idx, const V4<T>* __r
 // formulas as prep / stageD — coordinate e_{order[i-1]}, random Philox(seed; j = user position, i, k)
 template <typename T>
 __global__ void gen_actions_kernel(int N, int i0, int nb, int policy, const int* __restrict__ order, uint64_t seed,
-                                   int k, const int* __restrict__ sigma, T* __restrict__ S, size_t ldS) {
+                                   int k, const int* __restrict__ sigma, T* __restrict__ S, size_t ldS,
+                                   const T* __restrict__ rbs, int nblk_pol) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (size_t)N * nb) return;
   const int row = (int)(e % N), j = (int)(e / N);
   const int i = i0 + j;
   T v;
-  if (policy == 1) v = (order[i - 1] == row) ? T(1) : T(0);
+  if (policy == 3) v = block_region(sigma ? sigma[row] : row, N, nblk_pol) == (i - 1) % nblk_pol ? rbs[row] : T(0);
+  else if (policy == 1) v = (order[i - 1] == row) ? T(1) : T(0);
   else v = (T)philox_normal(seed, (uint32_t)k, (uint32_t)i, (uint32_t)(sigma ? sigma[row] : row));
   S[row + (size_t)j * ldS] = v;
 }
@@ -365,7 +372,7 @@ template <typename T>
 __global__ void stageD_kernel(int N, int iter, int niter, const IterCtl* __restrict__ ctl, const T* __restrict__ d,
                               const T* __restrict__ Gd, T* __restrict__ XV, T* __restrict__ Z, T* __restrict__ r,
                               T* __restrict__ s, V4<T>* __restrict__ xcs, int policy, const int* __restrict__ order,
-                              uint64_t seed, int k, const int* __restrict__ sigma) {
+                              uint64_t seed, int k, const int* __restrict__ sigma, int nblk_pol, T* __restrict__ rbs) {
   griddep_wait();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= N) return;
@@ -380,6 +387,17 @@ __global__ void stageD_kernel(int N, int iter, int niter, const IterCtl* __restr
     T sn;
     if (policy == 0) sn = rn;
     else if (policy == 1) sn = (order[iter] == row) ? T(1) : T(0);
+    else if (policy == 3) {   // BLOCKRES: iteration iter+1 is in-block position iter % b; a new block restarts
+      const int jb = iter % nblk_pol;   // from the current residual
+      T base;
+      if (jb == 0) {
+        rbs[row] = rn;
+        base = rn;
+      } else {
+        base = rbs[row];
+      }
+      sn = block_region(sigma ? sigma[row] : row, N, nblk_pol) == jb ? base : T(0);
+    }
     else sn = (T)philox_normal(seed, (uint32_t)k, (uint32_t)(iter + 1), (uint32_t)(sigma ? sigma[row] : row));
     s[row] = sn;
     xcs[row].w = sn;
@@ -815,17 +833,20 @@ int stage_blocks(int N) { return N > 0 ? (N + kTile - 1) / kTile : 1; }
 template <typename T>
 cudaError_t StepKernels<T>::prep(int N, const int* idx, const V4<T>* coords, const T* y, const T* mpred, int policy,
                                  const int* order, uint64_t seed, int k, const int* sigma, T* r, T* s, T* v, V4<T>* xcs,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int nblk_pol, T* rbs) {
   if (N <= 0) return cudaSuccess;
-  prep_kernel<T><<<nblk(N), 256, 0, st>>>(N, idx, coords, y, mpred, policy, order, seed, k, sigma, r, s, v, xcs);
+  prep_kernel<T><<<nblk(N), 256, 0, st>>>(N, idx, coords, y, mpred, policy, order, seed, k, sigma, r, s, v, xcs,
+                                          std::max(nblk_pol, 1), policy == 3 ? rbs : nullptr);
   return note_launch_err();
 }
 
 template <typename T>
 cudaError_t StepKernels<T>::gen_actions(int N, int i0, int nb, int policy, const int* order, uint64_t seed, int k,
-                                        const int* sigma, T* S, size_t ldS, cudaStream_t st) {
+                                        const int* sigma, T* S, size_t ldS, cudaStream_t st, const T* rbs,
+                                        int nblk_pol) {
   if ((size_t)N * nb == 0) return cudaSuccess;
-  gen_actions_kernel<T><<<nblk((size_t)N * nb), 256, 0, st>>>(N, i0, nb, policy, order, seed, k, sigma, S, ldS);
+  gen_actions_kernel<T><<<nblk((size_t)N * nb), 256, 0, st>>>(N, i0, nb, policy, order, seed, k, sigma, S, ldS, rbs,
+                                                              std::max(nblk_pol, 1));
   return note_launch_err();
 }
 
@@ -879,9 +900,9 @@ cudaError_t StepKernels<T>::stageC(int N, const T* V, const T* Z, int nV, const 
 template <typename T>
 cudaError_t StepKernels<T>::stageD(int N, int iter, int niter, const IterCtl* ctl, const T* d, const T* Gd, T* XV,
                                    T* Z, T* r, T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k,
-                                   const int* sigma, cudaStream_t st) {
+                                   const int* sigma, cudaStream_t st, int nblk_pol, T* rbs) {
   return launch_pdl(stageD_kernel<T>, dim3(nblk(N)), dim3(256), 0, st, N, iter, niter, ctl, d, Gd, XV, Z, r, s, xcs,
-                    policy, order, seed, k, sigma);
+                    policy, order, seed, k, sigma, std::max(nblk_pol, 1), rbs);
 }
 
 template <typename T>

@@ -46,12 +46,13 @@ template <typename T>
 struct StepKernels {
   static cudaError_t prep(int N, const int* idx, const V4<T>* coords, const T* y, const T* mpred, int policy,
                           const int* order, uint64_t seed, int k, const int* sigma, T* r, T* s, T* v, V4<T>* xcs,
-                          cudaStream_t st);
+                          cudaStream_t st, int nblk_pol = 1, T* rbs = nullptr);   // BLOCKRES: block size, r^(i0)
   static cudaError_t stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s, const T* r,
                             T* gp, const T* HM, int rin, double* part, int W, double* red, unsigned* cnt,
                             cudaStream_t st);
   static cudaError_t gen_actions(int N, int i0, int nb, int policy, const int* order, uint64_t seed, int k,
-                                 const int* sigma, T* S, size_t ldS, cudaStream_t st);
+                                 const int* sigma, T* S, size_t ldS, cudaStream_t st, const T* rbs = nullptr,
+                                 int nblk_pol = 1);
   // HM == nullptr in stageA: u = HM^T s is computed by hmts (side stream) into red[0, rin)
   static cudaError_t hmts(int N, const T* HM, int rin, const T* s, double* part, int W, double* red, unsigned* cnt,
                           cudaStream_t st);
@@ -66,7 +67,7 @@ struct StepKernels {
                             cudaStream_t st);
   static cudaError_t stageD(int N, int iter, int niter, const IterCtl* ctl, const T* d, const T* Gd, T* XV, T* Z, T* r,
                             T* s, V4<T>* xcs, int policy, const int* order, uint64_t seed, int k, const int* sigma,
-                            cudaStream_t st);
+                            cudaStream_t st, int nblk_pol = 1, T* rbs = nullptr);
   static cudaError_t dot(int N, const T* a, const T* b, double* part, double* out, unsigned* cnt, cudaStream_t st);
   // rows of the points a rank owns (lo <= idx < lo + nl; M = local rows), zeros for the others
   static cudaError_t gather_rows(int N, int C, const int* idx, const T* M, size_t ldm, T* out, size_t ldo, int lo, int nl,

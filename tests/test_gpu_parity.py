@@ -324,3 +324,18 @@ def test_reorth0_sphere48_fp64(policy, iters, rank):
         o = farthest_point_order(wl.coords[wl.obs_idx[0]], iters)
         wl.coord_order = [o.copy() for _ in range(wl.T)]
     compare(wl, "f64", 1e-9, 1e-9)
+
+
+# ------------------------------------------------ adaptive block policy (alg:projected_update per block, §8f row 3)
+@pytest.mark.parametrize("b,iters,rank", [(1, 12, 20), (3, 12, 20), (4, 16, 24), (5, 12, -1)])
+def test_blockres_policy_fp64(b, iters, rank):
+    """CAKF_POLICY_BLOCKRES: a block of b actions chosen at once from the block-start residual (restricted
+    to b regions of the observations) and executed as ONE multi-RHS tensor-core K2 per block; b = 1 is CG.
+    Against the oracle's sequential update on the same policy: fp64 1e-9, integer stats bit-exact."""
+    wl = make_workload("sphere48", policy="blockres", max_iter=iters, max_rank=rank, T=5, block_actions=b)
+    compare(wl, "f64", 1e-9, 1e-9)
+
+
+def test_blockres_policy_fp32():
+    wl = make_workload("sphere48", policy="blockres", max_iter=16, max_rank=24, T=4, block_actions=4)
+    compare_fp32_cancellation(wl)

@@ -197,3 +197,34 @@ def test_missing_steps_give_prior():
     sm = cakf.caks_smoother(ssm, tr, 2)
     for k in range(ssm.T + 1):
         assert np.allclose(tr[k].m, 0) and np.allclose(sm["var"][k], np.diag(ssm.Sigma(k)))
+
+
+def test_blockres_policy_pins():
+    """The adaptive block policy (alg:projected_update's batch Policy call per block of b actions):
+    b = 1 is CG exactly; for any b each block of actions spans the block-start residual (the actions sum to it),
+    and the iterative update on the recorded actions equals alg:projected_update on them."""
+    from oracle import cakf
+    from oracle.model import ssm_from_workload
+    from synth import make_workload
+    wl = make_workload("line8", policy="cg", max_iter=5, max_rank=-1, T=2)
+    ssm = ssm_from_workload(wl)
+    tr_cg = cakf.cakf_filter(ssm, "cg", 5)
+    tr_b1 = cakf.cakf_filter(ssm, "blockres", 5, block=1)
+    for a, b in zip(tr_cg, tr_b1):
+        assert np.array_equal(a.m, b.m) and np.array_equal(a.var, b.var)
+    wl = make_workload("sphere48", T=2, max_iter=9, max_rank=-1)
+    ssm = ssm_from_workload(wl)
+    tr = cakf.cakf_filter(ssm, "blockres", 9, block=3)
+    for k in (1, 2):
+        rec = tr[k]
+        S = rec.upd.S
+        assert S.shape[1] == 9 - rec.upd.rejected
+        # each block's actions are disjointly supported pieces of one residual
+        for blk in range(3):
+            cols = S[:, 3 * blk:3 * blk + 3]
+            assert np.all(np.count_nonzero(cols, axis=1) <= 1)
+        m, M, w, W = cakf.update_batch(rec.m_pred, rec.M_pred, ssm.Sigma(k), ssm.H(k), ssm.obs[k - 1][2], ssm.y(k), S)
+        assert np.allclose(m, rec.m, rtol=1e-9, atol=1e-9 * np.max(np.abs(rec.m)))
+        P1 = ssm.Sigma(k) - M @ M.T
+        P2 = ssm.Sigma(k) - rec.M @ rec.M.T
+        assert np.allclose(np.diag(P1), np.diag(P2), rtol=1e-8)
