@@ -87,6 +87,8 @@ CASES = {
     + [("sphere48", dict(policy="cg", max_iter=16, max_rank=24, T=5, reorth=False), "f64", True)],
     "sphere24": [("sphere24", dict(policy=p, max_iter=16, max_rank=24, T=4), d, True)
                  for p in ("random", "coord", "cg") for d in ("f64", "f32")],
+    "blockres": [("sphere48", dict(policy="blockres", max_iter=16, max_rank=24, T=5, block_actions=4), d, True)
+                 for d in ("f64", "f32")],
     "cfg2": [("cfg2", dict(policy=p, T=6), d, False) for p in ("random", "coord", "cg") for d in ("f64", "f32")]
     + [("cfg2", dict(policy="cg", T=6, max_iter=6, max_rank=16), d, False) for d in ("f64", "f32")],
 }
@@ -94,7 +96,7 @@ CASES = {
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cases", default="cfg1,sphere48,sphere24,cfg2")
+    ap.add_argument("--cases", default="cfg1,sphere48,sphere24,blockres,cfg2")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     rows = []
