@@ -214,6 +214,8 @@ struct Impl final : ImplBase {
   T *r = nullptr, *s = nullptr, *g = nullptr, *gp = nullptr, *d = nullptr, *Gd = nullptr, *Z = nullptr, *HM = nullptr;
   T* hmx = nullptr;   // [H m^- | H M^-] (N x (1 + rin)): gathered from the owners of the observed rows
   T* rbs = nullptr;   // CAKF_POLICY_BLOCKRES: the residual at the current block's start
+  void* samp_ws = nullptr;   // cakf_sample workspace (grow-only, freed at destroy)
+  size_t samp_bytes = 0;
   long long* k1_range = nullptr;   // multi-GPU: this rank's K1 unit range, balanced by active tile pairs
   T *ybuf = nullptr, *lam2 = nullptr, *partial = nullptr;
   size_t partial_cap = 0;
@@ -442,6 +444,7 @@ struct Impl final : ImplBase {
 
   ~Impl() override {
     if (st) cudaStreamSynchronize(st);
+    if (samp_ws) cudaFree(samp_ws);
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (arena) cudaFree(arena);
     if (ctl_init_host) cudaFreeHost(ctl_init_host);
@@ -1464,7 +1467,15 @@ struct Impl final : ImplBase {
     for (int k = 1; k <= T_; ++k) n_obs_total += (size_t)steps[k].N;
     T* xs = nullptr;
     const size_t bytes = ((size_t)(T_ + 1) * DS + 3 * DS + n_obs_total * S * 2 + 1024) * sizeof(T);
-    CK_CUDA(cudaMallocAsync(&xs, bytes, st));
+    // grow-only workspace kept by the handle (no allocation inside repeated sampler calls)
+    if (samp_bytes < bytes) {
+      if (samp_ws) CK_CUDA(cudaFreeAsync(samp_ws, st));
+      samp_ws = nullptr;
+      samp_bytes = 0;
+      CK_CUDA(cudaMallocAsync(&samp_ws, bytes, st));
+      samp_bytes = bytes;
+    }
+    xs = static_cast<T*>(samp_ws);
     T* xtmp = xs + (size_t)(T_ + 1) * DS;   // D x S scratch (user order staging)
     T* wsv = xtmp + DS;                     // w^s (D x S)
     T* xsm = wsv + DS;                      // one smoother sample (D x S)
@@ -1472,7 +1483,7 @@ struct Impl final : ImplBase {
     T* epsd = ust + n_obs_total * S;        // eps of all steps (device copy)
     std::vector<size_t> uoff(T_ + 2, 0);
     for (int k = 1; k <= T_; ++k) uoff[k + 1] = uoff[k] + (size_t)steps[k].N * S;
-    auto cleanup = [&]() { cudaFreeAsync(xs, st); };
+    auto cleanup = [&]() {};
     auto run = [&]() -> int {
       CK_CUDA(cudaMemcpyAsync(epsd, eps, n_obs_total * S * sizeof(T), cudaMemcpyDefault, st));
       // x_0 (user order) -> internal
