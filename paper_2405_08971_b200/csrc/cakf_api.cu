@@ -300,7 +300,6 @@ struct Impl final : ImplBase {
   std::vector<int64_t> obs_cache_h;    // host copy (host-pointer callers)
   int64_t* obs_cache_d = nullptr;      // device copy (device-pointer callers)
   int *idx_cache = nullptr, *sig_cache = nullptr, *siginv_cache = nullptr, *neq_d = nullptr;
-  int* neq_h = nullptr;                // pinned
   void* kd_ws = nullptr;
   size_t kd_ws_bytes = 0;
 
@@ -448,7 +447,6 @@ struct Impl final : ImplBase {
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (arena) cudaFree(arena);
     if (ctl_init_host) cudaFreeHost(ctl_init_host);
-    if (neq_h) cudaFreeHost(neq_h);
     if (comm) ncclCommDestroy(comm);
     if (sol) cusolverDnDestroy(sol);
     if (own_stream && st) cudaStreamDestroy(st);
@@ -703,7 +701,6 @@ struct Impl final : ImplBase {
       CK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
     CK_CUDA(cudaMallocHost(&ctl_init_host, sizeof(IterCtl)));
-    if (!neq_h) CK_CUDA(cudaMallocHost(&neq_h, sizeof(int)));
     std::memset(ctl_init_host, 0, sizeof(IterCtl));
     ctl_init_host->eta_min = INFINITY;
     // coordinates: copy (host or device doubles) and prescale by sqrt(2 nu)/ell
@@ -796,41 +793,39 @@ struct Impl final : ImplBase {
   }
 
   // Observations in the internal point order of this update: idx_out (kd order over the observed points),
-  // sigma[j] = the user's position of row j, sigma_inv its inverse.  An update whose obs_idx equals the
-  // previous one's reuses the cached order (a pure function of obs_idx, so bit-identical).
+  // sigma[j] = the user's position of row j, sigma_inv its inverse.  The order is a pure function of obs_idx
+  // and is kept in a cache (idx_cache, sig_cache, siginv_cache): host-pointer callers compare on the host and
+  // skip the recompute; device-pointer callers compare ON THE DEVICE (neq_d) and every kernel of the
+  // recompute returns at once on a hit — no host round trip, the update stays stream-ordered.
   int stage_obs(int N, const int64_t* obs_idx, int* idx_out) {
     CK_CUDA(cudaMemcpyAsync(stage64, obs_idx, (size_t)N * sizeof(int64_t), cudaMemcpyDefault, st));
     const bool obs_host = !is_device_ptr(obs_idx);
-    bool same_obs = false;
-    if (obs_cache_n == N) {   // same observation set as the cached update (ERA5-style fixed stations)
-      if (obs_host && obs_cache_h.size() == (size_t)N) {
-        same_obs = std::memcmp(obs_idx, obs_cache_h.data(), (size_t)N * sizeof(int64_t)) == 0;
-      } else {
-        CK_CUDA(obs_neq(N, stage64, obs_cache_d, neq_d, st));
-        CK_CUDA(cudaMemcpyAsync(neq_h, neq_d, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK_CUDA(cudaStreamSynchronize(st));
-        same_obs = *neq_h == 0;
-      }
+    const int* run = nullptr;   // nullptr: recompute unconditionally
+    bool recompute = true;
+    if (obs_host) {
+      recompute = !(obs_cache_n == N && obs_cache_h.size() == (size_t)N &&
+                    std::memcmp(obs_idx, obs_cache_h.data(), (size_t)N * sizeof(int64_t)) == 0);
+    } else if (obs_cache_n == N) {
+      CK_CUDA(obs_neq(N, stage64, obs_cache_d, neq_d, st));   // *neq_d = 1 iff the set changed
+      run = neq_d;
     }
-    if (same_obs) {
-      CK_CUDA(cudaMemcpyAsync(idx_out, idx_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(sigma, sig_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(sigma_inv, siginv_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-    } else {
+    if (recompute) {
       if (kd_obs) {   // internal order, then the per-update kd order over the observed points
-        CK_CUDA(obs_sort(N, (int)NXf, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, sigma_inv, st));
-        CK_CUDA(kd_obs_order<T>(N, idx_tmp, coords, sigma, sigma_inv, idx_out, sig_tmp, kd_ws, kd_ws_bytes, st));
+        CK_CUDA(obs_sort(N, (int)NXf, stage64, invperm_d, posof, obs_cnt, idx_tmp, sig_tmp, siginv_cache, st, run));
+        CK_CUDA(kd_obs_order<T>(N, idx_tmp, coords, sig_cache, siginv_cache, idx_cache, sig_tmp, kd_ws, kd_ws_bytes,
+                                st, run));
       } else {
-        CK_CUDA(obs_sort(N, (int)NXf, stage64, invperm_d, posof, obs_cnt, idx_out, sigma, sigma_inv, st));
+        CK_CUDA(obs_sort(N, (int)NXf, stage64, invperm_d, posof, obs_cnt, idx_cache, sig_cache, siginv_cache, st,
+                         run));
       }
-      CK_CUDA(cudaMemcpyAsync(idx_cache, idx_out, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(sig_cache, sigma, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
-      CK_CUDA(cudaMemcpyAsync(siginv_cache, sigma_inv, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
       CK_CUDA(cudaMemcpyAsync(obs_cache_d, stage64, (size_t)N * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
       if (obs_host) obs_cache_h.assign(obs_idx, obs_idx + N);
       else obs_cache_h.clear();
       obs_cache_n = N;
     }
+    CK_CUDA(cudaMemcpyAsync(idx_out, idx_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(sigma, sig_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(sigma_inv, siginv_cache, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, st));
     return CAKF_OK;
   }
 

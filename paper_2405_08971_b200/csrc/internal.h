@@ -125,10 +125,12 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
 // ---- per-update kd-tree order of the observed points (kd_order.cu)
 size_t kd_obs_workspace(int Nmax);
 // idx/sig_in_sorted: the observations in internal point order (obs_sort); writes idx_out, sig_out
-// (user position of each row) and sig_inv in the kd order
+// (user position of each row) and sig_inv in the kd order.  run (nullable device flag): every kernel
+// returns at once when *run == 0.  Sync-free, no library sort.
 template <typename T>
 cudaError_t kd_obs_order(int N, const int* idx, const V4<T>* coords, int* sig_out, int* sig_inv, int* idx_out,
-                         const int* sig_in_sorted, void* ws, size_t ws_bytes, cudaStream_t st);
+                         const int* sig_in_sorted, void* ws, size_t ws_bytes, cudaStream_t st,
+                         const int* run = nullptr);
 
 // columns k(X, x_{order[i0-1+c]}), c < nb, of the kernel matrix (coordinate actions)
 template <typename T>

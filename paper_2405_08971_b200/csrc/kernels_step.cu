@@ -728,13 +728,18 @@ __global__ void gather_coords_kernel(int N, const int* __restrict__ idx, const V
   out[j] = c;
 }
 
-// ---- observation sort: internal index order (spatially compact tiles), fully on device
-__global__ void obs_mark_kernel(int N, const int64_t* __restrict__ obs, const int* __restrict__ invperm,
-                                int* __restrict__ posof) {
+// ---- observation sort: internal index order (spatially compact tiles), fully on device; every kernel
+// returns at once when the (nullable) device flag *run is 0 (the observation cache hit, decided on device)
+__device__ __forceinline__ bool obs_skip(const int* run) { return run != nullptr && *run == 0; }
+__global__ void obs_mark_kernel(int N, const int* __restrict__ run, const int64_t* __restrict__ obs,
+                                const int* __restrict__ invperm, int* __restrict__ posof) {
+  if (obs_skip(run)) return;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < N) posof[invperm[obs[j]]] = j;
 }
-__global__ void obs_count_kernel(int NX, const int* __restrict__ posof, int* __restrict__ counts) {
+__global__ void obs_count_kernel(int NX, const int* __restrict__ run, const int* __restrict__ posof,
+                                 int* __restrict__ counts) {
+  if (obs_skip(run)) return;
   __shared__ int wsum[32];
   const int i = blockIdx.x * 1024 + threadIdx.x;
   const unsigned b = __ballot_sync(0xffffffffu, i < NX && posof[i] >= 0);
@@ -746,17 +751,28 @@ __global__ void obs_count_kernel(int NX, const int* __restrict__ posof, int* __r
     counts[blockIdx.x] = t;
   }
 }
-__global__ void obs_scan_kernel(int nb, int* __restrict__ counts) {   // one thread: exclusive scan, nb <= ~1k
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int run = 0;
-  for (int b = 0; b < nb; ++b) {
-    const int c = counts[b];
-    counts[b] = run;
-    run += c;
+__global__ void obs_scan_kernel(int nb, const int* __restrict__ run, int* __restrict__ counts) {
+  // one warp: exclusive scan of the per-block counts, 32 at a time
+  if (obs_skip(run) || blockIdx.x != 0) return;
+  const int lane = threadIdx.x & 31;
+  int carry = 0;
+  for (int b0 = 0; b0 < nb; b0 += 32) {
+    const int b = b0 + lane;
+    const int c = b < nb ? counts[b] : 0;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (b < nb) counts[b] = carry + inc - c;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
   }
 }
-__global__ void obs_scatter_kernel(int NX, const int* __restrict__ posof, const int* __restrict__ offsets,
-                                   int* __restrict__ idx_out, int* __restrict__ sigma, int* __restrict__ sigma_inv) {
+__global__ void obs_scatter_kernel(int NX, const int* __restrict__ run, const int* __restrict__ posof,
+                                   const int* __restrict__ offsets, int* __restrict__ idx_out, int* __restrict__ sigma,
+                                   int* __restrict__ sigma_inv) {
+  if (obs_skip(run)) return;
   __shared__ int wpre[33];
   const int i = blockIdx.x * 1024 + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1134,18 +1150,18 @@ template struct sampler_ops<float>;
 template struct sampler_ops<double>;
 
 cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int* posof, int* counts, int* idx_out,
-                     int* sigma, int* sigma_inv, cudaStream_t st) {
+                     int* sigma, int* sigma_inv, cudaStream_t st, const int* run) {
   if (N <= 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(posof, 0xff, (size_t)NX * sizeof(int), st);   // -1
+  cudaError_t e = cudaMemsetAsync(posof, 0xff, (size_t)NX * sizeof(int), st);   // -1 (scratch: harmless on a skip)
   if (e != cudaSuccess) return e;
-  obs_mark_kernel<<<nblk(N), 256, 0, st>>>(N, obs, invperm, posof);
+  obs_mark_kernel<<<nblk(N), 256, 0, st>>>(N, run, obs, invperm, posof);
   if ((e = note_launch_err()) != cudaSuccess) return e;
   const int nb = (NX + 1023) / 1024;
-  obs_count_kernel<<<nb, 1024, 0, st>>>(NX, posof, counts);
+  obs_count_kernel<<<nb, 1024, 0, st>>>(NX, run, posof, counts);
   if ((e = note_launch_err()) != cudaSuccess) return e;
-  obs_scan_kernel<<<1, 32, 0, st>>>(nb, counts);
+  obs_scan_kernel<<<1, 32, 0, st>>>(nb, run, counts);
   if ((e = note_launch_err()) != cudaSuccess) return e;
-  obs_scatter_kernel<<<nb, 1024, 0, st>>>(NX, posof, counts, idx_out, sigma, sigma_inv);
+  obs_scatter_kernel<<<nb, 1024, 0, st>>>(NX, run, posof, counts, idx_out, sigma, sigma_inv);
   return note_launch_err();
 }
 

@@ -20,9 +20,10 @@ struct IterCtl {
 
 int stage_blocks(int N);   // blocks (128-row tiles) of the stage kernels
 cudaError_t idx64_to32(int n, const int64_t* in, int* out, cudaStream_t st);
-// observations -> internal point order: idx_out ascending, sigma[j] = user position, sigma_inv inverse
+// observations -> internal point order: idx_out ascending, sigma[j] = user position, sigma_inv inverse.
+// run (nullable device flag): the kernels return at once when *run == 0
 cudaError_t obs_sort(int N, int NX, const int64_t* obs, const int* invperm, int* posof, int* counts, int* idx_out,
-                     int* sigma, int* sigma_inv, cudaStream_t st);
+                     int* sigma, int* sigma_inv, cudaStream_t st, const int* run = nullptr);
 // *neq = (a[0:n] != b[0:n]) (device buffers)
 cudaError_t obs_neq(int n, const int64_t* a, const int64_t* b, int* neq, cudaStream_t st);
 template <typename T>

@@ -56,3 +56,22 @@ def test_changing_observation_sets(policy):
 def test_three_point_grid():
     wl = make_workload("line8", n=3, T=4, policy="cg", max_iter=2, max_rank=2, test_every=0)
     compare(wl, "f64", 1e-9, 1e-9)
+
+
+def test_observation_cache_device_and_host_pointers():
+    """Same-size sets that alternate membership (A, A, B, B, A, A): the observation-order cache is decided on
+    the device for device-pointer obs_idx (no host round trip) and on the host for host arrays.  Both paths
+    must match the oracle and each other bit for bit (the order is a pure function of obs_idx)."""
+    wl = make_workload("sphere48", T=6, policy="cg", max_iter=10, max_rank=16)
+    n = wl.n_space
+    rng = np.random.default_rng(11)
+    A = np.sort(rng.choice(n, size=n // 3, replace=False))
+    B = np.sort(rng.choice(n, size=n // 3, replace=False))
+    _reobserve(wl, [A, A, B, B, A, A[::-1].copy()])
+    _, errs = compare(wl, "f64", 1e-9, 1e-9, on_device=True)
+    from test_gpu_parity import run_device
+    dev = run_device(wl, "f64", on_device=True)
+    host = run_device(wl, "f64", on_device=False)
+    for a, b in zip(dev[1:5], host[1:5]):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
