@@ -130,13 +130,10 @@ __device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* tm, int c0
       : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-      "%14, %15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
 }
 
 // Persistent: CTA b takes work items w = b, b + grid, ... with w -> (n tile fastest, m tile, split z),
@@ -263,7 +260,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else {
-    // ===== epilogue (warps 2-5): one output row per thread, 16 columns per TMEM load
+    // ===== epilogue (warps 2-5): one output row per thread, 8 columns per TMEM load
     const int quarter = warp & 3;
     const bool direct = work == nullptr;
     int gc = 0;
@@ -274,19 +271,68 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int row = m0 + quarter * 32 + lane;
       for (int c = c0; c < c1; ++c, ++gc) {
         const int lc = c - c0;
+        // while the MMAs of this chunk run: pull the tile's old C (or split partial) lines into L2 so the
+        // drain below reads them at L2 latency (the epilogue is on the critical path between chunks)
+        if ((direct ? beta != 0.0 : lc != 0) && row < M) {
+          const size_t esz = (direct && !Cd) ? 4 : 8;
+          const char* base = !direct ? reinterpret_cast<const char*>(work + (size_t)z * N * M + row)
+                             : Cd      ? reinterpret_cast<const char*>(Cd + row)
+                                       : reinterpret_cast<const char*>(C + row);
+          const size_t ldb = (direct ? ldc : (size_t)M) * esz;
+          for (int t = 0; t < ntile && n0 + t < N; ++t)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)(n0 + t) * ldb));
+        }
+        const bool readold = direct ? beta != 0.0 : lc != 0;
+        // the 8 columns' global operands (B exponents, the old C or the split partial) of batch cb, all
+        // loads issued before any use (predicated); software-pipelined one batch ahead of the TMEM drain
+        auto fetch = [&](int cb, int (&codeB)[8], double (&old)[8]) {
+          bool ok[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int n = n0 + cb + t;
+            ok[t] = row < M && cb + t < ntile && n < N;
+            codeB[t] = ok[t] ? __ldg(expB + (size_t)n * nchunk + c) : 0;
+          }
+          if (readold && (!direct || Cd)) {
+            const double* src = direct ? Cd + row : work + (size_t)z * N * M + row;
+            const size_t ld = direct ? ldc : (size_t)M;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) old[t] = ok[t] ? src[(size_t)(n0 + cb + t) * ld] : 0.0;
+          } else if (readold) {
+            float of[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) of[t] = ok[t] ? C[row + (size_t)(n0 + cb + t) * ldc] : 0.f;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) old[t] = (double)of[t];
+          } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) old[t] = 0.0;
+          }
+        };
+        int codeN[8];
+        double oldN[8];
+        fetch(0, codeN, oldN);   // the first batch's loads overlap the chunk's MMAs
         mbar_wait(smem_u32(done), gc & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int codeA = row < M ? expA[(size_t)row * nchunk + c] : 0;
         const int ea = dec_exp(codeA);
-        for (int cb = 0; cb < ntile; cb += 16) {
-          uint32_t r[I_S][16];
+        for (int cb = 0; cb < ntile; cb += 8) {
+          int codeB[8];
+          double old[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            codeB[t] = codeN[t];
+            old[t] = oldN[t];
+          }
+          if (cb + 8 < ntile) fetch(cb + 8, codeN, oldN);
+          uint32_t r[I_S][8];
           const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
 #pragma unroll
-          for (int L = 0; L < I_S; ++L) tmem_ld16(taddr + (uint32_t)L * acc_stride, r[L]);
+          for (int L = 0; L < I_S; ++L) tmem_ld8(taddr + (uint32_t)L * acc_stride, r[L]);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           if (row < M) {
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
+            for (int t = 0; t < 8; ++t) {
               const int n = n0 + cb + t;
               if (cb + t < ntile && n < N) {
                 // V = sum_L acc_L 2^{7(I_S-1-L)} exactly in int64 (|V| < 2^{31 + 7(I_S-1) + 1} <= 2^60),
@@ -294,21 +340,15 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 long long V = (int)r[0][t];
 #pragma unroll
                 for (int L = 1; L < I_S; ++L) V = (V << 7) + (long long)(int)r[L][t];
-                const int codeB = expB[(size_t)n * nchunk + c];
-                const int ex2 = ea + dec_exp(codeB) - 7 * (I_S + 1);
+                const int ex2 = ea + dec_exp(codeB[t]) - 7 * (I_S + 1);
                 double v = (double)V * __longlong_as_double((long long)(ex2 + 1023) << 52);
-                if (codeA == kExpNaN || codeB == kExpNaN) v = __longlong_as_double(0x7ff8000000000000ll);
+                if (codeA == kExpNaN || codeB[t] == kExpNaN) v = __longlong_as_double(0x7ff8000000000000ll);
                 if (direct) {
-                  if (Cd) {
-                    double* p = Cd + row + (size_t)n * ldc;
-                    *p = beta != 0.0 ? alpha * v + beta * *p : alpha * v;
-                  } else {
-                    float* p = C + row + (size_t)n * ldc;
-                    *p = (float)(beta != 0.0 ? alpha * v + beta * (double)*p : alpha * v);
-                  }
+                  const double o = beta != 0.0 ? alpha * v + beta * old[t] : alpha * v;
+                  if (Cd) Cd[row + (size_t)n * ldc] = o;
+                  else C[row + (size_t)n * ldc] = (float)o;
                 } else {
-                  double* p = work + ((size_t)z * N + n) * M + row;
-                  *p = lc == 0 ? v : *p + v;
+                  work[((size_t)z * N + n) * M + row] = lc == 0 ? v : old[t] + v;
                 }
               }
             }

@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--policies", default="cg,random,coord")
     ap.add_argument("--iters", default="16,32,64,128,256")
     ap.add_argument("--ranks", default="128,256,512,1024")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     args = ap.parse_args()
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
@@ -47,15 +48,15 @@ def main():
         for policy in args.policies.split(","):
             for iters in (int(x) for x in args.iters.split(",")):
                 for rank in (int(x) for x in args.ranks.split(",")):
-                    rec = {"workload": "cfg3", "policy": policy, "max_iter": iters, "max_rank": rank, "dtype": "f32"}
+                    rec = {"workload": "cfg3", "policy": policy, "max_iter": iters, "max_rank": rank, "dtype": args.dtype}
                     try:
                         wl = make_workload("cfg3", policy=policy, max_iter=iters, max_rank=rank)
                         if policy == "coord":
                             o = farthest_point_order(wl.coords[wl.obs_idx[0]], iters)
                             wl.coord_order = [o.copy() for _ in range(wl.T)]
                         trans, _ = runner.transitions(wl)
-                        h = runner.make_handle(wl, "f32", stream=stream.cuda_stream)
-                        inputs = runner.stage_inputs(wl, "f32")
+                        h = runner.make_handle(wl, args.dtype, stream=stream.cuda_stream)
+                        inputs = runner.stage_inputs(wl, args.dtype)
                         runner.run(h, trans, inputs)
                         torch.cuda.synchronize()
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
