@@ -21,8 +21,8 @@
 // Operands enter as K-major int8 planes [I_S][rows][Kp] (i8_planes_kernel, which also transposes
 // when the source is M-major).  Persistent CTAs (one per SM) over 128 x ntile (<= 96) output tiles;
 // warp 0 = TMA loader, warp 1 = MMA issuer (one elected lane, 2 x 15 MMAs per 64-deep K block),
-// warps 2-5 = epilogue (tcgen05.ld 32x32b, lane quarter = warp % 4), which drains TMEM after each
-// K chunk while the loader already streams the next one.
+// warps 2-9 = epilogue (tcgen05.ld 32x32b, lane quarter = warp % 4, two warps per quarter splitting the
+// columns), which drains TMEM after each K chunk while the loader already streams the next one.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -43,7 +43,8 @@ constexpr int I_S = 5;                        // 7-bit slices per operand (35 bi
 constexpr int I_KC = 8192;                    // K elements per exact int32 chunk (and per work item)
 constexpr int I_KBC = I_KC / I_BK;            // K blocks per chunk
 constexpr int I_MAXN = 96;                    // I_S accumulators of <= 96 columns in 512 TMEM columns
-constexpr int I_THREADS = 192;                // loader, MMA, 4 epilogue warps
+constexpr int I_EPI_WARPS = 8;               // two per TMEM lane quarter, each draining half the columns
+constexpr int I_THREADS = 64 + 32 * I_EPI_WARPS;   // loader, MMA, epilogue warps
 constexpr int I_APLANE = I_BM * I_BK;         // 8 KB
 constexpr int I_SMEM_BUDGET = 220 * 1024;
 static_assert((long long)I_S * 127 * 127 * I_KC < (1ll << 31), "int32 accumulators must stay exact");
@@ -183,7 +184,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(done), 1);
-    mbar_init(smem_u32(tfree), 4);
+    mbar_init(smem_u32(tfree), I_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -260,8 +261,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else {
-    // ===== epilogue (warps 2-5): one output row per thread, 8 columns per TMEM load
+    // ===== epilogue (warps 2-9): one output row per thread, 8 columns per TMEM load
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;   // warps 2-5: columns [0, ntile/2), warps 6-9: [ntile/2, ntile)
     const bool direct = work == nullptr;
     int gc = 0;
     for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
@@ -269,6 +271,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (!i8_item(w, ntiles, mt, ntile, lower, m0, n0, z)) continue;
       const int c0 = z * cps, c1 = min(nchunk, c0 + cps);
       const int row = m0 + quarter * 32 + lane;
+      const int cb0 = half * (ntile >> 1), cb1 = cb0 + (ntile >> 1);   // this warp's columns (ntile % 16 == 0)
       for (int c = c0; c < c1; ++c, ++gc) {
         const int lc = c - c0;
         // while the MMAs of this chunk run: pull the tile's old C (or split partial) lines into L2 so the
@@ -279,7 +282,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                              : Cd      ? reinterpret_cast<const char*>(Cd + row)
                                        : reinterpret_cast<const char*>(C + row);
           const size_t ldb = (direct ? ldc : (size_t)M) * esz;
-          for (int t = 0; t < ntile && n0 + t < N; ++t)
+          for (int t = cb0; t < cb1 && n0 + t < N; ++t)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)(n0 + t) * ldb));
         }
         const bool readold = direct ? beta != 0.0 : lc != 0;
@@ -311,12 +314,12 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         };
         int codeN[8];
         double oldN[8];
-        fetch(0, codeN, oldN);   // the first batch's loads overlap the chunk's MMAs
+        fetch(cb0, codeN, oldN);   // the first batch's loads overlap the chunk's MMAs
         mbar_wait(smem_u32(done), gc & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int codeA = row < M ? expA[(size_t)row * nchunk + c] : 0;
         const int ea = dec_exp(codeA);
-        for (int cb = 0; cb < ntile; cb += 8) {
+        for (int cb = cb0; cb < cb1; cb += 8) {
           int codeB[8];
           double old[8];
 #pragma unroll
@@ -324,7 +327,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             codeB[t] = codeN[t];
             old[t] = oldN[t];
           }
-          if (cb + 8 < ntile) fetch(cb + 8, codeN, oldN);
+          if (cb + 8 < cb1) fetch(cb + 8, codeN, oldN);
           uint32_t r[I_S][8];
           const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
 #pragma unroll

@@ -65,6 +65,9 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
@@ -242,6 +245,167 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
 }
 
+// Persistent variant for the un-split case (the truncation's M~ = F Q_r: D x r x c): one CTA per SM walks the
+// 128 x ntile (<= 128) output tiles (n fastest, so the CTAs sharing an A tile run together); the two TMEM
+// accumulators of a tile (2 x 128 columns) are double-buffered, so the epilogue of tile i overlaps the MMAs
+// of tile i + 1 and the loader streams straight across tile boundaries.
+constexpr int G_PN = 128;   // max ntile of the persistent kernel
+__global__ void __launch_bounds__(G_THREADS, 1)
+gemm_tc_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                       int nkb, int ntile, int ntiles, int nwork, int stages, float alpha, float beta,
+                       float* __restrict__ C, size_t ldc) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char* sbase = smem_raw + (base - raw);
+  const uint32_t b_plane = (uint32_t)ntile * G_BK * 2;
+  const uint32_t stage_bytes = ((3u * G_APLANE + 3u * b_plane) + 1023u) & ~1023u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sbase + stages * stage_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* done = empty + stages;   // [2] MMA -> epilogue, per accumulator buffer
+  uint64_t* tfree = done + 2;        // [2] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfree + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t acc_cols = G_PN;   // per accumulator; buffer b: big at 2b*128, small at (2b+1)*128
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&done[b]), 1);
+      mbar_init(smem_u32(&tfree[b]), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sm0 = smem_u32(sbase);
+
+  if (warp == 0) {
+    if (lane == 0) {   // ===== TMA loader: every K block of every tile of this CTA, in order
+      const uint32_t bytes = 3u * (uint32_t)G_APLANE + 3u * b_plane;
+      int it = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const int m0 = (w / ntiles) * G_BM, n0 = (w % ntiles) * ntile;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % stages;
+          if (it >= stages) mbar_wait(smem_u32(&empty[s]), ((it / stages) - 1) & 1);
+          const uint32_t bar = smem_u32(&full[s]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+          const uint32_t st0 = sm0 + s * stage_bytes;
+#pragma unroll
+          for (int pl = 0; pl < 3; ++pl) tma3(st0 + pl * G_APLANE, &tmA, kb * G_BK, m0, pl, bar);
+#pragma unroll
+          for (int pl = 0; pl < 3; ++pl) tma3(st0 + 3 * G_APLANE + pl * b_plane, &tmB, kb * G_BK, n0, pl, bar);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {   // ===== MMA issuer
+    const uint32_t idesc = idesc_bf16(G_BM, ntile);
+    int it = 0, i = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++i) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait(smem_u32(&tfree[b]), ((i >> 1) - 1) & 1);   // buffer b drained (tile i - 2)
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dbig = tmem + (uint32_t)(2 * b) * acc_cols, dsmall = dbig + acc_cols;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % stages;
+        mbar_wait(smem_u32(&full[s]), (it / stages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t a0 = sm0 + s * stage_bytes, b0 = a0 + 3 * G_APLANE;
+#pragma unroll
+          for (int j = 0; j < G_BK / 16; ++j) {
+            const uint64_t A1 = sdesc_sw64(a0 + 32 * j), A2 = sdesc_sw64(a0 + G_APLANE + 32 * j),
+                           A3 = sdesc_sw64(a0 + 2 * G_APLANE + 32 * j);
+            const uint64_t B1 = sdesc_sw64(b0 + 32 * j), B2 = sdesc_sw64(b0 + b_plane + 32 * j),
+                           B3 = sdesc_sw64(b0 + 2 * b_plane + 32 * j);
+            const uint32_t first = (kb | j) ? 1u : 0u;
+            mma_bf16(dbig, A1, B1, idesc, first);
+            mma_bf16(dsmall, A1, B2, idesc, first);
+            mma_bf16(dsmall, A2, B1, idesc, 1u);
+            mma_bf16(dsmall, A2, B2, idesc, 1u);
+            mma_bf16(dsmall, A1, B3, idesc, 1u);
+            mma_bf16(dsmall, A3, B1, idesc, 1u);
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&empty[s]))
+                       : "memory");
+          if (kb == nkb - 1)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&done[b]))
+                         : "memory");
+        }
+        __syncwarp();
+      }
+    }
+  } else {   // ===== epilogue (warps 2-5): D_big + D_small of tile i from buffer i & 1
+    const int quarter = warp & 3;
+    int i = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int m0 = (w / ntiles) * G_BM, n0 = (w % ntiles) * ntile;
+      const int row = m0 + quarter * 32 + lane;
+      mbar_wait(smem_u32(&done[b]), (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int cb = 0; cb < ntile; cb += 16) {
+        float old[16];
+        if (beta != 0.f) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int n = n0 + cb + t;
+            old[t] = (row < M && cb + t < ntile && n < N) ? C[row + (size_t)n * ldc] : 0.f;
+          }
+        }
+        uint32_t r[16], q[16];
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(2 * b) * acc_cols + (uint32_t)cb;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];"
+            : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
+              "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
+            : "r"(taddr + acc_cols));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int n = n0 + cb + t;
+            if (cb + t < ntile && n < N) {
+              const float v = nkb > 0 ? __uint_as_float(r[t]) + __uint_as_float(q[t]) : 0.f;
+              C[row + (size_t)n * ldc] = beta != 0.f ? fmaf(alpha, v, beta * old[t]) : alpha * v;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&tfree[b]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
 // planes[p][r][k] (r < R, k < Kp, zero for k >= K) from src element (r, k) at
 // KC ? src[k + r ld] (K contiguous) : src[r + k ld] (R contiguous; transposed through smem)
 template <bool KC>
@@ -356,6 +520,28 @@ cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, in
   }
   const bool reduce = Cd != nullptr || S > 1;
   if (reduce && (size_t)S * M * N > work_floats) return cudaErrorInvalidValue;
+  if (!reduce && nkb > 0 && use_tc_persist()) {   // tall output (the truncation's F Q_r): persistent kernel
+    const int pnt = (N + G_PN - 1) / G_PN;
+    int pn = (N + pnt - 1) / pnt;
+    pn = std::max(16, (pn + 15) / 16 * 16);
+    const uint32_t pstage = ((3u * G_APLANE + 3u * (uint32_t)pn * G_BK * 2) + 1023u) & ~1023u;
+    const int pstages = std::max(2, std::min(8, (int)((G_SMEM_BUDGET - 1024 - 256) / pstage)));
+    const size_t psmem = (size_t)pstages * pstage + 1024 + 256;
+    static PerDeviceOnce once_p;
+    {
+      const cudaError_t e = once_per_device(once_p, [] {
+        return cudaFuncSetAttribute(gemm_tc_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    G_SMEM_BUDGET);
+      });
+      if (e != cudaSuccess) return e;
+    }
+    CUtensorMap pA, pB;
+    if (!make_plane_map(&pA, Ap, M, Kp, G_BM) || !make_plane_map(&pB, Bp, N, Kp, pn)) return cudaErrorInvalidValue;
+    const int nwork = mt * pnt;
+    gemm_tc_persist_kernel<<<std::min(nwork, sm_count()), G_THREADS, psmem, st>>>(
+        pA, pB, M, N, nkb, pn, pnt, nwork, pstages, (float)alpha, (float)beta, C, ldc);
+    return note_launch_err();
+  }
   CUtensorMap tmA, tmB;
   if (!make_plane_map(&tmA, Ap, M, Kp, G_BM) || !make_plane_map(&tmB, Bp, N, Kp, ntile)) return cudaErrorInvalidValue;
   dim3 grid(mt, ntiles, S);
@@ -367,6 +553,11 @@ cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, in
   if (Cd) splitk_reduce_kernel<double><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, S, work, alpha, beta, Cd, ldc);
   else splitk_reduce_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, S, work, alpha, beta, C, ldc);
   return note_launch_err();
+}
+
+bool use_tc_persist() {
+  static const bool v = !env_is("CAKF_TC_PERSIST", '0');
+  return v;
 }
 
 bool use_tc_gemm() {

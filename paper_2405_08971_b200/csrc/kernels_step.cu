@@ -444,22 +444,43 @@ __global__ void mix_kernel(int NX, int Dp, int C, Mat3 A, int transpose, const T
 
 // fp32, 16-byte aligned columns: 4 points per thread (float4 loads / stores, Dp loads in flight of 16 B
 // instead of 4 B), the same per-element fp64 arithmetic as mix_kernel
-__global__ void mix4_kernel(int NX4, int Dp, int C, Mat3 A, int transpose, const float4* __restrict__ in, size_t ldi4,
-                            float4* __restrict__ out, size_t ldo4) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;   // grid (point quads, columns)
-  if (q >= NX4) return;
-  float4 x[3];
-  for (int t = 0; t < Dp; ++t) x[t] = in[q + (size_t)t * NX4 + (size_t)j * ldi4];
-  for (int dd = 0; dd < Dp; ++dd) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int t = 0; t < Dp; ++t) {
-      const double c = transpose ? A.a[t][dd] : A.a[dd][t];
-      a0 += c * (double)x[t].x;
-      a1 += c * (double)x[t].y;
-      a2 += c * (double)x[t].z;
-      a3 += c * (double)x[t].w;
+// float4 version: each thread owns kMixQ point quads (strided by the block, so every load instruction is
+// coalesced) of one column; all DP x kMixQ loads are issued before the first use (HBM-bound: bytes in flight)
+constexpr int kMixQ = 4;
+template <int DP>
+__global__ void __launch_bounds__(256) mix4_kernel(int NX4, int C, Mat3 A, int transpose, const float4* __restrict__ in,
+                                                   size_t ldi4, float4* __restrict__ out, size_t ldo4) {
+  const int j = blockIdx.y;   // grid (point quads / (256 kMixQ), columns)
+  const int q0 = blockIdx.x * blockDim.x * kMixQ + threadIdx.x;
+  double c[DP][DP];
+#pragma unroll
+  for (int dd = 0; dd < DP; ++dd)
+#pragma unroll
+    for (int t = 0; t < DP; ++t) c[dd][t] = transpose ? A.a[t][dd] : A.a[dd][t];
+  float4 x[kMixQ][DP];
+#pragma unroll
+  for (int u = 0; u < kMixQ; ++u) {
+    const int q = q0 + u * blockDim.x;
+#pragma unroll
+    for (int t = 0; t < DP; ++t)
+      x[u][t] = q < NX4 ? in[q + (size_t)t * NX4 + (size_t)j * ldi4] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < kMixQ; ++u) {
+    const int q = q0 + u * blockDim.x;
+    if (q >= NX4) continue;
+#pragma unroll
+    for (int dd = 0; dd < DP; ++dd) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+      for (int t = 0; t < DP; ++t) {
+        a0 += c[dd][t] * (double)x[u][t].x;
+        a1 += c[dd][t] * (double)x[u][t].y;
+        a2 += c[dd][t] * (double)x[u][t].z;
+        a3 += c[dd][t] * (double)x[u][t].w;
+      }
+      out[q + (size_t)dd * NX4 + (size_t)j * ldo4] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
     }
-    out[q + (size_t)dd * NX4 + (size_t)j * ldo4] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
   }
 }
 
@@ -946,9 +967,13 @@ cudaError_t StepKernels<T>::mix(int NX, int Dp, int C, const Mat3& A, bool trans
   if constexpr (sizeof(T) == 4) {
     if (NX % 4 == 0 && ldi % 4 == 0 && ldo % 4 == 0 && reinterpret_cast<uintptr_t>(in) % 16 == 0 &&
         reinterpret_cast<uintptr_t>(out) % 16 == 0) {
-      mix4_kernel<<<dim3(nblk(NX / 4), C), 256, 0, st>>>(NX / 4, Dp, C, A, transpose ? 1 : 0,
-                                                        reinterpret_cast<const float4*>(in), ldi / 4,
-                                                        reinterpret_cast<float4*>(out), ldo / 4);
+      const int nq = NX / 4;
+      const dim3 grid((unsigned)((nq + 256 * kMixQ - 1) / (256 * kMixQ)), (unsigned)C);
+      const float4* in4 = reinterpret_cast<const float4*>(in);
+      float4* out4 = reinterpret_cast<float4*>(out);
+      if (Dp == 1) mix4_kernel<1><<<grid, 256, 0, st>>>(nq, C, A, transpose ? 1 : 0, in4, ldi / 4, out4, ldo / 4);
+      else if (Dp == 2) mix4_kernel<2><<<grid, 256, 0, st>>>(nq, C, A, transpose ? 1 : 0, in4, ldi / 4, out4, ldo / 4);
+      else mix4_kernel<3><<<grid, 256, 0, st>>>(nq, C, A, transpose ? 1 : 0, in4, ldi / 4, out4, ldo / 4);
       return note_launch_err();
     }
   }

@@ -1,0 +1,50 @@
+"""The truncation's M~ = F Q_r (Sec. 3.2) on the persistent, double-buffered 3xBF16 kernel
+(kernels_gemm_tc.cu gemm_tc_persist_kernel) must equal the one-tile-per-CTA kernel bit for bit: same K-block
+order and the same two TMEM accumulators per tile, only the schedule differs.  cfg3-sized D (1808 row tiles,
+so every CTA cycles both accumulator buffers several times), truncation at every step; the switch
+CAKF_TC_PERSIST is read once per process, so each variant runs in its own interpreter."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2405_08971_b200 import CAKF_FILTER, CAKF_SMOOTH, runner
+from synth import make_workload
+wl = make_workload("cfg3", T=3, max_iter=16, max_rank=24)
+trans, _ = runner.transitions(wl)
+h = runner.make_handle(wl, "f32")
+runner.run(h, trans, runner.stage_inputs(wl, "f32"), smooth=True)
+h.sync()
+out = []
+for which in (CAKF_FILTER, CAKF_SMOOTH):
+    for k in range(wl.T + 1):
+        m, v = h.get(k, which)
+        out += [m, v]
+np.save(sys.argv[1], np.stack(out))
+""" % ROOT
+
+
+@pytest.fixture(autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_persistent_tc_gemm_bit_identical(tmp_path):
+    res = {}
+    for flag in ("0", "1"):
+        path = tmp_path / f"out{flag}.npy"
+        env = dict(os.environ, CAKF_TC_PERSIST=flag)
+        subprocess.run([sys.executable, "-c", SCRIPT, str(path)], check=True, env=env, timeout=600)
+        res[flag] = np.load(path)
+    assert np.all(np.isfinite(res["1"]))
+    assert np.array_equal(res["0"], res["1"])
