@@ -467,6 +467,66 @@ __global__ void i8_planes_kernel(const Src* __restrict__ src, int R, int K, int 
   }
 }
 
+// One pass for the K-contiguous case: block (chunk c, row r) holds the chunk's <= I_KC values in registers,
+// reduces their max to the chunk exponent (written, no atomics: the block owns the chunk) and writes the
+// slices — the source is read once instead of twice (i8_exps_kc_kernel + i8_planes_kernel<KC>).  Same
+// exponent code and the same slicing arithmetic, so the planes are bit-identical to the two-pass path.
+constexpr int I_SPLIT_T = 256;
+constexpr int I_SPLIT_G = I_KC / (4 * I_SPLIT_T);   // groups of 4 consecutive k per thread (8)
+template <typename Src>
+__global__ void __launch_bounds__(I_SPLIT_T) i8_split_kc_kernel(const Src* __restrict__ src, int K, int Kp, size_t ld,
+                                                                int nchunk, int* __restrict__ ex,
+                                                                int8_t* __restrict__ planes, size_t plane) {
+  __shared__ Src red[I_SPLIT_T / 32];
+  const int c = blockIdx.x, r = blockIdx.y;
+  const int k0 = c * I_KC, kend = min(Kp, k0 + I_KC);
+  const Src* row = src + (size_t)r * ld;
+  Src v[I_SPLIT_G][4];
+  Src m = Src(0);
+#pragma unroll
+  for (int g = 0; g < I_SPLIT_G; ++g) {
+    const int k = k0 + 4 * (g * I_SPLIT_T + threadIdx.x);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[g][j] = k + j < K && k + j < kend ? row[k + j] : Src(0);
+  }
+#pragma unroll
+  for (int g = 0; g < I_SPLIT_G; ++g)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m = fmax(m, nonfinite_abs(v[g][j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < I_SPLIT_T / 32; ++w) m = fmax(m, red[w]);
+  const int code = enc_exp(m);
+  if (threadIdx.x == 0) ex[(size_t)r * nchunk + c] = code;
+  const int e = dec_exp(code);
+#pragma unroll
+  for (int g = 0; g < I_SPLIT_G; ++g) {
+    const int k = k0 + 4 * (g * I_SPLIT_T + threadIdx.x);
+    if (k >= kend) continue;
+    uint32_t word[I_S] = {};
+    if (code != kExpNaN) {   // non-finite chunk: zero slices, the epilogue writes NaN
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // |t| < 1; each step t*128 and t - trunc(t) is exact in the source precision
+        Src t = (Src)ldexp((double)v[g][j], -e);
+#pragma unroll
+        for (int s_ = 0; s_ < I_S; ++s_) {
+          t *= Src(128);
+          const Src a = trunc(t);
+          word[s_] |= ((uint32_t)(int)a & 0xFFu) << (8 * j);
+          t -= a;
+        }
+      }
+    }
+    const size_t o = (size_t)r * Kp + k;
+#pragma unroll
+    for (int s_ = 0; s_ < I_S; ++s_) *reinterpret_cast<uint32_t*>(planes + s_ * plane + o) = word[s_];
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
     void* p = nullptr;
@@ -502,6 +562,11 @@ cudaError_t gemm_i8_split(const Src* src, int R, int K, size_t ld, bool k_contig
                           cudaStream_t st) {
   if (R <= 0 || K <= 0) return cudaSuccess;
   const int Kp = gemm_i8_kp(K), nchunk = gemm_i8_nchunk(K);
+  if (k_contig && use_i8_split_fused()) {   // one pass: chunk exponents and slices
+    i8_split_kc_kernel<Src><<<dim3(nchunk, R), I_SPLIT_T, 0, st>>>(src, K, Kp, ld, nchunk, ex, planes,
+                                                                    (size_t)R * Kp);
+    return note_launch_err();
+  }
   cudaError_t e = cudaMemsetAsync(ex, 0, (size_t)R * nchunk * sizeof(int), st);
   if (e != cudaSuccess) return e;
   if (k_contig) i8_exps_kc_kernel<Src><<<dim3(R, (K + 2047) / 2048), 256, 0, st>>>(src, R, K, ld, nchunk, ex);
@@ -565,6 +630,11 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
     i8_reduce_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, splits, lower ? 1 : 0, work, alpha,
                                                                             beta, C, ldc);
   return note_launch_err();
+}
+
+bool use_i8_split_fused() {
+  static const bool v = !env_is("CAKF_I8_SPLIT_FUSED", '0');
+  return v;
 }
 
 bool use_i8_gemm() {

@@ -82,3 +82,37 @@ def test_lowrank_gemm_gram_cancellation(dev):
     D, c = 231360, 40
     F = (rng.standard_normal((D, c)) * np.logspace(0, -6, c)).astype(np.float32)
     _check(F, F, True, False, 1.0, 0.0, None, dev, 1e-8)
+
+
+def test_fused_split_bit_identical(tmp_path):
+    """The one-pass exponent + slice kernel (i8_split_kc_kernel) produces the same planes as the two-pass
+    path (CAKF_I8_SPLIT_FUSED=0), so every product is bit-identical: several chunks, a partial last chunk,
+    K not a multiple of 16, zero rows, a NaN chunk and both operand orientations."""
+    import os
+    import subprocess
+    import sys
+    script = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2405_08971_b200 import binding
+rng = np.random.default_rng(21)
+outs = []
+for (m, n, k, ta, tb) in [(300, 70, 20003, True, False), (129, 65, 8191, False, True), (64, 513, 9000, True, True)]:
+    A = rng.standard_normal((k, m) if ta else (m, k)).astype(np.float32)
+    B = rng.standard_normal((n, k) if tb else (k, n)).astype(np.float32)
+    if ta: A[:, 3] = 0.0
+    else: A[3] = 0.0
+    if tb: B[1, 5] = np.nan
+    else: B[5, 1] = np.nan
+    C = binding.lowrank_gemm(torch.tensor(A, device="cuda"), torch.tensor(B, device="cuda"), transa=ta, transb=tb)
+    outs.append(C.cpu().numpy().ravel())
+np.save(sys.argv[1], np.concatenate(outs))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        path = tmp_path / f"o{flag}.npy"
+        subprocess.run([sys.executable, "-c", script, str(path)], check=True, timeout=600,
+                       env=dict(os.environ, CAKF_I8_SPLIT_FUSED=flag))
+        res[flag] = np.load(path)
+    assert np.array_equal(res["0"], res["1"], equal_nan=True)
+    assert np.isnan(res["1"]).any() and np.isfinite(res["1"]).any()
