@@ -527,6 +527,74 @@ __global__ void __launch_bounds__(I_SPLIT_T) i8_split_kc_kernel(const Src* __res
   }
 }
 
+// One pass for the rows-contiguous case with a single K chunk (K <= kRcMaxK: the M-major factor of
+// M^- U / M^- (M^-T x)): block = 32 rows, the whole [K][32] tile staged in shared memory with coalesced
+// row loads, the per-row maximum -> exponent, then the slices from shared memory.  Same codes and slicing
+// arithmetic as i8_exps_rc_kernel + i8_planes_kernel<RC>.
+constexpr int kRcMaxK = 1024;
+template <typename Src>
+constexpr int rc_max_k() { return sizeof(Src) == 4 ? kRcMaxK : kRcMaxK / 2; }
+template <typename Src>
+__global__ void __launch_bounds__(256) i8_split_rc_kernel(const Src* __restrict__ src, int R, int K, int Kp, size_t ld,
+                                                          int* __restrict__ ex, int8_t* __restrict__ planes,
+                                                          size_t plane) {
+  extern __shared__ __align__(16) unsigned char rc_raw[];
+  Src* tile = reinterpret_cast<Src*>(rc_raw);   // [Kp][33]
+  __shared__ Src red[8][32];
+  __shared__ int codes[32];
+  const int r0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  {
+    const int r = r0 + tx;
+    Src m = Src(0);
+#pragma unroll 8
+    for (int k = ty; k < Kp; k += 8) {
+      const Src v = (k < K && r < R) ? src[r + (size_t)k * ld] : Src(0);
+      tile[k * 33 + tx] = v;
+      m = fmax(m, nonfinite_abs(v));
+    }
+    red[ty][tx] = m;
+  }
+  __syncthreads();
+  if (ty == 0) {
+    Src m = red[0][tx];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) m = fmax(m, red[y][tx]);
+    const int code = enc_exp(m);
+    codes[tx] = code;
+    if (r0 + tx < R) ex[r0 + tx] = code;   // one chunk: ex[r * 1 + 0]
+  }
+  __syncthreads();
+  for (int kw = 0; kw < Kp; kw += 128) {
+    const int k = kw + 4 * tx;
+    if (k >= Kp) continue;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = ty + 8 * i, r = r0 + rl;
+      if (r >= R) continue;
+      const int code = codes[rl];
+      const int e = dec_exp(code);
+      uint32_t word[I_S] = {};
+      if (code != kExpNaN) {   // non-finite chunk: zero slices, the epilogue writes NaN
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          Src t = (Src)ldexp((double)tile[(k + j) * 33 + rl], -e);
+#pragma unroll
+          for (int s_ = 0; s_ < I_S; ++s_) {
+            t *= Src(128);
+            const Src a = trunc(t);
+            word[s_] |= ((uint32_t)(int)a & 0xFFu) << (8 * j);
+            t -= a;
+          }
+        }
+      }
+      const size_t o = (size_t)r * Kp + k;
+#pragma unroll
+      for (int s_ = 0; s_ < I_S; ++s_) *reinterpret_cast<uint32_t*>(planes + s_ * plane + o) = word[s_];
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
     void* p = nullptr;
@@ -565,6 +633,17 @@ cudaError_t gemm_i8_split(const Src* src, int R, int K, size_t ld, bool k_contig
   if (k_contig && use_i8_split_fused()) {   // one pass: chunk exponents and slices
     i8_split_kc_kernel<Src><<<dim3(nchunk, R), I_SPLIT_T, 0, st>>>(src, K, Kp, ld, nchunk, ex, planes,
                                                                     (size_t)R * Kp);
+    return note_launch_err();
+  }
+  if (!k_contig && Kp <= rc_max_k<Src>() && use_i8_split_fused()) {   // one pass: row exponents and slices
+    const size_t smem = (size_t)Kp * 33 * sizeof(Src);
+    static PerDeviceOnce once_rc;
+    const cudaError_t ce = once_per_device(once_rc, [] {
+      return cudaFuncSetAttribute(i8_split_rc_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)((size_t)rc_max_k<Src>() * 33 * sizeof(Src)));
+    });
+    if (ce != cudaSuccess) return ce;
+    i8_split_rc_kernel<Src><<<(R + 31) / 32, 256, smem, st>>>(src, R, K, Kp, ld, ex, planes, (size_t)R * Kp);
     return note_launch_err();
   }
   cudaError_t e = cudaMemsetAsync(ex, 0, (size_t)R * nchunk * sizeof(int), st);

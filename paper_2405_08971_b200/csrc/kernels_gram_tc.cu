@@ -12,7 +12,7 @@
 // take 6 bytes per element instead of 8.
 //
 // Per CTA: a 128-row x N_TILE (<= 256) output tile in TMEM.  Per K-block of 32:
-//   * warp-specialised: 8 producer warps evaluate the 128 x 32 Matérn block (FP32 pipe +
+//   * warp-specialised: 16 producer warps evaluate the 128 x 32 Matérn block (FP32 pipe +
 //     MUFU), split it and store the three planes in the K-major SWIZZLE_64B canonical layout;
 //     a 9th warp issues the MMAs; the two sides meet only at full / empty mbarriers;
 //   * a loader warp brings the three B planes (precomputed, K-major) and the block's column
@@ -40,10 +40,14 @@ namespace {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;                        // 32 bf16 = one 64-byte swizzle atom row
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 512;                  // producer warps (16): 4 column groups of 8 per tile row
+constexpr int TC_NG = TC_THREADS / 128;          // column groups per 32-column K-block
+constexpr int TC_KPT = 32 / TC_NG;               // columns (points) generated per producer thread and block
+constexpr int TC_MMA_WARP = TC_THREADS / 32, TC_LOAD_WARP = TC_MMA_WARP + 1;
+static_assert(TC_KPT % 8 == 0, "each producer thread writes whole 16-byte chunks of the swizzled rows");
 constexpr int TC_MAXN = 208;
-constexpr int A_STAGES = 2;                      // generated operand ring
-constexpr int B_STAGES = 4;                      // TMA operand ring (loads run 3 blocks ahead)
+constexpr int A_STAGES = 3;                      // generated operand ring
+constexpr int B_STAGES = 3;                      // TMA operand ring (loads run 2 blocks ahead)
 constexpr int TC_STAGES = B_STAGES;
 constexpr int A_PLANE = TC_BM * TC_BK * 2;       // 8 KB
 constexpr int B_PLANE = TC_MAXN * TC_BK * 2;     // 13 KB (multiple of the 512 B SW64 atom)
@@ -168,7 +172,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
   const int nk = act_cnt ? act_cnt[blockIdx.x] : (K + TC_BK - 1) / TC_BK;
   const int* my_list = act_cnt ? act_list + (size_t)blockIdx.x * act_stride : nullptr;
 
-  if (warp == 8) {
+  if (warp == TC_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(tmem_cols)
                  : "memory");
@@ -193,7 +197,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
   auto a_addr = [&](int s) { return smem_u32(a_base + s * A_STAGE_BYTES); };
   auto b_addr = [&](int s) { return smem_u32(b_base + s * B_STAGE_BYTES); };
 
-  if (warp == 8) {
+  if (warp == TC_MMA_WARP) {
     // ===== MMA issuer: one elected lane, back-to-back over the stage ring
     const uint32_t idesc = F16 ? idesc_f16(TC_BM, ntile) : idesc_bf16(TC_BM, ntile);
     for (int kb = 0; kb < nk; ++kb) {
@@ -232,7 +236,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
       }
       __syncwarp();
     }
-  } else if (warp == 9) {
+  } else if (warp == TC_LOAD_WARP) {
     // ===== TMA loader: the three B planes (64B-swizzled boxes, zero-filled beyond C / K) and the
     // block's 32 column coordinates, up to TC_STAGES blocks ahead of the MMAs
     if (lane == 0) {
@@ -261,8 +265,9 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
     }
     __syncwarp();
   } else {
-    // ===== producers (warps 0-7): A generation from the staged column coordinates
-    const int arow = tid & (TC_BM - 1), khalf = tid >> 7;
+    // ===== producers (warps 0-15): A generation from the staged column coordinates; thread = (tile row,
+    // group of TC_KPT consecutive columns of the K-block)
+    const int arow = tid & (TC_BM - 1), kq = tid >> 7;
     float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
     if (m0 + arow < M) xa = xr[m0 + arow];
     for (int kb = 0; kb < nk; ++kb) {
@@ -270,15 +275,15 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
       mbar_wait(smem_u32(&fullB[sb]), (kb / B_STAGES) & 1);                       // coords(kb) landed
       if (kb >= A_STAGES) mbar_wait(smem_u32(&emptyA[sa]), ((kb / A_STAGES) - 1) & 1);   // MMA(kb - 2) done
       const uint32_t a0 = a_addr(sa);
-      const float4* sxc = reinterpret_cast<const float4*>(b_base + sb * B_STAGE_BYTES + 3 * B_PLANE) + 16 * khalf;
-      uint32_t p1[8], p2[8], p3[8];   // bf16x2 packed
+      const float4* sxc = reinterpret_cast<const float4*>(b_base + sb * B_STAGE_BYTES + 3 * B_PLANE) + TC_KPT * kq;
+      uint32_t p1[TC_KPT / 2], p2[TC_KPT / 2], p3[TC_KPT / 2];   // bf16x2 packed
       if (!F16 && !diag_nogen) {
         // two columns per step on the packed f32x2 FMA-pipe ops (MUFU sqrt / ex2 stay scalar), then the
         // exact truncation split of both values at once: h1 = top 16 bits, r1 = v - h1, h2 = top of r1,
         // r2 = r1 - h2 (both subtractions exact); each plane's bf16x2 word is one byte permute of the
         // two values' high halves — the same planes as split3 + pack, in about half the instructions
 #pragma unroll
-        for (int q = 0; q < 16; q += 2) {
+        for (int q = 0; q < TC_KPT; q += 2) {
           const float4 c0 = sxc[q], c1 = sxc[q + 1];   // {x, x', y, y'}, {z, z', w, w'} of points k, k+1
           const float2 dx = __fadd2_rn(make_float2(c0.x, c0.y), make_float2(-xa.x, -xa.x));
           const float2 dy = __fadd2_rn(make_float2(c0.z, c0.w), make_float2(-xa.y, -xa.y));
@@ -296,7 +301,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
         }
       } else {
 #pragma unroll
-      for (int q = 0; q < 16; q += 2) {
+      for (int q = 0; q < TC_KPT; q += 2) {
         float kv[2];
         const float4 cA = sxc[q], cB = sxc[q + 1];   // pair-packed {x, x', y, y'}, {z, z', w, w'}
 #pragma unroll
@@ -320,8 +325,8 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
       }
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t off = sw64_off(arow, 2 * khalf + h);
+      for (int h = 0; h < TC_KPT / 8; ++h) {
+        const uint32_t off = sw64_off(arow, (TC_KPT / 8) * kq + h);
         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0 + off), "r"(p1[4 * h]), "r"(p1[4 * h + 1]),
                      "r"(p1[4 * h + 2]), "r"(p1[4 * h + 3])
                      : "memory");
@@ -341,9 +346,10 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int quarter = warp & 3;
     const int row = m0 + quarter * 32 + lane;
-    const int half_cols = ((ntile / 2) + 15) / 16 * 16;
-    const int c_begin = (warp >> 2) * half_cols;
-    const int c_end = (warp >> 2) ? ntile : half_cols;
+    // epilogue by the producer warps: lane quarter = warp % 4, the columns split into TC_NG parts
+    const int part_cols = ((ntile + TC_NG - 1) / TC_NG + 15) / 16 * 16;
+    const int c_begin = min(ntile, (warp >> 2) * part_cols);
+    const int c_end = min(ntile, c_begin + part_cols);
     for (int cb = c_begin; cb < c_end; cb += 16) {
       uint32_t r[16], q[16];
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
@@ -372,7 +378,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 8) {
+  if (warp == TC_MMA_WARP) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
   }
 }

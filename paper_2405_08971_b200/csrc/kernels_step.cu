@@ -19,7 +19,6 @@ namespace cakf {
 
 namespace {
 
-constexpr int kThreads = 256;
 // stage kernels: one 128-row tile per block, one row per thread (row-wise ops), 4 warps splitting the
 // columns of the column dots; per-block partial rows reduced in two deterministic levels
 constexpr int kTile = 128;
@@ -645,6 +644,45 @@ __global__ void ws_dense_kernel(size_t D, int n, int q, const T* __restrict__ X,
   else if (j <= n) Wf[p + (size_t)(j - 1) * D] = T(0);
   else Wf[p + (size_t)(j - 1) * D] = X[p + (size_t)(j - n) * D];
 }
+// float4 forms of ws_dense / kcar_build (D and N_X multiples of 4, 16-byte aligned buffers): the same values,
+// one 16-byte access per thread (these are pure streaming passes over D x (1 + n + q))
+__global__ void ws_dense4_kernel(size_t D4, int n, const float4* __restrict__ X, float4* __restrict__ Wf,
+                                 float4* __restrict__ ws) {
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (p >= D4) return;
+  if (j == 0) ws[p] = X[p];
+  else if (j <= n) Wf[p + (size_t)(j - 1) * D4] = make_float4(0.f, 0.f, 0.f, 0.f);
+  else Wf[p + (size_t)(j - 1) * D4] = X[p + (size_t)(j - n) * D4];
+}
+__device__ __forceinline__ float4 f4sub(float4 a, float4 b) {
+  return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+}
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__global__ void kcar_build4_kernel(size_t NX4, size_t D4, int n, int q, const float4* __restrict__ KV,
+                                   const float4* __restrict__ Z, const float4* __restrict__ Kx,
+                                   float4* __restrict__ KWf, float4* __restrict__ Kws) {
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (p >= D4) return;
+  const bool b0 = p < NX4;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j == 0) {
+    float4 v = Kx ? Kx[p] : zero;
+    if (b0 && n) v = f4add(v, Z ? f4sub(KV[p], Z[p]) : KV[p]);
+    Kws[p] = v;
+  } else if (j <= n) {
+    KWf[p + (size_t)(j - 1) * D4] = b0 ? KV[p + (size_t)j * NX4] : zero;
+  } else {
+    const int c = j - n;
+    float4 v = Kx[p + (size_t)c * D4];
+    if (b0 && n && Z) v = f4sub(v, Z[p + (size_t)c * NX4]);
+    KWf[p + (size_t)(j - 1) * D4] = v;
+  }
+}
+
 // kernel-applied carriers: (I (x) K) of ws_dense + ws_scatter, from K(X,T)[v V] and K(X,T) V t (block 0 only,
 // H = [E_train, 0]); grid (rows of D, 1 + n + q columns)
 template <typename T>
@@ -1049,6 +1087,15 @@ cudaError_t StepKernels<T>::kcar_build(int64_t NX, int Dp, int n, int q, const T
   const size_t D = (size_t)NX * Dp;
   if (D == 0) return cudaSuccess;
   if (n && !Z && (Kx || q)) return cudaErrorInvalidValue;
+  if constexpr (sizeof(T) == 4) {
+    auto al = [](const void* x) { return reinterpret_cast<uintptr_t>(x) % 16 == 0; };
+    if (NX % 4 == 0 && al(KV) && al(Z) && al(Kx) && al(KWf) && al(Kws)) {
+      kcar_build4_kernel<<<dim3(nblk(D / 4), 1 + n + q), 256, 0, st>>>(
+          (size_t)NX / 4, D / 4, n, q, reinterpret_cast<const float4*>(KV), reinterpret_cast<const float4*>(Z),
+          reinterpret_cast<const float4*>(Kx), reinterpret_cast<float4*>(KWf), reinterpret_cast<float4*>(Kws));
+      return note_launch_err();
+    }
+  }
   kcar_build_kernel<T><<<dim3(nblk(D), 1 + n + q), 256, 0, st>>>((size_t)NX, D, n, q, KV, Z, Kx, KWf, Kws);
   return note_launch_err();
 }
@@ -1056,7 +1103,16 @@ cudaError_t StepKernels<T>::kcar_build(int64_t NX, int Dp, int n, int q, const T
 template <typename T>
 cudaError_t StepKernels<T>::ws_build(int N, size_t D, int n, int q, const int* idx, const T* X, const T* XV,
                                      const T* R, T* Wf, T* ws, int lo, int nl, cudaStream_t st) {
-  ws_dense_kernel<T><<<dim3(nblk(D), n + q + 1), 256, 0, st>>>(D, n, q, X, Wf, ws);
+  bool vec = false;
+  if constexpr (sizeof(T) == 4) {
+    auto al = [](const void* x) { return reinterpret_cast<uintptr_t>(x) % 16 == 0; };
+    vec = D % 4 == 0 && al(X) && al(Wf) && al(ws);
+    if (vec)
+      ws_dense4_kernel<<<dim3(nblk(D / 4), n + q + 1), 256, 0, st>>>(D / 4, n, reinterpret_cast<const float4*>(X),
+                                                                     reinterpret_cast<float4*>(Wf),
+                                                                     reinterpret_cast<float4*>(ws));
+  }
+  if (!vec) ws_dense_kernel<T><<<dim3(nblk(D), n + q + 1), 256, 0, st>>>(D, n, q, X, Wf, ws);
   cudaError_t e = note_launch_err();
   if (e != cudaSuccess || N == 0) return e;
   ws_scatter_kernel<T><<<nblk((size_t)N * (n + q + 1)), 256, 0, st>>>(N, D, n, q, idx, XV, R, Wf, ws, lo, nl);

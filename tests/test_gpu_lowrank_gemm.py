@@ -85,9 +85,10 @@ def test_lowrank_gemm_gram_cancellation(dev):
 
 
 def test_fused_split_bit_identical(tmp_path):
-    """The one-pass exponent + slice kernel (i8_split_kc_kernel) produces the same planes as the two-pass
-    path (CAKF_I8_SPLIT_FUSED=0), so every product is bit-identical: several chunks, a partial last chunk,
-    K not a multiple of 16, zero rows, a NaN chunk and both operand orientations."""
+    """The one-pass exponent + slice kernels (i8_split_kc_kernel, and i8_split_rc_kernel for a rows-contiguous
+    operand with K <= 1024) produce the same planes as the two-pass path (CAKF_I8_SPLIT_FUSED=0), so every
+    product is bit-identical: several chunks, a partial last chunk, K not a multiple of 16, zero rows, a NaN
+    chunk, both operand orientations, and the RC fallback beyond K = 1024."""
     import os
     import subprocess
     import sys
@@ -97,7 +98,8 @@ sys.path.insert(0, %r)
 from paper_2405_08971_b200 import binding
 rng = np.random.default_rng(21)
 outs = []
-for (m, n, k, ta, tb) in [(300, 70, 20003, True, False), (129, 65, 8191, False, True), (64, 513, 9000, True, True)]:
+for (m, n, k, ta, tb) in [(300, 70, 20003, True, False), (129, 65, 8191, False, True), (64, 513, 9000, True, True),
+                          (1000, 65, 512, True, False), (300, 129, 1000, True, False), (200, 40, 1500, True, False)]:
     A = rng.standard_normal((k, m) if ta else (m, k)).astype(np.float32)
     B = rng.standard_normal((n, k) if tb else (k, n)).astype(np.float32)
     if ta: A[:, 3] = 0.0
