@@ -200,6 +200,94 @@ __global__ void __launch_bounds__(kFThreads) gemm_f64acc_strip_kernel(int m, int
   }
 }
 
+// Row-strip variant for fp32 B and C (the fp32 path's K = N^ products): 8 warps (2 x 4 of 32 x 16) per
+// 64 x 64 C tile, the A strip converted to fp64 once per CTA, the B tile and the old C tile of the NEXT
+// column tile streamed into shared memory with cp.async (fp32, double-buffered) while the DMMAs of the
+// current one run — no register prefetch, ~100 registers, two CTAs (16 warps) per SM.
+constexpr int kS2Threads = 256, kS2Pad = 68;   // fp32 row stride of the staged B / C tiles (16-byte rows)
+constexpr size_t kS2Smem = (size_t)kStripK * (kFT + 1) * sizeof(double) + 4 * (size_t)kFT * kS2Pad * sizeof(float);
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+template <typename TA>
+__global__ void __launch_bounds__(kS2Threads, 2) gemm_f64acc_strip2_kernel(int m, int n, int k, double alpha,
+                                                                             const TA* __restrict__ A, size_t lda,
+                                                                             const float* __restrict__ B, size_t ldb,
+                                                                             double beta, float* __restrict__ C,
+                                                                             size_t ldc) {
+  extern __shared__ __align__(16) double s2_smem[];
+  double(*As)[kFT + 1] = reinterpret_cast<double(*)[kFT + 1]>(s2_smem);   // [k][row]
+  float* Bsf = reinterpret_cast<float*>(s2_smem + kStripK * (kFT + 1));   // [2][col][k]
+  float* Csf = Bsf + 2 * kFT * kS2Pad;                                     // [2][col][row]
+  const int i0 = blockIdx.x * kFT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int kp = (k + 3) & ~3;
+  const bool readc = beta != 0.0;
+  // stage column tile j0 (B: 64 columns x k, C: 64 columns x 64 rows) into buffer b; 16-byte chunks, zero fill
+  auto stage = [&](int j0, int b) {
+    for (int x = threadIdx.x; x < kFT * 16; x += kS2Threads) {
+      const int cc = x >> 4, l0 = (x & 15) * 4, col = j0 + cc;
+      const int nb = (col < n && l0 < k) ? 4 * min(4, k - l0) : 0;
+      const float* src = B + (nb ? (size_t)col * ldb + l0 : 0);
+      cp_async16_zfill((uint32_t)__cvta_generic_to_shared(Bsf + (size_t)b * kFT * kS2Pad + cc * kS2Pad + l0), src, nb);
+      if (readc) {
+        const int nc = (col < n && i0 + l0 < m) ? 4 * min(4, m - i0 - l0) : 0;
+        const float* srcc = C + (nc ? (size_t)col * ldc + i0 + l0 : 0);
+        cp_async16_zfill((uint32_t)__cvta_generic_to_shared(Csf + (size_t)b * kFT * kS2Pad + cc * kS2Pad + l0), srcc,
+                         nc);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage(0, 0);
+  for (int x = threadIdx.x; x < kStripK * kFT; x += kS2Threads) {
+    const int r = x % kFT, l = x / kFT;
+    As[l][r] = (l < k && i0 + r < m) ? (double)A[(i0 + r) + (size_t)l * lda] : 0.0;
+  }
+  const int ntl = (n + kFT - 1) / kFT;
+  for (int jt = 0; jt < ntl; ++jt) {
+    const int j0 = jt * kFT, b = jt & 1;
+    if (jt + 1 < ntl) {
+      stage(j0 + kFT, b ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const float* Bt = Bsf + (size_t)b * kFT * kS2Pad;
+    double acc[4][2][2] = {};
+    for (int ks = 0; ks < kp; ks += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = As[ks + t][wm + 8 * mi + g];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) bf[ni] = (double)Bt[(wn + 8 * ni + g) * kS2Pad + ks + t];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    }
+    const float* Ct = Csf + (size_t)b * kFT * kS2Pad;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int rl = wm + 8 * mi + g, i = i0 + rl;
+      if (i >= m) continue;
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cl = wn + 8 * ni + 2 * t + h, j = j0 + cl;
+          if (j >= n) continue;
+          const double v = acc[mi][ni][h];
+          C[i + (size_t)j * ldc] = (float)(readc ? alpha * v + beta * (double)Ct[cl * kS2Pad + rl] : alpha * v);
+        }
+    }
+    __syncthreads();   // buffer b is restaged at tile jt + 2
+  }
+}
+
 template <typename TC>
 __global__ void gemm_f64acc_reduce_kernel(int m, int n, int S, const double* __restrict__ part, double alpha,
                                           double beta, TC* __restrict__ C, size_t ldc) {
@@ -239,11 +327,31 @@ cudaError_t launch_t(int m, int n, int k, double alpha, const TA* A, size_t lda,
 
 }  // namespace
 
+bool use_strip2() {
+  static const bool v = !env_is("CAKF_STRIP2", '0');
+  return v;
+}
+
 template <typename TA, typename TB, typename TC>
 cudaError_t gemm_f64acc(bool transa, bool transb, int m, int n, int k, double alpha, const TA* A, size_t lda,
                         const TB* B, size_t ldb, double beta, TC* C, size_t ldc, double* work, size_t work_doubles,
                         cudaStream_t st) {
   if (m <= 0 || n <= 0) return cudaSuccess;
+  if constexpr (sizeof(TB) == 4 && sizeof(TC) == 4) {
+    auto al16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+    if (!transa && !transb && k > 0 && k <= kStripK && m >= 8 * kFT && ldb % 4 == 0 && ldc % 4 == 0 && al16(B) &&
+        al16(C) && use_strip2()) {
+      static PerDeviceOnce once2;
+      const cudaError_t ce = once_per_device(once2, [] {
+        return cudaFuncSetAttribute(gemm_f64acc_strip2_kernel<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kS2Smem);
+      });
+      if (ce != cudaSuccess) return ce;
+      gemm_f64acc_strip2_kernel<TA><<<(m + kFT - 1) / kFT, kS2Threads, kS2Smem, st>>>(
+          m, n, k, alpha, A, lda, reinterpret_cast<const float*>(B), ldb, beta, reinterpret_cast<float*>(C), ldc);
+      return note_launch_err();
+    }
+  }
   if (!transa && !transb && k > 0 && k <= kStripK && sizeof(TC) == 4 && m >= 8 * kFT) {
     constexpr size_t smem = 2 * kStripK * (kFT + 1) * sizeof(double);
     static PerDeviceOnce once;

@@ -12,7 +12,7 @@
 // take 6 bytes per element instead of 8.
 //
 // Per CTA: a 128-row x N_TILE (<= 256) output tile in TMEM.  Per K-block of 32:
-//   * warp-specialised: 16 producer warps evaluate the 128 x 32 Matérn block (FP32 pipe +
+//   * warp-specialised: 8 producer warps evaluate the 128 x 32 Matérn block (FP32 pipe +
 //     MUFU), split it and store the three planes in the K-major SWIZZLE_64B canonical layout;
 //     a 9th warp issues the MMAs; the two sides meet only at full / empty mbarriers;
 //   * a loader warp brings the three B planes (precomputed, K-major) and the block's column
@@ -40,7 +40,7 @@ namespace {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;                        // 32 bf16 = one 64-byte swizzle atom row
-constexpr int TC_THREADS = 512;                  // producer warps (16): 4 column groups of 8 per tile row
+constexpr int TC_THREADS = 256;                  // producer warps (8): 2 column groups of 16 per tile row
 constexpr int TC_NG = TC_THREADS / 128;          // column groups per 32-column K-block
 constexpr int TC_KPT = 32 / TC_NG;               // columns (points) generated per producer thread and block
 constexpr int TC_MMA_WARP = TC_THREADS / 32, TC_LOAD_WARP = TC_MMA_WARP + 1;
@@ -180,7 +180,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
   }
   if (tid == 0) {
     for (int s = 0; s < A_STAGES; ++s) {
-      mbar_init(smem_u32(&fullA[s]), TC_THREADS);
+      mbar_init(smem_u32(&fullA[s]), TC_THREADS / 32);   // one arrive per producer warp
       mbar_init(smem_u32(&emptyA[s]), 1);
     }
     for (int s = 0; s < B_STAGES; ++s) {
@@ -265,7 +265,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
     }
     __syncwarp();
   } else {
-    // ===== producers (warps 0-15): A generation from the staged column coordinates; thread = (tile row,
+    // ===== producers (warps 0-7): A generation from the staged column coordinates; thread = (tile row,
     // group of TC_KPT consecutive columns of the K-block)
     const int arow = tid & (TC_BM - 1), kq = tid >> 7;
     float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -339,7 +339,8 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
                        : "memory");
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> tensor core
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fullA[sa])) : "memory");
+      __syncwarp();   // every lane's writes (each fenced) before lane 0's release: one arrive per warp
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fullA[sa])) : "memory");
     }
     // ===== epilogue: D = D_big + D_small (fp32 round-to-nearest)
     if (nk > 0) mbar_wait(smem_u32(done), 0);

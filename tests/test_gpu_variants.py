@@ -1,8 +1,11 @@
-"""The truncation's M~ = F Q_r (Sec. 3.2) on the persistent, double-buffered 3xBF16 kernel
-(kernels_gemm_tc.cu gemm_tc_persist_kernel) must equal the one-tile-per-CTA kernel bit for bit: same K-block
-order and the same two TMEM accumulators per tile, only the schedule differs.  cfg3-sized D (1808 row tiles,
-so every CTA cycles both accumulator buffers several times), truncation at every step; the switch
-CAKF_TC_PERSIST is read once per process, so each variant runs in its own interpreter."""
+"""Kernel variants that change only the schedule must agree bit for bit with the kernels they replace, on a
+cfg3-sized run (D = 231,360; truncation at every step; K = 16 smoother products):
+  * CAKF_TC_PERSIST: the truncation's M~ = F Q_r (Sec. 3.2) on the persistent, double-buffered
+    3xBF16 kernel vs one tile per CTA (same K-block order, same two TMEM accumulators per tile; 1808 row
+    tiles, so every CTA cycles both accumulator buffers several times);
+  * CAKF_STRIP2: the alg:mfks K = N^ products (B_k t, V t, (K(X,T)V) t) on the cp.async strip
+    kernel vs the register-prefetch strip kernel (same DMMA sequence per output).
+The switches are read once per process, so each variant runs in its own interpreter."""
 import os
 import subprocess
 import sys
@@ -39,11 +42,12 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-def test_persistent_tc_gemm_bit_identical(tmp_path):
+@pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2"])
+def test_variant_bit_identical(tmp_path, switch):
     res = {}
     for flag in ("0", "1"):
         path = tmp_path / f"out{flag}.npy"
-        env = dict(os.environ, CAKF_TC_PERSIST=flag)
+        env = dict(os.environ, **{switch: flag})
         subprocess.run([sys.executable, "-c", SCRIPT, str(path)], check=True, env=env, timeout=600)
         res[flag] = np.load(path)
     assert np.all(np.isfinite(res["1"]))
