@@ -384,7 +384,10 @@ def main():
     kw = {} if args.T is None else {"T": args.T}
     wl = make_workload(args.config, **kw)
     trans, _ = runner.transitions(wl)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream, made current: the library then runs on it (a null stream would make the
+    # library create its own, which the events below would not bracket: they would time the host enqueue)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     nccl_id = None
     if world > 1:
         obj = [binding.nccl_unique_id() if rank == 0 else None]

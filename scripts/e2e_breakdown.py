@@ -9,7 +9,8 @@ from synth import make_workload
 
 wl = make_workload("cfg3")
 trans, _ = runner.transitions(wl)
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
 h = runner.make_handle(wl, "f32", stream=stream.cuda_stream)
 dev_in = runner.stage_inputs(wl, "f32")
 host_in = []

@@ -43,7 +43,8 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()   # non-default: the handle runs on it and the events bracket its work
+    torch.cuda.set_stream(stream)
     with open(args.out, "a") as fo:
         for policy in args.policies.split(","):
             for iters in (int(x) for x in args.iters.split(",")):
