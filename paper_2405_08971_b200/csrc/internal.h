@@ -82,6 +82,8 @@ cudaError_t gemm_tc_split(const float* src, int R, int K, size_t ld, bool k_cont
 cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, int K, double alpha, double beta,
                         float* C, double* Cd, size_t ldc, float* work, size_t work_floats, cudaStream_t st);
 bool use_tc_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM instead
+bool use_k2_stack();   // CAKF_K2_STACK=0: six 3xBF16 MMAs per k-step in K2 instead of three stacked ones
+bool use_i8_stack();   // CAKF_I8_STACK=0: one MMA per slice pair, single accumulator buffer (A/B only)
 bool use_i8_split_fused();   // CAKF_I8_SPLIT_FUSED=0: the two-pass exponent + slice kernels (A/B only)
 bool use_tc_persist();   // CAKF_TC_PERSIST=0: un-split 3xBF16 GEMMs on the one-tile-per-CTA kernel (A/B only)
 constexpr size_t kGemmWorkFloats = (size_t)32 << 20;

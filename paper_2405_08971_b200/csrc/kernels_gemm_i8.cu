@@ -43,6 +43,7 @@ constexpr int I_S = 5;                        // 7-bit slices per operand (35 bi
 constexpr int I_KC = 8192;                    // K elements per exact int32 chunk (and per work item)
 constexpr int I_KBC = I_KC / I_BK;            // K blocks per chunk
 constexpr int I_MAXN = 96;                    // I_S accumulators of <= 96 columns in 512 TMEM columns
+constexpr int I_STACK_MAXN = 48;              // stacked, one chunk: I_S levels x 48 <= 256 columns, two buffers
 constexpr int I_EPI_WARPS = 8;               // two per TMEM lane quarter, each draining half the columns
 constexpr int I_THREADS = 64 + 32 * I_EPI_WARPS;   // loader, MMA, epilogue warps
 constexpr int I_APLANE = I_BM * I_BK;         // 8 KB
@@ -155,8 +156,8 @@ __device__ __forceinline__ bool i8_item(int w, int ntiles, int mt, int ntile, in
 __global__ void __launch_bounds__(I_THREADS, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const int* __restrict__ expA, const int* __restrict__ expB, int M, int N, int nkb, int nchunk, int cps,
-               int ntile, int ntiles, int mt, int nwork, int stages, int lower, double alpha, double beta,
-               float* __restrict__ C, double* __restrict__ Cd, size_t ldc, double* __restrict__ work) {
+               int ntile, int ntiles, int mt, int nwork, int stages, int lower, int stack, double alpha,
+               double beta, float* __restrict__ C, double* __restrict__ Cd, size_t ldc, double* __restrict__ work) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -165,12 +166,18 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const uint32_t stage_bytes = ((uint32_t)I_S * I_APLANE + (uint32_t)I_S * b_plane + 1023u) & ~1023u;
   uint64_t* full = reinterpret_cast<uint64_t*>(sbase + stages * stage_bytes);
   uint64_t* empty = full + stages;
-  uint64_t* done = empty + stages;    // MMA -> epilogue: chunk accumulated
-  uint64_t* tfree = done + 1;         // epilogue -> MMA: TMEM drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfree + 1);
+  uint64_t* done = empty + stages;    // [2] MMA -> epilogue: chunk accumulated (per accumulator buffer)
+  uint64_t* tfree = done + 2;         // [2] epilogue -> MMA: TMEM buffer drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfree + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t acc_stride = (uint32_t)((ntile + 31) / 32 * 32);
+  // stack: the B slices sit contiguously in shared memory, so one MMA A_s x [B_0 | ... | B_{4-s}] (N = (5-s)
+  // ntile) at TMEM column offset s ntile lands every product A_s B_t on level s + t's columns: 5 MMAs per
+  // 32-deep k-step instead of 15 (each A slice read once), levels ntile columns apart, and with ntile <= 48
+  // the 5 levels fit in 256 columns: two accumulator buffers, so the drain of chunk g overlaps the MMAs of
+  // chunk g + 1.  Otherwise: one accumulator per level (32-column aligned), one buffer.
+  const uint32_t acc_stride = stack ? (uint32_t)ntile : (uint32_t)((ntile + 31) / 32 * 32);
+  const int nbuf = (stack && I_S * ntile <= 256) ? 2 : 1;   // stacked ntile <= 48: two buffers; <= 96: one
 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -183,8 +190,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
-    mbar_init(smem_u32(done), 1);
-    mbar_init(smem_u32(tfree), I_EPI_WARPS);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&done[b]), 1);
+      mbar_init(smem_u32(&tfree[b]), I_EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -225,8 +234,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (!i8_item(w, ntiles, mt, ntile, lower, m0, n0, z)) continue;
       const int c0 = z * cps, c1 = min(nchunk, c0 + cps);
       for (int c = c0; c < c1; ++c, ++gc) {
-        if (gc > 0) mbar_wait(smem_u32(tfree), (gc - 1) & 1);   // epilogue drained the previous chunk
+        const int b = gc % nbuf;
+        if (gc >= nbuf) mbar_wait(smem_u32(&tfree[b]), ((gc / nbuf) - 1) & 1);   // buffer b drained
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tb = tmem + (uint32_t)b * 256u;
         const int kbe = min(nkb, (c + 1) * I_KBC);
         for (int kb = c * I_KBC; kb < kbe; ++kb, ++it) {
           const int s = it % stages;
@@ -237,14 +248,27 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const bool first_kb = kb == c * I_KBC;
 #pragma unroll
             for (int j = 0; j < I_BK / 32; ++j) {
+              if (stack) {   // N per MMA <= 256: B rows [off, off + 256) start off * 64 bytes in (8-row aligned)
 #pragma unroll
-              for (int L = 0; L < I_S; ++L) {
+                for (int sa = 0; sa < I_S; ++sa) {
+                  const int ntot = (I_S - sa) * ntile;
+                  for (int off = 0; off < ntot; off += 256) {
+                    const uint32_t acc = (first_kb && j == 0 && sa == 0) ? 0u : 1u;
+                    mma_s8(tb + (uint32_t)(sa * ntile + off), sdesc_sw64(a0 + sa * I_APLANE + 32 * j),
+                           sdesc_sw64(b0 + (uint32_t)off * I_BK + 32 * j), idesc_s8(I_BM, min(256, ntot - off)),
+                           acc);
+                  }
+                }
+              } else {
 #pragma unroll
-                for (int sa = 0; sa <= L; ++sa) {
-                  const int sb = L - sa;
-                  const uint32_t acc = (first_kb && j == 0 && sa == 0) ? 0u : 1u;
-                  mma_s8(tmem + (uint32_t)L * acc_stride, sdesc_sw64(a0 + sa * I_APLANE + 32 * j),
-                         sdesc_sw64(b0 + sb * b_plane + 32 * j), idesc, acc);
+                for (int L = 0; L < I_S; ++L) {
+#pragma unroll
+                  for (int sa = 0; sa <= L; ++sa) {
+                    const int sb = L - sa;
+                    const uint32_t acc = (first_kb && j == 0 && sa == 0) ? 0u : 1u;
+                    mma_s8(tb + (uint32_t)L * acc_stride, sdesc_sw64(a0 + sa * I_APLANE + 32 * j),
+                           sdesc_sw64(b0 + sb * b_plane + 32 * j), idesc, acc);
+                  }
                 }
               }
             }
@@ -253,7 +277,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                          : "memory");
             if (kb == kbe - 1)
               asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                               smem_u32(done))
+                               smem_u32(&done[b]))
                            : "memory");
           }
           __syncwarp();
@@ -315,7 +339,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int codeN[8];
         double oldN[8];
         fetch(cb0, codeN, oldN);   // the first batch's loads overlap the chunk's MMAs
-        mbar_wait(smem_u32(done), gc & 1);
+        const int b = gc % nbuf;
+        mbar_wait(smem_u32(&done[b]), (gc / nbuf) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int codeA = row < M ? expA[(size_t)row * nchunk + c] : 0;
         const int ea = dec_exp(codeA);
@@ -329,7 +354,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
           if (cb + 8 < cb1) fetch(cb + 8, codeN, oldN);
           uint32_t r[I_S][8];
-          const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
+          const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * 256u + (uint32_t)cb;
 #pragma unroll
           for (int L = 0; L < I_S; ++L) tmem_ld8(taddr + (uint32_t)L * acc_stride, r[L]);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -359,7 +384,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(tfree));
+        if (lane == 0) mbar_arrive(smem_u32(&tfree[b]));
       }
     }
   }
@@ -668,7 +693,11 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
   if (K <= 0) return cudaErrorInvalidValue;
   const int Kp = gemm_i8_kp(K), nchunk = gemm_i8_nchunk(K);
   const int nkb = (Kp + I_BK - 1) / I_BK;
-  const int ntiles = (N + I_MAXN - 1) / I_MAXN;
+  // stacked-B MMAs: one K chunk (the tall M-major products) -> ntile <= 48 with double-buffered accumulators
+  // (the drain overlaps the next tile); several chunks (K = D) -> ntile <= 96, one buffer, fewer A re-reads
+  const bool stack = use_i8_stack();
+  const int maxn = stack && nchunk == 1 ? I_STACK_MAXN : I_MAXN;
+  const int ntiles = (N + maxn - 1) / maxn;
   int ntile = (N + ntiles - 1) / ntiles;
   ntile = std::max(16, (ntile + 15) / 16 * 16);
   const int mt = (M + I_BM - 1) / I_BM;
@@ -697,8 +726,8 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
   const int nwork = mt * ntiles * splits;
   const int grid = std::min(nwork, sm_count());
   gemm_i8_kernel<<<grid, I_THREADS, smem, st>>>(tmA, tmB, expA, expB, M, N, nkb, nchunk, cps, ntile, ntiles, mt,
-                                                nwork, stages, lower ? 1 : 0, alpha, beta, C, Cd, ldc,
-                                                reduce ? work : nullptr);
+                                                nwork, stages, lower ? 1 : 0, stack ? 1 : 0, alpha, beta, C, Cd,
+                                                ldc, reduce ? work : nullptr);
   cudaError_t e = note_launch_err();
   if (e != cudaSuccess || !reduce) return e;
   const size_t tot = (size_t)M * N;
@@ -709,6 +738,11 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
     i8_reduce_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, splits, lower ? 1 : 0, work, alpha,
                                                                             beta, C, ldc);
   return note_launch_err();
+}
+
+bool use_i8_stack() {
+  static const bool v = !env_is("CAKF_I8_STACK", '0');
+  return v;
 }
 
 bool use_i8_split_fused() {

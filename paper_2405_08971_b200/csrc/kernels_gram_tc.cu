@@ -146,7 +146,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
                     const __grid_constant__ CUtensorMap tmX, int K, int C, int ntile,
                     float* __restrict__ Y, size_t ldy, float alpha, int diag_nogen,
                     const int* __restrict__ act_cnt, const int* __restrict__ act_list, int act_stride,
-                    const float* __restrict__ colinv, int oneacc) {
+                    const float* __restrict__ colinv, int oneacc, int stack) {
   constexpr int NPL = F16 ? 2 : 3;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -166,8 +166,12 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
   // two accumulators: D_big = sum a1 b1 (the exact leading products) and D_small = the five
   // correction products; summed in fp32 round-to-nearest in the epilogue (tensor-core
   // accumulation truncates, so keeping the small terms apart cuts the biased error ~6x)
-  const uint32_t acc_cols = ntile <= 32 ? 32 : ntile <= 64 ? 64 : ntile <= 128 ? 128 : 256;
-  const uint32_t tmem_cols = 2 * acc_cols;
+  // stack (3 x BF16, 3 ntile <= 256): the three B planes sit contiguously, so A1 x [B1|B2|B3] (N = 3 ntile),
+  // A2 x [B1|B2] at column offset ntile and A3 x B1 at ntile give D_big = [0, ntile) and the five correction
+  // products in [ntile, 3 ntile): 3 MMAs per k-step instead of 6 (each A plane read once)
+  const uint32_t acc_cols = stack ? (uint32_t)ntile : ntile <= 32 ? 32 : ntile <= 64 ? 64 : ntile <= 128 ? 128 : 256;
+  const uint32_t tmem_cols = stack ? 256u : 2 * acc_cols;
+  const uint32_t b_pl = stack ? (uint32_t)ntile * 64u : (uint32_t)B_PLANE;   // B plane stride in a stage
   // exact-zero culling: only this tile's active K-blocks (ascending), else all of them
   const int nk = act_cnt ? act_cnt[blockIdx.x] : (K + TC_BK - 1) / TC_BK;
   const int* my_list = act_cnt ? act_list + (size_t)blockIdx.x * act_stride : nullptr;
@@ -211,16 +215,22 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
         for (int j = 0; j < TC_BK / 16; ++j) {
           const uint64_t A1 = sdesc_sw64(a0 + 32 * j), A2 = sdesc_sw64(a0 + A_PLANE + 32 * j),
                          A3 = sdesc_sw64(a0 + 2 * A_PLANE + 32 * j);
-          const uint64_t B1 = sdesc_sw64(bb + 32 * j), B2 = sdesc_sw64(bb + B_PLANE + 32 * j),
-                         B3 = sdesc_sw64(bb + 2 * B_PLANE + 32 * j);
+          const uint64_t B1 = sdesc_sw64(bb + 32 * j), B2 = sdesc_sw64(bb + b_pl + 32 * j),
+                         B3 = sdesc_sw64(bb + 2 * b_pl + 32 * j);
           const uint32_t first = (kb | j) ? 1u : 0u;
-          mma_bf16(tmem, A1, B1, idesc, first);
-          mma_bf16(tmem + (oneacc ? 0u : acc_cols), A1, B2, idesc, oneacc ? 1u : first);
-          mma_bf16(tmem + (oneacc ? 0u : acc_cols), A2, B1, idesc, 1u);
-          if (!F16) {
-            mma_bf16(tmem + acc_cols, A2, B2, idesc, 1u);
-            mma_bf16(tmem + acc_cols, A1, B3, idesc, 1u);
+          if (!F16 && stack) {
+            mma_bf16(tmem, A1, B1, idesc_bf16(TC_BM, 3 * ntile), first);
+            mma_bf16(tmem + acc_cols, A2, B1, idesc_bf16(TC_BM, 2 * ntile), 1u);
             mma_bf16(tmem + acc_cols, A3, B1, idesc, 1u);
+          } else {
+            mma_bf16(tmem, A1, B1, idesc, first);
+            mma_bf16(tmem + (oneacc ? 0u : acc_cols), A1, B2, idesc, oneacc ? 1u : first);
+            mma_bf16(tmem + (oneacc ? 0u : acc_cols), A2, B1, idesc, 1u);
+            if (!F16) {
+              mma_bf16(tmem + acc_cols, A2, B2, idesc, 1u);
+              mma_bf16(tmem + acc_cols, A1, B3, idesc, 1u);
+              mma_bf16(tmem + acc_cols, A3, B1, idesc, 1u);
+            }
           }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -252,7 +262,7 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
         for (int pl = 0; pl < NPL; ++pl) {
           asm volatile(
               "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-              "[%5];" ::"r"(b0 + pl * B_PLANE),
+              "[%5];" ::"r"(b0 + pl * b_pl),
               "l"(&tmB), "r"(k0), "r"(n0), "r"(pl), "r"(bar)
               : "memory");
         }
@@ -366,12 +376,23 @@ gram_gemm_tc_kernel(const float4* __restrict__ xr, int M, const __grid_constant_
           : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
             "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
           : "r"(taddr + acc_cols));
+      uint32_t q2[16];
+      if (stack) {   // the second correction block [2 ntile, 3 ntile)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];"
+            : "=r"(q2[0]), "=r"(q2[1]), "=r"(q2[2]), "=r"(q2[3]), "=r"(q2[4]), "=r"(q2[5]), "=r"(q2[6]),
+              "=r"(q2[7]), "=r"(q2[8]), "=r"(q2[9]), "=r"(q2[10]), "=r"(q2[11]), "=r"(q2[12]), "=r"(q2[13]),
+              "=r"(q2[14]), "=r"(q2[15])
+            : "r"(taddr + 2 * acc_cols));
+      }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (row < M) {
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
           const int n = n0 + cb + t;
-          const float v = __uint_as_float(r[t]) + (oneacc ? 0.f : __uint_as_float(q[t]));
+          const float small = stack ? __uint_as_float(q[t]) + __uint_as_float(q2[t]) : __uint_as_float(q[t]);
+          const float v = __uint_as_float(r[t]) + (oneacc ? 0.f : small);
           if (cb + t < c_end && n < C) Y[row + (size_t)n * ldy] = nk > 0 ? (F16 ? alpha * colinv[n] * v : alpha * v) : 0.f;
         }
       }
@@ -496,11 +517,11 @@ cudaError_t launch_tc_nu(const float4* xr, int M, const float4* xc, int K, const
   if (colinv)
     gram_gemm_tc_kernel<NU2, true><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha,
                                                                            nogen, act_cnt, act_list, act_stride, colinv,
-                                                                           oneacc);
+                                                                           oneacc, 0);
   else
-    gram_gemm_tc_kernel<NU2, false><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha,
-                                                                            nogen, act_cnt, act_list, act_stride, nullptr,
-                                                                            0);
+    gram_gemm_tc_kernel<NU2, false><<<grid, TC_THREADS + 64, TC_SMEM, st>>>(
+        xr, M, tmB, tmX, K, C, ntile, Y, ldy, alpha, nogen, act_cnt, act_list, act_stride, nullptr, 0,
+        (3 * ntile <= 256 && use_k2_stack()) ? 1 : 0);
   return note_launch_err();
 }
 
@@ -560,6 +581,11 @@ size_t gram_gemm_tc_workspace(int K, int C) {
   const size_t Kp = ((size_t)K + TC_BK - 1) / TC_BK * TC_BK;
   // planes, column scales, and the pair-packed column coordinates (K rounded up to even) + alignment
   return 3 * Kp * (size_t)C * sizeof(uint16_t) + 2 * (size_t)C * sizeof(float) + ((size_t)K + 2) * 16 + 2048;
+}
+
+bool use_k2_stack() {
+  static const bool v = !env_is("CAKF_K2_STACK", '0');
+  return v;
 }
 
 bool use_f16_k2() {

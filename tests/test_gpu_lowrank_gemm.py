@@ -84,11 +84,14 @@ def test_lowrank_gemm_gram_cancellation(dev):
     _check(F, F, True, False, 1.0, 0.0, None, dev, 1e-8)
 
 
-def test_fused_split_bit_identical(tmp_path):
-    """The one-pass exponent + slice kernels (i8_split_kc_kernel, and i8_split_rc_kernel for a rows-contiguous
-    operand with K <= 1024) produce the same planes as the two-pass path (CAKF_I8_SPLIT_FUSED=0), so every
-    product is bit-identical: several chunks, a partial last chunk, K not a multiple of 16, zero rows, a NaN
-    chunk, both operand orientations, and the RC fallback beyond K = 1024."""
+@pytest.mark.parametrize("switch", ["CAKF_I8_SPLIT_FUSED", "CAKF_I8_STACK"])
+def test_variant_bit_identical(tmp_path, switch):
+    """Schedule-only variants are bit-identical (the slice products are exact integers in any order):
+    CAKF_I8_SPLIT_FUSED — the one-pass exponent + slice kernels (i8_split_kc_kernel; i8_split_rc_kernel for a
+    rows-contiguous operand with K <= 1024) vs the two-pass path; CAKF_I8_STACK — stacked-B MMAs (5 per
+    k-step, levels 48 columns apart, two TMEM buffers) vs one MMA per slice pair.  Cases: several chunks, a
+    partial last chunk, K not a multiple of 16, zero rows, a NaN chunk, both orientations, the RC fallback
+    beyond K = 1024, N above and below one tile."""
     import os
     import subprocess
     import sys
@@ -114,7 +117,7 @@ np.save(sys.argv[1], np.concatenate(outs))
     for flag in ("0", "1"):
         path = tmp_path / f"o{flag}.npy"
         subprocess.run([sys.executable, "-c", script, str(path)], check=True, timeout=600,
-                       env=dict(os.environ, CAKF_I8_SPLIT_FUSED=flag))
+                       env=dict(os.environ, **{switch: flag}))
         res[flag] = np.load(path)
     assert np.array_equal(res["0"], res["1"], equal_nan=True)
     assert np.isnan(res["1"]).any() and np.isfinite(res["1"]).any()
