@@ -693,10 +693,17 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
   if (K <= 0) return cudaErrorInvalidValue;
   const int Kp = gemm_i8_kp(K), nchunk = gemm_i8_nchunk(K);
   const int nkb = (Kp + I_BK - 1) / I_BK;
-  // stacked-B MMAs: one K chunk (the tall M-major products) -> ntile <= 48 with double-buffered accumulators
-  // (the drain overlaps the next tile); several chunks (K = D) -> ntile <= 96, one buffer, fewer A re-reads
-  const bool stack = use_i8_stack();
-  const int maxn = stack && nchunk == 1 ? I_STACK_MAXN : I_MAXN;
+  // stacked-B MMAs for one K chunk (the tall M-major products, K <= 8192): ntile <= 48 with double-buffered
+  // accumulators, the drain overlapping the next tile (S2 2.16 -> 1.82 ms).  Several chunks (K = D, long MMA
+  // runs per drain) stay on one MMA per slice pair with ntile <= 96: stacking there measured slower (ntile 48:
+  // more A re-reads; ntile 96 with N split at 256: 1.43 -> 1.60 ms for M^-T x)
+  const bool stack = use_i8_stack() && nchunk == 1;
+  static const int stack_maxn = [] {   // CAKF_I8_STACK_MAXN=96: one buffer, half the A re-reads (A/B only)
+    const char* e = getenv("CAKF_I8_STACK_MAXN");
+    const int v = e ? std::atoi(e) : I_STACK_MAXN;
+    return v == 96 ? 96 : I_STACK_MAXN;
+  }();
+  const int maxn = stack ? stack_maxn : I_MAXN;
   const int ntiles = (N + maxn - 1) / maxn;
   int ntile = (N + ntiles - 1) / ntiles;
   ntile = std::max(16, (ntile + 15) / 16 * 16);
