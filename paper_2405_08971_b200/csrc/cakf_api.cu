@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <cfloat>
 #include <mutex>
 #include <cmath>
@@ -136,6 +137,12 @@ bool fetch_doubles(const double* src, size_t n, std::vector<double>& out) {
   std::memcpy(out.data(), src, n * sizeof(double));
   return true;
 }
+// CAKF_SMOOTH_OVERLAP=0: the smoother's carrier products run in line with the truncation (A/B only)
+bool smooth_overlap() {
+  static const bool v = !env_is("CAKF_SMOOTH_OVERLAP", '0');
+  return v;
+}
+
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes at{};
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -185,6 +192,11 @@ struct Impl final : ImplBase {
   // side stream: u = (HM^-)^T s (HBM-bound) overlaps K1 (MUFU-bound) in every inner iteration
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // smoother: the kernel-applied carriers (Zk GEMM + kcar_build) on the side stream beside the truncation's
+  // Gram / eig / first GEMM of the same step (they only feed its second GEMM); ev_kcar joins them
+  cudaEvent_t ev_ws = nullptr, ev_kcar = nullptr;
+  cudaEvent_t f2_wait = nullptr;   // consumed by truncate_factor*: wait before the second factor's GEMM
+  std::function<int()> after_gram;  // consumed by truncate_factor*: enqueued right after the Gram (side work)
   double* part2 = nullptr;
   double* hmw = nullptr;   // HM u (fp64 rows), formed on the side stream
   bool side = [] { const char* e = getenv("CAKF_NO_SIDE_STREAM"); return !(e && e[0] == '1'); }();
@@ -453,6 +465,8 @@ struct Impl final : ImplBase {
     if (st2) cudaStreamDestroy(st2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_ws) cudaEventDestroy(ev_ws);
+    if (ev_kcar) cudaEventDestroy(ev_kcar);
   }
 
   template <typename U>
@@ -699,6 +713,8 @@ struct Impl final : ImplBase {
       }
       CK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       CK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      CK_CUDA(cudaEventCreateWithFlags(&ev_ws, cudaEventDisableTiming));
+      CK_CUDA(cudaEventCreateWithFlags(&ev_kcar, cudaEventDisableTiming));
     }
     CK_CUDA(cudaMallocHost(&ctl_init_host, sizeof(IterCtl)));
     std::memset(ctl_init_host, 0, sizeof(IterCtl));
@@ -1211,6 +1227,11 @@ struct Impl final : ImplBase {
     }
     CK(allreduce(Gm, (size_t)c * c));   // row-sharded factor: the Gram is the sum of the ranks' partial Grams
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
+    if (after_gram) {   // side-stream work that only the second GEMM needs: it runs beside the eigensolver
+      std::function<int()> job;
+      job.swap(after_gram);
+      CK(job());
+    }
     ps = prof_begin();
     CK(eig(c, rkeep, kept, dropped, failflag));
     prof_end(CAKF_PROF_TRUNC_EIG, ps);
@@ -1218,6 +1239,8 @@ struct Impl final : ImplBase {
     if (i8 && i8_mqr) {   // M~ = F Q_r with the fp64 eigenvectors sliced directly
       CK(gemm_i8_f32(OP_N, OP_N, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, c, 0.0, out, nullptr,
                      (int)D, false, QrD));
+      if (F2 && f2_wait) CK_CUDA(cudaStreamWaitEvent(st, f2_wait, 0));
+      f2_wait = nullptr;
       if (F2)
         CK(gemm_i8_f32(OP_N, OP_N, (int)D, rkeep, c, 1.0, F2, (int)D, nullptr, c, 0.0, out2, nullptr,
                        (int)D, false, QrD));
@@ -1227,6 +1250,8 @@ struct Impl final : ImplBase {
       CK_CUDA(gemm_tc_split(Qf, rkeep, c, (size_t)c, true, gpB, st));           // Q_r columns
       CK_CUDA(gemm_tc_run(gpA, (int)D, gpB, rkeep, c, 1.0, 0.0, out, nullptr, (size_t)D, gwork, kGemmWorkFloats,
                           st));
+      if (F2 && f2_wait) CK_CUDA(cudaStreamWaitEvent(st, f2_wait, 0));
+      f2_wait = nullptr;
       if (F2) {   // same Q_r planes
         CK_CUDA(gemm_tc_split(F2, (int)D, c, (size_t)D, false, gpA, st));
         CK_CUDA(gemm_tc_run(gpA, (int)D, gpB, rkeep, c, 1.0, 0.0, out2, nullptr, (size_t)D, gwork, kGemmWorkFloats,
@@ -1254,11 +1279,18 @@ struct Impl final : ImplBase {
     CK(gram_fp64(F, c));
     CK(allreduce(Gm, (size_t)c * c));   // row-sharded factor: the Gram is the sum of the ranks' partial Grams
     prof_end(CAKF_PROF_TRUNC_GRAM, ps);
+    if (after_gram) {   // side-stream work that only the second GEMM needs: it runs beside the eigensolver
+      std::function<int()> job;
+      job.swap(after_gram);
+      CK(job());
+    }
     ps = prof_begin();
     CK(eig(c, rkeep, kept, dropped, failflag));
     prof_end(CAKF_PROF_TRUNC_EIG, ps);
     ps = prof_begin();
     CK(gemm_impl(false, false, (int)D, rkeep, c, 1.0, F, (int)D, nullptr, QrD, c, 0.0, out, (int)D));
+    if (F2 && f2_wait) CK_CUDA(cudaStreamWaitEvent(st, f2_wait, 0));
+    f2_wait = nullptr;
     if (F2) CK(gemm_impl(false, false, (int)D, rkeep, c, 1.0, F2, (int)D, nullptr, QrD, c, 0.0, out2, (int)D));
     prof_end(CAKF_PROF_TRUNC_GEMM, ps);
     prof_end(CAKF_PROF_TRUNCATE, pk);
@@ -1340,22 +1372,56 @@ struct Impl final : ImplBase {
       CK_CUDA(StepKernels<T>::smooth_out(D, C, S.m, S.var, yb, S.ms, S.vs, st));
       // w^s_k, W^s_k = [W_k, (I - W W^T P^-) A^T W^s]   (lines 7-8)
       CK_CUDA(StepKernels<T>::ws_build(n ? N : 0, D, n, q, S.idx, X, S.XV, R, Wf, ws, (int)plo, (int)NX, st));
+      bool kcar_side = false;
       if (!smooth_k2) {
-        // (I (x) K) W^s_full = [[K(X,T) V; 0], Kx[:,1:] - [K(X,T) V t[:,1:]; 0]], same for w^s with column 0
-        pk = prof_begin();
-        if (n) CK(gemm(OP_N, OP_N, (int)NX, C, n, 1.0, S.KV + NX, (int)NX, tt, n, 0.0, Zk, (int)NX));
-        prof_end(CAKF_PROF_LOWRANK, pk);
-        CK_CUDA(StepKernels<T>::kcar_build(NX, Dp, n, q, S.KV, n ? Zk : nullptr, Yk, KWf, Kws, st));
+        // (I (x) K) W^s_full = [[K(X,T) V; 0], Kx[:,1:] - [K(X,T) V t[:,1:]; 0]], same for w^s with column 0.
+        // fp32 with K = n <= 64 (the workspace-free strip GEMM): on the side stream, beside the truncation's
+        // Gram and eig (16 SMs) — they only feed its second GEMM and the next step (joined below)
+        const int qn_ = n + q;
+        kcar_side = sizeof(T) == 4 && side && st2 && n <= 64 && NX >= 512 && smooth_overlap() && rcap >= 0 &&
+                    qn_ > rcap;   // a truncation follows: fork after its Gram, beside the eigensolver
+        const T* KVk = S.KV;
+        auto carriers = [this, n, q, C, KVk](cudaStream_t on) -> int {
+          cudaStream_t main_st = st;
+          st = on;   // gemm() and prof_* use the member stream
+          size_t pk2 = prof_begin();
+          int rc = CAKF_OK;
+          if (n) rc = gemm(OP_N, OP_N, (int)NX, C, n, 1.0, KVk + NX, (int)NX, tt, n, 0.0, Zk, (int)NX);
+          prof_end(CAKF_PROF_LOWRANK, pk2);
+          st = main_st;
+          CK(rc);
+          CK_CUDA(StepKernels<T>::kcar_build(NX, Dp, n, q, KVk, n ? Zk : nullptr, Yk, KWf, Kws, on));
+          return CAKF_OK;
+        };
+        if (kcar_side) {
+          after_gram = [this, carriers]() -> int {
+            CK_CUDA(cudaEventRecord(ev_ws, st));
+            CK_CUDA(cudaStreamWaitEvent(st2, ev_ws, 0));
+            CK(carriers(st2));
+            CK_CUDA(cudaEventRecord(ev_kcar, st2));
+            f2_wait = ev_kcar;
+            return CAKF_OK;
+          };
+        } else {
+          CK(carriers(st));
+        }
       }
       const int qn = n + q;
       if (rcap >= 0 && qn > rcap) {                                   // line 9 (R6)
-        CK(truncate_factor(Wf, qn, rcap, Ws, nullptr, nullptr, &ctl[k].nonfinite, smooth_k2 ? nullptr : KWf, KWs));
+        const int trc = truncate_factor(Wf, qn, rcap, Ws, nullptr, nullptr, &ctl[k].nonfinite,
+                                        smooth_k2 ? nullptr : KWf, KWs);
+        after_gram = nullptr;   // (consumed inside unless the truncation failed early)
+        CK(trc);
         q = rcap;
       } else {
+        if (f2_wait) CK_CUDA(cudaStreamWaitEvent(st, f2_wait, 0));
+        f2_wait = nullptr;
         std::swap(Wf, Ws);
         if (!smooth_k2) std::swap(KWf, KWs);
         q = qn;
       }
+      if (kcar_side) CK_CUDA(cudaStreamWaitEvent(st, ev_kcar, 0));   // carriers complete before the next step
+      f2_wait = nullptr;
       S.smoother_rank = q;
       CK(keep_carriers(k, q));
     }

@@ -974,7 +974,8 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
   // ---- 1. tridiagonalisation (one cluster of nc CTAs: 16 where the device can co-schedule it, else 8)
   {
     static const int smem_max_c16 = trd_smem_max_c(16), smem_max_c8 = trd_smem_max_c(8);
-    const int nc = trd_cluster_size();
+    static const int nc_env = [] { const char* e = getenv("CAKF_TRD_NC"); return e ? std::atoi(e) : 0; }();
+    const int nc = nc_env == 8 ? 8 : trd_cluster_size();   // CAKF_TRD_NC=8: the 8-CTA cluster (A/B only)
     auto kern = nc == 16 ? (c <= smem_max_c16 ? sytrd_cluster_kernel<16, true> : sytrd_cluster_kernel<16, false>)
                          : (c <= smem_max_c8 ? sytrd_cluster_kernel<8, true> : sytrd_cluster_kernel<8, false>);
     const size_t L = (c + nc - 1) / nc;

@@ -5,6 +5,8 @@ cfg3-sized run (D = 231,360; truncation at every step; K = 16 smoother products)
     tiles, so every CTA cycles both accumulator buffers several times);
   * CAKF_STRIP2: the alg:mfks K = N^ products (B_k t, V t, (K(X,T)V) t) on the cp.async strip
     kernel vs the register-prefetch strip kernel (same DMMA sequence per output).
+  * CAKF_SMOOTH_OVERLAP: the smoother's kernel-applied carriers (K(X,T)V t and the carrier assembly) on the
+    side stream beside the truncation's Gram and eigensolver vs in line (same kernels, same operands).
 The switches are read once per process, so each variant runs in its own interpreter."""
 import os
 import subprocess
@@ -42,7 +44,7 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-@pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2"])
+@pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2", "CAKF_SMOOTH_OVERLAP"])
 def test_variant_bit_identical(tmp_path, switch):
     res = {}
     for flag in ("0", "1"):
