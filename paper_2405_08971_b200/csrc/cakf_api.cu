@@ -270,9 +270,11 @@ struct Impl final : ImplBase {
   float *gwork = nullptr, *Qf = nullptr;
   int *gexA = nullptr, *gexB = nullptr;   // INT8-slice GEMM: per-(row, K chunk) exponents
   // contractions with K >= i8_min_k (the D- and N-long reductions: truncation Gram, M^T x, (HM)^T [v V],
-  // and the K = r products M (M^T x), M U) run on the INT8-slice GEMM; K = N^ = 64 (B_k t) through DGEMM
-  // (A/B in the bench, scripts/gemm_i8_bench.py); CAKF_I8_MIN_K overrides
-  int i8_min_k = [] { const char* e = getenv("CAKF_I8_MIN_K"); return e ? std::atoi(e) : 512; }();
+  // and the K = r_in products M (M^T x), M U, from r_in = 128 on) run on the INT8-slice GEMM; K = N^ = 64
+  // (B_k t, V t, (K(X,T)V) t) on the DMMA strip kernel.  (At 512 the early steps' M^- (M^-T x) with
+  // r_in = 128 .. 448 fell to the tiled DMMA kernel: 7 - 10 ms per call, ≈ 40 ms per cfg3 pass.)
+  // CAKF_I8_MIN_K overrides
+  int i8_min_k = [] { const char* e = getenv("CAKF_I8_MIN_K"); return e ? std::atoi(e) : 128; }();
   bool i8_mqr = [] { const char* e = getenv("CAKF_I8_MQR"); return e && e[0] == '1'; }();
   size_t gex_elems = 0;
 
@@ -1369,7 +1371,8 @@ struct Impl final : ImplBase {
       }
       prof_end(CAKF_PROF_LOWRANK, pk);
       // m^s_k = m_k + P_k A^T w^s ;  var^s_k = var_k - rowsumsq(P_k A^T W^s)   (lines 5-6)
-      CK_CUDA(StepKernels<T>::smooth_out(D, C, S.m, S.var, yb, S.ms, S.vs, st));
+      // (with the carriers below: nothing else in the step reads m^s_k / var^s_k)
+      if (smooth_k2) CK_CUDA(StepKernels<T>::smooth_out(D, C, S.m, S.var, yb, S.ms, S.vs, st));
       // w^s_k, W^s_k = [W_k, (I - W W^T P^-) A^T W^s]   (lines 7-8)
       CK_CUDA(StepKernels<T>::ws_build(n ? N : 0, D, n, q, S.idx, X, S.XV, R, Wf, ws, (int)plo, (int)NX, st));
       bool kcar_side = false;
@@ -1381,7 +1384,9 @@ struct Impl final : ImplBase {
         kcar_side = sizeof(T) == 4 && side && st2 && n <= 64 && NX >= 512 && smooth_overlap() && rcap >= 0 &&
                     qn_ > rcap;   // a truncation follows: fork after its Gram, beside the eigensolver
         const T* KVk = S.KV;
-        auto carriers = [this, n, q, C, KVk](cudaStream_t on) -> int {
+        T *mk = S.m, *vk = S.var, *msk = S.ms, *vsk = S.vs;
+        auto carriers = [this, n, q, C, KVk, mk, vk, msk, vsk](cudaStream_t on) -> int {
+          CK_CUDA(StepKernels<T>::smooth_out(D, C, mk, vk, yb, msk, vsk, on));   // m^s_k, var^s_k (lines 5-6)
           cudaStream_t main_st = st;
           st = on;   // gemm() and prof_* use the member stream
           size_t pk2 = prof_begin();
