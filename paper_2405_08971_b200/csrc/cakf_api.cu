@@ -634,7 +634,7 @@ struct Impl final : ImplBase {
       k1_mask = carve<unsigned short>((size_t)matvec_sym_units((int)Nmax) + 1);
       act_cnt_tt = carve<int>(no128);
       act_list_tt = carve<int>((size_t)no128 * no32);
-      k1_count = carve<int>(1);
+      k1_count = carve<int>(64);   // [0] active-unit count, then launch_k1_active_units' group counters
     }
     k1_sched = carve<unsigned>(4);
     k1_range = carve<long long>(2);

@@ -32,7 +32,8 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
                               const float4* sph32 = nullptr, float cut = 0.f, unsigned* sched = nullptr);
 // sched (nullable, 2 zero-initialised counters, one per handle): dynamic unit scheduling (CAKF_K1_DYN=0: off)
 int matvec_sym_blocks_per_tile_pair();   // warp blocks per 128 x 128 tile pair counted by done_pairs
-// compact ascending list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`
+// list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`, grouped by their
+// active-pair count (most first); count: a device workspace of >= 64 ints, count[0] = the list length.
 // urange (nullable, device): read [u_lo, u_hi) from it instead (the balanced multi-GPU split below)
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
                                    unsigned short* mask, int* count, cudaStream_t st, const long long* urange = nullptr);
@@ -85,6 +86,7 @@ bool use_tc_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM i
 bool use_k2_stack();   // CAKF_K2_STACK=0: six 3xBF16 MMAs per k-step in K2 instead of three stacked ones
 bool use_i8_stack();   // CAKF_I8_STACK=0: one MMA per slice pair, single accumulator buffer (A/B only)
 bool use_i8_split_fused();   // CAKF_I8_SPLIT_FUSED=0: the two-pass exponent + slice kernels (A/B only)
+bool use_split_rc8();   // CAKF_SPLIT_RC8=0: the 2-byte-store bf16x3 transpose-split (A/B only)
 bool use_tc_persist();   // CAKF_TC_PERSIST=0: un-split 3xBF16 GEMMs on the one-tile-per-CTA kernel (A/B only)
 constexpr size_t kGemmWorkFloats = (size_t)32 << 20;
 

@@ -604,35 +604,49 @@ __device__ unsigned sym_unit_mask(const float4* __restrict__ sph, int nt, int nb
 // one block: compact list of the units in [u_lo, u_hi) with at least one active tile pair, ordered by
 // decreasing number of active pairs (longest first, so the strided assignment of the K1 grid balances);
 // the order inside a bucket is arbitrary, which cannot change any result (each unit owns its partial slots)
-__global__ void k1_active_units_kernel(const float4* __restrict__ sph, int nt, int nb, long long u_lo, long long u_hi,
-                                       float cut, int* __restrict__ list, unsigned short* __restrict__ mask,
-                                       int* __restrict__ count, const long long* __restrict__ urange) {
+// Active-unit list of the symmetric K1 (units with at least one tile pair inside the cut), grouped by their
+// number of active tile pairs, most first (longest-first dynamic scheduling).  Three grid-wide launches:
+// count per group, offsets, scatter (the unit masks are recomputed, no per-unit buffer).  ws = count: [0] the
+// list length, [1 + c] group sizes, [1 + kGroups + c] running offsets.  The order inside a group is not
+// deterministic and does not need to be: every unit writes its own partial slots.
+constexpr int kK1Groups = SYM_S * SYM_S + 1;
+__device__ __forceinline__ void k1_unit_range(const long long* urange, long long& u_lo, long long& u_hi) {
   if (urange) {   // this rank's unit range, balanced by active tile pairs (k1_balanced_range_kernel)
     u_lo = urange[0];
     u_hi = urange[1];
   }
-  __shared__ int bucket[SYM_S * SYM_S + 1];
-  if (threadIdx.x <= SYM_S * SYM_S) bucket[threadIdx.x] = 0;
+}
+__global__ void k1_units_count_kernel(const float4* __restrict__ sph, int nt, int nb, long long u_lo, long long u_hi,
+                                      float cut, int* __restrict__ ws, const long long* __restrict__ urange) {
+  k1_unit_range(urange, u_lo, u_hi);
+  __shared__ int bucket[kK1Groups];
+  if (threadIdx.x < kK1Groups) bucket[threadIdx.x] = 0;
   __syncthreads();
-  for (long long u = u_lo + threadIdx.x; u < u_hi; u += blockDim.x) {
+  for (long long u = u_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; u < u_hi;
+       u += (long long)gridDim.x * blockDim.x) {
     const unsigned m = sym_unit_mask(sph, nt, nb, u, cut);
     if (m) atomicAdd(&bucket[__popc(m)], 1);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {   // exclusive offsets, 16 active pairs first
-    int run = 0;
-    for (int c = SYM_S * SYM_S; c >= 1; --c) {
-      const int t = bucket[c];
-      bucket[c] = run;
-      run += t;
-    }
-    *count = run;
+  if (threadIdx.x < kK1Groups && bucket[threadIdx.x]) atomicAdd(&ws[1 + threadIdx.x], bucket[threadIdx.x]);
+}
+__global__ void k1_units_offsets_kernel(int* __restrict__ ws) {   // one thread: 16 active pairs first
+  int run = 0;
+  for (int c = kK1Groups - 1; c >= 1; --c) {
+    ws[1 + kK1Groups + c] = run;
+    run += ws[1 + c];
   }
-  __syncthreads();
-  for (long long u = u_lo + threadIdx.x; u < u_hi; u += blockDim.x) {
+  ws[0] = run;
+}
+__global__ void k1_units_scatter_kernel(const float4* __restrict__ sph, int nt, int nb, long long u_lo, long long u_hi,
+                                        float cut, int* __restrict__ list, unsigned short* __restrict__ mask,
+                                        int* __restrict__ ws, const long long* __restrict__ urange) {
+  k1_unit_range(urange, u_lo, u_hi);
+  for (long long u = u_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; u < u_hi;
+       u += (long long)gridDim.x * blockDim.x) {
     const unsigned m = sym_unit_mask(sph, nt, nb, u, cut);
     if (m) {
-      const int pos = atomicAdd(&bucket[__popc(m)], 1);
+      const int pos = atomicAdd(&ws[1 + kK1Groups + __popc(m)], 1);
       list[pos] = (int)u;
       mask[pos] = (unsigned short)m;
     }
@@ -643,7 +657,15 @@ cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, lon
                                    unsigned short* mask, int* count, cudaStream_t st, const long long* urange) {
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
-  k1_active_units_kernel<<<1, 1024, 0, st>>>(sph, nt, nb, u_lo, u_hi, cut, list, mask, count, urange);
+  const long long U = (long long)nb * (nb + 1) / 2;   // upper bound of the unit range (urange lies inside)
+  const int grid = (int)std::max<long long>(1, std::min<long long>((U + 255) / 256, 8LL * num_sms()));
+  cudaError_t e = cudaMemsetAsync(count, 0, (size_t)(1 + 2 * kK1Groups) * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  k1_units_count_kernel<<<grid, 256, 0, st>>>(sph, nt, nb, u_lo, u_hi, cut, count, urange);
+  if ((e = note_launch_err()) != cudaSuccess) return e;
+  k1_units_offsets_kernel<<<1, 1, 0, st>>>(count);
+  if ((e = note_launch_err()) != cudaSuccess) return e;
+  k1_units_scatter_kernel<<<grid, 256, 0, st>>>(sph, nt, nb, u_lo, u_hi, cut, list, mask, count, urange);
   return note_launch_err();
 }
 
