@@ -438,6 +438,39 @@ __global__ void split_planes_kernel(const float* __restrict__ src, int R, int K,
   }
 }
 
+// Rows-contiguous source (the truncation's F = [M^- | B], D x c): 64 k x 32 rows per block, transposed
+// through shared memory; every thread splits 8 consecutive k of one row and writes one 16-byte chunk per
+// plane (the generic version above writes 2-byte elements).  Same exact split, same planes.
+__global__ void __launch_bounds__(256) split_planes_rc8_kernel(const float* __restrict__ src, int R, int K, int Kp,
+                                                               size_t ld, uint16_t* __restrict__ planes,
+                                                               size_t plane) {
+  __shared__ float tile[64][33];
+  const int k0 = blockIdx.x * 64, r0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // loads: 8 x 32
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int k = k0 + ty + 8 * i, r = r0 + tx;
+    tile[ty + 8 * i][tx] = (k < K && r < R) ? src[r + (size_t)k * ld] : 0.f;
+  }
+  __syncthreads();
+  const int rl = threadIdx.x >> 3, kq = threadIdx.x & 7, r = r0 + rl, k = k0 + 8 * kq;
+  if (r >= R || k >= Kp) return;
+  uint32_t w1[4], w2[4], w3[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t a1, a2, a3, b1, b2, b3;
+    split3(tile[8 * kq + 2 * j][rl], a1, a2, a3);
+    split3(tile[8 * kq + 2 * j + 1][rl], b1, b2, b3);
+    w1[j] = a1 | (b1 << 16);
+    w2[j] = a2 | (b2 << 16);
+    w3[j] = a3 | (b3 << 16);
+  }
+  const size_t e = (size_t)r * Kp + k;   // Kp % 8 == 0, k % 8 == 0: 16-byte aligned
+  *reinterpret_cast<uint4*>(planes + e) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+  *reinterpret_cast<uint4*>(planes + plane + e) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+  *reinterpret_cast<uint4*>(planes + 2 * plane + e) = make_uint4(w3[0], w3[1], w3[2], w3[3]);
+}
+
 template <typename O>
 __global__ void splitk_reduce_kernel(int M, int N, int S, const float* __restrict__ work, double alpha, double beta,
                                      O* __restrict__ C, size_t ldc) {
@@ -486,8 +519,13 @@ cudaError_t gemm_tc_split(const float* src, int R, int K, size_t ld, bool k_cont
   const int Kp = gemm_tc_kp(K);
   dim3 grid((Kp + 31) / 32, (R + 31) / 32);
   const size_t plane = (size_t)R * Kp;
-  if (k_contig) split_planes_kernel<true><<<grid, 256, 0, st>>>(src, R, K, Kp, ld, planes, plane);
-  else split_planes_kernel<false><<<grid, 256, 0, st>>>(src, R, K, Kp, ld, planes, plane);
+  if (k_contig) {
+    split_planes_kernel<true><<<grid, 256, 0, st>>>(src, R, K, Kp, ld, planes, plane);
+  } else if (reinterpret_cast<uintptr_t>(planes) % 16 == 0 && plane % 8 == 0 && use_split_rc8()) {
+    split_planes_rc8_kernel<<<dim3((Kp + 63) / 64, (R + 31) / 32), 256, 0, st>>>(src, R, K, Kp, ld, planes, plane);
+  } else {
+    split_planes_kernel<false><<<grid, 256, 0, st>>>(src, R, K, Kp, ld, planes, plane);
+  }
   return note_launch_err();
 }
 
@@ -553,6 +591,11 @@ cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, in
   if (Cd) splitk_reduce_kernel<double><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, S, work, alpha, beta, Cd, ldc);
   else splitk_reduce_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, S, work, alpha, beta, C, ldc);
   return note_launch_err();
+}
+
+bool use_split_rc8() {
+  static const bool v = !env_is("CAKF_SPLIT_RC8", '0');
+  return v;
 }
 
 bool use_tc_persist() {

@@ -7,6 +7,7 @@ cfg3-sized run (D = 231,360; truncation at every step; K = 16 smoother products)
     kernel vs the register-prefetch strip kernel (same DMMA sequence per output).
   * CAKF_SMOOTH_OVERLAP: the smoother's kernel-applied carriers (K(X,T)V t and the carrier assembly) on the
     side stream beside the truncation's Gram and eigensolver vs in line (same kernels, same operands).
+  * CAKF_SPLIT_RC8: the truncation's factor split into bf16 planes with 16-byte stores vs 2-byte stores.
 The switches are read once per process, so each variant runs in its own interpreter."""
 import os
 import subprocess
@@ -44,7 +45,7 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-@pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2", "CAKF_SMOOTH_OVERLAP"])
+@pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2", "CAKF_SMOOTH_OVERLAP", "CAKF_SPLIT_RC8"])
 def test_variant_bit_identical(tmp_path, switch):
     res = {}
     for flag in ("0", "1"):
