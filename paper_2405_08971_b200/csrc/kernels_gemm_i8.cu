@@ -508,11 +508,23 @@ __global__ void __launch_bounds__(I_SPLIT_T) i8_split_kc_kernel(const Src* __res
   const Src* row = src + (size_t)r * ld;
   Src v[I_SPLIT_G][4];
   Src m = Src(0);
+  // fp32 rows with 16-byte alignment (ld % 4 == 0, aligned base): one float4 load per group of 4
+  const bool vec = sizeof(Src) == 4 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
 #pragma unroll
   for (int g = 0; g < I_SPLIT_G; ++g) {
     const int k = k0 + 4 * (g * I_SPLIT_T + threadIdx.x);
+    if (vec && k + 3 < K && k + 3 < kend) {
+      if constexpr (sizeof(Src) == 4) {
+        const float4 q = *reinterpret_cast<const float4*>(row + k);
+        v[g][0] = q.x;
+        v[g][1] = q.y;
+        v[g][2] = q.z;
+        v[g][3] = q.w;
+      }
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[g][j] = k + j < K && k + j < kend ? row[k + j] : Src(0);
+      for (int j = 0; j < 4; ++j) v[g][j] = k + j < K && k + j < kend ? row[k + j] : Src(0);
+    }
   }
 #pragma unroll
   for (int g = 0; g < I_SPLIT_G; ++g)
@@ -572,7 +584,7 @@ __global__ void __launch_bounds__(256) i8_split_rc_kernel(const Src* __restrict_
   {
     const int r = r0 + tx;
     Src m = Src(0);
-#pragma unroll 8
+#pragma unroll 16
     for (int k = ty; k < Kp; k += 8) {
       const Src v = (k < K && r < R) ? src[r + (size_t)k * ld] : Src(0);
       tile[k * 33 + tx] = v;
