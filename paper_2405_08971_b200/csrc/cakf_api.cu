@@ -137,6 +137,12 @@ bool fetch_doubles(const double* src, size_t n, std::vector<double>& out) {
   std::memcpy(out.data(), src, n * sizeof(double));
   return true;
 }
+// CAKF_STAGE_AB=0: the inner loop's stages A and B as two kernels (A/B only)
+bool stage_ab() {
+  static const bool v = !env_is("CAKF_STAGE_AB", '0');
+  return v;
+}
+
 // CAKF_SMOOTH_OVERLAP=0: the smoother's carrier products run in line with the truncation (A/B only)
 bool smooth_overlap() {
   static const bool v = !env_is("CAKF_SMOOTH_OVERLAP", '0');
@@ -1059,11 +1065,17 @@ struct Impl final : ImplBase {
       }
       prof_end(CAKF_PROF_K1, pk);
       pk = prof_begin();
-      CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, fork ? nullptr : HM, rin, part, W, redA,
-                                     cnt, st));
-      if (fork) CK_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
-      CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 64, st,
-                                     fork ? hmw : nullptr));
+      if ((fork || rin == 0) && stage_ab()) {   // stage A + B in one pass (HM u from the side stream)
+        if (fork) CK_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+        CK_CUDA(StepKernels<T>::stageAB(N, kch, kpart, sig00, lam2, s, r, fork ? hmw : nullptr, g, V, i - 1, part, W,
+                                        redB, redA + rin, cnt + 64, st));
+      } else {
+        CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, fork ? nullptr : HM, rin, part, W, redA,
+                                       cnt, st));
+        if (fork) CK_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+        CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 64, st,
+                                       fork ? hmw : nullptr));
+      }
       if (reorth && i > 1) {  // CGS2 (R19): d = s - V c, then d -= V (V^T G d)
         CK_CUDA(StepKernels<T>::stageC(N, V, Z, i - 1, redB, s, g, d, Gd, s, redA, rin, redB + (i - 1), part, W, redC,
                                        cnt + 128, C, eps, i, 1, st));

@@ -310,6 +310,62 @@ stageB_kernel(int N, const T* __restrict__ HM, int rin, const double* __restrict
   reduce_blocks(nV + 1, W, part, cnt, red);
 }
 
+// ------------------------------------------------------------------ stage A + B in one pass
+// When u = (HM)^T s and w = HM u come from the side stream (hmw) — or r_in = 0 — stage A's g' feeds only
+// stage B, so one kernel forms g' and g = g' - w per row (the same arithmetic as the two kernels, so the
+// same bits), c = V^T g, s^T g and stage A's three dots in one block-wide + grid-wide reduction: one launch
+// and one reduction fewer per inner iteration, and no g' round trip through HBM.  red: [c | s^T g | s^T r,
+// s^T g', r^T r]; the finalising block copies the last three to ared_tail (= redA + r_in, stage C's ared).
+template <typename T>
+__global__ void __launch_bounds__(kTile)
+stageAB_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const T* __restrict__ lam2,
+               const T* __restrict__ s, const T* __restrict__ r, const double* __restrict__ wpre, T* __restrict__ g,
+               const T* __restrict__ V, int nV, double* __restrict__ part, int W, double* __restrict__ red,
+               double* __restrict__ ared_tail, unsigned* cnt) {
+  griddep_wait();
+  __shared__ double scratch[32 * 4];
+  const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};   // s.g, s.r, s.g', r.r
+  if (row < r1) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    for (; c + 32 <= nch; c += 32) {
+      T x[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) x[q] = partial[(size_t)(c + q) * N + row];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q & 3] += (double)x[q];
+    }
+    for (; c + 16 <= nch; c += 16) {
+      T x[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) x[q] = partial[(size_t)(c + q) * N + row];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q & 3] += (double)x[q];
+    }
+    for (; c < nch; ++c) acc[0] += (double)partial[(size_t)c * N + row];
+    const double ksum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    const T si = s[row], ri = r[row];
+    const T gpv = (T)(sig00 * ksum) + lam2[row] * si;                // g'  (stage A)
+    const T gi = wpre ? (T)((double)gpv - wpre[row]) : gpv;          // G s (stage B)
+    g[row] = gi;
+    a[0] = (double)si * (double)gi;
+    a[1] = (double)si * (double)ri;
+    a[2] = (double)si * (double)gpv;
+    a[3] = (double)ri * (double)ri;
+  }
+  block_sum<4>(a, scratch);
+  double* slot = part + (size_t)blockIdx.x * W;
+  if (threadIdx.x == 0) {
+    slot[nV] = a[0];
+    slot[nV + 1] = a[1];
+    slot[nV + 2] = a[2];
+    slot[nV + 3] = a[3];
+  }
+  tile_cols_dot(V, (size_t)N, nV, g, r0, r1, slot);               // c = V^T G s (g rows of this tile: own writes)
+  if (reduce_blocks(nV + 4, W, part, cnt, red) && threadIdx.x < 3) ared_tail[threadIdx.x] = red[nV + 1 + threadIdx.x];
+}
+
 // ------------------------------------------------------------------ stage C
 // d = sin - V c ; Gd = gin - Z c  (line 11; Z = G V so G d needs no second matvec, R18).
 // pass == 1 (first pass of CGS2, R19): also c2 = V^T Gd -> red[0..nV).
@@ -961,6 +1017,14 @@ cudaError_t StepKernels<T>::stageB(int N, const T* HM, int rin, const double* ur
   return launch_pdl(stageB_kernel<T>, dim3(stage_blocks(N)), dim3(kTile),
                     wpre ? 8 : sizeof(double) * (rin > 0 ? rin : 1), st, N, HM, rin, ured, gp, s, g, V, nV, part, W,
                     red, cnt, wpre);
+}
+
+template <typename T>
+cudaError_t StepKernels<T>::stageAB(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s,
+                                    const T* r, const double* wpre, T* g, const T* V, int nV, double* part, int W,
+                                    double* red, double* ared_tail, unsigned* cnt, cudaStream_t st) {
+  return launch_pdl(stageAB_kernel<T>, dim3(stage_blocks(N)), dim3(kTile), 0, st, N, nch, partial, sig00, lam2, s, r,
+                    wpre, g, V, nV, part, W, red, ared_tail, cnt);
 }
 
 template <typename T>

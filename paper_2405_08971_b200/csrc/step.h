@@ -59,6 +59,11 @@ struct StepKernels {
                           cudaStream_t st);
   // w = HM u (fp64) from the reduced u = red[0, rin) (side stream, after hmts)
   static cudaError_t hmu(int N, const T* HM, int rin, const double* ured, double* w, cudaStream_t st);
+  // stage A + B in one pass (u, HM u from the side stream in wpre, or r_in = 0 with wpre = nullptr):
+  // g = G s; red = [V^T g | s^T g | s^T r, s^T g', r^T r], the last three also to ared_tail
+  static cudaError_t stageAB(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s, const T* r,
+                             const double* wpre, T* g, const T* V, int nV, double* part, int W, double* red,
+                             double* ared_tail, unsigned* cnt, cudaStream_t st);
   static cudaError_t stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g, const T* V,
                             int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st,
                             const double* wpre = nullptr);

@@ -7,7 +7,9 @@ cfg3-sized run (D = 231,360; truncation at every step; K = 16 smoother products)
     kernel vs the register-prefetch strip kernel (same DMMA sequence per output).
   * CAKF_SMOOTH_OVERLAP: the smoother's kernel-applied carriers (K(X,T)V t and the carrier assembly) on the
     side stream beside the truncation's Gram and eigensolver vs in line (same kernels, same operands).
-  * CAKF_SPLIT_RC8: the truncation's factor split into bf16 planes with 16-byte stores vs 2-byte stores.
+  * CAKF_SPLIT_RC8: the truncation's factor split into bf16 planes with 16-byte stores vs 2-byte stores;
+  * CAKF_STAGE_AB: the inner loop's stages A and B (alg:update_pls lines 9-11) as one kernel vs
+    two (same per-row arithmetic, same block and grid reduction order).
 The switches are read once per process, so each variant runs in its own interpreter."""
 import os
 import subprocess
@@ -45,7 +47,8 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-@pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2", "CAKF_SMOOTH_OVERLAP", "CAKF_SPLIT_RC8"])
+@pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2", "CAKF_SMOOTH_OVERLAP", "CAKF_SPLIT_RC8",
+                                    "CAKF_STAGE_AB"])
 def test_variant_bit_identical(tmp_path, switch):
     res = {}
     for flag in ("0", "1"):
