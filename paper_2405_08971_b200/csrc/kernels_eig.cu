@@ -118,10 +118,13 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
     }
     return;
   }
-  // reflector jr from x = xs[jr+1 .. c) (smem), into vout; tau -> red[40 + (jr & 1)]; CTA 0 writes the outputs
-  auto reflector = [&](int jr, const double* xs, double dj, double* vout) {
+  // reflector jr from x = xs[jr+1 .. c) (smem), into vout; tau -> red[40 + (jr & 1)]; CTA 0 writes the outputs.
+  // s2_own >= 0: this thread's share of sum_{l >= jr+2} x_l^2 was already formed (with the column update)
+  auto reflector = [&](int jr, const double* xs, double dj, double* vout, double s2_own) {
     double s2 = 0.0;
-    for (int l = jr + 2 + tid; l < c; l += bd) s2 += xs[l] * xs[l];
+    if (s2_own >= 0.0) s2 = s2_own;
+    else
+      for (int l = jr + 2 + tid; l < c; l += bd) s2 += xs[l] * xs[l];
     s2 = warp_sum_d(s2);
     if (lane == 0) red[warp] = s2;
     __syncthreads();
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
   __syncthreads();
   for (int l = tid; l < c; l += bd) xb[l] = a.G[l];   // column 0 of G: no update yet
   __syncthreads();
-  reflector(0, xb, xb[0], vb);
+  reflector(0, xb, xb[0], vb, -1.0);
   __syncthreads();
 #ifdef CAKF_TRD_TIMING
   long long tacc[8] = {};
@@ -261,19 +264,26 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
     TRD_T(3)
     const double hk = 0.5 * tj * red[35];
     const double vn = vj[j + 1], wn = prw[j + 1] - hk * vn;
+    double s2n = 0.0;   // the next reflector's sum_{l >= j+3} x_l^2, formed with the update (one pass, one sync)
     for (int l = j + 1 + tid; l < c; l += bd) {
       const double w = prw[l] - hk * vj[l];
       wj[l] = w;
-      xb[l] -= vj[l] * wn + w * vn;   // update(j) of column j+1
+      const double x = xb[l] - (vj[l] * wn + w * vn);   // update(j) of column j+1
+      xb[l] = x;
+      if (l >= j + 3) s2n += x * x;
     }
     if (j + 4 <= c) {
-      __syncthreads();   // the reflector reads rows of column j+1 computed by other threads
       TRD_T(4)
-      reflector(j + 1, xb, xb[j + 1], vb + (size_t)(par ^ 1) * ld);
+      // (the reflector's own barrier orders these rows before its reads of other threads' rows)
+      // dj = x_{j+1} is only used by thread 0, which wrote that row itself
+      reflector(j + 1, xb, tid == 0 ? xb[j + 1] : 0.0, vb + (size_t)(par ^ 1) * ld, s2n);
       TRD_T(5)
-    } else if (writer && tid == 0) {   // j + 1 == c - 2: the last 2 x 2 block's column c-2
-      a.d[c - 2] = xb[c - 2];
-      a.e[c - 2] = xb[c - 1];
+    } else {   // j + 1 == c - 2: the last 2 x 2 block's column c-2 (rows c-2, c-1: lanes 0, 1 of warp 0)
+      __syncwarp();
+      if (writer && tid == 0) {
+        a.d[c - 2] = xb[c - 2];
+        a.e[c - 2] = xb[c - 1];
+      }
     }
     __syncthreads();   // xb / wj / vb complete before the next pass; pb, red[36..] are double-buffered
     TRD_T(6)
