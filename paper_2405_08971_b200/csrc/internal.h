@@ -84,6 +84,7 @@ cudaError_t gemm_tc_run(const uint16_t* Ap, int M, const uint16_t* Bp, int N, in
                         float* C, double* Cd, size_t ldc, float* work, size_t work_floats, cudaStream_t st);
 bool use_tc_gemm();   // CAKF_GEMM_F64=1: fp32 contractions through fp64 DGEMM instead
 bool use_k2_stack();   // CAKF_K2_STACK=0: six 3xBF16 MMAs per k-step in K2 instead of three stacked ones
+bool use_i8_pair();   // CAKF_I8_PAIR=1: CTA-pair A multicast in the stacked INT8 GEMM (A/B only; off)
 bool use_i8_stack();   // CAKF_I8_STACK=0: one MMA per slice pair, single accumulator buffer (A/B only)
 bool use_i8_split_fused();   // CAKF_I8_SPLIT_FUSED=0: the two-pass exponent + slice kernels (A/B only)
 bool use_split_rc8();   // CAKF_SPLIT_RC8=0: the 2-byte-store bf16x3 transpose-split (A/B only)

@@ -132,6 +132,15 @@ __device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* tm, int c0
       : "memory");
 }
 
+__device__ __forceinline__ void tma3_mc(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, uint32_t bar,
+                                        uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -156,7 +165,7 @@ __device__ __forceinline__ bool i8_item(int w, int ntiles, int mt, int ntile, in
 __global__ void __launch_bounds__(I_THREADS, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const int* __restrict__ expA, const int* __restrict__ expB, int M, int N, int nkb, int nchunk, int cps,
-               int ntile, int ntiles, int mt, int nwork, int stages, int lower, int stack, double alpha,
+               int ntile, int ntiles, int mt, int nwork, int stages, int lower, int stack, int mc, double alpha,
                double beta, float* __restrict__ C, double* __restrict__ Cd, size_t ldc, double* __restrict__ work) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -171,6 +180,17 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfree + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // mc = 2 (CTA pair, one cluster): both CTAs walk the same items (m tile, pair of n tiles) in lockstep, each
+  // computing its own n tile; every A plane of a K block is loaded once for the pair and multicast into both
+  // CTAs' shared memory (each CTA issues its share of the planes), halving the L2 -> SM traffic of A, the
+  // operand re-read by every n tile.  A stage is refilled only after both CTAs' MMAs released it.
+  const int crank = mc > 1 ? (int)(blockIdx.x % mc) : 0;
+  const int wfirst = blockIdx.x / mc, wstride = gridDim.x / mc;
+  auto item = [&](int w, int& m0, int& n0, int& z) {
+    if (!i8_item(w, ntiles, mt, ntile * mc, lower, m0, n0, z)) return false;
+    n0 += crank * ntile;
+    return true;
+  };
   // stack: the B slices sit contiguously in shared memory, so one MMA A_s x [B_0 | ... | B_{4-s}] (N = (5-s)
   // ntile) at TMEM column offset s ntile lands every product A_s B_t on level s + t's columns: 5 MMAs per
   // 32-deep k-step instead of 15 (each A slice read once), levels ntile columns apart, and with ntile <= 48
@@ -188,7 +208,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
+      mbar_init(smem_u32(&empty[s]), mc);   // released by the MMAs of every CTA of the pair
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&done[b]), 1);
@@ -198,6 +218,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (mc > 1) {   // the peer's barriers exist before any multicast lands on them
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const uint32_t sm0 = smem_u32(sbase);
@@ -206,9 +230,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {   // ===== TMA loader: the K blocks of every item's chunks, in order
       const uint32_t bytes = (uint32_t)I_S * I_APLANE + (uint32_t)I_S * b_plane;
       int it = 0;
-      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+      for (int w = wfirst; w < nwork; w += wstride) {
         int m0, n0, z;
-        if (!i8_item(w, ntiles, mt, ntile, lower, m0, n0, z)) continue;
+        if (!item(w, m0, n0, z)) continue;
         const int kb_begin = z * cps * I_KBC, kb_end = min(nkb, min(nchunk, (z + 1) * cps) * I_KBC);
         for (int kb = kb_begin; kb < kb_end; ++kb, ++it) {
           const int s = it % stages;
@@ -217,8 +241,14 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
           const uint32_t st0 = sm0 + s * stage_bytes;
           const int k0 = kb * I_BK;
+          if (mc > 1) {   // this CTA's share of the A planes, to both CTAs of the pair
 #pragma unroll
-          for (int pl = 0; pl < I_S; ++pl) tma3(st0 + pl * I_APLANE, &tmA, k0, m0, pl, bar);
+            for (int pl = 0; pl < I_S; ++pl)
+              if (pl % mc == crank) tma3_mc(st0 + pl * I_APLANE, &tmA, k0, m0, pl, bar, (uint16_t)((1u << mc) - 1u));
+          } else {
+#pragma unroll
+            for (int pl = 0; pl < I_S; ++pl) tma3(st0 + pl * I_APLANE, &tmA, k0, m0, pl, bar);
+          }
 #pragma unroll
           for (int pl = 0; pl < I_S; ++pl) tma3(st0 + I_S * I_APLANE + pl * b_plane, &tmB, k0, n0, pl, bar);
         }
@@ -229,9 +259,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // ===== MMA issuer: per chunk, level L = s + t accumulates alpha_s beta_t into accumulator L
     const uint32_t idesc = idesc_s8(I_BM, ntile);
     int it = 0, gc = 0;   // K block / chunk counters of this CTA
-    for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    for (int w = wfirst; w < nwork; w += wstride) {
       int m0, n0, z;
-      if (!i8_item(w, ntiles, mt, ntile, lower, m0, n0, z)) continue;
+      if (!item(w, m0, n0, z)) continue;
       const int c0 = z * cps, c1 = min(nchunk, c0 + cps);
       for (int c = c0; c < c1; ++c, ++gc) {
         const int b = gc % nbuf;
@@ -272,9 +302,16 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
               }
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(&empty[s]))
-                         : "memory");
+            if (mc > 1)   // release the stage in both CTAs (the peer may refill its A share into ours)
+              asm volatile(
+                  "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                      smem_u32(&empty[s])),
+                  "h"((uint16_t)((1u << mc) - 1u))
+                  : "memory");
+            else
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                               smem_u32(&empty[s]))
+                           : "memory");
             if (kb == kbe - 1)
               asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                smem_u32(&done[b]))
@@ -290,9 +327,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int half = (warp - 2) >> 2;   // warps 2-5: columns [0, ntile/2), warps 6-9: [ntile/2, ntile)
     const bool direct = work == nullptr;
     int gc = 0;
-    for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    for (int w = wfirst; w < nwork; w += wstride) {
       int m0, n0, z;
-      if (!i8_item(w, ntiles, mt, ntile, lower, m0, n0, z)) continue;
+      if (!item(w, m0, n0, z)) continue;
       const int c0 = z * cps, c1 = min(nchunk, c0 + cps);
       const int row = m0 + quarter * 32 + lane;
       const int cb0 = half * (ntile >> 1), cb1 = cb0 + (ntile >> 1);   // this warp's columns (ntile % 16 == 0)
@@ -390,6 +427,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (mc > 1) {   // no CTA leaves while its peer may still multicast into it or arrive on its barriers
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
@@ -716,7 +757,10 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
     return v == 96 ? 96 : I_STACK_MAXN;
   }();
   const int maxn = stack ? stack_maxn : I_MAXN;
-  const int ntiles = (N + maxn - 1) / maxn;
+  // CTA pairs sharing the A planes by multicast (stacked single-chunk products with >= 2 n tiles)
+  const int mc = (stack && !lower && use_i8_pair() && N > maxn) ? 2 : 1;
+  int ntiles = (N + maxn - 1) / maxn;
+  ntiles = (ntiles + mc - 1) / mc * mc;   // whole pairs (a tile past N computes padding only)
   int ntile = (N + ntiles - 1) / ntiles;
   ntile = std::max(16, (ntile + 15) / 16 * 16);
   const int mt = (M + I_BM - 1) / I_BM;
@@ -742,12 +786,35 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
   if (reduce && (size_t)splits * M * N > work_doubles) return cudaErrorInvalidValue;
   CUtensorMap tmA, tmB;
   if (!make_i8_map(&tmA, Ap, M, Kp, I_BM) || !make_i8_map(&tmB, Bp, N, Kp, ntile)) return cudaErrorInvalidValue;
-  const int nwork = mt * ntiles * splits;
-  const int grid = std::min(nwork, sm_count());
-  gemm_i8_kernel<<<grid, I_THREADS, smem, st>>>(tmA, tmB, expA, expB, M, N, nkb, nchunk, cps, ntile, ntiles, mt,
-                                                nwork, stages, lower ? 1 : 0, stack ? 1 : 0, alpha, beta, C, Cd,
-                                                ldc, reduce ? work : nullptr);
-  cudaError_t e = note_launch_err();
+  const int nunits = ntiles / mc;   // items: (m tile, n tile or pair of n tiles, K split)
+  const int nwork = mt * nunits * splits;
+  cudaError_t e;
+  if (mc > 1) {
+    const int grid = mc * std::min(nwork, sm_count() / mc);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(I_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = mc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel, tmA, tmB, expA, expB, M, N, nkb, nchunk, cps, ntile, nunits, mt,
+                           nwork, stages, lower ? 1 : 0, stack ? 1 : 0, mc, alpha, beta, C, Cd, ldc,
+                           reduce ? work : nullptr);
+    ++launch_counter();
+    if (e == cudaSuccess) e = cudaGetLastError();
+  } else {
+    const int grid = std::min(nwork, sm_count());
+    gemm_i8_kernel<<<grid, I_THREADS, smem, st>>>(tmA, tmB, expA, expB, M, N, nkb, nchunk, cps, ntile, nunits, mt,
+                                                  nwork, stages, lower ? 1 : 0, stack ? 1 : 0, 1, alpha, beta, C, Cd,
+                                                  ldc, reduce ? work : nullptr);
+    e = note_launch_err();
+  }
   if (e != cudaSuccess || !reduce) return e;
   const size_t tot = (size_t)M * N;
   if (Cd)
@@ -757,6 +824,11 @@ cudaError_t gemm_i8_run(const int8_t* Ap, const int* expA, int M, const int8_t* 
     i8_reduce_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, splits, lower ? 1 : 0, work, alpha,
                                                                             beta, C, ldc);
   return note_launch_err();
+}
+
+bool use_i8_pair() {   // off by default: measured no faster on the tall products (S2 1.86 -> 1.99 ms)
+  static const bool v = env_is("CAKF_I8_PAIR", '1');
+  return v;
 }
 
 bool use_i8_stack() {

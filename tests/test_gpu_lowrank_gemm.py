@@ -84,12 +84,13 @@ def test_lowrank_gemm_gram_cancellation(dev):
     _check(F, F, True, False, 1.0, 0.0, None, dev, 1e-8)
 
 
-@pytest.mark.parametrize("switch", ["CAKF_I8_SPLIT_FUSED", "CAKF_I8_STACK"])
+@pytest.mark.parametrize("switch", ["CAKF_I8_SPLIT_FUSED", "CAKF_I8_STACK", "CAKF_I8_PAIR"])
 def test_variant_bit_identical(tmp_path, switch):
     """Schedule-only variants are bit-identical (the slice products are exact integers in any order):
     CAKF_I8_SPLIT_FUSED — the one-pass exponent + slice kernels (i8_split_kc_kernel; i8_split_rc_kernel for a
     rows-contiguous operand with K <= 1024) vs the two-pass path; CAKF_I8_STACK — stacked-B MMAs (5 per
-    k-step, levels 48 columns apart, two TMEM buffers) vs one MMA per slice pair.  Cases: several chunks, a
+    k-step, levels 48 columns apart, two TMEM buffers) vs one MMA per slice pair; CAKF_I8_PAIR — CTA pairs
+    sharing the A planes by TMA multicast vs one CTA per tile.  Cases: several chunks, a
     partial last chunk, K not a multiple of 16, zero rows, a NaN chunk, both orientations, the RC fallback
     beyond K = 1024, N above and below one tile."""
     import os
