@@ -159,7 +159,12 @@ int cakf_update(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* y,
                 const void* noise_var, const int64_t* coord_order);
 
 /* Truncate step k (Sec. 3.2; R3/R4): keep the top min(max_rank, cols)
- * eigen-directions of M_k^T M_k, M~_k = M_k Q_r (eigendecomposition on device). */
+ * eigen-directions of M_k^T M_k, M~_k = M_k Q_r (eigendecomposition on device).
+ * Ordering: on a one-GPU fp32 handle the eigensolver and M Q_r may still run on an internal
+ * stream when this returns (they overlap the next update's prologue and first K1).  Every later
+ * call except cakf_predict / cakf_update (which order themselves after it) first joins that work
+ * into the handle's stream, so library calls stay stream-ordered; before synchronising the
+ * handle's stream yourself right after cakf_truncate, call cakf_sync (CAKF_TRUNC_OVERLAP=0: off). */
 int cakf_truncate(cakf_t h);
 
 /* Backward CAKS sweep k = T-1 .. 0 (alg:mfks; R6, R7) over the steps

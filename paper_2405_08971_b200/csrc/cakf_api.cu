@@ -137,6 +137,12 @@ bool fetch_doubles(const double* src, size_t n, std::vector<double>& out) {
   std::memcpy(out.data(), src, n * sizeof(double));
   return true;
 }
+// CAKF_TRUNC_OVERLAP=0: the filter truncation's eigensolver and M Q_r in line (A/B only)
+bool trunc_overlap() {
+  static const bool v = !env_is("CAKF_TRUNC_OVERLAP", '0');
+  return v;
+}
+
 // CAKF_STAGE_AB=0: the inner loop's stages A and B as two kernels (A/B only)
 bool stage_ab() {
   static const bool v = !env_is("CAKF_STAGE_AB", '0');
@@ -162,6 +168,9 @@ constexpr bool OP_N = false, OP_T = true;   // op(X) = X / X^T of the low-rank c
 
 struct ImplBase {
   virtual ~ImplBase() = default;
+  // the filter truncation's eigensolver / M Q_r may still run on the truncation stream (overlapping the next
+  // update's prologue and first K1); every entry point except predict / update joins it first
+  virtual int join_pending() { return CAKF_OK; }
   virtual int init(const cakf_config& cfg) = 0;
   virtual int reset() = 0;
   virtual int predict(const double* A, const double* Q, const void* b) = 0;
@@ -203,6 +212,18 @@ struct Impl final : ImplBase {
   cudaEvent_t ev_ws = nullptr, ev_kcar = nullptr;
   cudaEvent_t f2_wait = nullptr;   // consumed by truncate_factor*: wait before the second factor's GEMM
   std::function<int()> after_gram;  // consumed by truncate_factor*: enqueued right after the Gram (side work)
+  // filter truncation: eigensolver + M Q_r (and the next predict's M^- = A M~) on st_t, beside the next
+  // update's prologue and first K1 (they need only m^-); the update joins before gathering H M^-
+  cudaStream_t st_t = nullptr;
+  cudaEvent_t ev_tf = nullptr, ev_td = nullptr;
+  bool fork_trunc = false;     // set by truncate() around its truncate_factor call
+  bool trunc_pending = false;  // work on st_t not yet joined into st
+  int join_pending() override {
+    if (!trunc_pending) return CAKF_OK;
+    trunc_pending = false;
+    CK_CUDA(cudaStreamWaitEvent(st, ev_td, 0));
+    return CAKF_OK;
+  }
   double* part2 = nullptr;
   double* hmw = nullptr;   // HM u (fp64 rows), formed on the side stream
   bool side = [] { const char* e = getenv("CAKF_NO_SIDE_STREAM"); return !(e && e[0] == '1'); }();
@@ -471,6 +492,12 @@ struct Impl final : ImplBase {
     if (sol) cusolverDnDestroy(sol);
     if (own_stream && st) cudaStreamDestroy(st);
     if (st2) cudaStreamDestroy(st2);
+    if (st_t) {
+      cudaStreamSynchronize(st_t);
+      cudaStreamDestroy(st_t);
+    }
+    if (ev_tf) cudaEventDestroy(ev_tf);
+    if (ev_td) cudaEventDestroy(ev_td);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_ws) cudaEventDestroy(ev_ws);
@@ -721,6 +748,11 @@ struct Impl final : ImplBase {
       }
       CK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       CK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      if (sizeof(T) == 4 && world == 1 && trunc_overlap()) {
+        CK_CUDA(cudaStreamCreateWithFlags(&st_t, cudaStreamNonBlocking));
+        CK_CUDA(cudaEventCreateWithFlags(&ev_tf, cudaEventDisableTiming));
+        CK_CUDA(cudaEventCreateWithFlags(&ev_td, cudaEventDisableTiming));
+      }
       CK_CUDA(cudaEventCreateWithFlags(&ev_ws, cudaEventDisableTiming));
       CK_CUDA(cudaEventCreateWithFlags(&ev_kcar, cudaEventDisableTiming));
     }
@@ -803,7 +835,12 @@ struct Impl final : ImplBase {
     const T* src = P.truncated ? Mtil : P.Mk;
     const int rin = P.truncated ? P.rank_out : P.cols;
     S.rin = rin;                                                      // M^- = A M~   (Prop A.3)
-    if (rin) CK_CUDA(StepKernels<T>::mix((int)NX, Dp, rin, A, false, src, D, S.Mk, D, st));
+    if (rin) {
+      // M~ may still be in flight on the truncation stream: the mix follows it there (the update joins)
+      cudaStream_t ms = trunc_pending ? st_t : st;
+      CK_CUDA(StepKernels<T>::mix((int)NX, Dp, rin, A, false, src, D, S.Mk, D, ms));
+      if (trunc_pending) CK_CUDA(cudaEventRecord(ev_td, st_t));
+    }
     S.cols = rin;
     S.n = S.N = 0;
     S.missing = true;
@@ -920,6 +957,7 @@ struct Impl final : ImplBase {
     const int k = kcur;
     const int N = (int)n_obs;
     if (N == 0) {                                                     // IsMissing
+      CK(join_pending());   // rowvar reads M^-
       CK_CUDA(cudaMemcpyAsync(S.m, S.m_pred, D * sizeof(T), cudaMemcpyDeviceToDevice, st));
       S.cols = S.rin;
       S.n = 0;
@@ -962,8 +1000,15 @@ struct Impl final : ImplBase {
     // then r^(0) and the first action
     HM = hmx + N;
     CK_CUDA(StepKernels<T>::gather_rows(N, 1, S.idx, S.m_pred, D, hmx, N, (int)plo, (int)NX, st));
-    if (rin) CK_CUDA(StepKernels<T>::gather_rows(N, rin, S.idx, S.Mk, D, HM, N, (int)plo, (int)NX, st));
-    CK(allreduce(hmx, (size_t)N * (1 + rin)));
+    // H M^- needs M^- = A M~ (possibly still on the truncation stream): gathered after the first K1 then
+    if (niter == 0) CK(join_pending());   // no first K1 to hide the truncation behind
+    bool hm_ready = !trunc_pending;
+    if (hm_ready) {
+      if (rin) CK_CUDA(StepKernels<T>::gather_rows(N, rin, S.idx, S.Mk, D, HM, N, (int)plo, (int)NX, st));
+      CK(allreduce(hmx, (size_t)N * (1 + rin)));
+    } else {
+      CK(allreduce(hmx, (size_t)N));   // H m^- now, H M^- after the first K1
+    }
     CK_CUDA(StepKernels<T>::prep(N, S.idx, coords, ybuf, hmx, policy, order32, seed, k, sigma, r, s, S.XV, xcs, st, blk,
                                  rbs));
     const double sig00 = S.sig_t.a[0][0];
@@ -1003,16 +1048,18 @@ struct Impl final : ImplBase {
     }
     T* Sblk = tmp;   // N x b actions   (post-loop scratch, free during the loop)
     T* Yblk = Yb;    // N x b   K_TT S
+    auto fork_hm = [&]() -> int {   // u = HM^T s and HM u on the side stream (joined before stage B)
+      CK_CUDA(cudaEventRecord(ev_fork, st));
+      CK_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
+      CK_CUDA(StepKernels<T>::hmts(N, HM, rin, s, part2, W, redA, cnt + 256, st2));
+      CK_CUDA(StepKernels<T>::hmu(N, HM, rin, redA, hmw, st2));
+      CK_CUDA(cudaEventRecord(ev_join, st2));
+      return CAKF_OK;
+    };
     for (int i = 1; i <= niter; ++i) {
       // G s  (matrix-free: kernel rows on the fly + low-rank downdate + noise)
-      const bool fork = side && rin > 0;
-      if (fork) {   // u = HM^T s on the side stream, concurrently with K1 (joined before stage B)
-        CK_CUDA(cudaEventRecord(ev_fork, st));
-        CK_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
-        CK_CUDA(StepKernels<T>::hmts(N, HM, rin, s, part2, W, redA, cnt + 256, st2));
-        CK_CUDA(StepKernels<T>::hmu(N, HM, rin, redA, hmw, st2));
-        CK_CUDA(cudaEventRecord(ev_join, st2));
-      }
+      bool fork = side && rin > 0;
+      if (fork && hm_ready) CK(fork_hm());   // concurrently with K1
       size_t pk = prof_begin();
       const T* kpart = partial;
       int kch = nch;
@@ -1064,6 +1111,13 @@ struct Impl final : ImplBase {
       }
       }
       prof_end(CAKF_PROF_K1, pk);
+      if (!hm_ready) {   // first iteration beside the previous truncation: join it, gather H M^-, fork now
+        CK(join_pending());
+        if (rin) CK_CUDA(StepKernels<T>::gather_rows(N, rin, S.idx, S.Mk, D, HM, N, (int)plo, (int)NX, st));
+        CK(allreduce(HM, (size_t)N * rin));
+        hm_ready = true;
+        if (fork) CK(fork_hm());
+      }
       pk = prof_begin();
       if ((fork || rin == 0) && stage_ab()) {   // stage A + B in one pass (HM u from the side stream)
         if (fork) CK_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
@@ -1246,7 +1300,30 @@ struct Impl final : ImplBase {
       job.swap(after_gram);
       CK(job());
     }
-    ps = prof_begin();
+    // filter truncation: the eigensolver and M Q_r on st_t (joined by the next update / any other call)
+    const bool forked = fork_trunc && !F2;
+    cudaStream_t main_st = st;
+    if (forked) {
+      CK_CUDA(cudaEventRecord(ev_tf, st));
+      CK_CUDA(cudaStreamWaitEvent(st_t, ev_tf, 0));
+      st = st_t;
+    }
+    const int rc_t = truncate_eig_gemm(F, c, rkeep, out, kept, dropped, failflag, F2, out2, i8);
+    if (forked) {
+      st = main_st;
+      if (rc_t == CAKF_OK) {
+        CK_CUDA(cudaEventRecord(ev_td, st_t));
+        trunc_pending = true;
+      }
+    }
+    CK(rc_t);
+    prof_end(CAKF_PROF_TRUNCATE, pk);
+    return CAKF_OK;
+  }
+
+  int truncate_eig_gemm(const float* F, int c, int rkeep, float* out, double* kept, double* dropped, int* failflag,
+                        const float* F2, float* out2, bool i8) {
+    size_t ps = prof_begin();
     CK(eig(c, rkeep, kept, dropped, failflag));
     prof_end(CAKF_PROF_TRUNC_EIG, ps);
     ps = prof_begin();
@@ -1273,7 +1350,6 @@ struct Impl final : ImplBase {
       }
     }
     prof_end(CAKF_PROF_TRUNC_GEMM, ps);
-    prof_end(CAKF_PROF_TRUNCATE, pk);
     return CAKF_OK;
   }
 
@@ -1320,7 +1396,10 @@ struct Impl final : ImplBase {
       S.truncated = false;
       S.rank_out = S.cols;
     } else {
-      CK(truncate_factor(S.Mk, S.cols, rcap, Mtil, S.kept, &ctl[kcur].dropped, &ctl[kcur].nonfinite));   // Sec. 3.2
+      fork_trunc = st_t != nullptr;
+      const int trc = truncate_factor(S.Mk, S.cols, rcap, Mtil, S.kept, &ctl[kcur].dropped, &ctl[kcur].nonfinite);
+      fork_trunc = false;
+      CK(trc);   // Sec. 3.2
       S.truncated = true;
       S.rank_out = rcap;
     }
@@ -1814,18 +1893,25 @@ int cakf_create(const cakf_config* cfg, cakf_t* out) {
   return CAKF_OK;
 }
 
-#define HANDLE_CHECK(h)                                          \
+#define HANDLE_CHECK_NOJOIN(h)                                   \
   if (!(h) || !(h)->impl) return fail(CAKF_E_ARG, "NULL handle"); \
   DeviceGuard device_guard_((h)->device)
+// every entry point but predict / update first joins the filter truncation still running on its own stream
+#define HANDLE_CHECK(h)                                              \
+  HANDLE_CHECK_NOJOIN(h);                                            \
+  {                                                                  \
+    const int join_rc_ = (h)->impl->join_pending();                  \
+    if (join_rc_ != CAKF_OK) return join_rc_;                        \
+  }
 
 int cakf_reset(cakf_t h) { HANDLE_CHECK(h); return h->impl->reset(); }
 int cakf_predict(cakf_t h, const double* A_t, const double* Q_t, const void* b) {
-  HANDLE_CHECK(h);
+  HANDLE_CHECK_NOJOIN(h);
   return h->impl->predict(A_t, Q_t, b);
 }
 int cakf_update(cakf_t h, int64_t n_obs, const int64_t* obs_idx, const void* y, const void* noise_var,
                 const int64_t* coord_order) {
-  HANDLE_CHECK(h);
+  HANDLE_CHECK_NOJOIN(h);
   return h->impl->update(n_obs, obs_idx, y, noise_var, coord_order);
 }
 int cakf_truncate(cakf_t h) { HANDLE_CHECK(h); return h->impl->truncate(); }

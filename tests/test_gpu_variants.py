@@ -9,7 +9,9 @@ cfg3-sized run (D = 231,360; truncation at every step; K = 16 smoother products)
     side stream beside the truncation's Gram and eigensolver vs in line (same kernels, same operands).
   * CAKF_SPLIT_RC8: the truncation's factor split into bf16 planes with 16-byte stores vs 2-byte stores;
   * CAKF_STAGE_AB: the inner loop's stages A and B (alg:update_pls lines 9-11) as one kernel vs
-    two (same per-row arithmetic, same block and grid reduction order).
+    two (same per-row arithmetic, same block and grid reduction order);
+  * CAKF_TRUNC_OVERLAP: the filter truncation's eigensolver and M Q_r (and the next M^- = A M~) on their own
+    stream beside the next update's prologue and first K1, joined before H M^- is gathered.
 The switches are read once per process, so each variant runs in its own interpreter."""
 import os
 import subprocess
@@ -48,7 +50,7 @@ def _need_gpu():
 
 
 @pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2", "CAKF_SMOOTH_OVERLAP", "CAKF_SPLIT_RC8",
-                                    "CAKF_STAGE_AB"])
+                                    "CAKF_STAGE_AB", "CAKF_TRUNC_OVERLAP"])
 def test_variant_bit_identical(tmp_path, switch):
     res = {}
     for flag in ("0", "1"):
