@@ -9,9 +9,11 @@ from synth import make_workload
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 wl = make_workload("cfg4", T=T)
+stream = torch.cuda.Stream()   # a dedicated stream: the handle runs on it and the events bracket its work
+torch.cuda.set_stream(stream)
 t0 = time.time()
 trans, Sinf = runner.transitions(wl)
-h = runner.make_handle(wl, "f32")
+h = runner.make_handle(wl, "f32", stream=stream.cuda_stream)
 inputs = runner.stage_inputs(wl, "f32")
 h.profile(True)
 runner.run(h, trans, inputs, smooth=True)   # warm
