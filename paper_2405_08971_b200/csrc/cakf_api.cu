@@ -216,6 +216,8 @@ struct Impl final : ImplBase {
   // update's prologue and first K1 (they need only m^-); the update joins before gathering H M^-
   cudaStream_t st_t = nullptr;
   cudaEvent_t ev_tf = nullptr, ev_td = nullptr;
+  cudaStream_t st_e = nullptr;   // eigensolver side stream (T factors beside the divide and conquer)
+  cudaEvent_t ev_ea = nullptr, ev_eb = nullptr;
   bool fork_trunc = false;     // set by truncate() around its truncate_factor call
   bool trunc_pending = false;  // work on st_t not yet joined into st
   int join_pending() override {
@@ -498,6 +500,12 @@ struct Impl final : ImplBase {
     }
     if (ev_tf) cudaEventDestroy(ev_tf);
     if (ev_td) cudaEventDestroy(ev_td);
+    if (st_e) {
+      cudaStreamSynchronize(st_e);
+      cudaStreamDestroy(st_e);
+    }
+    if (ev_ea) cudaEventDestroy(ev_ea);
+    if (ev_eb) cudaEventDestroy(ev_eb);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_ws) cudaEventDestroy(ev_ws);
@@ -748,6 +756,9 @@ struct Impl final : ImplBase {
       }
       CK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       CK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      CK_CUDA(cudaStreamCreateWithFlags(&st_e, cudaStreamNonBlocking));
+      CK_CUDA(cudaEventCreateWithFlags(&ev_ea, cudaEventDisableTiming));
+      CK_CUDA(cudaEventCreateWithFlags(&ev_eb, cudaEventDisableTiming));
       if (sizeof(T) == 4 && world == 1 && trunc_overlap()) {
         CK_CUDA(cudaStreamCreateWithFlags(&st_t, cudaStreamNonBlocking));
         CK_CUDA(cudaEventCreateWithFlags(&ev_tf, cudaEventDisableTiming));
@@ -1248,7 +1259,8 @@ struct Impl final : ImplBase {
       CK_CUDA(StepKernels<double>::take_top(c, rkeep, Gm, eigw, QrD, kept, dropped, st));
       return CAKF_OK;
     }
-    CK_CUDA(eig_top(c, rkeep, Gm, eigws, eigws_bytes, QrD, kept, dropped, nullptr, failflag, st));
+    // the eigensolver's own side stream (the T factors beside the divide and conquer)
+    CK_CUDA(eig_top(c, rkeep, Gm, eigws, eigws_bytes, QrD, kept, dropped, nullptr, failflag, st, st_e, ev_ea, ev_eb));
     static const bool check = env_is("CAKF_EIG_CHECK", '1');
     if (check) {   // debug: residual of the returned eigenpairs against the (lower) Gram, on the host
       std::vector<double> G((size_t)c * c), Q((size_t)c * rkeep), w(c);

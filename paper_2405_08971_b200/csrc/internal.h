@@ -126,8 +126,10 @@ cudaError_t axpy(size_t n, double a, const T* x, T* y, cudaStream_t st);
 // eigenvalues; dropped (nullable) the sum of the c - r smallest; w_all (c, nullable) all eigenvalues
 // ascending; fail (nullable device int) set to 1 on a non-finite eigenvalue.
 size_t eig_workspace_bytes(int cmax);
+// side / ev_a / ev_b (nullable): a stream and two events for the T factors beside the divide and conquer
 cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, double* Qr, double* kept,
-                    double* dropped, double* w_all, int* fail, cudaStream_t st);
+                    double* dropped, double* w_all, int* fail, cudaStream_t st, cudaStream_t side = nullptr,
+                    cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr);
 
 // ---- per-update kd-tree order of the observed points (kd_order.cu)
 size_t kd_obs_workspace(int Nmax);

@@ -941,7 +941,8 @@ size_t eig_workspace_bytes(int cmax) {
 }
 
 cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, double* Qr, double* kept,
-                    double* dropped, double* w_all, int* fail, cudaStream_t st) {
+                    double* dropped, double* w_all, int* fail, cudaStream_t st, cudaStream_t side, cudaEvent_t ev_a,
+                    cudaEvent_t ev_b) {
   if (c <= 0 || r < 0 || r > c) return cudaErrorInvalidValue;
   if (eig_workspace_bytes(c) > ws_bytes) return cudaErrorInvalidValue;
   char* p = static_cast<char*>(ws);
@@ -1023,6 +1024,18 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
     le = cudaGetLastError();
     if (le != cudaSuccess) return le;
   }
+  // the back-transformation's T factors need only the reflectors: on the side stream (when given), beside the
+  // divide and conquer, joined before bt_apply
+  const int np = c > 2 ? (c - 2 + kBtNb - 1) / kBtNb : 0;
+  const bool larft_side = side && ev_a && ev_b && r > 0 && np > 0;
+  if (larft_side) {
+    cudaError_t e1 = cudaEventRecord(ev_a, st);
+    if (e1 == cudaSuccess) e1 = cudaStreamWaitEvent(side, ev_a, 0);
+    if (e1 != cudaSuccess) return e1;
+    bt_larft_kernel<<<np, kBtThreads, 0, side>>>(c, V, tau, Tp);
+    if ((e1 = note_launch_err()) != cudaSuccess) return e1;
+    if ((e1 = cudaEventRecord(ev_b, side)) != cudaSuccess) return e1;
+  }
   // ---- 2. divide and conquer on T
   dc_init_kernel<<<(unsigned)((cc + 255) / 256), 256, 0, st>>>(c, d, e, dl, Q);
   cudaError_t err = note_launch_err();
@@ -1067,8 +1080,9 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
   eig_values_kernel<<<1, 256, 0, st>>>(c, r, dl, kept, dropped, w_all, fail);
   if ((err = note_launch_err()) != cudaSuccess) return err;
   if (r == 0) return cudaSuccess;
-  const int np = c > 2 ? (c - 2 + kBtNb - 1) / kBtNb : 0;
-  if (np) {
+  if (larft_side) {
+    if ((err = cudaStreamWaitEvent(st, ev_b, 0)) != cudaSuccess) return err;
+  } else if (np) {
     bt_larft_kernel<<<np, kBtThreads, 0, st>>>(c, V, tau, Tp);
     if ((err = note_launch_err()) != cudaSuccess) return err;
   }
