@@ -158,12 +158,16 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
     __syncthreads();
     for (int a = 0; a < na; ++a) {
       if (!((amask >> (a * SYM_S)) & ((1u << SYM_S) - 1u))) continue;   // no active tile pair in this row tile
+      // row groups rotate with the row tile (warp w takes 16-row group (w + a) mod 8 of tile a): a warp whose
+      // rows sit far from this unit's columns in one row tile is near them in another, which evens out the
+      // culled work per warp before the unit-end barrier
+      const int tyr = (ty + 2 * a) & 15, wg = ((tid >> 5) + a) & 7;
       // rows kept negated (d = c - r) as scalars: the packed f32x2 ops broadcast a scalar operand
       float nrx[8], nry[8], nrz[8], rs[8];
       float2 racc2[8];   // per row: even / odd column partial sums
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        const float4 A = tI[(a * SYM_T / 2 + ty * 4 + h) * 2], B = tI[(a * SYM_T / 2 + ty * 4 + h) * 2 + 1];
+        const float4 A = tI[(a * SYM_T / 2 + tyr * 4 + h) * 2], B = tI[(a * SYM_T / 2 + tyr * 4 + h) * 2 + 1];
         nrx[2 * h] = -A.x; nrx[2 * h + 1] = -A.y; nry[2 * h] = -A.z; nry[2 * h + 1] = -A.w;
         nrz[2 * h] = -B.x; nrz[2 * h + 1] = -B.y; rs[2 * h] = B.z; rs[2 * h + 1] = B.w;
       }
@@ -183,7 +187,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
             const bool live = bj * SYM_S * SYM_T + b * SYM_T + q4 * 32 < n;   // beyond: only padding
             bool on = live;
             if (ulist && live) {
-              const float4 A = s16[a * 8 + (tid >> 5)], B = s128[b * 4 + q4];
+              const float4 A = s16[a * 8 + wg], B = s128[b * 4 + q4];
               const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
               on = sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w <= cut;
             }
@@ -253,7 +257,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
           continue;
         }
         if (ulist) {   // same test for this warp's 16 rows against the J tile (warp-uniform)
-          const float4 A = s16[a * 8 + (tid >> 5)], B = s128[b];
+          const float4 A = s16[a * 8 + wg], B = s128[b];
           const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
           if (sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w > cut) continue;
           if ((tid & 31) == 0) atomicAdd(&s_done, 1u);
@@ -317,7 +321,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
         w1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
       }
       w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
-      if (!(tx & 1)) rowacc[a * SYM_T + ty * 8 + (h8 ? 4 : 0) + (h4 ? 2 : 0) + (h2 ? 1 : 0)] += w1;
+      if (!(tx & 1)) rowacc[a * SYM_T + tyr * 8 + (h8 ? 4 : 0) + (h4 ? 2 : 0) + (h2 ? 1 : 0)] += w1;
     }
     __syncthreads();
     if (tid == 0 && done_pairs && ulist) atomicAdd(done_pairs, (unsigned long long)s_done);
