@@ -1,0 +1,7 @@
+#!/bin/bash
+# round 2 (4g): K1 sub-tile 3 square roots on the FMA pipe
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x -k "gram or fullsize or k1 or parity" > gpurun_out/r4g_pytest.log 2>&1; echo "pytest_rc=$?" >> gpurun_out/r4g_pytest.log
+timeout 900 python bench.py --no-dense --serving 0 --no-cpu-baseline > gpurun_out/r4g_bench.json 2> gpurun_out/r4g_bench.err
+timeout 900 python bench.py --no-dense --serving 0 --no-cpu-baseline > gpurun_out/r4g_bench2.json 2>> gpurun_out/r4g_bench.err
