@@ -311,6 +311,7 @@ struct Impl final : ImplBase {
   // output tile of K2, the ascending list of 32-column K-blocks not entirely below the fp32 underflow
   bool cull = false;
   float4 *sph_x128 = nullptr, *sph_x32 = nullptr, *sph_o128 = nullptr, *sph_o32 = nullptr, *sph_o16 = nullptr;
+  float4 *box_o32 = nullptr, *box_o16 = nullptr;   // bounding boxes {lo, hi} of the 32- / 16-point tiles (K1)
   int *act_cnt_sm = nullptr, *act_list_sm = nullptr, *act_cnt_po = nullptr, *act_list_po = nullptr;
   int act_stride_sm = 0, act_stride_po = 0;
   int *k1_list = nullptr, *k1_count = nullptr;
@@ -667,6 +668,7 @@ struct Impl final : ImplBase {
       sph_x128 = carve<float4>(nx128); sph_x32 = carve<float4>(nx32);
       sph_o128 = carve<float4>(no128); sph_o32 = carve<float4>(no32);
       sph_o16 = carve<float4>((Nmax + 15) / 16 + 1);
+      box_o32 = carve<float4>(2 * (size_t)no32); box_o16 = carve<float4>(2 * (size_t)((Nmax + 15) / 16 + 1));
       act_stride_sm = nx32; act_stride_po = no32;
       act_cnt_sm = carve<int>(nx128); act_list_sm = carve<int>((size_t)nx128 * nx32);
       act_cnt_po = carve<int>(nx128); act_list_po = carve<int>((size_t)nx128 * no32);
@@ -925,8 +927,8 @@ struct Impl final : ImplBase {
         if (cull) {
           const float4* xf = reinterpret_cast<const float4*>(xcs);
           CK_CUDA(launch_tile_spheres(xf, N, 128, sph_o128, st));
-          CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st));
-          CK_CUDA(launch_tile_spheres(xf, N, 16, sph_o16, st));
+          CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st, box_o32));
+          CK_CUDA(launch_tile_spheres(xf, N, 16, sph_o16, st, box_o16));
           CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)matvec_sym_tiles(N) * N * sizeof(T), st));
         }
         // shares > 1: the multi-GPU split (units balanced by active tile pairs), every share in turn into the
@@ -944,7 +946,7 @@ struct Impl final : ImplBase {
           CK_CUDA(launch_matvec_sym(nu2, reinterpret_cast<const float4*>(xcs), N, reinterpret_cast<float*>(partial),
                                     cull ? 0 : U * p / std::max(1, shares), cull ? U : U * (p + 1) / std::max(1, shares),
                                     st, nullptr, cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128,
-                                    sph_o32, kCullCut, k1_sched));
+                                    sph_o32, kCullCut, k1_sched, box_o16, box_o32));
         }
       } else {
         CK_CUDA(launch_matvec_partial<T>(nu2, xcs, N, xcs, N, nch, partial, st));
@@ -1028,8 +1030,8 @@ struct Impl final : ImplBase {
     if (cull && N > 0) {  // spheres of the sorted observation tiles; K2-post lists against them
       const float4* xf = reinterpret_cast<const float4*>(xcs);
       CK_CUDA(launch_tile_spheres(xf, N, 128, sph_o128, st));
-      CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st));
-      CK_CUDA(launch_tile_spheres(xf, N, 16, sph_o16, st));
+      CK_CUDA(launch_tile_spheres(xf, N, 32, sph_o32, st, box_o32));
+      CK_CUDA(launch_tile_spheres(xf, N, 16, sph_o16, st, box_o16));
       CK_CUDA(launch_k2_active(sph_x128 + plo / 128, (int)((NX + 127) / 128), sph_o32, (N + 31) / 32, kCullCut,
                                act_cnt_po, act_list_po, act_stride_po, cull_ctr + 1, st));
       k2_post_dense += (double)((NX + 127) / 128) * ((N + 31) / 32);
@@ -1101,7 +1103,7 @@ struct Impl final : ImplBase {
                                     cull ? 0 : U * rank / world, cull ? U : U * (rank + 1) / world, st,
                                     cull ? cull_ctr : nullptr,
                                     cull ? k1_list : nullptr, k1_count, k1_mask, sph_o16, sph_o128, sph_o32, kCullCut,
-                                    k1_sched));
+                                    k1_sched, box_o16, box_o32));
           if (cull) {
             const double nt = (double)((N + 127) / 128);
             k1_pairs_dense += (double)matvec_sym_blocks_per_tile_pair() * nt * (nt + 1) / 2 / world;   // warp blocks

@@ -24,12 +24,14 @@ int matvec_sym_block_points();       // points per tile block of the symmetric K
 // (sph16) is within cut of the J tile sphere (sph128); the skipped units' partial slots must hold zeros.
 // done_pairs (nullable) accumulates the evaluated 128 x 128 tile pairs.
 // With the 32-column sub-tile test (default; CAKF_K1_SUB=0 for the 128-column one) the warp test uses
-// sph32 (32-point spheres of the observations) and done_pairs counts 16 x 32 blocks.
+// sph32 (32-point spheres of the observations) and done_pairs counts 16 x 32 blocks; box16 / box32
+// (nullable, launch_tile_spheres' boxes of the same tiles) add the bounding-box distance test.
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
                               cudaStream_t st, unsigned long long* done_pairs = nullptr, const int* ulist = nullptr,
                               const int* ucount = nullptr, const unsigned short* umask = nullptr,
                               const float4* sph16 = nullptr, const float4* sph128 = nullptr,
-                              const float4* sph32 = nullptr, float cut = 0.f, unsigned* sched = nullptr);
+                              const float4* sph32 = nullptr, float cut = 0.f, unsigned* sched = nullptr,
+                              const float4* box16 = nullptr, const float4* box32 = nullptr);
 // sched (nullable, 2 zero-initialised counters, one per handle): dynamic unit scheduling (CAKF_K1_DYN=0: off)
 int matvec_sym_blocks_per_tile_pair();   // warp blocks per 128 x 128 tile pair counted by done_pairs
 // list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`, grouped by their
@@ -41,7 +43,8 @@ cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, lon
 cudaError_t launch_k1_balanced_range(const float4* sph, int n, float cut, int rank, int world, long long* urange,
                                      cudaStream_t st);
 // bounding spheres (x, y, z, radius) of consecutive tiles of `tile` points
-cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st);
+// box (nullable): per tile {lo, hi} axis-aligned bounding box, 2 float4 per tile
+cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st, float4* box = nullptr);
 // fp32 exact-zero cut: a prescaled distance above which ex2.approx.ftz(-a log2 e) flushes to 0
 constexpr float kCullCut = 88.0f;
 bool use_sym_k1();  // false if CAKF_K1_DENSE=1

@@ -96,11 +96,12 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
                   unsigned long long* __restrict__ done_pairs, const int* __restrict__ ulist,
                   const int* __restrict__ ucount, const unsigned short* __restrict__ umask,
                   const float4* __restrict__ sph16, const float4* __restrict__ sphJ, float cut,
-                  unsigned* __restrict__ sched) {
+                  unsigned* __restrict__ sched, const float4* __restrict__ box16, const float4* __restrict__ boxJ) {
   griddep_wait();   // PDL: the actions (xcs .w) come from the preceding stage kernel
   constexpr int NJS = SUB ? SYM_S * 4 : SYM_S;   // J spheres per unit
   extern __shared__ __align__(16) unsigned char sm_raw[];
   __shared__ float4 s16[SYM_S * 8], s128[NJS];   // this unit's 16-row group / J (sub-)tile spheres
+  __shared__ float4 b16[SYM_S * 8 * 2], bJ[NJS * 2];   // and their bounding boxes {lo, hi} (SUB)
   __shared__ unsigned s_done;                        // evaluated 16 x 128 warp blocks of this unit
   __shared__ unsigned s_next;                        // dynamic scheduling: this CTA's next work item
   float4* tI = reinterpret_cast<float4*>(sm_raw);                    // [SYM_S][128]
@@ -147,12 +148,24 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
       for (int c = 0; c < 8; ++c) mycol[b * SYM_T + c] = 0.f;
     const float4* sJ = diag ? tI : tJ;
     if (ulist) {
+      // a missing box is the whole space (no constraint beyond the sphere test)
+      const float4 blo = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f), bhi = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
       if (tid < SYM_S * 8) {
         const int g = bi * SYM_S * 8 + tid;
-        s16[tid] = g < (n + 15) / 16 ? sph16[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool in = g < (n + 15) / 16;
+        s16[tid] = in ? sph16[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (SUB) {
+          b16[2 * tid] = in && box16 ? box16[2 * g] : blo;
+          b16[2 * tid + 1] = in && box16 ? box16[2 * g + 1] : bhi;
+        }
       } else if (tid < SYM_S * 8 + NJS) {
         const int t = bj * NJS + tid - SYM_S * 8;
-        s128[tid - SYM_S * 8] = t < (SUB ? (n + 31) / 32 : nt) ? sphJ[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool in = t < (SUB ? (n + 31) / 32 : nt);
+        s128[tid - SYM_S * 8] = in ? sphJ[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (SUB) {
+          bJ[2 * (tid - SYM_S * 8)] = in && boxJ ? boxJ[2 * t] : blo;
+          bJ[2 * (tid - SYM_S * 8) + 1] = in && boxJ ? boxJ[2 * t + 1] : bhi;
+        }
       }
     }
     __syncthreads();
@@ -165,6 +178,28 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
       // rows kept negated (d = c - r) as scalars: the packed f32x2 ops broadcast a scalar operand
       float nrx[8], nry[8], nrz[8], rs[8];
       float2 racc2[8];   // per row: even / odd column partial sums
+      // SUB: the exact-zero test of this warp's 16 rows against all (<= 16) sub-tiles of the unit's J tiles at
+      // once, one sub-tile per lane (lane = 4 b + q4), one ballot: bit 4 b + q4 set = possibly nonzero.
+      // Both tests compare squares (no square root): sphere |c_A - c_B|^2 <= (cut + r_A + r_B)^2 and box
+      // gap^2 <= cut^2 — each a lower bound on every pair distance, so a skipped sub-tile holds exact zeros
+      unsigned act16 = 0u;
+      if constexpr (SUB) {
+        const int lane = tid & 31, b = lane >> 2, q4 = lane & 3;
+        bool on = false;
+        if (b < nbj && b >= (diag ? a : 0) && ((amask >> (a * SYM_S + b)) & 1u)) {
+          on = bj * SYM_S * SYM_T + b * SYM_T + q4 * 32 < n;   // beyond: only padding
+          if (ulist && on) {
+            const float4 A = s16[a * 8 + wg], B = s128[lane];
+            const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z, rr = cut + A.w + B.w;
+            const float4 Al = b16[2 * (a * 8 + wg)], Ah = b16[2 * (a * 8 + wg) + 1], Bl = bJ[2 * lane], Bh = bJ[2 * lane + 1];
+            const float gx = fmaxf(fmaxf(Bl.x - Ah.x, Al.x - Bh.x), 0.f), gy = fmaxf(fmaxf(Bl.y - Ah.y, Al.y - Bh.y), 0.f),
+                        gz = fmaxf(fmaxf(Bl.z - Ah.z, Al.z - Bh.z), 0.f);
+            on = fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= rr * rr && fmaf(gz, gz, fmaf(gy, gy, gx * gx)) <= cut * cut;
+          }
+        }
+        act16 = __ballot_sync(0xffffffffu, on);
+        if (ulist && lane == 0 && act16) atomicAdd(&s_done, (unsigned)__popc(act16));
+      }
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const float4 A = tI[(a * SYM_T / 2 + tyr * 4 + h) * 2], B = tI[(a * SYM_T / 2 + tyr * 4 + h) * 2 + 1];
@@ -181,20 +216,8 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
           // act: sub-tiles of this warp's 16 rows with a possibly nonzero value (warp-uniform).  A fully
           // active J tile runs all four pairs at once; otherwise the active sub-tiles run one by one in
           // the same order, so every accumulator sees the same operation sequence (skipped = exact zeros).
-          unsigned act = 0u;
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const bool live = bj * SYM_S * SYM_T + b * SYM_T + q4 * 32 < n;   // beyond: only padding
-            bool on = live;
-            if (ulist && live) {
-              const float4 A = s16[a * 8 + wg], B = s128[b * 4 + q4];
-              const float ex = A.x - B.x, ey = A.y - B.y, ez = A.z - B.z;
-              on = sqrtf(ex * ex + ey * ey + ez * ez) - A.w - B.w <= cut;
-            }
-            act |= on ? (1u << q4) : 0u;
-          }
+          const unsigned act = (act16 >> (4 * b)) & 0xFu;
           if (!act) continue;
-          if (ulist && (tid & 31) == 0) atomicAdd(&s_done, (unsigned)__popc(act));
           if (act == 0xFu) {
             float2 cx2[4], cy2[4], cz2[4], cs2[4], cacc2[4];
 #pragma unroll
@@ -365,19 +388,44 @@ __global__ void kernel_columns_kernel(const V4<T>* __restrict__ x, int N, const 
 }
 
 // Bounding sphere (center, radius inflated for rounding) of each tile of `tile` consecutive points.
-__global__ void tile_spheres_kernel(const float4* __restrict__ x, int n, int tile, float4* __restrict__ out) {
+// box (nullable): the tile's axis-aligned bounding box {lo, hi} (exact coordinates, .w unused), a second
+// lower bound on the distance between two tiles (the K1 sub-tile test takes the larger of the two)
+__global__ void tile_spheres_kernel(const float4* __restrict__ x, int n, int tile, float4* __restrict__ out,
+                                    float4* __restrict__ box) {
   __shared__ double red[4][32];
+  __shared__ float bred[6][32];
   __shared__ double cen[3];
   const int t0 = blockIdx.x * tile, t1 = min(n, t0 + tile);
   double sx = 0, sy = 0, sz = 0;
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
     const float4 p = x[i];
     sx += p.x; sy += p.y; sz += p.z;
+    lo[0] = fminf(lo[0], p.x); lo[1] = fminf(lo[1], p.y); lo[2] = fminf(lo[2], p.z);
+    hi[0] = fmaxf(hi[0], p.x); hi[1] = fmaxf(hi[1], p.y); hi[2] = fmaxf(hi[2], p.z);
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   sx = warp_sum(sx); sy = warp_sum(sy); sz = warp_sum(sz);
-  if (lane == 0) { red[0][w] = sx; red[1][w] = sy; red[2][w] = sz; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if (lane == 0) {
+    red[0][w] = sx; red[1][w] = sy; red[2][w] = sz;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { bred[c][w] = lo[c]; bred[3 + c][w] = hi[c]; }
+  }
   __syncthreads();
+  if (box && threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { bred[c][0] = fminf(bred[c][0], bred[c][q]); bred[3 + c][0] = fmaxf(bred[3 + c][0], bred[3 + c][q]); }
+    box[2 * blockIdx.x] = make_float4(bred[0][0], bred[1][0], bred[2][0], 0.f);
+    box[2 * blockIdx.x + 1] = make_float4(bred[3][0], bred[4][0], bred[5][0], 0.f);
+  }
   if (threadIdx.x == 0) {
     double a = 0, b = 0, c = 0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { a += red[0][q]; b += red[1][q]; c += red[2][q]; }
@@ -550,9 +598,9 @@ cudaError_t launch_matvec_partial(int nu2, const V4<T>* xr, int nrows, const V4<
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st) {
+cudaError_t launch_tile_spheres(const float4* x, int n, int tile, float4* out, cudaStream_t st, float4* box) {
   if (n <= 0) return cudaSuccess;
-  tile_spheres_kernel<<<(n + tile - 1) / tile, 128, 0, st>>>(x, n, tile, out);
+  tile_spheres_kernel<<<(n + tile - 1) / tile, 128, 0, st>>>(x, n, tile, out, box);
   return note_launch_err();
 }
 
@@ -730,6 +778,11 @@ bool use_k1_dyn() {   // CAKF_K1_DYN=0: static strided unit assignment instead o
   return v;
 }
 
+bool use_k1_box() {   // CAKF_K1_BOX=0: sphere test only (no bounding boxes) for the sub-tiles
+  static const bool v = !env_is("CAKF_K1_BOX", '0');
+  return v;
+}
+
 bool use_k1_sub() {   // CAKF_K1_SUB=0: exact-zero test per 128-column J tile instead of per 32-column sub-tile
   static const bool v = !env_is("CAKF_K1_SUB", '0');
   return v;
@@ -739,7 +792,7 @@ template <int NU2, bool SUB>
 cudaError_t launch_sym_t(const float4* x, int n, int nt, int nb, float* partial, long long u_begin, long long u_end,
                          cudaStream_t st, unsigned long long* done_pairs, const int* ulist, const int* ucount,
                          const unsigned short* umask, const float4* sph16, const float4* sphJ, float cut,
-                         unsigned* sched) {
+                         unsigned* sched, const float4* box16, const float4* boxJ) {
   const size_t smem = (size_t)2 * SYM_S * SYM_T * sizeof(float4) + (size_t)SYM_S * SYM_T * sizeof(float) +
                       (size_t)16 * SYM_S * SYM_T * sizeof(float);
   // resident CTAs per SM (one full wave; the units are strided over it), set up once per device (thread-safe)
@@ -768,14 +821,16 @@ cudaError_t launch_sym_t(const float4* x, int n, int nt, int nb, float* partial,
   const long long grid = std::min<long long>(u_end - u_begin, (long long)num_sms() * per_sm);
   return launch_pdl(matvec_sym_kernel<NU2, SUB>, dim3((unsigned)grid), dim3(256), smem, st, x, n, nt, nb, u_begin,
                     u_end, partial, done_pairs, ulist, ucount, umask, sph16, sphJ, cut,
-                    use_k1_dyn() ? sched : (unsigned*)nullptr);
+                    use_k1_dyn() ? sched : (unsigned*)nullptr, box16, boxJ);
 }
 
 cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, long long u_begin, long long u_end,
                               cudaStream_t st, unsigned long long* done_pairs, const int* ulist,
                               const int* ucount, const unsigned short* umask, const float4* sph16,
-                              const float4* sph128, const float4* sph32, float cut, unsigned* sched) {
+                              const float4* sph128, const float4* sph32, float cut, unsigned* sched,
+                              const float4* box16, const float4* box32) {
   if (n <= 0 || u_end <= u_begin) return cudaSuccess;
+  if (!use_k1_box()) box16 = box32 = nullptr;
   const int nt = (n + SYM_T - 1) / SYM_T;
   const int nb = (nt + SYM_S - 1) / SYM_S;
   const bool sub = use_k1_sub();
@@ -784,9 +839,9 @@ cudaError_t launch_matvec_sym(int nu2, const float4* x, int n, float* partial, l
 #define CAKF_SYM_CASE(NU)                                                                                           \
   case NU:                                                                                                         \
     return sub ? launch_sym_t<NU, true>(x, n, nt, nb, partial, u_begin, u_end, st, done_pairs, ulist, ucount,    \
-                                        umask, sph16, sph32, cut, sched)                                          \
+                                        umask, sph16, sph32, cut, sched, box16, box32)                            \
                : launch_sym_t<NU, false>(x, n, nt, nb, partial, u_begin, u_end, st, done_pairs, ulist, ucount,   \
-                                         umask, sph16, sph128, cut, sched);
+                                         umask, sph16, sph128, cut, sched, nullptr, nullptr);
     CAKF_SYM_CASE(1)
     CAKF_SYM_CASE(3)
     CAKF_SYM_CASE(5)
