@@ -198,7 +198,8 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
           }
         }
         act16 = __ballot_sync(0xffffffffu, on);
-        if (ulist && lane == 0 && act16) atomicAdd(&s_done, (unsigned)__popc(act16));
+        if (!act16) continue;   // nothing of this row tile for this warp (its row sums gain exact zeros only)
+        if (ulist && lane == 0) atomicAdd(&s_done, (unsigned)__popc(act16));
       }
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
@@ -209,7 +210,7 @@ matvec_sym_kernel(const float4* __restrict__ x, int n, int nt, int nb, long long
 #pragma unroll
       for (int q = 0; q < 8; ++q) racc2[q] = make_float2(0.f, 0.f);
       for (int b = diag ? a : 0; b < nbj; ++b) {
-        if (!((amask >> (a * SYM_S + b)) & 1u)) continue;   // every value of this tile pair is exactly 0
+        if (SUB ? !((act16 >> (4 * b)) & 0xFu) : !((amask >> (a * SYM_S + b)) & 1u)) continue;   // all exact zeros
         const bool offdiag = !(diag && a == b);
         if constexpr (SUB) {
           // 4 sub-tiles of 32 columns; lane tx owns the packed column pairs q4*32 + 2tx, +1 (q4 < 4).
