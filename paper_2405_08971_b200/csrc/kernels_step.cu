@@ -26,6 +26,58 @@ constexpr int kTile = 128;
 // out[j] = sum_{rows of this tile} A[row + j*ld] * v[row]: each lane owns 4 rows; 8 columns per warp pass
 // (32 independent loads in flight per lane), lane sums fp32/fp64, cross-lane sums fp64 by a multi-value
 // butterfly (9 shuffles for 8 columns)
+// the butterfly: 8 -> 4 -> 2 -> 1 values per lane, then a 4-lane sum; lane holds column
+// ((l>>4)&1)*4+((l>>3)&1)*2+((l>>2)&1); lanes with (l & 3) == 0 store it
+__device__ __forceinline__ void cols8_store(const double (&w8)[8], int j, int ncols, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  double w4[4], w2[2];
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double send = h16 ? w8[c] : w8[c + 4], keep = h16 ? w8[c + 4] : w8[c];
+    w4[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double send = h8 ? w4[c] : w4[c + 2], keep = h8 ? w4[c + 2] : w4[c];
+    w2[c] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double t = (h4 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? w2[0] : w2[1], 4);
+  t += __shfl_xor_sync(0xffffffffu, t, 2);
+  t += __shfl_xor_sync(0xffffffffu, t, 1);
+  const int col = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+  if ((lane & 3) == 0 && j + col < ncols) out[j + col] = t;
+}
+
+// fp32, ld % 4 == 0, 16-byte aligned A and v: each lane owns 4 consecutive rows (one 16-byte load per column),
+// 8 columns per warp pass — a quarter of the load instructions of the scalar form (the MIO queue is shared
+// with K1's MUFU and shared-memory traffic when this runs beside it on the side stream)
+__device__ void tile_cols_dot_v4(const float* __restrict__ A, size_t ld, int ncols, const float* __restrict__ v, int r0,
+                                 int r1, double* __restrict__ out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int row = r0 + 4 * lane;
+  const bool in = row < r1;   // r1 - r0 is a multiple of 4
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 x = in ? *reinterpret_cast<const float4*>(v + row) : z4;
+  const int rr = in ? row : r0;
+  for (int j = warp * 8; j < ncols; j += nw * 8) {
+    float4 xv[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      xv[c] = j + c < ncols ? __ldg(reinterpret_cast<const float4*>(A + (size_t)(j + c) * ld + rr)) : z4;
+    double w8[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float acc = fmaf(xv[c].x, x.x, 0.f);
+      acc = fmaf(xv[c].y, x.y, acc);
+      acc = fmaf(xv[c].z, x.z, acc);
+      acc = fmaf(xv[c].w, x.w, acc);
+      w8[c] = (double)acc;
+    }
+    cols8_store(w8, j, ncols, out);
+  }
+}
+
 template <typename T>
 __device__ void tile_cols_dot(const T* __restrict__ A, size_t ld, int ncols, const T* __restrict__ v, int r0, int r1,
                               double* __restrict__ out) {
@@ -33,6 +85,12 @@ __device__ void tile_cols_dot(const T* __restrict__ A, size_t ld, int ncols, con
   if (r1 <= r0) {
     for (int j = threadIdx.x; j < ncols; j += blockDim.x) out[j] = 0.0;
     return;
+  }
+  if constexpr (sizeof(T) == 4) {
+    if ((ld & 3) == 0 && ((((uintptr_t)A) | ((uintptr_t)v)) & 15) == 0 && (r0 & 3) == 0 && blockDim.x <= 128) {
+      tile_cols_dot_v4(A, ld, ncols, v, r0, r1, out);
+      return;
+    }
   }
   T x[4];
   int rr[4];
@@ -278,6 +336,46 @@ hmu_kernel(int N, const T* __restrict__ HM, int rin, const double* __restrict__ 
   __syncthreads();
   const int row = blockIdx.x * kTile + threadIdx.x;
   if (row < N) w[row] = row_gemv(HM, (size_t)N, rin, u, row);
+}
+
+// hmu with 4 consecutive rows per thread (one 16-byte load per column; fp32, N % 4 == 0, 16-byte aligned HM):
+// 512 rows per block; every row's fp64 accumulation is row_gemv's (columns ascending, column j into
+// acc[j & 3] below the last multiple of 8, the tail into acc[0]), so w is the same bits
+template <int MINB>
+__global__ void __launch_bounds__(kTile, MINB)
+hmu4_kernel(int N, const float* __restrict__ HM, int rin, const double* __restrict__ ured, double* __restrict__ w) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  double* u = reinterpret_cast<double*>(sm_raw);
+  for (int j = threadIdx.x; j < rin; j += blockDim.x) u[j] = ured[j];
+  __syncthreads();
+  const int row = (blockIdx.x * kTile + threadIdx.x) * 4;
+  if (row >= N) return;
+  double acc[4][4] = {};
+  const int n8 = rin & ~7;
+  int j = 0;
+  for (; j < n8; j += 8) {
+    float4 x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = __ldg(reinterpret_cast<const float4*>(HM + row + (size_t)(j + q) * N));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double c = u[j + q];
+      acc[0][q & 3] = fma((double)x[q].x, c, acc[0][q & 3]);
+      acc[1][q & 3] = fma((double)x[q].y, c, acc[1][q & 3]);
+      acc[2][q & 3] = fma((double)x[q].z, c, acc[2][q & 3]);
+      acc[3][q & 3] = fma((double)x[q].w, c, acc[3][q & 3]);
+    }
+  }
+  for (; j < rin; ++j) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(HM + row + (size_t)j * N));
+    const double c = u[j];
+    acc[0][0] = fma((double)x.x, c, acc[0][0]);
+    acc[1][0] = fma((double)x.y, c, acc[1][0]);
+    acc[2][0] = fma((double)x.z, c, acc[2][0]);
+    acc[3][0] = fma((double)x.w, c, acc[3][0]);
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) w[row + e] = (acc[e][0] + acc[e][1]) + (acc[e][2] + acc[e][3]);
 }
 
 // ------------------------------------------------------------------ stage B
@@ -1003,6 +1101,16 @@ cudaError_t StepKernels<T>::hmts(int N, const T* HM, int rin, const T* s, double
 template <typename T>
 cudaError_t StepKernels<T>::hmu(int N, const T* HM, int rin, const double* ured, double* w, cudaStream_t st) {
   if (rin <= 0 || N <= 0) return cudaSuccess;
+  if constexpr (sizeof(T) == 4) {
+    if ((N & 3) == 0 && ((uintptr_t)HM & 15) == 0) {
+      const int nb = (N / 4 + kTile - 1) / kTile;
+      if (side_slim())
+        hmu4_kernel<6><<<nb, kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
+      else
+        hmu4_kernel<1><<<nb, kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
+      return note_launch_err();
+    }
+  }
   if (side_slim())
     hmu_kernel<T, 6><<<stage_blocks(N), kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
   else
