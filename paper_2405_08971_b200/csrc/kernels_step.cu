@@ -149,6 +149,111 @@ __device__ void tile_cols_dot(const T* __restrict__ A, size_t ld, int ncols, con
   }
 }
 
+// fp32, ld % 4 == 0, 16-byte aligned V and Z: rows [r0, r1) of V c and Z c in fp64 with 16-byte loads — lane
+// owns 4 consecutive rows, warp w the columns j = w (mod 4) in ascending order; the warp partials go to
+// sv / sz [4 warps][128 rows] (shared), summed per row in warp order by the caller after a barrier
+__device__ void tile_rows_gemv2_v4(const float* __restrict__ V, const float* __restrict__ Z, size_t ld, int ncols,
+                                   const double* c, int r0, int r1, double* sv, double* sz) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = r0 + 4 * lane;
+  const int rr = row < r1 ? row : r0;
+  double av[4] = {0.0, 0.0, 0.0, 0.0}, az[4] = {0.0, 0.0, 0.0, 0.0};
+  int j = warp;
+  for (; j + 12 < ncols; j += 16) {
+    float4 xv[4], xz[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      xv[q] = __ldg(reinterpret_cast<const float4*>(V + (size_t)(j + 4 * q) * ld + rr));
+      xz[q] = __ldg(reinterpret_cast<const float4*>(Z + (size_t)(j + 4 * q) * ld + rr));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double cj = c[j + 4 * q];
+      av[0] = fma((double)xv[q].x, cj, av[0]); av[1] = fma((double)xv[q].y, cj, av[1]);
+      av[2] = fma((double)xv[q].z, cj, av[2]); av[3] = fma((double)xv[q].w, cj, av[3]);
+      az[0] = fma((double)xz[q].x, cj, az[0]); az[1] = fma((double)xz[q].y, cj, az[1]);
+      az[2] = fma((double)xz[q].z, cj, az[2]); az[3] = fma((double)xz[q].w, cj, az[3]);
+    }
+  }
+  for (; j < ncols; j += 4) {
+    const float4 xv = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ld + rr));
+    const float4 xz = __ldg(reinterpret_cast<const float4*>(Z + (size_t)j * ld + rr));
+    const double cj = c[j];
+    av[0] = fma((double)xv.x, cj, av[0]); av[1] = fma((double)xv.y, cj, av[1]);
+    av[2] = fma((double)xv.z, cj, av[2]); av[3] = fma((double)xv.w, cj, av[3]);
+    az[0] = fma((double)xz.x, cj, az[0]); az[1] = fma((double)xz.y, cj, az[1]);
+    az[2] = fma((double)xz.z, cj, az[2]); az[3] = fma((double)xz.w, cj, az[3]);
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    sv[warp * kTile + 4 * lane + e] = av[e];
+    sz[warp * kTile + 4 * lane + e] = az[e];
+  }
+}
+
+// fp32, N % 4 == 0, 16-byte aligned partial: sum over the nch K1 partial slots of rows [r0, r1) with 16-byte
+// loads — lane owns 4 consecutive rows, warp w the slots c = w (mod 4) ascending (fp64); the warp partials go
+// to sk [4 warps][128 rows] (shared), summed per row in warp order by the caller after a barrier
+__device__ void tile_slots_sum_v4(const float* __restrict__ partial, int N, int nch, int r0, int r1, double* sk) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = r0 + 4 * lane;
+  const int rr = row < r1 ? row : r0;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  int c = warp;
+  for (; c + 28 < nch; c += 32) {
+    float4 x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = __ldg(reinterpret_cast<const float4*>(partial + (size_t)(c + 4 * q) * N + rr));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      a[0] += (double)x[q].x; a[1] += (double)x[q].y; a[2] += (double)x[q].z; a[3] += (double)x[q].w;
+    }
+  }
+  for (; c < nch; c += 4) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(partial + (size_t)c * N + rr));
+    a[0] += (double)x.x; a[1] += (double)x.y; a[2] += (double)x.z; a[3] += (double)x.w;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) sk[warp * kTile + 4 * lane + e] = a[e];
+}
+
+// the K1 row sums of this block's rows: the 16-byte-load form when it applies (same in stage A and stage AB,
+// so the two stay bit-identical), else per row with 32 loads in flight
+template <typename T>
+__device__ __forceinline__ double tile_ksum(const T* __restrict__ partial, int N, int nch, int r0, int r1) {
+  const int row = r0 + threadIdx.x;
+  if constexpr (sizeof(T) == 4) {
+    if ((N & 3) == 0 && ((uintptr_t)partial & 15) == 0 && blockDim.x == kTile) {
+      __shared__ double sk[4 * kTile];
+      tile_slots_sum_v4(partial, N, nch, r0, r1, sk);
+      __syncthreads();
+      const int t = threadIdx.x;
+      return (sk[t] + sk[kTile + t]) + (sk[2 * kTile + t] + sk[3 * kTile + t]);
+    }
+  }
+  if (row >= r1) return 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int c = 0;
+  // 32 loads in flight per thread, then one 16-batch and the scalar tail: each acc[j] sees
+  // partial[c + j], partial[c + j + 4], ... in the same order as with 16-batches alone
+  for (; c + 32 <= nch; c += 32) {
+    T x[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) x[q] = partial[(size_t)(c + q) * N + row];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q & 3] += (double)x[q];
+  }
+  for (; c + 16 <= nch; c += 16) {
+    T x[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = partial[(size_t)(c + q) * N + row];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q & 3] += (double)x[q];
+  }
+  for (; c < nch; ++c) acc[0] += (double)partial[(size_t)c * N + row];
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
 // sum_j A[row + j*ld] c[j] in fp64 (c in shared memory); 16 independent loads in flight per thread
 template <typename T>
 __device__ __forceinline__ double row_gemv(const T* __restrict__ A, size_t ld, int ncols, const double* c, int row) {
@@ -272,27 +377,8 @@ stageA_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const
   __shared__ double scratch[32 * 3];
   const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[3] = {0.0, 0.0, 0.0};  // s.r, s.g', r.r
+  const double ksum = tile_ksum(partial, N, nch, r0, r1);
   if (row < r1) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int c = 0;
-    // 32 loads in flight per thread, then one 16-batch and the scalar tail: each acc[j] sees
-    // partial[c + j], partial[c + j + 4], ... in the same order as with 16-batches alone
-    for (; c + 32 <= nch; c += 32) {
-      T x[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) x[q] = partial[(size_t)(c + q) * N + row];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) acc[q & 3] += (double)x[q];
-    }
-    for (; c + 16 <= nch; c += 16) {
-      T x[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) x[q] = partial[(size_t)(c + q) * N + row];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q & 3] += (double)x[q];
-    }
-    for (; c < nch; ++c) acc[0] += (double)partial[(size_t)c * N + row];
-    const double ksum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     const T si = s[row], ri = r[row];
     const T g = (T)(sig00 * ksum) + lam2[row] * si;
     gp[row] = g;
@@ -424,25 +510,8 @@ stageAB_kernel(int N, int nch, const T* __restrict__ partial, double sig00, cons
   __shared__ double scratch[32 * 4];
   const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[4] = {0.0, 0.0, 0.0, 0.0};   // s.g, s.r, s.g', r.r
+  const double ksum = tile_ksum(partial, N, nch, r0, r1);
   if (row < r1) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int c = 0;
-    for (; c + 32 <= nch; c += 32) {
-      T x[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) x[q] = partial[(size_t)(c + q) * N + row];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) acc[q & 3] += (double)x[q];
-    }
-    for (; c + 16 <= nch; c += 16) {
-      T x[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) x[q] = partial[(size_t)(c + q) * N + row];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q & 3] += (double)x[q];
-    }
-    for (; c < nch; ++c) acc[0] += (double)partial[(size_t)c * N + row];
-    const double ksum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     const T si = s[row], ri = r[row];
     const T gpv = (T)(sig00 * ksum) + lam2[row] * si;                // g'  (stage A)
     const T gi = wpre ? (T)((double)gpv - wpre[row]) : gpv;          // G s (stage B)
@@ -483,9 +552,26 @@ stageC_kernel(int N, const T* __restrict__ V, const T* __restrict__ Z, int nV, c
   __syncthreads();
   const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[1] = {0.0};
+  double vc = 0.0, zc = 0.0;   // (V c)[row], (Z c)[row]
+  bool v4 = false;
+  if constexpr (sizeof(T) == 4) {
+    if ((N & 3) == 0 && ((((uintptr_t)V) | ((uintptr_t)Z)) & 15) == 0 && blockDim.x == kTile) {
+      __shared__ double sv[4 * kTile], sz[4 * kTile];
+      tile_rows_gemv2_v4(V, Z, (size_t)N, nV, c, r0, r1, sv, sz);
+      __syncthreads();
+      const int t = threadIdx.x;
+      vc = (sv[t] + sv[kTile + t]) + (sv[2 * kTile + t] + sv[3 * kTile + t]);
+      zc = (sz[t] + sz[kTile + t]) + (sz[2 * kTile + t] + sz[3 * kTile + t]);
+      v4 = true;
+    }
+  }
   if (row < r1) {
-    const double dv = (double)sin[row] - row_gemv(V, (size_t)N, nV, c, row);   // d = (I - V V^T G) s  (line 11)
-    const double gd = (double)gin[row] - row_gemv(Z, (size_t)N, nV, c, row);   // G d = G s - Z c
+    if (!v4) {
+      vc = row_gemv(V, (size_t)N, nV, c, row);
+      zc = row_gemv(Z, (size_t)N, nV, c, row);
+    }
+    const double dv = (double)sin[row] - vc;   // d = (I - V V^T G) s  (line 11)
+    const double gd = (double)gin[row] - zc;   // G d = G s - Z c
     d[row] = (T)dv;
     Gd[row] = (T)gd;
     a[0] = (double)s_eta[row] * gd;                               // eta = s^T G d        (line 12)
