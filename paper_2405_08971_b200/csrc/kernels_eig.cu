@@ -179,25 +179,24 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
     double* cg_ = a.colglob + (size_t)par * c;
     double* pbp = pb + (size_t)par * ld;
     const double tj = red[40 + par];
-    // ---- (a) fused pass: column pairs (lcA, lcA + 1) per warp, row pairs per lane
+    // ---- (a) fused pass: one column per warp (two when more than 32 are live: only while j < 16 (c - 32)),
+    // row pairs per lane — with the live columns shrinking to (c - j) / NC, one column per warp keeps twice
+    // the warps busy of the earlier column-pair form
     const int lc0 = q > j ? 0 : (j - q) / NC + 1;   // first local column with i > j
     const int r0 = (j + 1) & ~1;                     // first row pair (row j is dead: v_j[j] = 0)
     double sq = 0.0;
-    for (int lcA = lc0 + 2 * warp; lcA < nloc; lcA += 2 * nwarps) {
-      const bool hasB = lcA + 1 < nloc;
-      const int iA = q + NC * lcA, iB = iA + NC;
+    for (int lcA = lc0 + warp; lcA < nloc; lcA += nwarps) {
+      const int iA = q + NC * lcA;
       double* colA = A + (size_t)lcA * ld;
-      double* colB = A + (size_t)(lcA + 1) * ld;
       const double vpA = vprev[iA], wpA = wprev[iA];
-      const double vpB = hasB ? vprev[iB] : 0.0, wpB = hasB ? wprev[iB] : 0.0;
-      const bool pubA = iA == j + 1, pubB = hasB && iB == j + 1;
-      double accA = 0.0, accB = 0.0;
+      const bool pubA = iA == j + 1;
+      double accA = 0.0;
       for (int r = r0 + 2 * lane; r < c; r += 64) {
-        const double2 vp = *reinterpret_cast<const double2*>(vprev + r);
-        const double2 wp = *reinterpret_cast<const double2*>(wprev + r);
         const double2 vv = *reinterpret_cast<const double2*>(vj + r);
         double2 xa = *reinterpret_cast<double2*>(colA + r);
         if (j > 0) {
+          const double2 vp = *reinterpret_cast<const double2*>(vprev + r);
+          const double2 wp = *reinterpret_cast<const double2*>(wprev + r);
           xa.x -= vp.x * wpA + wp.x * vpA;
           xa.y -= vp.y * wpA + wp.y * vpA;
           *reinterpret_cast<double2*>(colA + r) = xa;
@@ -207,34 +206,13 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
           if (r >= j + 1) cg_[r] = xa.x;
           if (r + 1 < c) cg_[r + 1] = xa.y;
         }
-        if (hasB) {
-          double2 xb2 = *reinterpret_cast<double2*>(colB + r);
-          if (j > 0) {
-            xb2.x -= vp.x * wpB + wp.x * vpB;
-            xb2.y -= vp.y * wpB + wp.y * vpB;
-            *reinterpret_cast<double2*>(colB + r) = xb2;
-          }
-          accB += xb2.x * vv.x + xb2.y * vv.y;
-          if (pubB) {
-            if (r >= j + 1) cg_[r] = xb2.x;
-            if (r + 1 < c) cg_[r + 1] = xb2.y;
-          }
-        }
       }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        accA += __shfl_xor_sync(0xffffffffu, accA, off);
-        accB += __shfl_xor_sync(0xffffffffu, accB, off);
-      }
+      for (int off = 16; off > 0; off >>= 1) accA += __shfl_xor_sync(0xffffffffu, accA, off);
       if (lane == 0) {
         const double pA = tj * accA;
         pbp[iA] = pA;
         sq += pA * vj[iA];
-        if (hasB) {
-          const double pB = tj * accB;
-          pbp[iB] = pB;
-          sq += pB * vj[iB];
-        }
       }
     }
     TRD_T(0)
