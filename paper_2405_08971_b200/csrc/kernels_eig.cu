@@ -4,8 +4,9 @@
 //   1. Householder tridiagonalisation  C = H T H^T  in ONE thread-block cluster (16 CTAs; the matrix
 //      resident in their shared memory for c <= ~600, else in L2-resident global memory), one cluster
 //      barrier per column: every CTA owns whole columns (cyclically); the rank-2 update of step j is
-//      fused into the matvec pass of step j+1; p is exchanged through distributed shared memory and the
-//      next column through L2; every CTA then computes the next reflector itself.
+//      fused into the matvec pass of step j+1; p and the partial dots are pushed into every CTA's shared
+//      memory (DSMEM stores before the barrier), the next column goes through L2; every CTA then computes
+//      the next reflector itself.
 //   2. Cuppen divide and conquer on T (leaves of size 1, six launches per level): rank-one merges with
 //      deflation (negligible weight; close poles by Givens rotation), the secular equation per root by a
 //      safeguarded two-pole rational iteration in the distance to the nearer pole, Gu-Eisenstat
@@ -36,6 +37,7 @@ namespace {
 constexpr int kTrdThreads = 1024;
 constexpr int kTrdCluster = 16;
 constexpr int kTrdSmemBytes = 227 * 1024;
+constexpr int kTrdRed = 96;   // doubles of the tridiagonalisation's reduction / exchange scratch
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -78,7 +80,8 @@ struct TrdArgs {
 //               apply update(j-1) (A -= v w^T + w v^T) to the rows > j and form p_i = tau_j A[:, i] . v_j into
 //               my shared memory; the owner of column j+1 also publishes that column (post update(j-1)) in L2;
 //           (b) cluster barrier;
-//           (c) every CTA reads p (DSMEM, from the column owners), the partial dots (DSMEM) and column j+1 (L2),
+//           (c) every CTA finds p and the partial dots in its own shared memory (pushed by their owners over
+//               DSMEM during (a)), reads column j+1 (L2),
 //               forms w_j, applies update(j) to column j+1 and computes reflector j+1 itself (identical
 //               arithmetic in every CTA, no second barrier).
 // Layout: local columns with an even stride ldA >= c + 1 (the rows in [c, ldA) and the row entries of v / w
@@ -96,10 +99,9 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
   double* A = SMEM ? sm : a.Aglob + (size_t)q * L * ld;
   double* vb = SMEM ? sm + (size_t)L * ld : sm;   // [2][ld]  v_j by step parity
   double* wb = vb + 2 * (size_t)ld;                // [2][ld]  w_j by step parity
-  double* pb = wb + 2 * (size_t)ld;                // [2][ld]  p_i of my columns by step parity (read by the cluster)
-  double* prw = pb + 2 * (size_t)ld;               // [ld]     p of every row (gathered)
-  double* xb = prw + (size_t)ld;                   // [ld]     column j+1
-  double* red = xb + (size_t)ld;                   // [64]     red[36 + parity] = my partial dot, red[40 + parity] = tau_j
+  double* pb = wb + 2 * (size_t)ld;                // [2][ld]  p of every row by step parity (pushed by the column owners)
+  double* xb = pb + 3 * (size_t)ld;                // [ld]     column j+1 (one spare ld before it)
+  double* red = xb + (size_t)ld;                   // [kTrdRed] red[40 + parity] = tau_j, red[48 + 16 parity + q] = CTA q's partial dot
   const int nloc = q < c ? (c - q + NC - 1) / NC : 0;   // my columns i = q + NC * lc
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, bd = blockDim.x;
   const bool writer = q == 0;
@@ -209,32 +211,29 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) accA += __shfl_xor_sync(0xffffffffu, accA, off);
-      if (lane == 0) {
-        const double pA = tj * accA;
-        pbp[iA] = pA;
-        sq += pA * vj[iA];
-      }
+      // p_i into every CTA's p buffer of this parity (DSMEM push, lane q -> CTA q; visible after the barrier;
+      // staging p locally and pushing with the whole CTA after the pass measured slower, r4t)
+      const double pA = tj * accA;
+      if (lane < NC) cl.map_shared_rank(pbp, lane)[iA] = pA;
+      if (lane == 0) sq += pA * vj[iA];
     }
     TRD_T(0)
     if (lane == 0) red[warp] = sq;
     __syncthreads();
     TRD_T(1)
-    if (warp == 0) {
+    if (warp == 0) {   // my partial dot into every CTA's slot q of this parity
       double t = lane < nwarps ? red[lane] : 0.0;
       t = warp_sum_d(t);
-      if (lane == 0) red[36 + par] = t;
+      if (lane < NC) cl.map_shared_rank(red, lane)[48 + 16 * par + q] = t;
     }
     // ---- (b)
     cl.sync();
     TRD_T(2)
-    // ---- (c) p from the column owners (DSMEM), column j+1 (L2), the partial dots (DSMEM, warp 0)
-    for (int l = j + 1 + tid; l < c; l += bd) {
-      prw[l] = cl.map_shared_rank(pbp, l % NC)[l];
-      xb[l] = __ldcg(cg_ + l);
-    }
+    // ---- (c) p and the partial dots are local (pushed before the barrier); column j+1 from L2
+    const double* prw = pbp;
+    for (int l = j + 1 + tid; l < c; l += bd) xb[l] = __ldcg(cg_ + l);
     if (warp == 0) {
-      double t = 0.0;
-      if (lane < NC) t = cl.map_shared_rank(red, lane)[36 + par];
+      double t = lane < NC ? red[48 + 16 * par + lane] : 0.0;
       t = warp_sum_d(t);
       if (lane == 0) red[35] = t;
     }
@@ -873,7 +872,7 @@ int trd_smem_max_c(int nc) {
   for (int c = 1; c <= 4096; ++c) {
     const size_t L = (c + nc - 1) / nc;
     const size_t ld = trd_ld(c);
-    const size_t bytes = (L * ld + 8 * ld + 64) * sizeof(double);
+    const size_t bytes = (L * ld + 8 * ld + kTrdRed) * sizeof(double);
     if (bytes <= (size_t)kTrdSmemBytes) best = c;
   }
   return best;
@@ -970,7 +969,7 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
     const size_t L = (c + nc - 1) / nc;
     const bool in_smem = c <= (nc == 16 ? smem_max_c16 : smem_max_c8);
     const size_t ldt = trd_ld(c);
-    const size_t smem = in_smem ? (L * ldt + 8 * ldt + 64) * sizeof(double) : (8 * ldt + 64) * sizeof(double);
+    const size_t smem = in_smem ? (L * ldt + 8 * ldt + kTrdRed) * sizeof(double) : (8 * ldt + kTrdRed) * sizeof(double);
     if (smem > (size_t)kTrdSmemBytes) return cudaErrorInvalidValue;
     static PerDeviceOnce once;
     const cudaError_t ce = once_per_device(once, [] {
