@@ -60,7 +60,30 @@ __device__ void tile_cols_dot_v4(const float* __restrict__ A, size_t ld, int nco
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4 x = in ? *reinterpret_cast<const float4*>(v + row) : z4;
   const int rr = in ? row : r0;
-  for (int j = warp * 8; j < ncols; j += nw * 8) {
+  int j = warp * 8;
+  for (; j + nw * 8 < ncols; j += 2 * nw * 8) {   // two 8-column groups per pass: 16 loads in flight per lane
+    const int j2 = j + nw * 8;
+    float4 xv[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      xv[c] = j + c < ncols ? __ldg(reinterpret_cast<const float4*>(A + (size_t)(j + c) * ld + rr)) : z4;
+      xv[8 + c] = j2 + c < ncols ? __ldg(reinterpret_cast<const float4*>(A + (size_t)(j2 + c) * ld + rr)) : z4;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double w8[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float acc = fmaf(xv[8 * h + c].x, x.x, 0.f);
+        acc = fmaf(xv[8 * h + c].y, x.y, acc);
+        acc = fmaf(xv[8 * h + c].z, x.z, acc);
+        acc = fmaf(xv[8 * h + c].w, x.w, acc);
+        w8[c] = (double)acc;
+      }
+      cols8_store(w8, h ? j2 : j, ncols, out);
+    }
+  }
+  for (; j < ncols; j += nw * 8) {
     float4 xv[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c)
@@ -159,6 +182,22 @@ __device__ void tile_rows_gemv2_v4(const float* __restrict__ V, const float* __r
   const int rr = row < r1 ? row : r0;
   double av[4] = {0.0, 0.0, 0.0, 0.0}, az[4] = {0.0, 0.0, 0.0, 0.0};
   int j = warp;
+  for (; j + 28 < ncols; j += 32) {   // 16 loads in flight per lane
+    float4 xv[8], xz[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      xv[q] = __ldg(reinterpret_cast<const float4*>(V + (size_t)(j + 4 * q) * ld + rr));
+      xz[q] = __ldg(reinterpret_cast<const float4*>(Z + (size_t)(j + 4 * q) * ld + rr));
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double cj = c[j + 4 * q];
+      av[0] = fma((double)xv[q].x, cj, av[0]); av[1] = fma((double)xv[q].y, cj, av[1]);
+      av[2] = fma((double)xv[q].z, cj, av[2]); av[3] = fma((double)xv[q].w, cj, av[3]);
+      az[0] = fma((double)xz[q].x, cj, az[0]); az[1] = fma((double)xz[q].y, cj, az[1]);
+      az[2] = fma((double)xz[q].z, cj, az[2]); az[3] = fma((double)xz[q].w, cj, az[3]);
+    }
+  }
   for (; j + 12 < ncols; j += 16) {
     float4 xv[4], xz[4];
 #pragma unroll
@@ -200,6 +239,15 @@ __device__ void tile_slots_sum_v4(const float* __restrict__ partial, int N, int 
   const int rr = row < r1 ? row : r0;
   double a[4] = {0.0, 0.0, 0.0, 0.0};
   int c = warp;
+  for (; c + 60 < nch; c += 64) {   // 16 loads in flight per lane
+    float4 x[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = __ldg(reinterpret_cast<const float4*>(partial + (size_t)(c + 4 * q) * N + rr));
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      a[0] += (double)x[q].x; a[1] += (double)x[q].y; a[2] += (double)x[q].z; a[3] += (double)x[q].w;
+    }
+  }
   for (; c + 28 < nch; c += 32) {
     float4 x[8];
 #pragma unroll
