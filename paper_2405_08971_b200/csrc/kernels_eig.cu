@@ -37,7 +37,8 @@ namespace {
 constexpr int kTrdThreads = 1024;
 constexpr int kTrdCluster = 16;
 constexpr int kTrdSmemBytes = 227 * 1024;
-constexpr int kTrdRed = 96;   // doubles of the tridiagonalisation's reduction / exchange scratch
+constexpr int kTrdRed = 96;
+constexpr int kTrdReflWarps = 4;   // warps computing the next reflector while the others apply the rank-2 update   // doubles of the tridiagonalisation's reduction / exchange scratch
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -76,14 +77,14 @@ struct TrdArgs {
 
 
 // Householder tridiagonalisation in one cluster of NC CTAs, ONE cluster barrier per step:
-//   step j: (a) fused pass over my columns i > j (two columns per warp, two rows per lane as double2):
-//               apply update(j-1) (A -= v w^T + w v^T) to the rows > j and form p_i = tau_j A[:, i] . v_j into
-//               my shared memory; the owner of column j+1 also publishes that column (post update(j-1)) in L2;
+//   step j: (a) pass over my columns i > j (one column per warp, two rows per lane as double2): form
+//               p_i = tau_j A[:, i] . v_j (update(j-1) was applied in step j-1) and push it to every CTA; the
+//               owner of column j+1 also publishes that column in L2;
 //           (b) cluster barrier;
 //           (c) every CTA finds p and the partial dots in its own shared memory (pushed by their owners over
-//               DSMEM during (a)), reads column j+1 (L2),
-//               forms w_j, applies update(j) to column j+1 and computes reflector j+1 itself (identical
-//               arithmetic in every CTA, no second barrier).
+//               DSMEM during (a)), reads column j+1 (L2), forms w_j and applies update(j) to column j+1; then
+//               the first warps compute reflector j+1 (identical arithmetic in every CTA, no second cluster
+//               barrier) while the other warps apply update(j) to the CTA's columns i > j+1.
 // Layout: local columns with an even stride ldA >= c + 1 (the rows in [c, ldA) and the row entries of v / w
 // at and above c are zero), so the double2 pass may start one row early and run one row past the end.
 // Reflector convention (LAPACK dlarfg): H = I - tau v v^T, H x = beta e_1, v[j+1] = 1, v[j] = 0.
@@ -155,6 +156,34 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
       }
     }
   };
+  // the same reflector run by the first nthr threads only, with red[0, nwarps) already holding the warps'
+  // partial sums of sum_{l >= jr+2} x_l^2 (identical arithmetic: same partials, same reductions)
+  auto reflector_part = [&](int jr, const double* xs, double dj, double* vout, int nthr) {
+    double t = lane < nwarps ? red[lane] : 0.0;
+    t = warp_sum_d(t);
+    const double alpha = xs[jr + 1];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (t > 0.0) {
+      const double nrm = sqrt(alpha * alpha + t);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int l = jr + 1 + tid; l < c; l += nthr) {
+      const double v = l == jr + 1 ? 1.0 : xs[l] * scal;
+      vout[l] = v;
+      if (writer) a.V[l + (size_t)jr * c] = v;
+    }
+    if (tid == 0) {
+      vout[jr] = 0.0;
+      red[40 + (jr & 1)] = tau;
+      if (writer) {
+        a.tau[jr] = tau;
+        a.d[jr] = dj;
+        a.e[jr] = beta;
+      }
+    }
+  };
   __syncthreads();
   for (int l = tid; l < c; l += bd) xb[l] = a.G[l];   // column 0 of G: no update yet
   __syncthreads();
@@ -175,8 +204,6 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
   for (int j = 0; j + 3 <= c; ++j) {
     const int par = j & 1;
     const double* vj = vb + (size_t)par * ld;
-    const double* vprev = vb + (size_t)(par ^ 1) * ld;
-    const double* wprev = wb + (size_t)(par ^ 1) * ld;
     double* wj = wb + (size_t)par * ld;
     double* cg_ = a.colglob + (size_t)par * c;
     double* pbp = pb + (size_t)par * ld;
@@ -189,20 +216,12 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
     double sq = 0.0;
     for (int lcA = lc0 + warp; lcA < nloc; lcA += nwarps) {
       const int iA = q + NC * lcA;
-      double* colA = A + (size_t)lcA * ld;
-      const double vpA = vprev[iA], wpA = wprev[iA];
+      const double* colA = A + (size_t)lcA * ld;   // update(j-1) already applied (step j-1, beside its reflector)
       const bool pubA = iA == j + 1;
       double accA = 0.0;
       for (int r = r0 + 2 * lane; r < c; r += 64) {
         const double2 vv = *reinterpret_cast<const double2*>(vj + r);
-        double2 xa = *reinterpret_cast<double2*>(colA + r);
-        if (j > 0) {
-          const double2 vp = *reinterpret_cast<const double2*>(vprev + r);
-          const double2 wp = *reinterpret_cast<const double2*>(wprev + r);
-          xa.x -= vp.x * wpA + wp.x * vpA;
-          xa.y -= vp.y * wpA + wp.y * vpA;
-          *reinterpret_cast<double2*>(colA + r) = xa;
-        }
+        const double2 xa = *reinterpret_cast<const double2*>(colA + r);
         accA += xa.x * vv.x + xa.y * vv.y;
         if (pubA) {
           if (r >= j + 1) cg_[r] = xa.x;
@@ -251,9 +270,31 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
     }
     if (j + 4 <= c) {
       TRD_T(4)
-      // (the reflector's own barrier orders these rows before its reads of other threads' rows)
-      // dj = x_{j+1} is only used by thread 0, which wrote that row itself
-      reflector(j + 1, xb, tid == 0 ? xb[j + 1] : 0.0, vb + (size_t)(par ^ 1) * ld, s2n);
+      s2n = warp_sum_d(s2n);
+      if (lane == 0) red[warp] = s2n;
+      __syncthreads();   // xb, wj and the partial sums complete
+      if (warp < kTrdReflWarps) {
+        // the next reflector on the first warps (dj = x_{j+1}: thread 0 wrote that row itself) ...
+        reflector_part(j + 1, xb, tid == 0 ? xb[j + 1] : 0.0, vb + (size_t)(par ^ 1) * ld, kTrdReflWarps * 32);
+      } else {
+        // ... while the other warps apply update(j) (A -= v_j w_j^T + w_j v_j^T) to my columns i > j+1, rows
+        // from (j+2) & ~1: the next step's pass then only forms the dots (the same values it formed before)
+        const int lc1 = q > j + 1 ? 0 : (j + 1 - q) / NC + 1;
+        const int r1 = (j + 2) & ~1;
+        for (int lcA = lc1 + warp - kTrdReflWarps; lcA < nloc; lcA += nwarps - kTrdReflWarps) {
+          const int iA = q + NC * lcA;
+          double* colA = A + (size_t)lcA * ld;
+          const double vA = vj[iA], wA = wj[iA];
+          for (int r = r1 + 2 * lane; r < c; r += 64) {
+            const double2 vp = *reinterpret_cast<const double2*>(vj + r);
+            const double2 wp = *reinterpret_cast<const double2*>(wj + r);
+            double2 xa = *reinterpret_cast<double2*>(colA + r);
+            xa.x -= vp.x * wA + wp.x * vA;
+            xa.y -= vp.y * wA + wp.y * vA;
+            *reinterpret_cast<double2*>(colA + r) = xa;
+          }
+        }
+      }
       TRD_T(5)
     } else {   // j + 1 == c - 2: the last 2 x 2 block's column c-2 (rows c-2, c-1: lanes 0, 1 of warp 0)
       __syncwarp();
