@@ -281,10 +281,15 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
         // from (j+2) & ~1: the next step's pass then only forms the dots (the same values it formed before)
         const int lc1 = q > j + 1 ? 0 : (j + 1 - q) / NC + 1;
         const int r1 = (j + 2) & ~1;
-        for (int lcA = lc1 + warp - kTrdReflWarps; lcA < nloc; lcA += nwarps - kTrdReflWarps) {
-          const int iA = q + NC * lcA;
+        // column pairs per warp: v_j, w_j rows loaded once for two columns (the update is bound by
+        // shared-memory traffic; 18 pairs at most against 28 warps)
+        for (int lcA = lc1 + 2 * (warp - kTrdReflWarps); lcA < nloc; lcA += 2 * (nwarps - kTrdReflWarps)) {
+          const bool hasB = lcA + 1 < nloc;
+          const int iA = q + NC * lcA, iB = iA + NC;
           double* colA = A + (size_t)lcA * ld;
+          double* colB = A + (size_t)(lcA + 1) * ld;
           const double vA = vj[iA], wA = wj[iA];
+          const double vB = hasB ? vj[iB] : 0.0, wB = hasB ? wj[iB] : 0.0;
           for (int r = r1 + 2 * lane; r < c; r += 64) {
             const double2 vp = *reinterpret_cast<const double2*>(vj + r);
             const double2 wp = *reinterpret_cast<const double2*>(wj + r);
@@ -292,6 +297,12 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
             xa.x -= vp.x * wA + wp.x * vA;
             xa.y -= vp.y * wA + wp.y * vA;
             *reinterpret_cast<double2*>(colA + r) = xa;
+            if (hasB) {
+              double2 xb2 = *reinterpret_cast<double2*>(colB + r);
+              xb2.x -= vp.x * wB + wp.x * vB;
+              xb2.y -= vp.y * wB + wp.y * vB;
+              *reinterpret_cast<double2*>(colB + r) = xb2;
+            }
           }
         }
       }
