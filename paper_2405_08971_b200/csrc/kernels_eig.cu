@@ -396,6 +396,7 @@ constexpr int kDcPrepThreads = 256;
 // Per merge: z = Q^T u, sort the poles (merge of two ascending lists), deflate (dlaed2: negligible
 // weight; close poles -> Givens rotation).  Dynamic smem: 2 n doubles + n ints.
 __global__ void __launch_bounds__(kDcPrepThreads) dc_prep_kernel(DcArgs a) {
+  griddep_wait();   // PDL: the previous divide-and-conquer launch's outputs
   int o, n;
   const int m = blockIdx.x;
   if (!dc_merge(a.c, a.s, m, o, n)) return;
@@ -505,6 +506,7 @@ __global__ void __launch_bounds__(kDcPrepThreads) dc_prep_kernel(DcArgs a) {
 // of psi (poles <= t) and phi (poles > t) matched in value and slope (Bunch-Nielsen-Sorensen), falling back to
 // bisection (geometric while the bracket spans orders of magnitude) whenever the model step leaves the bracket.
 __global__ void dc_secular_kernel(DcArgs a) {
+  griddep_wait();   // PDL: the previous divide-and-conquer launch's outputs
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (gw >= a.c) return;
   const int m = gw / (2 * a.s);
@@ -596,6 +598,7 @@ __device__ __forceinline__ double lam_minus_d(const double* dK, const int* org, 
 
 // Gu-Eisenstat: zhat_i^2 = (lambda_i - d_i)/rho * prod_{j != i} (lambda_j - d_i)/(d_j - d_i); one warp per i
 __global__ void dc_zhat_kernel(DcArgs a) {
+  griddep_wait();   // PDL: the previous divide-and-conquer launch's outputs
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (gw >= a.c) return;
   const int m = gw / (2 * a.s);
@@ -633,6 +636,7 @@ __global__ void dc_zhat_kernel(DcArgs a) {
 // then the deflation rotations in reverse order, then the rows scattered to the local columns perm[s].
 constexpr int kVecWarps = 4;
 __global__ void __launch_bounds__(kVecWarps * 32) dc_vec_kernel(DcArgs a, int nmax) {
+  griddep_wait();   // PDL: the previous divide-and-conquer launch's outputs
   extern __shared__ __align__(16) double vbuf[];
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (gw >= a.c) return;
@@ -677,6 +681,7 @@ __global__ void __launch_bounds__(kVecWarps * 32) dc_vec_kernel(DcArgs a, int nm
 
 // final ascending position of each merged eigenvalue (ties by (K, deflated) order index)
 __global__ void dc_rank_kernel(DcArgs a) {
+  griddep_wait();   // PDL: the previous divide-and-conquer launch's outputs
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= a.c) return;
   const int m = x / (2 * a.s);
@@ -698,6 +703,7 @@ __global__ void dc_rank_kernel(DcArgs a) {
 // K chunks of 32 double-buffered through registers.
 constexpr int kGT = 32, kGK = 32, kGThreads = 64;
 __global__ void __launch_bounds__(kGThreads) dc_gemm_kernel(DcArgs a) {
+  griddep_wait();   // PDL: the previous divide-and-conquer launch's outputs
   const int c = a.c, s = a.s;
   const int tpm = (2 * s + kGT - 1) / kGT;   // tiles per merge side
   const int tiles_per_merge = tpm * tpm;
@@ -1089,20 +1095,18 @@ cudaError_t eig_top(int c, int r, const double* G, void* ws, size_t ws_bytes, do
     const size_t psmem = nmax * (2 * sizeof(double) + sizeof(int));
     const size_t vsmem = (size_t)kVecWarps * nmax * sizeof(double);
     if (psmem > 200 * 1024 || vsmem > 200 * 1024) return cudaErrorInvalidValue;
-    dc_prep_kernel<<<nmerge, kDcPrepThreads, psmem, st>>>(da);
-    if ((err = note_launch_err()) != cudaSuccess) return err;
+    // programmatic dependent launches: each kernel's launch and prologue overlap its predecessor's tail
+    // (every kernel waits with griddepcontrol.wait before touching memory)
+    if ((err = launch_pdl(dc_prep_kernel, dim3(nmerge), dim3(kDcPrepThreads), psmem, st, da)) != cudaSuccess) return err;
     const unsigned wblocks = (unsigned)((c * 32 + 255) / 256);
-    dc_secular_kernel<<<wblocks, 256, 0, st>>>(da);
-    if ((err = note_launch_err()) != cudaSuccess) return err;
-    dc_zhat_kernel<<<wblocks, 256, 0, st>>>(da);
-    if ((err = note_launch_err()) != cudaSuccess) return err;
-    dc_vec_kernel<<<(unsigned)((c + kVecWarps - 1) / kVecWarps), kVecWarps * 32, vsmem, st>>>(da, (int)nmax);
-    if ((err = note_launch_err()) != cudaSuccess) return err;
-    dc_rank_kernel<<<(c + 255) / 256, 256, 0, st>>>(da);
-    if ((err = note_launch_err()) != cudaSuccess) return err;
+    if ((err = launch_pdl(dc_secular_kernel, dim3(wblocks), dim3(256), 0, st, da)) != cudaSuccess) return err;
+    if ((err = launch_pdl(dc_zhat_kernel, dim3(wblocks), dim3(256), 0, st, da)) != cudaSuccess) return err;
+    if ((err = launch_pdl(dc_vec_kernel, dim3((unsigned)((c + kVecWarps - 1) / kVecWarps)), dim3(kVecWarps * 32), vsmem,
+                          st, da, (int)nmax)) != cudaSuccess)
+      return err;
+    if ((err = launch_pdl(dc_rank_kernel, dim3((c + 255) / 256), dim3(256), 0, st, da)) != cudaSuccess) return err;
     const int tpm = (2 * s + kGT - 1) / kGT;
-    dc_gemm_kernel<<<nmerge * tpm * tpm, kGThreads, 0, st>>>(da);
-    if ((err = note_launch_err()) != cudaSuccess) return err;
+    if ((err = launch_pdl(dc_gemm_kernel, dim3(nmerge * tpm * tpm), dim3(kGThreads), 0, st, da)) != cudaSuccess) return err;
     std::swap(Qcur, Qnext);
   }
   // ---- 3. back-transformation of the r wanted eigenvectors (compact WY panels), eigenvalue outputs
