@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(kBtThreads) bt_apply_kernel(int c, int r, int 
                                                               const double* __restrict__ Q, double* __restrict__ Qr) {
   extern __shared__ __align__(16) double Zs[];   // [kBtCols][c], then Vs[rmax][kBtPad]
   double* Vs = Zs + (size_t)kBtCols * c;
-  __shared__ double W[kBtNb][kBtCols], Ts[kBtNb][kBtNb + 1];
+  __shared__ double W[kBtNb][kBtCols], Ts[kBtNb][kBtNb + 1], Wh[2][kBtNb][kBtCols];
   const int j0c = blockIdx.x * kBtCols, ncol = min(kBtCols, r - j0c);
   for (int x = threadIdx.x; x < kBtCols * c; x += kBtThreads) {
     const int col = x / c, l = x % c;
@@ -842,6 +842,8 @@ __global__ void __launch_bounds__(kBtThreads) bt_apply_kernel(int c, int r, int 
   const int np = nref > 0 ? (nref + kBtNb - 1) / kBtNb : 0;
   const int ta = threadIdx.x % kBtNb, tcol = threadIdx.x / kBtNb;
   const bool wown = threadIdx.x < kBtNb * kBtCols;
+  const int half = threadIdx.x / (kBtNb * kBtCols), tcol2 = (threadIdx.x / kBtNb) % kBtCols;
+  static_assert(kBtThreads == 2 * kBtNb * kBtCols, "two row halves of the W = V^T Z outputs");
   auto stage = [&](int j0, int b, int r0, int nr) {   // Vs[rr][a] = v_{j0+a}[r0+rr] (zero above its support)
     for (int x = threadIdx.x; x < nr * kBtNb; x += kBtThreads) {
       const int rr = x % nr, a = x / nr, l = r0 + rr;
@@ -853,24 +855,20 @@ __global__ void __launch_bounds__(kBtThreads) bt_apply_kernel(int c, int r, int 
     const int r00 = j0 + 1, nrows = c - r00;
     const bool one = nrows <= rmax;
     for (int x = threadIdx.x; x < kBtNb * kBtNb; x += kBtThreads) Ts[x % kBtNb][x / kBtNb] = Tall[(size_t)p * kBtNb * kBtNb + x];
-    // W = V_p^T Z
-    double acc0 = 0.0, acc1 = 0.0;
+    // W = V_p^T Z: the even rows of each chunk on threads [0, 128), the odd rows on [128, 256) (the two
+    // accumulators of one thread before), summed even + odd
+    double acc = 0.0;
     for (int r0 = r00; r0 < c; r0 += rmax) {
       const int nr = min(rmax, c - r0);
       __syncthreads();
       stage(j0, b, r0, nr);
       __syncthreads();
-      if (wown) {
-        const double* z = Zs + (size_t)tcol * c + r0;
-        int rr = 0;
-        for (; rr + 1 < nr; rr += 2) {
-          acc0 += Vs[(size_t)rr * kBtPad + ta] * z[rr];
-          acc1 += Vs[(size_t)(rr + 1) * kBtPad + ta] * z[rr + 1];
-        }
-        if (rr < nr) acc0 += Vs[(size_t)rr * kBtPad + ta] * z[rr];
-      }
+      const double* z = Zs + (size_t)tcol2 * c + r0;
+      for (int rr = half; rr < nr; rr += 2) acc += Vs[(size_t)rr * kBtPad + ta] * z[rr];
     }
-    if (wown) W[ta][tcol] = acc0 + acc1;
+    Wh[half][ta][tcol2] = acc;
+    __syncthreads();
+    if (wown) W[ta][tcol] = Wh[0][ta][tcol] + Wh[1][ta][tcol];
     __syncthreads();
     double w2 = 0.0;   // W2 = T W
     if (wown)

@@ -473,7 +473,7 @@ hmu_kernel(int N, const T* __restrict__ HM, int rin, const double* __restrict__ 
 }
 
 // hmu with 4 consecutive rows per thread (one 16-byte load per column; fp32, N % 4 == 0, 16-byte aligned HM):
-// 512 rows per block; every row's fp64 accumulation is row_gemv's (columns ascending, column j into
+// 4 rows per thread; every row's fp64 accumulation is row_gemv's (columns ascending, column j into
 // acc[j & 3] below the last multiple of 8, the tail into acc[0]), so w is the same bits
 template <int MINB>
 __global__ void __launch_bounds__(kTile, MINB)
@@ -482,7 +482,7 @@ hmu4_kernel(int N, const float* __restrict__ HM, int rin, const double* __restri
   double* u = reinterpret_cast<double*>(sm_raw);
   for (int j = threadIdx.x; j < rin; j += blockDim.x) u[j] = ured[j];
   __syncthreads();
-  const int row = (blockIdx.x * kTile + threadIdx.x) * 4;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (row >= N) return;
   double acc[4][4] = {};
   const int n8 = rin & ~7;
@@ -1237,11 +1237,12 @@ cudaError_t StepKernels<T>::hmu(int N, const T* HM, int rin, const double* ured,
   if (rin <= 0 || N <= 0) return cudaSuccess;
   if constexpr (sizeof(T) == 4) {
     if ((N & 3) == 0 && ((uintptr_t)HM & 15) == 0) {
-      const int nb = (N / 4 + kTile - 1) / kTile;
+      constexpr int kHmu4Threads = 64;   // 256 rows per block: more, smaller blocks (two per slot beside K1)
+      const int nb = (N / 4 + kHmu4Threads - 1) / kHmu4Threads;
       if (side_slim())
-        hmu4_kernel<6><<<nb, kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
+        hmu4_kernel<6><<<nb, kHmu4Threads, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
       else
-        hmu4_kernel<1><<<nb, kTile, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
+        hmu4_kernel<1><<<nb, kHmu4Threads, sizeof(double) * rin, st>>>(N, HM, rin, ured, w);
       return note_launch_err();
     }
   }
