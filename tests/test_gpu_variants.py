@@ -11,7 +11,9 @@ cfg3-sized run (D = 231,360; truncation at every step; K = 16 smoother products)
   * CAKF_STAGE_AB: the inner loop's stages A and B (alg:update_pls lines 9-11) as one kernel vs
     two (same per-row arithmetic, same block and grid reduction order);
   * CAKF_TRUNC_OVERLAP: the filter truncation's eigensolver and M Q_r (and the next M^- = A M~) on their own
-    stream beside the next update's prologue and first K1, joined before H M^- is gathered.
+    stream beside the next update's prologue and first K1, joined before H M^- is gathered;
+  * CAKF_K1_BOX: K1's exact-zero sub-tile test with the bounding-box bound added to the sphere bound (both
+    are lower bounds on every pair distance, so the extra sub-tiles it skips hold exact zeros only).
 The switches are read once per process, so each variant runs in its own interpreter."""
 import os
 import subprocess
@@ -50,7 +52,7 @@ def _need_gpu():
 
 
 @pytest.mark.parametrize("switch", ["CAKF_TC_PERSIST", "CAKF_STRIP2", "CAKF_SMOOTH_OVERLAP", "CAKF_SPLIT_RC8",
-                                    "CAKF_STAGE_AB", "CAKF_TRUNC_OVERLAP"])
+                                    "CAKF_STAGE_AB", "CAKF_TRUNC_OVERLAP", "CAKF_K1_BOX"])
 def test_variant_bit_identical(tmp_path, switch):
     res = {}
     for flag in ("0", "1"):
