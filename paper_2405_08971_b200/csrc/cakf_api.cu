@@ -143,6 +143,14 @@ bool trunc_overlap() {
   return v;
 }
 
+// CAKF_SLOT_LISTS=0: the stage kernels sum all K1 partial slots (interleaved over the warps) instead of the
+// per-block lists of the slots that can be nonzero (A/B only; a different summation grouping, so not the
+// same bits — culling on / off stays bit-identical within either mode)
+bool slot_lists_on() {
+  static const bool v = !env_is("CAKF_SLOT_LISTS", '0');
+  return v;
+}
+
 // CAKF_STAGE_AB=0: the inner loop's stages A and B as two kernels (A/B only)
 bool stage_ab() {
   static const bool v = !env_is("CAKF_STAGE_AB", '0');
@@ -315,6 +323,7 @@ struct Impl final : ImplBase {
   int *act_cnt_sm = nullptr, *act_list_sm = nullptr, *act_cnt_po = nullptr, *act_list_po = nullptr;
   int act_stride_sm = 0, act_stride_po = 0;
   int *k1_list = nullptr, *k1_count = nullptr;
+  int *k1_plist = nullptr, *k1_pq = nullptr;   // per 512-row block: the K1 partial slots that can be nonzero (SlotList)
   unsigned short* k1_mask = nullptr;  // active symmetric K1 units of this update
   unsigned* k1_sched = nullptr;                           // K1 dynamic unit scheduling counters
   unsigned long long* cull_ctr = nullptr;  // [0] K1 tile pairs done, [1] K2-post blocks, [2] K2-smooth blocks
@@ -680,6 +689,11 @@ struct Impl final : ImplBase {
       k1_count = carve<int>(64);   // [0] active-unit count, then launch_k1_active_units' group counters
     }
     k1_sched = carve<unsigned>(4);
+    if (sizeof(T) == 4) {
+      const size_t nbk = (size_t)matvec_sym_blocks((int)Nmax);
+      k1_plist = carve<int>(nbk * nbk);
+      k1_pq = carve<int>(nbk * 5);
+    }
     k1_range = carve<long long>(2);
   }
 
@@ -1046,6 +1060,21 @@ struct Impl final : ImplBase {
         CK_CUDA(cudaMemsetAsync(partial, 0, (size_t)matvec_sym_tiles(N) * N * sizeof(T), st));
       }
     }
+    // the stage kernels sum only the K1 partial slots that can be nonzero, per 512-row block (all of them
+    // without culling: the same sums in the same order, so culling stays bit-identical); single rank only
+    // (the sharded K1 is summed by sum_partials before its all-reduce)
+    const bool slot_lists = sym && !coll && k1_plist && N > 0 && slot_lists_on();
+    if (slot_lists)
+      CK_CUDA(launch_k1_block_partners(cull ? sph_o128 : nullptr, N, kCullCut, k1_plist, k1_pq, st));
+    auto slots_for = [&](const T* kp) {
+      SlotList sl;
+      if (slot_lists && kp == partial) {
+        sl.plist = k1_plist;
+        sl.pq = k1_pq;
+        sl.nb = matvec_sym_blocks(N);
+      }
+      return sl;
+    };
     const int nch = sym ? matvec_sym_tiles(N)
                         : std::max(1, std::min<int>(matvec_chunks(N, N, sizeof(T)), (int)(partial_cap / N)));
     T* V = S.XV + N;
@@ -1135,10 +1164,10 @@ struct Impl final : ImplBase {
       if ((fork || rin == 0) && stage_ab()) {   // stage A + B in one pass (HM u from the side stream)
         if (fork) CK_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
         CK_CUDA(StepKernels<T>::stageAB(N, kch, kpart, sig00, lam2, s, r, fork ? hmw : nullptr, g, V, i - 1, part, W,
-                                        redB, redA + rin, cnt + 64, st));
+                                        redB, redA + rin, cnt + 64, st, slots_for(kpart)));
       } else {
         CK_CUDA(StepKernels<T>::stageA(N, kch, kpart, sig00, lam2, s, r, gp, fork ? nullptr : HM, rin, part, W, redA,
-                                       cnt, st));
+                                       cnt, st, slots_for(kpart)));
         if (fork) CK_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
         CK_CUDA(StepKernels<T>::stageB(N, HM, rin, redA, gp, s, g, V, i - 1, part, W, redB, cnt + 64, st,
                                        fork ? hmw : nullptr));

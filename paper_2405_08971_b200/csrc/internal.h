@@ -37,6 +37,9 @@ int matvec_sym_blocks_per_tile_pair();   // warp blocks per 128 x 128 tile pair 
 // list (+ tile-pair masks) of the sym units in [u_lo, u_hi) with a tile pair within `cut`, grouped by their
 // active-pair count (most first); count: a device workspace of >= 64 ints, count[0] = the list length.
 // urange (nullable, device): read [u_lo, u_hi) from it instead (the balanced multi-GPU split below)
+// per 512-row block of the symmetric K1: the active partner blocks (step.h SlotList; sph == nullptr: all)
+cudaError_t launch_k1_block_partners(const float4* sph, int n, float cut, int* plist, int* pq, cudaStream_t st);
+int matvec_sym_blocks(int n);   // 512-point blocks of the symmetric K1
 cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, long long u_hi, float cut, int* list,
                                    unsigned short* mask, int* count, cudaStream_t st, const long long* urange = nullptr);
 // multi-GPU: the unit range of `rank` with an equal share of the active tile pairs (deterministic) -> urange[2]

@@ -722,6 +722,66 @@ cudaError_t launch_k1_active_units(const float4* sph, int n, long long u_lo, lon
   return note_launch_err();
 }
 
+// Per 512-row block B of the symmetric K1: the partner blocks p whose unit (min(B, p), max(B, p)) is active
+// (the same predicate as the unit list; every partner without culling, sph == nullptr), ascending, and the
+// list positions of the quarter boundaries w * nb / 4 (step.h SlotList).  One block per B.
+__global__ void k1_block_partners_kernel(const float4* __restrict__ sph, int nt, int nb, float cut,
+                                         int* __restrict__ plist, int* __restrict__ pq) {
+  const int B = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  __shared__ int wsum[32];
+  __shared__ int base_s;
+  if (tid == 0) base_s = 0;
+  __syncthreads();
+  int* pl = plist + (size_t)B * nb;
+  for (int p0 = 0; p0 < nb; p0 += blockDim.x) {
+    const int p = p0 + tid;
+    bool act = false;
+    if (p < nb) {
+      if (!sph) {
+        act = true;
+      } else {
+        const long long bi = min(B, p), bj = max(B, p);
+        act = sym_unit_mask(sph, nt, nb, bi * nb - bi * (bi - 1) / 2 + (bj - bi), cut) != 0u;
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int off = base_s;
+    for (int q = 0; q < w; ++q) off += wsum[q];
+    if (act) pl[off + __popc(bal & ((1u << lane) - 1u))] = p;
+    __syncthreads();
+    if (tid == 0) {
+      int t = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += wsum[q];
+      base_s += t;
+    }
+    __syncthreads();
+  }
+  if (tid < 5) {   // first list entry with partner >= tid * nb / 4 (binary search of the ascending list)
+    const int P = (int)(((long long)tid * nb) / 4);
+    int lo = 0, hi = base_s;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (pl[mid] < P) lo = mid + 1;
+      else hi = mid;
+    }
+    pq[B * 5 + tid] = lo;
+  }
+}
+
+cudaError_t launch_k1_block_partners(const float4* sph, int n, float cut, int* plist, int* pq, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int nt = (n + SYM_T - 1) / SYM_T;
+  const int nb = (nt + SYM_S - 1) / SYM_S;
+  k1_block_partners_kernel<<<nb, 256, 0, st>>>(sph, nt, nb, cut, plist, pq);
+  return note_launch_err();
+}
+int matvec_sym_blocks(int n) {
+  const int nt = (n + SYM_T - 1) / SYM_T;
+  return (nt + SYM_S - 1) / SYM_S;
+}
+
 // Multi-GPU split of K1 by work (not by unit index): the units in index order carry popc(mask) active tile
 // pairs each; rank p takes the contiguous unit range whose prefix work falls in [W p / world, W (p+1) / world).
 // One block, each thread a contiguous chunk of units; deterministic (the same range on every rank).

@@ -265,15 +265,46 @@ __device__ void tile_slots_sum_v4(const float* __restrict__ partial, int N, int 
   for (int e = 0; e < 4; ++e) sk[warp * kTile + 4 * lane + e] = a[e];
 }
 
+// the same over the listed slots of the tile's 512-row block: warp w sums the active partners of quarter w
+// (slot lists, SlotList) in ascending order — skipped slots hold exact zeros, so the sums equal the full ones
+__device__ void tile_slots_list_v4(const float* __restrict__ partial, int N, const SlotList& sl, int r0, int r1,
+                                   double* sk) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = r0 + 4 * lane;
+  const int rr = row < r1 ? row : r0;
+  const int B = r0 / 512;
+  const int* pl = sl.plist + (size_t)B * sl.nb;
+  const int k1 = sl.pq[B * 5 + warp + 1];
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  int k = sl.pq[B * 5 + warp];
+  for (; k + 16 <= k1; k += 16) {
+    float4 x[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = __ldg(reinterpret_cast<const float4*>(partial + (size_t)__ldg(pl + k + q) * N + rr));
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      a[0] += (double)x[q].x; a[1] += (double)x[q].y; a[2] += (double)x[q].z; a[3] += (double)x[q].w;
+    }
+  }
+  for (; k < k1; ++k) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(partial + (size_t)__ldg(pl + k) * N + rr));
+    a[0] += (double)x.x; a[1] += (double)x.y; a[2] += (double)x.z; a[3] += (double)x.w;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) sk[warp * kTile + 4 * lane + e] = a[e];
+}
+
 // the K1 row sums of this block's rows: the 16-byte-load form when it applies (same in stage A and stage AB,
 // so the two stay bit-identical), else per row with 32 loads in flight
 template <typename T>
-__device__ __forceinline__ double tile_ksum(const T* __restrict__ partial, int N, int nch, int r0, int r1) {
+__device__ __forceinline__ double tile_ksum(const T* __restrict__ partial, int N, int nch, int r0, int r1,
+                                            const SlotList& sl) {
   const int row = r0 + threadIdx.x;
   if constexpr (sizeof(T) == 4) {
     if ((N & 3) == 0 && ((uintptr_t)partial & 15) == 0 && blockDim.x == kTile) {
       __shared__ double sk[4 * kTile];
-      tile_slots_sum_v4(partial, N, nch, r0, r1, sk);
+      if (sl.plist) tile_slots_list_v4(partial, N, sl, r0, r1, sk);
+      else tile_slots_sum_v4(partial, N, nch, r0, r1, sk);
       __syncthreads();
       const int t = threadIdx.x;
       return (sk[t] + sk[kTile + t]) + (sk[2 * kTile + t] + sk[3 * kTile + t]);
@@ -420,12 +451,12 @@ template <typename T>
 __global__ void __launch_bounds__(kTile)
 stageA_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const T* __restrict__ lam2,
               const T* __restrict__ s, const T* __restrict__ r, T* __restrict__ gp, const T* __restrict__ HM, int rin,
-              double* __restrict__ part, int W, double* __restrict__ red, unsigned* cnt) {
+              double* __restrict__ part, int W, double* __restrict__ red, unsigned* cnt, SlotList sl) {
   griddep_wait();
   __shared__ double scratch[32 * 3];
   const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[3] = {0.0, 0.0, 0.0};  // s.r, s.g', r.r
-  const double ksum = tile_ksum(partial, N, nch, r0, r1);
+  const double ksum = tile_ksum(partial, N, nch, r0, r1, sl);
   if (row < r1) {
     const T si = s[row], ri = r[row];
     const T g = (T)(sig00 * ksum) + lam2[row] * si;
@@ -553,12 +584,12 @@ __global__ void __launch_bounds__(kTile)
 stageAB_kernel(int N, int nch, const T* __restrict__ partial, double sig00, const T* __restrict__ lam2,
                const T* __restrict__ s, const T* __restrict__ r, const double* __restrict__ wpre, T* __restrict__ g,
                const T* __restrict__ V, int nV, double* __restrict__ part, int W, double* __restrict__ red,
-               double* __restrict__ ared_tail, unsigned* cnt) {
+               double* __restrict__ ared_tail, unsigned* cnt, SlotList sl) {
   griddep_wait();
   __shared__ double scratch[32 * 4];
   const int r0 = blockIdx.x * kTile, r1 = min(N, r0 + kTile), row = r0 + threadIdx.x;
   double a[4] = {0.0, 0.0, 0.0, 0.0};   // s.g, s.r, s.g', r.r
-  const double ksum = tile_ksum(partial, N, nch, r0, r1);
+  const double ksum = tile_ksum(partial, N, nch, r0, r1, sl);
   if (row < r1) {
     const T si = s[row], ri = r[row];
     const T gpv = (T)(sig00 * ksum) + lam2[row] * si;                // g'  (stage A)
@@ -1216,9 +1247,9 @@ cudaError_t StepKernels<T>::gen_actions(int N, int i0, int nb, int policy, const
 template <typename T>
 cudaError_t StepKernels<T>::stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s,
                                    const T* r, T* gp, const T* HM, int rin, double* part, int W, double* red,
-                                   unsigned* cnt, cudaStream_t st) {
+                                   unsigned* cnt, cudaStream_t st, SlotList sl) {
   return launch_pdl(stageA_kernel<T>, dim3(stage_blocks(N)), dim3(kTile), 0, st, N, nch, partial, sig00, lam2, s, r,
-                    gp, HM, rin, part, W, red, cnt);
+                    gp, HM, rin, part, W, red, cnt, sl);
 }
 
 template <typename T>
@@ -1265,9 +1296,9 @@ cudaError_t StepKernels<T>::stageB(int N, const T* HM, int rin, const double* ur
 template <typename T>
 cudaError_t StepKernels<T>::stageAB(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s,
                                     const T* r, const double* wpre, T* g, const T* V, int nV, double* part, int W,
-                                    double* red, double* ared_tail, unsigned* cnt, cudaStream_t st) {
+                                    double* red, double* ared_tail, unsigned* cnt, cudaStream_t st, SlotList sl) {
   return launch_pdl(stageAB_kernel<T>, dim3(stage_blocks(N)), dim3(kTile), 0, st, N, nch, partial, sig00, lam2, s, r,
-                    wpre, g, V, nV, part, W, red, ared_tail, cnt);
+                    wpre, g, V, nV, part, W, red, ared_tail, cnt, sl);
 }
 
 template <typename T>

@@ -43,6 +43,16 @@ cudaError_t convert(int rows, int cols, const S* src, size_t lds, D_* dst, size_
 cudaError_t accum_d2f(int rows, int cols, double beta, const double* Cd, size_t ldcd, float* C, size_t ldc,
                       cudaStream_t st);
 
+// The symmetric K1's partial slots that can hold nonzeros for each 512-row block B: plist[B * nb + k], k <
+// pq[B * 5 + 4], the active partner blocks of B in ascending order; pq[B * 5 + w] = the first entry with partner
+// >= w * nb / 4 (the stage kernels' warp w sums the partners of quarter w in ascending order, so the sums do not
+// depend on which slots were skipped).  plist == nullptr: sum all nch slots.
+struct SlotList {
+  const int* plist = nullptr;
+  const int* pq = nullptr;
+  int nb = 0;
+};
+
 template <typename T>
 struct StepKernels {
   static cudaError_t prep(int N, const int* idx, const V4<T>* coords, const T* y, const T* mpred, int policy,
@@ -50,7 +60,7 @@ struct StepKernels {
                           cudaStream_t st, int nblk_pol = 1, T* rbs = nullptr);   // BLOCKRES: block size, r^(i0)
   static cudaError_t stageA(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s, const T* r,
                             T* gp, const T* HM, int rin, double* part, int W, double* red, unsigned* cnt,
-                            cudaStream_t st);
+                            cudaStream_t st, SlotList sl = {});
   static cudaError_t gen_actions(int N, int i0, int nb, int policy, const int* order, uint64_t seed, int k,
                                  const int* sigma, T* S, size_t ldS, cudaStream_t st, const T* rbs = nullptr,
                                  int nblk_pol = 1);
@@ -63,7 +73,7 @@ struct StepKernels {
   // g = G s; red = [V^T g | s^T g | s^T r, s^T g', r^T r], the last three also to ared_tail
   static cudaError_t stageAB(int N, int nch, const T* partial, double sig00, const T* lam2, const T* s, const T* r,
                              const double* wpre, T* g, const T* V, int nV, double* part, int W, double* red,
-                             double* ared_tail, unsigned* cnt, cudaStream_t st);
+                             double* ared_tail, unsigned* cnt, cudaStream_t st, SlotList sl = {});
   static cudaError_t stageB(int N, const T* HM, int rin, const double* ured, const T* gp, const T* s, T* g, const T* V,
                             int nV, double* part, int W, double* red, unsigned* cnt, cudaStream_t st,
                             const double* wpre = nullptr);
