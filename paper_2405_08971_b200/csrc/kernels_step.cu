@@ -286,9 +286,17 @@ __device__ void tile_slots_list_v4(const float* __restrict__ partial, int N, con
       a[0] += (double)x[q].x; a[1] += (double)x[q].y; a[2] += (double)x[q].z; a[3] += (double)x[q].w;
     }
   }
-  for (; k < k1; ++k) {
-    const float4 x = __ldg(reinterpret_cast<const float4*>(partial + (size_t)__ldg(pl + k) * N + rr));
-    a[0] += (double)x.x; a[1] += (double)x.y; a[2] += (double)x.z; a[3] += (double)x.w;
+  for (; k < k1; k += 8) {   // the tail (most lists: ~29 partners over 4 warps) as one predicated batch
+    float4 x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      x[q] = k + q < k1 ? __ldg(reinterpret_cast<const float4*>(partial + (size_t)__ldg(pl + k + q) * N + rr))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k + q < k1) {
+        a[0] += (double)x[q].x; a[1] += (double)x[q].y; a[2] += (double)x[q].z; a[3] += (double)x[q].w;
+      }
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) sk[warp * kTile + 4 * lane + e] = a[e];
