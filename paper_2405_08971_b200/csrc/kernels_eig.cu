@@ -216,12 +216,25 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
     double sq = 0.0;
     for (int lcA = lc0 + warp; lcA < nloc; lcA += nwarps) {
       const int iA = q + NC * lcA;
-      const double* colA = A + (size_t)lcA * ld;   // update(j-1) already applied (step j-1, beside its reflector)
+      // SMEM: update(j-1) already applied (step j-1, beside its reflector); global-memory columns (large c):
+      // update(j-1) fused into this pass, one L2 read and write of the trailing matrix per step
+      double* colA = A + (size_t)lcA * ld;
       const bool pubA = iA == j + 1;
+      const bool fuse = !SMEM && j > 0;
+      const double* vprev = vb + (size_t)(par ^ 1) * ld;
+      const double* wprev = wb + (size_t)(par ^ 1) * ld;
+      const double vpA = fuse ? vprev[iA] : 0.0, wpA = fuse ? wprev[iA] : 0.0;
       double accA = 0.0;
       for (int r = r0 + 2 * lane; r < c; r += 64) {
         const double2 vv = *reinterpret_cast<const double2*>(vj + r);
-        const double2 xa = *reinterpret_cast<const double2*>(colA + r);
+        double2 xa = *reinterpret_cast<const double2*>(colA + r);
+        if (fuse) {
+          const double2 vp = *reinterpret_cast<const double2*>(vprev + r);
+          const double2 wp = *reinterpret_cast<const double2*>(wprev + r);
+          xa.x -= vp.x * wpA + wp.x * vpA;
+          xa.y -= vp.y * wpA + wp.y * vpA;
+          *reinterpret_cast<double2*>(colA + r) = xa;
+        }
         accA += xa.x * vv.x + xa.y * vv.y;
         if (pubA) {
           if (r >= j + 1) cg_[r] = xa.x;
@@ -268,7 +281,11 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_cluster_kernel(TrdArgs a
       xb[l] = x;
       if (l >= j + 3) s2n += x * x;
     }
-    if (j + 4 <= c) {
+    if (!SMEM && j + 4 <= c) {   // global-memory columns: the reflector on all warps, update(j) in the next pass
+      TRD_T(4)
+      reflector(j + 1, xb, tid == 0 ? xb[j + 1] : 0.0, vb + (size_t)(par ^ 1) * ld, s2n);
+      TRD_T(5)
+    } else if (j + 4 <= c) {
       TRD_T(4)
       s2n = warp_sum_d(s2n);
       if (lane == 0) red[warp] = s2n;
